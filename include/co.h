@@ -1,0 +1,191 @@
+/*
+ * co.h — C ABI of the B200-native continual-convolution step
+ * (Continual Inference Networks, arXiv 2204.03418).
+ *
+ * Citations: "P:a-b" = PAPER.md lines a-b (/root/reference), "S:a-b" = SPEC.md.
+ *
+ * What the library computes (the hot path of BASELINE.json's north_star):
+ *   a continual 3D / 2D / 1D convolution layer (co.Conv3d, co.Conv1d)
+ *   run for n_streams independent streams that share one clock.  Each
+ *   co_forward_step convolves one incoming frame with every temporal slice of
+ *   the kernel ("compute inputs step-by-step"), adds the partial sums into
+ *   a per-stream fp32 ring of pending outputs, emits the output whose receptive
+ *   field is complete (or reports Empty while n < delay), and
+ *   rotates the ring.  The emitted value equals the matching column of the
+ *   regular convolution (Definition 1).
+ *
+ * Conventions shared by every call
+ *  - Return value: CO_OK (0) or a negative co_status.  Nothing aborts, no C++
+ *    exception crosses the ABI; co_last_error() returns a thread-local message
+ *    for the last failing call on this thread.
+ *  - Pointers are DEVICE pointers unless the parameter says "host".
+ *  - Asynchrony: device work is enqueued on the caller's CUDA stream
+ *    (`co_stream` = cudaStream_t; NULL = legacy default stream) and calls
+ *    return after enqueue.  Host outputs (ready, ready_mask, n_ready, T_out,
+ *    info) are final on return because the clock lives on the host (a1).  No
+ *    call synchronises the device except the *_host variants, so step loops are
+ *    CUDA-graph capturable.
+ *  - Concurrency: a handle has a single writer; different handles
+ *    may run concurrently on different streams.  co_forward only reads the
+ *    packed weights and may overlap other calls on the same handle.
+ *  - Layout (Assumption 1): tensors keep the paper's LOGICAL order
+ *    (B, C, S1, S2) per step and (B, C, T, S1, S2) per clip, stored
+ *    CHANNELS-LAST: step memory is (B, S1, S2, C), clip memory is
+ *    (B, T, S1, S2, C), dense.  (PyTorch: torch.channels_last /
+ *    torch.channels_last_3d.)  Absent spatial axes have extent 1.
+ *  - Weights: (Cout, Cin/groups, kt, kh, kw) dense, in w_dtype (PyTorch's
+ *    Conv weight layout, Principle 1 P:71-80); bias: (Cout) fp32 or NULL.  The
+ *    library never rounds weights: they arrive already in w_dtype.
+ *  - Arithmetic: products in fp32 (bf16 x bf16 is exact in fp32), sums in
+ *    fp32, state in fp32; outputs rounded to out_dtype with round-to-nearest-even.
+ */
+#ifndef CO_H
+#define CO_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CO_ABI_VERSION 1
+#define CO_MAX_KT 32          /* temporal kernel extent supported by the kernels */
+
+typedef enum {
+  CO_OK = 0,
+  CO_ERR_ARG = -1,          /* bad descriptor / argument (e.g. p_t > f-1; groups not dividing channels) */
+  CO_ERR_SHAPE = -2,        /* shape, byte-count or meta mismatch; layer chaining in a stack */
+  CO_ERR_LENGTH = -3,       /* co_forward with T' < 1 */
+  CO_ERR_UNSUPPORTED = -4,  /* no sm_100a kernel for this combination (there is no CPU fallback) */
+  CO_ERR_CUDA = -5,         /* a CUDA runtime/driver error; message carries cudaGetErrorString */
+  CO_ERR_OOM = -6           /* device allocation failed */
+} co_status;
+
+typedef enum { CO_F32 = 0, CO_BF16 = 1 } co_dtype;
+typedef enum { CO_ACT_NONE = 0, CO_ACT_RELU = 1 } co_activation;
+/* Kernel family for the step (SURVEY §8a dispatch rule).  AUTO picks by shape. */
+typedef enum {
+  CO_KERNEL_AUTO = 0,
+  CO_KERNEL_DIRECT = 1,     /* generic CUDA-core kernel: any groups/dilation/stride, fp32 or bf16 */
+  CO_KERNEL_DENSE_TC = 2,   /* tcgen05/TMEM implicit GEMM with fused state epilogue (bf16, dense) */
+  CO_KERNEL_DEPTHWISE = 3   /* CUDA-core depthwise stencil (groups == Cin == Cout, bf16) */
+} co_kernel;
+
+typedef void* co_stream;                 /* cudaStream_t */
+typedef struct co_conv co_conv;          /* opaque: packed weights, fp32 state ring, host clock */
+typedef struct co_stack co_stack;        /* opaque: ordered layers + inter-layer activations */
+
+/* Layer descriptor.  Index 0 of kernel/stride/padding/dilation is temporal
+ * (kernel[0] = kt, padding[0] = temporal padding p).  Entries beyond
+ * spatial_rank are ignored (treated as 1 / 0). */
+typedef struct {
+  int32_t spatial_rank;                  /* 0: Conv1d over T; 1: (T,S1); 2: Conv3d (T,S1,S2) */
+  int32_t in_channels, out_channels, groups;
+  int32_t kernel[3], stride[3], padding[3], dilation[3];
+  int32_t in_spatial[2];                 /* S1, S2 of one step */
+  int64_t n_streams;                     /* B: independent streams, one shared clock */
+  int32_t in_dtype;                      /* co_dtype of x */
+  int32_t w_dtype;                       /* co_dtype of weights (must equal in_dtype) */
+  int32_t out_dtype;                     /* co_dtype of y */
+  int32_t activation;                    /* co_activation applied to emitted outputs (after bias) */
+  int32_t kernel_choice;                 /* co_kernel; AUTO = dispatch rule */
+} co_conv_desc;
+
+/* Clock + geometry of a handle.  n and head are the host clock (a1). */
+typedef struct {
+  int64_t n;                 /* stateful steps since clean */
+  int32_t head;              /* ceil((n-d)/s) mod R, floored mod: ring slot of the next output to complete */
+  int32_t ring_slots;        /* R = ceil((f-1)/s) pending outputs (0 when f = 1) */
+  int32_t delay;             /* d = f - p - 1 */
+  int32_t receptive_field;   /* f = dil_t (kt-1) + 1 */
+  int32_t stride_t;          /* s */
+  int32_t padding_t;         /* p */
+  int32_t out_spatial[2];    /* S1', S2' */
+  int32_t kernel_used;       /* co_kernel actually dispatched */
+} co_info;
+
+/* ---- lifetime ------------------------------------------------------------ */
+
+/* Create a layer.  `weights` (Cout, Cin/g, kt, kh, kw) in w_dtype and `bias`
+ * (Cout, fp32, may be NULL) are host pointers if weights_on_device == 0, else
+ * device pointers; both are copied and repacked, so the caller may free them on
+ * return.  The fp32 state (R slots x B x S1' x S2' x Cout) is allocated and
+ * zeroed (clean state, A8).  Errors: CO_ERR_ARG, CO_ERR_UNSUPPORTED, CO_ERR_OOM,
+ * CO_ERR_CUDA.  Synchronises the current device once (setup, not the hot path). */
+int co_conv_create(const co_conv_desc* desc, const void* weights, const float* bias,
+                   int weights_on_device, co_conv** out);
+int co_conv_destroy(co_conv* h);                      /* frees weights, state, clock; NULL ok */
+int co_conv_info(const co_conv* h, co_info* info);    /* host, final on return */
+int co_delay(const co_conv* h, int64_t* delay);       /* d = f - p - 1 */
+const char* co_kernel_name(const co_conv* h);         /* name of the dispatched step kernel */
+
+/* ---- call modes (Principle 2) ----------------------------------- */
+
+/* forward_step: x one step (B, S1, S2, Cin) channels-last in in_dtype;
+ * y (B, S1', S2', Cout) in out_dtype.  *ready (host) = 1 when the output is
+ * emitted (n >= d and (n-d) mod s == 0), else 0 (Empty) and y is left
+ * untouched.  x == NULL feeds an all-zero step (used for pad_end).  With
+ * update_state == 0 the ready output is computed from the current state and
+ * state + clock stay bitwise unchanged. */
+int co_forward_step(co_conv* h, const void* x, void* y, int update_state, int* ready, co_stream stream);
+
+/* Same step with HOST buffers: x_host / y_host are host memory (pinned for
+ * best speed); the call copies x in, runs the step, copies y out and
+ * synchronises `stream` before returning, so y_host is valid on return. */
+int co_forward_step_host(co_conv* h, const void* x_host, void* y_host, int update_state, int* ready,
+                         co_stream stream);
+
+/* forward_steps: the fold of co_forward_step over the T columns of the
+ * clip x (B, T, S1, S2, Cin), then p zero steps if pad_end.  y receives
+ * the Ready outputs compacted in time (A1): (B, n_ready, S1', S2', Cout); its
+ * capacity must be co_steps_ready_count(h, T, pad_end) columns.  ready_mask
+ * (host, may be NULL) gets T + (pad_end ? p : 0) flags; *n_ready (host).
+ * Bitwise equal to the fold of co_forward_step.  With update_state == 0
+ * the fold runs on a device copy of the state. */
+int co_forward_steps(co_conv* h, const void* x, int64_t T, void* y, uint8_t* ready_mask,
+                     int64_t* n_ready, int pad_end, int update_state, co_stream stream);
+/* Number of Ready ticks the next co_forward_steps(T, pad_end) will produce. */
+int co_steps_ready_count(const co_conv* h, int64_t T, int pad_end, int64_t* n_ready);
+
+/* forward: batch mode, x (B, T, S1, S2, Cin) -> y (B, T', S1', S2',
+ * Cout) with symmetric temporal zero padding p and T' = floor((T+2p-f)/s)+1
+ * (S:64).  Neither reads nor writes state.  CO_ERR_LENGTH if T' < 1. */
+int co_forward(co_conv* h, const void* x, int64_t T, void* y, int64_t* T_out, co_stream stream);
+int co_forward_out_len(const co_conv* h, int64_t T, int64_t* T_out);
+
+/* ---- state (Principle 3) -------------------------------------- */
+
+/* Canonical state: fp32 (R, B, S1', S2', Cout) dense, device memory.  Slot j
+ * holds output i_next + j, i_next = ceil((n-d)/s) the next output to complete;
+ * its value is the sum of contributions of the frames consumed so far (bias
+ * excluded, A9), 0 for outputs that are never emitted (i < 0).  `bytes` must
+ * equal co_state_bytes().  get fills *meta with the clock; set restores the
+ * clock from *meta (its geometry fields must match: CO_ERR_SHAPE).  A get ->
+ * set round trip is bitwise (checkpoint / resume). */
+int co_state_bytes(const co_conv* h, size_t* bytes);
+int co_state_get(co_conv* h, void* dst, size_t bytes, co_info* meta, co_stream stream);
+int co_state_set(co_conv* h, const void* src, size_t bytes, const co_info* meta, co_stream stream);
+/* clean_state(): zero state, n = 0. */
+int co_state_clean(co_conv* h, co_stream stream);
+
+/* ---- layer stack (Sequential; Principle 6 P:248-264) -------- */
+
+/* Chain layers: layer i's output geometry/dtype must equal layer i+1's input
+ * (CO_ERR_SHAPE otherwise) and all layers share n_streams.  The stack owns its
+ * inter-layer activation buffers, not its layers.  Each step threads the frame
+ * through the layers; an Empty output ends the tick and the downstream layers
+ * are not advanced (A7). */
+int co_stack_create(co_conv* const* layers, int n_layers, co_stack** out);
+int co_stack_destroy(co_stack* st);
+int co_stack_step(co_stack* st, const void* x, void* y, int update_state, int* ready, co_stream stream);
+/* Accumulated delay d_NN (Principle 6 in the worked-example reading, A3). */
+int co_stack_delay(const co_stack* st, int64_t* d_nn);
+int co_stack_clean(co_stack* st, co_stream stream);
+
+/* ---- misc ------------------------------------------------------------------ */
+const char* co_last_error(void);
+int co_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CO_H */

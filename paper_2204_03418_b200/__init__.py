@@ -1,0 +1,264 @@
+"""B200-native continual-convolution step (Continual Inference Networks, arXiv 2204.03418).
+
+Thin Python binding over the C ABI in ``include/co.h`` (``libco_b200.so``):
+argument marshalling only — every step of the path runs in the sm_100a
+kernels.  PyTorch supplies device memory and the current CUDA stream.
+
+Method names follow the paper (Principle 2; Principle 3, P:110-120;
+Listing 1): ``forward``, ``forward_step``, ``forward_steps``,
+``clean_state``, ``delay``, ``receptive_field``.
+
+Tensors keep the paper's logical dimension order (Assumption 1):
+a step is ``(B, C, *S)`` and a clip ``(B, C, T, *S)``, stored channels-last in
+memory (``torch.channels_last`` for ``(B, C, H, W)``); :func:`channels_last`
+converts.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence, Tuple
+
+import torch
+
+from . import _abi
+from ._abi import CoConvDesc, CoInfo, check, lib
+
+__all__ = ["Conv", "Stack", "channels_last", "is_channels_last", "load"]
+
+_DT = {torch.float32: _abi.CO_F32, torch.bfloat16: _abi.CO_BF16}
+
+
+def load():
+    """Load the native library (raises ImportError if it was not built)."""
+    return lib()
+
+
+def channels_last(x: torch.Tensor) -> torch.Tensor:
+    """Same logical tensor, channel axis (dim 1) stored innermost."""
+    return x.movedim(1, -1).contiguous().movedim(-1, 1)
+
+
+def is_channels_last(x: torch.Tensor) -> bool:
+    return x.movedim(1, -1).is_contiguous()
+
+
+def _empty_cl(shape: Sequence[int], dtype, device) -> torch.Tensor:
+    phys = (shape[0],) + tuple(shape[2:]) + (shape[1],)
+    return torch.empty(phys, dtype=dtype, device=device).movedim(-1, 1)
+
+
+def _stream(stream) -> C.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _tup(v, n=3, fill=1):
+    if isinstance(v, int):
+        return (v,) * n
+    v = tuple(v)
+    return v + (fill,) * (n - len(v))
+
+
+class Conv:
+    """A continual convolution layer over ``n_streams`` lockstep streams.
+
+    ``spatial_rank`` 2 is ``co.Conv3d`` (T, S1, S2), 1 is a (T, S1) conv and 0
+    is ``co.Conv1d`` over T.  ``weight`` is ``(Cout, Cin/groups, kt, *k_s)`` in
+    ``dtype`` (PyTorch's Conv weight layout); ``bias`` is ``(Cout,)``.
+    """
+
+    def __init__(self, in_channels: int, out_channels: int, kernel_size, *, weight: torch.Tensor,
+                 bias: Optional[torch.Tensor] = None, stride=1, padding=0, dilation=1, groups: int = 1,
+                 spatial_rank: int = 2, in_spatial: Sequence[int] = (1, 1), n_streams: int = 1,
+                 dtype: torch.dtype = torch.bfloat16, out_dtype: Optional[torch.dtype] = None,
+                 activation: Optional[str] = None, kernel: str = "auto", device="cuda"):
+        self.device = torch.device(device)
+        self.dtype, self.out_dtype = dtype, (out_dtype or dtype)
+        self.spatial_rank, self.n_streams = spatial_rank, n_streams
+        self.in_channels, self.out_channels = in_channels, out_channels
+        d = CoConvDesc()
+        d.spatial_rank, d.in_channels, d.out_channels, d.groups = spatial_rank, in_channels, out_channels, groups
+        d.kernel = (C.c_int32 * 3)(*_tup(kernel_size))
+        d.stride = (C.c_int32 * 3)(*_tup(stride))
+        d.padding = (C.c_int32 * 3)(*_tup(padding, fill=0))
+        d.dilation = (C.c_int32 * 3)(*_tup(dilation))
+        ins = tuple(in_spatial) + (1, 1)
+        d.in_spatial = (C.c_int32 * 2)(*ins[:2])
+        d.n_streams = n_streams
+        d.in_dtype = d.w_dtype = _DT[dtype]
+        d.out_dtype = _DT[self.out_dtype]
+        d.activation = {None: _abi.CO_ACT_NONE, "none": _abi.CO_ACT_NONE, "relu": _abi.CO_ACT_RELU}[activation]
+        d.kernel_choice = _abi.KERNELS[kernel]
+        self._desc = d
+        w = weight.detach().to(dtype).contiguous()
+        on_dev = int(w.is_cuda)
+        b = None
+        if bias is not None:
+            b = bias.detach().to(torch.float32).to(w.device).contiguous()
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            check(lib().co_conv_create(C.byref(d), C.c_void_p(w.data_ptr()),
+                                       C.c_void_p(b.data_ptr()) if b is not None else None, on_dev, C.byref(h)))
+        self._h = h
+        info = self.info()
+        self.out_spatial: Tuple[int, ...] = tuple(info.out_spatial[:spatial_rank])
+        self.in_spatial: Tuple[int, ...] = tuple(ins[:spatial_rank])
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().co_conv_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ---- attributes (Listing 1) ----
+    def info(self) -> CoInfo:
+        i = CoInfo()
+        check(lib().co_conv_info(self._h, C.byref(i)))
+        return i
+
+    @property
+    def delay(self) -> int:
+        return self.info().delay
+
+    @property
+    def receptive_field(self) -> int:
+        return self.info().receptive_field
+
+    @property
+    def kernel_name(self) -> str:
+        return lib().co_kernel_name(self._h).decode()
+
+    @property
+    def kernel_used(self) -> str:
+        return _abi.KERNEL_NAMES[self.info().kernel_used]
+
+    def _check_in(self, x: torch.Tensor, clip: bool):
+        exp = (self.n_streams, self.in_channels) + ((x.shape[2],) if clip else ()) + self.in_spatial
+        if tuple(x.shape) != exp:
+            raise ValueError(f"input shape {tuple(x.shape)} != {exp}")
+        if x.dtype != self.dtype or not x.is_cuda:
+            raise ValueError(f"input must be a CUDA {self.dtype} tensor")
+        if not is_channels_last(x):
+            raise ValueError("input must be channels-last (use paper_2204_03418_b200.channels_last)")
+
+    # ---- call modes (Principle 2) ----
+    def forward_step(self, x: Optional[torch.Tensor], update_state: bool = True, out: Optional[torch.Tensor] = None,
+                     stream=None) -> Optional[torch.Tensor]:
+        """One step.  Returns the emitted output or None (Empty)."""
+        if x is not None:
+            self._check_in(x, clip=False)
+        y = out if out is not None else _empty_cl((self.n_streams, self.out_channels) + self.out_spatial,
+                                                  self.out_dtype, self.device)
+        r = C.c_int()
+        check(lib().co_forward_step(self._h, C.c_void_p(x.data_ptr()) if x is not None else None,
+                                    C.c_void_p(y.data_ptr()), int(update_state), C.byref(r), _stream(stream)))
+        return y if r.value else None
+
+    def forward_steps(self, x: torch.Tensor, pad_end: bool = False, update_state: bool = True, stream=None):
+        """Fold of forward_step over the clip.  Returns (y compacted in
+        time, ready_mask) — y is (B, Cout, n_ready, *S')."""
+        self._check_in(x, clip=True)
+        T = x.shape[2]
+        cap = C.c_int64()
+        check(lib().co_steps_ready_count(self._h, T, int(pad_end), C.byref(cap)))
+        y = _empty_cl((self.n_streams, self.out_channels, cap.value) + self.out_spatial, self.out_dtype, self.device)
+        total = T + (self.info().padding_t if pad_end else 0)
+        mask = (C.c_uint8 * max(total, 1))()
+        nr = C.c_int64()
+        check(lib().co_forward_steps(self._h, C.c_void_p(x.data_ptr()), T, C.c_void_p(y.data_ptr()), mask,
+                                     C.byref(nr), int(pad_end), int(update_state), _stream(stream)))
+        return y, torch.tensor([bool(m) for m in mask[:total]], dtype=torch.bool)
+
+    def forward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        """Batch mode: the regular convolution of the clip; no state."""
+        self._check_in(x, clip=True)
+        T = x.shape[2]
+        Tp = C.c_int64()
+        check(lib().co_forward_out_len(self._h, T, C.byref(Tp)))
+        if Tp.value < 1:
+            raise ValueError(f"clip too short: T'={Tp.value}")
+        y = _empty_cl((self.n_streams, self.out_channels, Tp.value) + self.out_spatial, self.out_dtype, self.device)
+        check(lib().co_forward(self._h, C.c_void_p(x.data_ptr()), T, C.c_void_p(y.data_ptr()), C.byref(Tp),
+                               _stream(stream)))
+        return y
+
+    # ---- state (Principle 3) ----
+    def clean_state(self, stream=None):
+        check(lib().co_state_clean(self._h, _stream(stream)))
+
+    def state_dict_stream(self, stream=None):
+        """Canonical state (R, B, *S', Cout) fp32 and the clock (co_state_get)."""
+        nb = C.c_size_t()
+        check(lib().co_state_bytes(self._h, C.byref(nb)))
+        info = self.info()
+        st = torch.empty((info.ring_slots, self.n_streams) + self.out_spatial + (self.out_channels,),
+                         dtype=torch.float32, device=self.device)
+        meta = CoInfo()
+        check(lib().co_state_get(self._h, C.c_void_p(st.data_ptr()) if st.numel() else None, nb.value,
+                                 C.byref(meta), _stream(stream)))
+        return st, meta
+
+    def load_state_stream(self, state: torch.Tensor, meta: CoInfo, stream=None):
+        nb = C.c_size_t()
+        check(lib().co_state_bytes(self._h, C.byref(nb)))
+        state = state.to(torch.float32).contiguous()
+        check(lib().co_state_set(self._h, C.c_void_p(state.data_ptr()) if state.numel() else None, nb.value,
+                                 C.byref(meta), _stream(stream)))
+
+    @property
+    def n(self) -> int:
+        return self.info().n
+
+    @property
+    def head(self) -> int:
+        return self.info().head
+
+    # ---- host-buffer entry point (e2e) ----
+    def forward_step_host(self, x_host: torch.Tensor, y_host: torch.Tensor, update_state: bool = True,
+                          stream=None) -> bool:
+        r = C.c_int()
+        check(lib().co_forward_step_host(self._h, C.c_void_p(x_host.data_ptr()), C.c_void_p(y_host.data_ptr()),
+                                         int(update_state), C.byref(r), _stream(stream)))
+        return bool(r.value)
+
+
+class Stack:
+    """Sequential continual network: Empty short-circuits."""
+
+    def __init__(self, layers: Sequence[Conv]):
+        self.layers = list(layers)
+        arr = (C.c_void_p * len(layers))(*[l._h.value for l in layers])
+        h = C.c_void_p()
+        check(lib().co_stack_create(arr, len(layers), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().co_stack_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def delay(self) -> int:
+        d = C.c_int64()
+        check(lib().co_stack_delay(self._h, C.byref(d)))
+        return d.value
+
+    def forward_step(self, x: torch.Tensor, update_state: bool = True, out: Optional[torch.Tensor] = None,
+                     stream=None) -> Optional[torch.Tensor]:
+        last = self.layers[-1]
+        y = out if out is not None else _empty_cl((last.n_streams, last.out_channels) + last.out_spatial,
+                                                  last.out_dtype, last.device)
+        r = C.c_int()
+        check(lib().co_stack_step(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), int(update_state),
+                                  C.byref(r), _stream(stream)))
+        return y if r.value else None
+
+    def clean_state(self, stream=None):
+        check(lib().co_stack_clean(self._h, _stream(stream)))

@@ -1,0 +1,75 @@
+// common.cuh — definitions shared by the sm_100a kernels and the host library
+// of the continual-convolution step (arXiv 2204.03418).  Product code: shares
+// nothing with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace co {
+
+constexpr int kMaxKt = 32;   // == CO_MAX_KT
+
+enum Dtype : int { F32 = 0, BF16 = 1 };
+
+// Normalised layer geometry (absent spatial axes are extent 1, kernel 1).
+struct Geom {
+  int rank;
+  int Cin, Cout, groups, cig, cog;
+  int kt, kh, kw;
+  int st, sh, sw;        // strides (t, h, w)
+  int pt, ph, pw;        // paddings
+  int dt, dh, dw;        // dilations
+  int H, W, Ho, Wo;
+  int64_t B;
+  int in_dtype, out_dtype, act;
+  int f, delay, R;       // receptive field, d = f - p - 1, ring slots R = ceil((f-1)/s)
+  int Cq;                // ceil(Cout / 4): channel quads of the state layout
+  int64_t HWo;           // Ho * Wo
+  int64_t slot_elems;    // Cq * 4 * B * HWo
+};
+
+// Physical state layout (internal; co_state_get converts to the canonical one):
+//   S[slot][Cout/4][B * Ho * Wo][4] fp32,
+// i.e. for a fixed slot and channel quad the (stream, pixel) rows are
+// contiguous 16-byte float4s, so a warp of consecutive output pixels moves
+// 512 contiguous bytes per instruction.
+__host__ __device__ inline int64_t state_index(const Geom& g, int slot, int64_t pix, int o) {
+  return ((int64_t(slot) * g.Cq + (o >> 2)) * (g.B * g.HWo) + pix) * 4 + (o & 3);
+}
+
+// One step's clock decisions, computed on the host:
+// slot[k] is the ring slot of the output that temporal slice k of this frame
+// contributes to (-1: no contribution, i.e. an output that is never emitted or
+// a stride-skipped phase).  k = kt-1 completes (emit), k = 0 starts
+// (overwrite), 0 < k < kt-1 accumulate.
+struct StepArgs {
+  const void* x;         // frame of stream 0, channels-last (H, W, Cin); nullptr = zero frame
+  int64_t x_bstride;     // elements between consecutive streams
+  void* y;               // output of stream 0, channels-last (Ho, Wo, Cout)
+  int64_t y_bstride;
+  float* state;
+  int slot[kMaxKt];
+  int emit;              // ready: produce y from slice kt-1
+  int update;            // update_state: write the ring
+};
+
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T> __device__ __forceinline__ T from_f(float v);
+template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+__device__ __forceinline__ float activate(float v, int act) { return (act == 1 && v < 0.f) ? 0.f : v; }
+
+// ---- launchers implemented in the .cu files (host side) --------------------
+cudaError_t launch_step_direct(const Geom& g, const StepArgs& a, const float* w_direct, const float* bias,
+                               cudaStream_t s);
+cudaError_t launch_forward_direct(const Geom& g, const void* x, int64_t T, void* y, int64_t Tp,
+                                  const float* w_direct, const float* bias, cudaStream_t s);
+cudaError_t launch_state_get(const Geom& g, const float* state, float* dst, int head, int64_t i_next,
+                             int64_t m_next, cudaStream_t s);
+cudaError_t launch_state_set(const Geom& g, float* state, const float* src, int head, cudaStream_t s);
+cudaError_t launch_pack_direct_weights(const Geom& g, const void* w, float* w_direct, cudaStream_t s);
+
+}  // namespace co

@@ -1,0 +1,14 @@
+// dense_tc.cuh — interface of the dense tcgen05 / TMEM / TMA continual-conv
+// step kernel (K4, `k_step_dense_tc`).  Implementation: k_dense_tc.cu.
+#pragma once
+#include <string>
+#include "common.cuh"
+
+namespace co {
+struct DenseTC;
+bool dense_tc_supported(const Geom& g);
+DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err);
+void dense_tc_destroy(DenseTC* t);
+const char* dense_tc_name(const DenseTC* t);
+cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const float* bias, cudaStream_t s);
+}  // namespace co

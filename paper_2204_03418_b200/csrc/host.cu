@@ -1,0 +1,520 @@
+// host.cu — the C ABI (include/co.h): handle lifetime, validation, the host
+// clock, kernel dispatch, forward_steps folding,
+// canonical state transfer, the layer-stack driver (row a7) and the host-
+// buffer entry point.  No CPU compute path exists: every value is produced by
+// a CUDA kernel; if no kernel fits, the call fails with CO_ERR_UNSUPPORTED.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/co.h"
+#include "common.cuh"
+#include "dense_tc.cuh"
+#include "depthwise.cuh"
+
+using co::Geom;
+using co::StepArgs;
+
+// ----------------------------------------------------------------- errors
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CO_CUDA(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      return fail(e_ == cudaErrorMemoryAllocation ? CO_ERR_OOM : CO_ERR_CUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                          \
+  } while (0)
+
+extern "C" const char* co_last_error(void) { return g_err.c_str(); }
+extern "C" int co_abi_version(void) { return CO_ABI_VERSION; }
+
+// ----------------------------------------------------------------- integer helpers
+
+static inline int64_t floor_div(int64_t a, int64_t b) {
+  int64_t q = a / b;
+  if ((a % b != 0) && (a < 0)) --q;
+  return q;
+}
+static inline int64_t floor_mod(int64_t a, int64_t b) { return a - floor_div(a, b) * b; }
+static inline int64_t ceil_div(int64_t a, int64_t b) { return -floor_div(-a, b); }
+static inline size_t dsize(int dt) { return dt == co::F32 ? 4 : 2; }
+
+// ----------------------------------------------------------------- handle
+
+struct co_conv {
+  co_conv_desc desc;
+  Geom g;
+  int kernel_used = CO_KERNEL_DIRECT;
+  std::string kname;
+  float* w_direct = nullptr;   // [kt][kh][kw][Cin/g][Cout] fp32
+  float* bias = nullptr;       // (Cout) fp32, zeros when absent
+  float* state = nullptr;      // R * slot_elems fp32
+  int64_t n = 0;               // host clock: stateful steps since clean
+  co::DenseTC* tc = nullptr;   // dense tcgen05 resources (packed weights)
+  co::Depthwise* dw = nullptr; // depthwise resources
+  void* hx = nullptr;          // staging for *_host
+  void* hy = nullptr;
+};
+
+struct co_stack {
+  std::vector<co_conv*> layers;
+  std::vector<void*> act;      // inter-layer activations (one per layer but the last)
+};
+
+static int make_geom(const co_conv_desc* d, Geom& g) {
+  if (!d) return fail(CO_ERR_ARG, "null descriptor");
+  if (d->spatial_rank < 0 || d->spatial_rank > 2) return fail(CO_ERR_ARG, "spatial_rank must be 0, 1 or 2");
+  int k[3], s[3], p[3], dl[3], in[2];
+  for (int a = 0; a < 3; ++a) {
+    const bool present = (a == 0) || (a <= d->spatial_rank);
+    k[a] = present ? d->kernel[a] : 1;
+    s[a] = present ? d->stride[a] : 1;
+    p[a] = present ? d->padding[a] : 0;
+    dl[a] = present ? d->dilation[a] : 1;
+    if (k[a] < 1 || s[a] < 1 || dl[a] < 1 || p[a] < 0)
+      return fail(CO_ERR_ARG, "axis %d: kernel/stride/dilation must be >= 1 and padding >= 0", a);
+  }
+  for (int a = 0; a < 2; ++a) {
+    in[a] = (a < d->spatial_rank) ? d->in_spatial[a] : 1;
+    if (in[a] < 1) return fail(CO_ERR_ARG, "in_spatial[%d] must be >= 1", a);
+  }
+  if (d->in_channels < 1 || d->out_channels < 1 || d->groups < 1)
+    return fail(CO_ERR_ARG, "channels and groups must be >= 1");
+  if (d->in_channels % d->groups || d->out_channels % d->groups)
+    return fail(CO_ERR_ARG, "groups (%d) must divide in_channels (%d) and out_channels (%d)", d->groups,
+                d->in_channels, d->out_channels);
+  if (d->n_streams < 1) return fail(CO_ERR_ARG, "n_streams must be >= 1");
+  if (k[0] > CO_MAX_KT) return fail(CO_ERR_UNSUPPORTED, "temporal kernel %d > CO_MAX_KT", k[0]);
+  for (int t : {d->in_dtype, d->w_dtype, d->out_dtype})
+    if (t != CO_F32 && t != CO_BF16) return fail(CO_ERR_ARG, "dtype must be CO_F32 or CO_BF16");
+  if (d->w_dtype != d->in_dtype) return fail(CO_ERR_ARG, "w_dtype must equal in_dtype");
+  if (d->activation != CO_ACT_NONE && d->activation != CO_ACT_RELU) return fail(CO_ERR_ARG, "bad activation");
+  g = Geom{};
+  g.rank = d->spatial_rank;
+  g.Cin = d->in_channels; g.Cout = d->out_channels; g.groups = d->groups;
+  g.cig = g.Cin / g.groups; g.cog = g.Cout / g.groups;
+  g.kt = k[0]; g.kh = k[1]; g.kw = k[2];
+  g.st = s[0]; g.sh = s[1]; g.sw = s[2];
+  g.pt = p[0]; g.ph = p[1]; g.pw = p[2];
+  g.dt = dl[0]; g.dh = dl[1]; g.dw = dl[2];
+  g.H = in[0]; g.W = in[1];
+  const int64_t ho = (int64_t(g.H) + 2 * g.ph - int64_t(g.dh) * (g.kh - 1) - 1);
+  const int64_t wo = (int64_t(g.W) + 2 * g.pw - int64_t(g.dw) * (g.kw - 1) - 1);
+  if (ho < 0 || wo < 0) return fail(CO_ERR_ARG, "spatial kernel larger than padded input");
+  g.Ho = int(ho / g.sh + 1); g.Wo = int(wo / g.sw + 1);
+  g.B = d->n_streams;
+  g.in_dtype = d->in_dtype; g.out_dtype = d->out_dtype; g.act = d->activation;
+  g.f = g.dt * (g.kt - 1) + 1;
+  if (g.pt > g.f - 1) return fail(CO_ERR_ARG, "temporal padding %d > f-1 = %d (S:51)", g.pt, g.f - 1);
+  g.delay = g.f - g.pt - 1;
+  g.R = int(ceil_div(g.f - 1, g.st));
+  g.Cq = (g.Cout + 3) / 4;
+  g.HWo = int64_t(g.Ho) * g.Wo;
+  g.slot_elems = int64_t(g.Cq) * 4 * g.B * g.HWo;
+  return CO_OK;
+}
+
+// The host clock (a1 / a5): which ring slot each temporal slice of the frame at
+// padded index m = n + p feeds.  Slice k of frame m contributes to output i
+// with i s + k dil = m (A20); only outputs i >= 0 are ever emitted.
+static int clock_args(const Geom& g, int64_t n, StepArgs& a) {
+  const int64_t m = n + g.pt;
+  const int ready = (n >= g.delay) && floor_mod(n - g.delay, g.st) == 0;
+  for (int k = 0; k < co::kMaxKt; ++k) a.slot[k] = -1;
+  for (int k = 0; k < g.kt; ++k) {
+    const int64_t q = m - int64_t(k) * g.dt;
+    if (floor_mod(q, g.st) != 0) continue;
+    const int64_t i = floor_div(q, g.st);
+    if (i < 0 || g.R == 0) continue;
+    a.slot[k] = int(floor_mod(i, g.R));
+  }
+  a.emit = ready;
+  return ready;
+}
+
+static int head_of(const Geom& g, int64_t n) {
+  if (g.R == 0) return 0;
+  return int(floor_mod(ceil_div(n - g.delay, g.st), g.R));
+}
+
+static bool dense_tc_fits(const Geom& g) { return co::dense_tc_supported(g); }
+static bool depthwise_fits(const Geom& g) { return co::depthwise_supported(g); }
+
+extern "C" int co_conv_create(const co_conv_desc* desc, const void* weights, const float* bias,
+                              int weights_on_device, co_conv** out) {
+  if (!out) return fail(CO_ERR_ARG, "null out");
+  *out = nullptr;
+  Geom g;
+  if (int r = make_geom(desc, g)) return r;
+  if (!weights) return fail(CO_ERR_ARG, "null weights");
+  // Dispatch rule: fp32 -> CUDA cores (TF32 would break 1e-4);
+  // bf16 dense contractions -> tcgen05; bf16 depthwise -> CUDA-core stencil.
+  int kern = desc->kernel_choice;
+  if (kern == CO_KERNEL_AUTO) {
+    if (g.in_dtype == co::BF16 && depthwise_fits(g)) kern = CO_KERNEL_DEPTHWISE;
+    else if (g.in_dtype == co::BF16 && dense_tc_fits(g)) kern = CO_KERNEL_DENSE_TC;
+    else kern = CO_KERNEL_DIRECT;
+  }
+  if (kern == CO_KERNEL_DENSE_TC && !dense_tc_fits(g))
+    return fail(CO_ERR_UNSUPPORTED, "dense tcgen05 kernel does not support this layer shape/dtype");
+  if (kern == CO_KERNEL_DEPTHWISE && !depthwise_fits(g))
+    return fail(CO_ERR_UNSUPPORTED, "depthwise kernel does not support this layer shape/dtype");
+  if (kern != CO_KERNEL_DIRECT && kern != CO_KERNEL_DENSE_TC && kern != CO_KERNEL_DEPTHWISE)
+    return fail(CO_ERR_ARG, "bad kernel_choice");
+
+  co_conv* h = new (std::nothrow) co_conv();
+  if (!h) return fail(CO_ERR_OOM, "host allocation");
+  h->desc = *desc;
+  h->g = g;
+  h->kernel_used = kern;
+  auto cleanup = [&](int code) { co_conv_destroy(h); return code; };
+
+  const int64_t wn = int64_t(g.Cout) * g.cig * g.kt * g.kh * g.kw;
+  const size_t wbytes = size_t(wn) * dsize(g.in_dtype);
+  void* wdev = nullptr;
+  cudaError_t e;
+  if (!weights_on_device) {
+    if ((e = cudaMalloc(&wdev, wbytes)) != cudaSuccess) return cleanup(fail(CO_ERR_OOM, "weights: %s", cudaGetErrorString(e)));
+    if ((e = cudaMemcpy(wdev, weights, wbytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+      return cleanup(fail(CO_ERR_CUDA, "weights copy: %s", cudaGetErrorString(e)));
+  }
+  const void* wsrc = weights_on_device ? weights : wdev;
+  auto freew = [&]() { if (wdev) cudaFree(wdev); wdev = nullptr; };
+  if ((e = cudaMalloc(&h->w_direct, sizeof(float) * wn)) != cudaSuccess) { freew(); return cleanup(fail(CO_ERR_OOM, "%s", cudaGetErrorString(e))); }
+  if ((e = co::launch_pack_direct_weights(g, wsrc, h->w_direct, 0)) != cudaSuccess) { freew(); return cleanup(fail(CO_ERR_CUDA, "pack: %s", cudaGetErrorString(e))); }
+  if ((e = cudaMalloc(&h->bias, sizeof(float) * g.Cout)) != cudaSuccess) { freew(); return cleanup(fail(CO_ERR_OOM, "%s", cudaGetErrorString(e))); }
+  if (bias) {
+    e = cudaMemcpy(h->bias, bias, sizeof(float) * g.Cout, weights_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+  } else {
+    e = cudaMemset(h->bias, 0, sizeof(float) * g.Cout);
+  }
+  if (e != cudaSuccess) { freew(); return cleanup(fail(CO_ERR_CUDA, "bias: %s", cudaGetErrorString(e))); }
+  if (g.R > 0) {
+    if ((e = cudaMalloc(&h->state, sizeof(float) * g.slot_elems * g.R)) != cudaSuccess) { freew(); return cleanup(fail(CO_ERR_OOM, "state (%lld bytes): %s", (long long)(sizeof(float) * g.slot_elems * g.R), cudaGetErrorString(e))); }
+    if ((e = cudaMemset(h->state, 0, sizeof(float) * g.slot_elems * g.R)) != cudaSuccess) { freew(); return cleanup(fail(CO_ERR_CUDA, "%s", cudaGetErrorString(e))); }
+  }
+  h->kname = "k_step_direct";
+  if (kern == CO_KERNEL_DENSE_TC) {
+    std::string err;
+    h->tc = co::dense_tc_create(g, wsrc, err);
+    if (!h->tc) { freew(); return cleanup(fail(CO_ERR_CUDA, "dense_tc_create: %s", err.c_str())); }
+    h->kname = co::dense_tc_name(h->tc);
+  } else if (kern == CO_KERNEL_DEPTHWISE) {
+    std::string err;
+    h->dw = co::depthwise_create(g, wsrc, err);
+    if (!h->dw) { freew(); return cleanup(fail(CO_ERR_CUDA, "depthwise_create: %s", err.c_str())); }
+    h->kname = co::depthwise_name(h->dw);
+  }
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) { freew(); return cleanup(fail(CO_ERR_CUDA, "create: %s", cudaGetErrorString(e))); }
+  freew();
+  *out = h;
+  return CO_OK;
+}
+
+extern "C" int co_conv_destroy(co_conv* h) {
+  if (!h) return CO_OK;
+  if (h->tc) co::dense_tc_destroy(h->tc);
+  if (h->dw) co::depthwise_destroy(h->dw);
+  cudaFree(h->w_direct);
+  cudaFree(h->bias);
+  cudaFree(h->state);
+  cudaFree(h->hx);
+  cudaFree(h->hy);
+  delete h;
+  return CO_OK;
+}
+
+extern "C" int co_conv_info(const co_conv* h, co_info* info) {
+  if (!h || !info) return fail(CO_ERR_ARG, "null argument");
+  const Geom& g = h->g;
+  info->n = h->n;
+  info->head = head_of(g, h->n);
+  info->ring_slots = g.R;
+  info->delay = g.delay;
+  info->receptive_field = g.f;
+  info->stride_t = g.st;
+  info->padding_t = g.pt;
+  info->out_spatial[0] = g.Ho;
+  info->out_spatial[1] = g.Wo;
+  info->kernel_used = h->kernel_used;
+  return CO_OK;
+}
+
+extern "C" int co_delay(const co_conv* h, int64_t* delay) {
+  if (!h || !delay) return fail(CO_ERR_ARG, "null argument");
+  *delay = h->g.delay;
+  return CO_OK;
+}
+
+extern "C" const char* co_kernel_name(const co_conv* h) { return h ? h->kname.c_str() : ""; }
+
+// ----------------------------------------------------------------- step
+
+static int launch_step(co_conv* h, const StepArgs& a, cudaStream_t s) {
+  cudaError_t e;
+  switch (h->kernel_used) {
+    case CO_KERNEL_DENSE_TC: e = co::dense_tc_step(h->tc, h->g, a, h->bias, s); break;
+    case CO_KERNEL_DEPTHWISE: e = co::depthwise_step(h->dw, h->g, a, h->bias, s); break;
+    default: e = co::launch_step_direct(h->g, a, h->w_direct, h->bias, s); break;
+  }
+  if (e != cudaSuccess) return fail(CO_ERR_CUDA, "step kernel %s: %s", h->kname.c_str(), cudaGetErrorString(e));
+  return CO_OK;
+}
+
+// One clock tick on `state` (the handle's ring or a scratch copy).
+static int step_impl(co_conv* h, int64_t& n, float* state, const void* x, int64_t x_bstride, void* y,
+                     int64_t y_bstride, int update_state, int* ready, cudaStream_t s) {
+  StepArgs a;
+  const int r = clock_args(h->g, n, a);
+  a.x = x; a.x_bstride = x_bstride;
+  a.y = y; a.y_bstride = y_bstride;
+  a.state = state;
+  a.update = update_state ? 1 : 0;
+  if (r || update_state) {   // nothing to do on an Empty tick that does not update
+    if (int rc = launch_step(h, a, s)) return rc;
+  }
+  if (update_state) ++n;
+  if (ready) *ready = r;
+  return CO_OK;
+}
+
+extern "C" int co_forward_step(co_conv* h, const void* x, void* y, int update_state, int* ready,
+                               co_stream stream) {
+  if (!h) return fail(CO_ERR_ARG, "null handle");
+  if (!y) return fail(CO_ERR_ARG, "null y");
+  const Geom& g = h->g;
+  return step_impl(h, h->n, h->state, x, int64_t(g.H) * g.W * g.Cin, y, g.HWo * g.Cout, update_state, ready,
+                   (cudaStream_t)stream);
+}
+
+extern "C" int co_forward_step_host(co_conv* h, const void* x_host, void* y_host, int update_state, int* ready,
+                                    co_stream stream) {
+  if (!h || !y_host) return fail(CO_ERR_ARG, "null argument");
+  const Geom& g = h->g;
+  const size_t xb = size_t(g.B) * g.H * g.W * g.Cin * dsize(g.in_dtype);
+  const size_t yb = size_t(g.B) * g.HWo * g.Cout * dsize(g.out_dtype);
+  if (!h->hx) CO_CUDA(cudaMalloc(&h->hx, xb));
+  if (!h->hy) CO_CUDA(cudaMalloc(&h->hy, yb));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (x_host) CO_CUDA(cudaMemcpyAsync(h->hx, x_host, xb, cudaMemcpyHostToDevice, s));
+  int r = 0;
+  if (int rc = step_impl(h, h->n, h->state, x_host ? h->hx : nullptr, int64_t(g.H) * g.W * g.Cin, h->hy,
+                         g.HWo * g.Cout, update_state, &r, s))
+    return rc;
+  if (r) CO_CUDA(cudaMemcpyAsync(y_host, h->hy, yb, cudaMemcpyDeviceToHost, s));
+  CO_CUDA(cudaStreamSynchronize(s));
+  if (ready) *ready = r;
+  return CO_OK;
+}
+
+extern "C" int co_steps_ready_count(const co_conv* h, int64_t T, int pad_end, int64_t* n_ready) {
+  if (!h || !n_ready || T < 0) return fail(CO_ERR_ARG, "bad argument");
+  const Geom& g = h->g;
+  const int64_t total = T + (pad_end ? g.pt : 0);
+  int64_t c = 0;
+  for (int64_t t = 0; t < total; ++t) {
+    const int64_t n = h->n + t;
+    c += (n >= g.delay) && floor_mod(n - g.delay, g.st) == 0;
+  }
+  *n_ready = c;
+  return CO_OK;
+}
+
+extern "C" int co_forward_steps(co_conv* h, const void* x, int64_t T, void* y, uint8_t* ready_mask,
+                                int64_t* n_ready, int pad_end, int update_state, co_stream stream) {
+  if (!h || (!x && T > 0) || T < 0) return fail(CO_ERR_ARG, "bad argument");
+  const Geom& g = h->g;
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t cap = 0;
+  co_steps_ready_count(h, T, pad_end, &cap);
+  if (cap > 0 && !y) return fail(CO_ERR_ARG, "null y");
+  const int64_t frame = int64_t(g.H) * g.W * g.Cin;
+  const int64_t oframe = g.HWo * g.Cout;
+  const size_t isz = dsize(g.in_dtype), osz = dsize(g.out_dtype);
+  // update_state = 0: run the fold on a scratch copy of the ring and clock.
+  float* state = h->state;
+  int64_t n = h->n;
+  float* scratch = nullptr;
+  if (!update_state && g.R > 0) {
+    CO_CUDA(cudaMallocAsync((void**)&scratch, sizeof(float) * g.slot_elems * g.R, s));
+    CO_CUDA(cudaMemcpyAsync(scratch, h->state, sizeof(float) * g.slot_elems * g.R, cudaMemcpyDeviceToDevice, s));
+    state = scratch;
+  }
+  int64_t& clock = update_state ? h->n : n;
+  const int64_t total = T + (pad_end ? g.pt : 0);
+  int64_t r_count = 0;
+  int rc = CO_OK;
+  for (int64_t t = 0; t < total && rc == CO_OK; ++t) {
+    const void* xt = (t < T) ? static_cast<const char*>(x) + size_t(t) * frame * isz : nullptr;
+    void* yt = static_cast<char*>(y) + size_t(r_count) * oframe * osz;
+    int r = 0;
+    rc = step_impl(h, clock, state, xt, T * frame, r_count < cap ? yt : nullptr, cap * oframe, 1, &r, s);
+    if (ready_mask) ready_mask[t] = uint8_t(r);
+    r_count += r;
+  }
+  if (scratch) cudaFreeAsync(scratch, s);
+  if (rc) return rc;
+  if (n_ready) *n_ready = r_count;
+  return CO_OK;
+}
+
+extern "C" int co_forward_out_len(const co_conv* h, int64_t T, int64_t* T_out) {
+  if (!h || !T_out) return fail(CO_ERR_ARG, "null argument");
+  const Geom& g = h->g;
+  *T_out = floor_div(T + 2 * g.pt - g.f, g.st) + 1;
+  return CO_OK;
+}
+
+extern "C" int co_forward(co_conv* h, const void* x, int64_t T, void* y, int64_t* T_out, co_stream stream) {
+  if (!h || !x || !y) return fail(CO_ERR_ARG, "null argument");
+  int64_t Tp = 0;
+  co_forward_out_len(h, T, &Tp);
+  if (Tp < 1) return fail(CO_ERR_LENGTH, "T' = %lld < 1 (T = %lld too short, S:63-65)", (long long)Tp, (long long)T);
+  cudaError_t e = co::launch_forward_direct(h->g, x, T, y, Tp, h->w_direct, h->bias, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(CO_ERR_CUDA, "forward kernel: %s", cudaGetErrorString(e));
+  if (T_out) *T_out = Tp;
+  return CO_OK;
+}
+
+// ----------------------------------------------------------------- state
+
+extern "C" int co_state_bytes(const co_conv* h, size_t* bytes) {
+  if (!h || !bytes) return fail(CO_ERR_ARG, "null argument");
+  const Geom& g = h->g;
+  *bytes = sizeof(float) * size_t(g.R) * g.B * g.HWo * g.Cout;
+  return CO_OK;
+}
+
+extern "C" int co_state_get(co_conv* h, void* dst, size_t bytes, co_info* meta, co_stream stream) {
+  if (!h) return fail(CO_ERR_ARG, "null handle");
+  size_t need = 0;
+  co_state_bytes(h, &need);
+  if (bytes != need) return fail(CO_ERR_SHAPE, "state bytes %zu != %zu", bytes, need);
+  const Geom& g = h->g;
+  if (need) {
+    if (!dst) return fail(CO_ERR_ARG, "null dst");
+    const int64_t i_next = ceil_div(h->n - g.delay, g.st);
+    cudaError_t e = co::launch_state_get(g, h->state, (float*)dst, head_of(g, h->n), i_next, h->n + g.pt,
+                                         (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(CO_ERR_CUDA, "state_get: %s", cudaGetErrorString(e));
+  }
+  if (meta) co_conv_info(h, meta);
+  return CO_OK;
+}
+
+extern "C" int co_state_set(co_conv* h, const void* src, size_t bytes, const co_info* meta, co_stream stream) {
+  if (!h || !meta) return fail(CO_ERR_ARG, "null argument");
+  size_t need = 0;
+  co_state_bytes(h, &need);
+  if (bytes != need) return fail(CO_ERR_SHAPE, "state bytes %zu != %zu", bytes, need);
+  const Geom& g = h->g;
+  if (meta->ring_slots != g.R || meta->delay != g.delay || meta->stride_t != g.st ||
+      meta->receptive_field != g.f || meta->out_spatial[0] != g.Ho || meta->out_spatial[1] != g.Wo || meta->n < 0)
+    return fail(CO_ERR_SHAPE, "state meta does not match this layer");
+  if (need) {
+    if (!src) return fail(CO_ERR_ARG, "null src");
+    cudaError_t e = co::launch_state_set(g, h->state, (const float*)src, head_of(g, meta->n), (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(CO_ERR_CUDA, "state_set: %s", cudaGetErrorString(e));
+  }
+  h->n = meta->n;
+  return CO_OK;
+}
+
+extern "C" int co_state_clean(co_conv* h, co_stream stream) {
+  if (!h) return fail(CO_ERR_ARG, "null handle");
+  const Geom& g = h->g;
+  if (g.R > 0) CO_CUDA(cudaMemsetAsync(h->state, 0, sizeof(float) * g.slot_elems * g.R, (cudaStream_t)stream));
+  h->n = 0;
+  return CO_OK;
+}
+
+// ----------------------------------------------------------------- stack
+
+extern "C" int co_stack_create(co_conv* const* layers, int n_layers, co_stack** out) {
+  if (!layers || n_layers < 1 || !out) return fail(CO_ERR_ARG, "bad argument");
+  *out = nullptr;
+  for (int l = 0; l < n_layers; ++l)
+    if (!layers[l]) return fail(CO_ERR_ARG, "null layer %d", l);
+  for (int l = 0; l + 1 < n_layers; ++l) {
+    const Geom& a = layers[l]->g;
+    const Geom& b = layers[l + 1]->g;
+    if (a.B != b.B || a.Cout != b.Cin || a.Ho != b.H || a.Wo != b.W || a.out_dtype != b.in_dtype)
+      return fail(CO_ERR_SHAPE, "layer %d output (B=%lld C=%d %dx%d dt=%d) != layer %d input (B=%lld C=%d %dx%d dt=%d)",
+                  l, (long long)a.B, a.Cout, a.Ho, a.Wo, a.out_dtype, l + 1, (long long)b.B, b.Cin, b.H, b.W, b.in_dtype);
+  }
+  co_stack* st = new (std::nothrow) co_stack();
+  if (!st) return fail(CO_ERR_OOM, "host allocation");
+  st->layers.assign(layers, layers + n_layers);
+  for (int l = 0; l + 1 < n_layers; ++l) {
+    const Geom& a = layers[l]->g;
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, size_t(a.B) * a.HWo * a.Cout * dsize(a.out_dtype));
+    if (e != cudaSuccess) { co_stack_destroy(st); return fail(CO_ERR_OOM, "stack activation: %s", cudaGetErrorString(e)); }
+    st->act.push_back(p);
+  }
+  *out = st;
+  return CO_OK;
+}
+
+extern "C" int co_stack_destroy(co_stack* st) {
+  if (!st) return CO_OK;
+  for (void* p : st->act) cudaFree(p);
+  delete st;
+  return CO_OK;
+}
+
+extern "C" int co_stack_step(co_stack* st, const void* x, void* y, int update_state, int* ready, co_stream stream) {
+  if (!st || !y) return fail(CO_ERR_ARG, "null argument");
+  const void* cur = x;
+  const int L = int(st->layers.size());
+  for (int l = 0; l < L; ++l) {
+    void* out = (l + 1 < L) ? st->act[l] : y;
+    int r = 0;
+    if (int rc = co_forward_step(st->layers[l], cur, out, update_state, &r, stream)) return rc;
+    if (!r) {   // Empty ends the tick; downstream layers are not advanced
+      if (ready) *ready = 0;
+      return CO_OK;
+    }
+    cur = out;
+  }
+  if (ready) *ready = 1;
+  return CO_OK;
+}
+
+extern "C" int co_stack_delay(const co_stack* st, int64_t* d_nn) {
+  if (!st || !d_nn) return fail(CO_ERR_ARG, "null argument");
+  // Principle 6 in the worked-example reading (A3).
+  int64_t s_acc = 0, p_acc = 0, f_acc = 0;
+  for (size_t l = 0; l < st->layers.size(); ++l) {
+    const Geom& g = st->layers[l]->g;
+    if (l == 0) { s_acc = g.st; p_acc = g.pt; f_acc = g.f; }
+    else { p_acc += int64_t(g.pt) * s_acc; f_acc += int64_t(g.f - 1) * s_acc; s_acc *= g.st; }
+  }
+  *d_nn = f_acc - p_acc - 1;
+  return CO_OK;
+}
+
+extern "C" int co_stack_clean(co_stack* st, co_stream stream) {
+  if (!st) return fail(CO_ERR_ARG, "null stack");
+  for (co_conv* h : st->layers)
+    if (int rc = co_state_clean(h, stream)) return rc;
+  return CO_OK;
+}
