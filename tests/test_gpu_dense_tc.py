@@ -1,0 +1,113 @@
+"""GPU parity of the dense tcgen05 step kernel (k_step_dense_tc) against the
+fp64 oracle and against the generic CUDA-core kernel, through the C ABI.
+
+Sizes span several tiles, both channel parts and a ragged last tile; the
+exact-integer regime is compared bit for bit.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from tests.helpers import make_pair, np_of, rel_err, to_cl
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    # C2-shaped halo mode: 3x3 spatial, pad 1, several tiles per stream, ragged rows
+    "halo_c2like": dict(desc=O.Desc(2, 64, 64, (3, 3, 3), padding=(0, 1, 1), in_spatial=(13, 24)), B=3),
+    "halo_c2like_pt1": dict(desc=O.Desc(2, 32, 64, (3, 3, 3), padding=(1, 1, 1), in_spatial=(9, 30)), B=2),
+    "halo_wide": dict(desc=O.Desc(2, 16, 32, (3, 3, 3), padding=(0, 1, 1), in_spatial=(5, 56)), B=2),
+    "halo_kt5": dict(desc=O.Desc(2, 16, 32, (5, 3, 3), padding=(0, 1, 1), in_spatial=(7, 11)), B=2),
+    "halo_kt1": dict(desc=O.Desc(2, 64, 64, (1, 3, 3), padding=(0, 1, 1), in_spatial=(10, 12)), B=2),
+    "halo_nopad": dict(desc=O.Desc(2, 16, 32, (3, 3, 3), in_spatial=(9, 10)), B=2),
+    # C5-shaped flat mode: 25 joints, kt 9, dilation 2, rows span streams, ragged tail
+    "flat_c5like": dict(desc=O.Desc(1, 32, 32, (9, 1), dilation=(2, 1), in_spatial=(25, 1)), B=7),
+    "flat_conv1d": dict(desc=O.Desc(0, 48, 32, (3,), padding=(1,)), B=300),
+}
+
+
+def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0):
+    d, B = CASES[case]["desc"], CASES[case]["B"]
+    rng = np.random.default_rng(seed)
+    if integer:
+        W = rng.integers(-2, 3, d.w_shape).astype(np.float64)
+        b = rng.integers(-2, 3, d.cout).astype(np.float64)
+    else:
+        W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
+        b = rng.standard_normal(d.cout) * 0.1
+    conv, sm, Wq, bq = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="dense_tc")
+    ref_conv, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="direct")
+    assert conv.kernel_used == "dense_tc", conv.kernel_name
+    H, Wd = d.in_hw
+    shp = (B, d.cin) + ((H,) if d.spatial_rank >= 1 else ()) + ((Wd,) if d.spatial_rank >= 2 else ())
+    steps = steps or (d.receptive_field + 4)
+    ys, refs, yds = [], [], []
+    for t in range(steps):
+        x = rng.integers(-2, 3, shp).astype(np.float64) if integer else rng.standard_normal(shp)
+        xt = to_cl(x, torch.bfloat16)
+        y = conv.forward_step(xt)
+        yd = ref_conv.forward_step(xt)
+        r = sm.forward_step(np_of(xt))
+        assert (y is None) == (r is None) == (yd is None)
+        assert (conv.n, conv.head) == (sm.n, sm.head)
+        if y is not None:
+            ys.append(np_of(y)); refs.append(r.reshape(y.shape)); yds.append(np_of(yd))
+    return conv, np.stack(ys), np.stack(refs), np.stack(yds)
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_dense_tc_vs_oracle(case):
+    conv, y, ref, yd = _run(case)
+    assert rel_err(y, ref) <= 2e-2
+    # fp32 accumulation of exact bf16 products: in practice ~1e-6 relative
+    assert rel_err(y, ref) <= 1e-4
+    assert rel_err(y, yd) <= 1e-4
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_dense_tc_exact_integer_bitwise(case):
+    _, y, ref, yd = _run(case, integer=True)
+    assert np.array_equal(y, ref)
+    assert np.array_equal(y, yd)
+
+
+@pytest.mark.parametrize("case", ["halo_c2like", "flat_c5like"])
+def test_dense_tc_bf16_output(case):
+    _, y, ref, _ = _run(case, out_dtype=torch.bfloat16)
+    assert rel_err(y, ref) <= 2e-2
+
+
+@pytest.mark.parametrize("case", ["halo_c2like", "flat_c5like"])
+def test_dense_tc_state_and_steps(case):
+    """State get vs oracle O5, update_state=False purity, forward_steps fold."""
+    d, B = CASES[case]["desc"], CASES[case]["B"]
+    rng = np.random.default_rng(5)
+    W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
+    b = rng.standard_normal(d.cout) * 0.1
+    conv, sm, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="dense_tc")
+    conv2, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="dense_tc")
+    H, Wd = d.in_hw
+    shp = (B, d.cin) + ((H,) if d.spatial_rank >= 1 else ()) + ((Wd,) if d.spatial_rank >= 2 else ())
+    T = d.receptive_field + 3
+    frames = [to_cl(rng.standard_normal(shp), torch.bfloat16) for _ in range(T)]
+    for x in frames:
+        conv.forward_step(x)
+        sm.forward_step(np_of(x))
+    st, meta = conv.state_dict_stream()
+    ref = sm.state()
+    got = np_of(st).reshape((ref.shape[0], B) + d.out_spatial + (d.cout,)).transpose(0, 1, 4, 2, 3)
+    assert rel_err(got, ref) <= 1e-4
+    probe = to_cl(rng.standard_normal(shp), torch.bfloat16)
+    y_peek = conv.forward_step(probe, update_state=False)
+    st1, _ = conv.state_dict_stream()
+    assert torch.equal(st, st1)
+    assert torch.equal(y_peek, conv.forward_step(probe))
+    clip = torch.stack([f for f in frames], dim=2)       # (B, C, T, *S), channels-last per frame
+    from paper_2204_03418_b200 import channels_last
+    ys, mask = conv2.forward_steps(channels_last(clip))
+    conv3, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="dense_tc")
+    fold = [y for y in (conv3.forward_step(x) for x in frames) if y is not None]
+    assert ys.shape[2] == len(fold)
+    for i, f in enumerate(fold):
+        assert torch.equal(ys[:, :, i], f)
