@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", type=int, default=2, help="BASELINE.json config index (1-based)")
     ap.add_argument("--impl", default="co", choices=["co", "reference"])
-    ap.add_argument("--streams", type=int, default=None, help="override streams per GPU")
+    ap.add_argument("--streams", type=int, default=None, help="override streams per GPU (default: the config's count)")
     ap.add_argument("--kernel", default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -157,19 +157,23 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- workload
 
-def layer_bytes_flops(L, cfg):
-    """Algorithmic HBM bytes and FLOPs per stream-step of one layer (SURVEY §8d):
-    B_alg = x_t + y_t + 2 (kt-1) Cout H'W' * 4 (fp32 partial-sum state RMW);
-    F = 2 Cout (Cin/g) kt kh kw H'W'."""
-    H, W = cfg.in_spatial[0], (cfg.in_spatial[1] if cfg.spatial_rank >= 2 else 1)
+def layer_geom(L, in_spatial, spatial_rank):
+    H, W = in_spatial[0], (in_spatial[1] if spatial_rank >= 2 else 1)
     kh, kw = L.kernel[1], L.kernel[2]
     Ho = (H + 2 * L.padding[1] - L.dilation[1] * (kh - 1) - 1) // L.stride[1] + 1
     Wo = (W + 2 * L.padding[2] - L.dilation[2] * (kw - 1) - 1) // L.stride[2] + 1
-    esz = 2 if str(cfg.dtype).endswith("bfloat16") else 4
+    return H, W, Ho, Wo
+
+
+def layer_bytes_flops(L, in_spatial, spatial_rank, esz):
+    """Algorithmic HBM bytes and FLOPs per stream-step of one layer (SURVEY §8d):
+    B_alg = x_t + y_t + 2 (kt-1) Cout H'W' * 4 (fp32 partial-sum state RMW);
+    F = 2 Cout (Cin/g) kt kh kw H'W'."""
+    H, W, Ho, Wo = layer_geom(L, in_spatial, spatial_rank)
     x_b = L.cin * H * W * esz
     y_b = L.cout * Ho * Wo * esz
     st_b = 2 * (L.kernel[0] - 1) * L.cout * Ho * Wo * 4
-    flops = 2.0 * L.cout * (L.cin // L.groups) * L.kernel[0] * kh * kw * Ho * Wo
+    flops = 2.0 * L.cout * (L.cin // L.groups) * L.kernel[0] * L.kernel[1] * L.kernel[2] * Ho * Wo
     return x_b + y_b + st_b, flops, (x_b, y_b, st_b)
 
 
@@ -182,8 +186,13 @@ def measured_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
+# FP32 CUDA-core peak (no measured figure exists): 148 SMs x 128 FP32 lanes x
+# 2 FLOP/FMA x 1.965 GHz boost clock (B200_PROFILING.md unit counts / clocks).
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
 def ncu_traffic(kernel_name):
-    """dram bytes (read+write) per launch from the committed ncu --set full summary."""
+    """dram bytes (read+write) per stream-step from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
@@ -192,98 +201,135 @@ def ncu_traffic(kernel_name):
     return j.get(kernel_name)
 
 
+def build_layers(cfg, B, kernel="auto"):
+    """The config's continual conv layers on this rank's B streams (bf16
+    inter-layer activations, ReLU where the config says, A15)."""
+    import torch
+    import paper_2204_03418_b200 as co
+    from paper_2204_03418_b200 import synth
+    convs, spat = [], tuple(cfg.in_spatial)
+    for L, (W, b) in zip(cfg.layers, synth.params(cfg)):
+        c = co.Conv(L.cin, L.cout, L.kernel, weight=W.cuda(), bias=b.cuda(), stride=L.stride, padding=L.padding,
+                    dilation=L.dilation, groups=L.groups, spatial_rank=cfg.spatial_rank, in_spatial=spat,
+                    n_streams=B, dtype=cfg.dtype, out_dtype=cfg.dtype, activation="relu" if L.relu else None,
+                    kernel=kernel)
+        convs.append(c)
+        spat = tuple(c.out_spatial) + (1,) * (2 - len(c.out_spatial))
+    return convs
+
+
 def run_co(args, world, rank):
     import torch
     import paper_2204_03418_b200 as co
     from paper_2204_03418_b200 import synth
 
     cfg = synth.config(args.config)
+    # weak scaling (the path partitions into independent streams): each rank runs
+    # the config's stream count on its own GPU, global streams [r B, (r+1) B)
     B = args.streams or cfg.n_streams
-    if len(cfg.layers) != 1:
-        raise SystemExit("bench.py times single-layer configs (C1, C2, C5); stacks: bench_stack.py")
-    L = cfg.layers[0]
-    (W, b) = synth.params(cfg)[0]
-    conv = co.Conv(L.cin, L.cout, L.kernel, weight=W.cuda(), bias=b.cuda(), stride=L.stride, padding=L.padding,
-                   dilation=L.dilation, groups=L.groups, spatial_rank=cfg.spatial_rank, in_spatial=cfg.in_spatial,
-                   n_streams=B, dtype=cfg.dtype, out_dtype=cfg.dtype, kernel=args.kernel)
-    frame_bytes = B * math.prod(synth.in_shape(cfg)) * (2 if cfg.dtype == torch.bfloat16 else 4)
+    B_global = B * world
+    convs = build_layers(cfg, B, args.kernel)
+    esz = 2 if cfg.dtype == torch.bfloat16 else 4
+    frame_bytes = B * math.prod(synth.in_shape(cfg)) * esz
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
-    G = max(8, math.ceil(4 * l2 / frame_bytes))
-    G = min(G, 64)
-    n_global = B * world
-    pool = [synth.frame(cfg, t, rank * B, (rank + 1) * B, n_global=n_global) for t in range(G)]
-    y = co._empty_cl((B, L.cout) + conv.out_spatial, cfg.dtype, "cuda")
+    G = min(max(8, math.ceil(4 * l2 / frame_bytes)), 64)
+    pool = [synth.frame(cfg, t, rank * B, (rank + 1) * B, n_global=B_global) for t in range(G)]
+    acts = [co._empty_cl((B, c.out_channels) + c.out_spatial, c.out_dtype, "cuda") for c in convs]
     stream = torch.cuda.current_stream()
-    # warm-up: fill the delay so every timed step is a Ready (steady-state) step
-    for n in range(max(args.warmup, 3, conv.delay + 1)):
-        conv.forward_step(pool[n % G], out=y)
+    nL = len(convs)
+
+    def tick(x, evs=None):
+        cur = x
+        for l, c in enumerate(convs):
+            y = c.forward_step(cur, out=acts[l])
+            if evs is not None:
+                evs[l].record(stream)
+            if y is None:
+                return False
+            cur = y
+        return True
+
+    # warm-up: fill every layer's delay so each timed tick runs all layers (steady state)
+    d_nn = co.Stack(convs).delay if nL > 1 else convs[0].delay
+    for n in range(max(args.warmup, 3) + d_nn):
+        tick(pool[n % G])
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     K = args.steps
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    evl = [[torch.cuda.Event(enable_timing=True) for _ in range(nL)] for _ in range(K)]
     sampler = ClockSampler(torch.cuda.current_device())
     with sampler:
-        ev[0].record(stream)
         for k in range(K):
-            conv.forward_step(pool[k % G], out=y)
-            ev[k + 1].record(stream)
-        # sample clocks while the queued steps run
-        t_end = time.time() + 30
-        while not ev[K].query() and time.time() < t_end:
+            ev0[k].record(stream)
+            assert tick(pool[k % G], evl[k])
+        t_end = time.time() + 60
+        while not evl[K - 1][-1].query() and time.time() < t_end:
             sampler.sample()
             time.sleep(0.005)
         torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(K)]      # ms per launch (one kernel per step)
-    elapsed_ms = ev[0].elapsed_time(ev[K])
+    elapsed_ms = ev0[0].elapsed_time(evl[K - 1][-1])
+    layer_ms = [statistics.mean(([ev0[k].elapsed_time(evl[k][0]) for k in range(K)] if l == 0 else
+                                 [evl[k][l - 1].elapsed_time(evl[k][l]) for k in range(K)])) for l in range(nL)]
     [elapsed_max] = all_reduce([elapsed_ms], op=_max_op())
     [total_ss] = all_reduce([float(B * K)], op=_sum_op())
     value = total_ss / (elapsed_max / 1e3)
 
-    # roofline of the (single) step kernel
-    bytes_ss, flops_ss, parts = layer_bytes_flops(L, cfg)
     hbm, bf16, src = measured_peaks()
-    kern_ms = statistics.mean(per)
-    ach_gbs = bytes_ss * B / (kern_ms / 1e3) / 1e9
-    ach_tf = flops_ss * B / (kern_ms / 1e3) / 1e12
-    t_hbm = bytes_ss / (hbm * 1e9)
-    t_tc = flops_ss / (bf16 * 1e12)
-    bound = "hbm" if t_hbm >= t_tc else "tensor"
-    if conv.kernel_used == "direct" and cfg.dtype == torch.float32:
-        bound = "hbm" if t_hbm >= flops_ss / 74.4e12 else "alu"
-    roof = {"bound": bound, "kernel": conv.kernel_name, "peak_source": src}
-    if bound == "hbm":
-        roof.update({"achieved": round(ach_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach_gbs / hbm, 4)})
-    elif bound == "tensor":
-        roof.update({"achieved": round(ach_tf, 2), "peak": bf16, "unit": "TFLOP/s", "frac": round(ach_tf / bf16, 4)})
-    else:
-        roof.update({"achieved": round(ach_tf, 2), "peak": 74.4, "unit": "TFLOP/s", "frac": round(ach_tf / 74.4, 4)})
-    tr = ncu_traffic(conv.kernel_name)
-    roof["traffic"] = None if tr is None else tr.get("bytes_per_stream_step", 0) * B
-    roof["alg_bytes_per_launch"] = bytes_ss * B
-    roof["tensor_frac_of_peak"] = round(ach_tf / bf16, 4)
-
+    layers, spat = [], tuple(cfg.in_spatial)
+    for l, (L, c) in enumerate(zip(cfg.layers, convs)):
+        bytes_ss, flops_ss, parts = layer_bytes_flops(L, spat, cfg.spatial_rank, esz)
+        spat = tuple(c.out_spatial) + (1,) * (2 - len(c.out_spatial))
+        ms = layer_ms[l]
+        t_hbm = bytes_ss / (hbm * 1e9)
+        if c.kernel_used == "dense_tc":
+            t_cmp, peak_c, unit_c, bound_c = flops_ss / (bf16 * 1e12), bf16, "TFLOP/s", "tensor"
+        else:
+            t_cmp, peak_c, unit_c, bound_c = flops_ss / (FP32_PEAK_TFLOPS * 1e12), FP32_PEAK_TFLOPS, "TFLOP/s", "alu"
+        ach_gbs = bytes_ss * B / (ms / 1e3) / 1e9
+        ach_tf = flops_ss * B / (ms / 1e3) / 1e12
+        if t_hbm >= t_cmp:
+            roof = {"bound": "hbm", "achieved": round(ach_gbs, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(ach_gbs / hbm, 4)}
+        else:
+            roof = {"bound": bound_c, "achieved": round(ach_tf, 2), "peak": round(peak_c, 1), "unit": unit_c,
+                    "frac": round(ach_tf / peak_c, 4)}
+        tr = ncu_traffic(c.kernel_name)
+        roof.update({"kernel": c.kernel_name, "ms_per_launch": round(ms, 4),
+                     "alg_bytes_per_launch": int(bytes_ss * B), "alg_flops_per_launch": flops_ss * B,
+                     "traffic": None if tr is None else int(tr.get("bytes_per_stream_step", 0) * B),
+                     "peak_source": src, "tensor_or_alu_frac": round(ach_tf / peak_c, 4)})
+        layers.append(roof)
+    dom = max(range(nL), key=lambda l: layer_ms[l])
+    roof = dict(layers[dom])
+    if nL > 1:
+        roof["share_of_step"] = round(layer_ms[dom] / sum(layer_ms), 4)
+    L0 = cfg.layers[0]
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(elapsed_max / K, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16" if cfg.dtype == torch.bfloat16 else "f32",
         "data": "synthetic (seeded N(0,1) frames, N(0,1/fan_in) weights; BASELINE.json configs[%d])" % (args.config - 1),
-        "config": {"workload": cfg.workload, "streams_per_gpu": B, "global_streams": n_global,
-                   "layer": {"cin": L.cin, "cout": L.cout, "kernel": list(L.kernel), "padding": list(L.padding),
-                             "stride": list(L.stride), "dilation": list(L.dilation), "groups": L.groups,
-                             "in_spatial": list(cfg.in_spatial)},
-                   "state": "fp32 partial-sum ring", "kernel": conv.kernel_name,
+        "config": {"workload": cfg.workload, "streams_per_gpu": B, "global_streams": B_global,
+                   "layers": [{"cin": L.cin, "cout": L.cout, "kernel": list(L.kernel), "padding": list(L.padding),
+                               "stride": list(L.stride), "dilation": list(L.dilation), "groups": L.groups,
+                               "relu": L.relu} for L in cfg.layers],
+                   "in_spatial": list(cfg.in_spatial), "state": "fp32 partial-sum ring",
+                   "kernels": [c.kernel_name for c in convs],
                    "parallelism": f"stream-shard x{world} (no data-path collective)",
-                   "l2_policy": f"inputs larger than L2: per-step working set {round((frame_bytes + B*bytes_ss - parts[0]*B)/1e6)} MB "
-                                f"> L2 {l2 // 2**20} MiB; input pool of {G} distinct frames"},
-        "gpu_launches": K,
+                   "l2_policy": f"inputs larger than L2: per-step working set "
+                                f"{round(sum(l['alg_bytes_per_launch'] for l in layers) / 1e6)} MB > L2 "
+                                f"{l2 // 2**20} MiB; input pool of {G} distinct frames"},
+        "gpu_launches": K * nL,
         "roofline": roof,
+        "layers": layers if nL > 1 else None,
         "clocks": sampler.summary(),
     }
-    return out, conv, pool, cfg, B
+    return out, convs, pool, cfg, B
 
 
 def _max_op():
@@ -296,21 +342,26 @@ def _sum_op():
     return dist.ReduceOp.SUM if dist.is_available() else None
 
 
-def run_e2e(args, conv, pool, cfg, B, world):
-    """Same metric through the public host-buffer API: H2D of the frame from
-    pinned memory, the step, D2H of the output, every step."""
+def run_e2e(args, convs, pool, cfg, B, world):
+    """Same metric through the public host-buffer C-ABI call (co_forward_step_host
+    / co_stack_step_host): H2D of the frame from pinned memory, the tick, D2H of
+    the output, every step."""
     import torch
+    import paper_2204_03418_b200 as co
     K = args.e2e_steps
+    last = convs[-1]
+    stack = co.Stack(convs) if len(convs) > 1 else None
+    fn = stack.forward_step_host if stack else last.forward_step_host
     xh = [p.movedim(1, -1).contiguous().cpu().pin_memory() for p in pool[:2]]
-    yh = torch.empty((B,) + tuple(conv.out_spatial) + (conv.out_channels,), dtype=conv.out_dtype).pin_memory()
+    yh = torch.empty((B,) + tuple(last.out_spatial) + (last.out_channels,), dtype=last.out_dtype).pin_memory()
     for i in range(2):
-        conv.forward_step_host(xh[i % 2], yh)
+        fn(xh[i % 2], yh)
     torch.cuda.synchronize()
     barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for k in range(K):
-        conv.forward_step_host(xh[k % 2], yh)
+        assert fn(xh[k % 2], yh)
     e.record()
     torch.cuda.synchronize()
     [ms] = all_reduce([s.elapsed_time(e)], op=_max_op())
@@ -319,18 +370,32 @@ def run_e2e(args, conv, pool, cfg, B, world):
             "d2h_bytes_per_step": int(yh.numel() * yh.element_size()), "steps": K}
 
 
+def oracle_machine(cfg, n_streams):
+    """The fp64 oracle for the config: a StepMachine (one layer) or a Stack."""
+    import oracle as O
+    from paper_2204_03418_b200 import synth
+    params = synth.params(cfg)
+    descs, spat = [], tuple(cfg.in_spatial)
+    for L in cfg.layers:
+        d = O.Desc(cfg.spatial_rank, L.cin, L.cout, L.kernel, L.stride, L.padding, L.dilation, L.groups, spat)
+        descs.append(d)
+        spat = d.out_spatial
+    Ws = [W.double().numpy() for W, _ in params]
+    bs = [b.double().numpy() for _, b in params]
+    if len(descs) == 1:
+        return O.StepMachine(descs[0], Ws[0], bs[0], n_streams), descs[0].delay
+    nL = len(descs)
+    st = O.Stack(descs, Ws, bs, [int(L.relu) for L in cfg.layers], [1] * (nL - 1) + [0], n_streams)
+    return st, sum(d.delay for d in descs)
+
+
 def oracle_sample(cfg, n_streams, ticks, pool_fn):
     """Time the fp64 oracle (as it stands) on `n_streams` streams for `ticks`
-    Ready ticks after an untimed fill of the delay.  Returns (stream-steps/s, threads)."""
-    import numpy as np
-    import oracle as O
-    L = cfg.layers[0]
-    (W, b) = __import__("paper_2204_03418_b200.synth", fromlist=["params"]).params(cfg)[0]
-    d = O.Desc(cfg.spatial_rank, L.cin, L.cout, L.kernel, L.stride, L.padding, L.dilation, L.groups, cfg.in_spatial)
-    sm = O.StepMachine(d, W.double().numpy(), b.double().numpy(), n_streams)
-    for t in range(d.delay):
+    Ready ticks after an untimed fill of the delay.  Returns (stream-steps/s, seconds)."""
+    sm, delay = oracle_machine(cfg, n_streams)
+    for t in range(delay):
         sm.forward_step(pool_fn(t))
-    frames = [pool_fn(d.delay + t) for t in range(ticks)]
+    frames = [pool_fn(delay + t) for t in range(ticks)]
     t0 = time.perf_counter()
     for x in frames:
         assert sm.forward_step(x) is not None
@@ -340,7 +405,6 @@ def oracle_sample(cfg, n_streams, ticks, pool_fn):
 
 def cpu_baseline(cfg, B_gpu):
     """Oracle on a bounded sample of the same workload (about 10-30 s of CPU)."""
-    import torch
     from paper_2204_03418_b200 import synth
     cores = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
@@ -398,9 +462,9 @@ def main():
             print(json.dumps(out), flush=True)
         return
     world, rank, local = dist_setup(args)
-    out, conv, pool, cfg, B = run_co(args, world, rank)
+    out, convs, pool, cfg, B = run_co(args, world, rank)
     if not args.no_e2e:
-        out["e2e"] = run_e2e(args, conv, pool, cfg, B, world)
+        out["e2e"] = run_e2e(args, convs, pool, cfg, B, world)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, B)
     if rank == 0:

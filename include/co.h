@@ -177,6 +177,11 @@ int co_state_clean(co_conv* h, co_stream stream);
 int co_stack_create(co_conv* const* layers, int n_layers, co_stack** out);
 int co_stack_destroy(co_stack* st);
 int co_stack_step(co_stack* st, const void* x, void* y, int update_state, int* ready, co_stream stream);
+/* Same tick with HOST buffers (first layer's input, last layer's output):
+ * copies x_host in, runs the tick, copies y_host out if Ready, synchronises
+ * `stream`; y_host is valid on return. */
+int co_stack_step_host(co_stack* st, const void* x_host, void* y_host, int update_state, int* ready,
+                       co_stream stream);
 /* Accumulated delay d_NN (Principle 6 in the worked-example reading, A3). */
 int co_stack_delay(const co_stack* st, int64_t* d_nn);
 int co_stack_clean(co_stack* st, co_stream stream);

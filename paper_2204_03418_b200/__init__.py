@@ -260,5 +260,14 @@ class Stack:
                                   C.byref(r), _stream(stream)))
         return y if r.value else None
 
+    def forward_step_host(self, x_host: torch.Tensor, y_host: torch.Tensor, update_state: bool = True,
+                          stream=None) -> bool:
+        """One tick with host (pinned) buffers: x_host (B, *S, Cin), y_host
+        (B, *S', Cout) channels-last; synchronises the stream."""
+        r = C.c_int()
+        check(lib().co_stack_step_host(self._h, C.c_void_p(x_host.data_ptr()), C.c_void_p(y_host.data_ptr()),
+                                       int(update_state), C.byref(r), _stream(stream)))
+        return bool(r.value)
+
     def clean_state(self, stream=None):
         check(lib().co_stack_clean(self._h, _stream(stream)))

@@ -24,7 +24,7 @@ KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 EXPORTS = ["co_conv_create", "co_conv_destroy", "co_conv_info", "co_delay", "co_kernel_name",
            "co_forward_step", "co_forward_step_host", "co_forward_steps", "co_steps_ready_count",
            "co_forward", "co_forward_out_len", "co_state_bytes", "co_state_get", "co_state_set",
-           "co_state_clean", "co_stack_create", "co_stack_destroy", "co_stack_step", "co_stack_delay",
+           "co_state_clean", "co_stack_create", "co_stack_destroy", "co_stack_step", "co_stack_step_host", "co_stack_delay",
            "co_stack_clean", "co_last_error", "co_abi_version"]
 
 
@@ -80,6 +80,7 @@ def lib():
             L.co_stack_create.argtypes = [C.POINTER(vp), C.c_int, C.POINTER(vp)]
             L.co_stack_destroy.argtypes = [vp]
             L.co_stack_step.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_int), vp]
+            L.co_stack_step_host.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_int), vp]
             L.co_stack_delay.argtypes = [vp, i64p]
             L.co_stack_clean.argtypes = [vp, vp]
             L.co_last_error.restype = C.c_char_p

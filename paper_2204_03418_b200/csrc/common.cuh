@@ -27,14 +27,20 @@ struct Geom {
   int Cq;                // ceil(Cout / 4): channel quads of the state layout
   int64_t HWo;           // Ho * Wo
   int64_t slot_elems;    // Cq * 4 * B * HWo
+  int state_cl;          // physical state layout: 0 = quad-major, 1 = channels-last (see state_index)
 };
 
-// Physical state layout (internal; co_state_get converts to the canonical one):
-//   S[slot][Cout/4][B * Ho * Wo][4] fp32,
-// i.e. for a fixed slot and channel quad the (stream, pixel) rows are
-// contiguous 16-byte float4s, so a warp of consecutive output pixels moves
-// 512 contiguous bytes per instruction.
+// Physical state layouts (internal; co_state_get converts to the canonical one):
+//  quad-major (state_cl = 0, dense / direct kernels):
+//   S[slot][Cout/4][B * Ho * Wo][4] fp32 -- for a fixed slot and channel quad
+//   the (stream, pixel) rows are contiguous float4s, so a warp of consecutive
+//   output pixels (one TMEM lane each) moves 512 contiguous bytes per access;
+//  channels-last (state_cl = 1, depthwise kernels, Cout % 4 == 0):
+//   S[slot][B * Ho * Wo][Cout] fp32 -- a thread owns one (pixel, channel quad)
+//   and consecutive threads take consecutive quads, so the state, the
+//   channels-last frame and the output are all read/written contiguously.
 __host__ __device__ inline int64_t state_index(const Geom& g, int slot, int64_t pix, int o) {
+  if (g.state_cl) return (int64_t(slot) * (g.B * g.HWo) + pix) * g.Cout + o;
   return ((int64_t(slot) * g.Cq + (o >> 2)) * (g.B * g.HWo) + pix) * 4 + (o & 3);
 }
 

@@ -77,6 +77,8 @@ struct co_conv {
 struct co_stack {
   std::vector<co_conv*> layers;
   std::vector<void*> act;      // inter-layer activations (one per layer but the last)
+  void* hx = nullptr;          // staging for co_stack_step_host
+  void* hy = nullptr;
 };
 
 static int make_geom(const co_conv_desc* d, Geom& g) {
@@ -180,6 +182,8 @@ extern "C" int co_conv_create(const co_conv_desc* desc, const void* weights, con
   if (kern != CO_KERNEL_DIRECT && kern != CO_KERNEL_DENSE_TC && kern != CO_KERNEL_DEPTHWISE)
     return fail(CO_ERR_ARG, "bad kernel_choice");
 
+  // the depthwise kernels stream a channels-last state ring (common.cuh)
+  g.state_cl = (kern == CO_KERNEL_DEPTHWISE) ? 1 : 0;
   co_conv* h = new (std::nothrow) co_conv();
   if (!h) return fail(CO_ERR_OOM, "host allocation");
   h->desc = *desc;
@@ -477,6 +481,8 @@ extern "C" int co_stack_create(co_conv* const* layers, int n_layers, co_stack** 
 extern "C" int co_stack_destroy(co_stack* st) {
   if (!st) return CO_OK;
   for (void* p : st->act) cudaFree(p);
+  cudaFree(st->hx);
+  cudaFree(st->hy);
   delete st;
   return CO_OK;
 }
@@ -496,6 +502,25 @@ extern "C" int co_stack_step(co_stack* st, const void* x, void* y, int update_st
     cur = out;
   }
   if (ready) *ready = 1;
+  return CO_OK;
+}
+
+extern "C" int co_stack_step_host(co_stack* st, const void* x_host, void* y_host, int update_state, int* ready,
+                                  co_stream stream) {
+  if (!st || !x_host || !y_host) return fail(CO_ERR_ARG, "null argument");
+  const Geom& g0 = st->layers.front()->g;
+  const Geom& gl = st->layers.back()->g;
+  const size_t xb = size_t(g0.B) * g0.H * g0.W * g0.Cin * dsize(g0.in_dtype);
+  const size_t yb = size_t(gl.B) * gl.HWo * gl.Cout * dsize(gl.out_dtype);
+  if (!st->hx) CO_CUDA(cudaMalloc(&st->hx, xb));
+  if (!st->hy) CO_CUDA(cudaMalloc(&st->hy, yb));
+  cudaStream_t s = (cudaStream_t)stream;
+  CO_CUDA(cudaMemcpyAsync(st->hx, x_host, xb, cudaMemcpyHostToDevice, s));
+  int r = 0;
+  if (int rc = co_stack_step(st, st->hx, st->hy, update_state, &r, stream)) return rc;
+  if (r) CO_CUDA(cudaMemcpyAsync(y_host, st->hy, yb, cudaMemcpyDeviceToHost, s));
+  CO_CUDA(cudaStreamSynchronize(s));
+  if (ready) *ready = r;
   return CO_OK;
 }
 

@@ -22,11 +22,14 @@
 //    its start address shifted by (u * Wp + v) pixels (implicit im2col: no data
 //    is duplicated).  Output rows are enumerated in the halo's padded width Wp,
 //    the Wp - Wo junk columns are computed and discarded.
-//  * Warp roles: warp 0 = TMA producer, warp 1 = MMA issuer (one thread) and
-//    TMEM owner, warps 4-7 and 8-11 = two epilogue warpgroups that take
-//    alternating items, each with its own TMEM accumulator buffer, so the MMAs
-//    of item i+1 overlap the state traffic of item i.  Epilogue threads issue
-//    the state loads of their item BEFORE waiting for the accumulator.
+//  * Warp roles: warps 0 .. 4 EG-1 = EG epilogue warpgroups (warp w reads TMEM
+//    lane quadrant w % 4), warp 4 EG = TMA producer, warp 4 EG + 1 = MMA issuer
+//    (one thread) and TMEM owner.  The EG groups take items round-robin, each
+//    with its own TMEM accumulator buffer, so the MMAs of later items overlap
+//    the state traffic of earlier ones, and EG items' state loads are in
+//    flight at once (the step is HBM-bound: the state RMW is ~80% of its bytes).
+//    Epilogue threads issue the state loads of their item BEFORE waiting for
+//    the accumulator.
 //  * State layout S[slot][Cout/4][B*Ho*Wo][4] fp32: thread = output pixel, a
 //    warp moves 512 contiguous bytes per float4 instruction.
 #include <cuda.h>
@@ -34,6 +37,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "dense_tc.cuh"
@@ -43,8 +47,8 @@ namespace co {
 
 namespace {
 
-constexpr int kStages = 2;
-constexpr int kThreads = 384;     // 12 warps: producer, mma, 2 idle, 2 x 4 epilogue
+constexpr int kMaxStages = 4;   // A-operand pipeline depth: as many as fit in shared memory
+__host__ __device__ constexpr int tc_threads(int eg) { return 32 * (4 * eg + 2); }
 constexpr int kApad = 512;        // slack after each A stage (junk rows may read past the box)
 
 struct TcParams {
@@ -56,6 +60,7 @@ struct TcParams {
   int64_t n_tiles, n_items;
   int n_split;
   int a_bytes, a_stride;          // A box bytes, A stage stride in smem
+  int stages;                     // A pipeline depth (<= kMaxStages)
   int chunk_stride;               // bytes between 8-channel groups inside an A stage
   int w_bytes;                    // packed weights of one part
   int w_off;                      // A stages start here (1 KB aligned)
@@ -78,27 +83,29 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int KT, int CC>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int KT, int CC, int EG>
+__global__ void __launch_bounds__(tc_threads(EG), 1)
     k_step_dense_tc(const __grid_constant__ CUtensorMap tmap, const TcParams p) {
   constexpr int N = KT * CC;
-  constexpr int TMEM_COLS = (N <= 128) ? 256 : 512;
-  constexpr int BUF = TMEM_COLS / 2;
+  constexpr int BUF = (N <= 128) ? 128 : 256;
+  static_assert(EG * BUF <= 512, "accumulator buffers exceed TMEM");
+  constexpr int TMEM_COLS = 512;
+  constexpr int kProducer = 4 * EG, kMma = 4 * EG + 1;
   static_assert(N % 16 == 0 && N <= 256, "invalid UMMA N");
   static_assert(CC % 16 == 0, "CC must be a multiple of 16");
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* w_s = smem;                                  // [K/8][N][16 B]
-  uint8_t* a_s = smem + p.w_off;                        // kStages x a_stride
-  uint64_t* bars = reinterpret_cast<uint64_t*>(a_s + kStages * p.a_stride);
-  uint64_t* full = bars;                                // [kStages]
-  uint64_t* empty = bars + kStages;                     // [kStages]
-  uint64_t* acc_full = bars + 2 * kStages;              // [2]
-  uint64_t* acc_empty = bars + 2 * kStages + 2;         // [2]
-  uint64_t* w_full = bars + 2 * kStages + 4;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 5);
-  float* bias_s = reinterpret_cast<float*>(bars + 2 * kStages + 6);
+  uint8_t* a_s = smem + p.w_off;                        // stages x a_stride
+  uint64_t* bars = reinterpret_cast<uint64_t*>(a_s + p.stages * p.a_stride);
+  uint64_t* full = bars;                                // [kMaxStages]
+  uint64_t* empty = bars + kMaxStages;                  // [kMaxStages]
+  uint64_t* acc_full = bars + 2 * kMaxStages;           // [EG]
+  uint64_t* acc_empty = bars + 2 * kMaxStages + EG;     // [EG]
+  uint64_t* w_full = bars + 2 * kMaxStages + 2 * EG;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 2 * EG + 1);
+  float* bias_s = reinterpret_cast<float*>(bars + 2 * kMaxStages + 2 * EG + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -106,20 +113,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int part = blockIdx.x % p.n_split;
   const int c0 = part * CC;                             // first output channel of this part
 
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
-    for (int e = 0; e < 2; ++e) { ptx::mbar_init(&acc_full[e], 1); ptx::mbar_init(&acc_empty[e], 128); }
+  if (warp == kProducer && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int e = 0; e < EG; ++e) { ptx::mbar_init(&acc_full[e], 1); ptx::mbar_init(&acc_empty[e], 128); }
     ptx::mbar_init(w_full, 1);
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_holder, TMEM_COLS);
+  if (warp == kMma) ptx::tmem_alloc(tmem_holder, TMEM_COLS);
   if (threadIdx.x < CC) bias_s[threadIdx.x] = p.bias[c0 + threadIdx.x];
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  if (warp == 0) {
+  if (warp == kProducer) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       ptx::prefetch_tmap(&tmap);
@@ -129,10 +136,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n = min(32768, p.w_bytes - off);
         ptx::bulk_g2s(w_s + off, wsrc + off, n, w_full);
       }
-      int li = 0;
-      for (int64_t item = blockIdx.x; item < p.n_items; item += grid, ++li) {
-        const int s = li % kStages;
-        ptx::mbar_wait(&empty[s], ((li / kStages) & 1) ^ 1);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t item = blockIdx.x; item < p.n_items; item += grid) {
+        ptx::mbar_wait(&empty[s], ph ^ 1);
         ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes);
         const int64_t tile = item / p.n_split;
         uint8_t* dst = a_s + s * p.a_stride;
@@ -143,64 +150,70 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ho0 = int(tile % p.tiles_per_stream) * p.MT;
           ptx::tma_load_5d(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
         }
+        if (++s == p.stages) { s = 0; ph ^= 1; }
       }
     }
     return;
   }
-  if (warp == 2 || warp == 3) return;
 
-  if (warp == 1) {
+  if (warp == kMma) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, N);
       ptx::mbar_wait(w_full, 0);
       const uint32_t a_base = ptx::smem_u32(a_s);
-      const uint32_t w_base = ptx::smem_u32(w_s);
-      const int kc_per_tap = p.Cin / 8;
-      const int taps = p.kh * p.kw;
-      int li = 0;
-      for (int64_t item = blockIdx.x; item < p.n_items; item += grid, ++li) {
-        const int s = li % kStages;
-        const int e = li & 1;
-        const int j = li >> 1;
-        ptx::mbar_wait(&acc_empty[e], (j & 1) ^ 1);
+      // Descriptors are advanced by adding (byte offset >> 4) to their 14-bit
+      // start-address field (shared memory < 256 KB, so it never carries out).
+      const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_u32(w_s), N * 16, 128);
+      const int kc2 = p.Cin / 16;                       // MMAs (K = 16) per spatial tap
+      const uint32_t chunk16 = uint32_t(p.chunk_stride) >> 3;   // 2 channel groups, in 16 B units
+      int s = 0;
+      uint32_t ph = 0;
+      int e = 0;
+      uint32_t eph = 0;
+      for (int64_t item = blockIdx.x; item < p.n_items; item += grid) {
+        ptx::mbar_wait(&acc_empty[e], eph ^ 1);
         ptx::tc_fence_after();
-        ptx::mbar_wait(&full[s], (li / kStages) & 1);
+        ptx::mbar_wait(&full[s], ph);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem + uint32_t(e * BUF);
-        const uint32_t a_stage = a_base + uint32_t(s * p.a_stride);
+        const uint64_t a_desc0 = ptx::smem_desc(a_base + uint32_t(s * p.a_stride), p.chunk_stride, 128);
+        uint64_t bd = b_desc0;
         uint32_t acc = 0;
-        for (int tap = 0; tap < taps; ++tap) {
-          const int u = tap / p.kw, v = tap - (tap / p.kw) * p.kw;
-          const uint32_t a_tap = a_stage + uint32_t((u * p.Wp + v) * 16);
-          for (int kc = 0; kc < kc_per_tap; kc += 2) {
-            const uint64_t ad = ptx::smem_desc(a_tap + uint32_t(kc * p.chunk_stride), p.chunk_stride, 128);
-            const uint64_t bd = ptx::smem_desc(w_base + uint32_t((tap * kc_per_tap + kc) * N * 16), N * 16, 128);
-            ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, acc);
-            acc = 1;
+        for (int u = 0; u < p.kh; ++u) {
+          for (int v = 0; v < p.kw; ++v) {
+            uint64_t ad = a_desc0 + uint64_t(u * p.Wp + v);   // tap (u, v): shift by u Wp + v rows
+            for (int kc = 0; kc < kc2; ++kc) {
+              ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, acc);
+              acc = 1;
+              ad += chunk16;
+              bd += uint64_t(2 * N);                         // 2 groups of N rows x 16 B
+            }
           }
         }
         ptx::tc_commit(&empty[s]);      // A stage free once these MMAs retire
         ptx::tc_commit(&acc_full[e]);   // accumulator e ready for the epilogue
+        if (++s == p.stages) { s = 0; ph ^= 1; }
+        if (++e == EG) { e = 0; eph ^= 1; }
       }
     }
     __syncwarp();
-    bar_sync_named(1, 32 + 256);
+    bar_sync_named(1, 32 + 128 * EG);
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, TMEM_COLS);
     return;
   }
 
-  // ===================== epilogue warpgroups (warps 4..11) =====================
-  const int e = (warp - 4) >> 2;                       // 0 or 1
+  // ===================== epilogue warpgroups (warps 0 .. 4 EG - 1) =====================
+  const int e = warp >> 2;                             // group = accumulator buffer
   const int q = warp & 3;                              // TMEM lane quadrant of this warp
   const int m = q * 32 + lane;                         // accumulator row = tile pixel
   const int64_t plane = p.plane;
   constexpr int NQ = CC / 4;                           // channel quads per thread
   constexpr int NS = (KT > 1) ? KT - 1 : 1;
   int li = e;
-  for (int64_t item = blockIdx.x + int64_t(e) * grid; item < p.n_items; item += 2 * int64_t(grid), li += 2) {
-    const int j = li >> 1;
+  for (int64_t item = blockIdx.x + int64_t(e) * grid; item < p.n_items; item += EG * int64_t(grid), li += EG) {
+    const int j = li / EG;
     const int64_t tile = item / p.n_split;
     // ---- this row's output pixel
     bool valid;
@@ -310,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_before();
     ptx::mbar_arrive(&acc_empty[e]);
   }
-  bar_sync_named(1, 32 + 256);
+  bar_sync_named(1, 32 + 128 * EG);
 }
 
 // ------------------------------------------------------------------ host side
@@ -339,14 +352,15 @@ __global__ void k_pack_tc_weights(const __nv_bfloat16* __restrict__ w, __nv_bflo
 typedef void (*KernFn)(const CUtensorMap, const TcParams);
 
 struct Variant {
-  int KT, CC;
+  int KT, CC, EG;
   KernFn fn;
 };
 
-#define CO_TC_VARIANT(kt, cc) {kt, cc, (KernFn)k_step_dense_tc<kt, cc>}
+#define CO_TC_VARIANT(kt, cc, eg) {kt, cc, eg, (KernFn)k_step_dense_tc<kt, cc, eg>}
 const Variant kVariants[] = {
-    CO_TC_VARIANT(1, 32), CO_TC_VARIANT(1, 64), CO_TC_VARIANT(2, 32), CO_TC_VARIANT(3, 16),
-    CO_TC_VARIANT(3, 32), CO_TC_VARIANT(5, 16), CO_TC_VARIANT(5, 32), CO_TC_VARIANT(9, 16),
+    CO_TC_VARIANT(1, 32, 4), CO_TC_VARIANT(1, 64, 4), CO_TC_VARIANT(2, 32, 4), CO_TC_VARIANT(3, 16, 4),
+    CO_TC_VARIANT(3, 32, 2), CO_TC_VARIANT(3, 32, 3), CO_TC_VARIANT(3, 32, 4), CO_TC_VARIANT(5, 16, 4),
+    CO_TC_VARIANT(5, 32, 2), CO_TC_VARIANT(9, 16, 2),
 };
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -365,7 +379,7 @@ struct Plan {
   bool ok = false;
   const Variant* var = nullptr;
   int n_split = 0, flat = 0, MT = 0, Wp = 0, tiles_per_stream = 0;
-  int a_bytes = 0, a_stride = 0, chunk_stride = 0, w_bytes = 0;
+  int a_bytes = 0, a_stride = 0, chunk_stride = 0, w_bytes = 0, stages = 2;
   int64_t n_tiles = 0;
   size_t smem = 0;
 };
@@ -390,18 +404,24 @@ Plan make_plan(const Geom& g) {
   const int a_bytes = (g.Cin / 8) * a_rows * 16;
   const int a_stride = ((a_bytes + kApad + 1023) / 1024) * 1024;
   const int64_t K = int64_t(g.Cin) * g.kh * g.kw;
-  // largest CC (fewest parts) whose weights + A stages fit in shared memory
+  // largest CC (fewest parts) whose weights + A stages fit in shared memory;
+  // among equal CC the most epilogue groups (CO_TC_EG=<n> pins it, for A/B runs)
+  const char* eg_env = getenv("CO_TC_EG");
+  const int eg_pin = eg_env ? atoi(eg_env) : 0;
   for (const Variant& v : kVariants) {
     if (v.KT != g.kt || g.Cout % v.CC != 0) continue;
+    if (eg_pin && v.EG != eg_pin) continue;
     const int N = v.KT * v.CC;
     const int64_t w_bytes = int64_t(N) * K * 2;
-    const size_t smem = 1024 + size_t((w_bytes + 1023) / 1024 * 1024) + kStages * size_t(a_stride) + 256 + v.CC * 4;
-    if (smem > kSmemLimit) continue;
-    if (!pl.ok || v.CC > pl.var->CC) {
+    const size_t fixed = 1024 + size_t((w_bytes + 1023) / 1024 * 1024) + 256 + v.CC * 4;
+    if (fixed + 2 * size_t(a_stride) > kSmemLimit) continue;
+    const int stages = int(std::min<size_t>(kMaxStages, (kSmemLimit - fixed) / size_t(a_stride)));
+    if (!pl.ok || v.CC > pl.var->CC || (v.CC == pl.var->CC && v.EG > pl.var->EG)) {
       pl.ok = true;
       pl.var = &v;
       pl.w_bytes = int(w_bytes);
-      pl.smem = smem;
+      pl.stages = stages;
+      pl.smem = fixed + size_t(stages) * a_stride;
     }
   }
   if (!pl.ok) return pl;
@@ -452,7 +472,9 @@ DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, dev);
   char buf[96];
-  snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d>", pl.var->KT, pl.var->CC);
+  snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d>", pl.var->KT, pl.var->CC, pl.var->EG);
+  if (getenv("CO_LOG")) fprintf(stderr, "[co] %s: %d parts, %lld tiles, A stages %d x %d B, smem %zu B\n", buf,
+                                pl.n_split, (long long)pl.n_tiles, pl.stages, pl.a_stride, pl.smem);
   t->name = buf;
   return t;
 }
@@ -515,7 +537,7 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   p.kh = g.kh; p.kw = g.kw; p.ph = g.ph; p.pw = g.pw;
   p.flat = pl.flat; p.MT = pl.MT; p.Wp = pl.Wp; p.tiles_per_stream = pl.tiles_per_stream;
   p.n_tiles = pl.n_tiles; p.n_split = pl.n_split; p.n_items = pl.n_tiles * pl.n_split;
-  p.a_bytes = pl.a_bytes; p.a_stride = pl.a_stride; p.chunk_stride = pl.chunk_stride; p.w_bytes = pl.w_bytes;
+  p.a_bytes = pl.a_bytes; p.a_stride = pl.a_stride; p.stages = pl.stages; p.chunk_stride = pl.chunk_stride; p.w_bytes = pl.w_bytes;
   p.w_off = (pl.w_bytes + 1023) / 1024 * 1024;
   for (int k = 0; k < kMaxKt; ++k) p.slot[k] = a.slot[k];
   p.emit = a.emit; p.update = a.update; p.act = g.act; p.out_f32 = (g.out_dtype == F32);
@@ -528,8 +550,8 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   const int per = t->num_sms / pl.n_split;
   const int64_t grid = std::min<int64_t>(per, pl.n_tiles) * pl.n_split;
   void* args[] = {&map, &p};
-  return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->fn), dim3(unsigned(grid)), dim3(kThreads), args,
-                          pl.smem, s);
+  return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->fn), dim3(unsigned(grid)),
+                          dim3(tc_threads(pl.var->EG)), args, pl.smem, s);
 }
 
 }  // namespace co

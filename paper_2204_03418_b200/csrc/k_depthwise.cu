@@ -1,12 +1,405 @@
-// k_depthwise.cu — placeholder until the depthwise kernels land.
+// k_depthwise.cu — K2 / K3: depthwise (groups == Cin == Cout) continual-
+// convolution step kernels on CUDA cores (BASELINE.json north_star
+// "Depthwise/grouped step kernel: runs on CUDA cores with vectorised 128-bit
+// coalesced loads, shared-memory staging of the spatial halo").
+//
+// A depthwise layer has (kt kh kw) MACs per output element (C3-a: 27, C3-b: 5)
+// against 2 (kt-1) fp32 state accesses, so it is HBM-bound by two orders of
+// magnitude (AI 2.7 and 0.3 FLOP/B); tensor cores have nothing to
+// contract.  Both kernels therefore aim at streaming the fp32 state ring at HBM
+// bandwidth:
+//  * state layout channels-last, S[slot][B*Ho*Wo][C] (common.cuh state_cl = 1):
+//    a thread owns one (output pixel, channel quad); consecutive threads take
+//    consecutive quads of the same pixel, so every state / frame / output
+//    access of a warp is one contiguous run (512 B of state per float4 access);
+//  * each thread first issues the state loads of a batch of NB items (emit slot
+//    + the kt-2 accumulating slots), then computes, so NB x (kt-1) x 16 B per
+//    thread are in flight;
+//  * K2 (spatial kh x kw stencil): persistent CTAs keep the packed fp32 weights
+//    [kt][kh][kw][C] in shared memory; per tile (stream, band of TH output
+//    rows) the input halo (TH+kh-1) x (W+2pw) x C is staged in shared memory by
+//    cp.async (16 B, zero-fill = spatial padding) while the first batch's state
+//    loads are already in flight; the 3x3 taps are then read from shared memory
+//    (8 B per tap per thread, conflict-free: consecutive threads, consecutive
+//    8-byte words);
+//  * K3 (temporal-only, 1x1 spatial): a pure streaming kernel, no halo.
+//
+// Per item (BASELINE.json north_star):
+//   y = S[slot_{kt-1}] + P_{kt-1} + b  (emitted when ready, activation, RNE)
+//   S[slot_k] += P_k  for 0 < k < kt-1;   S[slot_0] = P_0 (after the emit read)
+// with P_k = W[:, k] (*) x_t per channel.  The slots come from the host clock.
+#include <algorithm>
+#include <cstdio>
+#include <string>
+
 #include "depthwise.cuh"
+
 namespace co {
-struct Depthwise { int dummy; };
-bool depthwise_supported(const Geom&) { return false; }
-Depthwise* depthwise_create(const Geom&, const void*, std::string& err) { err = "not built"; return nullptr; }
-void depthwise_destroy(Depthwise* t) { delete t; }
-const char* depthwise_name(const Depthwise*) { return "k_step_depthwise"; }
-cudaError_t depthwise_step(Depthwise*, const Geom&, const StepArgs&, const float*, cudaStream_t) {
-  return cudaErrorNotSupported;
+
+namespace {
+
+constexpr int kDwThreads = 256;
+constexpr int kNB = 4;                  // items per thread per batch (state loads in flight)
+constexpr size_t kHaloBudget = 48 * 1024;
+
+struct DwParams {
+  const __nv_bfloat16* x;               // frame of stream 0 (nullptr = zero frame)
+  int64_t x_bstride;                    // elements between streams
+  void* y;
+  int64_t y_bstride;
+  float* state;                         // S[slot][plane][C]
+  const float* w;                       // [kt][kh][kw][C] fp32
+  const float* bias;                    // [C]
+  int slot[kMaxKt];
+  int emit, update, act, out_f32;
+  int C, Cq, H, W, Ho, Wo, ph, pw;
+  int64_t HWo, plane;
+  int TH, bands;                        // K2 tiling: TH output rows per tile
+  int64_t n_tiles;
+  int WC, HR;                           // halo width (W + 2 pw) and rows (TH + kh - 1)
+};
+
+__device__ __forceinline__ float4 ld_bf16x4(const __nv_bfloat16* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&u.x);
+  const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
+  const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+  return make_float4(fa.x, fa.y, fb.x, fb.y);
 }
+
+__device__ __forceinline__ void st_out4(const DwParams& p, int64_t b, int64_t pin, int q, float4 v) {
+  const int64_t off = b * p.y_bstride + pin * p.C + 4 * q;
+  if (p.out_f32) {
+    *reinterpret_cast<float4*>(static_cast<float*>(p.y) + off) = v;
+  } else {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&lo);
+    u.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.y) + off) = u;
+  }
+}
+
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 f4_fma(float4 w, float4 x, float4 acc) {
+  return make_float4(fmaf(w.x, x.x, acc.x), fmaf(w.y, x.y, acc.y), fmaf(w.z, x.z, acc.z), fmaf(w.w, x.w, acc.w));
+}
+__device__ __forceinline__ float4 f4_act(float4 v, int act) {
+  if (act == 1) {
+    v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+  }
+  return v;
+}
+__device__ __forceinline__ float4* srow(const DwParams& p, int slot, int64_t pix, int q) {
+  return reinterpret_cast<float4*>(p.state + (int64_t(slot) * p.plane + pix) * p.C) + q;
+}
+
+// Prefetched state of one item: [0] = emit slot (k = kt-1), [k] = slot k (0 < k < kt-1).
+template <int KT>
+struct Pre {
+  float4 s[KT > 1 ? KT - 1 : 1];
+};
+
+template <int KT>
+__device__ __forceinline__ void prefetch(const DwParams& p, int64_t pix, int q, Pre<KT>& pr) {
+  if (KT > 1) {
+    if (p.emit) pr.s[0] = __ldcs(srow(p, p.slot[KT - 1], pix, q));
+    if (p.update) {
+#pragma unroll
+      for (int k = 1; k < KT - 1; ++k)
+        if (p.slot[k] >= 0) pr.s[k] = __ldcs(srow(p, p.slot[k], pix, q));
+    }
+  }
+}
+
+// Apply the step to one item given its per-slice partials P(k).
+template <int KT, typename PF>
+__device__ __forceinline__ void apply(const DwParams& p, int64_t b, int64_t pin, int64_t pix, int q,
+                                      const Pre<KT>& pr, const float4 bias4, PF P) {
+  if (p.emit) {
+    float4 v = f4_add(P(KT - 1), bias4);
+    if (KT > 1) v = f4_add(pr.s[0], v);
+    st_out4(p, b, pin, q, f4_act(v, p.act));
+  }
+  if (KT > 1 && p.update) {
+#pragma unroll
+    for (int k = KT - 2; k >= 1; --k)
+      if (p.slot[k] >= 0) __stcs(srow(p, p.slot[k], pix, q), f4_add(pr.s[k], P(k)));
+    if (p.slot[0] >= 0) __stcs(srow(p, p.slot[0], pix, q), P(0));
+  }
+}
+
+// ------------------------------------------------------------------ K2: spatial stencil
+template <int KT, int KH, int KW>
+__global__ void __launch_bounds__(kDwThreads, (KT <= 3 && KH * KW <= 9) ? 3 : 2) k_step_dw_st(const DwParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  float* ws = reinterpret_cast<float*>(smem);                       // [KT][KH][KW][C]
+  float* bs = ws + KT * KH * KW * p.C;                              // [C]
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(bs + p.C);   // [HR][WC][C]
+  const int tid = threadIdx.x;
+  for (int i = tid; i < KT * KH * KW * p.C; i += blockDim.x) ws[i] = p.w[i];
+  for (int i = tid; i < p.C; i += blockDim.x) bs[i] = p.bias[i];
+  const int c8 = p.C / 8;
+  const int halo_chunks = p.HR * p.WC * c8;
+  const uint32_t xs_u32 = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
+
+  for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    const int64_t b = tile / p.bands;
+    const int ho0 = int(tile % p.bands) * p.TH;
+    const int th = min(p.TH, p.Ho - ho0);
+    const int n_items = th * p.Wo * p.Cq;
+    __syncthreads();   // previous tile finished reading xs (and ws/bs are visible)
+
+    // (1) first batch's state loads go out before the halo is staged
+    Pre<KT> pre[kNB];
+    auto item_pix = [&](int it, int& q, int& r, int& wo) {
+      q = it % p.Cq;
+      const int pw_ = it / p.Cq;
+      wo = pw_ % p.Wo;
+      r = pw_ / p.Wo;
+    };
+#pragma unroll
+    for (int j = 0; j < kNB; ++j) {
+      const int it = tid + j * kDwThreads;
+      if (it < n_items) {
+        int q, r, wo;
+        item_pix(it, q, r, wo);
+        prefetch<KT>(p, b * p.HWo + int64_t(ho0 + r) * p.Wo + wo, q, pre[j]);
+      }
+    }
+    // (2) input halo -> shared memory (cp.async 16 B, zero fill outside the frame)
+    const __nv_bfloat16* xb = p.x ? p.x + b * p.x_bstride : nullptr;
+    for (int i = tid; i < halo_chunks; i += blockDim.x) {
+      const int ch = i % c8;
+      const int pc = i / c8;
+      const int c = pc % p.WC, r = pc / p.WC;
+      const int hi = ho0 - p.ph + r, wi = c - p.pw;
+      const bool in = xb && hi >= 0 && hi < p.H && wi >= 0 && wi < p.W;
+      // src-size 0 zero-fills; the (unread) address stays a valid one
+      const void* src = in ? static_cast<const void*>(xb + (int64_t(hi) * p.W + wi) * p.C + ch * 8)
+                           : static_cast<const void*>(p.w);
+      const uint32_t dst = xs_u32 + uint32_t(i) * 16u;
+      const int sz = in ? 16 : 0;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(sz) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+
+    // (3) items in batches of kNB per thread
+    for (int base = 0; base < n_items; base += kNB * kDwThreads) {
+      if (base > 0) {
+#pragma unroll
+        for (int j = 0; j < kNB; ++j) {
+          const int it = base + tid + j * kDwThreads;
+          if (it < n_items) {
+            int q, r, wo;
+            item_pix(it, q, r, wo);
+            prefetch<KT>(p, b * p.HWo + int64_t(ho0 + r) * p.Wo + wo, q, pre[j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kNB; ++j) {
+        const int it = base + tid + j * kDwThreads;
+        if (it >= n_items) continue;
+        int q, r, wo;
+        item_pix(it, q, r, wo);
+        // all kt partials in one pass over the taps (same per-slice FMA order
+        // as k_step_direct: u-major, then v)
+        float4 acc[KT];
+#pragma unroll
+        for (int k = 0; k < KT; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < KH; ++u)
+#pragma unroll
+          for (int v = 0; v < KW; ++v) {
+            const float4 xv = ld_bf16x4(xs + (int64_t(r + u) * p.WC + (wo + v)) * p.C + 4 * q);
+#pragma unroll
+            for (int k = 0; k < KT; ++k)
+              acc[k] = f4_fma(reinterpret_cast<const float4*>(ws + (k * KH * KW + u * KW + v) * p.C)[q], xv, acc[k]);
+          }
+        auto P = [&](int k) -> float4 { return acc[k]; };
+        const int64_t pin = int64_t(ho0 + r) * p.Wo + wo;
+        apply<KT>(p, b, pin, b * p.HWo + pin, q, pre[j], reinterpret_cast<const float4*>(bs)[q], P);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K3: temporal only
+template <int KT>
+__global__ void __launch_bounds__(kDwThreads) k_step_dw_t(const DwParams p) {
+  const int64_t n_items = p.plane * p.Cq;
+  const int64_t stride = int64_t(gridDim.x) * kDwThreads;
+  for (int64_t base = int64_t(blockIdx.x) * kDwThreads + threadIdx.x; base < n_items; base += kNB * stride) {
+    Pre<KT> pre[kNB];
+    float4 xv[kNB];
+#pragma unroll
+    for (int j = 0; j < kNB; ++j) {
+      const int64_t it = base + j * stride;
+      if (it < n_items) {
+        const int q = int(it % p.Cq);
+        const int64_t pix = it / p.Cq;
+        prefetch<KT>(p, pix, q, pre[j]);
+        const int64_t b = pix / p.HWo;
+        xv[j] = p.x ? ld_bf16x4(p.x + b * p.x_bstride + (pix - b * p.HWo) * p.C + 4 * q)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kNB; ++j) {
+      const int64_t it = base + j * stride;
+      if (it >= n_items) continue;
+      const int q = int(it % p.Cq);
+      const int64_t pix = it / p.Cq;
+      const int64_t b = pix / p.HWo;
+      auto P = [&](int k) -> float4 {
+        return f4_fma(__ldg(reinterpret_cast<const float4*>(p.w + k * p.C) + q), xv[j], make_float4(0.f, 0.f, 0.f, 0.f));
+      };
+      apply<KT>(p, b, pix - b * p.HWo, pix, q, pre[j], __ldg(reinterpret_cast<const float4*>(p.bias) + q), P);
+    }
+  }
+}
+
+// (C, 1, kt, kh, kw) bf16 -> [kt][kh][kw][C] fp32 (exact)
+__global__ void k_pack_dw(const __nv_bfloat16* __restrict__ w, float* __restrict__ out, int C, int kt, int kh,
+                          int kw) {
+  const int n = C * kt * kh * kw;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int r = i;
+  const int v = r % kw; r /= kw;
+  const int u = r % kh; r /= kh;
+  const int k = r % kt; r /= kt;
+  const int c = r;
+  out[((k * kh + u) * kw + v) * C + c] = __bfloat162float(w[i]);
+}
+
+typedef void (*DwFn)(const DwParams);
+struct DwVariant {
+  int KT, KH, KW;
+  DwFn fn;
+};
+#define CO_DW_ST(kt, kh, kw) {kt, kh, kw, (DwFn)k_step_dw_st<kt, kh, kw>}
+#define CO_DW_T(kt) {kt, 1, 1, (DwFn)k_step_dw_t<kt>}
+const DwVariant kDwVariants[] = {
+    CO_DW_ST(1, 3, 3), CO_DW_ST(2, 3, 3), CO_DW_ST(3, 3, 3), CO_DW_ST(5, 3, 3), CO_DW_ST(3, 5, 5),
+    CO_DW_T(2), CO_DW_T(3), CO_DW_T(4), CO_DW_T(5), CO_DW_T(7), CO_DW_T(9),
+};
+
+struct DwPlan {
+  const DwVariant* var = nullptr;
+  bool temporal = false;
+  int TH = 0, bands = 0, HR = 0, WC = 0;
+  int64_t n_tiles = 0;
+  size_t smem = 0;
+};
+
+bool make_dw_plan(const Geom& g, DwPlan& pl) {
+  if (g.in_dtype != BF16 || g.groups != g.Cin || g.Cin != g.Cout || g.Cin % 8 != 0) return false;
+  if (g.sh != 1 || g.sw != 1 || g.dh != 1 || g.dw != 1) return false;
+  const bool temporal = (g.kh == 1 && g.kw == 1 && g.ph == 0 && g.pw == 0);
+  for (const DwVariant& v : kDwVariants) {
+    if (v.KT != g.kt) continue;
+    if (temporal ? (v.KH != 1) : (v.KH != g.kh || v.KW != g.kw)) continue;
+    pl.var = &v;
+  }
+  if (!pl.var) return false;
+  pl.temporal = temporal;
+  if (temporal) return true;
+  pl.WC = g.W + 2 * g.pw;
+  const size_t row_bytes = size_t(pl.WC) * g.Cin * 2;
+  int TH = int(kHaloBudget / row_bytes) - (g.kh - 1);
+  if (TH < 1) {
+    if (size_t(g.kh) * row_bytes > 160 * 1024) return false;
+    TH = 1;
+  }
+  TH = std::min(TH, g.Ho);
+  pl.TH = TH;
+  pl.HR = TH + g.kh - 1;
+  pl.bands = (g.Ho + TH - 1) / TH;
+  pl.n_tiles = g.B * pl.bands;
+  pl.smem = size_t(g.kt * g.kh * g.kw + 1) * g.Cin * 4 + size_t(pl.HR) * row_bytes;
+  return pl.smem <= 227 * 1024;
+}
+
+}  // namespace
+
+struct Depthwise {
+  DwPlan pl;
+  float* w = nullptr;
+  int grid = 0;
+  std::string name;
+};
+
+bool depthwise_supported(const Geom& g) {
+  DwPlan pl;
+  return make_dw_plan(g, pl);
+}
+
+Depthwise* depthwise_create(const Geom& g, const void* w_dev, std::string& err) {
+  DwPlan pl;
+  if (!make_dw_plan(g, pl)) { err = "unsupported shape"; return nullptr; }
+  Depthwise* t = new Depthwise();
+  t->pl = pl;
+  const int n = g.Cin * g.kt * g.kh * g.kw;
+  cudaError_t e = cudaMalloc(&t->w, size_t(n) * 4);
+  if (e != cudaSuccess) { err = cudaGetErrorString(e); delete t; return nullptr; }
+  k_pack_dw<<<(n + 255) / 256, 256>>>(static_cast<const __nv_bfloat16*>(w_dev), t->w, g.Cin, g.kt, g.kh, g.kw);
+  if ((e = cudaGetLastError()) != cudaSuccess) { err = cudaGetErrorString(e); depthwise_destroy(t); return nullptr; }
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (!pl.temporal) {
+    e = cudaFuncSetAttribute(pl.var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
+    if (e != cudaSuccess) { err = cudaGetErrorString(e); depthwise_destroy(t); return nullptr; }
+  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.var->fn, kDwThreads, pl.temporal ? 0 : pl.smem);
+  per_sm = std::max(per_sm, 1);
+  if (pl.temporal) {
+    const int64_t items = g.B * g.HWo * (g.Cout / 4);
+    const int64_t need = (items + int64_t(kNB) * kDwThreads - 1) / (int64_t(kNB) * kDwThreads);
+    t->grid = int(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * per_sm)));
+  } else {
+    t->grid = int(std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, int64_t(sms) * per_sm)));
+  }
+  char buf[96];
+  if (pl.temporal)
+    snprintf(buf, sizeof(buf), "k_step_dw_t<%d>", pl.var->KT);
+  else
+    snprintf(buf, sizeof(buf), "k_step_dw_st<%d,%d,%d>", pl.var->KT, pl.var->KH, pl.var->KW);
+  t->name = buf;
+  return t;
+}
+
+void depthwise_destroy(Depthwise* t) {
+  if (!t) return;
+  cudaFree(t->w);
+  delete t;
+}
+
+const char* depthwise_name(const Depthwise* t) { return t->name.c_str(); }
+
+cudaError_t depthwise_step(Depthwise* t, const Geom& g, const StepArgs& a, const float* bias, cudaStream_t s) {
+  const DwPlan& pl = t->pl;
+  DwParams p{};
+  p.x = static_cast<const __nv_bfloat16*>(a.x);
+  p.x_bstride = a.x_bstride;
+  p.y = a.y;
+  p.y_bstride = a.y_bstride;
+  p.state = a.state;
+  p.w = t->w;
+  p.bias = bias;
+  for (int k = 0; k < kMaxKt; ++k) p.slot[k] = a.slot[k];
+  p.emit = a.emit; p.update = a.update; p.act = g.act; p.out_f32 = (g.out_dtype == F32);
+  p.C = g.Cout; p.Cq = g.Cout / 4; p.H = g.H; p.W = g.W; p.Ho = g.Ho; p.Wo = g.Wo; p.ph = g.ph; p.pw = g.pw;
+  p.HWo = g.HWo; p.plane = g.B * g.HWo;
+  p.TH = pl.TH; p.bands = pl.bands; p.n_tiles = pl.n_tiles; p.WC = pl.WC; p.HR = pl.HR;
+  void* args[] = {&p};
+  return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->fn), dim3(unsigned(t->grid)), dim3(kDwThreads), args,
+                          pl.temporal ? 0 : pl.smem, s);
+}
+
 }  // namespace co

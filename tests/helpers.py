@@ -68,3 +68,16 @@ def rel_err(y, ref):
         ref = ref.reshape(y.shape)
     rms = float(np.sqrt(np.mean(np.square(ref)))) if ref.size else 0.0
     return float(np.abs(y - ref).max()) / max(rms, 1e-30) if ref.size else 0.0
+
+
+def assert_bf16_rounding_bound(y, ref, fp32_tol=1e-4):
+    """bf16 outputs y vs the fp64 oracle ref (A16): y = RNE_bf16(v) with v the
+    fp32 result, |v - ref| <= fp32_tol * RMS(ref); RNE has relative error
+    <= u = 2^-8 (8 significant bits), so elementwise
+    |y - ref| <= 2^-8 (|ref| + eps) + eps, eps = fp32_tol * RMS(ref)."""
+    y, ref = np.asarray(y, np.float64), np.asarray(ref, np.float64).reshape(np.shape(y))
+    eps = fp32_tol * float(np.sqrt(np.mean(np.square(ref))))
+    bound = 2.0 ** -8 * (np.abs(ref) + eps) + eps
+    bad = np.abs(y - ref) > bound
+    assert not bad.any(), f"{int(bad.sum())} elements exceed the bf16 rounding bound; worst excess " \
+                          f"{float((np.abs(y - ref) - bound).max()):.3e}"

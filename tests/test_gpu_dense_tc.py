@@ -9,7 +9,7 @@ import pytest
 import torch
 
 import oracle as O
-from tests.helpers import make_pair, np_of, rel_err, to_cl
+from tests.helpers import assert_bf16_rounding_bound, make_pair, np_of, rel_err, to_cl
 
 pytestmark = pytest.mark.gpu
 
@@ -74,8 +74,10 @@ def test_dense_tc_exact_integer_bitwise(case):
 
 @pytest.mark.parametrize("case", ["halo_c2like", "flat_c5like"])
 def test_dense_tc_bf16_output(case):
+    # A16: bf16 outputs are checked against the RNE error bound
     _, y, ref, _ = _run(case, out_dtype=torch.bfloat16)
     assert rel_err(y, ref) <= 2e-2
+    assert_bf16_rounding_bound(y, ref)
 
 
 @pytest.mark.parametrize("case", ["halo_c2like", "flat_c5like"])
