@@ -32,6 +32,19 @@
 //    the accumulator.
 //  * State layout S[slot][Cout/4][B*Ho*Wo][4] fp32: thread = output pixel, a
 //    warp moves 512 contiguous bytes per float4 instruction.
+//
+// Three operand modes share the warp roles and the fused epilogue:
+//  * HALO (spatial stride 1, weights fit in shared memory): the above;
+//  * FLAT (1x1 spatial): rows = (stream, pixel) flattened, one 128-row box;
+//  * KLOOP (spatial stride > 1, or weights too large to stay resident): a
+//    classic K pipeline.  Per (tap (u,v), block of kb input channels) one stage
+//    holds the A chunk -- 128 output pixels x kb channels, gathered by ONE TMA
+//    box whose traversal strides (elementStrides) equal the spatial conv
+//    stride, so strided im2col costs nothing -- and the B chunk (kb x N packed
+//    weights, one bulk copy).  Small-Cin stems (Cin < 16, TMA needs 16-byte
+//    rows) are first packed "W-im2col": xp[b,h,wo,(v,c)] = x[b,h,wo*sw+v-pw,c]
+//    padded to a multiple of 16 channels, which turns the layer into a
+//    (kt, kh, 1) convolution over xp with K = kh * roundup(kw*Cin, 16).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -47,23 +60,28 @@ namespace co {
 
 namespace {
 
-constexpr int kMaxStages = 4;   // A-operand pipeline depth: as many as fit in shared memory
+constexpr int kMaxStages = 6;   // operand pipeline depth: as many as fit in shared memory
 __host__ __device__ constexpr int tc_threads(int eg) { return 32 * (4 * eg + 2); }
 constexpr int kApad = 512;        // slack after each A stage (junk rows may read past the box)
+enum { MODE_HALO = 0, MODE_FLAT = 1, MODE_KLOOP = 2 };
 
 struct TcParams {
   int B, H, W, Cin, Cout, Ho, Wo;
   int64_t HWo, plane;             // plane = B * HWo
   int kh, kw, ph, pw;
-  int flat;                       // 1: 1x1 spatial, rows = (stream, pixel) flattened
+  int sh, sw, dh, dw;
+  int mode;
   int MT, Wp, tiles_per_stream;   // halo mode geometry
+  int TH, TW, tiles_h, tiles_w;   // kloop output tile (TH x TW <= 128 pixels)
+  int kb, n_cb;                   // kloop: input channels per K chunk, chunks per tap
+  int b_bytes, b_off;             // kloop: B chunk bytes, B offset inside a stage
   int64_t n_tiles, n_items;
   int n_split;
-  int a_bytes, a_stride;          // A box bytes, A stage stride in smem
-  int stages;                     // A pipeline depth (<= kMaxStages)
+  int a_bytes, a_stride;          // A box bytes, stage stride in smem
+  int stages;                     // pipeline depth (<= kMaxStages)
   int chunk_stride;               // bytes between 8-channel groups inside an A stage
   int w_bytes;                    // packed weights of one part
-  int w_off;                      // A stages start here (1 KB aligned)
+  int w_off;                      // stages start here (1 KB aligned)
   int slot[kMaxKt];
   int emit, update, act, out_f32;
   int Cq;
@@ -83,44 +101,54 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int KT, int CC, int EG>
+// CE: output channels per epilogue pass (bounds the prefetched-state registers
+// at (kt-1) * CE / 4 float4 per thread); KH, KW, KC (= Cin / 16) > 0: compile-
+// time tap / K loops of the HALO / FLAT modes, fully unrolled, so the issuing
+// warp spends ~3 uniform instructions per tcgen05.mma.
+template <int KT, int CC, int EG, int CE, int KH = 0, int KW = 0, int KC = 0>
 __global__ void __launch_bounds__(tc_threads(EG), 1)
     k_step_dense_tc(const __grid_constant__ CUtensorMap tmap, const TcParams p) {
   constexpr int N = KT * CC;
-  constexpr int BUF = (N <= 128) ? 128 : 256;
-  static_assert(EG * BUF <= 512, "accumulator buffers exceed TMEM");
+  // TMEM accumulator ring: as many N-column buffers as 512 columns hold, at
+  // least one per epilogue group, so the MMA can run ahead of the state traffic.
+  constexpr int BUF = (N + 31) / 32 * 32;
+  constexpr int NBUF = (512 / BUF) < 8 ? (512 / BUF) : 8;
+  static_assert(NBUF >= EG, "accumulator buffers exceed TMEM");
   constexpr int TMEM_COLS = 512;
   constexpr int kProducer = 4 * EG, kMma = 4 * EG + 1;
   static_assert(N % 16 == 0 && N <= 256, "invalid UMMA N");
-  static_assert(CC % 16 == 0, "CC must be a multiple of 16");
+  static_assert(CC % CE == 0 && CE % 16 == 0, "CE must divide CC, multiple of 16");
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* w_s = smem;                                  // [K/8][N][16 B]
+  // 1 KB alignment by pointer arithmetic on the __shared__ array (an integer
+  // round trip would turn every derived access into a generic one)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* w_s = smem;                                  // [K/8][N][16 B] (HALO / FLAT)
   uint8_t* a_s = smem + p.w_off;                        // stages x a_stride
   uint64_t* bars = reinterpret_cast<uint64_t*>(a_s + p.stages * p.a_stride);
   uint64_t* full = bars;                                // [kMaxStages]
   uint64_t* empty = bars + kMaxStages;                  // [kMaxStages]
-  uint64_t* acc_full = bars + 2 * kMaxStages;           // [EG]
-  uint64_t* acc_empty = bars + 2 * kMaxStages + EG;     // [EG]
-  uint64_t* w_full = bars + 2 * kMaxStages + 2 * EG;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 2 * EG + 1);
-  float* bias_s = reinterpret_cast<float*>(bars + 2 * kMaxStages + 2 * EG + 2);
+  uint64_t* acc_full = bars + 2 * kMaxStages;           // [NBUF]
+  uint64_t* acc_empty = bars + 2 * kMaxStages + NBUF;   // [NBUF]
+  uint64_t* w_full = bars + 2 * kMaxStages + 2 * NBUF;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 2 * NBUF + 1);
+  float* bias_s = reinterpret_cast<float*>(bars + 2 * kMaxStages + 2 * NBUF + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int grid = gridDim.x;
   const int part = blockIdx.x % p.n_split;
   const int c0 = part * CC;                             // first output channel of this part
+  const bool kloop = (p.mode == MODE_KLOOP);
 
   if (warp == kProducer && lane == 0) {
     for (int s = 0; s < p.stages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
-    for (int e = 0; e < EG; ++e) { ptx::mbar_init(&acc_full[e], 1); ptx::mbar_init(&acc_empty[e], 128); }
+    for (int e = 0; e < NBUF; ++e) { ptx::mbar_init(&acc_full[e], 1); ptx::mbar_init(&acc_empty[e], 128); }
     ptx::mbar_init(w_full, 1);
     ptx::fence_mbar_init();
   }
   if (warp == kMma) ptx::tmem_alloc(tmem_holder, TMEM_COLS);
-  if (threadIdx.x < CC) bias_s[threadIdx.x] = p.bias[c0 + threadIdx.x];
+  for (int i = threadIdx.x; i < CC; i += blockDim.x) bias_s[i] = p.bias[c0 + i];
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -130,27 +158,50 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
     // ===================== TMA producer =====================
     if (lane == 0) {
       ptx::prefetch_tmap(&tmap);
-      ptx::mbar_arrive_expect_tx(w_full, p.w_bytes);
       const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wpack) + size_t(part) * p.w_bytes;
-      for (int off = 0; off < p.w_bytes; off += 32768) {
-        const int n = min(32768, p.w_bytes - off);
-        ptx::bulk_g2s(w_s + off, wsrc + off, n, w_full);
-      }
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t item = blockIdx.x; item < p.n_items; item += grid) {
-        ptx::mbar_wait(&empty[s], ph ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes);
-        const int64_t tile = item / p.n_split;
-        uint8_t* dst = a_s + s * p.a_stride;
-        if (p.flat) {
-          ptx::tma_load_3d(dst, &tmap, &full[s], 0, int(tile * 128), 0);
-        } else {
-          const int b = int(tile / p.tiles_per_stream);
-          const int ho0 = int(tile % p.tiles_per_stream) * p.MT;
-          ptx::tma_load_5d(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
+      if (!kloop) {
+        ptx::mbar_arrive_expect_tx(w_full, p.w_bytes);
+        for (int off = 0; off < p.w_bytes; off += 32768) {
+          const int n = min(32768, p.w_bytes - off);
+          ptx::bulk_g2s(w_s + off, wsrc + off, n, w_full);
         }
-        if (++s == p.stages) { s = 0; ph ^= 1; }
+        for (int64_t item = blockIdx.x; item < p.n_items; item += grid) {
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes);
+          const int64_t tile = item / p.n_split;
+          uint8_t* dst = a_s + s * p.a_stride;
+          if (p.mode == MODE_FLAT) {
+            ptx::tma_load_3d(dst, &tmap, &full[s], 0, int(tile * 128), 0);
+          } else {
+            const int b = int(tile / p.tiles_per_stream);
+            const int ho0 = int(tile % p.tiles_per_stream) * p.MT;
+            ptx::tma_load_5d(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
+          }
+          if (++s == p.stages) { s = 0; ph ^= 1; }
+        }
+      } else {
+        const int per_stream = p.tiles_h * p.tiles_w;
+        for (int64_t item = blockIdx.x; item < p.n_items; item += grid) {
+          const int64_t tile = item / p.n_split;
+          const int b = int(tile / per_stream);
+          const int r = int(tile % per_stream);
+          const int ho0 = (r / p.tiles_w) * p.TH, wo0 = (r % p.tiles_w) * p.TW;
+          const uint8_t* bsrc = wsrc;
+          for (int u = 0; u < p.kh; ++u)
+            for (int v = 0; v < p.kw; ++v)
+              for (int cb = 0; cb < p.n_cb; ++cb) {
+                ptx::mbar_wait(&empty[s], ph ^ 1);
+                ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes + p.b_bytes);
+                uint8_t* dst = a_s + s * p.a_stride;
+                ptx::tma_load_5d(dst, &tmap, &full[s], 0, wo0 * p.sw + v * p.dw - p.pw,
+                                 ho0 * p.sh + u * p.dh - p.ph, cb * (p.kb / 8), b);
+                ptx::bulk_g2s(dst + p.b_off, bsrc, p.b_bytes, &full[s]);
+                bsrc += p.b_bytes;
+                if (++s == p.stages) { s = 0; ph ^= 1; }
+              }
+        }
       }
     }
     return;
@@ -158,19 +209,21 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
 
   if (warp == kMma) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, N);
+    // The whole warp runs the loop (warp-uniform descriptors live in uniform
+    // registers); one elected lane issues each tcgen05.mma / commit.
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, N);
+    const uint32_t a_base = ptx::smem_u32(a_s);
+    // Descriptors are advanced by adding (byte offset >> 4) to their 14-bit
+    // start-address field (shared memory < 256 KB, so it never carries out).
+    const uint32_t chunk16 = uint32_t(p.chunk_stride) >> 3;   // 2 channel groups, in 16 B units
+    int s = 0;
+    uint32_t ph = 0;
+    int e = 0;
+    uint32_t eph = 0;
+    if (!kloop) {
       ptx::mbar_wait(w_full, 0);
-      const uint32_t a_base = ptx::smem_u32(a_s);
-      // Descriptors are advanced by adding (byte offset >> 4) to their 14-bit
-      // start-address field (shared memory < 256 KB, so it never carries out).
       const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_u32(w_s), N * 16, 128);
       const int kc2 = p.Cin / 16;                       // MMAs (K = 16) per spatial tap
-      const uint32_t chunk16 = uint32_t(p.chunk_stride) >> 3;   // 2 channel groups, in 16 B units
-      int s = 0;
-      uint32_t ph = 0;
-      int e = 0;
-      uint32_t eph = 0;
       for (int64_t item = blockIdx.x; item < p.n_items; item += grid) {
         ptx::mbar_wait(&acc_empty[e], eph ^ 1);
         ptx::tc_fence_after();
@@ -178,23 +231,72 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem + uint32_t(e * BUF);
         const uint64_t a_desc0 = ptx::smem_desc(a_base + uint32_t(s * p.a_stride), p.chunk_stride, 128);
-        uint64_t bd = b_desc0;
-        uint32_t acc = 0;
-        for (int u = 0; u < p.kh; ++u) {
-          for (int v = 0; v < p.kw; ++v) {
-            uint64_t ad = a_desc0 + uint64_t(u * p.Wp + v);   // tap (u, v): shift by u Wp + v rows
-            for (int kc = 0; kc < kc2; ++kc) {
-              ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, acc);
-              acc = 1;
-              ad += chunk16;
-              bd += uint64_t(2 * N);                         // 2 groups of N rows x 16 B
+        if constexpr (KH > 0) {
+          if (ptx::elect_one()) {
+#pragma unroll
+            for (int u = 0; u < KH; ++u)
+#pragma unroll
+              for (int v = 0; v < KW; ++v) {
+                const uint64_t ad = a_desc0 + uint64_t(u * p.Wp + v);
+#pragma unroll
+                for (int kc = 0; kc < KC; ++kc)
+                  ptx::mma_bf16_ss(d_tmem, ad + uint64_t(kc) * chunk16,
+                                   b_desc0 + uint64_t(((u * KW + v) * KC + kc) * 2 * N), idesc,
+                                   (u | v | kc) ? 1u : 0u);
+              }
+          }
+          __syncwarp();
+        } else {
+          uint64_t bd = b_desc0;
+          uint32_t acc = 0;
+          for (int u = 0; u < p.kh; ++u) {
+            for (int v = 0; v < p.kw; ++v) {
+              uint64_t ad = a_desc0 + uint64_t(u * p.Wp + v);   // tap (u, v): shift by u Wp + v rows
+              for (int kc = 0; kc < kc2; ++kc) {
+                if (ptx::elect_one()) ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, acc);
+                __syncwarp();
+                acc = 1;
+                ad += chunk16;
+                bd += uint64_t(2 * N);                         // 2 groups of N rows x 16 B
+              }
             }
           }
         }
-        ptx::tc_commit(&empty[s]);      // A stage free once these MMAs retire
-        ptx::tc_commit(&acc_full[e]);   // accumulator e ready for the epilogue
+        if (ptx::elect_one()) {
+          ptx::tc_commit(&empty[s]);      // A stage free once these MMAs retire
+          ptx::tc_commit(&acc_full[e]);   // accumulator e ready for the epilogue
+        }
+        __syncwarp();
         if (++s == p.stages) { s = 0; ph ^= 1; }
-        if (++e == EG) { e = 0; eph ^= 1; }
+        if (++e == NBUF) { e = 0; eph ^= 1; }
+      }
+    } else {
+      const int n_chunks = p.kh * p.kw * p.n_cb;
+      const int nk = p.kb / 16;                         // MMAs per chunk (<= 4)
+      for (int64_t item = blockIdx.x; item < p.n_items; item += grid) {
+        ptx::mbar_wait(&acc_empty[e], eph ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem + uint32_t(e * BUF);
+        for (int ch = 0; ch < n_chunks; ++ch) {
+          ptx::mbar_wait(&full[s], ph);
+          ptx::tc_fence_after();
+          const uint32_t st = a_base + uint32_t(s * p.a_stride);
+          const uint64_t ad = ptx::smem_desc(st, p.chunk_stride, 128);
+          const uint64_t bd = ptx::smem_desc(st + uint32_t(p.b_off), N * 16, 128);
+          if (ptx::elect_one()) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (j < nk)
+                ptx::mma_bf16_ss(d_tmem, ad + uint64_t(j) * chunk16, bd + uint64_t(j * 2 * N), idesc,
+                                 (ch | j) ? 1u : 0u);
+            ptx::tc_commit(&empty[s]);    // stage free once these MMAs retire
+          }
+          __syncwarp();
+          if (++s == p.stages) { s = 0; ph ^= 1; }
+        }
+        if (ptx::elect_one()) ptx::tc_commit(&acc_full[e]);
+        __syncwarp();
+        if (++e == NBUF) { e = 0; eph ^= 1; }
       }
     }
     __syncwarp();
@@ -205,123 +307,137 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
   }
 
   // ===================== epilogue warpgroups (warps 0 .. 4 EG - 1) =====================
-  const int e = warp >> 2;                             // group = accumulator buffer
+  const int e = warp >> 2;                             // group
   const int q = warp & 3;                              // TMEM lane quadrant of this warp
   const int m = q * 32 + lane;                         // accumulator row = tile pixel
   const int64_t plane = p.plane;
-  constexpr int NQ = CC / 4;                           // channel quads per thread
+  constexpr int NQ = CE / 4;                           // channel quads per thread and pass
   constexpr int NS = (KT > 1) ? KT - 1 : 1;
   int li = e;
   for (int64_t item = blockIdx.x + int64_t(e) * grid; item < p.n_items; item += EG * int64_t(grid), li += EG) {
-    const int j = li / EG;
+    const int buf = li % NBUF;                         // accumulator buffer of this item
+    const uint32_t bph = uint32_t(li / NBUF) & 1u;
     const int64_t tile = item / p.n_split;
     // ---- this row's output pixel
     bool valid;
     int64_t pix, b;
-    if (p.flat) {
+    if (p.mode == MODE_FLAT) {
       pix = tile * 128 + m;
       valid = pix < plane;
       b = valid ? pix / p.HWo : 0;
-    } else {
+    } else if (p.mode == MODE_HALO) {
       b = tile / p.tiles_per_stream;
       const int ho = int(tile % p.tiles_per_stream) * p.MT + m / p.Wp;
       const int wo = m % p.Wp;
       valid = (m < p.MT * p.Wp) && (wo < p.Wo) && (ho < p.Ho);
       pix = b * p.HWo + int64_t(ho) * p.Wo + wo;
+    } else {
+      const int per_stream = p.tiles_h * p.tiles_w;
+      b = tile / per_stream;
+      const int r = int(tile % per_stream);
+      const int ho = (r / p.tiles_w) * p.TH + m / p.TW;
+      const int wo = (r % p.tiles_w) * p.TW + m % p.TW;
+      valid = (m < p.TH * p.TW) && (wo < p.Wo) && (ho < p.Ho);
+      pix = b * p.HWo + int64_t(ho) * p.Wo + wo;
     }
-    // ---- prefetch the state this pixel needs (before the accumulator is ready)
-    float4 sv[NS][NQ];
-    if (KT > 1 && valid) {
-      if (p.emit) {
-        const float4* src = reinterpret_cast<const float4*>(p.state) +
-                            (int64_t(p.slot[KT - 1]) * p.Cq + c0 / 4) * plane + pix;
-#pragma unroll
-        for (int i = 0; i < NQ; ++i) sv[0][i] = __ldcs(src + int64_t(i) * plane);
-      }
-      if (p.update) {
-#pragma unroll
-        for (int k = 1; k < KT - 1; ++k) {
-          if (p.slot[k] < 0) continue;
+    const uint32_t t_row = tmem + (uint32_t(q * 32) << 16) + uint32_t(buf * BUF);
+#pragma unroll 1
+    for (int cb = 0; cb < CC; cb += CE) {
+      // ---- prefetch the state this pass needs (pass 0: before the accumulator is ready)
+      float4 sv[NS][NQ];
+      if (KT > 1 && valid) {
+        if (p.emit) {
           const float4* src = reinterpret_cast<const float4*>(p.state) +
-                              (int64_t(p.slot[k]) * p.Cq + c0 / 4) * plane + pix;
+                              (int64_t(p.slot[KT - 1]) * p.Cq + (c0 + cb) / 4) * plane + pix;
 #pragma unroll
-          for (int i = 0; i < NQ; ++i) sv[k][i] = __ldcs(src + int64_t(i) * plane);
+          for (int i = 0; i < NQ; ++i) sv[0][i] = __ldcs(src + int64_t(i) * plane);
         }
-      }
-    }
-    ptx::mbar_wait(&acc_full[e], j & 1);
-    ptx::tc_fence_after();
-    const uint32_t t_row = tmem + (uint32_t(q * 32) << 16) + uint32_t(e * BUF);
-    float v[16];
-    // ---- (1) complete + emit
-    if (p.emit) {
+        if (p.update) {
 #pragma unroll
-      for (int c = 0; c < CC; c += 16) {
-        ptx::tmem_ld16(t_row + uint32_t((KT - 1) * CC + c), v);
-        ptx::tc_wait_ld();
-        if (valid) {
+          for (int k = 1; k < KT - 1; ++k) {
+            if (p.slot[k] < 0) continue;
+            const float4* src = reinterpret_cast<const float4*>(p.state) +
+                                (int64_t(p.slot[k]) * p.Cq + (c0 + cb) / 4) * plane + pix;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float s = 0.f;
-            if (KT > 1) {
-              const float4 t4 = sv[0][(c + i) >> 2];
-              s = ((i & 3) == 0) ? t4.x : ((i & 3) == 1) ? t4.y : ((i & 3) == 2) ? t4.z : t4.w;
-            }
-            float r = v[i] + s + bias_s[c + i];
-            v[i] = (p.act == 1 && r < 0.f) ? 0.f : r;
-          }
-          const int64_t yoff = b * p.y_bstride + (pix - b * p.HWo) * p.Cout + c0 + c;
-          if (p.out_f32) {
-            float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + yoff);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) yp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-          } else {
-            uint4* yp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + yoff);
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-              yp[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
-                                 pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+            for (int i = 0; i < NQ; ++i) sv[k][i] = __ldcs(src + int64_t(i) * plane);
           }
         }
       }
-    }
-    if (p.update && KT > 1) {
-      // ---- (2) accumulate into pending outputs
+      if (cb == 0) {
+        ptx::mbar_wait(&acc_full[buf], bph);
+        ptx::tc_fence_after();
+      }
+      float v[16];
+      // ---- (1) complete + emit
+      if (p.emit) {
 #pragma unroll
-      for (int k = KT - 2; k >= 1; --k) {
-        if (p.slot[k] < 0) continue;
-        float4* dst = reinterpret_cast<float4*>(p.state) + (int64_t(p.slot[k]) * p.Cq + c0 / 4) * plane + pix;
-#pragma unroll
-        for (int c = 0; c < CC; c += 16) {
-          ptx::tmem_ld16(t_row + uint32_t(k * CC + c), v);
+        for (int c = 0; c < CE; c += 16) {
+          ptx::tmem_ld16(t_row + uint32_t((KT - 1) * CC + cb + c), v);
           ptx::tc_wait_ld();
           if (valid) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              float4 t4 = sv[k][c / 4 + i];
-              t4.x += v[4 * i]; t4.y += v[4 * i + 1]; t4.z += v[4 * i + 2]; t4.w += v[4 * i + 3];
-              __stcs(dst + int64_t(c / 4 + i) * plane, t4);
+            for (int i = 0; i < 16; ++i) {
+              float sacc = 0.f;
+              if (KT > 1) {
+                const float4 t4 = sv[0][(c + i) >> 2];
+                sacc = ((i & 3) == 0) ? t4.x : ((i & 3) == 1) ? t4.y : ((i & 3) == 2) ? t4.z : t4.w;
+              }
+              float r = v[i] + sacc + bias_s[cb + c + i];
+              v[i] = (p.act == 1 && r < 0.f) ? 0.f : r;
+            }
+            const int64_t yoff = b * p.y_bstride + (pix - b * p.HWo) * p.Cout + c0 + cb + c;
+            if (p.out_f32) {
+              float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + yoff);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) yp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            } else {
+              uint4* yp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + yoff);
+#pragma unroll
+              for (int i = 0; i < 2; ++i)
+                yp[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                                   pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
             }
           }
         }
       }
-      // ---- (3) start the newest output (overwrites the emitted slot)
-      if (p.slot[0] >= 0) {
-        float4* dst = reinterpret_cast<float4*>(p.state) + (int64_t(p.slot[0]) * p.Cq + c0 / 4) * plane + pix;
+      if (p.update && KT > 1) {
+        // ---- (2) accumulate into pending outputs
 #pragma unroll
-        for (int c = 0; c < CC; c += 16) {
-          ptx::tmem_ld16(t_row + uint32_t(c), v);
-          ptx::tc_wait_ld();
-          if (valid) {
+        for (int k = KT - 2; k >= 1; --k) {
+          if (p.slot[k] < 0) continue;
+          float4* dst = reinterpret_cast<float4*>(p.state) + (int64_t(p.slot[k]) * p.Cq + (c0 + cb) / 4) * plane + pix;
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              __stcs(dst + int64_t(c / 4 + i) * plane, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+          for (int c = 0; c < CE; c += 16) {
+            ptx::tmem_ld16(t_row + uint32_t(k * CC + cb + c), v);
+            ptx::tc_wait_ld();
+            if (valid) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                float4 t4 = sv[k][c / 4 + i];
+                t4.x += v[4 * i]; t4.y += v[4 * i + 1]; t4.z += v[4 * i + 2]; t4.w += v[4 * i + 3];
+                __stcs(dst + int64_t(c / 4 + i) * plane, t4);
+              }
+            }
+          }
+        }
+        // ---- (3) start the newest output (overwrites the emitted slot)
+        if (p.slot[0] >= 0) {
+          float4* dst = reinterpret_cast<float4*>(p.state) + (int64_t(p.slot[0]) * p.Cq + (c0 + cb) / 4) * plane + pix;
+#pragma unroll
+          for (int c = 0; c < CE; c += 16) {
+            ptx::tmem_ld16(t_row + uint32_t(cb + c), v);
+            ptx::tc_wait_ld();
+            if (valid) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                __stcs(dst + int64_t(c / 4 + i) * plane, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+            }
           }
         }
       }
     }
     ptx::tc_fence_before();
-    ptx::mbar_arrive(&acc_empty[e]);
+    ptx::mbar_arrive(&acc_empty[buf]);
   }
   bar_sync_named(1, 32 + 128 * EG);
 }
@@ -331,7 +447,7 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
 __global__ void k_pack_tc_weights(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ out, int Cout,
                                   int Cin, int kt, int kh, int kw, int CC, int n_split) {
   // (Cout, Cin, kt, kh, kw) -> [part][K/8][N][8], N = kt*CC rows (n = k*CC + c),
-  // K index = (u*kw + v)*Cin + ci.
+  // K index = (u*kw + v)*Cin + ci.  Each K chunk of a tap is one contiguous block.
   const int64_t total = int64_t(Cout) * Cin * kt * kh * kw;
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= total) return;
@@ -349,18 +465,73 @@ __global__ void k_pack_tc_weights(const __nv_bfloat16* __restrict__ w, __nv_bflo
   out[int64_t(part) * K * N + ((kidx / 8) * N + n) * 8 + (kidx % 8)] = w[i];
 }
 
+// W-im2col of the weights for a small-Cin stem: (Cout, Cin, kt, kh, kw) ->
+// (Cout, Kp, kt, kh, 1) with channel j = v*Cin + c (zero for j >= kw*Cin).
+__global__ void k_wcols_weights(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ out, int Cout,
+                                int Cin, int kt, int kh, int kw, int Kp) {
+  const int64_t total = int64_t(Cout) * Kp * kt * kh;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  int64_t r = i;
+  const int u = int(r % kh); r /= kh;
+  const int k = int(r % kt); r /= kt;
+  const int j = int(r % Kp); r /= Kp;
+  const int o = int(r);
+  __nv_bfloat16 val = __float2bfloat16_rn(0.f);
+  if (j < kw * Cin) {
+    const int v = j / Cin, c = j % Cin;
+    val = w[(((int64_t(o) * Cin + c) * kt + k) * kh + u) * kw + v];
+  }
+  out[i] = val;
+}
+
+// W-im2col of one step's frame: xp[b][h][wo][j] = x[b][h][wo*sw + v*dw - pw][c],
+// j = v*Cin + c, zero outside the frame and for j >= kw*Cin.  One thread
+// writes 8 channels (16 B).
+__global__ void k_wcols_frame(const __nv_bfloat16* __restrict__ x, int64_t x_bstride, __nv_bfloat16* __restrict__ xp,
+                              int64_t B, int H, int W, int Cin, int Wo, int kw, int sw, int dw, int pw, int Kp) {
+  const int K8 = Kp / 8;
+  const int64_t total = B * H * Wo * K8;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int j8 = int(i % K8);
+  int64_t r = i / K8;
+  const int wo = int(r % Wo); r /= Wo;
+  const int h = int(r % H);
+  const int64_t b = r / H;
+  __align__(16) __nv_bfloat16 vals[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int j = j8 * 8 + t;
+    float val = 0.f;
+    if (x && j < kw * Cin) {
+      const int v = j / Cin, c = j % Cin;
+      const int wi = wo * sw + v * dw - pw;
+      if (wi >= 0 && wi < W) val = __bfloat162float(x[b * x_bstride + (int64_t(h) * W + wi) * Cin + c]);
+    }
+    vals[t] = __float2bfloat16_rn(val);
+  }
+  *reinterpret_cast<uint4*>(xp + i * 8) = *reinterpret_cast<const uint4*>(vals);
+}
+
 typedef void (*KernFn)(const CUtensorMap, const TcParams);
 
 struct Variant {
-  int KT, CC, EG;
+  int KT, CC, EG, CE;
   KernFn fn;
+  int KH = 0, KW = 0, KC = 0;     // > 0: specialised (unrolled) HALO/FLAT variant for this kernel / Cin
 };
 
-#define CO_TC_VARIANT(kt, cc, eg) {kt, cc, eg, (KernFn)k_step_dense_tc<kt, cc, eg>}
+#define CO_TC_VARIANT(kt, cc, eg, ce) {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce>}
+#define CO_TC_SPEC(kt, cc, eg, ce, kh, kw, kc) \
+  {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, kh, kw, kc>, kh, kw, kc}
 const Variant kVariants[] = {
-    CO_TC_VARIANT(1, 32, 4), CO_TC_VARIANT(1, 64, 4), CO_TC_VARIANT(2, 32, 4), CO_TC_VARIANT(3, 16, 4),
-    CO_TC_VARIANT(3, 32, 2), CO_TC_VARIANT(3, 32, 3), CO_TC_VARIANT(3, 32, 4), CO_TC_VARIANT(5, 16, 4),
-    CO_TC_VARIANT(5, 32, 2), CO_TC_VARIANT(9, 16, 2),
+    CO_TC_SPEC(3, 32, 2, 32, 3, 3, 4), CO_TC_SPEC(3, 32, 3, 32, 3, 3, 4), CO_TC_SPEC(9, 16, 2, 16, 1, 1, 16),
+    CO_TC_VARIANT(1, 32, 4, 32), CO_TC_VARIANT(1, 64, 4, 32), CO_TC_VARIANT(1, 128, 2, 32),
+    CO_TC_VARIANT(2, 32, 4, 32), CO_TC_VARIANT(2, 64, 2, 32), CO_TC_VARIANT(3, 16, 4, 16),
+    CO_TC_VARIANT(3, 32, 2, 32), CO_TC_VARIANT(3, 32, 3, 32), CO_TC_VARIANT(3, 32, 4, 32),
+    CO_TC_VARIANT(3, 64, 2, 32), CO_TC_VARIANT(5, 16, 4, 16), CO_TC_VARIANT(5, 32, 2, 16),
+    CO_TC_VARIANT(9, 16, 2, 16),
 };
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -378,66 +549,137 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 struct Plan {
   bool ok = false;
   const Variant* var = nullptr;
-  int n_split = 0, flat = 0, MT = 0, Wp = 0, tiles_per_stream = 0;
-  int a_bytes = 0, a_stride = 0, chunk_stride = 0, w_bytes = 0, stages = 2;
+  Geom gk;                        // geometry the kernel sees (the W-im2col'd one for a stem)
+  int wcols = 0, Kp = 0;          // small-Cin stem packed W-im2col
+  int mode = MODE_HALO;
+  int n_split = 0, MT = 0, Wp = 0, tiles_per_stream = 0;
+  int TH = 0, TW = 0, tiles_h = 0, tiles_w = 0, kb = 0, n_cb = 0, b_bytes = 0, b_off = 0;
+  int a_bytes = 0, a_stride = 0, chunk_stride = 0, w_bytes = 0, w_off = 0, stages = 2;
   int64_t n_tiles = 0;
   size_t smem = 0;
 };
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
-Plan make_plan(const Geom& g) {
-  Plan pl;
-  if (g.in_dtype != BF16 || g.groups != 1 || g.Cin % 16 != 0 || g.Cin / 8 > 256) return pl;
-  if (g.sh != 1 || g.sw != 1 || g.dh != 1 || g.dw != 1) return pl;
-  if (g.Cout % 4 != 0) return pl;
+int pinned_eg() {
+  const char* eg_env = getenv("CO_TC_EG");      // A/B runs only
+  return eg_env ? atoi(eg_env) : 0;
+}
+
+// HALO / FLAT: weights resident.  Largest CC whose weights + 2 A stages fit.
+bool plan_resident(const Geom& g, Plan& pl) {
+  if (g.sh != 1 || g.sw != 1 || g.dh != 1 || g.dw != 1 || g.Cin % 16 != 0 || g.Cin / 8 > 256) return false;
   const bool flat = (g.kh == 1 && g.kw == 1 && g.ph == 0 && g.pw == 0);
-  int Wp = 1, MT = 1, halo_rows = 1, a_rows = 128;
+  int Wp = 1, MT = 1, a_rows = 128;
   if (!flat) {
     Wp = g.Wo + g.kw - 1;
-    if (Wp > 128 || Wp > 256) return pl;
+    if (Wp > 128) return false;
     MT = std::min(128 / Wp, g.Ho);
-    halo_rows = MT + g.kh - 1;
-    if (halo_rows > 256) return pl;
+    const int halo_rows = MT + g.kh - 1;
+    if (halo_rows > 256) return false;
     a_rows = Wp * halo_rows;
   }
   const int a_bytes = (g.Cin / 8) * a_rows * 16;
   const int a_stride = ((a_bytes + kApad + 1023) / 1024) * 1024;
   const int64_t K = int64_t(g.Cin) * g.kh * g.kw;
-  // largest CC (fewest parts) whose weights + A stages fit in shared memory;
-  // among equal CC the most epilogue groups (CO_TC_EG=<n> pins it, for A/B runs)
-  const char* eg_env = getenv("CO_TC_EG");
-  const int eg_pin = eg_env ? atoi(eg_env) : 0;
+  const int eg_pin = pinned_eg();
+  const Variant* best = nullptr;
   for (const Variant& v : kVariants) {
     if (v.KT != g.kt || g.Cout % v.CC != 0) continue;
+    if (v.KH && (v.KH != g.kh || v.KW != g.kw || v.KC * 16 != g.Cin)) continue;
     if (eg_pin && v.EG != eg_pin) continue;
-    const int N = v.KT * v.CC;
-    const int64_t w_bytes = int64_t(N) * K * 2;
-    const size_t fixed = 1024 + size_t((w_bytes + 1023) / 1024 * 1024) + 256 + v.CC * 4;
+    const int64_t w_bytes = int64_t(v.KT * v.CC) * K * 2;
+    const size_t fixed = 1024 + size_t((w_bytes + 1023) / 1024 * 1024) + 512 + v.CC * 4;
     if (fixed + 2 * size_t(a_stride) > kSmemLimit) continue;
-    const int stages = int(std::min<size_t>(kMaxStages, (kSmemLimit - fixed) / size_t(a_stride)));
-    if (!pl.ok || v.CC > pl.var->CC || (v.CC == pl.var->CC && v.EG > pl.var->EG)) {
-      pl.ok = true;
-      pl.var = &v;
+    // prefer: more channels per part, then a specialised (unrolled) variant, then more groups
+    auto rank = [](const Variant* x) { return x->CC * 1000 + (x->KH ? 100 : 0) + x->EG; };
+    if (!best || rank(&v) > rank(best)) {
+      best = &v;
       pl.w_bytes = int(w_bytes);
-      pl.stages = stages;
-      pl.smem = fixed + size_t(stages) * a_stride;
+      pl.stages = int(std::min<size_t>(kMaxStages, (kSmemLimit - fixed) / size_t(a_stride)));
+      pl.smem = fixed + size_t(pl.stages) * a_stride;
     }
   }
-  if (!pl.ok) return pl;
-  pl.n_split = g.Cout / pl.var->CC;
-  pl.flat = flat;
+  if (!best) return false;
+  pl.var = best;
+  pl.mode = flat ? MODE_FLAT : MODE_HALO;
   pl.MT = MT;
   pl.Wp = Wp;
   pl.a_bytes = a_bytes;
   pl.a_stride = a_stride;
   pl.chunk_stride = a_rows * 16;
+  pl.w_off = (pl.w_bytes + 1023) / 1024 * 1024;
   if (flat) {
     pl.n_tiles = (g.B * g.HWo + 127) / 128;
   } else {
     pl.tiles_per_stream = (g.Ho + MT - 1) / MT;
     pl.n_tiles = g.B * pl.tiles_per_stream;
   }
+  return true;
+}
+
+// KLOOP: K streamed through a stage ring; any spatial stride/dilation <= 8.
+bool plan_kloop(const Geom& g, Plan& pl) {
+  if (g.Cin % 16 != 0 || g.Cin / 8 > 256 || g.sh > 8 || g.sw > 8) return false;
+  const int TW = std::min(g.Wo, 128);
+  const int TH = std::max(1, std::min(128 / TW, g.Ho));
+  if (TW * g.sw > 256 || TH * g.sh > 256) return false;
+  const int kb = (g.Cin % 64 == 0) ? 64 : (g.Cin % 32 == 0) ? 32 : 16;
+  const int rows = TH * TW;
+  const int a_bytes = (kb / 8) * rows * 16;
+  const int eg_pin = pinned_eg();
+  const Variant* best = nullptr;
+  for (const Variant& v : kVariants) {
+    if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH) continue;
+    if (eg_pin && v.EG != eg_pin) continue;
+    // prefer the widest N (fewest A re-reads), then more groups
+    auto rank = [](const Variant* x) { return x->CC * 1000 + x->EG; };
+    if (!best || rank(&v) > rank(best)) best = &v;
+  }
+  if (!best) return false;
+  const int N = best->KT * best->CC;
+  const int b_bytes = (kb / 8) * N * 16;
+  // A chunk, slack for the junk rows the 128-row MMA reads past it, then B
+  const int b_off = (a_bytes + (128 - rows) * 16 + 127) / 128 * 128;
+  const int stage = (b_off + b_bytes + 1023) / 1024 * 1024;
+  const size_t fixed = 1024 + 512 + best->CC * 4;
+  const int stages = int(std::min<size_t>(kMaxStages, (kSmemLimit - fixed) / size_t(stage)));
+  if (stages < 2) return false;
+  pl.var = best;
+  pl.mode = MODE_KLOOP;
+  pl.TH = TH; pl.TW = TW;
+  pl.tiles_h = (g.Ho + TH - 1) / TH;
+  pl.tiles_w = (g.Wo + TW - 1) / TW;
+  pl.kb = kb; pl.n_cb = g.Cin / kb;
+  pl.a_bytes = a_bytes; pl.b_bytes = b_bytes; pl.b_off = b_off;
+  pl.a_stride = stage;
+  pl.stages = stages;
+  pl.chunk_stride = rows * 16;
+  pl.w_bytes = int(int64_t(N) * g.Cin * g.kh * g.kw * 2);
+  pl.w_off = 0;
+  pl.smem = fixed + size_t(stages) * stage;
+  pl.n_tiles = g.B * pl.tiles_h * pl.tiles_w;
+  return true;
+}
+
+Plan make_plan(const Geom& g) {
+  Plan pl;
+  if (g.in_dtype != BF16 || g.groups != 1 || g.Cout % 4 != 0) return pl;
+  pl.gk = g;
+  if (g.Cin < 16 && g.Cin * g.kw <= 64) {
+    // small-Cin stem: W-im2col'd frame, kernel (kt, kh, 1), stride (st, sh, 1)
+    pl.wcols = 1;
+    pl.Kp = (g.Cin * g.kw + 15) / 16 * 16;
+    Geom& k = pl.gk;
+    k.Cin = pl.Kp; k.cig = pl.Kp;
+    k.W = g.Wo; k.kw = 1; k.sw = 1; k.pw = 0; k.dw = 1;
+  } else if (g.Cin % 16 != 0) {
+    return pl;
+  }
+  const char* mode = getenv("CO_TC_MODE");      // A/B runs only: "kloop" forces the K pipeline
+  const bool force_kloop = mode && std::string(mode) == "kloop";
+  pl.ok = (!force_kloop && plan_resident(pl.gk, pl)) || plan_kloop(pl.gk, pl);
+  if (pl.ok) pl.n_split = g.Cout / pl.var->CC;
   return pl;
 }
 
@@ -446,7 +688,7 @@ Plan make_plan(const Geom& g) {
 struct DenseTC {
   Plan pl;
   __nv_bfloat16* wpack = nullptr;
-  float* xstage = nullptr;   // contiguous staging for strided clips in flat mode
+  __nv_bfloat16* xstage = nullptr;   // dense staging (strided clips in flat mode, zero frames, W-im2col)
   size_t xstage_bytes = 0;
   int num_sms = 148;
   std::string name;
@@ -460,21 +702,38 @@ DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
   if (!get_encode()) { err = "cuTensorMapEncodeTiled unavailable"; return nullptr; }
   DenseTC* t = new DenseTC();
   t->pl = pl;
-  const int64_t total = int64_t(g.Cout) * g.Cin * g.kt * g.kh * g.kw;
+  const Geom& k = pl.gk;
+  const int64_t total = int64_t(k.Cout) * k.Cin * k.kt * k.kh * k.kw;
   cudaError_t e = cudaMalloc(&t->wpack, size_t(total) * 2);
   if (e != cudaSuccess) { err = cudaGetErrorString(e); delete t; return nullptr; }
-  k_pack_tc_weights<<<unsigned((total + 255) / 256), 256>>>(static_cast<const __nv_bfloat16*>(w_dev), t->wpack,
-                                                           g.Cout, g.Cin, g.kt, g.kh, g.kw, pl.var->CC, pl.n_split);
-  if ((e = cudaGetLastError()) != cudaSuccess) { err = cudaGetErrorString(e); dense_tc_destroy(t); return nullptr; }
-  e = cudaFuncSetAttribute(pl.var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
+  const __nv_bfloat16* wsrc = static_cast<const __nv_bfloat16*>(w_dev);
+  __nv_bfloat16* wtmp = nullptr;
+  if (pl.wcols) {
+    if ((e = cudaMalloc(&wtmp, size_t(total) * 2)) != cudaSuccess) { err = cudaGetErrorString(e); dense_tc_destroy(t); return nullptr; }
+    k_wcols_weights<<<unsigned((total + 255) / 256), 256>>>(wsrc, wtmp, g.Cout, g.Cin, g.kt, g.kh, g.kw, pl.Kp);
+    wsrc = wtmp;
+  }
+  k_pack_tc_weights<<<unsigned((total + 255) / 256), 256>>>(wsrc, t->wpack, k.Cout, k.Cin, k.kt, k.kh, k.kw,
+                                                           pl.var->CC, pl.n_split);
+  e = cudaGetLastError();
+  if (wtmp) { cudaDeviceSynchronize(); cudaFree(wtmp); }
+  if (e != cudaSuccess) { err = cudaGetErrorString(e); dense_tc_destroy(t); return nullptr; }
+  // one kernel variant may serve several layers with different footprints: allow the maximum
+  e = cudaFuncSetAttribute(pl.var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemLimit));
   if (e != cudaSuccess) { err = cudaGetErrorString(e); dense_tc_destroy(t); return nullptr; }
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, dev);
-  char buf[96];
-  snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d>", pl.var->KT, pl.var->CC, pl.var->EG);
-  if (getenv("CO_LOG")) fprintf(stderr, "[co] %s: %d parts, %lld tiles, A stages %d x %d B, smem %zu B\n", buf,
-                                pl.n_split, (long long)pl.n_tiles, pl.stages, pl.a_stride, pl.smem);
+  char buf[128];
+  const char* mname = pl.mode == MODE_KLOOP ? (pl.wcols ? ",kloop+wcols" : ",kloop") : "";
+  if (pl.var->KH)
+    snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d,%dx%dx%d%s>", pl.var->KT, pl.var->CC, pl.var->EG,
+             pl.var->KH, pl.var->KW, pl.var->KC * 16, mname);
+  else
+    snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d%s>", pl.var->KT, pl.var->CC, pl.var->EG, mname);
+  if (getenv("CO_LOG"))
+    fprintf(stderr, "[co] %s: %d parts, %lld tiles, %d stages x %d B, smem %zu B\n", buf, pl.n_split,
+            (long long)pl.n_tiles, pl.stages, pl.a_stride, pl.smem);
   t->name = buf;
   return t;
 }
@@ -488,23 +747,39 @@ void dense_tc_destroy(DenseTC* t) {
 
 const char* dense_tc_name(const DenseTC* t) { return t->name.c_str(); }
 
+static cudaError_t ensure_stage(DenseTC* t, size_t need) {
+  if (t->xstage_bytes >= need) return cudaSuccess;
+  cudaFree(t->xstage);
+  t->xstage = nullptr;
+  t->xstage_bytes = 0;
+  cudaError_t e = cudaMalloc(&t->xstage, need);
+  if (e == cudaSuccess) t->xstage_bytes = need;
+  return e;
+}
+
 cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const float* bias, cudaStream_t s) {
   const Plan& pl = t->pl;
+  const Geom& k = pl.gk;
   const void* x = a.x;
   int64_t x_bstride = a.x_bstride;
   const int64_t frame = int64_t(g.H) * g.W * g.Cin;
-  if (!x || (pl.flat && x_bstride != frame)) {
+  if (pl.wcols) {
+    // small-Cin stem: W-im2col the frame (a zero frame stays zero)
+    const int64_t kframe = int64_t(k.H) * k.W * k.Cin;
+    if (cudaError_t e = ensure_stage(t, size_t(g.B) * kframe * 2)) return e;
+    const int64_t n = g.B * k.H * k.W * (k.Cin / 8);
+    k_wcols_frame<<<unsigned((n + 255) / 256), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), x_bstride,
+                                                            t->xstage, g.B, g.H, g.W, g.Cin, g.Wo, g.kw, g.sw, g.dw,
+                                                            g.pw, pl.Kp);
+    if (cudaError_t e = cudaGetLastError()) return e;
+    x = t->xstage;
+    x_bstride = kframe;
+  } else if (!x || (pl.mode == MODE_FLAT && x_bstride != frame)) {
     // zero frame (pad_end) or a strided clip column in flat mode: stage it densely
-    const size_t need = size_t(g.B) * frame * 2;
-    if (t->xstage_bytes < need) {
-      cudaFree(t->xstage);
-      cudaError_t e = cudaMalloc(&t->xstage, need);
-      if (e != cudaSuccess) return e;
-      t->xstage_bytes = need;
-    }
+    if (cudaError_t e = ensure_stage(t, size_t(g.B) * frame * 2)) return e;
     cudaError_t e = x ? cudaMemcpy2DAsync(t->xstage, frame * 2, x, x_bstride * 2, frame * 2, g.B,
                                           cudaMemcpyDeviceToDevice, s)
-                      : cudaMemsetAsync(t->xstage, 0, need, s);
+                      : cudaMemsetAsync(t->xstage, 0, size_t(g.B) * frame * 2, s);
     if (e != cudaSuccess) return e;
     x = t->xstage;
     x_bstride = frame;
@@ -512,19 +787,27 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   CUtensorMap map;
   CUresult r;
   auto encode = get_encode();
-  if (pl.flat) {
-    cuuint64_t dims[3] = {8, cuuint64_t(g.B * g.HWo), cuuint64_t(g.Cin / 8)};
-    cuuint64_t strides[2] = {cuuint64_t(g.Cin) * 2, 16};
-    cuuint32_t box[3] = {8, 128, cuuint32_t(g.Cin / 8)};
+  if (pl.mode == MODE_FLAT) {
+    cuuint64_t dims[3] = {8, cuuint64_t(k.B * k.HWo), cuuint64_t(k.Cin / 8)};
+    cuuint64_t strides[2] = {cuuint64_t(k.Cin) * 2, 16};
+    cuuint32_t box[3] = {8, 128, cuuint32_t(k.Cin / 8)};
     cuuint32_t es[3] = {1, 1, 1};
     r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(x), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
-    cuuint64_t dims[5] = {8, cuuint64_t(g.W), cuuint64_t(g.H), cuuint64_t(g.Cin / 8), cuuint64_t(g.B)};
-    cuuint64_t strides[4] = {cuuint64_t(g.Cin) * 2, cuuint64_t(g.W) * g.Cin * 2, 16, cuuint64_t(x_bstride) * 2};
-    cuuint32_t box[5] = {8, cuuint32_t(pl.Wp), cuuint32_t(pl.MT + g.kh - 1), cuuint32_t(g.Cin / 8), 1};
-    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    cuuint64_t dims[5] = {8, cuuint64_t(k.W), cuuint64_t(k.H), cuuint64_t(k.Cin / 8), cuuint64_t(k.B)};
+    cuuint64_t strides[4] = {cuuint64_t(k.Cin) * 2, cuuint64_t(k.W) * k.Cin * 2, 16, cuuint64_t(x_bstride) * 2};
+    cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+    if (pl.mode == MODE_HALO) {
+      box[0] = 8; box[1] = cuuint32_t(pl.Wp); box[2] = cuuint32_t(pl.MT + k.kh - 1); box[3] = cuuint32_t(k.Cin / 8);
+      box[4] = 1;
+    } else {
+      // strided gather: TMA loads ceil(box / elementStride) elements per dimension
+      box[0] = 8; box[1] = cuuint32_t(pl.TW * k.sw); box[2] = cuuint32_t(pl.TH * k.sh); box[3] = cuuint32_t(pl.kb / 8);
+      box[4] = 1;
+      es[1] = cuuint32_t(k.sw); es[2] = cuuint32_t(k.sh);
+    }
     r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(x), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -532,14 +815,18 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
 
   TcParams p{};
-  p.B = int(g.B); p.H = g.H; p.W = g.W; p.Cin = g.Cin; p.Cout = g.Cout; p.Ho = g.Ho; p.Wo = g.Wo;
+  p.B = int(g.B); p.H = k.H; p.W = k.W; p.Cin = k.Cin; p.Cout = g.Cout; p.Ho = g.Ho; p.Wo = g.Wo;
   p.HWo = g.HWo; p.plane = g.B * g.HWo;
-  p.kh = g.kh; p.kw = g.kw; p.ph = g.ph; p.pw = g.pw;
-  p.flat = pl.flat; p.MT = pl.MT; p.Wp = pl.Wp; p.tiles_per_stream = pl.tiles_per_stream;
+  p.kh = k.kh; p.kw = k.kw; p.ph = k.ph; p.pw = k.pw;
+  p.sh = k.sh; p.sw = k.sw; p.dh = k.dh; p.dw = k.dw;
+  p.mode = pl.mode;
+  p.MT = pl.MT; p.Wp = pl.Wp; p.tiles_per_stream = pl.tiles_per_stream;
+  p.TH = pl.TH; p.TW = pl.TW; p.tiles_h = pl.tiles_h; p.tiles_w = pl.tiles_w;
+  p.kb = pl.kb; p.n_cb = pl.n_cb; p.b_bytes = pl.b_bytes; p.b_off = pl.b_off;
   p.n_tiles = pl.n_tiles; p.n_split = pl.n_split; p.n_items = pl.n_tiles * pl.n_split;
-  p.a_bytes = pl.a_bytes; p.a_stride = pl.a_stride; p.stages = pl.stages; p.chunk_stride = pl.chunk_stride; p.w_bytes = pl.w_bytes;
-  p.w_off = (pl.w_bytes + 1023) / 1024 * 1024;
-  for (int k = 0; k < kMaxKt; ++k) p.slot[k] = a.slot[k];
+  p.a_bytes = pl.a_bytes; p.a_stride = pl.a_stride; p.stages = pl.stages; p.chunk_stride = pl.chunk_stride;
+  p.w_bytes = pl.w_bytes; p.w_off = pl.w_off;
+  for (int i = 0; i < kMaxKt; ++i) p.slot[i] = a.slot[i];
   p.emit = a.emit; p.update = a.update; p.act = g.act; p.out_f32 = (g.out_dtype == F32);
   p.Cq = g.Cq;
   p.state = a.state;
@@ -547,7 +834,7 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   p.y_bstride = a.y_bstride;
   p.wpack = t->wpack;
   p.bias = bias;
-  const int per = t->num_sms / pl.n_split;
+  const int per = std::max(1, t->num_sms / pl.n_split);
   const int64_t grid = std::min<int64_t>(per, pl.n_tiles) * pl.n_split;
   void* args[] = {&map, &p};
   return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->fn), dim3(unsigned(grid)),

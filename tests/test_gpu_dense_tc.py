@@ -24,10 +24,23 @@ CASES = {
     # C5-shaped flat mode: 25 joints, kt 9, dilation 2, rows span streams, ragged tail
     "flat_c5like": dict(desc=O.Desc(1, 32, 32, (9, 1), dilation=(2, 1), in_spatial=(25, 1)), B=7),
     "flat_conv1d": dict(desc=O.Desc(0, 48, 32, (3,), padding=(1,)), B=300),
+    # KLOOP mode: K streamed through the stage ring, A gathered by strided TMA
+    "kloop_s2": dict(desc=O.Desc(2, 32, 64, (3, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1), in_spatial=(13, 18)), B=2),
+    "kloop_c4l3like": dict(desc=O.Desc(2, 128, 128, (3, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1),
+                                       in_spatial=(12, 20)), B=2),
+    "kloop_bigK": dict(desc=O.Desc(2, 256, 64, (3, 3, 3), padding=(0, 1, 1), in_spatial=(7, 9)), B=2),
+    "kloop_dil": dict(desc=O.Desc(2, 16, 32, (2, 3, 3), padding=(0, 2, 2), dilation=(1, 2, 2), in_spatial=(9, 9)), B=2),
+    "kloop_wide": dict(desc=O.Desc(2, 16, 32, (3, 1, 3), stride=(1, 1, 2), padding=(0, 0, 1), in_spatial=(3, 300)), B=2),
+    "kloop_kt1_s2": dict(desc=O.Desc(2, 64, 128, (1, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1), in_spatial=(10, 14)), B=3),
+    # small-Cin stems: W-im2col'd frame (C4 layer 1 shaped), KLOOP (stride 2) and HALO (stride 1)
+    "stem_c4like": dict(desc=O.Desc(2, 3, 32, (5, 7, 7), stride=(1, 2, 2), padding=(0, 3, 3), in_spatial=(20, 22)), B=2),
+    "stem_halo": dict(desc=O.Desc(2, 3, 16, (3, 3, 3), padding=(1, 1, 1), in_spatial=(9, 10)), B=2),
 }
+FORCE_KLOOP = {"halo_c2like", "halo_kt5", "flat_c5like"}   # also run these through the K pipeline
 
 
-def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0):
+def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force_kloop=False):
+    import os
     d, B = CASES[case]["desc"], CASES[case]["B"]
     rng = np.random.default_rng(seed)
     if integer:
@@ -36,9 +49,16 @@ def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0):
     else:
         W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
         b = rng.standard_normal(d.cout) * 0.1
-    conv, sm, Wq, bq = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="dense_tc")
+    if force_kloop:
+        os.environ["CO_TC_MODE"] = "kloop"
+    try:
+        conv, sm, Wq, bq = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="dense_tc")
+    finally:
+        os.environ.pop("CO_TC_MODE", None)
     ref_conv, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="direct")
     assert conv.kernel_used == "dense_tc", conv.kernel_name
+    if force_kloop or case.startswith("kloop") or case == "stem_c4like":
+        assert "kloop" in conv.kernel_name, conv.kernel_name
     H, Wd = d.in_hw
     shp = (B, d.cin) + ((H,) if d.spatial_rank >= 1 else ()) + ((Wd,) if d.spatial_rank >= 2 else ())
     steps = steps or (d.receptive_field + 4)
@@ -72,6 +92,15 @@ def test_dense_tc_exact_integer_bitwise(case):
     assert np.array_equal(y, yd)
 
 
+@pytest.mark.parametrize("case", sorted(FORCE_KLOOP))
+def test_dense_tc_forced_kloop(case):
+    """The same layers through the K pipeline (CO_TC_MODE=kloop) agree with the oracle."""
+    _, y, ref, yd = _run(case, force_kloop=True)
+    assert rel_err(y, ref) <= 1e-4 and rel_err(y, yd) <= 1e-4
+    _, y, ref, _ = _run(case, integer=True, force_kloop=True)
+    assert np.array_equal(y, ref)
+
+
 @pytest.mark.parametrize("case", ["halo_c2like", "flat_c5like"])
 def test_dense_tc_bf16_output(case):
     # A16: bf16 outputs are checked against the RNE error bound
@@ -80,7 +109,7 @@ def test_dense_tc_bf16_output(case):
     assert_bf16_rounding_bound(y, ref)
 
 
-@pytest.mark.parametrize("case", ["halo_c2like", "flat_c5like"])
+@pytest.mark.parametrize("case", ["halo_c2like", "flat_c5like", "kloop_s2", "stem_c4like"])
 def test_dense_tc_state_and_steps(case):
     """State get vs oracle O5, update_state=False purity, forward_steps fold."""
     d, B = CASES[case]["desc"], CASES[case]["B"]
@@ -113,3 +142,38 @@ def test_dense_tc_state_and_steps(case):
     assert ys.shape[2] == len(fold)
     for i, f in enumerate(fold):
         assert torch.equal(ys[:, :, i], f)
+
+
+def test_c4_stack_reduced_spatial_vs_oracle():
+    """BASELINE.json configs[3] (Slow-style 5-layer stack: 3->64->128->256->256->512,
+    kernels 5x7x7 s2, 1x3x3, 3x3x3 s2, 3x3x3, 3x3x3 s2, BN folded, ReLU x4) at a
+    reduced 32x32 input so the fp64 oracle stays fast: every layer runs on the
+    tensor-core kernel (stem W-im2col, HALO, KLOOP); delay d_NN = sum(kt-1) = 10."""
+    import paper_2204_03418_b200 as co
+    from paper_2204_03418_b200 import synth
+    cfg = synth.config(4, n_streams=2, in_spatial=(32, 32))
+    params = synth.params(cfg)
+    convs, descs, Ws, bs, spat = [], [], [], [], tuple(cfg.in_spatial)
+    for l, (L, (W, b)) in enumerate(zip(cfg.layers, params)):
+        last = l == len(cfg.layers) - 1
+        c = co.Conv(L.cin, L.cout, L.kernel, weight=W.cuda(), bias=b.cuda(), stride=L.stride, padding=L.padding,
+                    dilation=L.dilation, groups=L.groups, spatial_rank=2, in_spatial=spat, n_streams=cfg.n_streams,
+                    dtype=torch.bfloat16, out_dtype=torch.float32 if last else torch.bfloat16,
+                    activation="relu" if L.relu else None)
+        assert c.kernel_used == "dense_tc", (l, c.kernel_name)
+        d = O.Desc(2, L.cin, L.cout, L.kernel, L.stride, L.padding, L.dilation, L.groups, spat)
+        convs.append(c); descs.append(d); Ws.append(W.double().numpy()); bs.append(b.double().numpy())
+        spat = d.out_spatial
+    stack = co.Stack(convs)
+    assert stack.delay == 10
+    ost = O.Stack(descs, Ws, bs, [int(L.relu) for L in cfg.layers], [1, 1, 1, 1, 0], cfg.n_streams)
+    ys, refs = [], []
+    for t in range(13):
+        x = synth.frame(cfg, t)
+        y = stack.forward_step(x)
+        r = ost.forward_step(np_of(x))
+        assert (y is None) == (r is None) == (t < 10)
+        if y is not None:
+            ys.append(np_of(y)); refs.append(r)
+    y, ref = np.stack(ys), np.stack(refs).reshape(np.stack(ys).shape)
+    assert rel_err(y, ref) <= 2e-2
