@@ -70,20 +70,9 @@ def dist_setup(args):
     return world, rank, local
 
 
-def all_reduce(vals, op):
-    import torch
-    import torch.distributed as dist
-    if not (dist.is_available() and dist.is_initialized()):
-        return vals
-    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=op)
-    return t.tolist()
-
-
 def barrier():
-    import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized():
-        dist.barrier()
+    from paper_2204_03418_b200 import shard
+    shard.barrier()
 
 
 # ----------------------------------------------------------------- clocks
@@ -191,14 +180,15 @@ def measured_peaks():
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 
-def ncu_traffic(kernel_name):
-    """dram bytes (read+write) per stream-step from the committed ncu --set full summary."""
+def ncu_traffic(key):
+    """dram bytes (read+write) per stream-step of layer `key` ("<config>/L<i>") from the
+    committed ncu --set full summaries (scripts/ncu_summary.py -> profiles/ncu_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         j = json.load(f)
-    return j.get(kernel_name)
+    return j.get(key)
 
 
 def build_layers(cfg, B, kernel="auto"):
@@ -226,14 +216,15 @@ def run_co(args, world, rank):
     cfg = synth.config(args.config)
     # weak scaling (the path partitions into independent streams): each rank runs
     # the config's stream count on its own GPU, global streams [r B, (r+1) B)
-    B = args.streams or cfg.n_streams
-    B_global = B * world
+    from paper_2204_03418_b200 import shard as sh
+    sd = sh.shard(rank, world, args.streams or cfg.n_streams)
+    B, B_global = sd.per_rank, sd.n_global
     convs = build_layers(cfg, B, args.kernel)
     esz = 2 if cfg.dtype == torch.bfloat16 else 4
     frame_bytes = B * math.prod(synth.in_shape(cfg)) * esz
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     G = min(max(8, math.ceil(4 * l2 / frame_bytes)), 64)
-    pool = [synth.frame(cfg, t, rank * B, (rank + 1) * B, n_global=B_global) for t in range(G)]
+    pool = [synth.frame(cfg, t, sd.lo, sd.hi, n_global=B_global) for t in range(G)]
     acts = [co._empty_cl((B, c.out_channels) + c.out_spatial, c.out_dtype, "cuda") for c in convs]
     stream = torch.cuda.current_stream()
     nL = len(convs)
@@ -274,9 +265,8 @@ def run_co(args, world, rank):
     elapsed_ms = ev0[0].elapsed_time(evl[K - 1][-1])
     layer_ms = [statistics.mean(([ev0[k].elapsed_time(evl[k][0]) for k in range(K)] if l == 0 else
                                  [evl[k][l - 1].elapsed_time(evl[k][l]) for k in range(K)])) for l in range(nL)]
-    [elapsed_max] = all_reduce([elapsed_ms], op=_max_op())
-    [total_ss] = all_reduce([float(B * K)], op=_sum_op())
-    value = total_ss / (elapsed_max / 1e3)
+    red = sh.reduce_counters(stream_steps=B * K, elapsed_ms=elapsed_ms)
+    elapsed_max, value = red["elapsed_ms"], red["throughput"]
 
     hbm, bf16, src = measured_peaks()
     layers, spat = [], tuple(cfg.in_spatial)
@@ -297,7 +287,7 @@ def run_co(args, world, rank):
         else:
             roof = {"bound": bound_c, "achieved": round(ach_tf, 2), "peak": round(peak_c, 1), "unit": unit_c,
                     "frac": round(ach_tf / peak_c, 4)}
-        tr = ncu_traffic(c.kernel_name)
+        tr = ncu_traffic(f"{cfg.name}/L{l}")
         roof.update({"kernel": c.kernel_name, "ms_per_launch": round(ms, 4),
                      "alg_bytes_per_launch": int(bytes_ss * B), "alg_flops_per_launch": flops_ss * B,
                      "traffic": None if tr is None else int(tr.get("bytes_per_stream_step", 0) * B),
@@ -332,16 +322,6 @@ def run_co(args, world, rank):
     return out, convs, pool, cfg, B
 
 
-def _max_op():
-    import torch.distributed as dist
-    return dist.ReduceOp.MAX if dist.is_available() else None
-
-
-def _sum_op():
-    import torch.distributed as dist
-    return dist.ReduceOp.SUM if dist.is_available() else None
-
-
 def run_e2e(args, convs, pool, cfg, B, world):
     """Same metric through the public host-buffer C-ABI call (co_forward_step_host
     / co_stack_step_host): H2D of the frame from pinned memory, the tick, D2H of
@@ -364,9 +344,9 @@ def run_e2e(args, convs, pool, cfg, B, world):
         assert fn(xh[k % 2], yh)
     e.record()
     torch.cuda.synchronize()
-    [ms] = all_reduce([s.elapsed_time(e)], op=_max_op())
-    [tot] = all_reduce([float(B * K)], op=_sum_op())
-    return {"value": round(tot / (ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": int(xh[0].numel() * xh[0].element_size()),
+    from paper_2204_03418_b200 import shard as sh
+    red = sh.reduce_counters(stream_steps=B * K, elapsed_ms=s.elapsed_time(e))
+    return {"value": round(red["throughput"], 1), "unit": UNIT, "h2d_bytes_per_step": int(xh[0].numel() * xh[0].element_size()),
             "d2h_bytes_per_step": int(yh.numel() * yh.element_size()), "steps": K}
 
 

@@ -81,3 +81,24 @@ def assert_bf16_rounding_bound(y, ref, fp32_tol=1e-4):
     bad = np.abs(y - ref) > bound
     assert not bad.any(), f"{int(bad.sum())} elements exceed the bf16 rounding bound; worst excess " \
                           f"{float((np.abs(y - ref) - bound).max()):.3e}"
+
+
+def build_config_layers(cfg, B, last_fp32=True, kernel="auto", out_dtype=None):
+    """The config's layers on B streams exactly as bench.py builds them (same
+    dispatch, kernels and launch geometry); the final layer emits fp32 for
+    parity (A16: same kernel, only the final conversion differs)."""
+    import paper_2204_03418_b200 as co
+    from paper_2204_03418_b200 import synth
+    convs, descs, Ws, bs, spat = [], [], [], [], tuple(cfg.in_spatial)
+    params = synth.params(cfg)
+    for l, (L, (W, b)) in enumerate(zip(cfg.layers, params)):
+        last = l == len(cfg.layers) - 1
+        od = out_dtype or (torch.float32 if (last and last_fp32) else cfg.dtype)
+        c = co.Conv(L.cin, L.cout, L.kernel, weight=W.cuda(), bias=b.cuda(), stride=L.stride, padding=L.padding,
+                    dilation=L.dilation, groups=L.groups, spatial_rank=cfg.spatial_rank, in_spatial=spat,
+                    n_streams=B, dtype=cfg.dtype, out_dtype=od, activation="relu" if L.relu else None,
+                    kernel=kernel)
+        d = O.Desc(cfg.spatial_rank, L.cin, L.cout, L.kernel, L.stride, L.padding, L.dilation, L.groups, spat)
+        convs.append(c); descs.append(d); Ws.append(W.double().numpy()); bs.append(b.double().numpy())
+        spat = tuple(c.out_spatial) + (1,) * (2 - len(c.out_spatial))
+    return convs, descs, Ws, bs

@@ -1,0 +1,123 @@
+"""Parity at BASELINE.json's FULL sizes, in the launch configuration bench.py
+times (same stream counts, dispatch, kernels and grids):
+
+* sampled streams (first, middle, last) against the fp64 oracle, element by
+  element, over every Ready tick of a run that covers the whole delay;
+* every stream, every layer: the step outputs equal the batch forward
+  (co_forward, the CUDA-core direct kernel) of the frames that layer consumed
+  -- Definition 1, a property that holds at any size;
+* ready flags / clock identical to the oracle on every tick.
+
+Tolerances (BASELINE.json north_star): fp32 C1 1e-4 RMS (test_gpu_direct.py);
+bf16 inputs with fp32 accumulation 2e-2 RMS on fp32 outputs (A16).  Single
+layers see exact bf16 inputs, so they are held to 1e-4.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from tests.helpers import assert_bf16_rounding_bound, build_config_layers, np_of, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _stack_run(cfg, convs, T, keep):
+    """Run T ticks of the layer chain; returns per-layer lists of (inputs, outputs)
+    for all streams (on device) and the sampled final outputs."""
+    import paper_2204_03418_b200 as co
+    from paper_2204_03418_b200 import synth
+    ins = [[] for _ in convs]
+    outs = [[] for _ in convs]
+    ready = []
+    for t in range(T):
+        cur = synth.frame(cfg, t)
+        r_all = True
+        for l, c in enumerate(convs):
+            if keep:
+                ins[l].append(cur)
+            y = c.forward_step(cur)
+            if y is None:
+                r_all = False
+                break
+            if keep:
+                outs[l].append(y)
+            cur = y
+        ready.append(r_all)
+    return ins, outs, ready
+
+
+def _sampled(x, idx):
+    return np_of(x[idx])
+
+
+@pytest.mark.parametrize("cid", [2, 3, 4, 5])
+def test_fullsize_sampled_streams_vs_oracle(cid):
+    from paper_2204_03418_b200 import synth
+    cfg = synth.config(cid)
+    B = cfg.n_streams
+    convs, descs, Ws, bs = build_config_layers(cfg, B)
+    d_nn = sum(d.delay for d in descs)
+    T = d_nn + 3
+    idx = sorted({0, B // 2, B - 1})
+    if len(convs) == 1:
+        om = O.StepMachine(descs[0], Ws[0], bs[0], len(idx))
+    else:
+        om = O.Stack(descs, Ws, bs, [int(L.relu) for L in cfg.layers], [1] * (len(convs) - 1) + [0], len(idx))
+    ys, refs = [], []
+    for t in range(T):
+        x = synth.frame(cfg, t)
+        cur, ready = x, True
+        for c in convs:
+            cur = c.forward_step(cur)
+            if cur is None:
+                ready = False
+                break
+        r = om.forward_step(_sampled(x, idx))
+        assert ready == (r is not None) == (t >= d_nn), (t, ready)
+        if ready:
+            ys.append(_sampled(cur, idx)); refs.append(r.reshape(ys[-1].shape))
+    y, ref = np.stack(ys), np.stack(refs)
+    assert len(ys) == T - d_nn
+    tol = 1e-4 if len(convs) == 1 else 2e-2
+    assert rel_err(y, ref) <= tol, rel_err(y, ref)
+
+
+@pytest.mark.parametrize("cid", [2, 3, 4, 5])
+def test_fullsize_step_equals_batch_all_streams(cid):
+    """Every stream of every layer: step outputs == batch forward of the inputs
+    that layer consumed, computed on the GPU by the direct kernel."""
+    import paper_2204_03418_b200 as co
+    from paper_2204_03418_b200 import synth
+    cfg = synth.config(cid)
+    B = cfg.n_streams
+    convs, descs, Ws, bs = build_config_layers(cfg, B)
+    T = sum(d.delay for d in descs) + 2
+    ins, outs, ready = _stack_run(cfg, convs, T, keep=True)
+    for l, (c, d) in enumerate(zip(convs, descs)):
+        if not outs[l]:
+            continue
+        # checker: the same layer (weights, bias, activation) on the direct CUDA-core kernel, fp32 out
+        L = cfg.layers[l]
+        (W, b) = synth.params(cfg)[l]
+        chk = co.Conv(L.cin, L.cout, L.kernel, weight=W.cuda(), bias=b.cuda(), stride=L.stride, padding=L.padding,
+                      dilation=L.dilation, groups=L.groups, spatial_rank=cfg.spatial_rank, in_spatial=c.in_spatial,
+                      n_streams=B, dtype=cfg.dtype, out_dtype=torch.float32,
+                      activation="relu" if L.relu else None, kernel="direct")
+        clip = torch.stack(ins[l], dim=2)                      # (B, C, T_l, *S) channels-last per frame
+        clip = co.channels_last(clip)
+        yb = chk.forward(clip)                                 # (B, Cout, T'_l, *S')
+        n = len(outs[l])
+        ys = torch.stack(outs[l], dim=2).float()
+        assert yb.shape[2] >= n
+        yb = yb[:, :, :n].float()
+        if c.out_dtype == torch.float32:
+            err = (ys - yb).abs().max().item() / yb.pow(2).mean().sqrt().item()
+            assert err <= 1e-4, (l, err)
+        else:
+            # bf16 emitted outputs: the RNE bound around the fp32 batch result
+            eps = 1e-4 * yb.pow(2).mean().sqrt().item()
+            excess = ((ys - yb).abs() - (2.0 ** -8 * (yb.abs() + eps) + eps)).max().item()
+            assert excess <= 0, (l, excess)
+        del chk, clip, yb, ys
+        torch.cuda.empty_cache()
