@@ -11,6 +11,8 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libco_b200.so")
+if os.environ.get("CO_LIB_VARIANT"):            # experiment builds only (build.py --variant)
+    LIB_PATH = os.path.join(_HERE, f"libco_b200_{os.environ['CO_LIB_VARIANT']}.so")
 
 CO_OK, CO_ERR_ARG, CO_ERR_SHAPE, CO_ERR_LENGTH, CO_ERR_UNSUPPORTED, CO_ERR_CUDA, CO_ERR_OOM = 0, -1, -2, -3, -4, -5, -6
 CO_F32, CO_BF16 = 0, 1

@@ -51,12 +51,12 @@ def _newer(src_list, target):
     return any(os.path.getmtime(s) > t for s in src_list)
 
 
-def _compile(src: str, force: bool, verbose: bool) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+def _compile(src: str, force: bool, verbose: bool, bdir: str = BUILD, extra=()) -> str:
+    obj = os.path.join(bdir, os.path.basename(src) + ".o")
     if force or _newer([src] + _deps(), obj):
-        cmd = [nvcc()] + NVCC_FLAGS + ["-c", src, "-o", obj]
+        cmd = [nvcc()] + NVCC_FLAGS + list(extra) + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        log = os.path.join(BUILD, os.path.basename(src) + ".log")
+        log = os.path.join(bdir, os.path.basename(src) + ".log")
         with open(log, "w") as f:
             f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
         if r.returncode != 0:
@@ -66,24 +66,31 @@ def _compile(src: str, force: bool, verbose: bool) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Build libco_b200.so; `variant` + `defines` build an experiment copy
+    libco_b200_<variant>.so (loaded when CO_LIB_VARIANT=<variant>)."""
+    bdir = BUILD + (f"_{variant}" if variant else "")
+    lib = LIB if not variant else LIB.replace(".so", f"_{variant}.so")
+    extra = [f"-D{d}" for d in defines]
+    os.makedirs(bdir, exist_ok=True)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force, verbose), srcs))
-    if force or _newer(objs, LIB):
-        tmp = LIB + f".{os.getpid()}.tmp"
+        objs = list(ex.map(lambda s: _compile(s, force, verbose, bdir, extra), srcs))
+    if force or _newer(objs, lib):
+        tmp = lib + f".{os.getpid()}.tmp"
         cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs + ["-lpthread", "-ldl", "-lrt"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--variant", default="")
+    ap.add_argument("--define", action="append", default=[])
     a = ap.parse_args()
-    print(build(a.force, a.verbose))
+    print(build(a.force, a.verbose, a.variant, a.define))

@@ -1,0 +1,146 @@
+// bw_probe.cu — HBM streaming microbenchmark for the state read-modify-write
+// pattern of the dense step epilogue (experiment tool, not product code).
+//
+// State C2-shaped: 256 streams x 3136 px x 64 ch fp32, R = 2 slots (411 MB).
+// One "item" = 128 pixel rows x 32 channels; per item a thread (= row) reads
+// 2 slots x 8 quads (float4) and writes 2 slots x 8 quads + 64 B of bf16 y.
+//   mode 0: quad-major layout  S[slot][Cq][plane][4]     (current kernel)
+//   mode 1: channels-last      S[slot][plane][C], thread = (pixel, quad)
+//   mode 2: plain float4 copy of the same byte volume (reference)
+// usage: bw_probe <mode> <threads per block> <blocks per SM> <items in flight per thread>
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+constexpr long long B = 256, HW = 3136, C = 64, R = 2;
+constexpr long long PLANE = B * HW;                 // pixels
+constexpr int CQ = C / 4;
+
+template <int NI>
+__global__ void k_quadmajor(float4* __restrict__ st, __nv_bfloat16* __restrict__ y, long long n_items) {
+  // item = (tile of 128 pixels, channel half); thread = pixel row of the tile
+  const int row = threadIdx.x & 127;
+  const int sub = threadIdx.x >> 7;                 // several items per block
+  const int per_block = blockDim.x >> 7;
+  for (long long it0 = (long long)blockIdx.x * per_block + sub; it0 < n_items; it0 += (long long)gridDim.x * per_block * NI) {
+    float4 a[NI][2][8];
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const long long it = it0 + (long long)j * gridDim.x * per_block;
+      if (it >= n_items) continue;
+      const long long pix = (it >> 1) * 128 + row;
+      const int q0 = (int)(it & 1) * 8;
+      if (pix >= PLANE) continue;
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[j][s][q] = __ldcs(st + ((long long)s * CQ + q0 + q) * PLANE + pix);
+    }
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const long long it = it0 + (long long)j * gridDim.x * per_block;
+      if (it >= n_items) continue;
+      const long long pix = (it >> 1) * 128 + row;
+      const int q0 = (int)(it & 1) * 8;
+      if (pix >= PLANE) continue;
+      uint4 yv[4];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 v0 = a[j][0][q], v1 = a[j][1][q];
+        v0.x += 1.f; v1.y += 1.f;
+        __stcs(st + ((long long)0 * CQ + q0 + q) * PLANE + pix, v1);
+        __stcs(st + ((long long)1 * CQ + q0 + q) * PLANE + pix, v0);
+        reinterpret_cast<float*>(yv)[q] = v0.x + v1.x;
+      }
+      *reinterpret_cast<uint4*>(y + pix * C + q0 * 4) = yv[0];
+      *reinterpret_cast<uint4*>(y + pix * C + q0 * 4 + 8) = yv[1];
+      *reinterpret_cast<uint4*>(y + pix * C + q0 * 4 + 16) = yv[2];
+      *reinterpret_cast<uint4*>(y + pix * C + q0 * 4 + 24) = yv[3];
+    }
+  }
+}
+
+template <int NI>
+__global__ void k_chlast(float4* __restrict__ st, uint2* __restrict__ y, long long n) {
+  // thread = (pixel, quad); state S[slot][plane][C]
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * NI) {
+    float4 a[NI][2];
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const long long i = i0 + j * stride;
+      if (i < n) { a[j][0] = __ldcs(st + i); a[j][1] = __ldcs(st + n + i); }
+    }
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const long long i = i0 + j * stride;
+      if (i >= n) continue;
+      float4 v0 = a[j][0], v1 = a[j][1];
+      v0.x += 1.f; v1.y += 1.f;
+      __stcs(st + i, v1);
+      __stcs(st + n + i, v0);
+      y[i] = make_uint2(__float_as_uint(v0.x), __float_as_uint(v1.x));
+    }
+  }
+}
+
+template <int NI>
+__global__ void k_copy(const float4* __restrict__ a, float4* __restrict__ b, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * NI) {
+    float4 v[NI];
+#pragma unroll
+    for (int j = 0; j < NI; ++j) if (i0 + j * stride < n) v[j] = __ldcs(a + i0 + j * stride);
+#pragma unroll
+    for (int j = 0; j < NI; ++j) if (i0 + j * stride < n) __stcs(b + i0 + j * stride, v[j]);
+  }
+}
+
+int main(int argc, char** argv) {
+  const int mode = atoi(argv[1]), threads = atoi(argv[2]), bps = atoi(argv[3]), ni = atoi(argv[4]);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const long long st_elems = R * C * PLANE;         // floats
+  float4* st;
+  void* y;
+  cudaMalloc(&st, st_elems * 4);
+  cudaMalloc(&y, PLANE * C * 2 + 4096);
+  cudaMemset(st, 0, st_elems * 4);
+  float4* other = nullptr;
+  const long long bytes_rw = st_elems * 4 * 2 + PLANE * C * 2;   // state read+write + y write
+  if (mode == 2) cudaMalloc(&other, bytes_rw / 2 + 4096);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int grid = sms * bps;
+  auto launch = [&]() {
+    if (mode == 0) {
+      const long long n_items = (PLANE + 127) / 128 * 2;
+      if (ni == 1) k_quadmajor<1><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items);
+      else k_quadmajor<2><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items);
+    } else if (mode == 1) {
+      const long long n = PLANE * CQ;
+      if (ni == 1) k_chlast<1><<<grid, threads>>>(st, (uint2*)y, n);
+      else if (ni == 2) k_chlast<2><<<grid, threads>>>(st, (uint2*)y, n);
+      else k_chlast<4><<<grid, threads>>>(st, (uint2*)y, n);
+    } else {
+      const long long n = bytes_rw / 2 / 16;
+      if (ni == 1) k_copy<1><<<grid, threads>>>(st, other, n);
+      else if (ni == 2) k_copy<2><<<grid, threads>>>(st, other, n);
+      else k_copy<4><<<grid, threads>>>(st, other, n);
+    }
+  };
+  for (int i = 0; i < 3; ++i) launch();
+  cudaEventRecord(e0);
+  const int reps = 20;
+  for (int i = 0; i < reps; ++i) launch();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const cudaError_t err = cudaGetLastError();
+  printf("mode %d threads %d blocks/SM %d NI %d: %.1f us/launch, %.1f GB/s %s\n", mode, threads, bps, ni,
+         ms * 1e3 / reps, bytes_rw / (ms / reps * 1e-3) / 1e9, err == cudaSuccess ? "" : cudaGetErrorString(err));
+  return 0;
+}
