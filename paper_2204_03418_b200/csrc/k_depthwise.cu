@@ -40,7 +40,7 @@ namespace {
 
 constexpr int kDwThreads = 256;
 constexpr int kNB = 4;                  // items per thread per batch (state loads in flight)
-constexpr size_t kHaloBudget = 48 * 1024;
+constexpr size_t kHaloBudget = 72 * 1024;
 
 struct DwParams {
   const __nv_bfloat16* x;               // frame of stream 0 (nullptr = zero frame)
@@ -132,97 +132,97 @@ __device__ __forceinline__ void apply(const DwParams& p, int64_t b, int64_t pin,
 }
 
 // ------------------------------------------------------------------ K2: spatial stencil
-template <int KT, int KH, int KW>
-__global__ void __launch_bounds__(kDwThreads, (KT <= 3 && KH * KW <= 9) ? 3 : 2) k_step_dw_st(const DwParams p) {
+// Thread = (channel quad q, fixed for the thread's life) x strips of PX output
+// pixels of one row.  Per strip: the state of its PX pixels is loaded first,
+// then for each tap row u the PX+KW-1 input columns are read from the staged
+// halo once and every (v, k) weight float4 once, so shared-memory traffic per
+// pixel is (KT*KH*KW*16 + KH*(PX+KW-1)*8) / PX bytes -- PX times less than a
+// thread-per-pixel stencil, which made the first K2 shared-memory bound.
+// The per-slice FMA order (u-major, then v) is k_step_direct's, so the two
+// kernels agree bitwise.
+template <int KT, int KH, int KW, int PX>
+__global__ void __launch_bounds__(256, 2) k_step_dw_st(const DwParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   float* ws = reinterpret_cast<float*>(smem);                       // [KT][KH][KW][C]
   float* bs = ws + KT * KH * KW * p.C;                              // [C]
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(bs + p.C);   // [HR][WC][C]
   const int tid = threadIdx.x;
-  for (int i = tid; i < KT * KH * KW * p.C; i += blockDim.x) ws[i] = p.w[i];
-  for (int i = tid; i < p.C; i += blockDim.x) bs[i] = p.bias[i];
+  const int nthr = blockDim.x;                                      // = Cq * n_srow
+  for (int i = tid; i < KT * KH * KW * p.C; i += nthr) ws[i] = p.w[i];
+  for (int i = tid; i < p.C; i += nthr) bs[i] = p.bias[i];
+  const int q = tid % p.Cq;                                         // this thread's channel quad
+  const int srow = tid / p.Cq;
+  const int n_srow = nthr / p.Cq;
+  const int spr = (p.Wo + PX - 1) / PX;                             // strips per output row
   const int c8 = p.C / 8;
-  const int halo_chunks = p.HR * p.WC * c8;
+  const int row_chunks = p.WC * c8;
   const uint32_t xs_u32 = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
+  const float4* ws4 = reinterpret_cast<const float4*>(ws) + q;     // + ((k*KH + u)*KW + v) * Cq
+  const float4 bias4 = reinterpret_cast<const float4*>(bs)[q];
+  (void)bias4;
 
   for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
     const int64_t b = tile / p.bands;
     const int ho0 = int(tile % p.bands) * p.TH;
     const int th = min(p.TH, p.Ho - ho0);
-    const int n_items = th * p.Wo * p.Cq;
     __syncthreads();   // previous tile finished reading xs (and ws/bs are visible)
-
-    // (1) first batch's state loads go out before the halo is staged
-    Pre<KT> pre[kNB];
-    auto item_pix = [&](int it, int& q, int& r, int& wo) {
-      q = it % p.Cq;
-      const int pw_ = it / p.Cq;
-      wo = pw_ % p.Wo;
-      r = pw_ / p.Wo;
-    };
-#pragma unroll
-    for (int j = 0; j < kNB; ++j) {
-      const int it = tid + j * kDwThreads;
-      if (it < n_items) {
-        int q, r, wo;
-        item_pix(it, q, r, wo);
-        prefetch<KT>(p, b * p.HWo + int64_t(ho0 + r) * p.Wo + wo, q, pre[j]);
-      }
-    }
-    // (2) input halo -> shared memory (cp.async 16 B, zero fill outside the frame)
+    // input halo -> shared memory (cp.async 16 B, zero fill outside the frame)
     const __nv_bfloat16* xb = p.x ? p.x + b * p.x_bstride : nullptr;
-    for (int i = tid; i < halo_chunks; i += blockDim.x) {
-      const int ch = i % c8;
-      const int pc = i / c8;
-      const int c = pc % p.WC, r = pc / p.WC;
-      const int hi = ho0 - p.ph + r, wi = c - p.pw;
-      const bool in = xb && hi >= 0 && hi < p.H && wi >= 0 && wi < p.W;
-      // src-size 0 zero-fills; the (unread) address stays a valid one
-      const void* src = in ? static_cast<const void*>(xb + (int64_t(hi) * p.W + wi) * p.C + ch * 8)
-                           : static_cast<const void*>(p.w);
-      const uint32_t dst = xs_u32 + uint32_t(i) * 16u;
-      const int sz = in ? 16 : 0;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(sz) : "memory");
+    for (int r = 0; r < p.HR; ++r) {
+      const int hi = ho0 - p.ph + r;
+      const bool row_in = xb && hi >= 0 && hi < p.H;
+      for (int i = tid; i < row_chunks; i += nthr) {
+        const int c = i / c8, ch = i - (i / c8) * c8;
+        const int wi = c - p.pw;
+        const bool in = row_in && wi >= 0 && wi < p.W;
+        // src-size 0 zero-fills; the (unread) address stays a valid one
+        const void* src = in ? static_cast<const void*>(xb + (int64_t(hi) * p.W + wi) * p.C + ch * 8)
+                             : static_cast<const void*>(p.w);
+        const uint32_t dst = xs_u32 + uint32_t(r * row_chunks + i) * 16u;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(in ? 16 : 0)
+                     : "memory");
+      }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 
-    // (3) items in batches of kNB per thread
-    for (int base = 0; base < n_items; base += kNB * kDwThreads) {
-      if (base > 0) {
+    for (int sidx = srow; sidx < th * spr; sidx += n_srow) {
+      const int r = sidx / spr;
+      const int wo0 = (sidx - r * spr) * PX;
+      const int64_t pin0 = int64_t(ho0 + r) * p.Wo + wo0;           // pixel index inside the stream
+      const int64_t pix0 = b * p.HWo + pin0;
+      // (1) the strip's state goes out first
+      Pre<KT> pre[PX];
 #pragma unroll
-        for (int j = 0; j < kNB; ++j) {
-          const int it = base + tid + j * kDwThreads;
-          if (it < n_items) {
-            int q, r, wo;
-            item_pix(it, q, r, wo);
-            prefetch<KT>(p, b * p.HWo + int64_t(ho0 + r) * p.Wo + wo, q, pre[j]);
+      for (int j = 0; j < PX; ++j)
+        if (wo0 + j < p.Wo) prefetch<KT>(p, pix0 + j, q, pre[j]);
+      // (2) all kt partials of the PX pixels, one pass over the taps
+      float4 acc[KT][PX];
+#pragma unroll
+      for (int k = 0; k < KT; ++k)
+#pragma unroll
+        for (int j = 0; j < PX; ++j) acc[k][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < KH; ++u) {
+        float4 xv[PX + KW - 1];
+        const __nv_bfloat16* xr = xs + (int64_t(r + u) * p.WC + wo0) * p.C + 4 * q;
+#pragma unroll
+        for (int t = 0; t < PX + KW - 1; ++t) xv[t] = ld_bf16x4(xr + int64_t(t) * p.C);
+#pragma unroll
+        for (int v = 0; v < KW; ++v)
+#pragma unroll
+          for (int k = 0; k < KT; ++k) {
+            const float4 w = ws4[((k * KH + u) * KW + v) * p.Cq];
+#pragma unroll
+            for (int j = 0; j < PX; ++j) acc[k][j] = f4_fma(w, xv[j + v], acc[k][j]);
           }
-        }
       }
+      // (3) emit / accumulate / start
 #pragma unroll
-      for (int j = 0; j < kNB; ++j) {
-        const int it = base + tid + j * kDwThreads;
-        if (it >= n_items) continue;
-        int q, r, wo;
-        item_pix(it, q, r, wo);
-        // all kt partials in one pass over the taps (same per-slice FMA order
-        // as k_step_direct: u-major, then v)
-        float4 acc[KT];
-#pragma unroll
-        for (int k = 0; k < KT; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int u = 0; u < KH; ++u)
-#pragma unroll
-          for (int v = 0; v < KW; ++v) {
-            const float4 xv = ld_bf16x4(xs + (int64_t(r + u) * p.WC + (wo + v)) * p.C + 4 * q);
-#pragma unroll
-            for (int k = 0; k < KT; ++k)
-              acc[k] = f4_fma(reinterpret_cast<const float4*>(ws + (k * KH * KW + u * KW + v) * p.C)[q], xv, acc[k]);
-          }
-        auto P = [&](int k) -> float4 { return acc[k]; };
-        const int64_t pin = int64_t(ho0 + r) * p.Wo + wo;
-        apply<KT>(p, b, pin, b * p.HWo + pin, q, pre[j], reinterpret_cast<const float4*>(bs)[q], P);
+      for (int j = 0; j < PX; ++j) {
+        if (wo0 + j >= p.Wo) continue;
+        auto P = [&](int k) -> float4 { return acc[k][j]; };
+        apply<KT>(p, b, pin0 + j, pix0 + j, q, pre[j], reinterpret_cast<const float4*>(bs)[q], P);
       }
     }
   }
@@ -281,8 +281,12 @@ typedef void (*DwFn)(const DwParams);
 struct DwVariant {
   int KT, KH, KW;
   DwFn fn;
+  int PX = 1;                           // K2: output pixels per thread strip
 };
-#define CO_DW_ST(kt, kh, kw) {kt, kh, kw, (DwFn)k_step_dw_st<kt, kh, kw>}
+#ifndef CO_DW_PX
+#define CO_DW_PX 2                      // output pixels per thread strip (experiments: -DCO_DW_PX=n)
+#endif
+#define CO_DW_ST(kt, kh, kw) {kt, kh, kw, (DwFn)k_step_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>, (kt <= 3 ? CO_DW_PX : 2)}
 #define CO_DW_T(kt) {kt, 1, 1, (DwFn)k_step_dw_t<kt>}
 const DwVariant kDwVariants[] = {
     CO_DW_ST(1, 3, 3), CO_DW_ST(2, 3, 3), CO_DW_ST(3, 3, 3), CO_DW_ST(5, 3, 3), CO_DW_ST(3, 5, 5),
@@ -292,6 +296,7 @@ const DwVariant kDwVariants[] = {
 struct DwPlan {
   const DwVariant* var = nullptr;
   bool temporal = false;
+  int threads = kDwThreads;             // K2: Cq * (rows of strips) <= 256
   int TH = 0, bands = 0, HR = 0, WC = 0;
   int64_t n_tiles = 0;
   size_t smem = 0;
@@ -309,7 +314,9 @@ bool make_dw_plan(const Geom& g, DwPlan& pl) {
   if (!pl.var) return false;
   pl.temporal = temporal;
   if (temporal) return true;
-  pl.WC = g.W + 2 * g.pw;
+  // staged halo width: every strip reads PX + kw - 1 columns (zero beyond the frame)
+  const int px = pl.var->PX;
+  pl.WC = std::max(g.W + 2 * g.pw, (g.Wo + px - 1) / px * px + g.kw - 1);
   const size_t row_bytes = size_t(pl.WC) * g.Cin * 2;
   int TH = int(kHaloBudget / row_bytes) - (g.kh - 1);
   if (TH < 1) {
@@ -322,6 +329,9 @@ bool make_dw_plan(const Geom& g, DwPlan& pl) {
   pl.bands = (g.Ho + TH - 1) / TH;
   pl.n_tiles = g.B * pl.bands;
   pl.smem = size_t(g.kt * g.kh * g.kw + 1) * g.Cin * 4 + size_t(pl.HR) * row_bytes;
+  const int Cq = g.Cin / 4;
+  if (Cq > 256) return false;
+  pl.threads = Cq * (256 / Cq);
   return pl.smem <= 227 * 1024;
 }
 
@@ -356,7 +366,8 @@ Depthwise* depthwise_create(const Geom& g, const void* w_dev, std::string& err) 
     e = cudaFuncSetAttribute(pl.var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
     if (e != cudaSuccess) { err = cudaGetErrorString(e); depthwise_destroy(t); return nullptr; }
   }
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.var->fn, kDwThreads, pl.temporal ? 0 : pl.smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.var->fn, pl.temporal ? kDwThreads : pl.threads,
+                                                pl.temporal ? 0 : pl.smem);
   per_sm = std::max(per_sm, 1);
   if (pl.temporal) {
     const int64_t items = g.B * g.HWo * (g.Cout / 4);
@@ -398,8 +409,8 @@ cudaError_t depthwise_step(Depthwise* t, const Geom& g, const StepArgs& a, const
   p.HWo = g.HWo; p.plane = g.B * g.HWo;
   p.TH = pl.TH; p.bands = pl.bands; p.n_tiles = pl.n_tiles; p.WC = pl.WC; p.HR = pl.HR;
   void* args[] = {&p};
-  return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->fn), dim3(unsigned(t->grid)), dim3(kDwThreads), args,
-                          pl.temporal ? 0 : pl.smem, s);
+  return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->fn), dim3(unsigned(t->grid)),
+                          dim3(pl.temporal ? kDwThreads : pl.threads), args, pl.temporal ? 0 : pl.smem, s);
 }
 
 }  // namespace co
