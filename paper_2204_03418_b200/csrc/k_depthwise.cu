@@ -39,7 +39,10 @@ namespace co {
 namespace {
 
 constexpr int kDwThreads = 256;
-constexpr int kNB = 4;                  // items per thread per batch (state loads in flight)
+#ifndef CO_DW_NB
+#define CO_DW_NB 2
+#endif
+constexpr int kNB = CO_DW_NB;           // K3 items per thread per batch (state loads in flight)
 constexpr size_t kHaloBudget = 72 * 1024;
 
 struct DwParams {
@@ -141,7 +144,10 @@ __device__ __forceinline__ void apply(const DwParams& p, int64_t b, int64_t pin,
 // The per-slice FMA order (u-major, then v) is k_step_direct's, so the two
 // kernels agree bitwise.
 template <int KT, int KH, int KW, int PX>
-__global__ void __launch_bounds__(256, 2) k_step_dw_st(const DwParams p) {
+#ifndef CO_DW_ST_MINB
+#define CO_DW_ST_MINB 2
+#endif
+__global__ void __launch_bounds__(256, CO_DW_ST_MINB) k_step_dw_st(const DwParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   float* ws = reinterpret_cast<float*>(smem);                       // [KT][KH][KW][C]
   float* bs = ws + KT * KH * KW * p.C;                              // [C]
@@ -229,8 +235,11 @@ __global__ void __launch_bounds__(256, 2) k_step_dw_st(const DwParams p) {
 }
 
 // ------------------------------------------------------------------ K3: temporal only
+#ifndef CO_DW_T_MINB
+#define CO_DW_T_MINB 3                  // K3 measured best at 2 items x 3 CTAs per SM; experiments: resident CTAs per SM the registers must allow
+#endif
 template <int KT>
-__global__ void __launch_bounds__(kDwThreads) k_step_dw_t(const DwParams p) {
+__global__ void __launch_bounds__(kDwThreads, CO_DW_T_MINB) k_step_dw_t(const DwParams p) {
   const int64_t n_items = p.plane * p.Cq;
   const int64_t stride = int64_t(gridDim.x) * kDwThreads;
   for (int64_t base = int64_t(blockIdx.x) * kDwThreads + threadIdx.x; base < n_items; base += kNB * stride) {
