@@ -61,7 +61,9 @@ namespace co {
 namespace {
 
 constexpr int kMaxStages = 6;   // operand pipeline depth: as many as fit in shared memory
-__host__ __device__ constexpr int tc_threads(int eg) { return 32 * (4 * eg + 2); }
+// EG epilogue groups of 4*CS warps (CS warps share a TMEM lane quadrant and split
+// its columns), then the producer and MMA warps
+__host__ __device__ constexpr int tc_threads(int eg, int cs = 1) { return 32 * (4 * eg * cs + 2); }
 constexpr int kApad = 512;        // slack after each A stage (junk rows may read past the box)
 enum { MODE_HALO = 0, MODE_FLAT = 1, MODE_KLOOP = 2 };
 
@@ -84,6 +86,8 @@ struct TcParams {
   int w_off;                      // stages start here (1 KB aligned)
   int slot[kMaxKt];
   int emit, update, act, out_f32;
+  int dbg;                        // CO_TC_DEBUG bits (experiments only): 1 no state/y traffic, 2 no MMA,
+                                  // 4 no A loads, 8 no TMEM reads, 16 (with 2) no accumulator handshakes
   int Cq;
   float* state;
   void* y;
@@ -105,8 +109,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 // at (kt-1) * CE / 4 float4 per thread); KH, KW, KC (= Cin / 16) > 0: compile-
 // time tap / K loops of the HALO / FLAT modes, fully unrolled, so the issuing
 // warp spends ~3 uniform instructions per tcgen05.mma.
-template <int KT, int CC, int EG, int CE, int KH = 0, int KW = 0, int KC = 0>
-__global__ void __launch_bounds__(tc_threads(EG), 1)
+template <int KT, int CC, int EG, int CE, int KH = 0, int KW = 0, int KC = 0, int CS = 1>
+__global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     k_step_dense_tc(const __grid_constant__ CUtensorMap tmap, const TcParams p) {
   constexpr int N = KT * CC;
   // TMEM accumulator ring: as many N-column buffers as 512 columns hold, at
@@ -115,7 +119,8 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
   constexpr int NBUF = (512 / BUF) < 8 ? (512 / BUF) : 8;
   static_assert(NBUF >= EG, "accumulator buffers exceed TMEM");
   constexpr int TMEM_COLS = 512;
-  constexpr int kProducer = 4 * EG, kMma = 4 * EG + 1;
+  constexpr int kProducer = 4 * EG * CS, kMma = 4 * EG * CS + 1;
+  static_assert(CC % (CS * CE) == 0, "channel split must tile CC");
   static_assert(N % 16 == 0 && N <= 256, "invalid UMMA N");
   static_assert(CC % CE == 0 && CE % 16 == 0, "CE must divide CC, multiple of 16");
 
@@ -143,7 +148,7 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
 
   if (warp == kProducer && lane == 0) {
     for (int s = 0; s < p.stages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
-    for (int e = 0; e < NBUF; ++e) { ptx::mbar_init(&acc_full[e], 1); ptx::mbar_init(&acc_empty[e], 128); }
+    for (int e = 0; e < NBUF; ++e) { ptx::mbar_init(&acc_full[e], 1); ptx::mbar_init(&acc_empty[e], 128 * CS); }
     ptx::mbar_init(w_full, 1);
     ptx::fence_mbar_init();
   }
@@ -169,6 +174,11 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
         }
         for (int64_t item = blockIdx.x; item < p.n_items; item += grid) {
           ptx::mbar_wait(&empty[s], ph ^ 1);
+          if (p.dbg & 4) {
+            ptx::mbar_arrive(&full[s]);
+            if (++s == p.stages) { s = 0; ph ^= 1; }
+            continue;
+          }
           ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes);
           const int64_t tile = item / p.n_split;
           uint8_t* dst = a_s + s * p.a_stride;
@@ -225,14 +235,14 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
       const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_u32(w_s), N * 16, 128);
       const int kc2 = p.Cin / 16;                       // MMAs (K = 16) per spatial tap
       for (int64_t item = blockIdx.x; item < p.n_items; item += grid) {
-        ptx::mbar_wait(&acc_empty[e], eph ^ 1);
+        if (!(p.dbg & 16)) ptx::mbar_wait(&acc_empty[e], eph ^ 1);
         ptx::tc_fence_after();
         ptx::mbar_wait(&full[s], ph);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem + uint32_t(e * BUF);
         const uint64_t a_desc0 = ptx::smem_desc(a_base + uint32_t(s * p.a_stride), p.chunk_stride, 128);
         if constexpr (KH > 0) {
-          if (ptx::elect_one()) {
+          if (!(p.dbg & 2) && ptx::elect_one()) {
 #pragma unroll
             for (int u = 0; u < KH; ++u)
 #pragma unroll
@@ -300,15 +310,17 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
       }
     }
     __syncwarp();
-    bar_sync_named(1, 32 + 128 * EG);
+    bar_sync_named(1, 32 + 128 * EG * CS);
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, TMEM_COLS);
     return;
   }
 
   // ===================== epilogue warpgroups (warps 0 .. 4 EG - 1) =====================
-  const int e = warp >> 2;                             // group
+  const int e = warp / (4 * CS);                       // group
   const int q = warp & 3;                              // TMEM lane quadrant of this warp
+  const int cs = (warp >> 2) % CS;                     // column share of this warp
+  constexpr int CPW = CC / CS;                         // output channels per warp
   const int m = q * 32 + lane;                         // accumulator row = tile pixel
   const int64_t plane = p.plane;
   constexpr int NQ = CE / 4;                           // channel quads per thread and pass
@@ -342,10 +354,10 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
     }
     const uint32_t t_row = tmem + (uint32_t(q * 32) << 16) + uint32_t(buf * BUF);
 #pragma unroll 1
-    for (int cb = 0; cb < CC; cb += CE) {
+    for (int cb = cs * CPW; cb < (cs + 1) * CPW; cb += CE) {
       // ---- prefetch the state this pass needs (pass 0: before the accumulator is ready)
       float4 sv[NS][NQ];
-      if (KT > 1 && valid) {
+      if (KT > 1 && valid && !(p.dbg & 1)) {
         if (p.emit) {
           const float4* src = reinterpret_cast<const float4*>(p.state) +
                               (int64_t(p.slot[KT - 1]) * p.Cq + (c0 + cb) / 4) * plane + pix;
@@ -363,7 +375,7 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
           }
         }
       }
-      if (cb == 0) {
+      if (cb == cs * CPW && !(p.dbg & 16)) {
         ptx::mbar_wait(&acc_full[buf], bph);
         ptx::tc_fence_after();
       }
@@ -372,18 +384,22 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
       if (p.emit) {
 #pragma unroll
         for (int c = 0; c < CE; c += 16) {
-          ptx::tmem_ld16(t_row + uint32_t((KT - 1) * CC + cb + c), v);
+          if (!(p.dbg & 8)) ptx::tmem_ld16(t_row + uint32_t((KT - 1) * CC + cb + c), v);
           ptx::tc_wait_ld();
-          if (valid) {
+          if (valid && !(p.dbg & 1)) {
+            // y = (P + S) + b, the activation only behind a uniform branch
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              float sacc = 0.f;
+            for (int i = 0; i < 16; i += 4) {
+              const float4 bb = *reinterpret_cast<const float4*>(bias_s + cb + c + i);
               if (KT > 1) {
                 const float4 t4 = sv[0][(c + i) >> 2];
-                sacc = ((i & 3) == 0) ? t4.x : ((i & 3) == 1) ? t4.y : ((i & 3) == 2) ? t4.z : t4.w;
+                v[i] += t4.x; v[i + 1] += t4.y; v[i + 2] += t4.z; v[i + 3] += t4.w;
               }
-              float r = v[i] + sacc + bias_s[cb + c + i];
-              v[i] = (p.act == 1 && r < 0.f) ? 0.f : r;
+              v[i] += bb.x; v[i + 1] += bb.y; v[i + 2] += bb.z; v[i + 3] += bb.w;
+            }
+            if (p.act == 1) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
             }
             const int64_t yoff = b * p.y_bstride + (pix - b * p.HWo) * p.Cout + c0 + cb + c;
             if (p.out_f32) {
@@ -408,9 +424,9 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
           float4* dst = reinterpret_cast<float4*>(p.state) + (int64_t(p.slot[k]) * p.Cq + (c0 + cb) / 4) * plane + pix;
 #pragma unroll
           for (int c = 0; c < CE; c += 16) {
-            ptx::tmem_ld16(t_row + uint32_t(k * CC + cb + c), v);
+            if (!(p.dbg & 8)) ptx::tmem_ld16(t_row + uint32_t(k * CC + cb + c), v);
             ptx::tc_wait_ld();
-            if (valid) {
+            if (valid && !(p.dbg & 1)) {
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 float4 t4 = sv[k][c / 4 + i];
@@ -425,9 +441,9 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
           float4* dst = reinterpret_cast<float4*>(p.state) + (int64_t(p.slot[0]) * p.Cq + (c0 + cb) / 4) * plane + pix;
 #pragma unroll
           for (int c = 0; c < CE; c += 16) {
-            ptx::tmem_ld16(t_row + uint32_t(cb + c), v);
+            if (!(p.dbg & 8)) ptx::tmem_ld16(t_row + uint32_t(cb + c), v);
             ptx::tc_wait_ld();
-            if (valid) {
+            if (valid && !(p.dbg & 1)) {
 #pragma unroll
               for (int i = 0; i < 4; ++i)
                 __stcs(dst + int64_t(c / 4 + i) * plane, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
@@ -439,7 +455,7 @@ __global__ void __launch_bounds__(tc_threads(EG), 1)
     ptx::tc_fence_before();
     ptx::mbar_arrive(&acc_empty[buf]);
   }
-  bar_sync_named(1, 32 + 128 * EG);
+  bar_sync_named(1, 32 + 128 * EG * CS);
 }
 
 // ------------------------------------------------------------------ host side
@@ -520,12 +536,16 @@ struct Variant {
   int KT, CC, EG, CE;
   KernFn fn;
   int KH = 0, KW = 0, KC = 0;     // > 0: specialised (unrolled) HALO/FLAT variant for this kernel / Cin
+  int CS = 1;                     // epilogue warps per TMEM lane quadrant (column split)
 };
 
 #define CO_TC_VARIANT(kt, cc, eg, ce) {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce>}
 #define CO_TC_SPEC(kt, cc, eg, ce, kh, kw, kc) \
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, kh, kw, kc>, kh, kw, kc}
+#define CO_TC_SPLIT(kt, cc, eg, ce, kh, kw, kc, cs) \
+  {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, kh, kw, kc, cs>, kh, kw, kc, cs}
 const Variant kVariants[] = {
+    CO_TC_SPLIT(3, 32, 2, 16, 3, 3, 4, 2), CO_TC_SPLIT(3, 32, 3, 16, 3, 3, 4, 2),
     CO_TC_SPEC(3, 32, 2, 32, 3, 3, 4), CO_TC_SPEC(3, 32, 3, 32, 3, 3, 4), CO_TC_SPEC(9, 16, 2, 16, 1, 1, 16),
     CO_TC_VARIANT(1, 32, 4, 32), CO_TC_VARIANT(1, 64, 4, 32), CO_TC_VARIANT(1, 128, 2, 32),
     CO_TC_VARIANT(2, 32, 4, 32), CO_TC_VARIANT(2, 64, 2, 32), CO_TC_VARIANT(3, 16, 4, 16),
@@ -561,6 +581,11 @@ struct Plan {
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
+int pinned_cs() {
+  const char* v = getenv("CO_TC_CS");           // A/B runs only
+  return v ? atoi(v) : 1;
+}
+
 int pinned_eg() {
   const char* eg_env = getenv("CO_TC_EG");      // A/B runs only
   return eg_env ? atoi(eg_env) : 0;
@@ -588,6 +613,7 @@ bool plan_resident(const Geom& g, Plan& pl) {
     if (v.KT != g.kt || g.Cout % v.CC != 0) continue;
     if (v.KH && (v.KH != g.kh || v.KW != g.kw || v.KC * 16 != g.Cin)) continue;
     if (eg_pin && v.EG != eg_pin) continue;
+    if (v.CS != pinned_cs()) continue;
     const int64_t w_bytes = int64_t(v.KT * v.CC) * K * 2;
     const size_t fixed = 1024 + size_t((w_bytes + 1023) / 1024 * 1024) + 512 + v.CC * 4;
     if (fixed + 2 * size_t(a_stride) > kSmemLimit) continue;
@@ -630,7 +656,7 @@ bool plan_kloop(const Geom& g, Plan& pl) {
   const int eg_pin = pinned_eg();
   const Variant* best = nullptr;
   for (const Variant& v : kVariants) {
-    if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH) continue;
+    if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.CS != 1) continue;
     if (eg_pin && v.EG != eg_pin) continue;
     // prefer the widest N (fewest A re-reads), then more groups
     auto rank = [](const Variant* x) { return x->CC * 1000 + x->EG; };
@@ -727,8 +753,8 @@ DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
   char buf[128];
   const char* mname = pl.mode == MODE_KLOOP ? (pl.wcols ? ",kloop+wcols" : ",kloop") : "";
   if (pl.var->KH)
-    snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d,%dx%dx%d%s>", pl.var->KT, pl.var->CC, pl.var->EG,
-             pl.var->KH, pl.var->KW, pl.var->KC * 16, mname);
+    snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d,%dx%dx%d%s%s>", pl.var->KT, pl.var->CC, pl.var->EG,
+             pl.var->KH, pl.var->KW, pl.var->KC * 16, pl.var->CS > 1 ? ",split" : "", mname);
   else
     snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d%s>", pl.var->KT, pl.var->CC, pl.var->EG, mname);
   if (getenv("CO_LOG"))
@@ -828,6 +854,8 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   p.w_bytes = pl.w_bytes; p.w_off = pl.w_off;
   for (int i = 0; i < kMaxKt; ++i) p.slot[i] = a.slot[i];
   p.emit = a.emit; p.update = a.update; p.act = g.act; p.out_f32 = (g.out_dtype == F32);
+  static const int dbg = getenv("CO_TC_DEBUG") ? atoi(getenv("CO_TC_DEBUG")) : 0;
+  p.dbg = dbg;
   p.Cq = g.Cq;
   p.state = a.state;
   p.y = a.y;
@@ -838,7 +866,7 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   const int64_t grid = std::min<int64_t>(per, pl.n_tiles) * pl.n_split;
   void* args[] = {&map, &p};
   return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->fn), dim3(unsigned(grid)),
-                          dim3(tc_threads(pl.var->EG)), args, pl.smem, s);
+                          dim3(tc_threads(pl.var->EG, pl.var->CS)), args, pl.smem, s);
 }
 
 }  // namespace co

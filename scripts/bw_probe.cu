@@ -18,7 +18,7 @@ constexpr long long PLANE = B * HW;                 // pixels
 constexpr int CQ = C / 4;
 
 template <int NI>
-__global__ void k_quadmajor(float4* __restrict__ st, __nv_bfloat16* __restrict__ y, long long n_items) {
+__global__ void k_quadmajor(float4* __restrict__ st, __nv_bfloat16* __restrict__ y, long long n_items, int work) {
   // item = (tile of 128 pixels, channel half); thread = pixel row of the tile
   const int row = threadIdx.x & 127;
   const int sub = threadIdx.x >> 7;                 // several items per block
@@ -45,6 +45,10 @@ __global__ void k_quadmajor(float4* __restrict__ st, __nv_bfloat16* __restrict__
       const int q0 = (int)(it & 1) * 8;
       if (pix >= PLANE) continue;
       uint4 yv[4];
+      // synthetic per-item ALU work (dependent chain), folded into the stored values
+      float z = a[j][0][0].x;
+      for (int w = 0; w < work; ++w) z = fmaf(z, 0.999f, 1e-7f);
+      a[j][0][0].x = z;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         float4 v0 = a[j][0][q], v1 = a[j][1][q];
@@ -99,6 +103,7 @@ __global__ void k_copy(const float4* __restrict__ a, float4* __restrict__ b, lon
 
 int main(int argc, char** argv) {
   const int mode = atoi(argv[1]), threads = atoi(argv[2]), bps = atoi(argv[3]), ni = atoi(argv[4]);
+  const int work = argc > 5 ? atoi(argv[5]) : 0;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const long long st_elems = R * C * PLANE;         // floats
@@ -117,8 +122,8 @@ int main(int argc, char** argv) {
   auto launch = [&]() {
     if (mode == 0) {
       const long long n_items = (PLANE + 127) / 128 * 2;
-      if (ni == 1) k_quadmajor<1><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items);
-      else k_quadmajor<2><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items);
+      if (ni == 1) k_quadmajor<1><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items, work);
+      else k_quadmajor<2><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items, work);
     } else if (mode == 1) {
       const long long n = PLANE * CQ;
       if (ni == 1) k_chlast<1><<<grid, threads>>>(st, (uint2*)y, n);
@@ -140,7 +145,7 @@ int main(int argc, char** argv) {
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   const cudaError_t err = cudaGetLastError();
-  printf("mode %d threads %d blocks/SM %d NI %d: %.1f us/launch, %.1f GB/s %s\n", mode, threads, bps, ni,
+  printf("mode %d threads %d blocks/SM %d NI %d work %d: %.1f us/launch, %.1f GB/s %s\n", mode, threads, bps, ni, work,
          ms * 1e3 / reps, bytes_rw / (ms / reps * 1e-3) / 1e9, err == cudaSuccess ? "" : cudaGetErrorString(err));
   return 0;
 }
