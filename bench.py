@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--kernel", default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     return ap.parse_args()
 
 
@@ -323,31 +323,34 @@ def run_co(args, world, rank):
 
 
 def run_e2e(args, convs, pool, cfg, B, world):
-    """Same metric through the public host-buffer C-ABI call (co_forward_step_host
-    / co_stack_step_host): H2D of the frame from pinned memory, the tick, D2H of
-    the output, every step."""
+    """Same metric through the public host-buffer C-ABI streaming call
+    (co_forward_steps_host / co_stack_steps_host): every step copies its frame
+    H2D from pinned memory and its output D2H, overlapped with the neighbouring
+    steps' compute; timed on the host around the (synchronising) call."""
     import torch
     import paper_2204_03418_b200 as co
-    K = args.e2e_steps
+    from paper_2204_03418_b200 import shard as sh
     last = convs[-1]
     stack = co.Stack(convs) if len(convs) > 1 else None
-    fn = stack.forward_step_host if stack else last.forward_step_host
-    xh = [p.movedim(1, -1).contiguous().cpu().pin_memory() for p in pool[:2]]
-    yh = torch.empty((B,) + tuple(last.out_spatial) + (last.out_channels,), dtype=last.out_dtype).pin_memory()
-    for i in range(2):
-        fn(xh[i % 2], yh)
-    torch.cuda.synchronize()
-    barrier()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
+    target = stack or last
+    frame = pool[0].movedim(1, -1).contiguous()
+    fbytes = frame.numel() * frame.element_size()
+    K = max(4, min(args.e2e_steps, (2 << 30) // fbytes))
+    xh = torch.empty((K,) + tuple(frame.shape), dtype=frame.dtype).pin_memory()
     for k in range(K):
-        assert fn(xh[k % 2], yh)
-    e.record()
+        xh[k].copy_(pool[k % len(pool)].movedim(1, -1))
+    yh = torch.empty((K, B) + tuple(last.out_spatial) + (last.out_channels,), dtype=last.out_dtype).pin_memory()
+    target.forward_steps_host(xh[:2], yh)            # warm-up (allocates the staging buffers)
     torch.cuda.synchronize()
-    from paper_2204_03418_b200 import shard as sh
-    red = sh.reduce_counters(stream_steps=B * K, elapsed_ms=s.elapsed_time(e))
-    return {"value": round(red["throughput"], 1), "unit": UNIT, "h2d_bytes_per_step": int(xh[0].numel() * xh[0].element_size()),
-            "d2h_bytes_per_step": int(yh.numel() * yh.element_size()), "steps": K}
+    sh.barrier()
+    t0 = time.perf_counter()
+    n, _ = target.forward_steps_host(xh, yh)
+    dt = time.perf_counter() - t0
+    assert n == K                                    # delay already filled by the timed run
+    red = sh.reduce_counters(stream_steps=B * K, elapsed_ms=dt * 1e3)
+    return {"value": round(red["throughput"], 1), "unit": UNIT, "h2d_bytes_per_step": int(fbytes),
+            "d2h_bytes_per_step": int(yh[0].numel() * yh.element_size()), "steps": K,
+            "api": "co_stack_steps_host" if stack else "co_forward_steps_host"}
 
 
 def oracle_machine(cfg, n_streams):

@@ -134,6 +134,17 @@ int co_forward_step(co_conv* h, const void* x, void* y, int update_state, int* r
 int co_forward_step_host(co_conv* h, const void* x_host, void* y_host, int update_state, int* ready,
                          co_stream stream);
 
+/* Streaming with HOST buffers: T frames, TIME-major on the host, x_host
+ * (T, B, S1, S2, Cin) pinned memory (frame t of all streams contiguous, the
+ * order frames arrive in online inference); the Ready outputs are written
+ * compacted to y_host (n_ready, B, S1', S2', Cout).  The H2D copy of frame t+1
+ * and the D2H copy of output t-1 overlap step t (double-buffered device
+ * staging, two extra internal streams); state updates as co_forward_step with
+ * update_state = 1.  Synchronises `stream` before returning: y_host, ready_mask
+ * (host, may be NULL, T flags) and *n_ready are final on return. */
+int co_forward_steps_host(co_conv* h, const void* x_host, int64_t T, void* y_host, uint8_t* ready_mask,
+                          int64_t* n_ready, co_stream stream);
+
 /* forward_steps: the fold of co_forward_step over the T columns of the
  * clip x (B, T, S1, S2, Cin), then p zero steps if pad_end.  y receives
  * the Ready outputs compacted in time (A1): (B, n_ready, S1', S2', Cout); its
@@ -182,6 +193,10 @@ int co_stack_step(co_stack* st, const void* x, void* y, int update_state, int* r
  * `stream`; y_host is valid on return. */
 int co_stack_step_host(co_stack* st, const void* x_host, void* y_host, int update_state, int* ready,
                        co_stream stream);
+/* co_forward_steps_host for a stack: time-major host frames of layer 0 in, the
+ * last layer's Ready outputs (compacted) out, copies overlapped with the ticks. */
+int co_stack_steps_host(co_stack* st, const void* x_host, int64_t T, void* y_host, uint8_t* ready_mask,
+                        int64_t* n_ready, co_stream stream);
 /* Accumulated delay d_NN (Principle 6 in the worked-example reading, A3). */
 int co_stack_delay(const co_stack* st, int64_t* d_nn);
 int co_stack_clean(co_stack* st, co_stream stream);

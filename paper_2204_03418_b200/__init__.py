@@ -59,6 +59,16 @@ def _tup(v, n=3, fill=1):
     return v + (fill,) * (n - len(v))
 
 
+def _steps_host(fn, handle, x_host: torch.Tensor, y_host: torch.Tensor, stream):
+    """x_host: (T, B, *S, Cin) pinned, time-major; y_host: (>= n_ready, B, *S', Cout) pinned."""
+    T = x_host.shape[0]
+    mask = (C.c_uint8 * max(T, 1))()
+    nr = C.c_int64()
+    check(fn(handle, C.c_void_p(x_host.data_ptr()), T, C.c_void_p(y_host.data_ptr()), mask, C.byref(nr),
+             _stream(stream)))
+    return nr.value, torch.tensor([bool(m) for m in mask[:T]], dtype=torch.bool)
+
+
 class Conv:
     """A continual convolution layer over ``n_streams`` lockstep streams.
 
@@ -216,7 +226,12 @@ class Conv:
     def head(self) -> int:
         return self.info().head
 
-    # ---- host-buffer entry point (e2e) ----
+    # ---- host-buffer entry points (e2e) ----
+    def forward_steps_host(self, x_host: torch.Tensor, y_host: torch.Tensor, stream=None):
+        """Stream T time-major host frames through the layer with overlapped
+        copies (co_forward_steps_host).  Returns (n_ready, ready_mask)."""
+        return _steps_host(lib().co_forward_steps_host, self._h, x_host, y_host, stream)
+
     def forward_step_host(self, x_host: torch.Tensor, y_host: torch.Tensor, update_state: bool = True,
                           stream=None) -> bool:
         r = C.c_int()
@@ -268,6 +283,10 @@ class Stack:
         check(lib().co_stack_step_host(self._h, C.c_void_p(x_host.data_ptr()), C.c_void_p(y_host.data_ptr()),
                                        int(update_state), C.byref(r), _stream(stream)))
         return bool(r.value)
+
+    def forward_steps_host(self, x_host: torch.Tensor, y_host: torch.Tensor, stream=None):
+        """co_stack_steps_host: (n_ready, ready_mask)."""
+        return _steps_host(lib().co_stack_steps_host, self._h, x_host, y_host, stream)
 
     def clean_state(self, stream=None):
         check(lib().co_stack_clean(self._h, _stream(stream)))

@@ -24,9 +24,9 @@ KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 
 # every entry point include/co.h declares (checked by tests/test_abi_load.py)
 EXPORTS = ["co_conv_create", "co_conv_destroy", "co_conv_info", "co_delay", "co_kernel_name",
-           "co_forward_step", "co_forward_step_host", "co_forward_steps", "co_steps_ready_count",
+           "co_forward_step", "co_forward_step_host", "co_forward_steps_host", "co_forward_steps", "co_steps_ready_count",
            "co_forward", "co_forward_out_len", "co_state_bytes", "co_state_get", "co_state_set",
-           "co_state_clean", "co_stack_create", "co_stack_destroy", "co_stack_step", "co_stack_step_host", "co_stack_delay",
+           "co_state_clean", "co_stack_create", "co_stack_destroy", "co_stack_step", "co_stack_step_host", "co_stack_steps_host", "co_stack_delay",
            "co_stack_clean", "co_last_error", "co_abi_version"]
 
 
@@ -71,6 +71,8 @@ def lib():
             L.co_kernel_name.restype = C.c_char_p
             L.co_forward_step.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_int), vp]
             L.co_forward_step_host.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_int), vp]
+            L.co_forward_steps_host.argtypes = [vp, vp, C.c_int64, vp, C.POINTER(C.c_uint8), i64p, vp]
+            L.co_stack_steps_host.argtypes = [vp, vp, C.c_int64, vp, C.POINTER(C.c_uint8), i64p, vp]
             L.co_forward_steps.argtypes = [vp, vp, C.c_int64, vp, C.POINTER(C.c_uint8), i64p, C.c_int, C.c_int, vp]
             L.co_steps_ready_count.argtypes = [vp, C.c_int64, C.c_int, i64p]
             L.co_forward.argtypes = [vp, vp, C.c_int64, vp, i64p, vp]

@@ -59,6 +59,46 @@ static inline size_t dsize(int dt) { return dt == co::F32 ? 4 : 2; }
 
 // ----------------------------------------------------------------- handle
 
+// Double-buffered H2D -> step -> D2H pipeline for the *_steps_host entry points:
+// frame t+1 is copied in and output t-1 copied out while step t computes.
+struct HostPipe {
+  void* x[2] = {nullptr, nullptr};
+  void* y[2] = {nullptr, nullptr};
+  size_t xb = 0, yb = 0;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
+  bool ok = false;
+};
+
+static void pipe_free(HostPipe& P) {
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(P.x[i]); cudaFree(P.y[i]);
+    if (P.in_done[i]) cudaEventDestroy(P.in_done[i]);
+    if (P.comp_done[i]) cudaEventDestroy(P.comp_done[i]);
+    if (P.out_done[i]) cudaEventDestroy(P.out_done[i]);
+  }
+  if (P.s_in) cudaStreamDestroy(P.s_in);
+  if (P.s_out) cudaStreamDestroy(P.s_out);
+  P = HostPipe{};
+}
+
+static cudaError_t pipe_init(HostPipe& P, size_t xb, size_t yb) {
+  if (P.ok && P.xb == xb && P.yb == yb) return cudaSuccess;
+  pipe_free(P);
+  cudaError_t e;
+  for (int i = 0; i < 2; ++i) {
+    if ((e = cudaMalloc(&P.x[i], xb)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&P.y[i], yb)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&P.in_done[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&P.comp_done[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&P.out_done[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+  }
+  if ((e = cudaStreamCreateWithFlags(&P.s_in, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithFlags(&P.s_out, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  P.xb = xb; P.yb = yb; P.ok = true;
+  return cudaSuccess;
+}
+
 struct co_conv {
   co_conv_desc desc;
   Geom g;
@@ -72,6 +112,7 @@ struct co_conv {
   co::Depthwise* dw = nullptr; // depthwise resources
   void* hx = nullptr;          // staging for *_host
   void* hy = nullptr;
+  HostPipe pipe;               // staging for co_forward_steps_host
 };
 
 struct co_stack {
@@ -79,6 +120,7 @@ struct co_stack {
   std::vector<void*> act;      // inter-layer activations (one per layer but the last)
   void* hx = nullptr;          // staging for co_stack_step_host
   void* hy = nullptr;
+  HostPipe pipe;               // staging for co_stack_steps_host
 };
 
 static int make_geom(const co_conv_desc* d, Geom& g) {
@@ -242,6 +284,7 @@ extern "C" int co_conv_destroy(co_conv* h) {
   cudaFree(h->state);
   cudaFree(h->hx);
   cudaFree(h->hy);
+  pipe_free(h->pipe);
   delete h;
   return CO_OK;
 }
@@ -327,6 +370,58 @@ extern "C" int co_forward_step_host(co_conv* h, const void* x_host, void* y_host
   CO_CUDA(cudaStreamSynchronize(s));
   if (ready) *ready = r;
   return CO_OK;
+}
+
+// The pipelined host loop shared by co_forward_steps_host / co_stack_steps_host.
+// `tick(x_dev, y_dev, &ready, stream)` runs one step; frames are time-major on
+// the host.  Output r (the r-th Ready tick) lands at y_host + r * yb.
+template <typename Tick>
+static int run_steps_host(HostPipe& P, const void* x_host, int64_t T, void* y_host, size_t xb, size_t yb,
+                          uint8_t* ready_mask, int64_t* n_ready, cudaStream_t s, Tick tick) {
+  if (cudaError_t e = pipe_init(P, xb, yb)) return fail(e == cudaErrorMemoryAllocation ? CO_ERR_OOM : CO_ERR_CUDA,
+                                                         "host pipeline: %s", cudaGetErrorString(e));
+  int64_t r = 0;
+  for (int64_t t = 0; t < T; ++t) {
+    const int b = int(t & 1);
+    // x[b] may be overwritten once step t-2 has consumed it
+    if (t >= 2) CO_CUDA(cudaStreamWaitEvent(P.s_in, P.comp_done[b], 0));
+    CO_CUDA(cudaMemcpyAsync(P.x[b], static_cast<const char*>(x_host) + size_t(t) * xb, xb, cudaMemcpyHostToDevice,
+                            P.s_in));
+    CO_CUDA(cudaEventRecord(P.in_done[b], P.s_in));
+    CO_CUDA(cudaStreamWaitEvent(s, P.in_done[b], 0));
+    if (t >= 2) CO_CUDA(cudaStreamWaitEvent(s, P.out_done[b], 0));   // y[b] copied out
+    int rd = 0;
+    if (int rc = tick(P.x[b], P.y[b], &rd, s)) return rc;
+    CO_CUDA(cudaEventRecord(P.comp_done[b], s));
+    if (rd) {
+      CO_CUDA(cudaStreamWaitEvent(P.s_out, P.comp_done[b], 0));
+      CO_CUDA(cudaMemcpyAsync(static_cast<char*>(y_host) + size_t(r) * yb, P.y[b], yb, cudaMemcpyDeviceToHost,
+                              P.s_out));
+      ++r;
+    }
+    CO_CUDA(cudaEventRecord(P.out_done[b], P.s_out));
+    if (ready_mask) ready_mask[t] = uint8_t(rd);
+  }
+  CO_CUDA(cudaStreamSynchronize(P.s_out));
+  CO_CUDA(cudaStreamSynchronize(s));
+  if (n_ready) *n_ready = r;
+  return CO_OK;
+}
+
+extern "C" int co_forward_steps_host(co_conv* h, const void* x_host, int64_t T, void* y_host, uint8_t* ready_mask,
+                                     int64_t* n_ready, co_stream stream) {
+  if (!h || (!x_host && T > 0) || T < 0) return fail(CO_ERR_ARG, "bad argument");
+  const Geom& g = h->g;
+  int64_t cap = 0;
+  co_steps_ready_count(h, T, 0, &cap);
+  if (cap > 0 && !y_host) return fail(CO_ERR_ARG, "null y_host");
+  const size_t xb = size_t(g.B) * g.H * g.W * g.Cin * dsize(g.in_dtype);
+  const size_t yb = size_t(g.B) * g.HWo * g.Cout * dsize(g.out_dtype);
+  return run_steps_host(h->pipe, x_host, T, y_host, xb, yb, ready_mask, n_ready, (cudaStream_t)stream,
+                        [&](const void* x, void* y, int* rd, cudaStream_t s) {
+                          return step_impl(h, h->n, h->state, x, int64_t(g.H) * g.W * g.Cin, y, g.HWo * g.Cout, 1,
+                                           rd, s);
+                        });
 }
 
 extern "C" int co_steps_ready_count(const co_conv* h, int64_t T, int pad_end, int64_t* n_ready) {
@@ -482,6 +577,7 @@ extern "C" int co_stack_destroy(co_stack* st) {
   if (!st) return CO_OK;
   for (void* p : st->act) cudaFree(p);
   cudaFree(st->hx);
+  pipe_free(st->pipe);
   cudaFree(st->hy);
   delete st;
   return CO_OK;
@@ -522,6 +618,19 @@ extern "C" int co_stack_step_host(co_stack* st, const void* x_host, void* y_host
   CO_CUDA(cudaStreamSynchronize(s));
   if (ready) *ready = r;
   return CO_OK;
+}
+
+extern "C" int co_stack_steps_host(co_stack* st, const void* x_host, int64_t T, void* y_host, uint8_t* ready_mask,
+                                   int64_t* n_ready, co_stream stream) {
+  if (!st || (!x_host && T > 0) || T < 0 || !y_host) return fail(CO_ERR_ARG, "bad argument");
+  const Geom& g0 = st->layers.front()->g;
+  const Geom& gl = st->layers.back()->g;
+  const size_t xb = size_t(g0.B) * g0.H * g0.W * g0.Cin * dsize(g0.in_dtype);
+  const size_t yb = size_t(gl.B) * gl.HWo * gl.Cout * dsize(gl.out_dtype);
+  return run_steps_host(st->pipe, x_host, T, y_host, xb, yb, ready_mask, n_ready, (cudaStream_t)stream,
+                        [&](const void* x, void* y, int* rd, cudaStream_t s) {
+                          return co_stack_step(st, x, y, 1, rd, (co_stream)s);
+                        });
 }
 
 extern "C" int co_stack_delay(const co_stack* st, int64_t* d_nn) {

@@ -35,6 +35,11 @@ CASES = {
     # small-Cin stems: W-im2col'd frame (C4 layer 1 shaped), KLOOP (stride 2) and HALO (stride 1)
     "stem_c4like": dict(desc=O.Desc(2, 3, 32, (5, 7, 7), stride=(1, 2, 2), padding=(0, 3, 3), in_spatial=(20, 22)), B=2),
     "stem_halo": dict(desc=O.Desc(2, 3, 16, (3, 3, 3), padding=(1, 1, 1), in_spatial=(9, 10)), B=2),
+    # temporal stride > 1 (Principle 5): skipped ticks are Empty, only
+    # the slices feeding an emitted output touch the ring (A20)
+    "halo_st2": dict(desc=O.Desc(2, 32, 32, (3, 3, 3), stride=(2, 1, 1), padding=(1, 1, 1), in_spatial=(6, 7)), B=2),
+    "kloop_st3": dict(desc=O.Desc(2, 32, 32, (5, 3, 3), stride=(3, 2, 2), padding=(2, 1, 1), in_spatial=(9, 8)), B=2),
+    "flat_st2_dil2": dict(desc=O.Desc(1, 32, 32, (3, 1), stride=(2, 1), dilation=(2, 1), in_spatial=(25, 1)), B=3),
 }
 FORCE_KLOOP = {"halo_c2like", "halo_kt5", "flat_c5like"}   # also run these through the K pipeline
 
@@ -57,11 +62,11 @@ def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force
         os.environ.pop("CO_TC_MODE", None)
     ref_conv, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="direct")
     assert conv.kernel_used == "dense_tc", conv.kernel_name
-    if force_kloop or case.startswith("kloop") or case == "stem_c4like":
+    if force_kloop or case.startswith("kloop") or case == "stem_c4like":  # (kloop_st3: spatial stride 2)
         assert "kloop" in conv.kernel_name, conv.kernel_name
     H, Wd = d.in_hw
     shp = (B, d.cin) + ((H,) if d.spatial_rank >= 1 else ()) + ((Wd,) if d.spatial_rank >= 2 else ())
-    steps = steps or (d.receptive_field + 4)
+    steps = steps or (d.receptive_field + 4 + 3 * (d.stride[0] - 1))
     ys, refs, yds = [], [], []
     for t in range(steps):
         x = rng.integers(-2, 3, shp).astype(np.float64) if integer else rng.standard_normal(shp)
@@ -109,7 +114,7 @@ def test_dense_tc_bf16_output(case):
     assert_bf16_rounding_bound(y, ref)
 
 
-@pytest.mark.parametrize("case", ["halo_c2like", "flat_c5like", "kloop_s2", "stem_c4like"])
+@pytest.mark.parametrize("case", ["halo_c2like", "flat_c5like", "kloop_s2", "stem_c4like", "halo_st2", "kloop_st3"])
 def test_dense_tc_state_and_steps(case):
     """State get vs oracle O5, update_state=False purity, forward_steps fold."""
     d, B = CASES[case]["desc"], CASES[case]["B"]
@@ -133,7 +138,9 @@ def test_dense_tc_state_and_steps(case):
     y_peek = conv.forward_step(probe, update_state=False)
     st1, _ = conv.state_dict_stream()
     assert torch.equal(st, st1)
-    assert torch.equal(y_peek, conv.forward_step(probe))
+    y_real = conv.forward_step(probe)
+    assert (y_peek is None) == (y_real is None)      # an Empty tick under temporal stride stays Empty
+    assert y_peek is None or torch.equal(y_peek, y_real)
     clip = torch.stack([f for f in frames], dim=2)       # (B, C, T, *S), channels-last per frame
     from paper_2204_03418_b200 import channels_last
     ys, mask = conv2.forward_steps(channels_last(clip))

@@ -33,6 +33,11 @@ CASES = {
     "t_c3b": dict(desc=dw(192, (5, 1, 1), in_spatial=(28, 28)), B=2),
     "t_kt9_dil2": dict(desc=dw(64, (9, 1, 1), dilation=(2, 1, 1), in_spatial=(25, 1), rank=1), B=3),
     "t_kt3_pt2": dict(desc=dw(8, (3, 1, 1), (2, 0, 0), in_spatial=(3, 3)), B=5),
+    # temporal stride > 1 (Principle 5)
+    "st_st2": dict(desc=O.Desc(2, 16, 16, (3, 3, 3), stride=(2, 1, 1), padding=(1, 1, 1), groups=16,
+                               in_spatial=(7, 6)), B=2),
+    "t_st3": dict(desc=O.Desc(2, 24, 24, (5, 1, 1), stride=(3, 1, 1), padding=(2, 0, 0), groups=24,
+                              in_spatial=(4, 5)), B=2),
 }
 
 
@@ -56,7 +61,7 @@ def _run(case, integer=False, out_dtype=torch.float32, activation=None, seed=0, 
     ref_conv, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="direct",
                                   activation=activation)
     assert conv.kernel_used == "depthwise", conv.kernel_name
-    steps = steps or (d.receptive_field + 4)
+    steps = steps or (d.receptive_field + 4 + 3 * (d.stride[0] - 1))
     ys, refs, yds = [], [], []
     for t in range(steps):
         x = rng.integers(-2, 3, _shape(d, B)).astype(np.float64) if integer else rng.standard_normal(_shape(d, B))
@@ -97,7 +102,7 @@ def test_depthwise_bf16_output_and_relu(case):
     assert (y >= 0).all()
 
 
-@pytest.mark.parametrize("case", ["st_ragged", "t_kt9_dil2", "st_pt1"])
+@pytest.mark.parametrize("case", ["st_ragged", "t_kt9_dil2", "st_pt1", "st_st2", "t_st3"])
 def test_depthwise_state_steps_and_purity(case):
     """co_state_get vs oracle O5 (channels-last physical ring -> canonical
     layout), get->set round trip, update_state=False purity, forward_steps =
@@ -130,7 +135,8 @@ def test_depthwise_state_steps_and_purity(case):
     st1, m1 = conv.state_dict_stream()
     assert torch.equal(st, st1) and m1.n == meta.n
     y1, y2 = conv.forward_step(probe), conv2.forward_step(probe)
-    assert torch.equal(y_peek, y1) and torch.equal(y1, y2)
+    assert (y_peek is None) == (y1 is None) == (y2 is None)   # Empty ticks under temporal stride
+    assert y1 is None or (torch.equal(y_peek, y1) and torch.equal(y1, y2))
     # forward_steps (with pad_end) == fold of forward_step, and == batch forward
     clip = channels_last(torch.stack(frames, dim=2))
     c3, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="depthwise")

@@ -242,3 +242,40 @@ def test_error_codes():
     with pytest.raises(CoError) as e:
         c.load_state_stream(torch.zeros(2, 1, 4, 4, 4, device="cuda"), meta)
     assert e.value.code == CO_ERR_SHAPE
+
+
+@pytest.mark.parametrize("kernel", ["direct", "dense_tc"])
+def test_steps_host_pipeline_matches_device_fold(kernel):
+    """co_forward_steps_host (time-major pinned frames, copies overlapped with the
+    steps) == the fold of co_forward_step on device tensors, bitwise; ready mask
+    and clock identical; and the stack variant likewise."""
+    import paper_2204_03418_b200 as co
+    rng = np.random.default_rng(900)
+    d = O.Desc(2, 16, 32, (3, 3, 3), padding=(0, 1, 1), in_spatial=(6, 7))
+    dt = torch.bfloat16
+    W, b = rng.standard_normal(d.w_shape) / 12, rng.standard_normal(32) * 0.1
+    a, _, _, _ = make_pair(d, W, b, 3, dtype=dt, out_dtype=dt, kernel=kernel)
+    c, _, _, _ = make_pair(d, W, b, 3, dtype=dt, out_dtype=dt, kernel=kernel)
+    T = 7
+    frames = [to_cl(rng.standard_normal((3, 16, 6, 7)), dt) for _ in range(T)]
+    fold = [y for y in (a.forward_step(x) for x in frames) if y is not None]
+    xh = torch.stack([f.movedim(1, -1).contiguous().cpu() for f in frames]).pin_memory()   # (T, B, H, W, C)
+    yh = torch.zeros((T, 3, 6, 7, 32), dtype=dt).pin_memory()
+    n, mask = c.forward_steps_host(xh, yh)
+    assert n == len(fold) == int(mask.sum()) and mask.tolist() == [t >= 2 for t in range(T)]
+    for i, f in enumerate(fold):
+        assert torch.equal(yh[i], f.movedim(1, -1).cpu())
+    assert (c.n, c.head) == (a.n, a.head)
+    # stack of two layers
+    d2 = O.Desc(2, 32, 8, (2, 1, 1), in_spatial=(6, 7))
+    W2, b2 = rng.standard_normal(d2.w_shape) / 8, rng.standard_normal(8) * 0.1
+    a2, _, _, _ = make_pair(d2, W2, b2, 3, dtype=dt, out_dtype=dt)
+    c2, _, _, _ = make_pair(d2, W2, b2, 3, dtype=dt, out_dtype=dt)
+    a.clean_state(); c.clean_state()
+    sa, sc = co.Stack([a, a2]), co.Stack([c, c2])
+    fold = [y for y in (sa.forward_step(x) for x in frames) if y is not None]
+    yh2 = torch.zeros((T, 3, 6, 7, 8), dtype=dt).pin_memory()
+    n, mask = sc.forward_steps_host(xh, yh2)
+    assert n == len(fold) == 4
+    for i, f in enumerate(fold):
+        assert torch.equal(yh2[i], f.movedim(1, -1).cpu())
