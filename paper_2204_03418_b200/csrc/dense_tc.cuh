@@ -7,6 +7,9 @@
 namespace co {
 struct DenseTC;
 bool dense_tc_supported(const Geom& g);
+// Fill g's tile-padded state-row fields (spad, sTH, sTW, sRS, stiles_*, splane)
+// for the tiles the kernel's plan uses.
+void dense_tc_state_layout(Geom& g);
 DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err);
 void dense_tc_destroy(DenseTC* t);
 const char* dense_tc_name(const DenseTC* t);

@@ -172,7 +172,8 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
   g.R = int(ceil_div(g.f - 1, g.st));
   g.Cq = (g.Cout + 3) / 4;
   g.HWo = int64_t(g.Ho) * g.Wo;
-  g.slot_elems = int64_t(g.Cq) * 4 * g.B * g.HWo;
+  g.splane = g.B * g.HWo;
+  g.slot_elems = int64_t(g.Cq) * 4 * g.splane;
   return CO_OK;
 }
 
@@ -224,8 +225,13 @@ extern "C" int co_conv_create(const co_conv_desc* desc, const void* weights, con
   if (kern != CO_KERNEL_DIRECT && kern != CO_KERNEL_DENSE_TC && kern != CO_KERNEL_DEPTHWISE)
     return fail(CO_ERR_ARG, "bad kernel_choice");
 
-  // the depthwise kernels stream a channels-last state ring (common.cuh)
+  // the depthwise kernels stream a channels-last state ring, the dense tensor-core
+  // kernel a tile-padded quad-major one (common.cuh)
   g.state_cl = (kern == CO_KERNEL_DEPTHWISE) ? 1 : 0;
+  if (kern == CO_KERNEL_DENSE_TC) {
+    co::dense_tc_state_layout(g);
+    g.slot_elems = int64_t(g.Cq) * 4 * g.splane;
+  }
   co_conv* h = new (std::nothrow) co_conv();
   if (!h) return fail(CO_ERR_OOM, "host allocation");
   h->desc = *desc;

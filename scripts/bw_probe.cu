@@ -17,10 +17,15 @@ constexpr long long B = 256, HW = 3136, C = 64, R = 2;
 constexpr long long PLANE = B * HW;                 // pixels
 constexpr int CQ = C / 4;
 
-template <int NI>
+template <int NI, bool HALO, bool PAD = false>
 __global__ void k_quadmajor(float4* __restrict__ st, __nv_bfloat16* __restrict__ y, long long n_items, int work) {
-  // item = (tile of 128 pixels, channel half); thread = pixel row of the tile
-  const int row = threadIdx.x & 127;
+  // item = (tile of 128 pixels, channel half); thread = pixel row of the tile.
+  // HALO: the dense kernel's C2 tile shape -- 2 output rows of 56 in a 58-wide
+  // padded halo, rows m -> pixel (m/58)*56 + m%58, 112 valid of 128 lanes.
+  const int m = threadIdx.x & 127;
+  const int row = HALO ? (m / 58) * 56 + m % 58 : m;
+  const bool lane_ok = HALO ? (m % 58 < 56 && m < 116) : true;
+  const int TP = HALO ? 112 : 128;
   const int sub = threadIdx.x >> 7;                 // several items per block
   const int per_block = blockDim.x >> 7;
   for (long long it0 = (long long)blockIdx.x * per_block + sub; it0 < n_items; it0 += (long long)gridDim.x * per_block * NI) {
@@ -29,21 +34,21 @@ __global__ void k_quadmajor(float4* __restrict__ st, __nv_bfloat16* __restrict__
     for (int j = 0; j < NI; ++j) {
       const long long it = it0 + (long long)j * gridDim.x * per_block;
       if (it >= n_items) continue;
-      const long long pix = (it >> 1) * 128 + row;
+      const long long pix = (it >> 1) * TP + row;
       const int q0 = (int)(it & 1) * 8;
-      if (pix >= PLANE) continue;
+      if (pix >= PLANE || !lane_ok) continue;
 #pragma unroll
       for (int s = 0; s < 2; ++s)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) a[j][s][q] = __ldcs(st + ((long long)s * CQ + q0 + q) * PLANE + pix);
+        for (int q = 0; q < 8; ++q) a[j][s][q] = __ldcs(st + ((long long)s * CQ + q0 + q) * PLANE + (PAD ? (it >> 1) * 128 + m : pix));
     }
 #pragma unroll
     for (int j = 0; j < NI; ++j) {
       const long long it = it0 + (long long)j * gridDim.x * per_block;
       if (it >= n_items) continue;
-      const long long pix = (it >> 1) * 128 + row;
+      const long long pix = (it >> 1) * TP + row;
       const int q0 = (int)(it & 1) * 8;
-      if (pix >= PLANE) continue;
+      if (pix >= PLANE || !lane_ok) continue;
       uint4 yv[4];
       // synthetic per-item ALU work (dependent chain), folded into the stored values
       float z = a[j][0][0].x;
@@ -53,8 +58,9 @@ __global__ void k_quadmajor(float4* __restrict__ st, __nv_bfloat16* __restrict__
       for (int q = 0; q < 8; ++q) {
         float4 v0 = a[j][0][q], v1 = a[j][1][q];
         v0.x += 1.f; v1.y += 1.f;
-        __stcs(st + ((long long)0 * CQ + q0 + q) * PLANE + pix, v1);
-        __stcs(st + ((long long)1 * CQ + q0 + q) * PLANE + pix, v0);
+        const long long sp = PAD ? (it >> 1) * 128 + m : pix;
+        __stcs(st + ((long long)0 * CQ + q0 + q) * PLANE + sp, v1);
+        __stcs(st + ((long long)1 * CQ + q0 + q) * PLANE + sp, v0);
         reinterpret_cast<float*>(yv)[q] = v0.x + v1.x;
       }
       *reinterpret_cast<uint4*>(y + pix * C + q0 * 4) = yv[0];
@@ -122,8 +128,15 @@ int main(int argc, char** argv) {
   auto launch = [&]() {
     if (mode == 0) {
       const long long n_items = (PLANE + 127) / 128 * 2;
-      if (ni == 1) k_quadmajor<1><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items, work);
-      else k_quadmajor<2><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items, work);
+      if (ni == 1) k_quadmajor<1, false><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items, work);
+      else k_quadmajor<2, false><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items, work);
+    } else if (mode == 4) {
+      const long long n_items = (PLANE + 111) / 112 * 2 * 112 / 128 - 2;   // padded rows stay inside the buffer
+      k_quadmajor<1, true, true><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items, work);
+    } else if (mode == 3) {
+      const long long n_items = (PLANE + 111) / 112 * 2;
+      if (ni == 1) k_quadmajor<1, true><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items, work);
+      else k_quadmajor<2, true><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items, work);
     } else if (mode == 1) {
       const long long n = PLANE * CQ;
       if (ni == 1) k_chlast<1><<<grid, threads>>>(st, (uint2*)y, n);
