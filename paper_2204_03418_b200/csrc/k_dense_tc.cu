@@ -87,6 +87,8 @@ struct TcParams {
   int w_off;                      // stages start here (1 KB aligned)
   int slot[kMaxKt];
   int emit, update, act, out_f32;
+  int swa, a_rows;                // A staged swizzled: 0 none, 1 128-B rows ([Cin/64][rows][128 B]),
+                                  // 2 64-B rows (KLOOP with kb = 32); rows per 64-channel block
   int dbg;                        // CO_TC_DEBUG bits (experiments only): 1 no state/y traffic, 2 no MMA,
                                   // 4 no A loads, 8 no TMEM reads, 16 (with 2) no accumulator handshakes
   int Cq;
@@ -110,7 +112,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 // at (kt-1) * CE / 4 float4 per thread); KH, KW, KC (= Cin / 16) > 0: compile-
 // time tap / K loops of the HALO / FLAT modes, fully unrolled, so the issuing
 // warp spends ~3 uniform instructions per tcgen05.mma.
-template <int KT, int CC, int EG, int CE, int KH = 0, int KW = 0, int KC = 0, int CS = 1>
+template <int KT, int CC, int EG, int CE, int KH = 0, int KW = 0, int KC = 0, int CS = 1, int PAIR = 1>
 __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     k_step_dense_tc(const __grid_constant__ CUtensorMap tmap, const TcParams p) {
   constexpr int N = KT * CC;
@@ -137,26 +139,41 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   uint64_t* acc_full = bars + 2 * kMaxStages;           // [NBUF]
   uint64_t* acc_empty = bars + 2 * kMaxStages + NBUF;   // [NBUF]
   uint64_t* w_full = bars + 2 * kMaxStages + 2 * NBUF;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 2 * NBUF + 1);
-  float* bias_s = reinterpret_cast<float*>(bars + 2 * kMaxStages + 2 * NBUF + 2);
+  uint64_t* w_peer = bars + 2 * kMaxStages + 2 * NBUF + 1;   // PAIR: the peer's weight half landed
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 2 * NBUF + 2);
+  // 16-byte aligned: the epilogue reads the bias as float4
+  float* bias_s = reinterpret_cast<float*>(bars + ((2 * kMaxStages + 2 * NBUF + 3 + 1) & ~1));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int grid = gridDim.x;
-  const int part = blockIdx.x % p.n_split;
+  // CTA pairs (cta_group::2, PAIR == 2): the cluster's two CTAs share one M = 256
+  // MMA issued by the leader; each holds the A rows of its own 128-row tile and
+  // half (N/2 rows) of the part's weights, so per-CTA weight shared memory halves.
+  const uint32_t rank = (PAIR == 2) ? ptx::cluster_ctarank() : 0u;
+  const bool leader = (rank == 0);
+  const int unit = blockIdx.x / PAIR;                   // work unit: a CTA or a CTA pair
+  const int n_units = grid / PAIR;
+  const int part = unit % p.n_split;
   const int c0 = part * CC;                             // first output channel of this part
   const bool kloop = (p.mode == MODE_KLOOP);
+  constexpr int NB = N / PAIR;                          // weight rows held by this CTA
+  auto tile_of = [&](int64_t item) -> int64_t { return (item / p.n_split) * PAIR + rank; };
 
   if (warp == kProducer && lane == 0) {
     for (int s = 0; s < p.stages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
-    for (int e = 0; e < NBUF; ++e) { ptx::mbar_init(&acc_full[e], 1); ptx::mbar_init(&acc_empty[e], 128 * CS); }
+    for (int e = 0; e < NBUF; ++e) { ptx::mbar_init(&acc_full[e], 1); ptx::mbar_init(&acc_empty[e], 128 * CS * PAIR); }
     ptx::mbar_init(w_full, 1);
+    ptx::mbar_init(w_peer, 1);
     ptx::fence_mbar_init();
   }
-  if (warp == kMma) ptx::tmem_alloc(tmem_holder, TMEM_COLS);
+  if (warp == kMma) {
+    if constexpr (PAIR == 2) ptx::tmem_alloc_pair(tmem_holder, TMEM_COLS);
+    else ptx::tmem_alloc(tmem_holder, TMEM_COLS);
+  }
   for (int i = threadIdx.x; i < CC; i += blockDim.x) bias_s[i] = p.bias[c0 + i];
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR == 2) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
@@ -164,7 +181,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     // ===================== TMA producer =====================
     if (lane == 0) {
       ptx::prefetch_tmap(&tmap);
-      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wpack) + size_t(part) * p.w_bytes;
+      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wpack) + size_t(part * PAIR + rank) * p.w_bytes;
       int s = 0;
       uint32_t ph = 0;
       if (!kloop) {
@@ -173,29 +190,38 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
           const int n = min(32768, p.w_bytes - off);
           ptx::bulk_g2s(w_s + off, wsrc + off, n, w_full);
         }
-        for (int64_t item = blockIdx.x; item < p.n_items; item += grid) {
+        if constexpr (PAIR == 2) {
+          if (!leader) {   // tell the leader's MMA warp that this half of the weights landed
+            ptx::mbar_wait(w_full, 0);
+            ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(w_peer), 0));
+          }
+        }
+        for (int64_t item = unit; item < p.n_items; item += n_units) {
           ptx::mbar_wait(&empty[s], ph ^ 1);
           if (p.dbg & 4) {
-            ptx::mbar_arrive(&full[s]);
+            if (leader) ptx::mbar_arrive(&full[s]);
             if (++s == p.stages) { s = 0; ph ^= 1; }
             continue;
           }
-          ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes);
-          const int64_t tile = item / p.n_split;
+          // the leader's barrier counts both CTAs' A bytes (pair-TMA completes on it)
+          if (leader) ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes * PAIR);
+          const int64_t tile = tile_of(item);
           uint8_t* dst = a_s + s * p.a_stride;
           if (p.mode == MODE_FLAT) {
-            ptx::tma_load_3d(dst, &tmap, &full[s], 0, int(tile * 128), 0);
+            if constexpr (PAIR == 2) ptx::tma_load_3d_pair(dst, &tmap, &full[s], 0, int(tile * 128), 0);
+            else ptx::tma_load_3d(dst, &tmap, &full[s], 0, int(tile * 128), 0);
           } else {
             const int b = int(tile / p.tiles_per_stream);
             const int ho0 = int(tile % p.tiles_per_stream) * p.MT;
-            ptx::tma_load_5d(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
+            if constexpr (PAIR == 2) ptx::tma_load_5d_pair(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
+            else ptx::tma_load_5d(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
           }
           if (++s == p.stages) { s = 0; ph ^= 1; }
         }
       } else {
         const int per_stream = p.tiles_h * p.tiles_w;
-        for (int64_t item = blockIdx.x; item < p.n_items; item += grid) {
-          const int64_t tile = item / p.n_split;
+        for (int64_t item = unit; item < p.n_items; item += n_units) {
+          const int64_t tile = tile_of(item);
           const int b = int(tile / per_stream);
           const int r = int(tile % per_stream);
           const int ho0 = (r / p.tiles_w) * p.TH, wo0 = (r % p.tiles_w) * p.TW;
@@ -207,7 +233,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
                 ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes + p.b_bytes);
                 uint8_t* dst = a_s + s * p.a_stride;
                 ptx::tma_load_5d(dst, &tmap, &full[s], 0, wo0 * p.sw + v * p.dw - p.pw,
-                                 ho0 * p.sh + u * p.dh - p.ph, cb * (p.kb / 8), b);
+                                 ho0 * p.sh + u * p.dh - p.ph, p.swa ? cb : cb * (p.kb / 8), b);   // swizzled: kb-channel blocks
                 ptx::bulk_g2s(dst + p.b_off, bsrc, p.b_bytes, &full[s]);
                 bsrc += p.b_bytes;
                 if (++s == p.stages) { s = 0; ph ^= 1; }
@@ -215,14 +241,11 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
         }
       }
     }
-    return;
-  }
-
-  if (warp == kMma) {
+  } else if (warp == kMma) {
     // ===================== MMA issuer =====================
     // The whole warp runs the loop (warp-uniform descriptors live in uniform
     // registers); one elected lane issues each tcgen05.mma / commit.
-    constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, N);
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(128 * PAIR, N);
     const uint32_t a_base = ptx::smem_u32(a_s);
     // Descriptors are advanced by adding (byte offset >> 4) to their 14-bit
     // start-address field (shared memory < 256 KB, so it never carries out).
@@ -231,29 +254,46 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     uint32_t ph = 0;
     int e = 0;
     uint32_t eph = 0;
-    if (!kloop) {
+    auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t acc) {
+      if constexpr (PAIR == 2) ptx::mma_bf16_ss_pair(d, ad, bd, idesc, acc);
+      else ptx::mma_bf16_ss(d, ad, bd, idesc, acc);
+    };
+    auto commit = [&](uint64_t* bar) {
+      if constexpr (PAIR == 2) ptx::tc_commit_pair(bar, 0x3);   // both CTAs' copies of the barrier
+      else ptx::tc_commit(bar);
+    };
+    if (PAIR == 2 && !leader) {
+      // the peer's tensor-core work is issued by the leader
+    } else if (!kloop) {
       ptx::mbar_wait(w_full, 0);
-      const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_u32(w_s), N * 16, 128);
+      if constexpr (PAIR == 2) ptx::mbar_wait(w_peer, 0);
+      const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_u32(w_s), NB * 16, 128);
       const int kc2 = p.Cin / 16;                       // MMAs (K = 16) per spatial tap
-      for (int64_t item = blockIdx.x; item < p.n_items; item += grid) {
+      for (int64_t item = unit; item < p.n_items; item += n_units) {
         if (!(p.dbg & 16)) ptx::mbar_wait(&acc_empty[e], eph ^ 1);
         ptx::tc_fence_after();
         ptx::mbar_wait(&full[s], ph);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem + uint32_t(e * BUF);
-        const uint64_t a_desc0 = ptx::smem_desc(a_base + uint32_t(s * p.a_stride), p.chunk_stride, 128);
+        const uint64_t a_desc0 = p.swa ? ptx::smem_desc_sw128(a_base + uint32_t(s * p.a_stride))
+                                       : ptx::smem_desc(a_base + uint32_t(s * p.a_stride), p.chunk_stride, 128);
+        // K16 step kc of a tap: 32 B along the swizzled 128-B row (next 64-channel
+        // block every 4 steps), or two 8-channel core-matrix groups unswizzled
+        auto kc_off = [&](int kc) -> uint64_t {
+          return p.swa ? uint64_t((kc >> 2) * p.a_rows * 8 + (kc & 3) * 2) : uint64_t(kc) * chunk16;
+        };
+        const uint32_t row16 = p.swa ? 8u : 1u;        // one halo row in 16-B units
         if constexpr (KH > 0) {
           if (!(p.dbg & 2) && ptx::elect_one()) {
 #pragma unroll
             for (int u = 0; u < KH; ++u)
 #pragma unroll
               for (int v = 0; v < KW; ++v) {
-                const uint64_t ad = a_desc0 + uint64_t(u * p.Wp + v);
+                const uint64_t ad = a_desc0 + uint64_t(u * p.Wp + v) * row16;
 #pragma unroll
                 for (int kc = 0; kc < KC; ++kc)
-                  ptx::mma_bf16_ss(d_tmem, ad + uint64_t(kc) * chunk16,
-                                   b_desc0 + uint64_t(((u * KW + v) * KC + kc) * 2 * N), idesc,
-                                   (u | v | kc) ? 1u : 0u);
+                  mma(d_tmem, ad + kc_off(kc), b_desc0 + uint64_t(((u * KW + v) * KC + kc) * 2 * NB),
+                      (u | v | kc) ? 1u : 0u);
               }
           }
           __syncwarp();
@@ -262,20 +302,19 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
           uint32_t acc = 0;
           for (int u = 0; u < p.kh; ++u) {
             for (int v = 0; v < p.kw; ++v) {
-              uint64_t ad = a_desc0 + uint64_t(u * p.Wp + v);   // tap (u, v): shift by u Wp + v rows
+              const uint64_t ad = a_desc0 + uint64_t(u * p.Wp + v) * row16;   // tap (u, v): shift by u Wp + v rows
               for (int kc = 0; kc < kc2; ++kc) {
-                if (ptx::elect_one()) ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, acc);
+                if (ptx::elect_one()) mma(d_tmem, ad + kc_off(kc), bd, acc);
                 __syncwarp();
                 acc = 1;
-                ad += chunk16;
-                bd += uint64_t(2 * N);                         // 2 groups of N rows x 16 B
+                bd += uint64_t(2 * NB);                        // 2 groups of NB rows x 16 B
               }
             }
           }
         }
         if (ptx::elect_one()) {
-          ptx::tc_commit(&empty[s]);      // A stage free once these MMAs retire
-          ptx::tc_commit(&acc_full[e]);   // accumulator e ready for the epilogue
+          commit(&empty[s]);      // A stage free once these MMAs retire
+          commit(&acc_full[e]);   // accumulator e ready for the epilogue
         }
         __syncwarp();
         if (++s == p.stages) { s = 0; ph ^= 1; }
@@ -284,7 +323,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     } else {
       const int n_chunks = p.kh * p.kw * p.n_cb;
       const int nk = p.kb / 16;                         // MMAs per chunk (<= 4)
-      for (int64_t item = blockIdx.x; item < p.n_items; item += grid) {
+      for (int64_t item = unit; item < p.n_items; item += n_units) {
         ptx::mbar_wait(&acc_empty[e], eph ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem + uint32_t(e * BUF);
@@ -292,13 +331,15 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
           ptx::mbar_wait(&full[s], ph);
           ptx::tc_fence_after();
           const uint32_t st = a_base + uint32_t(s * p.a_stride);
-          const uint64_t ad = ptx::smem_desc(st, p.chunk_stride, 128);
+          const uint64_t ad = p.swa == 1 ? ptx::smem_desc_sw128(st)
+                              : p.swa == 2 ? ptx::smem_desc_sw64(st) : ptx::smem_desc(st, p.chunk_stride, 128);
           const uint64_t bd = ptx::smem_desc(st + uint32_t(p.b_off), N * 16, 128);
+          const uint64_t astep = p.swa ? 2u : chunk16;     // one K16 step: 32 B of a swizzled row
           if (ptx::elect_one()) {
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               if (j < nk)
-                ptx::mma_bf16_ss(d_tmem, ad + uint64_t(j) * chunk16, bd + uint64_t(j * 2 * N), idesc,
+                ptx::mma_bf16_ss(d_tmem, ad + uint64_t(j) * astep, bd + uint64_t(j * 2 * N), idesc,
                                  (ch | j) ? 1u : 0u);
             ptx::tc_commit(&empty[s]);    // stage free once these MMAs retire
           }
@@ -311,12 +352,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       }
     }
     __syncwarp();
-    bar_sync_named(1, 32 + 128 * EG * CS);
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, TMEM_COLS);
-    return;
-  }
-
+  } else {
   // ===================== epilogue warpgroups (warps 0 .. 4 EG - 1) =====================
   const int e = warp / (4 * CS);                       // group
   const int q = warp & 3;                              // TMEM lane quadrant of this warp
@@ -328,10 +364,10 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   constexpr int NQ = CE / 4;                           // channel quads per thread and pass
   constexpr int NS = (KT > 1) ? KT - 1 : 1;
   int li = e;
-  for (int64_t item = blockIdx.x + int64_t(e) * grid; item < p.n_items; item += EG * int64_t(grid), li += EG) {
+  for (int64_t item = unit + int64_t(e) * n_units; item < p.n_items; item += EG * int64_t(n_units), li += EG) {
     const int buf = li % NBUF;                         // accumulator buffer of this item
     const uint32_t bph = uint32_t(li / NBUF) & 1u;
-    const int64_t tile = item / p.n_split;
+    const int64_t tile = tile_of(item);
     // ---- this row's output pixel
     bool valid;
     int64_t pix, b;
@@ -343,7 +379,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       b = tile / p.tiles_per_stream;
       const int ho = int(tile % p.tiles_per_stream) * p.MT + m / p.Wp;
       const int wo = m % p.Wp;
-      valid = (m < p.MT * p.Wp) && (wo < p.Wo) && (ho < p.Ho);
+      valid = (m < p.MT * p.Wp) && (wo < p.Wo) && (ho < p.Ho) && (tile < p.n_tiles);
       pix = b * p.HWo + int64_t(ho) * p.Wo + wo;
     } else {
       const int per_stream = p.tiles_h * p.tiles_w;
@@ -457,16 +493,26 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       }
     }
     ptx::tc_fence_before();
-    ptx::mbar_arrive(&acc_empty[buf]);
+    if constexpr (PAIR == 2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&acc_empty[buf]), 0));
+    else ptx::mbar_arrive(&acc_empty[buf]);
   }
-  bar_sync_named(1, 32 + 128 * EG * CS);
+  }
+  // ===================== teardown (all threads) =====================
+  ptx::tc_fence_before();
+  if constexpr (PAIR == 2) ptx::cluster_sync(); else __syncthreads();
+  if (warp == kMma) {
+    ptx::tc_fence_after();
+    if constexpr (PAIR == 2) ptx::tmem_dealloc_pair(tmem, TMEM_COLS);
+    else ptx::tmem_dealloc(tmem, TMEM_COLS);
+  }
 }
 
 // ------------------------------------------------------------------ host side
 
 __global__ void k_pack_tc_weights(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ out, int Cout,
-                                  int Cin, int kt, int kh, int kw, int CC, int n_split) {
-  // (Cout, Cin, kt, kh, kw) -> [part][K/8][N][8], N = kt*CC rows (n = k*CC + c),
+                                  int Cin, int kt, int kh, int kw, int CC, int n_split, int pair) {
+  // (Cout, Cin, kt, kh, kw) -> [part][half][K/8][N/pair][8], N = kt*CC rows
+  // (n = k*CC + c; a CTA pair splits them into halves n < N/2 and n >= N/2),
   // K index = (u*kw + v)*Cin + ci.  Each K chunk of a tap is one contiguous block.
   const int64_t total = int64_t(Cout) * Cin * kt * kh * kw;
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -482,7 +528,8 @@ __global__ void k_pack_tc_weights(const __nv_bfloat16* __restrict__ w, __nv_bflo
   const int64_t K = int64_t(Cin) * kh * kw;
   const int64_t kidx = int64_t(u * kw + v) * Cin + ci;
   const int n = k * CC + c;
-  out[int64_t(part) * K * N + ((kidx / 8) * N + n) * 8 + (kidx % 8)] = w[i];
+  const int NB = N / pair, half = n / NB, nn = n - half * NB;
+  out[int64_t(part * pair + half) * K * NB + ((kidx / 8) * NB + nn) * 8 + (kidx % 8)] = w[i];
 }
 
 // W-im2col of the weights for a small-Cin stem: (Cout, Cin, kt, kh, kw) ->
@@ -541,6 +588,7 @@ struct Variant {
   KernFn fn;
   int KH = 0, KW = 0, KC = 0;     // > 0: specialised (unrolled) HALO/FLAT variant for this kernel / Cin
   int CS = 1;                     // epilogue warps per TMEM lane quadrant (column split)
+  int PAIR = 1;                   // 2: CTA pairs (cta_group::2, M = 256), HALO / FLAT only
 };
 
 #define CO_TC_VARIANT(kt, cc, eg, ce) {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce>}
@@ -548,7 +596,11 @@ struct Variant {
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, kh, kw, kc>, kh, kw, kc}
 #define CO_TC_SPLIT(kt, cc, eg, ce, kh, kw, kc, cs) \
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, kh, kw, kc, cs>, kh, kw, kc, cs}
+#define CO_TC_PAIR(kt, cc, eg, ce, kh, kw, kc) \
+  {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, kh, kw, kc, 1, 2>, kh, kw, kc, 1, 2}
 const Variant kVariants[] = {
+    CO_TC_PAIR(3, 32, 2, 32, 3, 3, 4), CO_TC_PAIR(3, 32, 3, 32, 3, 3, 4), CO_TC_PAIR(9, 16, 2, 16, 1, 1, 16),
+    CO_TC_PAIR(1, 128, 2, 32, 3, 3, 4), CO_TC_SPEC(1, 128, 2, 32, 3, 3, 4),
     CO_TC_SPLIT(3, 32, 2, 16, 3, 3, 4, 2), CO_TC_SPLIT(3, 32, 3, 16, 3, 3, 4, 2),
     CO_TC_SPEC(3, 32, 2, 32, 3, 3, 4), CO_TC_SPEC(3, 32, 3, 32, 3, 3, 4), CO_TC_SPEC(9, 16, 2, 16, 1, 1, 16),
     CO_TC_VARIANT(1, 32, 4, 32), CO_TC_VARIANT(1, 64, 4, 32), CO_TC_VARIANT(1, 128, 2, 32),
@@ -575,6 +627,7 @@ struct Plan {
   const Variant* var = nullptr;
   Geom gk;                        // geometry the kernel sees (the W-im2col'd one for a stem)
   int wcols = 0, Kp = 0;          // small-Cin stem packed W-im2col
+  int swa = 0;                    // HALO: 128-B swizzled A (Cin % 64 == 0)
   int mode = MODE_HALO;
   int n_split = 0, MT = 0, Wp = 0, tiles_per_stream = 0;
   int TH = 0, TW = 0, tiles_h = 0, tiles_w = 0, kb = 0, n_cb = 0, b_bytes = 0, b_off = 0;
@@ -584,6 +637,23 @@ struct Plan {
 };
 
 constexpr size_t kSmemLimit = 227 * 1024;
+// Shared memory the planner fills before it takes more stages: beyond ~190 KB
+// the L1 left over (< ~38 KB) can no longer land the epilogue's in-flight
+// state loads and HBM throughput drops ~20% (measured: scripts/bw_probe.cu,
+// full bandwidth at 190 KB of shared memory, -18% at 200 KB).
+constexpr size_t kSmemBudget = 190 * 1024;
+
+// 128-B swizzled A operand (TMA boxes with 128-B rows instead of 16-B ones):
+// default on, CO_TC_SWA=0 restores the interleaved layout (A/B runs).
+bool swa_enabled() {
+  const char* v = getenv("CO_TC_SWA");
+  return !v || atoi(v) != 0;
+}
+
+int pinned_pair() {
+  const char* v = getenv("CO_TC_PAIR");         // A/B runs only
+  return v ? atoi(v) : 1;
+}
 
 int pinned_cs() {
   const char* v = getenv("CO_TC_CS");           // A/B runs only
@@ -612,21 +682,28 @@ bool plan_resident(const Geom& g, Plan& pl) {
   const int a_stride = ((a_bytes + kApad + 1023) / 1024) * 1024;
   const int64_t K = int64_t(g.Cin) * g.kh * g.kw;
   const int eg_pin = pinned_eg();
+  const char* pair_env = getenv("CO_TC_PAIR");    // A/B runs: pin 1 or 2
   const Variant* best = nullptr;
+  int64_t best_rank = -1;
   for (const Variant& v : kVariants) {
     if (v.KT != g.kt || g.Cout % v.CC != 0) continue;
     if (v.KH && (v.KH != g.kh || v.KW != g.kw || v.KC * 16 != g.Cin)) continue;
     if (eg_pin && v.EG != eg_pin) continue;
-    if (v.CS != pinned_cs()) continue;
-    const int64_t w_bytes = int64_t(v.KT * v.CC) * K * 2;
+    if (v.CS != pinned_cs() || (pair_env && v.PAIR != atoi(pair_env))) continue;
+    const int64_t w_bytes = int64_t(v.KT * v.CC) * K * 2 / v.PAIR;   // per CTA
     const size_t fixed = 1024 + size_t((w_bytes + 1023) / 1024 * 1024) + 512 + v.CC * 4;
     if (fixed + 2 * size_t(a_stride) > kSmemLimit) continue;
-    // prefer: more channels per part, then a specialised (unrolled) variant, then more groups
-    auto rank = [](const Variant* x) { return x->CC * 1000 + (x->KH ? 100 : 0) + x->EG; };
-    if (!best || rank(&v) > rank(best)) {
+    const bool fits = fixed + 2 * size_t(a_stride) <= kSmemBudget;
+    // prefer: staying under the L1 cliff (a CTA pair halves the resident
+    // weights), more channels per part, a specialised (unrolled) variant, one
+    // CTA over a pair (measured faster when both fit), more epilogue groups
+    const int64_t rank = (fits ? 1000000 : 0) + v.CC * 1000 + (v.KH ? 100 : 0) + (v.PAIR == 1 ? 10 : 0) + v.EG;
+    if (rank > best_rank) {
       best = &v;
+      best_rank = rank;
       pl.w_bytes = int(w_bytes);
-      pl.stages = int(std::min<size_t>(kMaxStages, (kSmemLimit - fixed) / size_t(a_stride)));
+      const size_t cap = fits ? kSmemBudget : kSmemLimit;
+      pl.stages = int(std::min<size_t>(kMaxStages, (cap - fixed) / size_t(a_stride)));
       pl.smem = fixed + size_t(pl.stages) * a_stride;
     }
   }
@@ -660,7 +737,7 @@ bool plan_kloop(const Geom& g, Plan& pl) {
   const int eg_pin = pinned_eg();
   const Variant* best = nullptr;
   for (const Variant& v : kVariants) {
-    if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.CS != 1) continue;
+    if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.CS != 1 || v.PAIR != 1) continue;
     if (eg_pin && v.EG != eg_pin) continue;
     // prefer the widest N (fewest A re-reads), then more groups
     auto rank = [](const Variant* x) { return x->CC * 1000 + x->EG; };
@@ -670,10 +747,13 @@ bool plan_kloop(const Geom& g, Plan& pl) {
   const int N = best->KT * best->CC;
   const int b_bytes = (kb / 8) * N * 16;
   // A chunk, slack for the junk rows the 128-row MMA reads past it, then B
-  const int b_off = (a_bytes + (128 - rows) * 16 + 127) / 128 * 128;
+  // swizzled A (kb == 64): 128-B rows; the 128-row MMA reads up to 16 KB
+  const int swa = !swa_enabled() ? 0 : kb == 64 ? 1 : kb == 32 ? 2 : 0;
+  const int b_off = swa ? std::max(a_bytes, 128 * kb * 2) : (a_bytes + (128 - rows) * 16 + 127) / 128 * 128;
   const int stage = (b_off + b_bytes + 1023) / 1024 * 1024;
   const size_t fixed = 1024 + 512 + best->CC * 4;
-  const int stages = int(std::min<size_t>(kMaxStages, (kSmemLimit - fixed) / size_t(stage)));
+  const size_t cap = (fixed + 2 * size_t(stage) <= kSmemBudget) ? kSmemBudget : kSmemLimit;
+  const int stages = int(std::min<size_t>(kMaxStages, (cap - fixed) / size_t(stage)));
   if (stages < 2) return false;
   pl.var = best;
   pl.mode = MODE_KLOOP;
@@ -685,6 +765,7 @@ bool plan_kloop(const Geom& g, Plan& pl) {
   pl.a_stride = stage;
   pl.stages = stages;
   pl.chunk_stride = rows * 16;
+  pl.swa = swa;
   pl.w_bytes = int(int64_t(N) * g.Cin * g.kh * g.kw * 2);
   pl.w_off = 0;
   pl.smem = fixed + size_t(stages) * stage;
@@ -709,6 +790,7 @@ Plan make_plan(const Geom& g) {
   const char* mode = getenv("CO_TC_MODE");      // A/B runs only: "kloop" forces the K pipeline
   const bool force_kloop = mode && std::string(mode) == "kloop";
   pl.ok = (!force_kloop && plan_resident(pl.gk, pl)) || plan_kloop(pl.gk, pl);
+  if (pl.ok && pl.mode != MODE_KLOOP && pl.gk.Cin % 64 == 0 && swa_enabled()) pl.swa = 1;
   if (pl.ok) pl.n_split = g.Cout / pl.var->CC;
   return pl;
 }
@@ -758,7 +840,7 @@ DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
     wsrc = wtmp;
   }
   k_pack_tc_weights<<<unsigned((total + 255) / 256), 256>>>(wsrc, t->wpack, k.Cout, k.Cin, k.kt, k.kh, k.kw,
-                                                           pl.var->CC, pl.n_split);
+                                                           pl.var->CC, pl.n_split, pl.var->PAIR);
   e = cudaGetLastError();
   if (wtmp) { cudaDeviceSynchronize(); cudaFree(wtmp); }
   if (e != cudaSuccess) { err = cudaGetErrorString(e); dense_tc_destroy(t); return nullptr; }
@@ -771,8 +853,9 @@ DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
   char buf[128];
   const char* mname = pl.mode == MODE_KLOOP ? (pl.wcols ? ",kloop+wcols" : ",kloop") : "";
   if (pl.var->KH)
-    snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d,%dx%dx%d%s%s>", pl.var->KT, pl.var->CC, pl.var->EG,
-             pl.var->KH, pl.var->KW, pl.var->KC * 16, pl.var->CS > 1 ? ",split" : "", mname);
+    snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d,%dx%dx%d%s%s%s>", pl.var->KT, pl.var->CC, pl.var->EG,
+             pl.var->KH, pl.var->KW, pl.var->KC * 16, pl.var->CS > 1 ? ",split" : "",
+             pl.var->PAIR > 1 ? ",pair" : "", mname);
   else
     snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d%s>", pl.var->KT, pl.var->CC, pl.var->EG, mname);
   if (getenv("CO_LOG"))
@@ -832,18 +915,26 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   CUresult r;
   auto encode = get_encode();
   if (pl.mode == MODE_FLAT) {
-    cuuint64_t dims[3] = {8, cuuint64_t(k.B * k.HWo), cuuint64_t(k.Cin / 8)};
-    cuuint64_t strides[2] = {cuuint64_t(k.Cin) * 2, 16};
-    cuuint32_t box[3] = {8, 128, cuuint32_t(k.Cin / 8)};
+    const cuuint32_t cw = pl.swa ? 64 : 8;    // channels per row of the box (128-B swizzled or 16-B)
+    cuuint64_t dims[3] = {cw, cuuint64_t(k.B * k.HWo), cuuint64_t(k.Cin / cw)};
+    cuuint64_t strides[2] = {cuuint64_t(k.Cin) * 2, cw * 2};
+    cuuint32_t box[3] = {cw, 128, cuuint32_t(k.Cin / cw)};
     cuuint32_t es[3] = {1, 1, 1};
     r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(x), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+               CU_TENSOR_MAP_INTERLEAVE_NONE, pl.swa ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
     cuuint64_t dims[5] = {8, cuuint64_t(k.W), cuuint64_t(k.H), cuuint64_t(k.Cin / 8), cuuint64_t(k.B)};
     cuuint64_t strides[4] = {cuuint64_t(k.Cin) * 2, cuuint64_t(k.W) * k.Cin * 2, 16, cuuint64_t(x_bstride) * 2};
     cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
-    if (pl.mode == MODE_HALO) {
+    CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE;
+    if (pl.mode == MODE_HALO && pl.swa) {
+      // 64-channel (128-B) rows, swizzled: smem [Cin/64][halo rows][128 B]
+      dims[0] = 64; dims[3] = cuuint64_t(k.Cin / 64); strides[2] = 128;
+      box[0] = 64; box[1] = cuuint32_t(pl.Wp); box[2] = cuuint32_t(pl.MT + k.kh - 1); box[3] = cuuint32_t(k.Cin / 64);
+      box[4] = 1;
+      sw = CU_TENSOR_MAP_SWIZZLE_128B;
+    } else if (pl.mode == MODE_HALO) {
       box[0] = 8; box[1] = cuuint32_t(pl.Wp); box[2] = cuuint32_t(pl.MT + k.kh - 1); box[3] = cuuint32_t(k.Cin / 8);
       box[4] = 1;
     } else {
@@ -851,9 +942,14 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
       box[0] = 8; box[1] = cuuint32_t(pl.TW * k.sw); box[2] = cuuint32_t(pl.TH * k.sh); box[3] = cuuint32_t(pl.kb / 8);
       box[4] = 1;
       es[1] = cuuint32_t(k.sw); es[2] = cuuint32_t(k.sh);
+      if (pl.swa) {   // one swizzled kb-channel row (128 B or 64 B) per output pixel
+        dims[0] = cuuint64_t(pl.kb); dims[3] = cuuint64_t(k.Cin / pl.kb); strides[2] = cuuint64_t(pl.kb) * 2;
+        box[0] = cuuint32_t(pl.kb); box[3] = 1;
+        sw = pl.swa == 1 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+      }
     }
     r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(x), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
@@ -867,24 +963,41 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   p.MT = pl.MT; p.Wp = pl.Wp; p.tiles_per_stream = pl.tiles_per_stream;
   p.TH = pl.TH; p.TW = pl.TW; p.tiles_h = pl.tiles_h; p.tiles_w = pl.tiles_w;
   p.kb = pl.kb; p.n_cb = pl.n_cb; p.b_bytes = pl.b_bytes; p.b_off = pl.b_off;
-  p.n_tiles = pl.n_tiles; p.n_split = pl.n_split; p.n_items = pl.n_tiles * pl.n_split;
+  const int pair = pl.var->PAIR;
+  const int64_t units_tiles = (pl.n_tiles + pair - 1) / pair;     // tiles per unit position (pairs take 2)
+  p.n_tiles = pl.n_tiles; p.n_split = pl.n_split; p.n_items = units_tiles * pl.n_split;
   p.a_bytes = pl.a_bytes; p.a_stride = pl.a_stride; p.stages = pl.stages; p.chunk_stride = pl.chunk_stride;
   p.w_bytes = pl.w_bytes; p.w_off = pl.w_off;
   for (int i = 0; i < kMaxKt; ++i) p.slot[i] = a.slot[i];
   p.emit = a.emit; p.update = a.update; p.act = g.act; p.out_f32 = (g.out_dtype == F32);
   static const int dbg = getenv("CO_TC_DEBUG") ? atoi(getenv("CO_TC_DEBUG")) : 0;
   p.dbg = dbg;
+  p.swa = pl.swa;
+  p.a_rows = pl.chunk_stride / 16;
   p.Cq = g.Cq;
   p.state = a.state;
   p.y = a.y;
   p.y_bstride = a.y_bstride;
   p.wpack = t->wpack;
   p.bias = bias;
-  const int per = std::max(1, t->num_sms / pl.n_split);
-  const int64_t grid = std::min<int64_t>(per, pl.n_tiles) * pl.n_split;
+  const int per = std::max(1, t->num_sms / pair / pl.n_split);
+  const int64_t grid = std::min<int64_t>(per, units_tiles) * pl.n_split * pair;
   void* args[] = {&map, &p};
-  return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->fn), dim3(unsigned(grid)),
-                          dim3(tc_threads(pl.var->EG, pl.var->CS)), args, pl.smem, s);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(tc_threads(pl.var->EG, pl.var->CS));
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (pair > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(pair);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(pl.var->fn), args);
 }
 
 }  // namespace co

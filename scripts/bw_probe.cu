@@ -17,8 +17,24 @@ constexpr long long B = 256, HW = 3136, C = 64, R = 2;
 constexpr long long PLANE = B * HW;                 // pixels
 constexpr int CQ = C / 4;
 
-template <int NI, bool HALO, bool PAD = false>
+template <int F>
+__device__ __forceinline__ float4 ld_flavor(const float4* p) {
+  float4 v;
+  if constexpr (F == 0) return __ldcs(p);
+  if constexpr (F == 1) return __ldcg(p);
+  if constexpr (F == 2) {
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+  }
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+
+template <int NI, bool HALO, bool PAD = false, int F = 0>
 __global__ void k_quadmajor(float4* __restrict__ st, __nv_bfloat16* __restrict__ y, long long n_items, int work) {
+  extern __shared__ float4 dummy_smem[];        // optional: shrink L1 like the dense kernel's 200 KB carve-out
+  work &= 0xffff;
+  if (work == 0xfff) dummy_smem[threadIdx.x] = make_float4(0, 0, 0, 0);
   // item = (tile of 128 pixels, channel half); thread = pixel row of the tile.
   // HALO: the dense kernel's C2 tile shape -- 2 output rows of 56 in a 58-wide
   // padded halo, rows m -> pixel (m/58)*56 + m%58, 112 valid of 128 lanes.
@@ -40,7 +56,7 @@ __global__ void k_quadmajor(float4* __restrict__ st, __nv_bfloat16* __restrict__
 #pragma unroll
       for (int s = 0; s < 2; ++s)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) a[j][s][q] = __ldcs(st + ((long long)s * CQ + q0 + q) * PLANE + (PAD ? (it >> 1) * 128 + m : pix));
+        for (int q = 0; q < 8; ++q) a[j][s][q] = ld_flavor<F>(st + ((long long)s * CQ + q0 + q) * PLANE + (PAD ? (it >> 1) * 128 + m : pix));
     }
 #pragma unroll
     for (int j = 0; j < NI; ++j) {
@@ -109,7 +125,12 @@ __global__ void k_copy(const float4* __restrict__ a, float4* __restrict__ b, lon
 
 int main(int argc, char** argv) {
   const int mode = atoi(argv[1]), threads = atoi(argv[2]), bps = atoi(argv[3]), ni = atoi(argv[4]);
-  const int work = argc > 5 ? atoi(argv[5]) : 0;
+  const int work = argc > 5 ? atoi(argv[5]) : 0;             // low 16 bits: ALU work; bits 16+: load flavour
+  const int smem_bytes = argc > 6 ? atoi(argv[6]) : 0;       // unused dynamic shared memory (L1 carve-out)
+  cudaFuncSetAttribute(k_quadmajor<1, true, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaFuncSetAttribute(k_quadmajor<1, true, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaFuncSetAttribute(k_quadmajor<1, true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaFuncSetAttribute(k_quadmajor<1, true, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const long long st_elems = R * C * PLANE;         // floats
@@ -132,7 +153,11 @@ int main(int argc, char** argv) {
       else k_quadmajor<2, false><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items, work);
     } else if (mode == 4) {
       const long long n_items = (PLANE + 111) / 112 * 2 * 112 / 128 - 2;   // padded rows stay inside the buffer
-      k_quadmajor<1, true, true><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items, work);
+      const int f = work >> 16;
+      if (f == 0) k_quadmajor<1, true, true, 0><<<grid, threads, smem_bytes>>>(st, (__nv_bfloat16*)y, n_items, work);
+      if (f == 1) k_quadmajor<1, true, true, 1><<<grid, threads, smem_bytes>>>(st, (__nv_bfloat16*)y, n_items, work);
+      if (f == 2) k_quadmajor<1, true, true, 2><<<grid, threads, smem_bytes>>>(st, (__nv_bfloat16*)y, n_items, work);
+      if (f == 3) k_quadmajor<1, true, true, 3><<<grid, threads, smem_bytes>>>(st, (__nv_bfloat16*)y, n_items, work);
     } else if (mode == 3) {
       const long long n_items = (PLANE + 111) / 112 * 2;
       if (ni == 1) k_quadmajor<1, true><<<grid, threads>>>(st, (__nv_bfloat16*)y, n_items, work);
@@ -158,7 +183,7 @@ int main(int argc, char** argv) {
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   const cudaError_t err = cudaGetLastError();
-  printf("mode %d threads %d blocks/SM %d NI %d work %d: %.1f us/launch, %.1f GB/s %s\n", mode, threads, bps, ni, work,
+  printf("mode %d threads %d blocks/SM %d NI %d work %d smem %d: %.1f us/launch, %.1f GB/s %s\n", mode, threads, bps, ni, work, smem_bytes,
          ms * 1e3 / reps, bytes_rw / (ms / reps * 1e-3) / 1e9, err == cudaSuccess ? "" : cudaGetErrorString(err));
   return 0;
 }

@@ -16,6 +16,8 @@ pytestmark = pytest.mark.gpu
 CASES = {
     # C2-shaped halo mode: 3x3 spatial, pad 1, several tiles per stream, ragged rows
     "halo_c2like": dict(desc=O.Desc(2, 64, 64, (3, 3, 3), padding=(0, 1, 1), in_spatial=(13, 24)), B=3),
+    "halo_c2like_oddtiles": dict(desc=O.Desc(2, 64, 64, (3, 3, 3), padding=(0, 1, 1), in_spatial=(12, 24)), B=3),
+    "flat_c5full": dict(desc=O.Desc(1, 256, 256, (9, 1), dilation=(2, 1), in_spatial=(25, 1)), B=7),
     "halo_c2like_pt1": dict(desc=O.Desc(2, 32, 64, (3, 3, 3), padding=(1, 1, 1), in_spatial=(9, 30)), B=2),
     "halo_wide": dict(desc=O.Desc(2, 16, 32, (3, 3, 3), padding=(0, 1, 1), in_spatial=(5, 56)), B=2),
     "halo_kt5": dict(desc=O.Desc(2, 16, 32, (5, 3, 3), padding=(0, 1, 1), in_spatial=(7, 11)), B=2),
@@ -42,9 +44,10 @@ CASES = {
     "flat_st2_dil2": dict(desc=O.Desc(1, 32, 32, (3, 1), stride=(2, 1), dilation=(2, 1), in_spatial=(25, 1)), B=3),
 }
 FORCE_KLOOP = {"halo_c2like", "halo_kt5", "flat_c5like"}   # also run these through the K pipeline
+PAIR_CASES = ["halo_c2like", "halo_c2like_oddtiles", "flat_c5full"]   # CTA-pair (cta_group::2) variants
 
 
-def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force_kloop=False):
+def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force_kloop=False, pair=False):
     import os
     d, B = CASES[case]["desc"], CASES[case]["B"]
     rng = np.random.default_rng(seed)
@@ -56,10 +59,15 @@ def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force
         b = rng.standard_normal(d.cout) * 0.1
     if force_kloop:
         os.environ["CO_TC_MODE"] = "kloop"
+    if pair:
+        os.environ["CO_TC_PAIR"] = "2"
     try:
         conv, sm, Wq, bq = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="dense_tc")
     finally:
         os.environ.pop("CO_TC_MODE", None)
+        os.environ.pop("CO_TC_PAIR", None)
+    if pair:
+        assert "pair" in conv.kernel_name, conv.kernel_name
     ref_conv, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="direct")
     assert conv.kernel_used == "dense_tc", conv.kernel_name
     if force_kloop or case.startswith("kloop") or case == "stem_c4like":  # (kloop_st3: spatial stride 2)
@@ -95,6 +103,16 @@ def test_dense_tc_exact_integer_bitwise(case):
     _, y, ref, yd = _run(case, integer=True)
     assert np.array_equal(y, ref)
     assert np.array_equal(y, yd)
+
+
+@pytest.mark.parametrize("case", PAIR_CASES)
+def test_dense_tc_cta_pair(case):
+    """The CTA-pair variants (M = 256 over two SMs, weights split by N) agree
+    with the oracle and, in the exact-integer regime, bit for bit."""
+    _, y, ref, yd = _run(case, pair=True)
+    assert rel_err(y, ref) <= 1e-4 and rel_err(y, yd) <= 1e-4
+    _, y, ref, _ = _run(case, integer=True, pair=True)
+    assert np.array_equal(y, ref)
 
 
 @pytest.mark.parametrize("case", sorted(FORCE_KLOOP))
