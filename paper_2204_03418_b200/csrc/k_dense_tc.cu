@@ -553,32 +553,35 @@ __global__ void k_wcols_weights(const __nv_bfloat16* __restrict__ w, __nv_bfloat
 }
 
 // W-im2col of one step's frame: xp[b][h][wo][j] = x[b][h][wo*sw + v*dw - pw][c],
-// j = v*Cin + c, zero outside the frame and for j >= kw*Cin.  One thread
-// writes 8 channels (16 B).
-__global__ void k_wcols_frame(const __nv_bfloat16* __restrict__ x, int64_t x_bstride, __nv_bfloat16* __restrict__ xp,
-                              int64_t B, int H, int W, int Cin, int Wo, int kw, int sw, int dw, int pw, int Kp) {
-  const int K8 = Kp / 8;
-  const int64_t total = B * H * Wo * K8;
+// j = v*Cin + c, zero outside the frame and for j >= kw*Cin.  One thread per
+// output pixel builds its KP channels in registers (unrolled, compile-time j)
+// and writes them as KP/8 16-byte stores (consecutive threads, consecutive
+// 2*KP-byte rows); the inputs it reads overlap its neighbours' (L1 hits).
+template <int KP>
+__global__ void __launch_bounds__(256) k_wcols_frame(const __nv_bfloat16* __restrict__ x, int64_t x_bstride,
+                                                     __nv_bfloat16* __restrict__ xp, int64_t B, int H, int W,
+                                                     int Cin, int Wo, int kw, int sw, int dw, int pw) {
+  const int64_t total = B * H * Wo;
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= total) return;
-  const int j8 = int(i % K8);
-  int64_t r = i / K8;
-  const int wo = int(r % Wo); r /= Wo;
+  const int wo = int(i % Wo);
+  const int64_t r = i / Wo;
   const int h = int(r % H);
   const int64_t b = r / H;
-  __align__(16) __nv_bfloat16 vals[8];
+  const __nv_bfloat16* xr = x ? x + b * x_bstride + int64_t(h) * W * Cin : nullptr;
+  __align__(16) __nv_bfloat16 vals[KP];
+  const __nv_bfloat16 zero = __float2bfloat16_rn(0.f);
 #pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const int j = j8 * 8 + t;
-    float val = 0.f;
-    if (x && j < kw * Cin) {
-      const int v = j / Cin, c = j % Cin;
-      const int wi = wo * sw + v * dw - pw;
-      if (wi >= 0 && wi < W) val = __bfloat162float(x[b * x_bstride + (int64_t(h) * W + wi) * Cin + c]);
-    }
-    vals[t] = __float2bfloat16_rn(val);
+  for (int j = 0; j < KP; ++j) {
+    __nv_bfloat16 val = zero;
+    const int v = j / Cin, c = j - (j / Cin) * Cin;
+    const int wi = wo * sw + v * dw - pw;
+    if (xr && v < kw && wi >= 0 && wi < W) val = xr[int64_t(wi) * Cin + c];
+    vals[j] = val;
   }
-  *reinterpret_cast<uint4*>(xp + i * 8) = *reinterpret_cast<const uint4*>(vals);
+  uint4* dst = reinterpret_cast<uint4*>(xp + i * KP);
+#pragma unroll
+  for (int t = 0; t < KP / 8; ++t) dst[t] = reinterpret_cast<const uint4*>(vals)[t];
 }
 
 typedef void (*KernFn)(const CUtensorMap, const TcParams);
@@ -894,10 +897,15 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
     // small-Cin stem: W-im2col the frame (a zero frame stays zero)
     const int64_t kframe = int64_t(k.H) * k.W * k.Cin;
     if (cudaError_t e = ensure_stage(t, size_t(g.B) * kframe * 2)) return e;
-    const int64_t n = g.B * k.H * k.W * (k.Cin / 8);
-    k_wcols_frame<<<unsigned((n + 255) / 256), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), x_bstride,
-                                                            t->xstage, g.B, g.H, g.W, g.Cin, g.Wo, g.kw, g.sw, g.dw,
-                                                            g.pw, pl.Kp);
+    const int64_t n = g.B * k.H * k.W;
+    const unsigned nb = unsigned((n + 255) / 256);
+    const __nv_bfloat16* xs = static_cast<const __nv_bfloat16*>(x);
+    switch (pl.Kp) {
+      case 16: k_wcols_frame<16><<<nb, 256, 0, s>>>(xs, x_bstride, t->xstage, g.B, g.H, g.W, g.Cin, g.Wo, g.kw, g.sw, g.dw, g.pw); break;
+      case 32: k_wcols_frame<32><<<nb, 256, 0, s>>>(xs, x_bstride, t->xstage, g.B, g.H, g.W, g.Cin, g.Wo, g.kw, g.sw, g.dw, g.pw); break;
+      case 48: k_wcols_frame<48><<<nb, 256, 0, s>>>(xs, x_bstride, t->xstage, g.B, g.H, g.W, g.Cin, g.Wo, g.kw, g.sw, g.dw, g.pw); break;
+      default: k_wcols_frame<64><<<nb, 256, 0, s>>>(xs, x_bstride, t->xstage, g.B, g.H, g.W, g.Cin, g.Wo, g.kw, g.sw, g.dw, g.pw); break;
+    }
     if (cudaError_t e = cudaGetLastError()) return e;
     x = t->xstage;
     x_bstride = kframe;
