@@ -603,7 +603,7 @@ struct Variant {
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, kh, kw, kc, 1, 2>, kh, kw, kc, 1, 2}
 const Variant kVariants[] = {
     CO_TC_PAIR(3, 32, 2, 32, 3, 3, 4), CO_TC_PAIR(3, 32, 3, 32, 3, 3, 4), CO_TC_PAIR(9, 16, 2, 16, 1, 1, 16),
-    CO_TC_PAIR(1, 128, 2, 32, 3, 3, 4), CO_TC_SPEC(1, 128, 2, 32, 3, 3, 4),
+    CO_TC_PAIR(1, 128, 2, 32, 3, 3, 4), CO_TC_SPEC(1, 128, 2, 32, 3, 3, 4), CO_TC_PAIR(3, 64, 2, 32, 3, 3, 4),
     CO_TC_SPLIT(3, 32, 2, 16, 3, 3, 4, 2), CO_TC_SPLIT(3, 32, 3, 16, 3, 3, 4, 2),
     CO_TC_SPEC(3, 32, 2, 32, 3, 3, 4), CO_TC_SPEC(3, 32, 3, 32, 3, 3, 4), CO_TC_SPEC(9, 16, 2, 16, 1, 1, 16),
     CO_TC_VARIANT(1, 32, 4, 32), CO_TC_VARIANT(1, 64, 4, 32), CO_TC_VARIANT(1, 128, 2, 32),
@@ -698,9 +698,10 @@ bool plan_resident(const Geom& g, Plan& pl) {
     if (fixed + 2 * size_t(a_stride) > kSmemLimit) continue;
     const bool fits = fixed + 2 * size_t(a_stride) <= kSmemBudget;
     // prefer: staying under the L1 cliff (a CTA pair halves the resident
-    // weights), more channels per part, a specialised (unrolled) variant, one
-    // CTA over a pair (measured faster when both fit), more epilogue groups
-    const int64_t rank = (fits ? 1000000 : 0) + v.CC * 1000 + (v.KH ? 100 : 0) + (v.PAIR == 1 ? 10 : 0) + v.EG;
+    // weights), one CTA over a pair (measured faster on C2 when both fit: the
+    // pair's 64-channel epilogue costs more than its MMA saves), more channels
+    // per part, a specialised (unrolled) variant, more epilogue groups
+    const int64_t rank = (fits ? 10000000 : 0) + (v.PAIR == 1 ? 1000000 : 0) + v.CC * 1000 + (v.KH ? 100 : 0) + v.EG;
     if (rank > best_rank) {
       best = &v;
       best_rank = rank;
