@@ -114,7 +114,10 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 // warp spends ~3 uniform instructions per tcgen05.mma.
 template <int KT, int CC, int EG, int CE, int KH = 0, int KW = 0, int KC = 0, int CS = 1, int PAIR = 1>
 __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
-    k_step_dense_tc(const __grid_constant__ CUtensorMap tmap, const TcParams p) {
+    k_step_dense_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap wmap,
+                    const TcParams p) {
+  // wmap: the packed weights as a tensor, used by KLOOP CTA pairs (each CTA
+  // streams its N/2 half of every B chunk with a pair TMA load)
   constexpr int N = KT * CC;
   // TMEM accumulator ring: as many N-column buffers as 512 columns hold, at
   // least one per epilogue group, so the MMA can run ahead of the state traffic.
@@ -226,16 +229,25 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
           const int r = int(tile % per_stream);
           const int ho0 = (r / p.tiles_w) * p.TH, wo0 = (r % p.tiles_w) * p.TW;
           const uint8_t* bsrc = wsrc;
+          int kg = 0;                                   // K-group (8 channels) index of the chunk
           for (int u = 0; u < p.kh; ++u)
             for (int v = 0; v < p.kw; ++v)
               for (int cb = 0; cb < p.n_cb; ++cb) {
                 ptx::mbar_wait(&empty[s], ph ^ 1);
-                ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes + p.b_bytes);
                 uint8_t* dst = a_s + s * p.a_stride;
-                ptx::tma_load_5d(dst, &tmap, &full[s], 0, wo0 * p.sw + v * p.dw - p.pw,
-                                 ho0 * p.sh + u * p.dh - p.ph, p.swa ? cb : cb * (p.kb / 8), b);   // swizzled: kb-channel blocks
-                ptx::bulk_g2s(dst + p.b_off, bsrc, p.b_bytes, &full[s]);
+                const int cw = wo0 * p.sw + v * p.dw - p.pw, ch = ho0 * p.sh + u * p.dh - p.ph;
+                const int cc = p.swa ? cb : cb * (p.kb / 8);   // swizzled: kb-channel blocks
+                if constexpr (PAIR == 2) {
+                  if (leader) ptx::mbar_arrive_expect_tx(&full[s], (p.a_bytes + p.b_bytes) * PAIR);
+                  ptx::tma_load_5d_pair(dst, &tmap, &full[s], 0, cw, ch, cc, b);
+                  ptx::tma_load_4d_pair(dst + p.b_off, &wmap, &full[s], 0, 0, kg / (p.kb / 8), part * PAIR + int(rank));
+                } else {
+                  ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes + p.b_bytes);
+                  ptx::tma_load_5d(dst, &tmap, &full[s], 0, cw, ch, cc, b);
+                  ptx::bulk_g2s(dst + p.b_off, bsrc, p.b_bytes, &full[s]);
+                }
                 bsrc += p.b_bytes;
+                kg += p.kb / 8;
                 if (++s == p.stages) { s = 0; ph ^= 1; }
               }
         }
@@ -333,20 +345,22 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
           const uint32_t st = a_base + uint32_t(s * p.a_stride);
           const uint64_t ad = p.swa == 1 ? ptx::smem_desc_sw128(st)
                               : p.swa == 2 ? ptx::smem_desc_sw64(st) : ptx::smem_desc(st, p.chunk_stride, 128);
-          const uint64_t bd = ptx::smem_desc(st + uint32_t(p.b_off), N * 16, 128);
+          // B: core-matrix layout, or (pairs) swizzled kb-element rows like A
+          const uint64_t bd = (PAIR == 1) ? ptx::smem_desc(st + uint32_t(p.b_off), NB * 16, 128)
+                              : p.kb == 64 ? ptx::smem_desc_sw128(st + uint32_t(p.b_off))
+                                           : ptx::smem_desc_sw64(st + uint32_t(p.b_off));
+          const uint64_t bstep = (PAIR == 1) ? uint64_t(2 * NB) : 2u;
           const uint64_t astep = p.swa ? 2u : chunk16;     // one K16 step: 32 B of a swizzled row
           if (ptx::elect_one()) {
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              if (j < nk)
-                ptx::mma_bf16_ss(d_tmem, ad + uint64_t(j) * astep, bd + uint64_t(j * 2 * N), idesc,
-                                 (ch | j) ? 1u : 0u);
-            ptx::tc_commit(&empty[s]);    // stage free once these MMAs retire
+              if (j < nk) mma(d_tmem, ad + uint64_t(j) * astep, bd + uint64_t(j) * bstep, (ch | j) ? 1u : 0u);
+            commit(&empty[s]);    // stage free once these MMAs retire
           }
           __syncwarp();
           if (++s == p.stages) { s = 0; ph ^= 1; }
         }
-        if (ptx::elect_one()) ptx::tc_commit(&acc_full[e]);
+        if (ptx::elect_one()) commit(&acc_full[e]);
         __syncwarp();
         if (++e == NBUF) { e = 0; eph ^= 1; }
       }
@@ -387,7 +401,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       const int r = int(tile % per_stream);
       const int ho = (r / p.tiles_w) * p.TH + m / p.TW;
       const int wo = (r % p.tiles_w) * p.TW + m % p.TW;
-      valid = (m < p.TH * p.TW) && (wo < p.Wo) && (ho < p.Ho);
+      valid = (m < p.TH * p.TW) && (wo < p.Wo) && (ho < p.Ho) && (tile < p.n_tiles);
       pix = b * p.HWo + int64_t(ho) * p.Wo + wo;
     }
     // state row: the TMEM lane inside the tile (tile-padded layout, common.cuh)
@@ -510,7 +524,9 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
 // ------------------------------------------------------------------ host side
 
 __global__ void k_pack_tc_weights(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ out, int Cout,
-                                  int Cin, int kt, int kh, int kw, int CC, int n_split, int pair) {
+                                  int Cin, int kt, int kh, int kw, int CC, int n_split, int pair, int kblk) {
+  // kblk > 0 (KLOOP CTA pairs): [part][half][K/kblk][N/pair][kblk] instead --
+  // kblk-element (128-B / 64-B) rows a swizzled TMA box loads in one request
   // (Cout, Cin, kt, kh, kw) -> [part][half][K/8][N/pair][8], N = kt*CC rows
   // (n = k*CC + c; a CTA pair splits them into halves n < N/2 and n >= N/2),
   // K index = (u*kw + v)*Cin + ci.  Each K chunk of a tap is one contiguous block.
@@ -529,7 +545,10 @@ __global__ void k_pack_tc_weights(const __nv_bfloat16* __restrict__ w, __nv_bflo
   const int64_t kidx = int64_t(u * kw + v) * Cin + ci;
   const int n = k * CC + c;
   const int NB = N / pair, half = n / NB, nn = n - half * NB;
-  out[int64_t(part * pair + half) * K * NB + ((kidx / 8) * NB + nn) * 8 + (kidx % 8)] = w[i];
+  if (kblk)
+    out[int64_t(part * pair + half) * K * NB + ((kidx / kblk) * NB + nn) * kblk + (kidx % kblk)] = w[i];
+  else
+    out[int64_t(part * pair + half) * K * NB + ((kidx / 8) * NB + nn) * 8 + (kidx % 8)] = w[i];
 }
 
 // W-im2col of the weights for a small-Cin stem: (Cout, Cin, kt, kh, kw) ->
@@ -584,7 +603,7 @@ __global__ void __launch_bounds__(256) k_wcols_frame(const __nv_bfloat16* __rest
   for (int t = 0; t < KP / 8; ++t) dst[t] = reinterpret_cast<const uint4*>(vals)[t];
 }
 
-typedef void (*KernFn)(const CUtensorMap, const TcParams);
+typedef void (*KernFn)(const CUtensorMap, const CUtensorMap, const TcParams);
 
 struct Variant {
   int KT, CC, EG, CE;
@@ -599,11 +618,14 @@ struct Variant {
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, kh, kw, kc>, kh, kw, kc}
 #define CO_TC_SPLIT(kt, cc, eg, ce, kh, kw, kc, cs) \
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, kh, kw, kc, cs>, kh, kw, kc, cs}
+#define CO_TC_PAIRG(kt, cc, eg, ce) \
+  {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, 0, 0, 0, 1, 2>, 0, 0, 0, 1, 2}
 #define CO_TC_PAIR(kt, cc, eg, ce, kh, kw, kc) \
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, kh, kw, kc, 1, 2>, kh, kw, kc, 1, 2}
 const Variant kVariants[] = {
     CO_TC_PAIR(3, 32, 2, 32, 3, 3, 4), CO_TC_PAIR(3, 32, 3, 32, 3, 3, 4), CO_TC_PAIR(9, 16, 2, 16, 1, 1, 16),
     CO_TC_PAIR(1, 128, 2, 32, 3, 3, 4), CO_TC_SPEC(1, 128, 2, 32, 3, 3, 4), CO_TC_PAIR(3, 64, 2, 32, 3, 3, 4),
+    CO_TC_PAIRG(3, 64, 2, 32), CO_TC_PAIRG(5, 32, 2, 16),
     CO_TC_SPLIT(3, 32, 2, 16, 3, 3, 4, 2), CO_TC_SPLIT(3, 32, 3, 16, 3, 3, 4, 2),
     CO_TC_SPEC(3, 32, 2, 32, 3, 3, 4), CO_TC_SPEC(3, 32, 3, 32, 3, 3, 4), CO_TC_SPEC(9, 16, 2, 16, 1, 1, 16),
     CO_TC_VARIANT(1, 32, 4, 32), CO_TC_VARIANT(1, 64, 4, 32), CO_TC_VARIANT(1, 128, 2, 32),
@@ -653,6 +675,15 @@ bool swa_enabled() {
   return !v || atoi(v) != 0;
 }
 
+// KLOOP CTA pairs (each CTA streams half of every weight chunk through a
+// swizzled 128-B-row TMA box): default for 64-channel K chunks (C4 L3 / L5
+// measured ~8% faster, L4 equal); 32-channel chunks (the stem) stay single.
+// CO_TC_KPAIR=1|2 pins it (A/B runs).
+int kloop_pair(int kb) {
+  const char* v = getenv("CO_TC_KPAIR");
+  return v ? atoi(v) : (kb == 64 ? 2 : 1);
+}
+
 int pinned_pair() {
   const char* v = getenv("CO_TC_PAIR");         // A/B runs only
   return v ? atoi(v) : 1;
@@ -698,10 +729,10 @@ bool plan_resident(const Geom& g, Plan& pl) {
     if (fixed + 2 * size_t(a_stride) > kSmemLimit) continue;
     const bool fits = fixed + 2 * size_t(a_stride) <= kSmemBudget;
     // prefer: staying under the L1 cliff (a CTA pair halves the resident
-    // weights), one CTA over a pair (measured faster on C2 when both fit: the
-    // pair's 64-channel epilogue costs more than its MMA saves), more channels
-    // per part, a specialised (unrolled) variant, more epilogue groups
-    const int64_t rank = (fits ? 10000000 : 0) + (v.PAIR == 1 ? 1000000 : 0) + v.CC * 1000 + (v.KH ? 100 : 0) + v.EG;
+    // weights), a specialised (unrolled) variant, one CTA over a pair (measured
+    // faster on C2 when both fit: the pair's 64-channel epilogue costs more than
+    // its MMA saves), more channels per part, more epilogue groups
+    const int64_t rank = (fits ? 100000000 : 0) + (v.KH ? 10000000 : 0) + (v.PAIR == 1 ? 1000000 : 0) + v.CC * 1000 + v.EG;
     if (rank > best_rank) {
       best = &v;
       best_rank = rank;
@@ -740,20 +771,26 @@ bool plan_kloop(const Geom& g, Plan& pl) {
   const int a_bytes = (kb / 8) * rows * 16;
   const int eg_pin = pinned_eg();
   const Variant* best = nullptr;
-  for (const Variant& v : kVariants) {
-    if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.CS != 1 || v.PAIR != 1) continue;
-    if (eg_pin && v.EG != eg_pin) continue;
-    // prefer the widest N (fewest A re-reads), then more groups
-    auto rank = [](const Variant* x) { return x->CC * 1000 + x->EG; };
-    if (!best || rank(&v) > rank(best)) best = &v;
+  const int want = kloop_pair(kb);
+  for (int pair : {want, 3 - want}) {           // the preferred pairing, else the other
+    if (getenv("CO_TC_KPAIR") && pair != want) break;
+    for (const Variant& v : kVariants) {
+      if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.CS != 1 || v.PAIR != pair) continue;
+      if (eg_pin && v.EG != eg_pin) continue;
+      // prefer the widest N (fewest A re-reads), then more groups
+      auto rank = [](const Variant* x) { return x->CC * 1000 + x->EG; };
+      if (!best || rank(&v) > rank(best)) best = &v;
+    }
+    if (best) break;
   }
   if (!best) return false;
   const int N = best->KT * best->CC;
-  const int b_bytes = (kb / 8) * N * 16;
+  const int b_bytes = (kb / 8) * (N / best->PAIR) * 16;      // this CTA's share of a B chunk
   // A chunk, slack for the junk rows the 128-row MMA reads past it, then B
   // swizzled A (kb == 64): 128-B rows; the 128-row MMA reads up to 16 KB
   const int swa = !swa_enabled() ? 0 : kb == 64 ? 1 : kb == 32 ? 2 : 0;
-  const int b_off = swa ? std::max(a_bytes, 128 * kb * 2) : (a_bytes + (128 - rows) * 16 + 127) / 128 * 128;
+  int b_off = swa ? std::max(a_bytes, 128 * kb * 2) : (a_bytes + (128 - rows) * 16 + 127) / 128 * 128;
+  if (best->PAIR == 2) b_off = (b_off + 1023) / 1024 * 1024;   // swizzled B rows: 1 KB-aligned atoms
   const int stage = (b_off + b_bytes + 1023) / 1024 * 1024;
   const size_t fixed = 1024 + 512 + best->CC * 4;
   const size_t cap = (fixed + 2 * size_t(stage) <= kSmemBudget) ? kSmemBudget : kSmemLimit;
@@ -770,7 +807,7 @@ bool plan_kloop(const Geom& g, Plan& pl) {
   pl.stages = stages;
   pl.chunk_stride = rows * 16;
   pl.swa = swa;
-  pl.w_bytes = int(int64_t(N) * g.Cin * g.kh * g.kw * 2);
+  pl.w_bytes = int(int64_t(N / best->PAIR) * g.Cin * g.kh * g.kw * 2);
   pl.w_off = 0;
   pl.smem = fixed + size_t(stages) * stage;
   pl.n_tiles = g.B * pl.tiles_h * pl.tiles_w;
@@ -844,7 +881,8 @@ DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
     wsrc = wtmp;
   }
   k_pack_tc_weights<<<unsigned((total + 255) / 256), 256>>>(wsrc, t->wpack, k.Cout, k.Cin, k.kt, k.kh, k.kw,
-                                                           pl.var->CC, pl.n_split, pl.var->PAIR);
+                                                           pl.var->CC, pl.n_split, pl.var->PAIR,
+                                                           (pl.mode == MODE_KLOOP && pl.var->PAIR == 2) ? pl.kb : 0);
   e = cudaGetLastError();
   if (wtmp) { cudaDeviceSynchronize(); cudaFree(wtmp); }
   if (e != cudaSuccess) { err = cudaGetErrorString(e); dense_tc_destroy(t); return nullptr; }
@@ -861,7 +899,8 @@ DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
              pl.var->KH, pl.var->KW, pl.var->KC * 16, pl.var->CS > 1 ? ",split" : "",
              pl.var->PAIR > 1 ? ",pair" : "", mname);
   else
-    snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d%s>", pl.var->KT, pl.var->CC, pl.var->EG, mname);
+    snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d%s%s>", pl.var->KT, pl.var->CC, pl.var->EG,
+             pl.var->PAIR > 1 ? ",pair" : "", mname);
   if (getenv("CO_LOG"))
     fprintf(stderr, "[co] %s: %d parts, %lld tiles, %d stages x %d B, smem %zu B\n", buf, pl.n_split,
             (long long)pl.n_tiles, pl.stages, pl.a_stride, pl.smem);
@@ -991,7 +1030,22 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   p.bias = bias;
   const int per = std::max(1, t->num_sms / pair / pl.n_split);
   const int64_t grid = std::min<int64_t>(per, units_tiles) * pl.n_split * pair;
-  void* args[] = {&map, &p};
+  // KLOOP pairs stream their weight halves through a tensor map over the packed
+  // weights [part*2 + half][K/8][N/2][8]: box = one chunk (kb/8 K-groups)
+  CUtensorMap wmap = map;
+  if (pl.mode == MODE_KLOOP && pl.var->PAIR == 2) {
+    const int NBh = pl.var->KT * pl.var->CC / 2;
+    const int64_t nblk = int64_t(k.Cin) * k.kh * k.kw / pl.kb;        // kb-element K blocks
+    cuuint64_t dims[4] = {cuuint64_t(pl.kb), cuuint64_t(NBh), cuuint64_t(nblk), cuuint64_t(pl.n_split * 2)};
+    cuuint64_t strides[3] = {cuuint64_t(pl.kb) * 2, cuuint64_t(NBh) * pl.kb * 2, cuuint64_t(nblk) * NBh * pl.kb * 2};
+    cuuint32_t box[4] = {cuuint32_t(pl.kb), cuuint32_t(NBh), 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (encode(&wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, t->wpack, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, pl.kb == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  void* args[] = {&map, &wmap, &p};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(grid));
   cfg.blockDim = dim3(tc_threads(pl.var->EG, pl.var->CS));

@@ -45,6 +45,7 @@ CASES = {
 }
 FORCE_KLOOP = {"halo_c2like", "halo_kt5", "flat_c5like"}   # also run these through the K pipeline
 PAIR_CASES = ["halo_c2like", "halo_c2like_oddtiles", "flat_c5full"]   # CTA-pair (cta_group::2) variants
+KPAIR_CASES = ["kloop_c4l3like", "kloop_bigK", "kloop_st3", "stem_c4like", "kloop_s2"]   # KLOOP CTA pairs
 
 
 def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force_kloop=False, pair=False):
@@ -61,11 +62,13 @@ def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force
         os.environ["CO_TC_MODE"] = "kloop"
     if pair:
         os.environ["CO_TC_PAIR"] = "2"
+        os.environ["CO_TC_KPAIR"] = "2"
     try:
         conv, sm, Wq, bq = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="dense_tc")
     finally:
         os.environ.pop("CO_TC_MODE", None)
         os.environ.pop("CO_TC_PAIR", None)
+        os.environ.pop("CO_TC_KPAIR", None)
     if pair:
         assert "pair" in conv.kernel_name, conv.kernel_name
     ref_conv, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="direct")
@@ -105,7 +108,7 @@ def test_dense_tc_exact_integer_bitwise(case):
     assert np.array_equal(y, yd)
 
 
-@pytest.mark.parametrize("case", PAIR_CASES)
+@pytest.mark.parametrize("case", PAIR_CASES + KPAIR_CASES)
 def test_dense_tc_cta_pair(case):
     """The CTA-pair variants (M = 256 over two SMs, weights split by N) agree
     with the oracle and, in the exact-integer regime, bit for bit."""
