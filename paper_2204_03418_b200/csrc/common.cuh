@@ -30,24 +30,26 @@ struct Geom {
   int state_cl;          // physical state layout: 0 = quad-major, 1 = channels-last (see state_index)
   // tile-padded quad-major rows (dense tensor-core handles): state row of
   // output pixel (b, ho, wo) = tile * 128 + m, m = its TMEM lane in that tile
-  int spad, sTH, sTW, sRS, stiles_h, stiles_w;
-  int64_t splane;        // state rows per (slot, channel quad): B*HWo, or n_tiles*128 when padded
+  int spad, sflat, sTH, sTW, sRS, stiles_h, stiles_w;
+  int64_t splane;        // state rows per slot and channel quad: B*HWo, or n_tiles*128 when tile-blocked
 };
 
 // Physical state layouts (internal; co_state_get converts to the canonical one):
 //  quad-major (state_cl = 0, dense / direct kernels):
-//   S[slot][Cout/4][splane][4] fp32 -- for a fixed slot and channel quad the
-//   rows are contiguous float4s.  Direct kernel: row = b*HWo + pixel.  Dense
-//   tensor-core kernel (spad = 1): row = tile*128 + TMEM lane, so each warp of
-//   an epilogue moves exactly one aligned 512-byte run per access (its tiles
-//   hold e.g. 2 output rows of 56 in 58 lanes, which unpadded would straddle
-//   128-byte lines -- measured 21% of HBM bandwidth, scripts/bw_probe.cu);
+//   direct kernel: S[slot][Cout/4][B*HWo][4] fp32, row = b*HWo + pixel;
+//   dense tensor-core kernel (spad = 1, tile-blocked):
+//   S[slot][tile][Cout/4][128][4] -- the 128 rows of a tile are its TMEM lanes,
+//   so each warp of an epilogue moves exactly one aligned 512-byte run per
+//   access (its halo tiles hold e.g. 2 output rows of 56 in 58 lanes, which
+//   unpadded would straddle 128-byte lines: -21% HBM bandwidth in
+//   scripts/bw_probe.cu), and a thread's channel quads sit 2 KB apart, so
+//   every state access is an immediate offset from one base per slot;
 //  channels-last (state_cl = 1, depthwise kernels, Cout % 4 == 0):
 //   S[slot][B * Ho * Wo][Cout] fp32 -- a thread owns one (pixel, channel quad)
 //   and consecutive threads take consecutive quads, so the state, the
 //   channels-last frame and the output are all read/written contiguously.
 __host__ __device__ inline int64_t state_row(const Geom& g, int64_t pix) {
-  if (!g.spad) return pix;
+  if (!g.spad || g.sflat) return pix;   // FLAT tiles are 128 consecutive pixels
   const int64_t b = pix / g.HWo;
   const int r = int(pix - b * g.HWo);
   const int ho = r / g.Wo, wo = r - (r / g.Wo) * g.Wo;
@@ -57,7 +59,11 @@ __host__ __device__ inline int64_t state_row(const Geom& g, int64_t pix) {
 }
 __host__ __device__ inline int64_t state_index(const Geom& g, int slot, int64_t pix, int o) {
   if (g.state_cl) return (int64_t(slot) * (g.B * g.HWo) + pix) * g.Cout + o;
-  return ((int64_t(slot) * g.Cq + (o >> 2)) * g.splane + state_row(g, pix)) * 4 + (o & 3);
+  if (g.spad) {
+    const int64_t row = state_row(g, pix);
+    return (((int64_t(slot) * (g.splane >> 7) + (row >> 7)) * g.Cq + (o >> 2)) * 128 + (row & 127)) * 4 + (o & 3);
+  }
+  return ((int64_t(slot) * g.Cq + (o >> 2)) * g.splane + pix) * 4 + (o & 3);
 }
 
 // One step's clock decisions, computed on the host:

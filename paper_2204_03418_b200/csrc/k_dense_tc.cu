@@ -70,7 +70,7 @@ enum { MODE_HALO = 0, MODE_FLAT = 1, MODE_KLOOP = 2 };
 struct TcParams {
   int B, H, W, Cin, Cout, Ho, Wo;
   int64_t HWo, plane;             // plane = B * HWo
-  int64_t splane;                 // state rows per (slot, quad): n_tiles*128 (padded) or plane (FLAT)
+  int64_t splane;                 // state tiles * 128 (tile-blocked rows S[slot][tile][Cq][128][4])
   int kh, kw, ph, pw;
   int sh, sw, dh, dw;
   int mode;
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   constexpr int CPW = CC / CS;                         // output channels per warp
   const int m = q * 32 + lane;                         // accumulator row = tile pixel
   const int64_t plane = p.plane;
-  const int64_t splane = p.splane;                     // state rows per (slot, quad)
+  const int64_t stiles = p.splane >> 7;                // state tiles per slot (S[slot][tile][Cq][128][4])
   constexpr int NQ = CE / 4;                           // channel quads per thread and pass
   constexpr int NS = (KT > 1) ? KT - 1 : 1;
   int li = e;
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       pix = b * p.HWo + int64_t(ho) * p.Wo + wo;
     }
     // state row: the TMEM lane inside the tile (tile-padded layout, common.cuh)
-    const int64_t srow = (p.mode == MODE_FLAT) ? pix : tile * 128 + m;
+    const int64_t stile = tile;                        // state block of this item (row m of the tile)
     const uint32_t t_row = tmem + (uint32_t(q * 32) << 16) + uint32_t(buf * BUF);
 #pragma unroll 1
     for (int cb = cs * CPW; cb < (cs + 1) * CPW; cb += CE) {
@@ -414,18 +414,18 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       if (KT > 1 && valid && !(p.dbg & 1)) {
         if (p.emit) {
           const float4* src = reinterpret_cast<const float4*>(p.state) +
-                              (int64_t(p.slot[KT - 1]) * p.Cq + (c0 + cb) / 4) * splane + srow;
+                              ((int64_t(p.slot[KT - 1]) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
-          for (int i = 0; i < NQ; ++i) sv[0][i] = __ldcs(src + int64_t(i) * splane);
+          for (int i = 0; i < NQ; ++i) sv[0][i] = __ldcs(src + i * 128);
         }
         if (p.update) {
 #pragma unroll
           for (int k = 1; k < KT - 1; ++k) {
             if (p.slot[k] < 0) continue;
             const float4* src = reinterpret_cast<const float4*>(p.state) +
-                                (int64_t(p.slot[k]) * p.Cq + (c0 + cb) / 4) * splane + srow;
+                                ((int64_t(p.slot[k]) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
-            for (int i = 0; i < NQ; ++i) sv[k][i] = __ldcs(src + int64_t(i) * splane);
+            for (int i = 0; i < NQ; ++i) sv[k][i] = __ldcs(src + i * 128);
           }
         }
       }
@@ -475,7 +475,8 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
 #pragma unroll
         for (int k = KT - 2; k >= 1; --k) {
           if (p.slot[k] < 0) continue;
-          float4* dst = reinterpret_cast<float4*>(p.state) + (int64_t(p.slot[k]) * p.Cq + (c0 + cb) / 4) * splane + srow;
+          float4* dst = reinterpret_cast<float4*>(p.state) +
+                        ((int64_t(p.slot[k]) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
           for (int c = 0; c < CE; c += 16) {
             if (!(p.dbg & 8)) ptx::tmem_ld16(t_row + uint32_t(k * CC + cb + c), v);
@@ -485,14 +486,15 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
               for (int i = 0; i < 4; ++i) {
                 float4 t4 = sv[k][c / 4 + i];
                 t4.x += v[4 * i]; t4.y += v[4 * i + 1]; t4.z += v[4 * i + 2]; t4.w += v[4 * i + 3];
-                __stcs(dst + int64_t(c / 4 + i) * splane, t4);
+                __stcs(dst + (c / 4 + i) * 128, t4);
               }
             }
           }
         }
         // ---- (3) start the newest output (overwrites the emitted slot)
         if (p.slot[0] >= 0) {
-          float4* dst = reinterpret_cast<float4*>(p.state) + (int64_t(p.slot[0]) * p.Cq + (c0 + cb) / 4) * splane + srow;
+          float4* dst = reinterpret_cast<float4*>(p.state) +
+                        ((int64_t(p.slot[0]) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
           for (int c = 0; c < CE; c += 16) {
             if (!(p.dbg & 8)) ptx::tmem_ld16(t_row + uint32_t(cb + c), v);
@@ -500,7 +502,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
             if (valid && !(p.dbg & 1)) {
 #pragma unroll
               for (int i = 0; i < 4; ++i)
-                __stcs(dst + int64_t(c / 4 + i) * splane, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+                __stcs(dst + (c / 4 + i) * 128, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
             }
           }
         }
@@ -852,9 +854,15 @@ bool dense_tc_supported(const Geom& g) { return make_plan(g).ok && get_encode() 
 void dense_tc_state_layout(Geom& g) {
   const Plan pl = make_plan(g);
   g.spad = 0;
+  g.sflat = 0;
   g.splane = g.B * g.HWo;
-  if (!pl.ok || pl.mode == MODE_FLAT) return;     // FLAT tiles are 128 consecutive pixels already
+  if (!pl.ok) return;
   g.spad = 1;
+  if (pl.mode == MODE_FLAT) {          // tiles are 128 consecutive pixels: row = pixel
+    g.sflat = 1;
+    g.splane = (g.B * g.HWo + 127) / 128 * 128;
+    return;
+  }
   if (pl.mode == MODE_HALO) {
     g.sTH = pl.MT; g.sTW = g.Wo; g.sRS = pl.Wp; g.stiles_h = pl.tiles_per_stream; g.stiles_w = 1;
   } else {
