@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define CO_ABI_VERSION 1
+#define CO_ABI_VERSION 2
 #define CO_MAX_KT 32          /* temporal kernel extent supported by the kernels */
 
 typedef enum {
@@ -70,6 +70,14 @@ typedef enum {
   CO_KERNEL_DEPTHWISE = 3   /* CUDA-core depthwise stencil (groups == Cin == Cout, bf16) */
 } co_kernel;
 
+/* Per-stream state layout (BASELINE.json north_star "Per-stream state layout";
+ * SURVEY §8f row f1).  PSUM: the fp32 ring of R pending partial sums (each frame
+ * contracted with all kt slices once, 2(kt-1) fp32 state accesses per output).
+ * RAW: a ring of the last f input frames in the input dtype (SPEC's layout,
+ * S:227); a Ready step contracts the whole window (K = kt kh kw Cin/g),
+ * a non-Ready step only stores its frame.  Same outputs (Definition 1). */
+typedef enum { CO_STATE_PSUM = 0, CO_STATE_RAW = 1 } co_state_layout;
+
 typedef void* co_stream;                 /* cudaStream_t */
 typedef struct co_conv co_conv;          /* opaque: packed weights, fp32 state ring, host clock */
 typedef struct co_stack co_stack;        /* opaque: ordered layers + inter-layer activations */
@@ -88,6 +96,7 @@ typedef struct {
   int32_t out_dtype;                     /* co_dtype of y */
   int32_t activation;                    /* co_activation applied to emitted outputs (after bias) */
   int32_t kernel_choice;                 /* co_kernel; AUTO = dispatch rule */
+  int32_t state_layout;                  /* co_state_layout (PSUM = 0 default) */
 } co_conv_desc;
 
 /* Clock + geometry of a handle.  n and head are the host clock (a1). */
@@ -101,6 +110,7 @@ typedef struct {
   int32_t padding_t;         /* p */
   int32_t out_spatial[2];    /* S1', S2' */
   int32_t kernel_used;       /* co_kernel actually dispatched */
+  int32_t state_layout;      /* co_state_layout of the handle */
 } co_info;
 
 /* ---- lifetime ------------------------------------------------------------ */
@@ -165,11 +175,13 @@ int co_forward_out_len(const co_conv* h, int64_t T, int64_t* T_out);
 
 /* ---- state (Principle 3) -------------------------------------- */
 
-/* Canonical state: fp32 (R, B, S1', S2', Cout) dense, device memory.  Slot j
- * holds output i_next + j, i_next = ceil((n-d)/s) the next output to complete;
- * its value is the sum of contributions of the frames consumed so far (bias
- * excluded, A9), 0 for outputs that are never emitted (i < 0).  `bytes` must
- * equal co_state_bytes().  get fills *meta with the clock; set restores the
+/* Canonical state, PSUM layout: fp32 (R, B, S1', S2', Cout) dense, device memory.
+ * Slot j holds output i_next + j, i_next = ceil((n-d)/s) the next output to
+ * complete; its value is the sum of contributions of the frames consumed so far
+ * (bias excluded, A9), 0 for outputs that are never emitted (i < 0).
+ * RAW layout: in_dtype (f-1, B, S1, S2, Cin): slot j holds padded frame
+ * m-(f-1)+j, m = n + p the next frame's padded index (oldest first; the start
+ * padding is zero).  `bytes` must equal co_state_bytes().  get fills *meta with the clock; set restores the
  * clock from *meta (its geometry fields must match: CO_ERR_SHAPE).  A get ->
  * set round trip is bitwise (checkpoint / resume). */
 int co_state_bytes(const co_conv* h, size_t* bytes);

@@ -83,6 +83,7 @@ def lib():
             L.or_step_forward_steps.argtypes = [C.c_void_p, dp, C.c_int, C.c_int, C.c_int,
                                                 C.POINTER(C.c_uint8), dp]
             L.or_step_state.argtypes = [C.c_void_p, dp]
+            L.or_step_history.argtypes = [C.c_void_p, dp]
             L.or_bruteforce_tick.argtypes = [C.POINTER(_Desc), dp, dp, C.c_int, dp, C.c_int, dp]
             L.or_stack_new.argtypes = [C.c_int, C.POINTER(_Desc), C.POINTER(dp), C.POINTER(dp),
                                        C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int]
@@ -275,6 +276,15 @@ class StepMachine:
         n_ready = lib().or_step_forward_steps(self._h, _dp(x), T, int(pad_end), int(update_state),
                                               mask.ctypes.data_as(C.POINTER(C.c_uint8)), _dp(y))
         return np.ascontiguousarray(y[:, :, :n_ready]), mask.astype(bool)
+
+    def history(self) -> np.ndarray:
+        """The raw history (f-1, B, Cin, S1, S2): last f-1 padded frames, oldest first."""
+        f = self.d.receptive_field
+        H, W = self.d.in_hw
+        h = np.zeros((max(f - 1, 0), self.B, self.d.cin, H, W))
+        if f > 1:
+            lib().or_step_history(self._h, _dp(h))
+        return h
 
     def state(self) -> np.ndarray:
         """O5 canonical state (R,B,Cout,S1',S2')."""

@@ -342,6 +342,15 @@ void or_step_state(const or_step* sm, double* state) {
   }
 }
 
+/* The raw history itself (SPEC's state): the last f-1 padded
+ * frames, oldest first, hist[j] = padded frame m_next-(f-1)+j, frames before
+ * the start padding and the start padding itself being zero.  Read-only
+ * accessor (no arithmetic): the CUDA path's raw-input-ring layout (SURVEY
+ * §8f f1) exposes exactly this through co_state_get. */
+void or_step_history(const or_step* sm, double* out) {
+  memcpy(out, sm->hist, sizeof(double) * (size_t)(sm->f - 1) * sm->frame_elems);
+}
+
 /* ---------------------------------------------------------------- O7 */
 
 int or_bruteforce_tick(const or_desc* in, const double* W, const double* bias,

@@ -86,6 +86,8 @@ int or_step_forward_steps(or_step* sm, const double* x, int T, int pad_end,
  * (start padding included as zeros), bias excluded; outputs i < 0 (never
  * emitted) are 0.  Layout (R, B, Cout, S1', S2'). */
 void or_step_state(const or_step* sm, double* state);
+/* Raw history: the last f-1 padded frames, oldest first, (f-1, B, Cin, S1, S2). */
+void or_step_history(const or_step* sm, double* out);
 
 /* O7: brute-force sliding window.  hist holds every real frame fed
  * so far, (B,Cin,n+1,S1,S2) with n+1 frames (x_0..x_n).  Re-runs O2 with no

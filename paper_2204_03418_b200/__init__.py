@@ -81,7 +81,8 @@ class Conv:
                  bias: Optional[torch.Tensor] = None, stride=1, padding=0, dilation=1, groups: int = 1,
                  spatial_rank: int = 2, in_spatial: Sequence[int] = (1, 1), n_streams: int = 1,
                  dtype: torch.dtype = torch.bfloat16, out_dtype: Optional[torch.dtype] = None,
-                 activation: Optional[str] = None, kernel: str = "auto", device="cuda"):
+                 activation: Optional[str] = None, kernel: str = "auto", state_layout: str = "psum",
+                 device="cuda"):
         self.device = torch.device(device)
         self.dtype, self.out_dtype = dtype, (out_dtype or dtype)
         self.spatial_rank, self.n_streams = spatial_rank, n_streams
@@ -99,6 +100,8 @@ class Conv:
         d.out_dtype = _DT[self.out_dtype]
         d.activation = {None: _abi.CO_ACT_NONE, "none": _abi.CO_ACT_NONE, "relu": _abi.CO_ACT_RELU}[activation]
         d.kernel_choice = _abi.KERNELS[kernel]
+        d.state_layout = _abi.STATE_LAYOUTS[state_layout]
+        self.state_layout = state_layout
         self._desc = d
         w = weight.detach().to(dtype).contiguous()
         on_dev = int(w.is_cuda)
@@ -200,12 +203,17 @@ class Conv:
         check(lib().co_state_clean(self._h, _stream(stream)))
 
     def state_dict_stream(self, stream=None):
-        """Canonical state (R, B, *S', Cout) fp32 and the clock (co_state_get)."""
+        """Canonical state and the clock (co_state_get): PSUM (R, B, *S', Cout)
+        fp32; RAW (f-1, B, *S, Cin) in the input dtype (the last f-1 frames)."""
         nb = C.c_size_t()
         check(lib().co_state_bytes(self._h, C.byref(nb)))
         info = self.info()
-        st = torch.empty((info.ring_slots, self.n_streams) + self.out_spatial + (self.out_channels,),
-                         dtype=torch.float32, device=self.device)
+        if self.state_layout == "raw":
+            st = torch.empty((info.ring_slots, self.n_streams) + self.in_spatial + (self.in_channels,),
+                             dtype=self.dtype, device=self.device)
+        else:
+            st = torch.empty((info.ring_slots, self.n_streams) + self.out_spatial + (self.out_channels,),
+                             dtype=torch.float32, device=self.device)
         meta = CoInfo()
         check(lib().co_state_get(self._h, C.c_void_p(st.data_ptr()) if st.numel() else None, nb.value,
                                  C.byref(meta), _stream(stream)))
@@ -214,7 +222,7 @@ class Conv:
     def load_state_stream(self, state: torch.Tensor, meta: CoInfo, stream=None):
         nb = C.c_size_t()
         check(lib().co_state_bytes(self._h, C.byref(nb)))
-        state = state.to(torch.float32).contiguous()
+        state = state.to(self.dtype if self.state_layout == "raw" else torch.float32).contiguous()
         check(lib().co_state_set(self._h, C.c_void_p(state.data_ptr()) if state.numel() else None, nb.value,
                                  C.byref(meta), _stream(stream)))
 

@@ -17,6 +17,8 @@ if os.environ.get("CO_LIB_VARIANT"):            # experiment builds only (build.
 CO_OK, CO_ERR_ARG, CO_ERR_SHAPE, CO_ERR_LENGTH, CO_ERR_UNSUPPORTED, CO_ERR_CUDA, CO_ERR_OOM = 0, -1, -2, -3, -4, -5, -6
 CO_F32, CO_BF16 = 0, 1
 CO_ACT_NONE, CO_ACT_RELU = 0, 1
+CO_STATE_PSUM, CO_STATE_RAW = 0, 1
+STATE_LAYOUTS = {"psum": CO_STATE_PSUM, "raw": CO_STATE_RAW}
 CO_KERNEL_AUTO, CO_KERNEL_DIRECT, CO_KERNEL_DENSE_TC, CO_KERNEL_DEPTHWISE = 0, 1, 2, 3
 KERNELS = {"auto": CO_KERNEL_AUTO, "direct": CO_KERNEL_DIRECT, "dense_tc": CO_KERNEL_DENSE_TC,
            "depthwise": CO_KERNEL_DEPTHWISE}
@@ -35,13 +37,14 @@ class CoConvDesc(C.Structure):
                 ("groups", C.c_int32), ("kernel", C.c_int32 * 3), ("stride", C.c_int32 * 3),
                 ("padding", C.c_int32 * 3), ("dilation", C.c_int32 * 3), ("in_spatial", C.c_int32 * 2),
                 ("n_streams", C.c_int64), ("in_dtype", C.c_int32), ("w_dtype", C.c_int32),
-                ("out_dtype", C.c_int32), ("activation", C.c_int32), ("kernel_choice", C.c_int32)]
+                ("out_dtype", C.c_int32), ("activation", C.c_int32), ("kernel_choice", C.c_int32),
+                ("state_layout", C.c_int32)]
 
 
 class CoInfo(C.Structure):
     _fields_ = [("n", C.c_int64), ("head", C.c_int32), ("ring_slots", C.c_int32), ("delay", C.c_int32),
                 ("receptive_field", C.c_int32), ("stride_t", C.c_int32), ("padding_t", C.c_int32),
-                ("out_spatial", C.c_int32 * 2), ("kernel_used", C.c_int32)]
+                ("out_spatial", C.c_int32 * 2), ("kernel_used", C.c_int32), ("state_layout", C.c_int32)]
 
 
 class CoError(RuntimeError):

@@ -31,6 +31,11 @@ struct Geom {
   // tile-padded quad-major rows (dense tensor-core handles): state row of
   // output pixel (b, ho, wo) = tile * 128 + m, m = its TMEM lane in that tile
   int spad, sflat, sTH, sTW, sRS, stiles_h, stiles_w;
+  // RAW state layout (co_state_layout RAW): ring of f + 1 input
+  // frames [slot][B][H][W][Cin] in in_dtype (f data slots + one scratch slot
+  // for update_state = 0); a Ready step reads the window's kt slots
+  int raw;
+  int64_t frame_elems;   // H * W * Cin
   int64_t splane;        // state rows per slot and channel quad: B*HWo, or n_tiles*128 when tile-blocked
 };
 
@@ -89,6 +94,10 @@ template <> __device__ __forceinline__ float from_f<float>(float v) { return v; 
 template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
 __device__ __forceinline__ float activate(float v, int act) { return (act == 1 && v < 0.f) ? 0.f : v; }
+
+// RAW layout step (StepArgs.state = ring, slot[k] = ring slot of temporal tap k)
+cudaError_t launch_step_direct_raw(const Geom& g, const StepArgs& a, const float* w_direct, const float* bias,
+                                   cudaStream_t s);
 
 // ---- launchers implemented in the .cu files (host side) --------------------
 cudaError_t launch_step_direct(const Geom& g, const StepArgs& a, const float* w_direct, const float* bias,

@@ -151,6 +151,7 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
     if (t != CO_F32 && t != CO_BF16) return fail(CO_ERR_ARG, "dtype must be CO_F32 or CO_BF16");
   if (d->w_dtype != d->in_dtype) return fail(CO_ERR_ARG, "w_dtype must equal in_dtype");
   if (d->activation != CO_ACT_NONE && d->activation != CO_ACT_RELU) return fail(CO_ERR_ARG, "bad activation");
+  if (d->state_layout != CO_STATE_PSUM && d->state_layout != CO_STATE_RAW) return fail(CO_ERR_ARG, "bad state_layout");
   g = Geom{};
   g.rank = d->spatial_rank;
   g.Cin = d->in_channels; g.Cout = d->out_channels; g.groups = d->groups;
@@ -174,7 +175,21 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
   g.HWo = int64_t(g.Ho) * g.Wo;
   g.splane = g.B * g.HWo;
   g.slot_elems = int64_t(g.Cq) * 4 * g.splane;
+  g.raw = d->state_layout == CO_STATE_RAW;
+  g.frame_elems = int64_t(g.H) * g.W * g.Cin;
   return CO_OK;
+}
+
+// Device bytes of a handle's state: the fp32 partial-sum ring (PSUM), or the
+// ring of f + 1 input frames (RAW: f data slots + a scratch slot).
+static size_t state_alloc_bytes(const Geom& g) {
+  if (g.raw) return size_t(g.f + 1) * g.B * g.frame_elems * dsize(g.in_dtype);
+  return sizeof(float) * g.slot_elems * g.R;
+}
+// Canonical state bytes (co_state_bytes): PSUM (R, B, S', Cout) fp32; RAW (f-1, B, S, Cin) in_dtype.
+static size_t state_canon_bytes(const Geom& g) {
+  if (g.raw) return size_t(g.f - 1) * g.B * g.frame_elems * dsize(g.in_dtype);
+  return sizeof(float) * size_t(g.R) * g.B * g.HWo * g.Cout;
 }
 
 // The host clock (a1 / a5): which ring slot each temporal slice of the frame at
@@ -201,7 +216,7 @@ static int head_of(const Geom& g, int64_t n) {
 }
 
 static bool dense_tc_fits(const Geom& g) { return co::dense_tc_supported(g); }
-static bool depthwise_fits(const Geom& g) { return co::depthwise_supported(g); }
+static bool depthwise_fits(const Geom& g) { return !g.raw && co::depthwise_supported(g); }
 
 extern "C" int co_conv_create(const co_conv_desc* desc, const void* weights, const float* bias,
                               int weights_on_device, co_conv** out) {
@@ -259,9 +274,10 @@ extern "C" int co_conv_create(const co_conv_desc* desc, const void* weights, con
     e = cudaMemset(h->bias, 0, sizeof(float) * g.Cout);
   }
   if (e != cudaSuccess) { freew(); return cleanup(fail(CO_ERR_CUDA, "bias: %s", cudaGetErrorString(e))); }
-  if (g.R > 0) {
-    if ((e = cudaMalloc(&h->state, sizeof(float) * g.slot_elems * g.R)) != cudaSuccess) { freew(); return cleanup(fail(CO_ERR_OOM, "state (%lld bytes): %s", (long long)(sizeof(float) * g.slot_elems * g.R), cudaGetErrorString(e))); }
-    if ((e = cudaMemset(h->state, 0, sizeof(float) * g.slot_elems * g.R)) != cudaSuccess) { freew(); return cleanup(fail(CO_ERR_CUDA, "%s", cudaGetErrorString(e))); }
+  if (state_alloc_bytes(g) > 0) {
+    const size_t sb = state_alloc_bytes(g);
+    if ((e = cudaMalloc(&h->state, sb)) != cudaSuccess) { freew(); return cleanup(fail(CO_ERR_OOM, "state (%lld bytes): %s", (long long)sb, cudaGetErrorString(e))); }
+    if ((e = cudaMemset(h->state, 0, sb)) != cudaSuccess) { freew(); return cleanup(fail(CO_ERR_CUDA, "%s", cudaGetErrorString(e))); }
   }
   h->kname = "k_step_direct";
   if (kern == CO_KERNEL_DENSE_TC) {
@@ -308,6 +324,8 @@ extern "C" int co_conv_info(const co_conv* h, co_info* info) {
   info->out_spatial[0] = g.Ho;
   info->out_spatial[1] = g.Wo;
   info->kernel_used = h->kernel_used;
+  info->state_layout = g.raw ? CO_STATE_RAW : CO_STATE_PSUM;
+  if (g.raw) info->ring_slots = g.f - 1;
   return CO_OK;
 }
 
@@ -323,6 +341,15 @@ extern "C" const char* co_kernel_name(const co_conv* h) { return h ? h->kname.c_
 
 static int launch_step(co_conv* h, const StepArgs& a, cudaStream_t s) {
   cudaError_t e;
+  if (h->g.raw) {
+    switch (h->kernel_used) {
+      case CO_KERNEL_DENSE_TC: e = co::dense_tc_step(h->tc, h->g, a, h->bias, s); break;
+      case CO_KERNEL_DEPTHWISE: e = co::depthwise_step(h->dw, h->g, a, h->bias, s); break;
+      default: e = co::launch_step_direct_raw(h->g, a, h->w_direct, h->bias, s); break;
+    }
+    if (e != cudaSuccess) return fail(CO_ERR_CUDA, "raw step kernel %s: %s", h->kname.c_str(), cudaGetErrorString(e));
+    return CO_OK;
+  }
   switch (h->kernel_used) {
     case CO_KERNEL_DENSE_TC: e = co::dense_tc_step(h->tc, h->g, a, h->bias, s); break;
     case CO_KERNEL_DEPTHWISE: e = co::depthwise_step(h->dw, h->g, a, h->bias, s); break;
@@ -333,8 +360,40 @@ static int launch_step(co_conv* h, const StepArgs& a, cudaStream_t s) {
 }
 
 // One clock tick on `state` (the handle's ring or a scratch copy).
+// RAW layout tick: store the frame in its ring slot (or the scratch slot when
+// the state must not change), then on a Ready tick contract the window's kt
+// ring slots; a non-Ready tick moves one frame and launches nothing.
+static int step_raw(co_conv* h, int64_t& n, float* state, const void* x, int64_t x_bstride, void* y,
+                    int64_t y_bstride, int update_state, int* ready, cudaStream_t s) {
+  const Geom& g = h->g;
+  const int64_t m = n + g.pt;
+  const int r = (n >= g.delay) && floor_mod(n - g.delay, g.st) == 0;
+  const int cur = update_state ? int(floor_mod(m, g.f)) : g.f;
+  const size_t fb = size_t(g.frame_elems) * dsize(g.in_dtype);
+  char* slot = reinterpret_cast<char*>(state) + size_t(cur) * g.B * fb;
+  if (x) CO_CUDA(cudaMemcpy2DAsync(slot, fb, x, size_t(x_bstride) * dsize(g.in_dtype), fb, g.B,
+                                   cudaMemcpyDeviceToDevice, s));
+  else CO_CUDA(cudaMemsetAsync(slot, 0, g.B * fb, s));
+  if (r) {
+    StepArgs a;
+    for (int k = 0; k < co::kMaxKt; ++k) a.slot[k] = -1;
+    for (int k = 0; k + 1 < g.kt; ++k) a.slot[k] = int(floor_mod(m - int64_t(g.kt - 1 - k) * g.dt, g.f));
+    a.slot[g.kt - 1] = cur;
+    a.x = nullptr; a.x_bstride = g.frame_elems;
+    a.y = y; a.y_bstride = y_bstride;
+    a.state = state;
+    a.emit = 1;
+    a.update = 0;
+    if (int rc = launch_step(h, a, s)) return rc;
+  }
+  if (update_state) ++n;
+  if (ready) *ready = r;
+  return CO_OK;
+}
+
 static int step_impl(co_conv* h, int64_t& n, float* state, const void* x, int64_t x_bstride, void* y,
                      int64_t y_bstride, int update_state, int* ready, cudaStream_t s) {
+  if (h->g.raw) return step_raw(h, n, state, x, x_bstride, y, y_bstride, update_state, ready, s);
   StepArgs a;
   const int r = clock_args(h->g, n, a);
   a.x = x; a.x_bstride = x_bstride;
@@ -458,9 +517,9 @@ extern "C" int co_forward_steps(co_conv* h, const void* x, int64_t T, void* y, u
   float* state = h->state;
   int64_t n = h->n;
   float* scratch = nullptr;
-  if (!update_state && g.R > 0) {
-    CO_CUDA(cudaMallocAsync((void**)&scratch, sizeof(float) * g.slot_elems * g.R, s));
-    CO_CUDA(cudaMemcpyAsync(scratch, h->state, sizeof(float) * g.slot_elems * g.R, cudaMemcpyDeviceToDevice, s));
+  if (!update_state && state_alloc_bytes(g) > 0) {
+    CO_CUDA(cudaMallocAsync((void**)&scratch, state_alloc_bytes(g), s));
+    CO_CUDA(cudaMemcpyAsync(scratch, h->state, state_alloc_bytes(g), cudaMemcpyDeviceToDevice, s));
     state = scratch;
   }
   int64_t& clock = update_state ? h->n : n;
@@ -504,7 +563,7 @@ extern "C" int co_forward(co_conv* h, const void* x, int64_t T, void* y, int64_t
 extern "C" int co_state_bytes(const co_conv* h, size_t* bytes) {
   if (!h || !bytes) return fail(CO_ERR_ARG, "null argument");
   const Geom& g = h->g;
-  *bytes = sizeof(float) * size_t(g.R) * g.B * g.HWo * g.Cout;
+  *bytes = state_canon_bytes(g);
   return CO_OK;
 }
 
@@ -514,7 +573,15 @@ extern "C" int co_state_get(co_conv* h, void* dst, size_t bytes, co_info* meta, 
   co_state_bytes(h, &need);
   if (bytes != need) return fail(CO_ERR_SHAPE, "state bytes %zu != %zu", bytes, need);
   const Geom& g = h->g;
-  if (need) {
+  if (need && g.raw) {   // canonical slot j = padded frame m-(f-1)+j, m = n + p
+    if (!dst) return fail(CO_ERR_ARG, "null dst");
+    const size_t sb = size_t(g.B) * g.frame_elems * dsize(g.in_dtype);
+    for (int j = 0; j < g.f - 1; ++j) {
+      const int src = int(floor_mod(h->n + g.pt - (g.f - 1) + j, g.f));
+      CO_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + j * sb, reinterpret_cast<char*>(h->state) + src * sb, sb,
+                              cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    }
+  } else if (need) {
     if (!dst) return fail(CO_ERR_ARG, "null dst");
     const int64_t i_next = ceil_div(h->n - g.delay, g.st);
     cudaError_t e = co::launch_state_get(g, h->state, (float*)dst, head_of(g, h->n), i_next, h->n + g.pt,
@@ -531,10 +598,18 @@ extern "C" int co_state_set(co_conv* h, const void* src, size_t bytes, const co_
   co_state_bytes(h, &need);
   if (bytes != need) return fail(CO_ERR_SHAPE, "state bytes %zu != %zu", bytes, need);
   const Geom& g = h->g;
-  if (meta->ring_slots != g.R || meta->delay != g.delay || meta->stride_t != g.st ||
+  if (meta->ring_slots != (g.raw ? g.f - 1 : g.R) || meta->delay != g.delay || meta->stride_t != g.st ||
       meta->receptive_field != g.f || meta->out_spatial[0] != g.Ho || meta->out_spatial[1] != g.Wo || meta->n < 0)
     return fail(CO_ERR_SHAPE, "state meta does not match this layer");
-  if (need) {
+  if (need && g.raw) {
+    if (!src) return fail(CO_ERR_ARG, "null src");
+    const size_t sb = size_t(g.B) * g.frame_elems * dsize(g.in_dtype);
+    for (int j = 0; j < g.f - 1; ++j) {
+      const int dstslot = int(floor_mod(meta->n + g.pt - (g.f - 1) + j, g.f));
+      CO_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(h->state) + dstslot * sb, static_cast<const char*>(src) + j * sb,
+                              sb, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    }
+  } else if (need) {
     if (!src) return fail(CO_ERR_ARG, "null src");
     cudaError_t e = co::launch_state_set(g, h->state, (const float*)src, head_of(g, meta->n), (cudaStream_t)stream);
     if (e != cudaSuccess) return fail(CO_ERR_CUDA, "state_set: %s", cudaGetErrorString(e));
@@ -546,7 +621,7 @@ extern "C" int co_state_set(co_conv* h, const void* src, size_t bytes, const co_
 extern "C" int co_state_clean(co_conv* h, co_stream stream) {
   if (!h) return fail(CO_ERR_ARG, "null handle");
   const Geom& g = h->g;
-  if (g.R > 0) CO_CUDA(cudaMemsetAsync(h->state, 0, sizeof(float) * g.slot_elems * g.R, (cudaStream_t)stream));
+  if (state_alloc_bytes(g) > 0) CO_CUDA(cudaMemsetAsync(h->state, 0, state_alloc_bytes(g), (cudaStream_t)stream));
   h->n = 0;
   return CO_OK;
 }

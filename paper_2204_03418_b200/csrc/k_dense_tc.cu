@@ -849,7 +849,7 @@ struct DenseTC {
   std::string name;
 };
 
-bool dense_tc_supported(const Geom& g) { return make_plan(g).ok && get_encode() != nullptr; }
+bool dense_tc_supported(const Geom& g) { return !g.raw && make_plan(g).ok && get_encode() != nullptr; }
 
 void dense_tc_state_layout(Geom& g) {
   const Plan pl = make_plan(g);

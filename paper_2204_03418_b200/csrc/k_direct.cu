@@ -73,6 +73,28 @@ __global__ void __launch_bounds__(256) k_step_direct(Geom g, StepArgs a, const f
   if (a.slot[0] >= 0) a.state[state_index(g, a.slot[0], pix, o)] = P(0);
 }
 
+// RAW layout: the whole window column from the ring of input
+// frames -- y = b + sum_k W[:,:,k] (*) frame(slot[k]) -- with no state written
+// (the host stored the frame in its ring slot before the launch).
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(256) k_step_direct_raw(Geom g, StepArgs a, const float* __restrict__ w,
+                                                         const float* __restrict__ bias) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = g.B * g.HWo * g.Cout;
+  if (idx >= total) return;
+  const int o = int(idx % g.Cout);
+  const int64_t pix = idx / g.Cout;
+  const int64_t b = pix / g.HWo;
+  const int p = int(pix - b * g.HWo);
+  const int ho = p / g.Wo, wo = p - (p / g.Wo) * g.Wo;
+  const int grp = o / g.cog;
+  const Tin* ring = static_cast<const Tin*>(static_cast<const void*>(a.state));
+  float acc = bias ? bias[o] : 0.f;
+  for (int k = 0; k < g.kt; ++k)
+    acc += slice_partial<Tin>(g, ring + (int64_t(a.slot[k]) * g.B + b) * g.frame_elems, w, k, ho, wo, o, grp);
+  static_cast<Tout*>(a.y)[b * a.y_bstride + int64_t(p) * g.Cout + o] = from_f<Tout>(activate(acc, g.act));
+}
+
 template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(256) k_forward_direct(Geom g, const Tin* __restrict__ x, int64_t T,
                                                         Tout* __restrict__ y, int64_t Tp,
@@ -161,6 +183,22 @@ cudaError_t launch_step_direct(const Geom& g, const StepArgs& a, const float* w,
     k_step_direct<__nv_bfloat16, float><<<nb, 256, 0, s>>>(g, a, w, bias);
   else
     k_step_direct<__nv_bfloat16, __nv_bfloat16><<<nb, 256, 0, s>>>(g, a, w, bias);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step_direct_raw(const Geom& g, const StepArgs& a, const float* w, const float* bias,
+                                   cudaStream_t s) {
+  const int64_t n = g.B * g.HWo * g.Cout;
+  if (n == 0) return cudaSuccess;
+  const unsigned nb = blocks_for(n, 256);
+  if (g.in_dtype == F32 && g.out_dtype == F32)
+    k_step_direct_raw<float, float><<<nb, 256, 0, s>>>(g, a, w, bias);
+  else if (g.in_dtype == F32 && g.out_dtype == BF16)
+    k_step_direct_raw<float, __nv_bfloat16><<<nb, 256, 0, s>>>(g, a, w, bias);
+  else if (g.in_dtype == BF16 && g.out_dtype == F32)
+    k_step_direct_raw<__nv_bfloat16, float><<<nb, 256, 0, s>>>(g, a, w, bias);
+  else
+    k_step_direct_raw<__nv_bfloat16, __nv_bfloat16><<<nb, 256, 0, s>>>(g, a, w, bias);
   return cudaGetLastError();
 }
 

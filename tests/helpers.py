@@ -36,7 +36,7 @@ def logical_step_shape(d: O.Desc, B: int):
 
 
 def make_pair(d: O.Desc, W: np.ndarray, b, B: int, dtype=torch.float32, out_dtype=torch.float32,
-              kernel="auto", activation=None):
+              kernel="auto", activation=None, state_layout="psum"):
     """(CUDA-path Conv, oracle StepMachine) with identical weights."""
     import paper_2204_03418_b200 as co
     Wt = torch.from_numpy(np.asarray(W, np.float64)).to(dtype)
@@ -45,7 +45,7 @@ def make_pair(d: O.Desc, W: np.ndarray, b, B: int, dtype=torch.float32, out_dtyp
                    bias=None if bt is None else bt.cuda(), stride=d.stride, padding=d.padding,
                    dilation=d.dilation, groups=d.groups, spatial_rank=d.spatial_rank,
                    in_spatial=d.in_spatial, n_streams=B, dtype=dtype, out_dtype=out_dtype,
-                   activation=activation, kernel=kernel)
+                   activation=activation, kernel=kernel, state_layout=state_layout)
     Wq = Wt.double().numpy()
     bq = None if bt is None else bt.double().numpy()
     sm = O.StepMachine(d, Wq, bq, B)

@@ -423,3 +423,24 @@ def test_stack_bf16_activations_exact_regime():
         y = st.forward_step(x[:, :, t])
         if t >= 2:
             assert np.array_equal(y, h[:, :, t - 2])
+
+
+def test_step_history_is_the_last_padded_frames():
+    """O3's raw history (the RAW layout's canonical state): after n steps it holds
+    the padded frames n+p-(f-1) .. n+p-1, i.e. the real frames fed so far and
+    zero frames for the start padding, oldest first."""
+    rng = np.random.default_rng(7)
+    d = O.Desc(2, 3, 4, (3, 3, 3), padding=(1, 1, 1), dilation=(2, 1, 1), in_spatial=(4, 5))
+    f, p = d.receptive_field, d.padding[0]
+    sm = O.StepMachine(d, rng.standard_normal(d.w_shape), None, 2)
+    xs = [rng.standard_normal((2, 3, 4, 5)) for _ in range(7)]
+    for n, x in enumerate(xs, start=1):
+        sm.forward_step(x)
+        h = sm.history()
+        assert h.shape == (f - 1, 2, 3, 4, 5)
+        for j in range(f - 1):
+            q = n + p - (f - 1) + j                 # padded index of history slot j
+            want = xs[q - p] if q >= p else np.zeros_like(x)
+            assert np.array_equal(h[j], want)
+    sm.forward_step(rng.standard_normal((2, 3, 4, 5)), update_state=False)
+    assert np.array_equal(sm.history()[-1], xs[-1])   # update_state=False leaves it unchanged
