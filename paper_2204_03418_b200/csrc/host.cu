@@ -216,7 +216,7 @@ static int head_of(const Geom& g, int64_t n) {
 }
 
 static bool dense_tc_fits(const Geom& g) { return co::dense_tc_supported(g); }
-static bool depthwise_fits(const Geom& g) { return !g.raw && co::depthwise_supported(g); }
+static bool depthwise_fits(const Geom& g) { return co::depthwise_supported(g); }
 
 extern "C" int co_conv_create(const co_conv_desc* desc, const void* weights, const float* bias,
                               int weights_on_device, co_conv** out) {

@@ -87,6 +87,8 @@ struct TcParams {
   int w_off;                      // stages start here (1 KB aligned)
   int slot[kMaxKt];
   int emit, update, act, out_f32;
+  int raw_kh, raw_B;              // RAW layout: real spatial kh (the K loop walks kt*kh rows), streams per ring slot
+  int ring_slot[kMaxKt];          // RAW layout: ring slot of temporal tap k
   int swa, a_rows;                // A staged swizzled: 0 none, 1 128-B rows ([Cin/64][rows][128 B]),
                                   // 2 64-B rows (KLOOP with kb = 32); rows per 64-channel block
   int dbg;                        // CO_TC_DEBUG bits (experiments only): 1 no state/y traffic, 2 no MMA,
@@ -230,7 +232,11 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
           const int ho0 = (r / p.tiles_w) * p.TH, wo0 = (r % p.tiles_w) * p.TW;
           const uint8_t* bsrc = wsrc;
           int kg = 0;                                   // K-group (8 channels) index of the chunk
-          for (int u = 0; u < p.kh; ++u)
+          for (int uu = 0; uu < p.kh; ++uu) {
+            // RAW layout: row uu = (temporal tap k, spatial row u), frame from ring slot k
+            const int kk = p.raw_kh ? uu / p.raw_kh : 0;
+            const int u = p.raw_kh ? uu - kk * p.raw_kh : uu;
+            const int bb = p.raw_kh ? b + p.ring_slot[kk] * p.raw_B : b;
             for (int v = 0; v < p.kw; ++v)
               for (int cb = 0; cb < p.n_cb; ++cb) {
                 ptx::mbar_wait(&empty[s], ph ^ 1);
@@ -239,17 +245,18 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
                 const int cc = p.swa ? cb : cb * (p.kb / 8);   // swizzled: kb-channel blocks
                 if constexpr (PAIR == 2) {
                   if (leader) ptx::mbar_arrive_expect_tx(&full[s], (p.a_bytes + p.b_bytes) * PAIR);
-                  ptx::tma_load_5d_pair(dst, &tmap, &full[s], 0, cw, ch, cc, b);
+                  ptx::tma_load_5d_pair(dst, &tmap, &full[s], 0, cw, ch, cc, bb);
                   ptx::tma_load_4d_pair(dst + p.b_off, &wmap, &full[s], 0, 0, kg / (p.kb / 8), part * PAIR + int(rank));
                 } else {
                   ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes + p.b_bytes);
-                  ptx::tma_load_5d(dst, &tmap, &full[s], 0, cw, ch, cc, b);
+                  ptx::tma_load_5d(dst, &tmap, &full[s], 0, cw, ch, cc, bb);
                   ptx::bulk_g2s(dst + p.b_off, bsrc, p.b_bytes, &full[s]);
                 }
                 bsrc += p.b_bytes;
                 kg += p.kb / 8;
                 if (++s == p.stages) { s = 0; ph ^= 1; }
               }
+          }
         }
       }
     }
@@ -820,6 +827,17 @@ Plan make_plan(const Geom& g) {
   Plan pl;
   if (g.in_dtype != BF16 || g.groups != 1 || g.Cout % 4 != 0) return pl;
   pl.gk = g;
+  if (g.raw) {
+    // RAW layout: one window contraction per Ready step, the kt temporal taps
+    // folded into K (weights viewed as (Cout, Cin, 1, kt*kh, kw), the same
+    // memory); always the K pipeline, one accumulator (no slices, no state)
+    if (g.Cin % 16 != 0) return pl;
+    Geom& k = pl.gk;
+    k.kh = g.kt * g.kh; k.kt = 1;
+    pl.ok = plan_kloop(k, pl);
+    if (pl.ok) pl.n_split = g.Cout / pl.var->CC;
+    return pl;
+  }
   if (g.Cin < 16 && g.Cin * g.kw <= 64) {
     // small-Cin stem: W-im2col'd frame, kernel (kt, kh, 1), stride (st, sh, 1)
     pl.wcols = 1;
@@ -849,14 +867,14 @@ struct DenseTC {
   std::string name;
 };
 
-bool dense_tc_supported(const Geom& g) { return !g.raw && make_plan(g).ok && get_encode() != nullptr; }
+bool dense_tc_supported(const Geom& g) { return make_plan(g).ok && get_encode() != nullptr; }
 
 void dense_tc_state_layout(Geom& g) {
   const Plan pl = make_plan(g);
   g.spad = 0;
   g.sflat = 0;
   g.splane = g.B * g.HWo;
-  if (!pl.ok) return;
+  if (!pl.ok || g.raw) return;                // RAW: the state is the frame ring
   g.spad = 1;
   if (pl.mode == MODE_FLAT) {          // tiles are 128 consecutive pixels: row = pixel
     g.sflat = 1;
@@ -941,7 +959,12 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   const void* x = a.x;
   int64_t x_bstride = a.x_bstride;
   const int64_t frame = int64_t(g.H) * g.W * g.Cin;
-  if (pl.wcols) {
+  int64_t n_batch = k.B;                        // the tensor map's outermost extent
+  if (g.raw) {                                  // the frame ring: (f + 1) slots of B streams
+    x = a.state;
+    x_bstride = frame;
+    n_batch = k.B * (g.f + 1);
+  } else if (pl.wcols) {
     // small-Cin stem: W-im2col the frame (a zero frame stays zero)
     const int64_t kframe = int64_t(k.H) * k.W * k.Cin;
     if (cudaError_t e = ensure_stage(t, size_t(g.B) * kframe * 2)) return e;
@@ -980,7 +1003,7 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
                CU_TENSOR_MAP_INTERLEAVE_NONE, pl.swa ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
-    cuuint64_t dims[5] = {8, cuuint64_t(k.W), cuuint64_t(k.H), cuuint64_t(k.Cin / 8), cuuint64_t(k.B)};
+    cuuint64_t dims[5] = {8, cuuint64_t(k.W), cuuint64_t(k.H), cuuint64_t(k.Cin / 8), cuuint64_t(n_batch)};
     cuuint64_t strides[4] = {cuuint64_t(k.Cin) * 2, cuuint64_t(k.W) * k.Cin * 2, 16, cuuint64_t(x_bstride) * 2};
     cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
     CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE;
@@ -1028,6 +1051,9 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   p.emit = a.emit; p.update = a.update; p.act = g.act; p.out_f32 = (g.out_dtype == F32);
   static const int dbg = getenv("CO_TC_DEBUG") ? atoi(getenv("CO_TC_DEBUG")) : 0;
   p.dbg = dbg;
+  p.raw_kh = g.raw ? g.kh : 0;
+  p.raw_B = int(g.B);
+  for (int i = 0; i < kMaxKt; ++i) p.ring_slot[i] = g.raw ? a.slot[i] : -1;
   p.swa = pl.swa;
   p.a_rows = pl.chunk_stride / 16;
   p.Cq = g.Cq;

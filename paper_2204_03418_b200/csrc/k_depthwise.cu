@@ -60,6 +60,7 @@ struct DwParams {
   int TH, bands;                        // K2 tiling: TH output rows per tile
   int64_t n_tiles;
   int WC, HR;                           // halo width (W + 2 pw) and rows (TH + kh - 1)
+  int64_t frame;                        // RAW layout: elements of one stream's frame (H*W*C)
 };
 
 __device__ __forceinline__ float4 ld_bf16x4(const __nv_bfloat16* p) {
@@ -272,6 +273,46 @@ __global__ void __launch_bounds__(kDwThreads, CO_DW_T_MINB) k_step_dw_t(const Dw
   }
 }
 
+// ------------------------------------------------------------------ RAW layout
+// (SURVEY §8f f1): a Ready step reads the window's kt frames from the frame
+// ring (slot[k]) and writes y; no state traffic beyond those reads.  Thread =
+// (output pixel, channel quad), NB items per thread with all their loads
+// issued before the FMAs; taps read straight from global memory (the 3x3
+// neighbours of consecutive pixels are L1 hits).
+template <int KT, int KH, int KW>
+__global__ void __launch_bounds__(kDwThreads) k_step_dw_raw(const DwParams p) {
+  const int64_t n_items = p.plane * p.Cq;
+  const int64_t stride = int64_t(gridDim.x) * kDwThreads;
+  const __nv_bfloat16* ring = reinterpret_cast<const __nv_bfloat16*>(p.state);
+  for (int64_t it = int64_t(blockIdx.x) * kDwThreads + threadIdx.x; it < n_items; it += stride) {
+    const int q = int(it % p.Cq);
+    const int64_t pix = it / p.Cq;
+    const int64_t b = pix / p.HWo;
+    const int pin = int(pix - b * p.HWo);
+    const int ho = pin / p.Wo, wo = pin - (pin / p.Wo) * p.Wo;
+    float4 acc = __ldg(reinterpret_cast<const float4*>(p.bias) + q);
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+      const __nv_bfloat16* fr = ring + (int64_t(p.slot[k]) * (p.plane / p.HWo) + b) * p.frame + 4 * q;
+      float4 part = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < KH; ++u) {
+        const int hi = ho + u - p.ph;
+        if (hi < 0 || hi >= p.H) continue;
+#pragma unroll
+        for (int v = 0; v < KW; ++v) {
+          const int wi = wo + v - p.pw;
+          if (wi < 0 || wi >= p.W) continue;
+          const float4 w = __ldg(reinterpret_cast<const float4*>(p.w + ((k * KH + u) * KW + v) * p.C) + q);
+          part = f4_fma(w, ld_bf16x4(fr + (int64_t(hi) * p.W + wi) * p.C), part);
+        }
+      }
+      acc = f4_add(acc, part);
+    }
+    st_out4(p, b, pin, q, f4_act(acc, p.act));
+  }
+}
+
 // (C, 1, kt, kh, kw) bf16 -> [kt][kh][kw][C] fp32 (exact)
 __global__ void k_pack_dw(const __nv_bfloat16* __restrict__ w, float* __restrict__ out, int C, int kt, int kh,
                           int kw) {
@@ -291,12 +332,14 @@ struct DwVariant {
   int KT, KH, KW;
   DwFn fn;
   int PX = 1;                           // K2: output pixels per thread strip
+  DwFn raw = nullptr;                   // RAW-layout kernel for this shape
 };
 #ifndef CO_DW_PX
 #define CO_DW_PX 2                      // output pixels per thread strip (experiments: -DCO_DW_PX=n)
 #endif
-#define CO_DW_ST(kt, kh, kw) {kt, kh, kw, (DwFn)k_step_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>, (kt <= 3 ? CO_DW_PX : 2)}
-#define CO_DW_T(kt) {kt, 1, 1, (DwFn)k_step_dw_t<kt>}
+#define CO_DW_ST(kt, kh, kw) {kt, kh, kw, (DwFn)k_step_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>, \
+                              (kt <= 3 ? CO_DW_PX : 2), (DwFn)k_step_dw_raw<kt, kh, kw>}
+#define CO_DW_T(kt) {kt, 1, 1, (DwFn)k_step_dw_t<kt>, 1, (DwFn)k_step_dw_raw<kt, 1, 1>}
 const DwVariant kDwVariants[] = {
     CO_DW_ST(1, 3, 3), CO_DW_ST(2, 3, 3), CO_DW_ST(3, 3, 3), CO_DW_ST(5, 3, 3), CO_DW_ST(3, 5, 5),
     CO_DW_T(2), CO_DW_T(3), CO_DW_T(4), CO_DW_T(5), CO_DW_T(7), CO_DW_T(9),
@@ -322,7 +365,7 @@ bool make_dw_plan(const Geom& g, DwPlan& pl) {
   }
   if (!pl.var) return false;
   pl.temporal = temporal;
-  if (temporal) return true;
+  if (temporal || g.raw) return true;   // no staged halo (RAW reads the ring directly)
   // staged halo width: every strip reads PX + kw - 1 columns (zero beyond the frame)
   const int px = pl.var->PX;
   pl.WC = std::max(g.W + 2 * g.pw, (g.Wo + px - 1) / px * px + g.kw - 1);
@@ -371,6 +414,16 @@ Depthwise* depthwise_create(const Geom& g, const void* w_dev, std::string& err) 
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (g.raw) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.var->raw, kDwThreads, 0);
+    per_sm = std::max(per_sm, 1);
+    const int64_t items = g.B * g.HWo * (g.Cout / 4);
+    t->grid = int(std::max<int64_t>(1, std::min<int64_t>((items + kDwThreads - 1) / kDwThreads, int64_t(sms) * per_sm)));
+    char buf[96];
+    snprintf(buf, sizeof(buf), "k_step_dw_raw<%d,%d,%d>", pl.var->KT, pl.var->KH, pl.var->KW);
+    t->name = buf;
+    return t;
+  }
   if (!pl.temporal) {
     e = cudaFuncSetAttribute(pl.var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
     if (e != cudaSuccess) { err = cudaGetErrorString(e); depthwise_destroy(t); return nullptr; }
@@ -414,10 +467,14 @@ cudaError_t depthwise_step(Depthwise* t, const Geom& g, const StepArgs& a, const
   p.bias = bias;
   for (int k = 0; k < kMaxKt; ++k) p.slot[k] = a.slot[k];
   p.emit = a.emit; p.update = a.update; p.act = g.act; p.out_f32 = (g.out_dtype == F32);
+  p.frame = g.frame_elems;
   p.C = g.Cout; p.Cq = g.Cout / 4; p.H = g.H; p.W = g.W; p.Ho = g.Ho; p.Wo = g.Wo; p.ph = g.ph; p.pw = g.pw;
   p.HWo = g.HWo; p.plane = g.B * g.HWo;
   p.TH = pl.TH; p.bands = pl.bands; p.n_tiles = pl.n_tiles; p.WC = pl.WC; p.HR = pl.HR;
   void* args[] = {&p};
+  if (g.raw)
+    return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->raw), dim3(unsigned(t->grid)), dim3(kDwThreads),
+                            args, 0, s);
   return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->fn), dim3(unsigned(t->grid)),
                           dim3(pl.temporal ? kDwThreads : pl.threads), args, pl.temporal ? 0 : pl.smem, s);
 }

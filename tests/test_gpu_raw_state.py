@@ -106,3 +106,75 @@ def test_raw_state_roundtrip_purity_and_folds(seed):
         assert torch.equal(ys[:, :, i], f)
     if d.out_len(T) >= 1:
         assert rel_err(np_of(ys), O.forward(d, Wq, bq, clip)) <= 1e-4
+
+
+RAW_DENSE = {
+    "c2like": dict(desc=O.Desc(2, 64, 64, (3, 3, 3), padding=(0, 1, 1), in_spatial=(13, 24)), B=3),
+    "s2": dict(desc=O.Desc(2, 128, 128, (3, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1), in_spatial=(12, 20)), B=2),
+    "c5like": dict(desc=O.Desc(1, 256, 64, (9, 1), dilation=(2, 1), in_spatial=(25, 1)), B=5),
+    "st2_pt1": dict(desc=O.Desc(2, 32, 32, (3, 3, 3), stride=(2, 1, 1), padding=(1, 1, 1), in_spatial=(6, 7)), B=2),
+    "kt5_dil2": dict(desc=O.Desc(2, 16, 32, (5, 3, 3), padding=(2, 1, 1), dilation=(2, 1, 1), in_spatial=(7, 8)), B=2),
+}
+
+
+@pytest.mark.parametrize("case", list(RAW_DENSE))
+@pytest.mark.parametrize("integer", [False, True])
+def test_raw_dense_tc_vs_oracle(case, integer):
+    """The tensor-core RAW path: temporal taps folded into K of one K-pipelined
+    contraction per Ready step; bitwise in the exact-integer regime."""
+    d, B = RAW_DENSE[case]["desc"], RAW_DENSE[case]["B"]
+    rng = np.random.default_rng(3000)
+    if integer:
+        W = rng.integers(-2, 3, d.w_shape).astype(np.float64)
+        b = rng.integers(-2, 3, d.cout).astype(np.float64)
+    else:
+        W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
+        b = rng.standard_normal(d.cout) * 0.1
+    conv, sm, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="dense_tc", state_layout="raw")
+    assert conv.kernel_used == "dense_tc" and "kloop" in conv.kernel_name, conv.kernel_name
+    ys, refs = [], []
+    for t in range(d.receptive_field + 5):
+        x = rng.integers(-2, 3, _shape(d, B)).astype(np.float64) if integer else rng.standard_normal(_shape(d, B))
+        xt = to_cl(x, torch.bfloat16)
+        y = conv.forward_step(xt)
+        r = sm.forward_step(np_of(xt))
+        assert (y is None) == (r is None)
+        if y is not None:
+            ys.append(np_of(y)); refs.append(r.reshape(y.shape))
+    y, ref = np.stack(ys), np.stack(refs)
+    if integer:
+        assert np.array_equal(y, ref)
+    else:
+        assert rel_err(y, ref) <= 1e-4
+    st, _ = conv.state_dict_stream()
+    assert np.array_equal(_canon_to_oracle(st, d, B), sm.history())
+
+
+RAW_DW = {
+    "c3a": dict(desc=O.Desc(2, 192, 192, (3, 3, 3), padding=(0, 1, 1), groups=192, in_spatial=(28, 28)), B=2),
+    "c3b": dict(desc=O.Desc(2, 192, 192, (5, 1, 1), groups=192, in_spatial=(28, 28)), B=2),
+    "ragged_st2": dict(desc=O.Desc(2, 24, 24, (3, 3, 3), stride=(2, 1, 1), padding=(1, 1, 1), groups=24,
+                                   in_spatial=(9, 13)), B=3),
+    "t_dil2": dict(desc=O.Desc(1, 64, 64, (9, 1), dilation=(2, 1), groups=64, in_spatial=(25, 1)), B=3),
+}
+
+
+@pytest.mark.parametrize("case", list(RAW_DW))
+def test_raw_depthwise_vs_oracle(case):
+    d, B = RAW_DW[case]["desc"], RAW_DW[case]["B"]
+    rng = np.random.default_rng(4000)
+    W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
+    b = rng.standard_normal(d.cout) * 0.1
+    conv, sm, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="depthwise", state_layout="raw")
+    assert "dw_raw" in conv.kernel_name, conv.kernel_name
+    ys, refs = [], []
+    for t in range(d.receptive_field + 5):
+        xt = to_cl(rng.standard_normal(_shape(d, B)), torch.bfloat16)
+        y = conv.forward_step(xt)
+        r = sm.forward_step(np_of(xt))
+        assert (y is None) == (r is None)
+        if y is not None:
+            ys.append(np_of(y)); refs.append(r.reshape(y.shape))
+    assert rel_err(np.stack(ys), np.stack(refs)) <= 1e-4
+    st, _ = conv.state_dict_stream()
+    assert np.array_equal(_canon_to_oracle(st, d, B), sm.history())
