@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--impl", default="co", choices=["co", "reference"])
     ap.add_argument("--streams", type=int, default=None, help="override streams per GPU (default: the config's count)")
     ap.add_argument("--kernel", default="auto")
+    ap.add_argument("--state", default="psum", choices=["psum", "raw"],
+                    help="per-stream state layout: fp32 partial-sum ring (the configs' 'fp32 state', default) or the "
+                         "raw-input ring (SURVEY §8f f1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=16)
@@ -154,14 +157,18 @@ def layer_geom(L, in_spatial, spatial_rank):
     return H, W, Ho, Wo
 
 
-def layer_bytes_flops(L, in_spatial, spatial_rank, esz):
+def layer_bytes_flops(L, in_spatial, spatial_rank, esz, state="psum"):
     """Algorithmic HBM bytes and FLOPs per stream-step of one layer:
-    B_alg = x_t + y_t + 2 (kt-1) Cout H'W' * 4 (fp32 partial-sum state RMW);
+    PSUM: B_alg = x_t + y_t + 2 (kt-1) Cout H'W' * 4 (fp32 partial-sum state RMW);
+    RAW:  B_alg = x_t + y_t + x_t (ring store) + (kt-1) x (the window's past frames);
     F = 2 Cout (Cin/g) kt kh kw H'W'."""
     H, W, Ho, Wo = layer_geom(L, in_spatial, spatial_rank)
     x_b = L.cin * H * W * esz
     y_b = L.cout * Ho * Wo * esz
-    st_b = 2 * (L.kernel[0] - 1) * L.cout * Ho * Wo * 4
+    if state == "raw":
+        st_b = L.kernel[0] * x_b
+    else:
+        st_b = 2 * (L.kernel[0] - 1) * L.cout * Ho * Wo * 4
     flops = 2.0 * L.cout * (L.cin // L.groups) * L.kernel[0] * L.kernel[1] * L.kernel[2] * Ho * Wo
     return x_b + y_b + st_b, flops, (x_b, y_b, st_b)
 
@@ -191,7 +198,7 @@ def ncu_traffic(key):
     return j.get(key)
 
 
-def build_layers(cfg, B, kernel="auto"):
+def build_layers(cfg, B, kernel="auto", state="psum"):
     """The config's continual conv layers on this rank's B streams (bf16
     inter-layer activations, ReLU where the config says, A15)."""
     import torch
@@ -202,7 +209,7 @@ def build_layers(cfg, B, kernel="auto"):
         c = co.Conv(L.cin, L.cout, L.kernel, weight=W.cuda(), bias=b.cuda(), stride=L.stride, padding=L.padding,
                     dilation=L.dilation, groups=L.groups, spatial_rank=cfg.spatial_rank, in_spatial=spat,
                     n_streams=B, dtype=cfg.dtype, out_dtype=cfg.dtype, activation="relu" if L.relu else None,
-                    kernel=kernel)
+                    kernel=kernel, state_layout=state)
         convs.append(c)
         spat = tuple(c.out_spatial) + (1,) * (2 - len(c.out_spatial))
     return convs
@@ -219,7 +226,7 @@ def run_co(args, world, rank):
     from paper_2204_03418_b200 import shard as sh
     sd = sh.shard(rank, world, args.streams or cfg.n_streams)
     B, B_global = sd.per_rank, sd.n_global
-    convs = build_layers(cfg, B, args.kernel)
+    convs = build_layers(cfg, B, args.kernel, args.state)
     esz = 2 if cfg.dtype == torch.bfloat16 else 4
     frame_bytes = B * math.prod(synth.in_shape(cfg)) * esz
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
@@ -271,7 +278,7 @@ def run_co(args, world, rank):
     hbm, bf16, src = measured_peaks()
     layers, spat = [], tuple(cfg.in_spatial)
     for l, (L, c) in enumerate(zip(cfg.layers, convs)):
-        bytes_ss, flops_ss, parts = layer_bytes_flops(L, spat, cfg.spatial_rank, esz)
+        bytes_ss, flops_ss, parts = layer_bytes_flops(L, spat, cfg.spatial_rank, esz, args.state)
         spat = tuple(c.out_spatial) + (1,) * (2 - len(c.out_spatial))
         ms = layer_ms[l]
         t_hbm = bytes_ss / (hbm * 1e9)
@@ -287,7 +294,7 @@ def run_co(args, world, rank):
         else:
             roof = {"bound": bound_c, "achieved": round(ach_tf, 2), "peak": round(peak_c, 1), "unit": unit_c,
                     "frac": round(ach_tf / peak_c, 4)}
-        tr = ncu_traffic(f"{cfg.name}/L{l}")
+        tr = ncu_traffic(f"{cfg.name}/L{l}" + ("/raw" if args.state == "raw" else ""))
         roof.update({"kernel": c.kernel_name, "ms_per_launch": round(ms, 4),
                      "alg_bytes_per_launch": int(bytes_ss * B), "alg_flops_per_launch": flops_ss * B,
                      "traffic": None if tr is None else int(tr.get("bytes_per_stream_step", 0) * B),
@@ -308,7 +315,8 @@ def run_co(args, world, rank):
                    "layers": [{"cin": L.cin, "cout": L.cout, "kernel": list(L.kernel), "padding": list(L.padding),
                                "stride": list(L.stride), "dilation": list(L.dilation), "groups": L.groups,
                                "relu": L.relu} for L in cfg.layers],
-                   "in_spatial": list(cfg.in_spatial), "state": "fp32 partial-sum ring",
+                   "in_spatial": list(cfg.in_spatial),
+                   "state": "fp32 partial-sum ring" if args.state == "psum" else "raw-input ring (bf16 frames)",
                    "kernels": [c.kernel_name for c in convs],
                    "parallelism": f"stream-shard x{world} (no data-path collective)",
                    "l2_policy": f"inputs larger than L2: per-step working set "

@@ -87,7 +87,8 @@ struct TcParams {
   int w_off;                      // stages start here (1 KB aligned)
   int slot[kMaxKt];
   int emit, update, act, out_f32;
-  int raw_kh, raw_B;              // RAW layout: real spatial kh (the K loop walks kt*kh rows), streams per ring slot
+  int raw_kh, raw_B;
+  int kflat;                      // KLOOP over 128 flattened (stream, pixel) rows (RAW, 1x1 spatial)              // RAW layout: real spatial kh (the K loop walks kt*kh rows), streams per ring slot
   int ring_slot[kMaxKt];          // RAW layout: ring slot of temporal tap k
   int swa, a_rows;                // A staged swizzled: 0 none, 1 128-B rows ([Cin/64][rows][128 B]),
                                   // 2 64-B rows (KLOOP with kb = 32); rows per 64-channel block
@@ -227,8 +228,8 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
         const int per_stream = p.tiles_h * p.tiles_w;
         for (int64_t item = unit; item < p.n_items; item += n_units) {
           const int64_t tile = tile_of(item);
-          const int b = int(tile / per_stream);
-          const int r = int(tile % per_stream);
+          const int b = p.kflat ? 0 : int(tile / per_stream);
+          const int r = p.kflat ? 0 : int(tile % per_stream);
           const int ho0 = (r / p.tiles_w) * p.TH, wo0 = (r % p.tiles_w) * p.TW;
           const uint8_t* bsrc = wsrc;
           int kg = 0;                                   // K-group (8 channels) index of the chunk
@@ -243,7 +244,11 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
                 uint8_t* dst = a_s + s * p.a_stride;
                 const int cw = wo0 * p.sw + v * p.dw - p.pw, ch = ho0 * p.sh + u * p.dh - p.ph;
                 const int cc = p.swa ? cb : cb * (p.kb / 8);   // swizzled: kb-channel blocks
-                if constexpr (PAIR == 2) {
+                if (p.kflat) {    // rows tile*128 .. of ring slot k, viewed as a (B*HW, Cin) matrix
+                  ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes + p.b_bytes);
+                  ptx::tma_load_4d(dst, &tmap, &full[s], 0, int(tile * 128), cc, p.ring_slot[kk]);
+                  ptx::bulk_g2s(dst + p.b_off, bsrc, p.b_bytes, &full[s]);
+                } else if constexpr (PAIR == 2) {
                   if (leader) ptx::mbar_arrive_expect_tx(&full[s], (p.a_bytes + p.b_bytes) * PAIR);
                   ptx::tma_load_5d_pair(dst, &tmap, &full[s], 0, cw, ch, cc, bb);
                   ptx::tma_load_4d_pair(dst + p.b_off, &wmap, &full[s], 0, 0, kg / (p.kb / 8), part * PAIR + int(rank));
@@ -392,7 +397,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     // ---- this row's output pixel
     bool valid;
     int64_t pix, b;
-    if (p.mode == MODE_FLAT) {
+    if (p.mode == MODE_FLAT || p.kflat) {
       pix = tile * 128 + m;
       valid = pix < plane;
       b = valid ? pix / p.HWo : 0;
@@ -638,6 +643,7 @@ const Variant kVariants[] = {
     CO_TC_SPLIT(3, 32, 2, 16, 3, 3, 4, 2), CO_TC_SPLIT(3, 32, 3, 16, 3, 3, 4, 2),
     CO_TC_SPEC(3, 32, 2, 32, 3, 3, 4), CO_TC_SPEC(3, 32, 3, 32, 3, 3, 4), CO_TC_SPEC(9, 16, 2, 16, 1, 1, 16),
     CO_TC_VARIANT(1, 32, 4, 32), CO_TC_VARIANT(1, 64, 4, 32), CO_TC_VARIANT(1, 128, 2, 32),
+    CO_TC_VARIANT(1, 256, 2, 32),
     CO_TC_VARIANT(2, 32, 4, 32), CO_TC_VARIANT(2, 64, 2, 32), CO_TC_VARIANT(3, 16, 4, 16),
     CO_TC_VARIANT(3, 32, 2, 32), CO_TC_VARIANT(3, 32, 3, 32), CO_TC_VARIANT(3, 32, 4, 32),
     CO_TC_VARIANT(3, 64, 2, 32), CO_TC_VARIANT(5, 16, 4, 16), CO_TC_VARIANT(5, 32, 2, 16),
@@ -662,6 +668,7 @@ struct Plan {
   Geom gk;                        // geometry the kernel sees (the W-im2col'd one for a stem)
   int wcols = 0, Kp = 0;          // small-Cin stem packed W-im2col
   int swa = 0;                    // HALO: 128-B swizzled A (Cin % 64 == 0)
+  int kflat = 0;                  // RAW 1x1: KLOOP over flattened 128-row tiles
   int mode = MODE_HALO;
   int n_split = 0, MT = 0, Wp = 0, tiles_per_stream = 0;
   int TH = 0, TW = 0, tiles_h = 0, tiles_w = 0, kb = 0, n_cb = 0, b_bytes = 0, b_off = 0;
@@ -770,10 +777,11 @@ bool plan_resident(const Geom& g, Plan& pl) {
 }
 
 // KLOOP: K streamed through a stage ring; any spatial stride/dilation <= 8.
-bool plan_kloop(const Geom& g, Plan& pl) {
+bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
   if (g.Cin % 16 != 0 || g.Cin / 8 > 256 || g.sh > 8 || g.sw > 8) return false;
-  const int TW = std::min(g.Wo, 128);
-  const int TH = std::max(1, std::min(128 / TW, g.Ho));
+  // flat: rows are 128 consecutive (stream, pixel) pairs (RAW 1x1 layers)
+  const int TW = flat ? 128 : std::min(g.Wo, 128);
+  const int TH = flat ? 1 : std::max(1, std::min(128 / TW, g.Ho));
   if (TW * g.sw > 256 || TH * g.sh > 256) return false;
   const int kb = (g.Cin % 64 == 0) ? 64 : (g.Cin % 32 == 0) ? 32 : 16;
   const int rows = TH * TW;
@@ -820,6 +828,8 @@ bool plan_kloop(const Geom& g, Plan& pl) {
   pl.w_off = 0;
   pl.smem = fixed + size_t(stages) * stage;
   pl.n_tiles = g.B * pl.tiles_h * pl.tiles_w;
+  pl.kflat = flat;
+  if (flat) { pl.tiles_h = 1; pl.tiles_w = 1; pl.n_tiles = (g.B * g.HWo + 127) / 128; }
   return true;
 }
 
@@ -834,7 +844,8 @@ Plan make_plan(const Geom& g) {
     if (g.Cin % 16 != 0) return pl;
     Geom& k = pl.gk;
     k.kh = g.kt * g.kh; k.kt = 1;
-    pl.ok = plan_kloop(k, pl);
+    const bool flat = g.kh == 1 && g.kw == 1 && g.ph == 0 && g.pw == 0 && g.sh == 1 && g.sw == 1;
+    pl.ok = plan_kloop(k, pl, flat);
     if (pl.ok) pl.n_split = g.Cout / pl.var->CC;
     return pl;
   }
@@ -1002,6 +1013,17 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
     r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(x), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, pl.swa ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (pl.kflat) {
+    // ring slots as (B*HW rows, Cin) matrices: {cw, rows, Cin/cw, f+1 slots}
+    const cuuint32_t cw = pl.swa ? cuuint32_t(pl.kb) : 8;
+    cuuint64_t dims[4] = {cw, cuuint64_t(g.B * g.HWo), cuuint64_t(k.Cin / cw), cuuint64_t(g.f + 1)};
+    cuuint64_t strides[3] = {cuuint64_t(k.Cin) * 2, cuuint64_t(cw) * 2, cuuint64_t(g.B) * frame * 2};
+    cuuint32_t box[4] = {cw, 128, pl.swa ? 1u : cuuint32_t(pl.kb / 8), 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE,
+               pl.swa == 1 ? CU_TENSOR_MAP_SWIZZLE_128B : pl.swa == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
     cuuint64_t dims[5] = {8, cuuint64_t(k.W), cuuint64_t(k.H), cuuint64_t(k.Cin / 8), cuuint64_t(n_batch)};
     cuuint64_t strides[4] = {cuuint64_t(k.Cin) * 2, cuuint64_t(k.W) * k.Cin * 2, 16, cuuint64_t(x_bstride) * 2};
@@ -1052,6 +1074,7 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   static const int dbg = getenv("CO_TC_DEBUG") ? atoi(getenv("CO_TC_DEBUG")) : 0;
   p.dbg = dbg;
   p.raw_kh = g.raw ? g.kh : 0;
+  p.kflat = pl.kflat;
   p.raw_B = int(g.B);
   for (int i = 0; i < kMaxKt; ++i) p.ring_slot[i] = g.raw ? a.slot[i] : -1;
   p.swa = pl.swa;

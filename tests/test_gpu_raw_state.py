@@ -112,6 +112,8 @@ RAW_DENSE = {
     "c2like": dict(desc=O.Desc(2, 64, 64, (3, 3, 3), padding=(0, 1, 1), in_spatial=(13, 24)), B=3),
     "s2": dict(desc=O.Desc(2, 128, 128, (3, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1), in_spatial=(12, 20)), B=2),
     "c5like": dict(desc=O.Desc(1, 256, 64, (9, 1), dilation=(2, 1), in_spatial=(25, 1)), B=5),
+    "flat_ragged": dict(desc=O.Desc(1, 32, 128, (5, 1), padding=(2, 0), in_spatial=(25, 1)), B=7),
+    "flat_conv1d": dict(desc=O.Desc(0, 64, 64, (3,), stride=(2,)), B=300),
     "st2_pt1": dict(desc=O.Desc(2, 32, 32, (3, 3, 3), stride=(2, 1, 1), padding=(1, 1, 1), in_spatial=(6, 7)), B=2),
     "kt5_dil2": dict(desc=O.Desc(2, 16, 32, (5, 3, 3), padding=(2, 1, 1), dilation=(2, 1, 1), in_spatial=(7, 8)), B=2),
 }
