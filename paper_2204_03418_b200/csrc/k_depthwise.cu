@@ -280,36 +280,90 @@ __global__ void __launch_bounds__(kDwThreads, CO_DW_T_MINB) k_step_dw_t(const Dw
 // issued before the FMAs; taps read straight from global memory (the 3x3
 // neighbours of consecutive pixels are L1 hits).
 template <int KT, int KH, int KW>
-__global__ void __launch_bounds__(kDwThreads) k_step_dw_raw(const DwParams p) {
-  const int64_t n_items = p.plane * p.Cq;
-  const int64_t stride = int64_t(gridDim.x) * kDwThreads;
+__global__ void __launch_bounds__(kDwThreads, (KH * KW == 1) ? 3 : 2) k_step_dw_raw(const DwParams p) {
   const __nv_bfloat16* ring = reinterpret_cast<const __nv_bfloat16*>(p.state);
-  for (int64_t it = int64_t(blockIdx.x) * kDwThreads + threadIdx.x; it < n_items; it += stride) {
-    const int q = int(it % p.Cq);
-    const int64_t pix = it / p.Cq;
-    const int64_t b = pix / p.HWo;
-    const int pin = int(pix - b * p.HWo);
-    const int ho = pin / p.Wo, wo = pin - (pin / p.Wo) * p.Wo;
-    float4 acc = __ldg(reinterpret_cast<const float4*>(p.bias) + q);
+  const int64_t B = p.plane / p.HWo;
+  if constexpr (KH * KW == 1) {
+    // temporal only: 2 items per thread, all 2 x KT frame reads issued first
+    const int64_t n_items = p.plane * p.Cq;
+    const int64_t stride = int64_t(gridDim.x) * kDwThreads;
+    for (int64_t base = int64_t(blockIdx.x) * kDwThreads + threadIdx.x; base < n_items; base += 2 * stride) {
+      float4 xv[2][KT];
 #pragma unroll
-    for (int k = 0; k < KT; ++k) {
-      const __nv_bfloat16* fr = ring + (int64_t(p.slot[k]) * (p.plane / p.HWo) + b) * p.frame + 4 * q;
-      float4 part = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j = 0; j < 2; ++j) {
+        const int64_t it = base + j * stride;
+        if (it >= n_items) continue;
+        const int q = int(it % p.Cq);
+        const int64_t pix = it / p.Cq;
 #pragma unroll
-      for (int u = 0; u < KH; ++u) {
-        const int hi = ho + u - p.ph;
-        if (hi < 0 || hi >= p.H) continue;
-#pragma unroll
-        for (int v = 0; v < KW; ++v) {
-          const int wi = wo + v - p.pw;
-          if (wi < 0 || wi >= p.W) continue;
-          const float4 w = __ldg(reinterpret_cast<const float4*>(p.w + ((k * KH + u) * KW + v) * p.C) + q);
-          part = f4_fma(w, ld_bf16x4(fr + (int64_t(hi) * p.W + wi) * p.C), part);
-        }
+        for (int k = 0; k < KT; ++k)
+          xv[j][k] = ld_bf16x4(ring + (int64_t(p.slot[k]) * B) * p.frame + pix * p.C + 4 * q);
       }
-      acc = f4_add(acc, part);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int64_t it = base + j * stride;
+        if (it >= n_items) continue;
+        const int q = int(it % p.Cq);
+        const int64_t pix = it / p.Cq;
+        const int64_t b = pix / p.HWo;
+        float4 acc = __ldg(reinterpret_cast<const float4*>(p.bias) + q);
+#pragma unroll
+        for (int k = 0; k < KT; ++k)
+          acc = f4_add(acc, f4_fma(__ldg(reinterpret_cast<const float4*>(p.w + k * p.C) + q), xv[j][k],
+                                   make_float4(0.f, 0.f, 0.f, 0.f)));
+        st_out4(p, b, pix - b * p.HWo, q, f4_act(acc, p.act));
+      }
     }
-    st_out4(p, b, pin, q, f4_act(acc, p.act));
+  } else {
+    // spatial stencil: thread = fixed channel quad x strips of 2 output pixels;
+    // per (k, u) the strip's KW+1 input columns are read once (L1 serves the
+    // neighbouring strips' overlap), each weight float4 once per strip
+    constexpr int PX = 2;
+    const int nthr = blockDim.x;
+    const int q = int((int64_t(blockIdx.x) * nthr + threadIdx.x) % p.Cq);
+    const int64_t sgrp = (int64_t(blockIdx.x) * nthr + threadIdx.x) / p.Cq;
+    const int64_t n_sgrp = (int64_t(gridDim.x) * nthr) / p.Cq;
+    const int spr = (p.Wo + PX - 1) / PX;
+    const int64_t n_strips = B * p.Ho * spr;
+    const float4 bias4 = __ldg(reinterpret_cast<const float4*>(p.bias) + q);
+    for (int64_t sidx = sgrp; sidx < n_strips && sgrp < n_sgrp; sidx += n_sgrp) {
+      const int64_t b = sidx / (int64_t(p.Ho) * spr);
+      const int rr = int(sidx - b * p.Ho * spr);
+      const int ho = rr / spr, wo0 = (rr - (rr / spr) * spr) * PX;
+      float4 acc[PX];
+#pragma unroll
+      for (int j = 0; j < PX; ++j) acc[j] = bias4;
+#pragma unroll
+      for (int k = 0; k < KT; ++k) {
+        const __nv_bfloat16* fr = ring + (int64_t(p.slot[k]) * B + b) * p.frame + 4 * q;
+        float4 part[PX];
+#pragma unroll
+        for (int j = 0; j < PX; ++j) part[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < KH; ++u) {
+          const int hi = ho + u - p.ph;
+          if (hi < 0 || hi >= p.H) continue;
+          float4 xv[PX + KW - 1];
+#pragma unroll
+          for (int t = 0; t < PX + KW - 1; ++t) {
+            const int wi = wo0 + t - p.pw;
+            xv[t] = (wi >= 0 && wi < p.W) ? ld_bf16x4(fr + (int64_t(hi) * p.W + wi) * p.C)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int v = 0; v < KW; ++v) {
+            const float4 w = __ldg(reinterpret_cast<const float4*>(p.w + ((k * KH + u) * KW + v) * p.C) + q);
+#pragma unroll
+            for (int j = 0; j < PX; ++j) part[j] = f4_fma(w, xv[j + v], part[j]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < PX; ++j) acc[j] = f4_add(acc[j], part[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < PX; ++j)
+        if (wo0 + j < p.Wo) st_out4(p, b, int64_t(ho) * p.Wo + wo0 + j, q, f4_act(acc[j], p.act));
+    }
   }
 }
 
@@ -419,6 +473,11 @@ Depthwise* depthwise_create(const Geom& g, const void* w_dev, std::string& err) 
     per_sm = std::max(per_sm, 1);
     const int64_t items = g.B * g.HWo * (g.Cout / 4);
     t->grid = int(std::max<int64_t>(1, std::min<int64_t>((items + kDwThreads - 1) / kDwThreads, int64_t(sms) * per_sm)));
+    if (!pl.temporal) {   // the stencil maps threads to (quad, strip group): whole quad sets per grid
+      const int64_t cq = g.Cout / 4;
+      const int64_t thr = int64_t(t->grid) * kDwThreads;
+      if (thr < cq) t->grid = int((cq + kDwThreads - 1) / kDwThreads);
+    }
     char buf[96];
     snprintf(buf, sizeof(buf), "k_step_dw_raw<%d,%d,%d>", pl.var->KT, pl.var->KH, pl.var->KW);
     t->name = buf;
