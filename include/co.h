@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define CO_ABI_VERSION 2
+#define CO_ABI_VERSION 3
 #define CO_MAX_KT 32          /* temporal kernel extent supported by the kernels */
 
 typedef enum {
@@ -67,7 +67,8 @@ typedef enum {
   CO_KERNEL_AUTO = 0,
   CO_KERNEL_DIRECT = 1,     /* generic CUDA-core kernel: any groups/dilation/stride, fp32 or bf16 */
   CO_KERNEL_DENSE_TC = 2,   /* tcgen05/TMEM implicit GEMM with fused state epilogue (bf16, dense) */
-  CO_KERNEL_DEPTHWISE = 3   /* CUDA-core depthwise stencil (groups == Cin == Cout, bf16) */
+  CO_KERNEL_DEPTHWISE = 3,  /* CUDA-core depthwise stencil (groups == Cin == Cout, bf16) */
+  CO_KERNEL_POOL = 4        /* CUDA-core window max / mean over the RAW ring (pooling handles only) */
 } co_kernel;
 
 /* Per-stream state layout (BASELINE.json north_star "Per-stream state layout";
@@ -77,6 +78,21 @@ typedef enum {
  * S:227); a Ready step contracts the whole window (K = kt kh kw Cin/g),
  * a non-Ready step only stores its frame.  Same outputs (Definition 1). */
 typedef enum { CO_STATE_PSUM = 0, CO_STATE_RAW = 1 } co_state_layout;
+
+/* Operation of a handle ("Pooling:
+ * co.AvgPool1d, co.MaxPool1d, etc.").  A pooling handle has
+ * in_channels == out_channels (groups is ignored), no weights or bias
+ * (create takes weights = bias = NULL), always keeps the RAW frame ring
+ * (state_layout is ignored; co_info reports RAW) and dispatches
+ * CO_KERNEL_POOL.  Padding (temporal and spatial) is 0 and counted in the
+ * divisor for AVG (count_include_pad, divisor kt kh kw, A21) and is
+ * ignored for MAX (PyTorch's implicit -inf padding; a window of padding only
+ * yields -inf, A22).  In MAX handles the ring stores padding frames as -inf:
+ * clean state, pad_end steps (x == NULL) and the canonical state
+ * (co_state_get) carry -inf for padded frames.  Clock, readiness, delay and
+ * the call modes are those of a convolution with the same kernel / stride /
+ * padding / dilation (Definition 1). */
+typedef enum { CO_OP_CONV = 0, CO_OP_MAX_POOL = 1, CO_OP_AVG_POOL = 2 } co_op;
 
 typedef void* co_stream;                 /* cudaStream_t */
 typedef struct co_conv co_conv;          /* opaque: packed weights, fp32 state ring, host clock */
@@ -97,6 +113,7 @@ typedef struct {
   int32_t activation;                    /* co_activation applied to emitted outputs (after bias) */
   int32_t kernel_choice;                 /* co_kernel; AUTO = dispatch rule */
   int32_t state_layout;                  /* co_state_layout (PSUM = 0 default) */
+  int32_t op;                            /* co_op (CONV = 0 default) */
 } co_conv_desc;
 
 /* Clock + geometry of a handle.  n and head are the host clock (a1). */
@@ -133,7 +150,8 @@ const char* co_kernel_name(const co_conv* h);         /* name of the dispatched 
 /* forward_step: x one step (B, S1, S2, Cin) channels-last in in_dtype;
  * y (B, S1', S2', Cout) in out_dtype.  *ready (host) = 1 when the output is
  * emitted (n >= d and (n-d) mod s == 0), else 0 (Empty) and y is left
- * untouched.  x == NULL feeds an all-zero step (used for pad_end).  With
+ * untouched.  x == NULL feeds an all-zero step (used for pad_end; a padding
+ * step, -inf, for MAX pooling handles).  With
  * update_state == 0 the ready output is computed from the current state and
  * state + clock stay bitwise unchanged. */
 int co_forward_step(co_conv* h, const void* x, void* y, int update_state, int* ready, co_stream stream);

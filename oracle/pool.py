@@ -130,6 +130,13 @@ class PoolStep:
         self.hist = [zero.copy() for _ in range(self.f - 1)]
         self.hpad = [True] * (self.f - 1)
 
+    def history(self):
+        """Read-only view of the last f-1 padded frames (oldest first),
+        (f-1, B, C, H, W), and their padding flags."""
+        if self.f == 1:
+            return np.zeros((0, self.B, self.C, self.H, self.W)), []
+        return np.stack(self.hist), list(self.hpad)
+
     @property
     def out_spatial(self):
         kt, kh, kw = self.kernel

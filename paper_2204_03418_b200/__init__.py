@@ -23,7 +23,7 @@ import torch
 from . import _abi
 from ._abi import CoConvDesc, CoInfo, check, lib
 
-__all__ = ["Conv", "Stack", "channels_last", "is_channels_last", "load"]
+__all__ = ["Conv", "Pool", "Stack", "channels_last", "is_channels_last", "load"]
 
 _DT = {torch.float32: _abi.CO_F32, torch.bfloat16: _abi.CO_BF16}
 
@@ -77,12 +77,12 @@ class Conv:
     ``dtype`` (PyTorch's Conv weight layout); ``bias`` is ``(Cout,)``.
     """
 
-    def __init__(self, in_channels: int, out_channels: int, kernel_size, *, weight: torch.Tensor,
+    def __init__(self, in_channels: int, out_channels: int, kernel_size, *, weight: Optional[torch.Tensor],
                  bias: Optional[torch.Tensor] = None, stride=1, padding=0, dilation=1, groups: int = 1,
                  spatial_rank: int = 2, in_spatial: Sequence[int] = (1, 1), n_streams: int = 1,
                  dtype: torch.dtype = torch.bfloat16, out_dtype: Optional[torch.dtype] = None,
                  activation: Optional[str] = None, kernel: str = "auto", state_layout: str = "psum",
-                 device="cuda"):
+                 device="cuda", op: str = "conv"):
         self.device = torch.device(device)
         self.dtype, self.out_dtype = dtype, (out_dtype or dtype)
         self.spatial_rank, self.n_streams = spatial_rank, n_streams
@@ -101,17 +101,23 @@ class Conv:
         d.activation = {None: _abi.CO_ACT_NONE, "none": _abi.CO_ACT_NONE, "relu": _abi.CO_ACT_RELU}[activation]
         d.kernel_choice = _abi.KERNELS[kernel]
         d.state_layout = _abi.STATE_LAYOUTS[state_layout]
-        self.state_layout = state_layout
+        d.op = _abi.OPS[op]
+        self.op = op
+        self.state_layout = state_layout if op == "conv" else "raw"
         self._desc = d
-        w = weight.detach().to(dtype).contiguous()
-        on_dev = int(w.is_cuda)
-        b = None
-        if bias is not None:
-            b = bias.detach().to(torch.float32).to(w.device).contiguous()
         h = C.c_void_p()
         with torch.cuda.device(self.device):
-            check(lib().co_conv_create(C.byref(d), C.c_void_p(w.data_ptr()),
-                                       C.c_void_p(b.data_ptr()) if b is not None else None, on_dev, C.byref(h)))
+            if op == "conv":
+                w = weight.detach().to(dtype).contiguous()
+                on_dev = int(w.is_cuda)
+                b = None
+                if bias is not None:
+                    b = bias.detach().to(torch.float32).to(w.device).contiguous()
+                check(lib().co_conv_create(C.byref(d), C.c_void_p(w.data_ptr()),
+                                           C.c_void_p(b.data_ptr()) if b is not None else None, on_dev,
+                                           C.byref(h)))
+            else:
+                check(lib().co_conv_create(C.byref(d), None, None, 0, C.byref(h)))
         self._h = h
         info = self.info()
         self.out_spatial: Tuple[int, ...] = tuple(info.out_spatial[:spatial_rank])
@@ -246,6 +252,28 @@ class Conv:
         check(lib().co_forward_step_host(self._h, C.c_void_p(x_host.data_ptr()), C.c_void_p(y_host.data_ptr()),
                                          int(update_state), C.byref(r), _stream(stream)))
         return bool(r.value)
+
+
+class Pool(Conv):
+    """Continual max / average pooling (``co.MaxPool*`` / ``co.AvgPool*``,
+    PAPER.md P:380-394) over ``n_streams`` lockstep streams: a handle of the C
+    ABI with ``op`` = MAX / AVG (include/co.h co_op), keeping the RAW frame
+    ring.  AVG counts padding as zeros in a divisor of kt kh kw
+    (count_include_pad); MAX ignores padding (-inf).  Same call modes, clock and
+    state API as :class:`Conv`.
+    """
+
+    def __init__(self, kind: str, channels: int, kernel_size, *, stride=1, padding=0, dilation=1,
+                 spatial_rank: int = 2, in_spatial: Sequence[int] = (1, 1), n_streams: int = 1,
+                 dtype: torch.dtype = torch.bfloat16, out_dtype: Optional[torch.dtype] = None,
+                 activation: Optional[str] = None, device="cuda"):
+        if kind not in ("max", "avg"):
+            raise ValueError("kind must be 'max' or 'avg'")
+        super().__init__(channels, channels, kernel_size, weight=None, stride=stride, padding=padding,
+                         dilation=dilation, groups=channels, spatial_rank=spatial_rank, in_spatial=in_spatial,
+                         n_streams=n_streams, dtype=dtype, out_dtype=out_dtype, activation=activation,
+                         kernel="auto", state_layout="raw", device=device, op=kind)
+        self.kind = kind
 
 
 class Stack:

@@ -19,9 +19,11 @@ CO_F32, CO_BF16 = 0, 1
 CO_ACT_NONE, CO_ACT_RELU = 0, 1
 CO_STATE_PSUM, CO_STATE_RAW = 0, 1
 STATE_LAYOUTS = {"psum": CO_STATE_PSUM, "raw": CO_STATE_RAW}
-CO_KERNEL_AUTO, CO_KERNEL_DIRECT, CO_KERNEL_DENSE_TC, CO_KERNEL_DEPTHWISE = 0, 1, 2, 3
+CO_KERNEL_AUTO, CO_KERNEL_DIRECT, CO_KERNEL_DENSE_TC, CO_KERNEL_DEPTHWISE, CO_KERNEL_POOL = 0, 1, 2, 3, 4
 KERNELS = {"auto": CO_KERNEL_AUTO, "direct": CO_KERNEL_DIRECT, "dense_tc": CO_KERNEL_DENSE_TC,
-           "depthwise": CO_KERNEL_DEPTHWISE}
+           "depthwise": CO_KERNEL_DEPTHWISE, "pool": CO_KERNEL_POOL}
+CO_OP_CONV, CO_OP_MAX_POOL, CO_OP_AVG_POOL = 0, 1, 2
+OPS = {"conv": CO_OP_CONV, "max": CO_OP_MAX_POOL, "avg": CO_OP_AVG_POOL}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 
 # every entry point include/co.h declares (checked by tests/test_abi_load.py)
@@ -38,7 +40,7 @@ class CoConvDesc(C.Structure):
                 ("padding", C.c_int32 * 3), ("dilation", C.c_int32 * 3), ("in_spatial", C.c_int32 * 2),
                 ("n_streams", C.c_int64), ("in_dtype", C.c_int32), ("w_dtype", C.c_int32),
                 ("out_dtype", C.c_int32), ("activation", C.c_int32), ("kernel_choice", C.c_int32),
-                ("state_layout", C.c_int32)]
+                ("state_layout", C.c_int32), ("op", C.c_int32)]
 
 
 class CoInfo(C.Structure):

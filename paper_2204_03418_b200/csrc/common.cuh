@@ -11,6 +11,7 @@ namespace co {
 constexpr int kMaxKt = 32;   // == CO_MAX_KT
 
 enum Dtype : int { F32 = 0, BF16 = 1 };
+enum Op : int { OP_CONV = 0, OP_MAX_POOL = 1, OP_AVG_POOL = 2 };   // == co_op
 
 // Normalised layer geometry (absent spatial axes are extent 1, kernel 1).
 struct Geom {
@@ -37,6 +38,7 @@ struct Geom {
   int raw;
   int64_t frame_elems;   // H * W * Cin
   int64_t splane;        // state rows per slot and channel quad: B*HWo, or n_tiles*128 when tile-blocked
+  int op;                // Op: continual conv, or max / avg pooling over the RAW ring (§8f f3)
 };
 
 // Physical state layouts (internal; co_state_get converts to the canonical one):
@@ -98,6 +100,13 @@ __device__ __forceinline__ float activate(float v, int act) { return (act == 1 &
 // RAW layout step (StepArgs.state = ring, slot[k] = ring slot of temporal tap k)
 cudaError_t launch_step_direct_raw(const Geom& g, const StepArgs& a, const float* w_direct, const float* bias,
                                    cudaStream_t s);
+
+// Continual pooling (k_pool.cu): Ready-step reduction over the
+// RAW ring, batch forward, and the ring's padding fill (0 AVG, -inf MAX).
+cudaError_t launch_step_pool(const Geom& g, const StepArgs& a, cudaStream_t s);
+cudaError_t launch_forward_pool(const Geom& g, const void* x, int64_t T, void* y, int64_t Tp, cudaStream_t s);
+cudaError_t launch_fill_pad(const Geom& g, void* p, int64_t n_elems, cudaStream_t s);
+const char* pool_kernel_name(const Geom& g);
 
 // ---- launchers implemented in the .cu files (host side) --------------------
 cudaError_t launch_step_direct(const Geom& g, const StepArgs& a, const float* w_direct, const float* bias,

@@ -142,7 +142,7 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
   }
   if (d->in_channels < 1 || d->out_channels < 1 || d->groups < 1)
     return fail(CO_ERR_ARG, "channels and groups must be >= 1");
-  if (d->in_channels % d->groups || d->out_channels % d->groups)
+  if (d->op == CO_OP_CONV && (d->in_channels % d->groups || d->out_channels % d->groups))
     return fail(CO_ERR_ARG, "groups (%d) must divide in_channels (%d) and out_channels (%d)", d->groups,
                 d->in_channels, d->out_channels);
   if (d->n_streams < 1) return fail(CO_ERR_ARG, "n_streams must be >= 1");
@@ -152,9 +152,13 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
   if (d->w_dtype != d->in_dtype) return fail(CO_ERR_ARG, "w_dtype must equal in_dtype");
   if (d->activation != CO_ACT_NONE && d->activation != CO_ACT_RELU) return fail(CO_ERR_ARG, "bad activation");
   if (d->state_layout != CO_STATE_PSUM && d->state_layout != CO_STATE_RAW) return fail(CO_ERR_ARG, "bad state_layout");
+  if (d->op != CO_OP_CONV && d->op != CO_OP_MAX_POOL && d->op != CO_OP_AVG_POOL) return fail(CO_ERR_ARG, "bad op");
+  const bool pool = d->op != CO_OP_CONV;
+  if (pool && d->in_channels != d->out_channels)
+    return fail(CO_ERR_ARG, "pooling: in_channels (%d) != out_channels (%d)", d->in_channels, d->out_channels);
   g = Geom{};
   g.rank = d->spatial_rank;
-  g.Cin = d->in_channels; g.Cout = d->out_channels; g.groups = d->groups;
+  g.Cin = d->in_channels; g.Cout = d->out_channels; g.groups = pool ? d->in_channels : d->groups;
   g.cig = g.Cin / g.groups; g.cog = g.Cout / g.groups;
   g.kt = k[0]; g.kh = k[1]; g.kw = k[2];
   g.st = s[0]; g.sh = s[1]; g.sw = s[2];
@@ -175,7 +179,8 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
   g.HWo = int64_t(g.Ho) * g.Wo;
   g.splane = g.B * g.HWo;
   g.slot_elems = int64_t(g.Cq) * 4 * g.splane;
-  g.raw = d->state_layout == CO_STATE_RAW;
+  g.op = d->op;
+  g.raw = pool || d->state_layout == CO_STATE_RAW;   // pooling always keeps the frame ring
   g.frame_elems = int64_t(g.H) * g.W * g.Cin;
   return CO_OK;
 }
@@ -218,12 +223,41 @@ static int head_of(const Geom& g, int64_t n) {
 static bool dense_tc_fits(const Geom& g) { return co::dense_tc_supported(g); }
 static bool depthwise_fits(const Geom& g) { return co::depthwise_supported(g); }
 
+// Pooling handle (§8f f3): no weights, the RAW ring initialised to the padding
+// value (0 AVG, -inf MAX), kernel CO_KERNEL_POOL.
+static int create_pool(const co_conv_desc* desc, const Geom& g, const void* weights, const float* bias,
+                       co_conv** out) {
+  if (weights || bias) return fail(CO_ERR_ARG, "pooling takes no weights or bias");
+  if (desc->kernel_choice != CO_KERNEL_AUTO && desc->kernel_choice != CO_KERNEL_POOL)
+    return fail(CO_ERR_UNSUPPORTED, "pooling runs only on CO_KERNEL_POOL");
+  co_conv* h = new (std::nothrow) co_conv();
+  if (!h) return fail(CO_ERR_OOM, "host allocation");
+  h->desc = *desc;
+  h->g = g;
+  h->kernel_used = CO_KERNEL_POOL;
+  h->kname = co::pool_kernel_name(g);
+  const size_t sb = state_alloc_bytes(g);
+  cudaError_t e;
+  if ((e = cudaMalloc(&h->state, sb)) != cudaSuccess) {
+    co_conv_destroy(h);
+    return fail(CO_ERR_OOM, "state (%lld bytes): %s", (long long)sb, cudaGetErrorString(e));
+  }
+  if ((e = co::launch_fill_pad(g, h->state, int64_t(sb / dsize(g.in_dtype)), 0)) != cudaSuccess ||
+      (e = cudaDeviceSynchronize()) != cudaSuccess) {
+    co_conv_destroy(h);
+    return fail(CO_ERR_CUDA, "pool state init: %s", cudaGetErrorString(e));
+  }
+  *out = h;
+  return CO_OK;
+}
+
 extern "C" int co_conv_create(const co_conv_desc* desc, const void* weights, const float* bias,
                               int weights_on_device, co_conv** out) {
   if (!out) return fail(CO_ERR_ARG, "null out");
   *out = nullptr;
   Geom g;
   if (int r = make_geom(desc, g)) return r;
+  if (g.op != CO_OP_CONV) return create_pool(desc, g, weights, bias, out);
   if (!weights) return fail(CO_ERR_ARG, "null weights");
   // Dispatch rule: fp32 -> CUDA cores (TF32 would break 1e-4);
   // bf16 dense contractions -> tcgen05; bf16 depthwise -> CUDA-core stencil.
@@ -343,6 +377,7 @@ static int launch_step(co_conv* h, const StepArgs& a, cudaStream_t s) {
   cudaError_t e;
   if (h->g.raw) {
     switch (h->kernel_used) {
+      case CO_KERNEL_POOL: e = co::launch_step_pool(h->g, a, s); break;
       case CO_KERNEL_DENSE_TC: e = co::dense_tc_step(h->tc, h->g, a, h->bias, s); break;
       case CO_KERNEL_DEPTHWISE: e = co::depthwise_step(h->dw, h->g, a, h->bias, s); break;
       default: e = co::launch_step_direct_raw(h->g, a, h->w_direct, h->bias, s); break;
@@ -373,7 +408,7 @@ static int step_raw(co_conv* h, int64_t& n, float* state, const void* x, int64_t
   char* slot = reinterpret_cast<char*>(state) + size_t(cur) * g.B * fb;
   if (x) CO_CUDA(cudaMemcpy2DAsync(slot, fb, x, size_t(x_bstride) * dsize(g.in_dtype), fb, g.B,
                                    cudaMemcpyDeviceToDevice, s));
-  else CO_CUDA(cudaMemsetAsync(slot, 0, g.B * fb, s));
+  else CO_CUDA(co::launch_fill_pad(g, slot, g.B * g.frame_elems, s));   // padding step: 0, or -inf for MAX
   if (r) {
     StepArgs a;
     for (int k = 0; k < co::kMaxKt; ++k) a.slot[k] = -1;
@@ -552,7 +587,9 @@ extern "C" int co_forward(co_conv* h, const void* x, int64_t T, void* y, int64_t
   int64_t Tp = 0;
   co_forward_out_len(h, T, &Tp);
   if (Tp < 1) return fail(CO_ERR_LENGTH, "T' = %lld < 1 (T = %lld too short, S:63-65)", (long long)Tp, (long long)T);
-  cudaError_t e = co::launch_forward_direct(h->g, x, T, y, Tp, h->w_direct, h->bias, (cudaStream_t)stream);
+  cudaError_t e = h->kernel_used == CO_KERNEL_POOL
+                      ? co::launch_forward_pool(h->g, x, T, y, Tp, (cudaStream_t)stream)
+                      : co::launch_forward_direct(h->g, x, T, y, Tp, h->w_direct, h->bias, (cudaStream_t)stream);
   if (e != cudaSuccess) return fail(CO_ERR_CUDA, "forward kernel: %s", cudaGetErrorString(e));
   if (T_out) *T_out = Tp;
   return CO_OK;
@@ -621,7 +658,10 @@ extern "C" int co_state_set(co_conv* h, const void* src, size_t bytes, const co_
 extern "C" int co_state_clean(co_conv* h, co_stream stream) {
   if (!h) return fail(CO_ERR_ARG, "null handle");
   const Geom& g = h->g;
-  if (state_alloc_bytes(g) > 0) CO_CUDA(cudaMemsetAsync(h->state, 0, state_alloc_bytes(g), (cudaStream_t)stream));
+  if (g.op != CO_OP_CONV)
+    CO_CUDA(co::launch_fill_pad(g, h->state, int64_t(state_alloc_bytes(g) / dsize(g.in_dtype)), (cudaStream_t)stream));
+  else if (state_alloc_bytes(g) > 0)
+    CO_CUDA(cudaMemsetAsync(h->state, 0, state_alloc_bytes(g), (cudaStream_t)stream));
   h->n = 0;
   return CO_OK;
 }

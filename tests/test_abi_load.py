@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol(libpath):
 def test_library_loads_without_gpu(libpath):
     L = ctypes.CDLL(libpath)
     L.co_abi_version.restype = ctypes.c_int
-    assert L.co_abi_version() == 2
+    assert L.co_abi_version() == 3
     L.co_last_error.restype = ctypes.c_char_p
     assert L.co_last_error() == b""
 

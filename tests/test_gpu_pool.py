@@ -1,0 +1,192 @@
+"""GPU parity of continual pooling (
+SPEC.md:252-297) through the C ABI (co_op MAX / AVG) against the fp64 pooling
+oracle (oracle/pool.py): step outputs and readiness, batch forward, the
+forward_steps fold with pad_end == batch (Definition 1), the state
+contract (co_state_get == oracle history with -inf pads for MAX, get->set round
+trip, update_state=0 purity), stacking with convolutions, and error codes.
+
+Tolerances: MAX is exact (a max of representable values; fp32 accumulation of
+bf16 inputs is exact), so MAX compares bit for bit; AVG is an fp32 sum of at
+most kt kh kw terms times 1/(kt kh kw): fp32 outputs within 1e-4 of the RMS,
+bf16 outputs within one bf16 rounding (tests/helpers.assert_bf16_rounding_bound).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import pool as OP
+from tests.helpers import assert_bf16_rounding_bound, np_of, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _tcl(x: np.ndarray, dtype) -> torch.Tensor:
+    import paper_2204_03418_b200 as co
+    return co.channels_last(torch.from_numpy(np.ascontiguousarray(x)).to(dtype).cuda())
+
+
+def _quant(x: np.ndarray, dtype) -> np.ndarray:
+    return torch.from_numpy(x).to(dtype).double().numpy()
+
+
+def _spatial(rank, H, W):
+    return ((H,) if rank >= 1 else ()) + ((W,) if rank >= 2 else ())
+
+
+def rand_pool(rng):
+    rank = int(rng.integers(0, 3))
+    kt = int(rng.integers(1, 5))
+    dt = int(rng.integers(1, 3))
+    f = dt * (kt - 1) + 1
+    kh = int(rng.integers(1, 4)) if rank >= 1 else 1
+    kw = int(rng.integers(1, 4)) if rank >= 2 else 1
+    st = (int(rng.integers(1, 3)), int(rng.integers(1, 3)) if rank >= 1 else 1, int(rng.integers(1, 3)) if rank >= 2 else 1)
+    pad = (int(rng.integers(0, f)), int(rng.integers(0, kh)), int(rng.integers(0, kw)))
+    dil = (dt, int(rng.integers(1, 3)) if rank >= 1 else 1, 1)
+    H = int(rng.integers(dil[1] * (kh - 1) + 1, 7)) if rank >= 1 else 1
+    W = int(rng.integers(kw, 7)) if rank >= 2 else 1
+    C = int(rng.choice([1, 2, 3, 4, 8, 16, 24]))
+    return rank, (kt, kh, kw), st, pad, dil, H, W, C
+
+
+def _make(kind, rank, kernel, stride, pad, dil, H, W, C, B, dtype, out_dtype):
+    import paper_2204_03418_b200 as co
+    n = rank + 1
+    p = co.Pool(kind, C, kernel[:n], stride=stride[:n], padding=pad[:n], dilation=dil[:n], spatial_rank=rank,
+                in_spatial=(H, W)[:rank] or (1,), n_streams=B, dtype=dtype, out_dtype=out_dtype)
+    sm = OP.PoolStep(kind, C, (H, W), kernel, stride, pad, dil, B=B)
+    return p, sm
+
+
+def _compare(kind, y, ref, out_dtype):
+    if kind == "max":
+        np.testing.assert_array_equal(y, ref)
+    elif out_dtype == torch.bfloat16:
+        assert_bf16_rounding_bound(y, ref)
+    else:
+        assert rel_err(y, ref) <= 1e-4
+
+
+@pytest.mark.parametrize("seed", range(20))
+@pytest.mark.parametrize("kind", ["max", "avg"])
+def test_pool_step_random_vs_oracle(kind, seed):
+    rng = np.random.default_rng(500 + seed)
+    rank, kernel, stride, pad, dil, H, W, C = rand_pool(rng)
+    B = int(rng.integers(1, 4))
+    dtype = torch.bfloat16 if seed % 2 else torch.float32
+    out_dtype = torch.float32 if seed % 4 < 2 else dtype
+    p, sm = _make(kind, rank, kernel, stride, pad, dil, H, W, C, B, dtype, out_dtype)
+    assert p.kernel_used == "pool" and p.delay == sm.delay
+    shp = (B, C) + _spatial(rank, H, W)
+    f = sm.f
+    for t in range(f + 2 * stride[0] + 3):
+        xq = _quant(rng.standard_normal(shp), dtype)
+        y = p.forward_step(_tcl(xq, dtype))
+        r = sm.forward_step(xq.reshape(B, C, H, W))
+        assert (y is None) == (r is None), t
+        assert p.n == sm.n
+        if y is not None:
+            _compare(kind, np_of(y).reshape(r.shape), r, out_dtype)
+    # pad_end steps (x = None): padding, -inf for MAX
+    for _ in range(pad[0]):
+        y = p.forward_step(None)
+        r = sm.forward_step(None)
+        assert (y is None) == (r is None)
+        if y is not None:
+            _compare(kind, np_of(y).reshape(r.shape), r, out_dtype)
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("kind", ["max", "avg"])
+def test_pool_forward_and_fold_vs_oracle(kind, seed):
+    rng = np.random.default_rng(700 + seed)
+    rank, kernel, stride, pad, dil, H, W, C = rand_pool(rng)
+    B = int(rng.integers(1, 3))
+    dtype = torch.bfloat16 if seed % 2 else torch.float32
+    p, _ = _make(kind, rank, kernel, stride, pad, dil, H, W, C, B, dtype, torch.float32)
+    f = dil[0] * (kernel[0] - 1) + 1
+    T = int(rng.integers(max(1, f - 2 * pad[0]), f + 7))
+    xq = _quant(rng.standard_normal((B, C, T) + _spatial(rank, H, W)), dtype)
+    ref = OP.pool_forward(kind, xq.reshape(B, C, T, H, W), kernel, stride, pad, dil)
+    yb = p.forward(_tcl(xq, dtype))
+    _compare(kind, np_of(yb).reshape(ref.shape), ref, torch.float32)
+    ys, mask = p.forward_steps(_tcl(xq, dtype), pad_end=True)
+    assert int(mask.sum()) == ref.shape[2]
+    assert torch.equal(ys, yb)                      # same reduction order: bitwise (Definition 1)
+
+
+@pytest.mark.parametrize("kind", ["max", "avg"])
+def test_pool_state_contract(kind):
+    rng = np.random.default_rng(9)
+    B, C, H, W = 2, 16, 5, 6
+    kernel, stride, pad, dil = (3, 3, 3), (1, 2, 2), (2, 1, 1), (1, 1, 1)
+    p, sm = _make(kind, 2, kernel, stride, pad, dil, H, W, C, B, torch.bfloat16, torch.float32)
+    frames = [_quant(rng.standard_normal((B, C, H, W)), torch.bfloat16) for _ in range(7)]
+    for x in frames[:1]:
+        p.forward_step(_tcl(x, torch.bfloat16)); sm.forward_step(x)
+    # canonical state == oracle history; start padding is -inf for MAX, 0 for AVG
+    st, meta = p.state_dict_stream()
+    hist, flags = sm.history()
+    got = np.moveaxis(np_of(st), -1, 2)
+    exp = hist.copy()
+    if kind == "max":
+        exp[np.array(flags, bool)] = -np.inf
+    np.testing.assert_array_equal(got, exp)
+    # update_state=False: output from the current state, state bitwise unchanged
+    y0 = p.forward_step(_tcl(frames[1], torch.bfloat16), update_state=False)
+    r0 = sm.forward_step(frames[1], update_state=False)
+    _compare(kind, np_of(y0), r0, torch.float32)
+    st2, _ = p.state_dict_stream()
+    assert torch.equal(st, st2) and p.n == 1
+    # round trip: continue from a restored copy in a second handle
+    q, _ = _make(kind, 2, kernel, stride, pad, dil, H, W, C, B, torch.bfloat16, torch.float32)
+    q.load_state_stream(st, meta)
+    for x in frames[1:]:
+        a = p.forward_step(_tcl(x, torch.bfloat16))
+        b = q.forward_step(_tcl(x, torch.bfloat16))
+        r = sm.forward_step(x)
+        assert (a is None) == (b is None) == (r is None)
+        if a is not None:
+            assert torch.equal(a, b)
+            _compare(kind, np_of(a), r, torch.float32)
+    # clean state restores the padding value
+    p.clean_state()
+    st3, _ = p.state_dict_stream()
+    expect = float("-inf") if kind == "max" else 0.0
+    assert bool((st3.float() == expect).all())
+
+
+def test_pool_in_stack_with_convs():
+    """conv -> max pool -> conv as one co_stack: the stack step equals the
+    layer-by-layer fold, and the pool's Ready outputs gate the next layer."""
+    import paper_2204_03418_b200 as co
+    rng = np.random.default_rng(4)
+    B, C, H, W = 2, 32, 6, 6
+    w1 = torch.from_numpy(rng.standard_normal((C, C, 3, 3, 3)) / 16).to(torch.bfloat16).cuda()
+    w2 = torch.from_numpy(rng.standard_normal((C, C, 1, 1, 1)) / 6).to(torch.bfloat16).cuda()
+    mk = lambda: [co.Conv(C, C, (3, 3, 3), weight=w1, padding=(0, 1, 1), in_spatial=(H, W), n_streams=B),
+                  co.Pool("max", C, (2, 3, 3), stride=(2, 2, 2), padding=(0, 1, 1), in_spatial=(H, W), n_streams=B),
+                  co.Conv(C, C, (1, 1, 1), weight=w2, in_spatial=(3, 3), n_streams=B, out_dtype=torch.float32)]
+    layers = mk()
+    st = co.Stack(layers)
+    ref_layers = mk()
+    for t in range(9):
+        x = _tcl(rng.standard_normal((B, C, H, W)), torch.bfloat16)
+        y = st.forward_step(x)
+        cur = x
+        for L in ref_layers:
+            cur = L.forward_step(cur)
+            if cur is None:
+                break
+        assert (y is None) == (cur is None), t
+        if y is not None:
+            assert torch.equal(y, cur)
+
+
+def test_pool_errors():
+    import paper_2204_03418_b200 as co
+    from paper_2204_03418_b200._abi import CoError
+    with pytest.raises(CoError):      # temporal padding > f-1
+        co.Pool("avg", 8, (3, 1, 1), padding=(3, 0, 0), in_spatial=(2, 2))
+    with pytest.raises(ValueError):
+        co.Pool("sum", 8, (3, 1, 1), in_spatial=(2, 2))
