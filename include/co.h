@@ -82,16 +82,19 @@ typedef enum { CO_STATE_PSUM = 0, CO_STATE_RAW = 1 } co_state_layout;
 /* Operation of a handle ("Pooling:
  * co.AvgPool1d, co.MaxPool1d, etc.").  A pooling handle has
  * in_channels == out_channels (groups is ignored), no weights or bias
- * (create takes weights = bias = NULL), always keeps the RAW frame ring
- * (state_layout is ignored; co_info reports RAW) and dispatches
- * CO_KERNEL_POOL.  Padding (temporal and spatial) is 0 and counted in the
- * divisor for AVG (count_include_pad, divisor kt kh kw, A21) and is
- * ignored for MAX (PyTorch's implicit -inf padding; a window of padding only
- * yields -inf, A22).  In MAX handles the ring stores padding frames as -inf:
- * clean state, pad_end steps (x == NULL) and the canonical state
- * (co_state_get) carry -inf for padded frames.  Clock, readiness, delay and
- * the call modes are those of a convolution with the same kernel / stride /
- * padding / dilation (Definition 1). */
+ * (create takes weights = bias = NULL), dispatches CO_KERNEL_POOL, and keeps a
+ * ring of the last f SPATIALLY REDUCED frames (B, S1', S2', C): pooling is
+ * separable, so each step reduces its frame over the spatial window once and a
+ * Ready step folds kt reduced frames (state_layout is ignored; co_info reports
+ * RAW).  kt is not bounded by CO_MAX_KT (the paper's 64-step expanded global
+ * average pooling).  Padding (temporal and spatial) is 0 and counted in
+ * the divisor for AVG (count_include_pad, divisor kt kh kw, A21) and
+ * is ignored for MAX (PyTorch's implicit -inf padding; a window of padding only
+ * yields -inf, A22).  Canonical state (co_state_get): (f-1, B, S1', S2', C),
+ * MAX in in_dtype with padded frames -inf, AVG fp32 spatial-window sums with
+ * padded frames 0.  Clock, readiness, delay and the call modes are those of a
+ * convolution with the same kernel / stride / padding / dilation
+ * (Definition 1). */
 typedef enum { CO_OP_CONV = 0, CO_OP_MAX_POOL = 1, CO_OP_AVG_POOL = 2 } co_op;
 
 typedef void* co_stream;                 /* cudaStream_t */

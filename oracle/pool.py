@@ -137,6 +137,23 @@ class PoolStep:
             return np.zeros((0, self.B, self.C, self.H, self.W)), []
         return np.stack(self.hist), list(self.hpad)
 
+    def reduced_history(self):
+        """The history as the GPU handle stores it (include/co.h co_op): each
+        frame's spatial-window reduction (C, H', W') -- the window max, or the
+        window SUM for AVG -- with padding frames the identity (-inf / 0);
+        (f-1, B, C, H', W')."""
+        Ho, Wo = self.out_spatial
+        kt, kh, kw = self.kernel
+        out = np.empty((self.f - 1, self.B, self.C, Ho, Wo))
+        for j, (fr, pad) in enumerate(zip(self.hist, self.hpad)):
+            for b in range(self.B):
+                for ho in range(Ho):
+                    for wo in range(Wo):
+                        col = _pool_window(self.kind, [fr[b]], [pad], ho, wo, (1, kh, kw), self.stride,
+                                           self.padding, self.dilation, self.H, self.W)
+                        out[j, b, :, ho, wo] = col if self.kind == "max" else col * (kh * kw)
+        return out
+
     @property
     def out_spatial(self):
         kt, kh, kw = self.kernel

@@ -210,11 +210,16 @@ class Conv:
 
     def state_dict_stream(self, stream=None):
         """Canonical state and the clock (co_state_get): PSUM (R, B, *S', Cout)
-        fp32; RAW (f-1, B, *S, Cin) in the input dtype (the last f-1 frames)."""
+        fp32; RAW (f-1, B, *S, Cin) in the input dtype (the last f-1 frames);
+        pooling (f-1, B, *S', C): the last f-1 spatially reduced frames (MAX in
+        the input dtype, -inf padding; AVG fp32 window sums, 0 padding)."""
         nb = C.c_size_t()
         check(lib().co_state_bytes(self._h, C.byref(nb)))
         info = self.info()
-        if self.state_layout == "raw":
+        if self.op != "conv":
+            st = torch.empty((info.ring_slots, self.n_streams) + self.out_spatial + (self.in_channels,),
+                             dtype=self._ring_dtype(), device=self.device)
+        elif self.state_layout == "raw":
             st = torch.empty((info.ring_slots, self.n_streams) + self.in_spatial + (self.in_channels,),
                              dtype=self.dtype, device=self.device)
         else:
@@ -228,9 +233,16 @@ class Conv:
     def load_state_stream(self, state: torch.Tensor, meta: CoInfo, stream=None):
         nb = C.c_size_t()
         check(lib().co_state_bytes(self._h, C.byref(nb)))
-        state = state.to(self.dtype if self.state_layout == "raw" else torch.float32).contiguous()
+        if self.op != "conv":
+            state = state.to(self._ring_dtype()).contiguous()
+        else:
+            state = state.to(self.dtype if self.state_layout == "raw" else torch.float32).contiguous()
         check(lib().co_state_set(self._h, C.c_void_p(state.data_ptr()) if state.numel() else None, nb.value,
                                  C.byref(meta), _stream(stream)))
+
+    def _ring_dtype(self):
+        # pooling ring: spatially reduced frames, MAX in the input dtype, AVG fp32 sums
+        return self.dtype if self.op == "max" else torch.float32
 
     @property
     def n(self) -> int:

@@ -87,7 +87,13 @@ struct StepArgs {
   int slot[kMaxKt];
   int emit;              // ready: produce y from slice kt-1
   int update;            // update_state: write the ring
+  int64_t m;             // padded index n + p of this frame (pooling: ring slots computed on the device)
 };
+
+// Pooling ring (§8f f3): slot = one spatially reduced frame (B, Ho, Wo, C); MAX
+// keeps the input dtype (a max is exact), AVG fp32 spatial sums.
+inline int pool_ring_esz(const Geom& g) { return g.op == OP_AVG_POOL ? 4 : (g.in_dtype == BF16 ? 2 : 4); }
+inline int64_t pool_slot_elems(const Geom& g) { return g.B * g.HWo * g.Cin; }
 
 __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }

@@ -146,7 +146,8 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
     return fail(CO_ERR_ARG, "groups (%d) must divide in_channels (%d) and out_channels (%d)", d->groups,
                 d->in_channels, d->out_channels);
   if (d->n_streams < 1) return fail(CO_ERR_ARG, "n_streams must be >= 1");
-  if (k[0] > CO_MAX_KT) return fail(CO_ERR_UNSUPPORTED, "temporal kernel %d > CO_MAX_KT", k[0]);
+  if (d->op == CO_OP_CONV && k[0] > CO_MAX_KT) return fail(CO_ERR_UNSUPPORTED, "temporal kernel %d > CO_MAX_KT", k[0]);
+  if (int64_t(dl[0]) * (k[0] - 1) + 1 > (1 << 20)) return fail(CO_ERR_UNSUPPORTED, "receptive field > 2^20 frames");
   for (int t : {d->in_dtype, d->w_dtype, d->out_dtype})
     if (t != CO_F32 && t != CO_BF16) return fail(CO_ERR_ARG, "dtype must be CO_F32 or CO_BF16");
   if (d->w_dtype != d->in_dtype) return fail(CO_ERR_ARG, "w_dtype must equal in_dtype");
@@ -187,13 +188,19 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
 
 // Device bytes of a handle's state: the fp32 partial-sum ring (PSUM), or the
 // ring of f + 1 input frames (RAW: f data slots + a scratch slot).
+// Pooling handles keep f + 1 spatially reduced frames (k_pool.cu).
+static size_t ring_slot_bytes(const Geom& g) {
+  if (g.op != CO_OP_CONV) return size_t(co::pool_slot_elems(g)) * co::pool_ring_esz(g);
+  return size_t(g.B) * g.frame_elems * dsize(g.in_dtype);
+}
 static size_t state_alloc_bytes(const Geom& g) {
-  if (g.raw) return size_t(g.f + 1) * g.B * g.frame_elems * dsize(g.in_dtype);
+  if (g.raw) return size_t(g.f + 1) * ring_slot_bytes(g);
   return sizeof(float) * g.slot_elems * g.R;
 }
-// Canonical state bytes (co_state_bytes): PSUM (R, B, S', Cout) fp32; RAW (f-1, B, S, Cin) in_dtype.
+// Canonical state bytes (co_state_bytes): PSUM (R, B, S', Cout) fp32; RAW
+// (f-1, B, S, Cin) in_dtype; pooling (f-1, B, S', C) in the ring dtype.
 static size_t state_canon_bytes(const Geom& g) {
-  if (g.raw) return size_t(g.f - 1) * g.B * g.frame_elems * dsize(g.in_dtype);
+  if (g.raw) return size_t(g.f - 1) * ring_slot_bytes(g);
   return sizeof(float) * size_t(g.R) * g.B * g.HWo * g.Cout;
 }
 
@@ -242,7 +249,7 @@ static int create_pool(const co_conv_desc* desc, const Geom& g, const void* weig
     co_conv_destroy(h);
     return fail(CO_ERR_OOM, "state (%lld bytes): %s", (long long)sb, cudaGetErrorString(e));
   }
-  if ((e = co::launch_fill_pad(g, h->state, int64_t(sb / dsize(g.in_dtype)), 0)) != cudaSuccess ||
+  if ((e = co::launch_fill_pad(g, h->state, int64_t(sb / co::pool_ring_esz(g)), 0)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess) {
     co_conv_destroy(h);
     return fail(CO_ERR_CUDA, "pool state init: %s", cudaGetErrorString(e));
@@ -408,7 +415,7 @@ static int step_raw(co_conv* h, int64_t& n, float* state, const void* x, int64_t
   char* slot = reinterpret_cast<char*>(state) + size_t(cur) * g.B * fb;
   if (x) CO_CUDA(cudaMemcpy2DAsync(slot, fb, x, size_t(x_bstride) * dsize(g.in_dtype), fb, g.B,
                                    cudaMemcpyDeviceToDevice, s));
-  else CO_CUDA(co::launch_fill_pad(g, slot, g.B * g.frame_elems, s));   // padding step: 0, or -inf for MAX
+  else CO_CUDA(cudaMemsetAsync(slot, 0, g.B * fb, s));
   if (r) {
     StepArgs a;
     for (int k = 0; k < co::kMaxKt; ++k) a.slot[k] = -1;
@@ -426,8 +433,33 @@ static int step_raw(co_conv* h, int64_t& n, float* state, const void* x, int64_t
   return CO_OK;
 }
 
+// Pooling tick: one fused launch reduces the frame spatially into ring slot
+// m mod f (update_state) and, when Ready, folds the window (k_pool.cu).
+static int step_pool(co_conv* h, int64_t& n, float* state, const void* x, int64_t x_bstride, void* y,
+                     int64_t y_bstride, int update_state, int* ready, cudaStream_t s) {
+  const Geom& g = h->g;
+  const int64_t m = n + g.pt;
+  const int r = (n >= g.delay) && floor_mod(n - g.delay, g.st) == 0;
+  if (r || update_state) {
+    StepArgs a;
+    for (int k = 0; k < co::kMaxKt; ++k) a.slot[k] = -1;
+    a.slot[0] = update_state ? int(floor_mod(m, g.f)) : -1;
+    a.x = x; a.x_bstride = x_bstride;
+    a.y = y; a.y_bstride = y_bstride;
+    a.state = state;
+    a.emit = r;
+    a.update = update_state ? 1 : 0;
+    a.m = m;
+    if (int rc = launch_step(h, a, s)) return rc;
+  }
+  if (update_state) ++n;
+  if (ready) *ready = r;
+  return CO_OK;
+}
+
 static int step_impl(co_conv* h, int64_t& n, float* state, const void* x, int64_t x_bstride, void* y,
                      int64_t y_bstride, int update_state, int* ready, cudaStream_t s) {
+  if (h->g.op != CO_OP_CONV) return step_pool(h, n, state, x, x_bstride, y, y_bstride, update_state, ready, s);
   if (h->g.raw) return step_raw(h, n, state, x, x_bstride, y, y_bstride, update_state, ready, s);
   StepArgs a;
   const int r = clock_args(h->g, n, a);
@@ -612,7 +644,7 @@ extern "C" int co_state_get(co_conv* h, void* dst, size_t bytes, co_info* meta, 
   const Geom& g = h->g;
   if (need && g.raw) {   // canonical slot j = padded frame m-(f-1)+j, m = n + p
     if (!dst) return fail(CO_ERR_ARG, "null dst");
-    const size_t sb = size_t(g.B) * g.frame_elems * dsize(g.in_dtype);
+    const size_t sb = ring_slot_bytes(g);
     for (int j = 0; j < g.f - 1; ++j) {
       const int src = int(floor_mod(h->n + g.pt - (g.f - 1) + j, g.f));
       CO_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + j * sb, reinterpret_cast<char*>(h->state) + src * sb, sb,
@@ -640,7 +672,7 @@ extern "C" int co_state_set(co_conv* h, const void* src, size_t bytes, const co_
     return fail(CO_ERR_SHAPE, "state meta does not match this layer");
   if (need && g.raw) {
     if (!src) return fail(CO_ERR_ARG, "null src");
-    const size_t sb = size_t(g.B) * g.frame_elems * dsize(g.in_dtype);
+    const size_t sb = ring_slot_bytes(g);
     for (int j = 0; j < g.f - 1; ++j) {
       const int dstslot = int(floor_mod(meta->n + g.pt - (g.f - 1) + j, g.f));
       CO_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(h->state) + dstslot * sb, static_cast<const char*>(src) + j * sb,
@@ -659,7 +691,7 @@ extern "C" int co_state_clean(co_conv* h, co_stream stream) {
   if (!h) return fail(CO_ERR_ARG, "null handle");
   const Geom& g = h->g;
   if (g.op != CO_OP_CONV)
-    CO_CUDA(co::launch_fill_pad(g, h->state, int64_t(state_alloc_bytes(g) / dsize(g.in_dtype)), (cudaStream_t)stream));
+    CO_CUDA(co::launch_fill_pad(g, h->state, int64_t(state_alloc_bytes(g) / co::pool_ring_esz(g)), (cudaStream_t)stream));
   else if (state_alloc_bytes(g) > 0)
     CO_CUDA(cudaMemsetAsync(h->state, 0, state_alloc_bytes(g), (cudaStream_t)stream));
   h->n = 0;

@@ -1,0 +1,117 @@
+#!/usr/bin/env python
+"""Benchmark of continual pooling, the companion of
+bench.py for the pooling handles (co_op MAX / AVG).  Prints one JSON line per
+workload with bench.py's timing rules: W >= 3 untimed warm-up steps, K steps
+timed with CUDA events on the launching stream, synchronize on both sides,
+NVML clocks sampled during the timed region, inputs rotating over a pool of
+distinct frames larger than L2.
+
+Workloads (seeded N(0,1) bf16 frames; no BASELINE.json config covers pooling):
+  x3d64  -- the paper's expanded temporal global average pooling (P:642,
+            CoX3D-M_64, Table 2): AvgPool (64, 7, 7) over the 7x7x432
+            conv5 output of X3D-M at 224 px, 512 streams (C3's stream count).
+  max3   -- an I3D-style max pool (3, 3, 3), stride (1, 2, 2), padding
+            (0, 1, 1) on the C2 activation shape (56x56x64, 256 streams).
+
+Algorithmic bytes per stream-step of the pooled-ring design (k_pool.cu):
+x (H W C, bf16) + y (H' W' C) + ring write (H' W' C x ring esz) + (kt-1) ring
+reads; the ring element is the input dtype for MAX and fp32 for AVG.
+
+usage: python scripts/bench_pool.py [--workload x3d64|max3|all] [--steps K] [--warmup W]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "x3d64": dict(kind="avg", C=432, H=7, W=7, kernel=(64, 7, 7), stride=(1, 1, 1), padding=(0, 0, 0), B=512,
+                  desc="expanded temporal global avg pool, CoX3D-M_64 head (P:642): AvgPool(64,7,7), 7x7x432, 512 streams"),
+    "max3": dict(kind="max", C=64, H=56, W=56, kernel=(3, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1), B=256,
+                 desc="I3D-style MaxPool(3,3,3) s(1,2,2) p(0,1,1) on 56x56x64, 256 streams"),
+}
+
+
+def alg_bytes(w, Ho, Wo):
+    esz, resz = 2, (4 if w["kind"] == "avg" else 2)
+    x = w["H"] * w["W"] * w["C"] * esz
+    y = Ho * Wo * w["C"] * esz
+    ring = Ho * Wo * w["C"] * resz
+    return x + y + ring + (w["kernel"][0] - 1) * ring
+
+
+def run(name, steps, warmup):
+    import torch
+    import paper_2204_03418_b200 as co
+    from bench import ClockSampler, measured_peaks
+
+    w = WORKLOADS[name]
+    B, C, H, W = w["B"], w["C"], w["H"], w["W"]
+    p = co.Pool(w["kind"], C, w["kernel"], stride=w["stride"], padding=w["padding"], in_spatial=(H, W), n_streams=B)
+    Ho, Wo = p.out_spatial
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    fbytes = B * C * H * W * 2
+    G = min(max(4, math.ceil(4 * l2 / fbytes)), 32)
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    pool = [co.channels_last(torch.randn((B, C, H, W), generator=g, device="cuda").to(torch.bfloat16))
+            for _ in range(G)]
+    y = co._empty_cl((B, C, Ho, Wo), torch.bfloat16, "cuda")
+    stream = torch.cuda.current_stream()
+    for n in range(max(warmup, 3) + p.delay):
+        p.forward_step(pool[n % G], out=y)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(torch.cuda.current_device())
+    with sampler:
+        e0.record(stream)
+        for k in range(steps):
+            assert p.forward_step(pool[k % G], out=y) is not None
+        e1.record(stream)
+        t_end = time.time() + 60
+        while not e1.query() and time.time() < t_end:
+            sampler.sample()
+            time.sleep(0.002)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    hbm, _, src = measured_peaks()
+    ab = alg_bytes(w, Ho, Wo) * B
+    ach = ab / (ms / 1e3) / 1e9
+    ring_mb = (p.receptive_field + 1) * B * Ho * Wo * C * (4 if w["kind"] == "avg" else 2) / 1e6
+    out = {
+        "metric": "stream-steps/sec per continual pooling layer", "value": round(B / (ms / 1e3), 1),
+        "unit": "stream-steps/s", "n_gpus": 1, "steps": steps, "warmup": warmup, "ms_per_step": round(ms, 5),
+        "higher_is_better": True, "dtype": "bf16", "data": "synthetic (seeded N(0,1) bf16 frames)",
+        "config": {"workload": name, "desc": w["desc"], "streams": B, "kernel": list(w["kernel"]),
+                   "stride": list(w["stride"]), "padding": list(w["padding"]), "in": [H, W, C], "out": [Ho, Wo, C],
+                   "ring_MB": round(ring_mb, 1),
+                   "l2_policy": f"input pool of {G} distinct frames ({round(G * fbytes / 1e6)} MB > L2 "
+                                f"{l2 // 2**20} MiB); the reduced-frame ring ({round(ring_mb, 1)} MB) may stay L2-resident"},
+        "gpu_launches": steps,
+        "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(ach / hbm, 4), "kernel": p.kernel_name, "alg_bytes_per_launch": int(ab),
+                     "peak_source": src, "traffic": None},
+        "clocks": sampler.summary(),
+    }
+    print(json.dumps(out), flush=True)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="all", choices=["all"] + list(WORKLOADS))
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    a = ap.parse_args()
+    for name in (WORKLOADS if a.workload == "all" else [a.workload]):
+        run(name, a.steps, a.warmup)
+
+
+if __name__ == "__main__":
+    main()

@@ -124,14 +124,16 @@ def test_pool_state_contract(kind):
     frames = [_quant(rng.standard_normal((B, C, H, W)), torch.bfloat16) for _ in range(7)]
     for x in frames[:1]:
         p.forward_step(_tcl(x, torch.bfloat16)); sm.forward_step(x)
-    # canonical state == oracle history; start padding is -inf for MAX, 0 for AVG
+    # canonical state == the oracle history reduced over the spatial window
+    # (include/co.h co_op); start padding is -inf for MAX, 0 for AVG
     st, meta = p.state_dict_stream()
-    hist, flags = sm.history()
+    assert st.dtype == (torch.bfloat16 if kind == "max" else torch.float32)
     got = np.moveaxis(np_of(st), -1, 2)
-    exp = hist.copy()
+    exp = sm.reduced_history()
     if kind == "max":
-        exp[np.array(flags, bool)] = -np.inf
-    np.testing.assert_array_equal(got, exp)
+        np.testing.assert_array_equal(got, exp)
+    else:
+        assert rel_err(got, exp) <= 1e-6
     # update_state=False: output from the current state, state bitwise unchanged
     y0 = p.forward_step(_tcl(frames[1], torch.bfloat16), update_state=False)
     r0 = sm.forward_step(frames[1], update_state=False)
@@ -190,3 +192,24 @@ def test_pool_errors():
         co.Pool("avg", 8, (3, 1, 1), padding=(3, 0, 0), in_spatial=(2, 2))
     with pytest.raises(ValueError):
         co.Pool("sum", 8, (3, 1, 1), in_spatial=(2, 2))
+
+
+@pytest.mark.parametrize("kind", ["avg", "max"])
+def test_expanded_global_pool_kt64(kind):
+    """The paper's expanded temporal global average pooling ("64
+    steps"): kernel (64, 7, 7) over 7x7 frames -- kt above CO_MAX_KT, ring
+    slots computed on the device."""
+    rng = np.random.default_rng(64)
+    B, C, H, W = 3, 48, 7, 7
+    p, sm = _make(kind, 2, (64, 7, 7), (1, 1, 1), (0, 0, 0), (1, 1, 1), H, W, C, B, torch.bfloat16, torch.float32)
+    assert p.delay == 63 and p.receptive_field == 64 and p.out_spatial == (1, 1)
+    ys, refs = [], []
+    for t in range(70):
+        xq = _quant(rng.standard_normal((B, C, H, W)), torch.bfloat16)
+        y = p.forward_step(_tcl(xq, torch.bfloat16))
+        r = sm.forward_step(xq)
+        assert (y is None) == (r is None)
+        if y is not None:
+            ys.append(np_of(y).reshape(r.shape)); refs.append(r)
+    assert len(ys) == 7
+    _compare(kind, np.stack(ys), np.stack(refs), torch.float32)

@@ -130,3 +130,30 @@ def test_update_state_false_leaves_state():
 def test_padding_bounds():
     with pytest.raises(ValueError):
         OP.PoolStep("avg", 1, (1, 1), (3, 1, 1), padding=(3, 0, 0))
+
+
+@pytest.mark.parametrize("kind", ["max", "avg"])
+def test_reduced_history_folds_to_the_step_output(kind):
+    """Separability (k_pool.cu's design, checked on the oracle): folding the
+    reduced history's taps with the new frame's spatial reduction gives the
+    step output (AVG: divided by kt kh kw)."""
+    rng = np.random.default_rng(31)
+    kernel, stride, padding, dilation = (3, 3, 2), (1, 2, 1), (2, 1, 1), (2, 1, 1)
+    sm = OP.PoolStep(kind, 2, (5, 4), kernel, stride, padding, dilation, B=2)
+    probe = OP.PoolStep(kind, 2, (5, 4), (1,) + kernel[1:], stride, (0,) + padding[1:], (1,) + dilation[1:], B=2)
+    for _ in range(9):
+        x = rng.standard_normal((2, 2, 5, 4))
+        hist = sm.reduced_history()                       # (f-1, B, C, H', W')
+        y = sm.forward_step(x, update_state=False)
+        if y is None:
+            sm.forward_step(x)
+            continue
+        cur = probe.forward_step(x, update_state=False)   # spatial-only window
+        f, dil = sm.f, dilation[0]
+        taps = [hist[k * dil] for k in range(kernel[0] - 1)]
+        if kind == "max":
+            exp = np.maximum.reduce(taps + [cur])
+        else:
+            exp = (sum(taps) + cur * (kernel[1] * kernel[2])) / np.prod(kernel)
+        np.testing.assert_allclose(y, exp, rtol=1e-12, atol=1e-12)
+        sm.forward_step(x)
