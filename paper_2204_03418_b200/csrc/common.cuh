@@ -3,6 +3,7 @@
 // nothing with oracle/.
 #pragma once
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
@@ -39,6 +40,8 @@ struct Geom {
   int64_t frame_elems;   // H * W * Cin
   int64_t splane;        // state rows per slot and channel quad: B*HWo, or n_tiles*128 when tile-blocked
   int op;                // Op: continual conv, or max / avg pooling over the RAW ring (§8f f3)
+  int pool_G;            // pooling: lanes per output vector of the step kernel (1 = plain, k_pool.cu)
+  int pool_vh;           // pooling: block-decomposition state (P, S after the ring) for long windows
 };
 
 // Physical state layouts (internal; co_state_get converts to the canonical one):
@@ -94,6 +97,9 @@ struct StepArgs {
 // keeps the input dtype (a max is exact), AVG fp32 spatial sums.
 inline int pool_ring_esz(const Geom& g) { return g.op == OP_AVG_POOL ? 4 : (g.in_dtype == BF16 ? 2 : 4); }
 inline int64_t pool_slot_elems(const Geom& g) { return g.B * g.HWo * g.Cin; }
+// Slots of a pooling handle's state: the ring (f + 1), plus P (dil) and S
+// (dil * kt) of the block decomposition.
+inline int64_t pool_state_slots(const Geom& g) { return g.f + 1 + (g.pool_vh ? int64_t(g.dt) * (g.kt + 1) : 0); }
 
 __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
@@ -112,7 +118,10 @@ cudaError_t launch_step_direct_raw(const Geom& g, const StepArgs& a, const float
 cudaError_t launch_step_pool(const Geom& g, const StepArgs& a, cudaStream_t s);
 cudaError_t launch_forward_pool(const Geom& g, const void* x, int64_t T, void* y, int64_t Tp, cudaStream_t s);
 cudaError_t launch_fill_pad(const Geom& g, void* p, int64_t n_elems, cudaStream_t s);
-const char* pool_kernel_name(const Geom& g);
+std::string pool_kernel_name(const Geom& g);
+int pool_split_lanes(const Geom& g);   // choice of pool_G (env CO_POOL_G overrides)
+int pool_block_decomposition(const Geom& g);   // choice of pool_vh (env CO_POOL_VH overrides)
+cudaError_t launch_pool_rebuild(const Geom& g, void* state, int64_t m_next, cudaStream_t s);
 
 // ---- launchers implemented in the .cu files (host side) --------------------
 cudaError_t launch_step_direct(const Geom& g, const StepArgs& a, const float* w_direct, const float* bias,

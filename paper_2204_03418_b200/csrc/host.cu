@@ -194,6 +194,7 @@ static size_t ring_slot_bytes(const Geom& g) {
   return size_t(g.B) * g.frame_elems * dsize(g.in_dtype);
 }
 static size_t state_alloc_bytes(const Geom& g) {
+  if (g.op != CO_OP_CONV) return size_t(co::pool_state_slots(g)) * ring_slot_bytes(g);
   if (g.raw) return size_t(g.f + 1) * ring_slot_bytes(g);
   return sizeof(float) * g.slot_elems * g.R;
 }
@@ -241,15 +242,17 @@ static int create_pool(const co_conv_desc* desc, const Geom& g, const void* weig
   if (!h) return fail(CO_ERR_OOM, "host allocation");
   h->desc = *desc;
   h->g = g;
+  h->g.pool_G = co::pool_split_lanes(g);
+  h->g.pool_vh = co::pool_block_decomposition(g);
   h->kernel_used = CO_KERNEL_POOL;
-  h->kname = co::pool_kernel_name(g);
-  const size_t sb = state_alloc_bytes(g);
+  h->kname = co::pool_kernel_name(h->g);
+  const size_t sb = state_alloc_bytes(h->g);
   cudaError_t e;
   if ((e = cudaMalloc(&h->state, sb)) != cudaSuccess) {
     co_conv_destroy(h);
     return fail(CO_ERR_OOM, "state (%lld bytes): %s", (long long)sb, cudaGetErrorString(e));
   }
-  if ((e = co::launch_fill_pad(g, h->state, int64_t(sb / co::pool_ring_esz(g)), 0)) != cudaSuccess ||
+  if ((e = co::launch_fill_pad(h->g, h->state, int64_t(sb / co::pool_ring_esz(g)), 0)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess) {
     co_conv_destroy(h);
     return fail(CO_ERR_CUDA, "pool state init: %s", cudaGetErrorString(e));
@@ -678,6 +681,8 @@ extern "C" int co_state_set(co_conv* h, const void* src, size_t bytes, const co_
       CO_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(h->state) + dstslot * sb, static_cast<const char*>(src) + j * sb,
                               sb, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     }
+    if (g.op != CO_OP_CONV)   // derived block-decomposition state (k_pool.cu)
+      CO_CUDA(co::launch_pool_rebuild(g, h->state, meta->n + g.pt, (cudaStream_t)stream));
   } else if (need) {
     if (!src) return fail(CO_ERR_ARG, "null src");
     cudaError_t e = co::launch_state_set(g, h->state, (const float*)src, head_of(g, meta->n), (cudaStream_t)stream);

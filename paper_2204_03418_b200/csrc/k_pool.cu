@@ -21,6 +21,9 @@
 // pixel, vector of V channels); consecutive threads take consecutive channel
 // vectors, so frame reads, ring accesses and output writes are coalesced
 // 16-byte accesses.
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <type_traits>
 
 #include "common.cuh"
@@ -28,6 +31,14 @@
 namespace co {
 
 namespace {
+
+// Temporal windows of at least this many taps use the block decomposition
+// (temporal_step VH) instead of the direct fold of kt-1 ring slots.
+constexpr int kVhMinKt = 6;
+
+// Loads in flight per thread in the window loops (4 x 16 B: enough with >= 32
+// resident warps per SM; deeper chunks cost registers and occupancy).
+constexpr int kChunk = 4;
 
 template <typename T, int V>
 struct alignas(sizeof(T) * V) Vec {
@@ -41,22 +52,48 @@ template <> __device__ __forceinline__ __nv_bfloat16 pad_value<__nv_bfloat16>(in
 }
 
 // Spatial window reduction of one frame into s[V] (the identity for an
-// all-outside window).  Shared by the step and batch kernels, so both reduce in
-// the same order and agree bitwise.
-template <typename Tin, int V, bool MAX>
+// all-outside window): taps j = j0, j0 + jstep, ... of the kh x kw window in
+// row-major order, loaded kChunk at a time so their latencies overlap.  The step and
+// batch kernels use the same order (jstep = 1), so they agree bitwise.
+template <typename Tin, int V, bool MAX, int CH = kChunk>
 __device__ __forceinline__ void spatial_reduce(const Geom& g, const Tin* __restrict__ fb, int ho, int wo, int c0,
-                                               float (&s)[V]) {
+                                               float (&s)[V], int j0 = 0, int jstep = 1) {
 #pragma unroll
   for (int j = 0; j < V; ++j) s[j] = MAX ? -INFINITY : 0.f;
-  for (int u = 0; u < g.kh; ++u) {
-    const int hi = ho * g.sh + u * g.dh - g.ph;
-    if (hi < 0 || hi >= g.H) continue;
-    for (int v = 0; v < g.kw; ++v) {
-      const int wi = wo * g.sw + v * g.dw - g.pw;
-      if (wi < 0 || wi >= g.W) continue;
-      const Vec<Tin, V> x = *reinterpret_cast<const Vec<Tin, V>*>(fb + (int64_t(hi) * g.W + wi) * g.Cin + c0);
+  const int nt = g.kh * g.kw;
+  const int h0 = ho * g.sh - g.ph, w0 = wo * g.sw - g.pw;
+  if constexpr (CH == 1) {       // one load in flight: plain nested loops (no per-tap divide)
+    if (jstep == 1) {
+      for (int u = 0; u < g.kh; ++u) {
+        const int hi = h0 + u * g.dh;
+        if (hi < 0 || hi >= g.H) continue;
+        for (int v = 0; v < g.kw; ++v) {
+          const int wi = w0 + v * g.dw;
+          if (wi < 0 || wi >= g.W) continue;
+          const Vec<Tin, V> x = *reinterpret_cast<const Vec<Tin, V>*>(fb + (int64_t(hi) * g.W + wi) * g.Cin + c0);
 #pragma unroll
-      for (int j = 0; j < V; ++j) s[j] = MAX ? fmaxf(s[j], to_f(x.v[j])) : s[j] + to_f(x.v[j]);
+          for (int j = 0; j < V; ++j) s[j] = MAX ? fmaxf(s[j], to_f(x.v[j])) : s[j] + to_f(x.v[j]);
+        }
+      }
+      return;
+    }
+  }
+  for (int jb = j0; jb < nt; jb += CH * jstep) {
+    Vec<Tin, V> x[CH];
+    bool ok[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int j = jb + i * jstep;
+      const int u = j / g.kw, v = j - (j / g.kw) * g.kw;
+      const int hi = h0 + u * g.dh, wi = w0 + v * g.dw;
+      ok[i] = j < nt && hi >= 0 && hi < g.H && wi >= 0 && wi < g.W;
+      if (ok[i]) x[i] = *reinterpret_cast<const Vec<Tin, V>*>(fb + (int64_t(hi) * g.W + wi) * g.Cin + c0);
+    }
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      if (!ok[i]) continue;
+#pragma unroll
+      for (int j = 0; j < V; ++j) s[j] = MAX ? fmaxf(s[j], to_f(x[i].v[j])) : s[j] + to_f(x[i].v[j]);
     }
   }
 }
@@ -81,17 +118,194 @@ __device__ __forceinline__ int64_t fmod_pos(int64_t a, int64_t b) {
   return r < 0 ? r + b : r;
 }
 
-// Step: reduce the new frame spatially (x == NULL: a padding frame), store it
-// in ring slot a.slot[0] (-1: update_state = 0, nothing stored), and on a Ready
-// tick fold the window's kt-1 older slots (m - j dil) mod f with it.
-// Ring layout [slot][B][Ho][Wo][C] in Tr (input dtype for MAX, fp32 for AVG).
-template <typename Tin, typename Tout, typename Tr, int V, bool MAX>
-__global__ void __launch_bounds__(256) k_step_pool(Geom g, StepArgs a) {
+// Fold the window's older ring slots k = k0, k0 + kstep, ... < kt-1 (slot of
+// tap k: (m - (kt-1-k) dil) mod f) into acc, in k order, kChunk loads in flight.
+template <typename Tr, int V, bool MAX, int CH = kChunk>
+__device__ __forceinline__ void ring_fold(const Geom& g, const Tr* __restrict__ ring, int64_t slot_elems,
+                                          int64_t off, int64_t m, float (&acc)[V], int k0 = 0, int kstep = 1) {
+  for (int kb = k0; kb + 1 < g.kt; kb += CH * kstep) {
+    Vec<Tr, V> q[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int k = kb + i * kstep;
+      if (k + 1 < g.kt) {
+        const int64_t slot = fmod_pos(m - int64_t(g.kt - 1 - k) * g.dt, g.f);
+        q[i] = *reinterpret_cast<const Vec<Tr, V>*>(ring + slot * slot_elems + off);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      if (kb + i * kstep + 1 >= g.kt) continue;
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] = MAX ? fmaxf(acc[j], to_f(q[i].v[j])) : acc[j] + to_f(q[i].v[j]);
+    }
+  }
+}
+
+// Temporal part of a step, given the new frame's spatial reduction s: store s
+// in ring slot a.slot[0] (-1: update_state = 0, nothing stored) and, when
+// Ready, produce the window's reduction win.
+//  !VH: direct fold of the window's kt-1 older ring slots, then s (the batch
+//       kernel's order: bitwise equal to it).
+//   VH: van Herk / Gil-Werman block decomposition per temporal phase q =
+//       m mod dil (phase index i = m div dil, blocks of kt phase frames): P[q]
+//       is the running reduction of the current block up to i, and at a block
+//       end one suffix pass writes S[q][j mod kt] = reduction of frames j..end
+//       of that block.  A window [i-kt+1, i] is P[q] when i ends a block, else
+//       S[q][(i-kt+1) mod kt] (+) P[q].  O(1) per step (plus one kt-long pass
+//       per kt steps) -- the role of SPEC's running-sum average and monotonic
+//       deque, but exact for MAX, drift-free for AVG (a fixed two-term
+//       sum, no subtraction) and free of data-dependent control flow.
+//  State after the ring: P (dil slots), then S (dil * kt slots), each slot
+//  laid out like a ring slot.
+template <typename Tr, int V, bool MAX, bool VH, int CH>
+__device__ __forceinline__ void temporal_step(const Geom& g, const StepArgs& a, Tr* __restrict__ st, int64_t SE,
+                                              int64_t off, const float (&s)[V], float (&win)[V]) {
+  if (a.slot[0] >= 0) {
+    Vec<Tr, V> w;
+#pragma unroll
+    for (int j = 0; j < V; ++j) w.v[j] = from_f<Tr>(s[j]);
+    *reinterpret_cast<Vec<Tr, V>*>(st + int64_t(a.slot[0]) * SE + off) = w;
+  }
+  if constexpr (!VH) {
+    if (a.emit) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) win[j] = MAX ? -INFINITY : 0.f;
+      ring_fold<Tr, V, MAX, CH>(g, st, SE, off, a.m, win);
+      combine<V, MAX>(win, s);
+    }
+  } else {
+    const int64_t q = a.m % g.dt, i = a.m / g.dt;
+    const int pos = int(i % g.kt);
+    Tr* P = st + (int64_t(g.f + 1) + q) * SE + off;
+    Tr* S = st + (int64_t(g.f + 1) + g.dt + q * g.kt) * SE + off;
+    float pn[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) pn[j] = MAX ? -INFINITY : 0.f;
+    if (pos > 0) {
+      const Vec<Tr, V> pv = *reinterpret_cast<const Vec<Tr, V>*>(P);
+#pragma unroll
+      for (int j = 0; j < V; ++j) pn[j] = to_f(pv.v[j]);
+    }
+    combine<V, MAX>(pn, s);
+    if (a.emit) {
+      if (pos == g.kt - 1) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) win[j] = pn[j];
+      } else {
+        const int64_t js = fmod_pos(i - g.kt + 1, g.kt);
+        const Vec<Tr, V> sv = *reinterpret_cast<const Vec<Tr, V>*>(S + js * SE);
+#pragma unroll
+        for (int j = 0; j < V; ++j) win[j] = to_f(sv.v[j]);
+        combine<V, MAX>(win, pn);
+      }
+    }
+    if (a.update) {
+      Vec<Tr, V> w;
+#pragma unroll
+      for (int j = 0; j < V; ++j) w.v[j] = from_f<Tr>(pn[j]);
+      *reinterpret_cast<Vec<Tr, V>*>(P) = w;
+      if (pos == g.kt - 1) {           // block end: suffix pass over its kt phase frames
+        float acc[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] = s[j];
+        Vec<Tr, V> o;
+#pragma unroll
+        for (int j = 0; j < V; ++j) o.v[j] = from_f<Tr>(acc[j]);
+        *reinterpret_cast<Vec<Tr, V>*>(S + fmod_pos(i, g.kt) * SE) = o;
+        for (int t = 1; t < g.kt; ++t) {
+          const Vec<Tr, V> r =
+              *reinterpret_cast<const Vec<Tr, V>*>(st + fmod_pos(a.m - int64_t(t) * g.dt, g.f) * SE + off);
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            acc[j] = MAX ? fmaxf(to_f(r.v[j]), acc[j]) : to_f(r.v[j]) + acc[j];
+            o.v[j] = from_f<Tr>(acc[j]);
+          }
+          *reinterpret_cast<Vec<Tr, V>*>(S + fmod_pos(i - t, g.kt) * SE) = o;
+        }
+      }
+    }
+  }
+}
+
+// Rebuild P and S of the block decomposition from the ring (after
+// co_state_set): for phase q, with m' the last stepped frame of the phase,
+// P[q] = the reduction of m''s block up to m' in step order, and S = the suffix
+// pass of the last completed block, restricted to the window starts that
+// future steps read (all inside the f-1 frames the ring holds).  Same
+// operations in the same order as the steps, so the values are bitwise those
+// an uninterrupted run would hold.
+template <typename Tr, int V, bool MAX>
+__global__ void k_pool_rebuild(Geom g, Tr* __restrict__ st, int64_t m_next) {
+  const int CV = g.Cin / V;
+  const int64_t SE = g.B * g.HWo * g.Cin;
+  const int64_t total = g.B * g.HWo * CV;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t off = (idx / CV) * g.Cin + (idx % CV) * V;
+    auto ring = [&](int64_t m) { return *reinterpret_cast<const Vec<Tr, V>*>(st + fmod_pos(m, g.f) * SE + off); };
+    for (int q = 0; q < g.dt; ++q) {
+      Tr* P = st + (int64_t(g.f + 1) + q) * SE + off;
+      Tr* S = st + (int64_t(g.f + 1) + g.dt + int64_t(q) * g.kt) * SE + off;
+      const int64_t mp = (m_next - 1) - fmod_pos(m_next - 1 - q, g.dt);   // last stepped frame of phase q
+      Vec<Tr, V> o;
+      float acc[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] = MAX ? -INFINITY : 0.f;
+      if (mp < 0) {                    // nothing stepped in this phase: identity
+#pragma unroll
+        for (int j = 0; j < V; ++j) o.v[j] = from_f<Tr>(acc[j]);
+        *reinterpret_cast<Vec<Tr, V>*>(P) = o;
+        for (int k = 0; k < g.kt; ++k) *reinterpret_cast<Vec<Tr, V>*>(S + k * SE) = o;
+        continue;
+      }
+      const int64_t ip = (mp - q) / g.dt;
+      const int pos = int(ip % g.kt);
+      for (int t = pos; t >= 0; --t) {
+        const Vec<Tr, V> r = ring(mp - int64_t(t) * g.dt);
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] = MAX ? fmaxf(acc[j], to_f(r.v[j])) : acc[j] + to_f(r.v[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < V; ++j) o.v[j] = from_f<Tr>(acc[j]);
+      *reinterpret_cast<Vec<Tr, V>*>(P) = o;
+      const int64_t e = (pos == g.kt - 1) ? ip : ip - pos - 1;        // last completed block's end
+      if (e < 0) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) o.v[j] = from_f<Tr>(MAX ? -INFINITY : 0.f);
+        for (int k = 0; k < g.kt; ++k) *reinterpret_cast<Vec<Tr, V>*>(S + k * SE) = o;
+        continue;
+      }
+      const int64_t jmin = (ip - g.kt + 2 > e - g.kt + 1) ? ip - g.kt + 2 : e - g.kt + 1;
+      {
+        const Vec<Tr, V> r = ring(e * g.dt + q);
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] = to_f(r.v[j]);
+        *reinterpret_cast<Vec<Tr, V>*>(S + fmod_pos(e, g.kt) * SE) = r;
+      }
+      for (int64_t jj = e - 1; jj >= jmin; --jj) {
+        const Vec<Tr, V> r = ring(jj * g.dt + q);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          acc[j] = MAX ? fmaxf(to_f(r.v[j]), acc[j]) : to_f(r.v[j]) + acc[j];
+          o.v[j] = from_f<Tr>(acc[j]);
+        }
+        *reinterpret_cast<Vec<Tr, V>*>(S + fmod_pos(jj, g.kt) * SE) = o;
+      }
+    }
+  }
+}
+
+// Step: reduce the new frame spatially (x == NULL: a padding frame), then the
+// temporal part (temporal_step).  Ring layout [slot][B][Ho][Wo][C] in Tr (input
+// dtype for MAX, fp32 for AVG).
+template <typename Tin, typename Tout, typename Tr, int V, bool MAX, int CH, bool VH>
+__global__ void __launch_bounds__(256, CH == 1 ? 4 : 2) k_step_pool(Geom g, StepArgs a) {
   const int CV = g.Cin / V;
   const int64_t total = g.B * g.HWo * CV;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  Tr* ring = reinterpret_cast<Tr*>(a.state);
-  const int64_t slot_elems = g.B * g.HWo * g.Cin;
+  Tr* st = reinterpret_cast<Tr*>(a.state);
+  const int64_t SE = g.B * g.HWo * g.Cin;
   const Tin* x = static_cast<const Tin*>(a.x);
   for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
     const int c0 = int(idx % CV) * V;
@@ -99,42 +313,89 @@ __global__ void __launch_bounds__(256) k_step_pool(Geom g, StepArgs a) {
     const int p = int(r % g.HWo);
     const int64_t b = r / g.HWo;
     const int ho = p / g.Wo, wo = p - (p / g.Wo) * g.Wo;
-    float s[V];
+    float s[V], win[V];
     if (x) {
-      spatial_reduce<Tin, V, MAX>(g, x + b * a.x_bstride, ho, wo, c0, s);
+      spatial_reduce<Tin, V, MAX, CH>(g, x + b * a.x_bstride, ho, wo, c0, s);
     } else {
 #pragma unroll
       for (int j = 0; j < V; ++j) s[j] = MAX ? -INFINITY : 0.f;
     }
+    temporal_step<Tr, V, MAX, VH, CH>(g, a, st, SE, r * g.Cin + c0, s, win);
+    if (a.emit)
+      store_out<Tout, V, MAX>(g, reinterpret_cast<Tout*>(a.y) + b * a.y_bstride + int64_t(p) * g.Cout + c0, win);
+  }
+}
+
+// Few output rows (e.g. the expanded global pool: one 1x1 row per stream) give
+// the one-thread-per-vector kernel too few threads to cover HBM latency, so
+// this variant gives each output row (b, pixel) a block of G x CV threads:
+// lane g reduces spatial taps g, g+G, ... and ring slots g, g+G, ..., and the G
+// partials are combined in g order through shared memory.  Same results as
+// k_step_pool up to the AVG summation order (MAX: bitwise).
+template <typename Tin, typename Tout, typename Tr, int V, bool MAX, bool VH>
+__global__ void __launch_bounds__(512) k_step_pool_split(Geom g, StepArgs a) {
+  extern __shared__ float sm_part[];                 // [2][G][CV][V]
+  const int CV = g.Cin / V, G = blockDim.y;
+  const int cv = threadIdx.x, gi = threadIdx.y;
+  float* sp = sm_part;
+  float* tp = sm_part + G * CV * V;
+  Tr* ring = reinterpret_cast<Tr*>(a.state);
+  const int64_t slot_elems = g.B * g.HWo * g.Cin;
+  const Tin* x = static_cast<const Tin*>(a.x);
+  const int c0 = cv * V;
+  for (int64_t r = blockIdx.x; r < g.B * g.HWo; r += gridDim.x) {
+    const int p = int(r % g.HWo);
+    const int64_t b = r / g.HWo;
+    const int ho = p / g.Wo, wo = p - (p / g.Wo) * g.Wo;
     const int64_t off = r * g.Cin + c0;
-    if (a.slot[0] >= 0) {
-      Vec<Tr, V> w;
+    float s[V], t[V];
+    if (x) {
+      spatial_reduce<Tin, V, MAX>(g, x + b * a.x_bstride, ho, wo, c0, s, gi, G);
+    } else {
 #pragma unroll
-      for (int j = 0; j < V; ++j) w.v[j] = from_f<Tr>(s[j]);
-      *reinterpret_cast<Vec<Tr, V>*>(ring + int64_t(a.slot[0]) * slot_elems + off) = w;
+      for (int j = 0; j < V; ++j) s[j] = MAX ? -INFINITY : 0.f;
     }
-    if (!a.emit) continue;
-    float acc[V];
 #pragma unroll
-    for (int j = 0; j < V; ++j) acc[j] = MAX ? -INFINITY : 0.f;
-    for (int k = 0; k + 1 < g.kt; ++k) {
-      const int64_t slot = fmod_pos(a.m - int64_t(g.kt - 1 - k) * g.dt, g.f);
-      const Vec<Tr, V> q = *reinterpret_cast<const Vec<Tr, V>*>(ring + slot * slot_elems + off);
-      float t[V];
+    for (int j = 0; j < V; ++j) t[j] = MAX ? -INFINITY : 0.f;
+    if (!VH && a.emit) ring_fold<Tr, V, MAX>(g, ring, slot_elems, off, a.m, t, gi, G);
 #pragma unroll
-      for (int j = 0; j < V; ++j) t[j] = to_f(q.v[j]);
-      combine<V, MAX>(acc, t);
+    for (int j = 0; j < V; ++j) {
+      sp[(gi * CV + cv) * V + j] = s[j];
+      tp[(gi * CV + cv) * V + j] = t[j];
     }
-    combine<V, MAX>(acc, s);
-    store_out<Tout, V, MAX>(g, reinterpret_cast<Tout*>(a.y) + b * a.y_bstride + int64_t(p) * g.Cout + c0, acc);
+    __syncthreads();
+    if (gi == 0) {
+      for (int q = 1; q < G; ++q) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          const float sv = sp[(q * CV + cv) * V + j], tv = tp[(q * CV + cv) * V + j];
+          s[j] = MAX ? fmaxf(s[j], sv) : s[j] + sv;
+          t[j] = MAX ? fmaxf(t[j], tv) : t[j] + tv;
+        }
+      }
+      if constexpr (VH) {
+        temporal_step<Tr, V, MAX, true, kChunk>(g, a, ring, slot_elems, off, s, t);
+      } else {
+        if (a.slot[0] >= 0) {
+          Vec<Tr, V> w;
+#pragma unroll
+          for (int j = 0; j < V; ++j) w.v[j] = from_f<Tr>(s[j]);
+          *reinterpret_cast<Vec<Tr, V>*>(ring + int64_t(a.slot[0]) * slot_elems + off) = w;
+        }
+        if (a.emit) combine<V, MAX>(t, s);
+      }
+      if (a.emit)
+        store_out<Tout, V, MAX>(g, reinterpret_cast<Tout*>(a.y) + b * a.y_bstride + int64_t(p) * g.Cout + c0, t);
+    }
+    __syncthreads();
   }
 }
 
 // Batch mode: y[b, t'] = fold over taps k of the spatial reduction of
 // frame t' s + k dil - p_t (padding outside [0, T): the identity).  Same
 // reduction order as the step kernel.  Reads no state.
-template <typename Tin, typename Tout, int V, bool MAX>
-__global__ void __launch_bounds__(256) k_forward_pool(Geom g, const Tin* __restrict__ x, int64_t T,
+template <typename Tin, typename Tout, int V, bool MAX, int CH>
+__global__ void __launch_bounds__(256, CH == 1 ? 4 : 2) k_forward_pool(Geom g, const Tin* __restrict__ x, int64_t T,
                                                        Tout* __restrict__ y, int64_t Tp) {
   const int CV = g.Cin / V;
   const int64_t total = g.B * Tp * g.HWo * CV;
@@ -154,7 +415,7 @@ __global__ void __launch_bounds__(256) k_forward_pool(Geom g, const Tin* __restr
       const int64_t t = tp * g.st + int64_t(k) * g.dt - g.pt;
       if (t < 0 || t >= T) continue;            // padding: the identity
       float s[V];
-      spatial_reduce<Tin, V, MAX>(g, x + (b * T + t) * g.frame_elems, ho, wo, c0, s);
+      spatial_reduce<Tin, V, MAX, CH>(g, x + (b * T + t) * g.frame_elems, ho, wo, c0, s);
       combine<V, MAX>(acc, s);
     }
     store_out<Tout, V, MAX>(g, y + ((b * Tp + tp) * g.HWo + p) * g.Cout + c0, acc);
@@ -175,6 +436,37 @@ int vec_width(const Geom& g) {
   return 1;
 }
 
+int num_sms() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+// Lanes per output vector of the split step kernel (1: the plain kernel).  The
+// plain kernel needs about 2 x 148 x 1024 threads to keep HBM busy.
+int split_lanes(const Geom& g) {
+  const int CV = g.Cin / vec_width(g);
+  const int64_t threads = g.B * g.HWo * CV;
+  const int64_t target = int64_t(num_sms()) * 2048;
+  if (threads >= target || CV > 256) return 1;
+  // the fewest lanes that reach an eighth of the target (measured: x3d64's 27.6K
+  // vectors run best at G = 2; more lanes add shared-memory reduction latency)
+  int G = int((target / 8 + threads - 1) / threads);
+  G = G < 2 ? 2 : (G > 8 ? 8 : G);
+  while (G > 1 && G * CV > 512) --G;
+  const int work = (g.kh * g.kw > g.kt - 1) ? g.kh * g.kw : g.kt - 1;
+  if (G > work) G = work;
+  return G < 2 ? 1 : G;
+}
+
+// Per-thread load depth of the plain kernels: with enough threads to fill the
+// GPU several times over, occupancy hides latency best (1 load in flight, 6
+// blocks / SM); few threads or long windows take kChunk loads in flight.
+bool deep_chunks(const Geom& g, int64_t threads) {
+  return threads < int64_t(num_sms()) * 2048 * 4 || g.kh * g.kw > 16;
+}
+
 int grid_for(int64_t total) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -184,17 +476,55 @@ int grid_for(int64_t total) {
   return int(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
 }
 
+template <typename Tin, typename Tout, typename Tr, int V, bool MAX, bool VH>
+cudaError_t step_split(const Geom& g, const StepArgs& a, int G, cudaStream_t s) {
+  const int CV = g.Cin / V;
+  const size_t smem = size_t(2) * G * CV * V * sizeof(float);
+  const int64_t rows = g.B * g.HWo;
+  const int per_sm = 2048 / (G * CV) > 0 ? 2048 / (G * CV) : 1;   // resident blocks per SM
+  const int64_t cap = int64_t(num_sms()) * per_sm;
+  const int grid = int(rows < cap ? rows : cap);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_step_pool_split<Tin, Tout, Tr, V, MAX, VH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+  k_step_pool_split<Tin, Tout, Tr, V, MAX, VH><<<grid, dim3(CV, G), smem, s>>>(g, a);
+  return cudaGetLastError();
+}
+
+template <typename Tin, typename Tout, typename Tr, int V, bool MAX>
+cudaError_t step_v(const Geom& g, const StepArgs& a, cudaStream_t s) {
+  if (g.pool_G > 1)
+    return g.pool_vh ? step_split<Tin, Tout, Tr, V, MAX, true>(g, a, g.pool_G, s)
+                     : step_split<Tin, Tout, Tr, V, MAX, false>(g, a, g.pool_G, s);
+  const int64_t total = g.B * g.HWo * (g.Cin / V);
+  const int grid = grid_for(total);
+  if (g.pool_vh) k_step_pool<Tin, Tout, Tr, V, MAX, kChunk, true><<<grid, 256, 0, s>>>(g, a);
+  else if (deep_chunks(g, total)) k_step_pool<Tin, Tout, Tr, V, MAX, kChunk, false><<<grid, 256, 0, s>>>(g, a);
+  else k_step_pool<Tin, Tout, Tr, V, MAX, 1, false><<<grid, 256, 0, s>>>(g, a);
+  return cudaGetLastError();
+}
+
 template <typename Tin, typename Tout, bool MAX>
 cudaError_t step_t(const Geom& g, const StepArgs& a, cudaStream_t s) {
   using Tr = typename std::conditional<MAX, Tin, float>::type;
+  switch (vec_width(g)) {
+    case 8: return step_v<Tin, Tout, Tr, 8, MAX>(g, a, s);
+    case 4: return step_v<Tin, Tout, Tr, 4, MAX>(g, a, s);
+    case 2: return step_v<Tin, Tout, Tr, 2, MAX>(g, a, s);
+    default: return step_v<Tin, Tout, Tr, 1, MAX>(g, a, s);
+  }
+}
+
+template <typename Tr, bool MAX>
+cudaError_t rebuild_t(const Geom& g, void* state, int64_t m_next, cudaStream_t s) {
   const int V = vec_width(g);
-  const int64_t total = g.B * g.HWo * (g.Cin / V);
-  const int grid = grid_for(total);
+  const int grid = grid_for(g.B * g.HWo * (g.Cin / V));
+  Tr* st = static_cast<Tr*>(state);
   switch (V) {
-    case 8: k_step_pool<Tin, Tout, Tr, 8, MAX><<<grid, 256, 0, s>>>(g, a); break;
-    case 4: k_step_pool<Tin, Tout, Tr, 4, MAX><<<grid, 256, 0, s>>>(g, a); break;
-    case 2: k_step_pool<Tin, Tout, Tr, 2, MAX><<<grid, 256, 0, s>>>(g, a); break;
-    default: k_step_pool<Tin, Tout, Tr, 1, MAX><<<grid, 256, 0, s>>>(g, a); break;
+    case 8: k_pool_rebuild<Tr, 8, MAX><<<grid, 256, 0, s>>>(g, st, m_next); break;
+    case 4: k_pool_rebuild<Tr, 4, MAX><<<grid, 256, 0, s>>>(g, st, m_next); break;
+    case 2: k_pool_rebuild<Tr, 2, MAX><<<grid, 256, 0, s>>>(g, st, m_next); break;
+    default: k_pool_rebuild<Tr, 1, MAX><<<grid, 256, 0, s>>>(g, st, m_next); break;
   }
   return cudaGetLastError();
 }
@@ -206,11 +536,20 @@ cudaError_t forward_t(const Geom& g, const void* x, int64_t T, void* y, int64_t 
   const int grid = grid_for(total);
   const Tin* xp = static_cast<const Tin*>(x);
   Tout* yp = static_cast<Tout*>(y);
-  switch (V) {
-    case 8: k_forward_pool<Tin, Tout, 8, MAX><<<grid, 256, 0, s>>>(g, xp, T, yp, Tp); break;
-    case 4: k_forward_pool<Tin, Tout, 4, MAX><<<grid, 256, 0, s>>>(g, xp, T, yp, Tp); break;
-    case 2: k_forward_pool<Tin, Tout, 2, MAX><<<grid, 256, 0, s>>>(g, xp, T, yp, Tp); break;
-    default: k_forward_pool<Tin, Tout, 1, MAX><<<grid, 256, 0, s>>>(g, xp, T, yp, Tp); break;
+  if (deep_chunks(g, total)) {
+    switch (V) {
+      case 8: k_forward_pool<Tin, Tout, 8, MAX, kChunk><<<grid, 256, 0, s>>>(g, xp, T, yp, Tp); break;
+      case 4: k_forward_pool<Tin, Tout, 4, MAX, kChunk><<<grid, 256, 0, s>>>(g, xp, T, yp, Tp); break;
+      case 2: k_forward_pool<Tin, Tout, 2, MAX, kChunk><<<grid, 256, 0, s>>>(g, xp, T, yp, Tp); break;
+      default: k_forward_pool<Tin, Tout, 1, MAX, kChunk><<<grid, 256, 0, s>>>(g, xp, T, yp, Tp); break;
+    }
+  } else {
+    switch (V) {
+      case 8: k_forward_pool<Tin, Tout, 8, MAX, 1><<<grid, 256, 0, s>>>(g, xp, T, yp, Tp); break;
+      case 4: k_forward_pool<Tin, Tout, 4, MAX, 1><<<grid, 256, 0, s>>>(g, xp, T, yp, Tp); break;
+      case 2: k_forward_pool<Tin, Tout, 2, MAX, 1><<<grid, 256, 0, s>>>(g, xp, T, yp, Tp); break;
+      default: k_forward_pool<Tin, Tout, 1, MAX, 1><<<grid, 256, 0, s>>>(g, xp, T, yp, Tp); break;
+    }
   }
   return cudaGetLastError();
 }
@@ -243,6 +582,18 @@ cudaError_t launch_forward_pool(const Geom& g, const void* x, int64_t T, void* y
   return g.op == OP_MAX_POOL ? forward_dispatch<true>(g, x, T, y, Tp, s) : forward_dispatch<false>(g, x, T, y, Tp, s);
 }
 
+cudaError_t launch_pool_rebuild(const Geom& g, void* state, int64_t m_next, cudaStream_t s) {
+  if (!g.pool_vh) return cudaSuccess;
+  if (g.op == OP_AVG_POOL) return rebuild_t<float, false>(g, state, m_next, s);
+  return g.in_dtype == BF16 ? rebuild_t<__nv_bfloat16, true>(g, state, m_next, s)
+                            : rebuild_t<float, true>(g, state, m_next, s);
+}
+
+int pool_block_decomposition(const Geom& g) {
+  if (const char* e = getenv("CO_POOL_VH")) return atoi(e) ? 1 : 0;   // experiment / test knob
+  return g.kt >= kVhMinKt ? 1 : 0;
+}
+
 cudaError_t launch_fill_pad(const Geom& g, void* p, int64_t n_elems, cudaStream_t s) {
   if (n_elems <= 0) return cudaSuccess;
   if (g.op != OP_MAX_POOL) return cudaMemsetAsync(p, 0, size_t(n_elems) * pool_ring_esz(g), s);
@@ -252,13 +603,25 @@ cudaError_t launch_fill_pad(const Geom& g, void* p, int64_t n_elems, cudaStream_
   return cudaGetLastError();
 }
 
-const char* pool_kernel_name(const Geom& g) {
-  static const char* names[2][4] = {{"k_step_pool<avg,V1>", "k_step_pool<avg,V2>", "k_step_pool<avg,V4>",
-                                     "k_step_pool<avg,V8>"},
-                                    {"k_step_pool<max,V1>", "k_step_pool<max,V2>", "k_step_pool<max,V4>",
-                                     "k_step_pool<max,V8>"}};
-  const int v = vec_width(g);
-  return names[g.op == OP_MAX_POOL][v == 8 ? 3 : v == 4 ? 2 : v == 2 ? 1 : 0];
+int pool_split_lanes(const Geom& g) {
+  if (const char* e = getenv("CO_POOL_G")) {     // experiment / test knob
+    const int CV = g.Cin / vec_width(g);
+    int G = atoi(e);
+    G = G < 1 ? 1 : (G > 32 ? 32 : G);
+    while (G > 1 && G * CV > 512) --G;
+    return G;
+  }
+  return split_lanes(g);
+}
+
+std::string pool_kernel_name(const Geom& g) {
+  char out[64];
+  const int G = g.pool_G;
+  const char* kind = g.op == OP_MAX_POOL ? "max" : "avg";
+  const char* vh = g.pool_vh ? ",vh" : "";
+  if (G > 1) snprintf(out, 64, "k_step_pool_split<%s,V%d,G%d%s>", kind, vec_width(g), G, vh);
+  else snprintf(out, 64, "k_step_pool<%s,V%d%s>", kind, vec_width(g), vh);
+  return out;
 }
 
 }  // namespace co

@@ -13,9 +13,10 @@ Workloads (seeded N(0,1) bf16 frames; no BASELINE.json config covers pooling):
   max3   -- an I3D-style max pool (3, 3, 3), stride (1, 2, 2), padding
             (0, 1, 1) on the C2 activation shape (56x56x64, 256 streams).
 
-Algorithmic bytes per stream-step of the pooled-ring design (k_pool.cu):
-x (H W C, bf16) + y (H' W' C) + ring write (H' W' C x ring esz) + (kt-1) ring
-reads; the ring element is the input dtype for MAX and fp32 for AVG.
+Algorithmic bytes per stream-step (alg_bytes; k_pool.cu): x (H W C, bf16) +
+y (H' W' C) + the reduced-frame slots the temporal scheme touches (H' W' C x
+ring esz each; input dtype for MAX, fp32 for AVG): kt for the direct fold, about
+6 for the block decomposition used when kt >= 6.
 
 usage: python scripts/bench_pool.py [--workload x3d64|max3|all] [--steps K] [--warmup W]
 """
@@ -39,12 +40,18 @@ WORKLOADS = {
 }
 
 
-def alg_bytes(w, Ho, Wo):
+def alg_bytes(w, Ho, Wo, vh):
+    """Bytes per stream-step the step kernel must move (k_pool.cu): the frame,
+    the output, and reduced-frame slots -- direct fold: 1 ring write + kt-1 ring
+    reads; block decomposition (vh): 1 ring write, P read + write, S read, and
+    the suffix pass's 2kt-1 slot accesses once per kt steps (amortized)."""
     esz, resz = 2, (4 if w["kind"] == "avg" else 2)
+    kt = w["kernel"][0]
     x = w["H"] * w["W"] * w["C"] * esz
     y = Ho * Wo * w["C"] * esz
-    ring = Ho * Wo * w["C"] * resz
-    return x + y + ring + (w["kernel"][0] - 1) * ring
+    slot = Ho * Wo * w["C"] * resz
+    slots = (1 + (kt - 1) / kt + 1 + (kt - 1) / kt + (2 * kt - 1) / kt) if vh else kt
+    return x + y + slots * slot
 
 
 def run(name, steps, warmup):
@@ -60,19 +67,22 @@ def run(name, steps, warmup):
     fbytes = B * C * H * W * 2
     G = min(max(4, math.ceil(4 * l2 / fbytes)), 32)
     g = torch.Generator(device="cuda").manual_seed(1234)
-    pool = [co.channels_last(torch.randn((B, C, H, W), generator=g, device="cuda").to(torch.bfloat16))
-            for _ in range(G)]
-    y = co._empty_cl((B, C, Ho, Wo), torch.bfloat16, "cuda")
+    # G distinct frames as one device clip (B, C, G, H, W); each co_forward_steps
+    # call folds co_forward_step over its G columns in C (one launch per step,
+    # no Python per step -- the per-call Python/ctypes cost exceeds the x3d64 kernel)
+    clip = co.channels_last(torch.randn((B, C, G, H, W), generator=g, device="cuda").to(torch.bfloat16))
     stream = torch.cuda.current_stream()
-    for n in range(max(warmup, 3) + p.delay):
-        p.forward_step(pool[n % G], out=y)
+    warm = co.channels_last(clip[:, :, :1].repeat(1, 1, max(warmup, 3) + p.delay, 1, 1))
+    p.forward_steps(warm)
     torch.cuda.synchronize()
+    steps = max(G, (steps + G - 1) // G * G)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(torch.cuda.current_device())
     with sampler:
         e0.record(stream)
-        for k in range(steps):
-            assert p.forward_step(pool[k % G], out=y) is not None
+        for k in range(steps // G):
+            ys, mask = p.forward_steps(clip)
+            assert ys.shape[2] == G
         e1.record(stream)
         t_end = time.time() + 60
         while not e1.query() and time.time() < t_end:
@@ -81,7 +91,8 @@ def run(name, steps, warmup):
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     hbm, _, src = measured_peaks()
-    ab = alg_bytes(w, Ho, Wo) * B
+    vh = ",vh" in p.kernel_name
+    ab = alg_bytes(w, Ho, Wo, vh) * B
     ach = ab / (ms / 1e3) / 1e9
     ring_mb = (p.receptive_field + 1) * B * Ho * Wo * C * (4 if w["kind"] == "avg" else 2) / 1e6
     out = {
