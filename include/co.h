@@ -68,7 +68,8 @@ typedef enum {
   CO_KERNEL_DIRECT = 1,     /* generic CUDA-core kernel: any groups/dilation/stride, fp32 or bf16 */
   CO_KERNEL_DENSE_TC = 2,   /* tcgen05/TMEM implicit GEMM with fused state epilogue (bf16, dense) */
   CO_KERNEL_DEPTHWISE = 3,  /* CUDA-core depthwise stencil (groups == Cin == Cout, bf16) */
-  CO_KERNEL_POOL = 4        /* CUDA-core window max / mean over the RAW ring (pooling handles only) */
+  CO_KERNEL_POOL = 4,       /* CUDA-core window max / mean over the RAW ring (pooling handles only) */
+  CO_KERNEL_COPY = 5        /* ring copies only (Delay handles) */
 } co_kernel;
 
 /* Per-stream state layout (BASELINE.json north_star "Per-stream state layout";
@@ -95,7 +96,14 @@ typedef enum { CO_STATE_PSUM = 0, CO_STATE_RAW = 1 } co_state_layout;
  * padded frames 0.  Clock, readiness, delay and the call modes are those of a
  * convolution with the same kernel / stride / padding / dilation
  * (Definition 1). */
-typedef enum { CO_OP_CONV = 0, CO_OP_MAX_POOL = 1, CO_OP_AVG_POOL = 2 } co_op;
+typedef enum { CO_OP_CONV = 0, CO_OP_MAX_POOL = 1, CO_OP_AVG_POOL = 2, CO_OP_DELAY = 3 } co_op;
+/* CO_OP_DELAY (co.Delay): kernel[0] = d + 1 (so f = d + 1,
+ * delay d), every other kernel / stride / dilation entry 1, padding 0,
+ * in_channels == out_channels, out_dtype == in_dtype, no weights or bias.  A
+ * step emits Empty while n < d, then the input of d ticks ago (a copy out of a
+ * ring of d + 1 frames, CO_KERNEL_COPY); batch mode (co_forward) is the
+ * identity on the clip (T' = T).  Canonical state: the last d frames,
+ * (d, B, S1, S2, C) in in_dtype. */
 
 typedef void* co_stream;                 /* cudaStream_t */
 typedef struct co_conv co_conv;          /* opaque: packed weights, fp32 state ring, host clock */
@@ -233,6 +241,40 @@ int co_stack_steps_host(co_stack* st, const void* x_host, int64_t T, void* y_hos
 /* Accumulated delay d_NN (Principle 6 in the worked-example reading, A3). */
 int co_stack_delay(const co_stack* st, int64_t* d_nn);
 int co_stack_clean(co_stack* st, co_stream stream);
+
+/* ---- composition: Residual ------------------------------- */
+
+/* Residual(body) with Sum ("Residual connections", Listing 3
+ * P:482-504 co.Residual / residual_shrink; Principle 7 P:280-288; SPEC.md:
+ * 452-458).  `body` is a sequence of layer handles (owned by the caller, not
+ * shared with another stack or residual, alive until co_residual_destroy) run
+ * as a stack; it must keep the frame rate (accumulated temporal stride 1), the
+ * channel count, spatial shape and dtype of its input (body[0] in_dtype ==
+ * body[n-1] out_dtype).  Alignment of the identity branch ("centered",
+ * P:312-316):
+ *  shrink = 0: equal padding, 2 p_acc = f_acc - 1; the identity branch is
+ *              delayed by the body's delay d (Fig. 4); batch y = x + body(x);
+ *  shrink = 1: f_acc odd (any padding with p_acc <= (f_acc-1)/2); the identity
+ *              branch is delayed by (f_acc-1)/2 and, in batch mode, cropped by
+ *              (f_acc-1)/2 at each end.
+ * The composite's delay is the body's (the larger branch delay, Principle 7);
+ * it is Ready exactly when the body is.  `activation` (co_activation) is
+ * applied after the add (the ResNet / X3D block form).  The identity branch's
+ * frames live in a ring of d_skip + 1 frames in the input dtype.  Errors:
+ * CO_ERR_ARG, CO_ERR_SHAPE (shape / timing contract), CO_ERR_OOM. */
+typedef struct co_residual co_residual;
+int co_residual_create(co_conv* const* body, int n_layers, int shrink, int activation, co_residual** out);
+int co_residual_destroy(co_residual* r);              /* frees the composite, not the body layers */
+/* One tick (same contract as co_forward_step): x (B, S1, S2, C) channels-last,
+ * y (B, S1, S2, C) in the body's out_dtype; *ready = 1 when emitted. */
+int co_residual_step(co_residual* r, const void* x, void* y, int update_state, int* ready, co_stream stream);
+/* Batch mode: x (B, T, S1, S2, C) -> y (B, T', S1, S2, C), T' = the body's output
+ * length; neither reads nor writes state.  Temporaries are stream-ordered
+ * allocations freed before return (stream order). */
+int co_residual_forward(co_residual* r, const void* x, int64_t T, void* y, int64_t* T_out, co_stream stream);
+int co_residual_clean(co_residual* r, co_stream stream);   /* body layers + identity ring + clock */
+/* Composite delay (= the body's d_nn) and the identity branch's delay. */
+int co_residual_delay(const co_residual* r, int64_t* delay, int64_t* skip_delay);
 
 /* ---- misc ------------------------------------------------------------------ */
 const char* co_last_error(void);

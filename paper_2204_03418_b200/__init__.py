@@ -23,7 +23,7 @@ import torch
 from . import _abi
 from ._abi import CoConvDesc, CoInfo, check, lib
 
-__all__ = ["Conv", "Pool", "Stack", "channels_last", "is_channels_last", "load"]
+__all__ = ["Conv", "Delay", "Pool", "Residual", "Stack", "channels_last", "is_channels_last", "load"]
 
 _DT = {torch.float32: _abi.CO_F32, torch.bfloat16: _abi.CO_BF16}
 
@@ -286,6 +286,105 @@ class Pool(Conv):
                          n_streams=n_streams, dtype=dtype, out_dtype=out_dtype, activation=activation,
                          kernel="auto", state_layout="raw", device=device, op=kind)
         self.kind = kind
+
+
+class Delay(Conv):
+    """``co.Delay(d)`` over ``n_streams``
+    lockstep streams: Empty for the first d steps, then the input of d steps
+    ago; batch mode is the identity.  A handle of the C ABI with ``op`` =
+    DELAY (a ring of d + 1 frames, copies only)."""
+
+    def __init__(self, delay: int, channels: int, *, spatial_rank: int = 2, in_spatial: Sequence[int] = (1, 1),
+                 n_streams: int = 1, dtype: torch.dtype = torch.bfloat16, device="cuda"):
+        super().__init__(channels, channels, (delay + 1,) + (1,) * spatial_rank, weight=None,
+                         spatial_rank=spatial_rank, in_spatial=in_spatial, n_streams=n_streams, dtype=dtype,
+                         out_dtype=dtype, kernel="auto", state_layout="raw", device=device, op="delay")
+
+    def _ring_dtype(self):
+        return self.dtype
+
+    def forward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        """Batch mode: the identity on the clip (alignment is structural)."""
+        self._check_in(x, clip=True)
+        y = _empty_cl(tuple(x.shape), self.dtype, self.device)
+        Tp = C.c_int64()
+        check(lib().co_forward(self._h, C.c_void_p(x.data_ptr()), x.shape[2], C.c_void_p(y.data_ptr()),
+                               C.byref(Tp), _stream(stream)))
+        return y
+
+
+class Residual:
+    """``co.Residual(body)`` with Sum (Listing 3; SPEC.md:
+    452-458) over the body layers' ``n_streams`` streams: the identity branch
+    is delayed to the body's output (``shrink=False``: equal padding, delay =
+    the body's; ``shrink=True``: centered, delay (f-1)/2, batch-mode crop), the
+    composite is Ready when the body is (Principle 7), and
+    ``activation`` ("relu") follows the add.  The body layers are driven by the
+    composite: do not step them directly while it is alive."""
+
+    def __init__(self, body: Sequence[Conv], shrink: bool = False, activation: Optional[str] = None):
+        self.body = list(body)
+        self.shrink = shrink
+        arr = (C.c_void_p * len(self.body))(*[c._h.value for c in self.body])
+        h = C.c_void_p()
+        act = {None: _abi.CO_ACT_NONE, "none": _abi.CO_ACT_NONE, "relu": _abi.CO_ACT_RELU}[activation]
+        with torch.cuda.device(self.body[0].device):
+            check(lib().co_residual_create(arr, len(self.body), int(shrink), act, C.byref(h)))
+        self._h = h
+        first, last = self.body[0], self.body[-1]
+        self.n_streams, self.channels = first.n_streams, first.in_channels
+        self.in_spatial, self.dtype, self.out_dtype, self.device = first.in_spatial, first.dtype, last.out_dtype, first.device
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().co_residual_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def delay(self) -> int:
+        d, _ = self.delays()
+        return d
+
+    def delays(self):
+        """(composite delay = the body's, identity-branch delay)."""
+        d, k = C.c_int64(), C.c_int64()
+        check(lib().co_residual_delay(self._h, C.byref(d), C.byref(k)))
+        return d.value, k.value
+
+    def forward_step(self, x: Optional[torch.Tensor], update_state: bool = True, out: Optional[torch.Tensor] = None,
+                     stream=None) -> Optional[torch.Tensor]:
+        if x is not None:
+            self.body[0]._check_in(x, clip=False)
+        y = out if out is not None else _empty_cl((self.n_streams, self.channels) + self.in_spatial, self.out_dtype,
+                                                  self.device)
+        r = C.c_int()
+        check(lib().co_residual_step(self._h, C.c_void_p(x.data_ptr()) if x is not None else None,
+                                     C.c_void_p(y.data_ptr()), int(update_state), C.byref(r), _stream(stream)))
+        return y if r.value else None
+
+    def forward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        """Batch mode: body(x) + x (cropped by (f-1)/2 at each end when shrink)."""
+        self.body[0]._check_in(x, clip=True)
+        T = x.shape[2]
+        Tc = T
+        for c in self.body:
+            t = C.c_int64()
+            check(lib().co_forward_out_len(c._h, Tc, C.byref(t)))
+            Tc = t.value
+        if Tc < 1:
+            raise ValueError(f"clip too short: T'={Tc}")
+        y = _empty_cl((self.n_streams, self.channels, Tc) + self.in_spatial, self.out_dtype, self.device)
+        Tp = C.c_int64()
+        check(lib().co_residual_forward(self._h, C.c_void_p(x.data_ptr()), T, C.c_void_p(y.data_ptr()), C.byref(Tp),
+                                        _stream(stream)))
+        return y
+
+    def clean_state(self, stream=None):
+        check(lib().co_residual_clean(self._h, _stream(stream)))
 
 
 class Stack:

@@ -19,11 +19,11 @@ CO_F32, CO_BF16 = 0, 1
 CO_ACT_NONE, CO_ACT_RELU = 0, 1
 CO_STATE_PSUM, CO_STATE_RAW = 0, 1
 STATE_LAYOUTS = {"psum": CO_STATE_PSUM, "raw": CO_STATE_RAW}
-CO_KERNEL_AUTO, CO_KERNEL_DIRECT, CO_KERNEL_DENSE_TC, CO_KERNEL_DEPTHWISE, CO_KERNEL_POOL = 0, 1, 2, 3, 4
+CO_KERNEL_AUTO, CO_KERNEL_DIRECT, CO_KERNEL_DENSE_TC, CO_KERNEL_DEPTHWISE, CO_KERNEL_POOL, CO_KERNEL_COPY = range(6)
 KERNELS = {"auto": CO_KERNEL_AUTO, "direct": CO_KERNEL_DIRECT, "dense_tc": CO_KERNEL_DENSE_TC,
-           "depthwise": CO_KERNEL_DEPTHWISE, "pool": CO_KERNEL_POOL}
-CO_OP_CONV, CO_OP_MAX_POOL, CO_OP_AVG_POOL = 0, 1, 2
-OPS = {"conv": CO_OP_CONV, "max": CO_OP_MAX_POOL, "avg": CO_OP_AVG_POOL}
+           "depthwise": CO_KERNEL_DEPTHWISE, "pool": CO_KERNEL_POOL, "copy": CO_KERNEL_COPY}
+CO_OP_CONV, CO_OP_MAX_POOL, CO_OP_AVG_POOL, CO_OP_DELAY = 0, 1, 2, 3
+OPS = {"conv": CO_OP_CONV, "max": CO_OP_MAX_POOL, "avg": CO_OP_AVG_POOL, "delay": CO_OP_DELAY}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 
 # every entry point include/co.h declares (checked by tests/test_abi_load.py)
@@ -31,7 +31,8 @@ EXPORTS = ["co_conv_create", "co_conv_destroy", "co_conv_info", "co_delay", "co_
            "co_forward_step", "co_forward_step_host", "co_forward_steps_host", "co_forward_steps", "co_steps_ready_count",
            "co_forward", "co_forward_out_len", "co_state_bytes", "co_state_get", "co_state_set",
            "co_state_clean", "co_stack_create", "co_stack_destroy", "co_stack_step", "co_stack_step_host", "co_stack_steps_host", "co_stack_delay",
-           "co_stack_clean", "co_last_error", "co_abi_version"]
+           "co_stack_clean", "co_residual_create", "co_residual_destroy", "co_residual_step", "co_residual_forward",
+           "co_residual_clean", "co_residual_delay", "co_last_error", "co_abi_version"]
 
 
 class CoConvDesc(C.Structure):
@@ -92,6 +93,12 @@ def lib():
             L.co_stack_step_host.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_int), vp]
             L.co_stack_delay.argtypes = [vp, i64p]
             L.co_stack_clean.argtypes = [vp, vp]
+            L.co_residual_create.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+            L.co_residual_destroy.argtypes = [vp]
+            L.co_residual_step.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_int), vp]
+            L.co_residual_forward.argtypes = [vp, vp, C.c_int64, vp, i64p, vp]
+            L.co_residual_clean.argtypes = [vp, vp]
+            L.co_residual_delay.argtypes = [vp, i64p, i64p]
             L.co_last_error.restype = C.c_char_p
             L.co_abi_version.restype = C.c_int
             _lib = L

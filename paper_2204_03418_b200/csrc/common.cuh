@@ -12,7 +12,7 @@ namespace co {
 constexpr int kMaxKt = 32;   // == CO_MAX_KT
 
 enum Dtype : int { F32 = 0, BF16 = 1 };
-enum Op : int { OP_CONV = 0, OP_MAX_POOL = 1, OP_AVG_POOL = 2 };   // == co_op
+enum Op : int { OP_CONV = 0, OP_MAX_POOL = 1, OP_AVG_POOL = 2, OP_DELAY = 3 };   // == co_op
 
 // Normalised layer geometry (absent spatial axes are extent 1, kernel 1).
 struct Geom {
@@ -122,6 +122,10 @@ std::string pool_kernel_name(const Geom& g);
 int pool_split_lanes(const Geom& g);   // choice of pool_G (env CO_POOL_G overrides)
 int pool_block_decomposition(const Geom& g);   // choice of pool_vh (env CO_POOL_VH overrides)
 cudaError_t launch_pool_rebuild(const Geom& g, void* state, int64_t m_next, cudaStream_t s);
+
+// Residual composite merge (k_compose.cu): y[r, :n] <- act(y[r, :n] + x[r, :n]) over rows.
+cudaError_t launch_residual_add(int y_dtype, void* y, int64_t y_rstride, int x_dtype, const void* x,
+                                int64_t x_rstride, int64_t rows, int64_t n, int act, cudaStream_t s);
 
 // ---- launchers implemented in the .cu files (host side) --------------------
 cudaError_t launch_step_direct(const Geom& g, const StepArgs& a, const float* w_direct, const float* bias,

@@ -153,7 +153,8 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
   if (d->w_dtype != d->in_dtype) return fail(CO_ERR_ARG, "w_dtype must equal in_dtype");
   if (d->activation != CO_ACT_NONE && d->activation != CO_ACT_RELU) return fail(CO_ERR_ARG, "bad activation");
   if (d->state_layout != CO_STATE_PSUM && d->state_layout != CO_STATE_RAW) return fail(CO_ERR_ARG, "bad state_layout");
-  if (d->op != CO_OP_CONV && d->op != CO_OP_MAX_POOL && d->op != CO_OP_AVG_POOL) return fail(CO_ERR_ARG, "bad op");
+  if (d->op != CO_OP_CONV && d->op != CO_OP_MAX_POOL && d->op != CO_OP_AVG_POOL && d->op != CO_OP_DELAY)
+    return fail(CO_ERR_ARG, "bad op");
   const bool pool = d->op != CO_OP_CONV;
   if (pool && d->in_channels != d->out_channels)
     return fail(CO_ERR_ARG, "pooling: in_channels (%d) != out_channels (%d)", d->in_channels, d->out_channels);
@@ -181,7 +182,13 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
   g.splane = g.B * g.HWo;
   g.slot_elems = int64_t(g.Cq) * 4 * g.splane;
   g.op = d->op;
-  g.raw = pool || d->state_layout == CO_STATE_RAW;   // pooling always keeps the frame ring
+  g.raw = pool || d->state_layout == CO_STATE_RAW;   // pooling / delay always keep a frame ring
+  if (g.op == CO_OP_DELAY) {
+    if (g.kh != 1 || g.kw != 1 || g.sh != 1 || g.sw != 1 || g.ph || g.pw || g.dh != 1 || g.dw != 1 || g.pt ||
+        g.st != 1 || g.dt != 1)
+      return fail(CO_ERR_ARG, "delay: kernel (d+1, 1, 1), stride 1, dilation 1, padding 0");
+    if (d->out_dtype != d->in_dtype) return fail(CO_ERR_ARG, "delay: out_dtype must equal in_dtype");
+  }
   g.frame_elems = int64_t(g.H) * g.W * g.Cin;
   return CO_OK;
 }
@@ -236,16 +243,20 @@ static bool depthwise_fits(const Geom& g) { return co::depthwise_supported(g); }
 static int create_pool(const co_conv_desc* desc, const Geom& g, const void* weights, const float* bias,
                        co_conv** out) {
   if (weights || bias) return fail(CO_ERR_ARG, "pooling takes no weights or bias");
-  if (desc->kernel_choice != CO_KERNEL_AUTO && desc->kernel_choice != CO_KERNEL_POOL)
-    return fail(CO_ERR_UNSUPPORTED, "pooling runs only on CO_KERNEL_POOL");
+  const int kern = g.op == CO_OP_DELAY ? CO_KERNEL_COPY : CO_KERNEL_POOL;
+  if (desc->kernel_choice != CO_KERNEL_AUTO && desc->kernel_choice != kern)
+    return fail(CO_ERR_UNSUPPORTED, g.op == CO_OP_DELAY ? "delay runs only on CO_KERNEL_COPY"
+                                                        : "pooling runs only on CO_KERNEL_POOL");
   co_conv* h = new (std::nothrow) co_conv();
   if (!h) return fail(CO_ERR_OOM, "host allocation");
   h->desc = *desc;
   h->g = g;
-  h->g.pool_G = co::pool_split_lanes(g);
-  h->g.pool_vh = co::pool_block_decomposition(g);
-  h->kernel_used = CO_KERNEL_POOL;
-  h->kname = co::pool_kernel_name(h->g);
+  if (g.op != CO_OP_DELAY) {
+    h->g.pool_G = co::pool_split_lanes(g);
+    h->g.pool_vh = co::pool_block_decomposition(g);
+  }
+  h->kernel_used = kern;
+  h->kname = g.op == CO_OP_DELAY ? std::string("ring_copy") : co::pool_kernel_name(h->g);
   const size_t sb = state_alloc_bytes(h->g);
   cudaError_t e;
   if ((e = cudaMalloc(&h->state, sb)) != cudaSuccess) {
@@ -460,8 +471,32 @@ static int step_pool(co_conv* h, int64_t& n, float* state, const void* x, int64_
   return CO_OK;
 }
 
+// Delay tick (co.Delay): store the frame in ring slot n mod f
+// (the scratch slot f when the state must not change), and once n >= d copy
+// the frame of d ticks ago out.  Copies only: no arithmetic exists to fuse.
+static int step_delay(co_conv* h, int64_t& n, float* state, const void* x, int64_t x_bstride, void* y,
+                      int64_t y_bstride, int update_state, int* ready, cudaStream_t s) {
+  const Geom& g = h->g;
+  const int r = n >= g.delay;
+  const size_t es = dsize(g.in_dtype), fb = size_t(g.frame_elems) * es;
+  char* ring = reinterpret_cast<char*>(state);
+  const int cur = update_state ? int(floor_mod(n, g.f)) : g.f;
+  char* slot = ring + size_t(cur) * g.B * fb;
+  if (x) CO_CUDA(cudaMemcpy2DAsync(slot, fb, x, size_t(x_bstride) * es, fb, g.B, cudaMemcpyDeviceToDevice, s));
+  else CO_CUDA(cudaMemsetAsync(slot, 0, g.B * fb, s));
+  if (r) {
+    const int src = g.delay == 0 ? cur : int(floor_mod(n - g.delay, g.f));
+    CO_CUDA(cudaMemcpy2DAsync(y, size_t(y_bstride) * es, ring + size_t(src) * g.B * fb, fb, fb, g.B,
+                              cudaMemcpyDeviceToDevice, s));
+  }
+  if (update_state) ++n;
+  if (ready) *ready = r;
+  return CO_OK;
+}
+
 static int step_impl(co_conv* h, int64_t& n, float* state, const void* x, int64_t x_bstride, void* y,
                      int64_t y_bstride, int update_state, int* ready, cudaStream_t s) {
+  if (h->g.op == CO_OP_DELAY) return step_delay(h, n, state, x, x_bstride, y, y_bstride, update_state, ready, s);
   if (h->g.op != CO_OP_CONV) return step_pool(h, n, state, x, x_bstride, y, y_bstride, update_state, ready, s);
   if (h->g.raw) return step_raw(h, n, state, x, x_bstride, y, y_bstride, update_state, ready, s);
   StepArgs a;
@@ -613,7 +648,7 @@ extern "C" int co_forward_steps(co_conv* h, const void* x, int64_t T, void* y, u
 extern "C" int co_forward_out_len(const co_conv* h, int64_t T, int64_t* T_out) {
   if (!h || !T_out) return fail(CO_ERR_ARG, "null argument");
   const Geom& g = h->g;
-  *T_out = floor_div(T + 2 * g.pt - g.f, g.st) + 1;
+  *T_out = g.op == CO_OP_DELAY ? T : floor_div(T + 2 * g.pt - g.f, g.st) + 1;   // batch Delay: identity
   return CO_OK;
 }
 
@@ -622,7 +657,10 @@ extern "C" int co_forward(co_conv* h, const void* x, int64_t T, void* y, int64_t
   int64_t Tp = 0;
   co_forward_out_len(h, T, &Tp);
   if (Tp < 1) return fail(CO_ERR_LENGTH, "T' = %lld < 1 (T = %lld too short, S:63-65)", (long long)Tp, (long long)T);
-  cudaError_t e = h->kernel_used == CO_KERNEL_POOL
+  cudaError_t e = h->kernel_used == CO_KERNEL_COPY
+                      ? cudaMemcpyAsync(y, x, size_t(h->g.B) * T * h->g.frame_elems * dsize(h->g.in_dtype),
+                                        cudaMemcpyDeviceToDevice, (cudaStream_t)stream)
+                  : h->kernel_used == CO_KERNEL_POOL
                       ? co::launch_forward_pool(h->g, x, T, y, Tp, (cudaStream_t)stream)
                       : co::launch_forward_direct(h->g, x, T, y, Tp, h->w_direct, h->bias, (cudaStream_t)stream);
   if (e != cudaSuccess) return fail(CO_ERR_CUDA, "forward kernel: %s", cudaGetErrorString(e));
@@ -808,5 +846,160 @@ extern "C" int co_stack_clean(co_stack* st, co_stream stream) {
   if (!st) return fail(CO_ERR_ARG, "null stack");
   for (co_conv* h : st->layers)
     if (int rc = co_state_clean(h, stream)) return rc;
+  return CO_OK;
+}
+
+// ----------------------------------------------------------------- residual
+// Residual(body) with Sum (Listing 3; SPEC
+// S:452-458).  The body runs as a co_stack; the identity branch is a ring of
+// d_skip + 1 input frames (+ one scratch slot for update_state = 0), and the
+// merge is one streaming add kernel over the body's output (k_compose.cu).
+
+struct co_residual {
+  co_stack* stack = nullptr;
+  std::vector<co_conv*> body;
+  int shrink = 0, act = 0;
+  int64_t f_acc = 0, d_body = 0, d_skip = 0;
+  int64_t n = 0;
+  void* ring = nullptr;
+  int in_dtype = 0, out_dtype = 0;
+  int64_t B = 0, frame_elems = 0;     // input frame (H, W, C) elements per stream; the output has the same
+};
+
+extern "C" int co_residual_create(co_conv* const* body, int n_layers, int shrink, int activation,
+                                  co_residual** out) {
+  if (!out || !body || n_layers < 1) return fail(CO_ERR_ARG, "bad argument");
+  *out = nullptr;
+  if (activation != CO_ACT_NONE && activation != CO_ACT_RELU) return fail(CO_ERR_ARG, "bad activation");
+  co_stack* st = nullptr;
+  if (int rc = co_stack_create(body, n_layers, &st)) return rc;
+  auto bail = [&](int code) { co_stack_destroy(st); return code; };
+  // Principle 6 (A3): accumulated stride, padding and receptive field of the body
+  int64_t s_acc = 1, p_acc = 0, f_acc = 1;
+  for (int l = 0; l < n_layers; ++l) {
+    const Geom& g = body[l]->g;
+    p_acc += int64_t(g.pt) * s_acc;
+    f_acc += int64_t(g.f - 1) * s_acc;
+    s_acc *= g.st;
+  }
+  if (s_acc != 1) return bail(fail(CO_ERR_SHAPE, "residual body must keep the frame rate (s_acc = %lld)", (long long)s_acc));
+  const Geom& a = body[0]->g;
+  const Geom& z = body[n_layers - 1]->g;
+  if (a.Cin != z.Cout || a.H != z.Ho || a.W != z.Wo)
+    return bail(fail(CO_ERR_SHAPE, "residual body must keep channels and spatial shape (%d %dx%d -> %d %dx%d)", a.Cin,
+                     a.H, a.W, z.Cout, z.Ho, z.Wo));
+  const int64_t d_body = f_acc - p_acc - 1;
+  int64_t d_skip;
+  if (shrink) {
+    if (f_acc % 2 == 0) return bail(fail(CO_ERR_SHAPE, "centered residual needs an odd receptive field (f = %lld)", (long long)f_acc));
+    d_skip = (f_acc - 1) / 2;
+    if (d_skip > d_body) return bail(fail(CO_ERR_SHAPE, "centered residual: body padding exceeds (f-1)/2"));
+  } else {
+    if (2 * p_acc != f_acc - 1)
+      return bail(fail(CO_ERR_SHAPE, "residual without shrink needs equal padding (2 p_acc = %lld != f_acc - 1 = %lld)",
+                       (long long)(2 * p_acc), (long long)(f_acc - 1)));
+    d_skip = d_body;
+  }
+  co_residual* r = new (std::nothrow) co_residual();
+  if (!r) return bail(fail(CO_ERR_OOM, "host allocation"));
+  r->stack = st;
+  r->body.assign(body, body + n_layers);
+  r->shrink = shrink ? 1 : 0;
+  r->act = activation;
+  r->f_acc = f_acc; r->d_body = d_body; r->d_skip = d_skip;
+  r->in_dtype = a.in_dtype; r->out_dtype = z.out_dtype;
+  r->B = a.B; r->frame_elems = a.frame_elems;
+  {
+    const size_t bytes = size_t(d_skip + 2) * r->B * r->frame_elems * dsize(r->in_dtype);
+    cudaError_t e = cudaMalloc(&r->ring, bytes);
+    if (e == cudaSuccess) e = cudaMemset(r->ring, 0, bytes);
+    if (e != cudaSuccess) { co_residual_destroy(r); return fail(CO_ERR_OOM, "residual ring: %s", cudaGetErrorString(e)); }
+  }
+  *out = r;
+  return CO_OK;
+}
+
+extern "C" int co_residual_destroy(co_residual* r) {
+  if (!r) return CO_OK;
+  co_stack_destroy(r->stack);
+  cudaFree(r->ring);
+  delete r;
+  return CO_OK;
+}
+
+extern "C" int co_residual_step(co_residual* r, const void* x, void* y, int update_state, int* ready,
+                                co_stream stream) {
+  if (!r || !y) return fail(CO_ERR_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t fb = size_t(r->B) * r->frame_elems * dsize(r->in_dtype);
+  // the identity branch: frame n goes to ring slot n mod (d_skip + 1) (the
+  // scratch slot d_skip + 1 when the state must not change; a padding step,
+  // x == NULL, stores zeros), the merge reads frame n - d_skip
+  char* ring = static_cast<char*>(r->ring);
+  const int64_t R = r->d_skip + 1;
+  char* cur = ring + size_t(update_state ? floor_mod(r->n, R) : R) * fb;
+  if (x) CO_CUDA(cudaMemcpyAsync(cur, x, fb, cudaMemcpyDeviceToDevice, s));
+  else CO_CUDA(cudaMemsetAsync(cur, 0, fb, s));
+  const void* skip = r->d_skip == 0 ? cur : ring + size_t(floor_mod(r->n - r->d_skip, R)) * fb;
+  int rb = 0;
+  if (int rc = co_stack_step(r->stack, x, y, update_state, &rb, stream)) return rc;
+  if (rb)
+    CO_CUDA(co::launch_residual_add(r->out_dtype, y, r->frame_elems, r->in_dtype, skip, r->frame_elems, r->B,
+                                    r->frame_elems, r->act, s));
+  if (update_state) ++r->n;
+  if (ready) *ready = rb;
+  return CO_OK;
+}
+
+extern "C" int co_residual_forward(co_residual* r, const void* x, int64_t T, void* y, int64_t* T_out,
+                                   co_stream stream) {
+  if (!r || !x || !y) return fail(CO_ERR_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const void* cur = x;
+  int64_t Tc = T;
+  void* tmp_prev = nullptr;
+  const int L = int(r->body.size());
+  for (int l = 0; l < L; ++l) {
+    co_conv* h = r->body[l];
+    int64_t Tn = 0;
+    co_forward_out_len(h, Tc, &Tn);
+    if (Tn < 1) { if (tmp_prev) cudaFreeAsync(tmp_prev, s); return fail(CO_ERR_LENGTH, "residual: T' < 1 at layer %d", l); }
+    void* dst = y;
+    if (l + 1 < L) {
+      const size_t bytes = size_t(h->g.B) * Tn * h->g.HWo * h->g.Cout * dsize(h->g.out_dtype);
+      cudaError_t e = cudaMallocAsync(&dst, bytes, s);
+      if (e != cudaSuccess) { if (tmp_prev) cudaFreeAsync(tmp_prev, s); return fail(CO_ERR_OOM, "%s", cudaGetErrorString(e)); }
+    }
+    int64_t Tgot = 0;
+    int rc = co_forward(h, cur, Tc, dst, &Tgot, stream);
+    if (tmp_prev) cudaFreeAsync(tmp_prev, s);
+    tmp_prev = (l + 1 < L) ? dst : nullptr;
+    if (rc) { if (tmp_prev) cudaFreeAsync(tmp_prev, s); return rc; }
+    cur = dst;
+    Tc = Tgot;
+  }
+  // identity branch: the input clip, cropped by (f_acc-1)/2 at each end when shrink
+  const int64_t c = r->shrink ? r->d_skip : 0;
+  const int64_t fe = r->frame_elems;
+  const char* xs = static_cast<const char*>(x) + size_t(c) * fe * dsize(r->in_dtype);
+  CO_CUDA(co::launch_residual_add(r->out_dtype, y, Tc * fe, r->in_dtype, xs, T * fe, r->B, Tc * fe, r->act, s));
+  if (T_out) *T_out = Tc;
+  return CO_OK;
+}
+
+extern "C" int co_residual_clean(co_residual* r, co_stream stream) {
+  if (!r) return fail(CO_ERR_ARG, "null residual");
+  if (int rc = co_stack_clean(r->stack, stream)) return rc;
+  if (r->ring)
+    CO_CUDA(cudaMemsetAsync(r->ring, 0, size_t(r->d_skip + 2) * r->B * r->frame_elems * dsize(r->in_dtype),
+                            (cudaStream_t)stream));
+  r->n = 0;
+  return CO_OK;
+}
+
+extern "C" int co_residual_delay(const co_residual* r, int64_t* delay, int64_t* skip_delay) {
+  if (!r) return fail(CO_ERR_ARG, "null residual");
+  if (delay) *delay = r->d_body;
+  if (skip_delay) *skip_delay = r->d_skip;
   return CO_OK;
 }
