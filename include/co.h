@@ -242,6 +242,29 @@ int co_stack_steps_host(co_stack* st, const void* x_host, int64_t T, void* y_hos
 int co_stack_delay(const co_stack* st, int64_t* d_nn);
 int co_stack_clean(co_stack* st, co_stream stream);
 
+/* ---- per-stream clocks --------- */
+
+/* Streams join and leave independently.  A handle keeps one clock n (A19,
+ * P:283 "the same global clock"); stream b's own step count is n_b = n - join_b.
+ * co_state_clean_streams resets the state slices of the streams with
+ * mask[b] != 0 (host array of B flags) to the clean state (zero partial sums /
+ * frames; -inf for MAX pooling) and sets join_b = n; from then on stream b
+ * behaves as a fresh stream whose first frame is the next step's.  Under
+ * temporal stride s it must be called at n = 0 mod s (else CO_ERR_ARG), so the
+ * stream's Ready phase matches the handle's.  co_state_clean and co_state_set
+ * reset every join_b to 0.  Stream-ordered on `stream`. */
+int co_state_clean_streams(co_conv* h, const uint8_t* mask, co_stream stream);
+/* Per-stream readiness of the last step on the handle's clock (host array of B
+ * flags): ready[b] = the step was Ready and n_b >= d at that step. */
+int co_stream_ready(const co_conv* h, uint8_t* ready);
+/* Stack form: layer 0 is cleaned now; each later layer cleans stream b when
+ * its first valid input for b arrives (the layer below reports b ready), so
+ * every layer sees the fresh stream from its own first frame.  Later layers
+ * must have temporal stride 1 (else CO_ERR_UNSUPPORTED). */
+int co_stack_clean_streams(co_stack* st, const uint8_t* mask, co_stream stream);
+/* Per-stream readiness of the stack's last step (all 0 when it was Empty). */
+int co_stack_stream_ready(const co_stack* st, uint8_t* ready);
+
 /* ---- composition: Residual ------------------------------- */
 
 /* Residual(body) with Sum ("Residual connections", Listing 3

@@ -59,6 +59,17 @@ def _tup(v, n=3, fill=1):
     return v + (fill,) * (n - len(v))
 
 
+def _stream_mask(streams, B: int):
+    m = (C.c_uint8 * B)()
+    if isinstance(streams, torch.Tensor) and streams.dtype == torch.bool:
+        streams = torch.nonzero(streams).flatten().tolist()
+    for b in streams:
+        if not 0 <= int(b) < B:
+            raise ValueError(f"stream {b} out of range")
+        m[int(b)] = 1
+    return m
+
+
 def _steps_host(fn, handle, x_host: torch.Tensor, y_host: torch.Tensor, stream):
     """x_host: (T, B, *S, Cin) pinned, time-major; y_host: (>= n_ready, B, *S', Cout) pinned."""
     T = x_host.shape[0]
@@ -239,6 +250,19 @@ class Conv:
             state = state.to(self.dtype if self.state_layout == "raw" else torch.float32).contiguous()
         check(lib().co_state_set(self._h, C.c_void_p(state.data_ptr()) if state.numel() else None, nb.value,
                                  C.byref(meta), _stream(stream)))
+
+    # ---- per-stream clocks ----
+    def clean_streams(self, streams, stream=None):
+        """Reset the given streams (indices or a bool mask of length B) to the
+        clean state; each restarts its own clock at the next step."""
+        m = _stream_mask(streams, self.n_streams)
+        check(lib().co_state_clean_streams(self._h, m, _stream(stream)))
+
+    def stream_ready(self) -> torch.Tensor:
+        """Per-stream readiness (bool, B) of the last step."""
+        m = (C.c_uint8 * self.n_streams)()
+        check(lib().co_stream_ready(self._h, m))
+        return torch.tensor(list(m), dtype=torch.bool)
 
     def _ring_dtype(self):
         # pooling ring: spatially reduced frames, MAX in the input dtype, AVG fp32 sums
@@ -437,3 +461,16 @@ class Stack:
 
     def clean_state(self, stream=None):
         check(lib().co_stack_clean(self._h, _stream(stream)))
+
+    def clean_streams(self, streams, stream=None):
+        """Restart the given streams (indices or bool mask): layer 0 now, each
+        later layer when the stream's first valid input reaches it."""
+        m = _stream_mask(streams, self.layers[0].n_streams)
+        check(lib().co_stack_clean_streams(self._h, m, _stream(stream)))
+
+    def stream_ready(self) -> torch.Tensor:
+        """Per-stream readiness (bool, B) of the stack's last step."""
+        B = self.layers[-1].n_streams
+        m = (C.c_uint8 * B)()
+        check(lib().co_stack_stream_ready(self._h, m))
+        return torch.tensor(list(m), dtype=torch.bool)

@@ -31,7 +31,8 @@ EXPORTS = ["co_conv_create", "co_conv_destroy", "co_conv_info", "co_delay", "co_
            "co_forward_step", "co_forward_step_host", "co_forward_steps_host", "co_forward_steps", "co_steps_ready_count",
            "co_forward", "co_forward_out_len", "co_state_bytes", "co_state_get", "co_state_set",
            "co_state_clean", "co_stack_create", "co_stack_destroy", "co_stack_step", "co_stack_step_host", "co_stack_steps_host", "co_stack_delay",
-           "co_stack_clean", "co_residual_create", "co_residual_destroy", "co_residual_step", "co_residual_forward",
+           "co_stack_clean", "co_state_clean_streams", "co_stream_ready", "co_stack_clean_streams",
+           "co_stack_stream_ready", "co_residual_create", "co_residual_destroy", "co_residual_step", "co_residual_forward",
            "co_residual_clean", "co_residual_delay", "co_last_error", "co_abi_version"]
 
 
@@ -93,6 +94,10 @@ def lib():
             L.co_stack_step_host.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_int), vp]
             L.co_stack_delay.argtypes = [vp, i64p]
             L.co_stack_clean.argtypes = [vp, vp]
+            L.co_state_clean_streams.argtypes = [vp, C.POINTER(C.c_uint8), vp]
+            L.co_stream_ready.argtypes = [vp, C.POINTER(C.c_uint8)]
+            L.co_stack_clean_streams.argtypes = [vp, C.POINTER(C.c_uint8), vp]
+            L.co_stack_stream_ready.argtypes = [vp, C.POINTER(C.c_uint8)]
             L.co_residual_create.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
             L.co_residual_destroy.argtypes = [vp]
             L.co_residual_step.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_int), vp]

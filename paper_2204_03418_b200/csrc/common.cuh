@@ -123,6 +123,12 @@ int pool_split_lanes(const Geom& g);   // choice of pool_G (env CO_POOL_G overri
 int pool_block_decomposition(const Geom& g);   // choice of pool_vh (env CO_POOL_VH overrides)
 cudaError_t launch_pool_rebuild(const Geom& g, void* state, int64_t m_next, cudaStream_t s);
 
+// Per-stream clean (k_direct.cu): zero the listed streams'
+// partial-sum state (any PSUM layout), or fill their slices of a ring layout.
+cudaError_t launch_clean_streams_psum(const Geom& g, float* state, const int64_t* ids, int nm, cudaStream_t s);
+cudaError_t launch_fill_streams(void* ring, int esz, int64_t slots, int64_t B, int64_t per, const int64_t* ids, int nm,
+                                uint32_t value, cudaStream_t s);
+
 // Residual composite merge (k_compose.cu): y[r, :n] <- act(y[r, :n] + x[r, :n]) over rows.
 cudaError_t launch_residual_add(int y_dtype, void* y, int64_t y_rstride, int x_dtype, const void* x,
                                 int64_t x_rstride, int64_t rows, int64_t n, int act, cudaStream_t s);

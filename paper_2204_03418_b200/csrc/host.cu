@@ -113,10 +113,17 @@ struct co_conv {
   void* hx = nullptr;          // staging for *_host
   void* hy = nullptr;
   HostPipe pipe;               // staging for co_forward_steps_host
+  // per-stream clocks: stream b joined at tick join[b] (empty =
+  // all joined at 0); the last step on the handle's clock: its n and readiness
+  std::vector<int64_t> join;
+  int64_t last_n = -1;
+  int last_ready = 0;
 };
 
 struct co_stack {
   std::vector<co_conv*> layers;
+  std::vector<std::vector<uint8_t>> pending;   // per layer: streams whose clean waits for their first valid input
+  int last_ready = 0;
   std::vector<void*> act;      // inter-layer activations (one per layer but the last)
   void* hx = nullptr;          // staging for co_stack_step_host
   void* hy = nullptr;
@@ -494,8 +501,23 @@ static int step_delay(co_conv* h, int64_t& n, float* state, const void* x, int64
   return CO_OK;
 }
 
+static int step_dispatch(co_conv* h, int64_t& n, float* state, const void* x, int64_t x_bstride, void* y,
+                         int64_t y_bstride, int update_state, int* ready, cudaStream_t s);
+
+// Every tick goes through here; ticks on the handle's own clock record n and
+// readiness for the per-stream flags (co_stream_ready).
 static int step_impl(co_conv* h, int64_t& n, float* state, const void* x, int64_t x_bstride, void* y,
                      int64_t y_bstride, int update_state, int* ready, cudaStream_t s) {
+  const int64_t n0 = n;
+  int r = 0;
+  if (int rc = step_dispatch(h, n, state, x, x_bstride, y, y_bstride, update_state, &r, s)) return rc;
+  if (&n == &h->n) { h->last_n = n0; h->last_ready = r; }
+  if (ready) *ready = r;
+  return CO_OK;
+}
+
+static int step_dispatch(co_conv* h, int64_t& n, float* state, const void* x, int64_t x_bstride, void* y,
+                         int64_t y_bstride, int update_state, int* ready, cudaStream_t s) {
   if (h->g.op == CO_OP_DELAY) return step_delay(h, n, state, x, x_bstride, y, y_bstride, update_state, ready, s);
   if (h->g.op != CO_OP_CONV) return step_pool(h, n, state, x, x_bstride, y, y_bstride, update_state, ready, s);
   if (h->g.raw) return step_raw(h, n, state, x, x_bstride, y, y_bstride, update_state, ready, s);
@@ -727,6 +749,9 @@ extern "C" int co_state_set(co_conv* h, const void* src, size_t bytes, const co_
     if (e != cudaSuccess) return fail(CO_ERR_CUDA, "state_set: %s", cudaGetErrorString(e));
   }
   h->n = meta->n;
+  h->join.clear();          // per-stream join ticks are not part of the canonical state
+  h->last_n = -1;
+  h->last_ready = 0;
   return CO_OK;
 }
 
@@ -738,6 +763,9 @@ extern "C" int co_state_clean(co_conv* h, co_stream stream) {
   else if (state_alloc_bytes(g) > 0)
     CO_CUDA(cudaMemsetAsync(h->state, 0, state_alloc_bytes(g), (cudaStream_t)stream));
   h->n = 0;
+  h->join.clear();
+  h->last_n = -1;
+  h->last_ready = 0;
   return CO_OK;
 }
 
@@ -783,8 +811,25 @@ extern "C" int co_stack_step(co_stack* st, const void* x, void* y, int update_st
   if (!st || !y) return fail(CO_ERR_ARG, "null argument");
   const void* cur = x;
   const int L = int(st->layers.size());
+  st->last_ready = 0;
   for (int l = 0; l < L; ++l) {
     void* out = (l + 1 < L) ? st->act[l] : y;
+    if (l > 0 && update_state && !st->pending.empty() && !st->pending[l].empty()) {
+      // a joined stream reaches layer l with its first valid input: clean it here now
+      std::vector<uint8_t>& pend = st->pending[l];
+      std::vector<uint8_t> prev(pend.size()), mask(pend.size(), 0);
+      co_stream_ready(st->layers[l - 1], prev.data());
+      if (st->pending[l - 1].size() == prev.size())   // still waiting below: not a valid input yet
+        for (size_t b = 0; b < prev.size(); ++b) prev[b] &= st->pending[l - 1][b] ? 0 : 1;
+      bool any = false, left = false;
+      for (size_t b = 0; b < pend.size(); ++b) {
+        if (pend[b] && prev[b]) { mask[b] = 1; pend[b] = 0; any = true; }
+        left |= pend[b] != 0;
+      }
+      if (any)
+        if (int rc = co_state_clean_streams(st->layers[l], mask.data(), stream)) return rc;
+      if (!left) pend.clear();
+    }
     int r = 0;
     if (int rc = co_forward_step(st->layers[l], cur, out, update_state, &r, stream)) return rc;
     if (!r) {   // Empty ends the tick; downstream layers are not advanced
@@ -793,6 +838,7 @@ extern "C" int co_stack_step(co_stack* st, const void* x, void* y, int update_st
     }
     cur = out;
   }
+  st->last_ready = 1;
   if (ready) *ready = 1;
   return CO_OK;
 }
@@ -844,6 +890,8 @@ extern "C" int co_stack_delay(const co_stack* st, int64_t* d_nn) {
 
 extern "C" int co_stack_clean(co_stack* st, co_stream stream) {
   if (!st) return fail(CO_ERR_ARG, "null stack");
+  st->pending.clear();
+  st->last_ready = 0;
   for (co_conv* h : st->layers)
     if (int rc = co_state_clean(h, stream)) return rc;
   return CO_OK;
@@ -1001,5 +1049,88 @@ extern "C" int co_residual_delay(const co_residual* r, int64_t* delay, int64_t* 
   if (!r) return fail(CO_ERR_ARG, "null residual");
   if (delay) *delay = r->d_body;
   if (skip_delay) *skip_delay = r->d_skip;
+  return CO_OK;
+}
+
+// ----------------------------------------------------------------- per-stream clocks
+// streams join (and leave) independently.  A handle keeps one
+// clock (A19); stream b's own step count is n_b = n - join[b].  Cleaning
+// a stream resets its state slice to the clean state and sets join[b] = n; its
+// outputs are valid (co_stream_ready) on the handle's Ready ticks with
+// n_b >= d.  Under temporal stride s the join must fall on n = 0 mod s, so the
+// stream's Ready phase and the emitted outputs' ring slots (A20) are the
+// handle's.
+
+extern "C" int co_state_clean_streams(co_conv* h, const uint8_t* mask, co_stream stream) {
+  if (!h || !mask) return fail(CO_ERR_ARG, "null argument");
+  const Geom& g = h->g;
+  if (floor_mod(h->n, g.st) != 0)
+    return fail(CO_ERR_ARG, "per-stream clean at tick n = %lld: needs n = 0 mod s = %d", (long long)h->n, g.st);
+  std::vector<int64_t> ids;
+  for (int64_t b = 0; b < g.B; ++b)
+    if (mask[b]) ids.push_back(b);
+  if (ids.empty()) return CO_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t* dids = nullptr;
+  CO_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dids), ids.size() * sizeof(int64_t), s));
+  CO_CUDA(cudaMemcpyAsync(dids, ids.data(), ids.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  cudaError_t e = cudaSuccess;
+  const int nm = int(ids.size());
+  if (!g.raw && g.op == CO_OP_CONV) {
+    if (g.R > 0) e = co::launch_clean_streams_psum(g, h->state, dids, nm, s);
+  } else {
+    const size_t sb = ring_slot_bytes(g);
+    const int esz = g.op == CO_OP_CONV ? int(dsize(g.in_dtype)) : co::pool_ring_esz(g);
+    const int64_t slots = g.op == CO_OP_CONV ? g.f + 1 : co::pool_state_slots(g);
+    const int64_t per = int64_t(sb / esz) / g.B;
+    uint32_t value = 0;
+    if (g.op == CO_OP_MAX_POOL) value = esz == 2 ? 0xFF80u : 0xFF800000u;   // -inf: MAX's padding (A22)
+    e = co::launch_fill_streams(h->state, esz, slots, g.B, per, dids, nm, value, s);
+  }
+  cudaFreeAsync(dids, s);
+  if (e != cudaSuccess) return fail(CO_ERR_CUDA, "clean streams: %s", cudaGetErrorString(e));
+  if (h->join.empty()) h->join.assign(size_t(g.B), 0);
+  for (int64_t b : ids) h->join[size_t(b)] = h->n;
+  return CO_OK;
+}
+
+extern "C" int co_stream_ready(const co_conv* h, uint8_t* ready) {
+  if (!h || !ready) return fail(CO_ERR_ARG, "null argument");
+  const Geom& g = h->g;
+  for (int64_t b = 0; b < g.B; ++b) {
+    const int64_t jb = h->join.empty() ? 0 : h->join[size_t(b)];
+    ready[b] = uint8_t(h->last_ready && h->last_n >= 0 && h->last_n - jb >= g.delay);
+  }
+  return CO_OK;
+}
+
+extern "C" int co_stack_clean_streams(co_stack* st, const uint8_t* mask, co_stream stream) {
+  if (!st || !mask) return fail(CO_ERR_ARG, "null argument");
+  const int L = int(st->layers.size());
+  for (int l = 1; l < L; ++l)
+    if (st->layers[l]->g.st != 1)
+      return fail(CO_ERR_UNSUPPORTED, "per-stream clean in a stack needs temporal stride 1 after layer 0 (layer %d)", l);
+  if (int rc = co_state_clean_streams(st->layers[0], mask, stream)) return rc;
+  const size_t B = size_t(st->layers[0]->g.B);
+  if (st->pending.size() != size_t(L)) st->pending.assign(size_t(L), {});
+  for (int l = 1; l < L; ++l) {
+    std::vector<uint8_t>& p = st->pending[l];
+    if (p.empty()) p.assign(B, 0);
+    for (size_t b = 0; b < B; ++b) p[b] |= mask[b] ? 1 : 0;
+  }
+  return CO_OK;
+}
+
+extern "C" int co_stack_stream_ready(const co_stack* st, uint8_t* ready) {
+  if (!st || !ready) return fail(CO_ERR_ARG, "null argument");
+  const co_conv* last = st->layers.back();
+  if (!st->last_ready) {
+    for (int64_t b = 0; b < last->g.B; ++b) ready[b] = 0;
+    return CO_OK;
+  }
+  if (int rc = co_stream_ready(last, ready)) return rc;
+  for (const std::vector<uint8_t>& p : st->pending)      // a clean still pending in some layer
+    if (p.size() == size_t(last->g.B))
+      for (size_t b = 0; b < p.size(); ++b) ready[b] &= p[b] ? 0 : 1;
   return CO_OK;
 }

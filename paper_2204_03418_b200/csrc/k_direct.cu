@@ -244,3 +244,65 @@ cudaError_t launch_state_set(const Geom& g, float* state, const float* src, int 
 }
 
 }  // namespace co
+
+// ---- per-stream clean --------------------------------------
+namespace co {
+
+// PSUM layouts: zero every state element (slot, pixel, channel) of the listed
+// streams, through state_index so every physical layout (quad-major,
+// tile-blocked, channels-last) is covered.
+__global__ void k_clean_streams_psum(Geom g, float* __restrict__ state, const int64_t* __restrict__ ids, int nm) {
+  const int64_t per = g.HWo * g.Cout;
+  const int64_t total = int64_t(g.R) * nm * per;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int o = int(i % g.Cout);
+    int64_t r = i / g.Cout;
+    const int64_t p = r % g.HWo;
+    r /= g.HWo;
+    const int j = int(r % nm);
+    const int slot = int(r / nm);
+    state[state_index(g, slot, ids[j] * g.HWo + p, o)] = 0.f;
+  }
+}
+
+// Ring layouts ([slot][B][per-stream elements]): set the listed streams'
+// elements of every slot to `value` (a 2- or 4-byte bit pattern).
+template <typename T>
+__global__ void k_fill_streams(T* __restrict__ ring, int64_t slots, int64_t B, int64_t per, const int64_t* __restrict__ ids,
+                               int nm, T value) {
+  const int64_t total = slots * nm * per;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t e = i % per;
+    const int64_t r = i / per;
+    const int j = int(r % nm);
+    const int64_t slot = r / nm;
+    ring[(slot * B + ids[j]) * per + e] = value;
+  }
+}
+
+static int clean_grid(int64_t total) {
+  const int64_t b = (total + 255) / 256;
+  return int(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
+}
+
+cudaError_t launch_clean_streams_psum(const Geom& g, float* state, const int64_t* ids, int nm, cudaStream_t s) {
+  const int64_t total = int64_t(g.R) * nm * g.HWo * g.Cout;
+  if (total == 0) return cudaSuccess;
+  k_clean_streams_psum<<<clean_grid(total), 256, 0, s>>>(g, state, ids, nm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_streams(void* ring, int esz, int64_t slots, int64_t B, int64_t per, const int64_t* ids, int nm,
+                                uint32_t value, cudaStream_t s) {
+  const int64_t total = slots * nm * per;
+  if (total == 0) return cudaSuccess;
+  if (esz == 2)
+    k_fill_streams<uint16_t><<<clean_grid(total), 256, 0, s>>>(static_cast<uint16_t*>(ring), slots, B, per, ids, nm,
+                                                               uint16_t(value));
+  else
+    k_fill_streams<uint32_t><<<clean_grid(total), 256, 0, s>>>(static_cast<uint32_t*>(ring), slots, B, per, ids, nm,
+                                                               value);
+  return cudaGetLastError();
+}
+
+}  // namespace co
