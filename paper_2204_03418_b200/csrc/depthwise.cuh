@@ -12,4 +12,10 @@ Depthwise* depthwise_create(const Geom& g, const void* w_dev, std::string& err);
 void depthwise_destroy(Depthwise* t);
 const char* depthwise_name(const Depthwise* t);
 cudaError_t depthwise_step(Depthwise* t, const Geom& g, const StepArgs& a, const float* bias, cudaStream_t s);
+// Chunked steps: the fold of `total` ticks starting at clock n0
+// over a clip x (B, T, H, W, C) (ticks >= T are padding frames) in one launch,
+// state kept in registers; y (B, n_ready, Ho, Wo, C) with stream stride y_bstride.
+bool depthwise_chunkable(const Depthwise* t, const Geom& g);
+cudaError_t depthwise_steps(Depthwise* t, const Geom& g, const void* x, int64_t T, int64_t total, int64_t n0, void* y,
+                            int64_t y_bstride, float* state, const float* bias, cudaStream_t s);
 }  // namespace co

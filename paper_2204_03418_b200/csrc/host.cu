@@ -653,6 +653,22 @@ extern "C" int co_forward_steps(co_conv* h, const void* x, int64_t T, void* y, u
   const int64_t total = T + (pad_end ? g.pt : 0);
   int64_t r_count = 0;
   int rc = CO_OK;
+  if (total > 0 && h->kernel_used == CO_KERNEL_DEPTHWISE && co::depthwise_chunkable(h->dw, g)) {
+    // chunked: the whole fold in one launch, state in registers
+    cudaError_t e = co::depthwise_steps(h->dw, g, x, T, total, clock, y, cap * oframe, state, h->bias, s);
+    if (scratch) cudaFreeAsync(scratch, s);
+    if (e != cudaSuccess) return fail(CO_ERR_CUDA, "chunked steps: %s", cudaGetErrorString(e));
+    int last = 0;
+    for (int64_t t = 0; t < total; ++t) {
+      last = (clock + t) >= g.delay;
+      if (ready_mask) ready_mask[t] = uint8_t(last);
+      r_count += last;
+    }
+    if (update_state) { h->last_n = clock + total - 1; h->last_ready = last; }
+    clock += total;
+    if (n_ready) *n_ready = r_count;
+    return CO_OK;
+  }
   for (int64_t t = 0; t < total && rc == CO_OK; ++t) {
     const void* xt = (t < T) ? static_cast<const char*>(x) + size_t(t) * frame * isz : nullptr;
     void* yt = static_cast<char*>(y) + size_t(r_count) * oframe * osz;

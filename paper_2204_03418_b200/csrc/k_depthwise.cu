@@ -29,6 +29,7 @@
 //   S[slot_k] += P_k  for 0 < k < kt-1;   S[slot_0] = P_0 (after the emit read)
 // with P_k = W[:, k] (*) x_t per channel.  The slots come from the host clock.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 
@@ -273,6 +274,82 @@ __global__ void __launch_bounds__(kDwThreads, CO_DW_T_MINB) k_step_dw_t(const Dw
   }
 }
 
+// ------------------------------------------------------------------ K3c: chunked steps
+// SURVEY §8f f2 "chunked co_forward_steps that keeps state tiles on-chip across
+// T frames": a thread owns one (pixel, channel quad) for a whole clip and keeps
+// its kt-1 pending outputs in registers as a shift register, Q[j] = the output
+// completing j ticks ahead; per frame
+//   y = Q[0] + (P_{kt-1} + b),  Q[j-1] = Q[j] + P_{kt-1-j} (j = 1..kt-2),  Q[kt-2] = P_0
+// -- k_step_dw_t's operations in its order, so chunked and per-step folds agree
+// bitwise -- and the fp32 ring is read once before the clip and written once
+// after it (outputs i < 0, never emitted, are neither read nor written, as in
+// the per-step kernel).  HBM per stream-step: x + y (+ 2 (kt-1) state / T):
+// the state round trip that dominates the per-step kernel
+// leaves the hot loop.  Temporal stride 1, dilation 1 (R = kt - 1).
+struct ChunkArgs {
+  const __nv_bfloat16* x;               // clip of stream 0, (T, H*W*C); stream stride x_bstride
+  int64_t x_bstride, T, total;          // frames present, ticks to run (T + pad_end padding)
+  int64_t m0;                           // padded index n0 + p of the first tick
+  int64_t oi0;                          // output index of tick t: n0 + t - oi0 (when Ready)
+  int64_t y_bstride;
+  int d;                                // delay: tick t is Ready when n0 + t >= d
+  int64_t n0;
+};
+
+template <int KT>
+__global__ void __launch_bounds__(kDwThreads, 2) k_steps_dw_t(const DwParams p, const ChunkArgs c) {
+  constexpr int NQ = KT > 1 ? KT - 1 : 1;
+  const int64_t n_items = p.plane * p.Cq;
+  const int R = KT - 1;
+  for (int64_t it = int64_t(blockIdx.x) * kDwThreads + threadIdx.x; it < n_items;
+       it += int64_t(gridDim.x) * kDwThreads) {
+    const int q = int(it % p.Cq);
+    const int64_t pix = it / p.Cq;
+    const int64_t b = pix / p.HWo;
+    const int64_t pin = pix - b * p.HWo;
+    float4 w[KT];
+#pragma unroll
+    for (int k = 0; k < KT; ++k) w[k] = __ldg(reinterpret_cast<const float4*>(p.w + k * p.C) + q);
+    const float4 bias4 = __ldg(reinterpret_cast<const float4*>(p.bias) + q);
+    float4 Q[NQ];
+    const int64_t i0 = c.m0 - (KT - 1);            // output completing at the first tick
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      Q[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (KT > 1 && i0 + j >= 0) Q[j] = __ldcs(srow(p, int((i0 + j) % R), pix, q));
+    }
+    const __nv_bfloat16* xs = c.x + b * c.x_bstride + pin * p.C + 4 * q;
+    const int64_t fstride = int64_t(p.HWo) * p.C;
+    constexpr int U = 4;                           // frames in flight per thread
+    for (int64_t t0 = 0; t0 < c.total; t0 += U) {
+      float4 xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        xv[u] = (t0 + u < c.T) ? ld_bf16x4(xs + (t0 + u) * fstride) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t t = t0 + u;
+        if (t >= c.total) break;
+        auto P = [&](int k) { return f4_fma(w[k], xv[u], make_float4(0.f, 0.f, 0.f, 0.f)); };
+        if (c.n0 + t >= c.d) {
+          float4 v = f4_add(P(KT - 1), bias4);
+          if (KT > 1) v = f4_add(Q[0], v);
+          st_out4(p, b, (c.n0 + t - c.oi0) * p.HWo + pin, q, f4_act(v, p.act));
+        }
+        if (KT > 1) {
+#pragma unroll
+          for (int j = 1; j < KT - 1; ++j) Q[j - 1] = f4_add(Q[j], P(KT - 1 - j));
+          Q[NQ - 1] = P(0);
+        }
+      }
+    }
+    const int64_t i1 = c.m0 + c.total - (KT - 1);  // output completing at the next tick
+#pragma unroll
+    for (int j = 0; j < NQ; ++j)
+      if (KT > 1 && i1 + j >= 0) __stcs(srow(p, int((i1 + j) % R), pix, q), Q[j]);
+  }
+}
+
 // ------------------------------------------------------------------ RAW layout
 // (SURVEY §8f f1): a Ready step reads the window's kt frames from the frame
 // ring (slot[k]) and writes y; no state traffic beyond those reads.  Thread =
@@ -382,18 +459,20 @@ __global__ void k_pack_dw(const __nv_bfloat16* __restrict__ w, float* __restrict
 }
 
 typedef void (*DwFn)(const DwParams);
+typedef void (*DwChunkFn)(const DwParams, const ChunkArgs);
 struct DwVariant {
   int KT, KH, KW;
   DwFn fn;
   int PX = 1;                           // K2: output pixels per thread strip
   DwFn raw = nullptr;                   // RAW-layout kernel for this shape
+  DwChunkFn chunk = nullptr;            // chunked-steps kernel (temporal only)
 };
 #ifndef CO_DW_PX
 #define CO_DW_PX 2                      // output pixels per thread strip (experiments: -DCO_DW_PX=n)
 #endif
 #define CO_DW_ST(kt, kh, kw) {kt, kh, kw, (DwFn)k_step_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>, \
                               (kt <= 3 ? CO_DW_PX : 2), (DwFn)k_step_dw_raw<kt, kh, kw>}
-#define CO_DW_T(kt) {kt, 1, 1, (DwFn)k_step_dw_t<kt>, 1, (DwFn)k_step_dw_raw<kt, 1, 1>}
+#define CO_DW_T(kt) {kt, 1, 1, (DwFn)k_step_dw_t<kt>, 1, (DwFn)k_step_dw_raw<kt, 1, 1>, (DwChunkFn)k_steps_dw_t<kt>}
 const DwVariant kDwVariants[] = {
     CO_DW_ST(1, 3, 3), CO_DW_ST(2, 3, 3), CO_DW_ST(3, 3, 3), CO_DW_ST(5, 3, 3), CO_DW_ST(3, 5, 5),
     CO_DW_T(2), CO_DW_T(3), CO_DW_T(4), CO_DW_T(5), CO_DW_T(7), CO_DW_T(9),
@@ -504,6 +583,42 @@ Depthwise* depthwise_create(const Geom& g, const void* w_dev, std::string& err) 
     snprintf(buf, sizeof(buf), "k_step_dw_st<%d,%d,%d>", pl.var->KT, pl.var->KH, pl.var->KW);
   t->name = buf;
   return t;
+}
+
+bool depthwise_chunkable(const Depthwise* t, const Geom& g) {
+  if (const char* e = getenv("CO_CHUNK"))       // experiment / test knob: 0 = always fold per step
+    if (!atoi(e)) return false;
+  return t && t->pl.temporal && t->pl.var->chunk && !g.raw && g.st == 1 && g.dt == 1 && g.kt >= 2;
+}
+
+cudaError_t depthwise_steps(Depthwise* t, const Geom& g, const void* x, int64_t T, int64_t total, int64_t n0, void* y,
+                            int64_t y_bstride, float* state, const float* bias, cudaStream_t s) {
+  DwParams p{};
+  p.y = y;
+  p.y_bstride = y_bstride;
+  p.state = state;
+  p.w = t->w;
+  p.bias = bias;
+  p.act = g.act; p.out_f32 = (g.out_dtype == F32);
+  p.C = g.Cout; p.Cq = g.Cout / 4; p.H = g.H; p.W = g.W; p.Ho = g.Ho; p.Wo = g.Wo;
+  p.HWo = g.HWo; p.plane = g.B * g.HWo;
+  ChunkArgs c{};
+  c.x = static_cast<const __nv_bfloat16*>(x);
+  c.x_bstride = T * g.frame_elems;
+  c.T = T; c.total = total;
+  c.n0 = n0; c.m0 = n0 + g.pt; c.d = g.delay;
+  c.oi0 = n0 > g.delay ? n0 : g.delay;
+  c.y_bstride = y_bstride;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, t->pl.var->chunk, kDwThreads, 0);
+  const int64_t items = p.plane * p.Cq;
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>((items + kDwThreads - 1) / kDwThreads,
+                                                              int64_t(sms) * std::max(per_sm, 1))));
+  void* args[] = {&p, &c};
+  return cudaLaunchKernel(reinterpret_cast<const void*>(t->pl.var->chunk), dim3(unsigned(grid)), dim3(kDwThreads),
+                          args, 0, s);
 }
 
 void depthwise_destroy(Depthwise* t) {

@@ -1,0 +1,80 @@
+"""Chunked co_forward_steps (k_depthwise.cu k_steps_dw_t): the
+fold of a whole clip in one launch with the state in registers must equal the
+per-step fold bit for bit -- outputs, ready mask, clock and canonical state --
+across consecutive calls (state carried between chunks), pad_end, mid-stream
+starts (n0 > d) and update_state = 0, and match the fp64 oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from tests.helpers import make_pair, np_of, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _clip(rng, B, C, T, H, W):
+    import paper_2204_03418_b200 as co
+    x = rng.standard_normal((B, C, T, H, W))
+    return co.channels_last(torch.from_numpy(x).to(torch.bfloat16).cuda())
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("kt,pad", [(2, 0), (3, 1), (5, 0), (5, 4), (7, 2), (9, 0)])
+def test_chunked_equals_per_step_fold(kt, pad, out_dtype, monkeypatch):
+    rng = np.random.default_rng(kt * 10 + pad)
+    B, C, H, W = 3, 32, 4, 5
+    d = O.Desc(2, C, C, (kt, 1, 1), padding=(pad, 0, 0), groups=C, in_spatial=(H, W))
+    Wt = rng.standard_normal(d.w_shape) / np.sqrt(kt)
+    bt = rng.standard_normal(C) * 0.1
+    runs = {}
+    for chunk in ("1", "0"):
+        monkeypatch.setenv("CO_CHUNK", chunk)
+        conv, sm, _, _ = make_pair(d, Wt, bt, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="depthwise",
+                                   activation="relu")
+        rng2 = np.random.default_rng(1)
+        outs = []
+        for T, pe in ((3, False), (kt + 4, False), (1, False), (6, True)):   # n0 < d, n0 > d, tiny, pad_end
+            ys, mask = conv.forward_steps(_clip(rng2, B, C, T, H, W), pad_end=pe)
+            outs.append((ys.clone(), mask.clone(), conv.n))
+        probe, _ = conv.forward_steps(_clip(rng2, B, C, 4, H, W), update_state=False)
+        st, meta = conv.state_dict_stream()
+        runs[chunk] = (outs, probe.clone(), st.clone(), conv.n)
+    (oa, pa, sa, na), (ob, pb, sb, nb) = runs["1"], runs["0"]
+    assert na == nb
+    for (ya, ma, ca), (yb, mb, cb) in zip(oa, ob):
+        assert ca == cb and torch.equal(ma, mb)
+        assert torch.equal(ya, yb)
+    assert torch.equal(pa, pb)
+    assert torch.equal(sa, sb)
+
+
+def test_chunked_matches_oracle_and_continues_per_step(monkeypatch):
+    """A chunk, then per-step calls, then another chunk: every Ready output
+    matches the oracle fed the same frames."""
+    monkeypatch.setenv("CO_CHUNK", "1")
+    rng = np.random.default_rng(3)
+    B, C, H, W, kt = 2, 64, 3, 4, 5
+    d = O.Desc(2, C, C, (kt, 1, 1), groups=C, in_spatial=(H, W))
+    conv, sm, _, _ = make_pair(d, rng.standard_normal(d.w_shape) / 2, rng.standard_normal(C) * 0.1, B,
+                               dtype=torch.bfloat16, out_dtype=torch.float32, kernel="depthwise")
+    assert "k_step_dw_t" in conv.kernel_name
+    got, ref = [], []
+    for phase in ("chunk", "step", "chunk"):
+        clip = _clip(rng, B, C, 7, H, W)
+        frames = [np_of(clip[:, :, t]) for t in range(7)]
+        if phase == "chunk":
+            ys, mask = conv.forward_steps(clip)
+            got += [np_of(ys[:, :, i]) for i in range(ys.shape[2])]
+        else:
+            import paper_2204_03418_b200 as co
+            for t in range(7):
+                y = conv.forward_step(co.channels_last(clip[:, :, t]))
+                if y is not None:
+                    got.append(np_of(y))
+        for f in frames:
+            r = sm.forward_step(f)
+            if r is not None:
+                ref.append(r)
+    assert len(got) == len(ref) == 21 - (kt - 1)
+    assert rel_err(np.stack(got), np.stack(ref).reshape(np.stack(got).shape)) <= 1e-4
