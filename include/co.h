@@ -242,6 +242,40 @@ int co_stack_steps_host(co_stack* st, const void* x_host, int64_t T, void* y_hos
 int co_stack_delay(const co_stack* st, int64_t* d_nn);
 int co_stack_clean(co_stack* st, co_stream stream);
 
+/* ---- continual single-output multi-head attention -------- */
+
+/* co.MultiheadAttention in "single-output" mode (SPEC.md:
+ * 357-403) over n_streams lockstep streams: each step projects x_t (B, E) to
+ * q, k, v, pushes (k, v) into a ring of `window` = n entries and, once n
+ * entries are present (delay d = n - 1, stride 1; no early partial windows,
+ * S:392), emits the attention of the newest query against the n keys / values
+ * (per head softmax(q k^T / sqrt(E / heads)) v, heads concatenated) projected
+ * by W_o -- the last column of batch attention over the trailing n steps.
+ * Weights in PyTorch's nn.MultiheadAttention layout: w_qkv (3E, E) = [W_q; W_k;
+ * W_v], w_o (E, E), bf16; biases fp32 (3E) / (E), may be NULL; host pointers
+ * unless weights_on_device.  x, y bf16 (y fp32 if out_dtype = CO_F32).  Head
+ * dims 32, 64 or 128.  Canonical state: the last n-1 keys and values,
+ * (n-1, 2, B, E) bf16 (k then v per slot, oldest first). */
+typedef struct {
+  int32_t embed_dim, num_heads, window;
+  int64_t n_streams;
+  int32_t out_dtype;                     /* co_dtype of y */
+} co_mha_desc;
+typedef struct co_mha co_mha;
+int co_mha_create(const co_mha_desc* d, const void* w_qkv, const float* b_qkv, const void* w_o, const float* b_o,
+                  int weights_on_device, co_mha** out);
+int co_mha_destroy(co_mha* m);
+int co_mha_step(co_mha* m, const void* x, void* y, int update_state, int* ready, co_stream stream);
+/* Batch mode: x (B, T, E) -> y (B, T, E), full attention over the T columns
+ * (T == window for the paper's fixed-window form; any T >= 1 accepted).
+ * Neither reads nor writes state; stream-ordered temporaries. */
+int co_mha_forward(co_mha* m, const void* x, int64_t T, void* y, co_stream stream);
+int co_mha_clean(co_mha* m, co_stream stream);
+int co_mha_delay(const co_mha* m, int64_t* delay);
+int co_mha_state_bytes(const co_mha* m, size_t* bytes);
+int co_mha_state_get(co_mha* m, void* dst, size_t bytes, int64_t* n, co_stream stream);
+int co_mha_state_set(co_mha* m, const void* src, size_t bytes, int64_t n, co_stream stream);
+
 /* ---- per-stream clocks --------- */
 
 /* Streams join and leave independently.  A handle keeps one clock n (A19,

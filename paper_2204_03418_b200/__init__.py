@@ -21,9 +21,9 @@ from typing import Optional, Sequence, Tuple
 import torch
 
 from . import _abi
-from ._abi import CoConvDesc, CoInfo, check, lib
+from ._abi import CoConvDesc, CoInfo, CoMhaDesc, check, lib
 
-__all__ = ["Conv", "Delay", "Pool", "Residual", "Stack", "channels_last", "is_channels_last", "load"]
+__all__ = ["Conv", "Delay", "MultiheadAttention", "Pool", "Residual", "Stack", "channels_last", "is_channels_last", "load"]
 
 _DT = {torch.float32: _abi.CO_F32, torch.bfloat16: _abi.CO_BF16}
 
@@ -409,6 +409,89 @@ class Residual:
 
     def clean_state(self, stream=None):
         check(lib().co_residual_clean(self._h, _stream(stream)))
+
+
+class MultiheadAttention:
+    """``co.MultiheadAttention`` in "single-output" mode (PAPER.md P:430-432;
+    SPEC.md:357-403) over ``n_streams`` lockstep streams: a step takes x (B, E)
+    and, once ``window`` steps are buffered (delay window-1), returns the
+    attention of the newest query against the window's keys / values, projected
+    by W_o.  Weights in nn.MultiheadAttention's layout (``in_proj_weight``
+    (3E, E), ``in_proj_bias``, ``out_proj.weight``, ``out_proj.bias``)."""
+
+    def __init__(self, embed_dim: int, num_heads: int, window: int, *, in_proj_weight: torch.Tensor,
+                 out_proj_weight: torch.Tensor, in_proj_bias: Optional[torch.Tensor] = None,
+                 out_proj_bias: Optional[torch.Tensor] = None, n_streams: int = 1,
+                 out_dtype: torch.dtype = torch.bfloat16, device="cuda"):
+        self.E, self.heads, self.window, self.n_streams = embed_dim, num_heads, window, n_streams
+        self.out_dtype, self.device = out_dtype, torch.device(device)
+        d = CoMhaDesc()
+        d.embed_dim, d.num_heads, d.window, d.n_streams = embed_dim, num_heads, window, n_streams
+        d.out_dtype = _DT[out_dtype]
+        wq = in_proj_weight.detach().to(torch.bfloat16).contiguous().to(self.device)
+        wo = out_proj_weight.detach().to(torch.bfloat16).contiguous().to(self.device)
+        bq = None if in_proj_bias is None else in_proj_bias.detach().float().contiguous().to(self.device)
+        bo = None if out_proj_bias is None else out_proj_bias.detach().float().contiguous().to(self.device)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            check(lib().co_mha_create(C.byref(d), C.c_void_p(wq.data_ptr()),
+                                      C.c_void_p(bq.data_ptr()) if bq is not None else None, C.c_void_p(wo.data_ptr()),
+                                      C.c_void_p(bo.data_ptr()) if bo is not None else None, 1, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().co_mha_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def delay(self) -> int:
+        d = C.c_int64()
+        check(lib().co_mha_delay(self._h, C.byref(d)))
+        return d.value
+
+    def forward_step(self, x: torch.Tensor, update_state: bool = True, out: Optional[torch.Tensor] = None,
+                     stream=None) -> Optional[torch.Tensor]:
+        """x (B, E) bf16 -> (B, E) or None (Empty)."""
+        if tuple(x.shape) != (self.n_streams, self.E) or x.dtype != torch.bfloat16 or not x.is_contiguous():
+            raise ValueError(f"x must be a contiguous bf16 ({self.n_streams}, {self.E}) CUDA tensor")
+        y = out if out is not None else torch.empty((self.n_streams, self.E), dtype=self.out_dtype, device=self.device)
+        r = C.c_int()
+        check(lib().co_mha_step(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), int(update_state),
+                                C.byref(r), _stream(stream)))
+        return y if r.value else None
+
+    def forward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        """Batch mode: x (B, E, T) -> (B, E, T), full attention over the T columns."""
+        B, E, T = x.shape
+        xt = x.transpose(1, 2).contiguous().to(torch.bfloat16)           # (B, T, E)
+        y = torch.empty((B, T, E), dtype=self.out_dtype, device=self.device)
+        check(lib().co_mha_forward(self._h, C.c_void_p(xt.data_ptr()), T, C.c_void_p(y.data_ptr()), _stream(stream)))
+        return y.transpose(1, 2)
+
+    def clean_state(self, stream=None):
+        check(lib().co_mha_clean(self._h, _stream(stream)))
+
+    def state_dict_stream(self, stream=None):
+        """(state (window-1, 2, B, E) bf16: keys then values, oldest first; n)."""
+        nb = C.c_size_t()
+        check(lib().co_mha_state_bytes(self._h, C.byref(nb)))
+        st = torch.empty((self.window - 1, 2, self.n_streams, self.E), dtype=torch.bfloat16, device=self.device)
+        n = C.c_int64()
+        check(lib().co_mha_state_get(self._h, C.c_void_p(st.data_ptr()) if st.numel() else None, nb.value,
+                                     C.byref(n), _stream(stream)))
+        return st, n.value
+
+    def load_state_stream(self, state: torch.Tensor, n: int, stream=None):
+        nb = C.c_size_t()
+        check(lib().co_mha_state_bytes(self._h, C.byref(nb)))
+        state = state.to(torch.bfloat16).contiguous()
+        check(lib().co_mha_state_set(self._h, C.c_void_p(state.data_ptr()) if state.numel() else None, nb.value,
+                                     n, _stream(stream)))
 
 
 class Stack:

@@ -32,8 +32,14 @@ EXPORTS = ["co_conv_create", "co_conv_destroy", "co_conv_info", "co_delay", "co_
            "co_forward", "co_forward_out_len", "co_state_bytes", "co_state_get", "co_state_set",
            "co_state_clean", "co_stack_create", "co_stack_destroy", "co_stack_step", "co_stack_step_host", "co_stack_steps_host", "co_stack_delay",
            "co_stack_clean", "co_state_clean_streams", "co_stream_ready", "co_stack_clean_streams",
-           "co_stack_stream_ready", "co_residual_create", "co_residual_destroy", "co_residual_step", "co_residual_forward",
+           "co_stack_stream_ready", "co_mha_create", "co_mha_destroy", "co_mha_step", "co_mha_forward", "co_mha_clean",
+           "co_mha_delay", "co_mha_state_bytes", "co_mha_state_get", "co_mha_state_set", "co_residual_create", "co_residual_destroy", "co_residual_step", "co_residual_forward",
            "co_residual_clean", "co_residual_delay", "co_last_error", "co_abi_version"]
+
+
+class CoMhaDesc(C.Structure):
+    _fields_ = [("embed_dim", C.c_int32), ("num_heads", C.c_int32), ("window", C.c_int32),
+                ("n_streams", C.c_int64), ("out_dtype", C.c_int32)]
 
 
 class CoConvDesc(C.Structure):
@@ -98,6 +104,15 @@ def lib():
             L.co_stream_ready.argtypes = [vp, C.POINTER(C.c_uint8)]
             L.co_stack_clean_streams.argtypes = [vp, C.POINTER(C.c_uint8), vp]
             L.co_stack_stream_ready.argtypes = [vp, C.POINTER(C.c_uint8)]
+            L.co_mha_create.argtypes = [C.POINTER(CoMhaDesc), vp, vp, vp, vp, C.c_int, C.POINTER(vp)]
+            L.co_mha_destroy.argtypes = [vp]
+            L.co_mha_step.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_int), vp]
+            L.co_mha_forward.argtypes = [vp, vp, C.c_int64, vp, vp]
+            L.co_mha_clean.argtypes = [vp, vp]
+            L.co_mha_delay.argtypes = [vp, i64p]
+            L.co_mha_state_bytes.argtypes = [vp, C.POINTER(C.c_size_t)]
+            L.co_mha_state_get.argtypes = [vp, vp, C.c_size_t, i64p, vp]
+            L.co_mha_state_set.argtypes = [vp, vp, C.c_size_t, C.c_int64, vp]
             L.co_residual_create.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
             L.co_residual_destroy.argtypes = [vp]
             L.co_residual_step.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_int), vp]

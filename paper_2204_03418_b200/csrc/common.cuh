@@ -129,6 +129,22 @@ cudaError_t launch_clean_streams_psum(const Geom& g, float* state, const int64_t
 cudaError_t launch_fill_streams(void* ring, int esz, int64_t slots, int64_t B, int64_t per, const int64_t* ids, int nm,
                                 uint32_t value, cudaStream_t s);
 
+// Continual single-output MHA (k_mha.cu)
+struct MhaArgs {
+  const __nv_bfloat16* qkv;   // step: (B, 3E); batch: (B, T, 3E)
+  __nv_bfloat16* kring;       // [B][n][E] (step mode)
+  __nv_bfloat16* vring;
+  __nv_bfloat16* out;         // step: (B, E); batch: (B, T, E)
+  int64_t B, T;               // T: batch columns (batch mode), 1 in step mode
+  int E, heads, n;            // n = window
+  int64_t m;                  // step: index of this step (ring slot m mod n)
+  int store;                  // step: write (k_t, v_t) into the ring
+  int batch;                  // 1: keys / values from qkv over all T columns
+  float scale_log2e;          // log2(e) / sqrt(dh)
+};
+bool mha_supported(int E, int heads);
+cudaError_t launch_mha_attend(const MhaArgs& a, cudaStream_t s);
+
 // Residual composite merge (k_compose.cu): y[r, :n] <- act(y[r, :n] + x[r, :n]) over rows.
 cudaError_t launch_residual_add(int y_dtype, void* y, int64_t y_rstride, int x_dtype, const void* x,
                                 int64_t x_rstride, int64_t rows, int64_t n, int act, cudaStream_t s);

@@ -1150,3 +1150,194 @@ extern "C" int co_stack_stream_ready(const co_stack* st, uint8_t* ready) {
       for (size_t b = 0; b < p.size(); ++b) ready[b] &= p[b] ? 0 : 1;
   return CO_OK;
 }
+
+// ----------------------------------------------------------------- continual MHA
+// co.MultiheadAttention "single-output" (k_mha.cu): two kt = 1
+// layers (the input projection E -> 3E and the output projection E -> E, RAW
+// layout so the tensor-core K loop runs over 128 flattened stream rows) around
+// the attention kernel, and a (k, v) ring of `window` slots.
+
+struct co_mha {
+  co_mha_desc d{};
+  co_conv* in_proj = nullptr;
+  co_conv* out_proj = nullptr;
+  void* qkv = nullptr;       // (B, 3E) bf16
+  void* att = nullptr;       // (B, E) bf16
+  void* kring = nullptr;     // [n][B][E] bf16
+  void* vring = nullptr;
+  int64_t n = 0;
+};
+
+static co_conv_desc linear_desc(int64_t B, int cin, int cout, int out_dtype) {
+  co_conv_desc c{};
+  c.spatial_rank = 0;
+  c.in_channels = cin; c.out_channels = cout; c.groups = 1;
+  for (int a = 0; a < 3; ++a) { c.kernel[a] = 1; c.stride[a] = 1; c.padding[a] = 0; c.dilation[a] = 1; }
+  c.in_spatial[0] = c.in_spatial[1] = 1;
+  c.n_streams = B;
+  c.in_dtype = c.w_dtype = CO_BF16;
+  c.out_dtype = out_dtype;
+  c.activation = CO_ACT_NONE;
+  c.kernel_choice = CO_KERNEL_AUTO;
+  c.state_layout = CO_STATE_RAW;
+  c.op = CO_OP_CONV;
+  return c;
+}
+
+extern "C" int co_mha_create(const co_mha_desc* d, const void* w_qkv, const float* b_qkv, const void* w_o,
+                             const float* b_o, int weights_on_device, co_mha** out) {
+  if (!d || !w_qkv || !w_o || !out) return fail(CO_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (d->embed_dim < 1 || d->window < 1 || d->n_streams < 1) return fail(CO_ERR_ARG, "bad mha descriptor");
+  if (!co::mha_supported(d->embed_dim, d->num_heads))
+    return fail(CO_ERR_UNSUPPORTED, "mha: head dim E/heads must be 32, 64 or 128");
+  if (d->out_dtype != CO_BF16 && d->out_dtype != CO_F32) return fail(CO_ERR_ARG, "bad out_dtype");
+  co_mha* m = new (std::nothrow) co_mha();
+  if (!m) return fail(CO_ERR_OOM, "host allocation");
+  m->d = *d;
+  const int64_t B = d->n_streams, E = d->embed_dim;
+  co_conv_desc ci = linear_desc(B, int(E), int(3 * E), CO_BF16), co_ = linear_desc(B, int(E), int(E), d->out_dtype);
+  if (int rc = co_conv_create(&ci, w_qkv, b_qkv, weights_on_device, &m->in_proj)) { co_mha_destroy(m); return rc; }
+  if (int rc = co_conv_create(&co_, w_o, b_o, weights_on_device, &m->out_proj)) { co_mha_destroy(m); return rc; }
+  const size_t fb = size_t(B) * E * 2;
+  cudaError_t e = cudaMalloc(&m->qkv, 3 * fb);
+  if (e == cudaSuccess) e = cudaMalloc(&m->att, fb);
+  if (e == cudaSuccess) e = cudaMalloc(&m->kring, size_t(d->window) * fb);
+  if (e == cudaSuccess) e = cudaMalloc(&m->vring, size_t(d->window) * fb);
+  if (e == cudaSuccess) e = cudaMemset(m->kring, 0, size_t(d->window) * fb);
+  if (e == cudaSuccess) e = cudaMemset(m->vring, 0, size_t(d->window) * fb);
+  if (e != cudaSuccess) { co_mha_destroy(m); return fail(CO_ERR_OOM, "mha buffers: %s", cudaGetErrorString(e)); }
+  *out = m;
+  return CO_OK;
+}
+
+extern "C" int co_mha_destroy(co_mha* m) {
+  if (!m) return CO_OK;
+  co_conv_destroy(m->in_proj);
+  co_conv_destroy(m->out_proj);
+  cudaFree(m->qkv); cudaFree(m->att); cudaFree(m->kring); cudaFree(m->vring);
+  delete m;
+  return CO_OK;
+}
+
+static co::MhaArgs mha_args(const co_mha* m) {
+  co::MhaArgs a{};
+  a.E = m->d.embed_dim; a.heads = m->d.num_heads; a.n = m->d.window;
+  a.B = m->d.n_streams; a.T = 1;
+  a.scale_log2e = 1.4426950408889634f / sqrtf(float(a.E / a.heads));
+  return a;
+}
+
+extern "C" int co_mha_step(co_mha* m, const void* x, void* y, int update_state, int* ready, co_stream stream) {
+  if (!m || !x || !y) return fail(CO_ERR_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t B = m->d.n_streams, E = m->d.embed_dim;
+  int r0 = 0;
+  if (int rc = co_forward_step(m->in_proj, x, m->qkv, 1, &r0, stream)) return rc;   // kt = 1: always Ready
+  const int r = m->n >= m->d.window - 1;
+  if (r) {
+    co::MhaArgs a = mha_args(m);
+    a.qkv = static_cast<const __nv_bfloat16*>(m->qkv);
+    a.kring = static_cast<__nv_bfloat16*>(m->kring);
+    a.vring = static_cast<__nv_bfloat16*>(m->vring);
+    a.out = static_cast<__nv_bfloat16*>(m->att);
+    a.m = m->n; a.store = update_state ? 1 : 0;
+    CO_CUDA(co::launch_mha_attend(a, s));
+    int r1 = 0;
+    if (int rc = co_forward_step(m->out_proj, m->att, y, 1, &r1, stream)) return rc;
+  } else if (update_state) {   // not Ready: only the ring update (strided copies of k and v)
+    const size_t slot = size_t(m->n % m->d.window);
+    const size_t row = size_t(E) * 2, pitch = row * m->d.window;   // ring [B][n][E]
+    char* qkv = static_cast<char*>(m->qkv);
+    CO_CUDA(cudaMemcpy2DAsync(static_cast<char*>(m->kring) + slot * row, pitch, qkv + row, 3 * row, row, B,
+                              cudaMemcpyDeviceToDevice, s));
+    CO_CUDA(cudaMemcpy2DAsync(static_cast<char*>(m->vring) + slot * row, pitch, qkv + 2 * row, 3 * row, row, B,
+                              cudaMemcpyDeviceToDevice, s));
+  }
+  if (update_state) ++m->n;
+  if (ready) *ready = r;
+  return CO_OK;
+}
+
+extern "C" int co_mha_forward(co_mha* m, const void* x, int64_t T, void* y, co_stream stream) {
+  if (!m || !x || !y || T < 1) return fail(CO_ERR_ARG, "bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t B = m->d.n_streams, E = m->d.embed_dim;
+  void *qkv = nullptr, *att = nullptr;
+  CO_CUDA(cudaMallocAsync(&qkv, size_t(B) * T * 3 * E * 2, s));
+  cudaError_t e = cudaMallocAsync(&att, size_t(B) * T * E * 2, s);
+  int64_t To = 0;
+  int rc = CO_OK;
+  if (e != cudaSuccess) rc = fail(CO_ERR_OOM, "%s", cudaGetErrorString(e));
+  if (!rc) rc = co_forward(m->in_proj, x, T, qkv, &To, stream);
+  if (!rc) {
+    co::MhaArgs a = mha_args(m);
+    a.qkv = static_cast<const __nv_bfloat16*>(qkv);
+    a.out = static_cast<__nv_bfloat16*>(att);
+    a.T = T; a.batch = 1;
+    e = co::launch_mha_attend(a, s);
+    if (e != cudaSuccess) rc = fail(CO_ERR_CUDA, "mha attend: %s", cudaGetErrorString(e));
+  }
+  if (!rc) rc = co_forward(m->out_proj, att, T, y, &To, stream);
+  cudaFreeAsync(qkv, s);
+  if (att) cudaFreeAsync(att, s);
+  return rc;
+}
+
+extern "C" int co_mha_clean(co_mha* m, co_stream stream) {
+  if (!m) return fail(CO_ERR_ARG, "null mha");
+  const size_t fb = size_t(m->d.n_streams) * m->d.embed_dim * 2 * m->d.window;
+  CO_CUDA(cudaMemsetAsync(m->kring, 0, fb, (cudaStream_t)stream));
+  CO_CUDA(cudaMemsetAsync(m->vring, 0, fb, (cudaStream_t)stream));
+  m->n = 0;
+  return CO_OK;
+}
+
+extern "C" int co_mha_delay(const co_mha* m, int64_t* delay) {
+  if (!m || !delay) return fail(CO_ERR_ARG, "null argument");
+  *delay = m->d.window - 1;
+  return CO_OK;
+}
+
+extern "C" int co_mha_state_bytes(const co_mha* m, size_t* bytes) {
+  if (!m || !bytes) return fail(CO_ERR_ARG, "null argument");
+  *bytes = size_t(m->d.window - 1) * 2 * m->d.n_streams * m->d.embed_dim * 2;
+  return CO_OK;
+}
+
+// canonical slot j (oldest first) = step n - (n-1) + j, i.e. ring slot (n - (n_win-1) + j) mod n_win
+extern "C" int co_mha_state_get(co_mha* m, void* dst, size_t bytes, int64_t* n, co_stream stream) {
+  size_t need = 0;
+  if (int rc = co_mha_state_bytes(m, &need)) return rc;
+  if (bytes != need) return fail(CO_ERR_SHAPE, "state bytes %zu != %zu", bytes, need);
+  const int W = m->d.window;
+  const size_t row = size_t(m->d.embed_dim) * 2, fb = size_t(m->d.n_streams) * row, pitch = row * W;
+  for (int j = 0; j < W - 1; ++j) {   // ring [B][n][E] -> canonical (n-1, 2, B, E)
+    const size_t slot = size_t(floor_mod(m->n - (W - 1) + j, W));
+    char* o = static_cast<char*>(dst) + size_t(j) * 2 * fb;
+    CO_CUDA(cudaMemcpy2DAsync(o, row, static_cast<char*>(m->kring) + slot * row, pitch, row, m->d.n_streams,
+                              cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    CO_CUDA(cudaMemcpy2DAsync(o + fb, row, static_cast<char*>(m->vring) + slot * row, pitch, row, m->d.n_streams,
+                              cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  }
+  if (n) *n = m->n;
+  return CO_OK;
+}
+
+extern "C" int co_mha_state_set(co_mha* m, const void* src, size_t bytes, int64_t n, co_stream stream) {
+  size_t need = 0;
+  if (int rc = co_mha_state_bytes(m, &need)) return rc;
+  if (bytes != need || n < 0) return fail(CO_ERR_SHAPE, "state bytes %zu != %zu", bytes, need);
+  const int W = m->d.window;
+  const size_t row = size_t(m->d.embed_dim) * 2, fb = size_t(m->d.n_streams) * row, pitch = row * W;
+  for (int j = 0; j < W - 1; ++j) {
+    const size_t slot = size_t(floor_mod(n - (W - 1) + j, W));
+    const char* i = static_cast<const char*>(src) + size_t(j) * 2 * fb;
+    CO_CUDA(cudaMemcpy2DAsync(static_cast<char*>(m->kring) + slot * row, pitch, i, row, row, m->d.n_streams,
+                              cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    CO_CUDA(cudaMemcpy2DAsync(static_cast<char*>(m->vring) + slot * row, pitch, i + fb, row, row, m->d.n_streams,
+                              cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  }
+  m->n = n;
+  return CO_OK;
+}

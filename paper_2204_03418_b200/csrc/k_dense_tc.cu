@@ -794,7 +794,9 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
     for (const Variant& v : kVariants) {
       if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.CS != 1 || v.PAIR != pair) continue;
       if (eg_pin && v.EG != eg_pin) continue;
-      // prefer the widest N (fewest A re-reads), then more groups
+      // prefer the widest N (fewest A re-reads), then more groups; narrower
+      // parts do not help few-row GEMMs (measured on the MHA projections: the
+      // K pipeline's latency per item, not the SM count, bounds them)
       auto rank = [](const Variant* x) { return x->CC * 1000 + x->EG; };
       if (!best || rank(&v) > rank(best)) best = &v;
     }

@@ -1,0 +1,80 @@
+"""GPU parity of the continual single-output MHA (include/co.h
+co_mha_*) against the fp64 oracle (oracle/mha.py): readiness (d = window-1),
+step outputs = the last column of attention over the trailing window, batch
+mode, update_state = 0 purity, state get/set round trip and clean state; head
+dims 32 / 64 / 128 and windows 1..64.  The path keeps q/k/v and the attention
+output in bf16 between its three launches, so outputs are held to the bf16
+bar, 2e-2 of the RMS (A16)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import mha as OM
+from tests.helpers import np_of, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _bf16(a):
+    return torch.from_numpy(np.asarray(a, np.float64)).to(torch.bfloat16).double().numpy()
+
+
+def _make(E, heads, window, B, rng, out_dtype=torch.float32):
+    import paper_2204_03418_b200 as co
+    p = {"heads": heads}
+    for n in ("Wq", "Wk", "Wv", "Wo"):
+        p[n] = _bf16(rng.standard_normal((E, E)) / np.sqrt(E))
+    for n in ("bq", "bk", "bv", "bo"):
+        p[n] = torch.from_numpy(rng.standard_normal(E) * 0.1).float().double().numpy()
+    m = co.MultiheadAttention(E, heads, window, n_streams=B, out_dtype=out_dtype,
+                              in_proj_weight=torch.from_numpy(np.concatenate([p["Wq"], p["Wk"], p["Wv"]])),
+                              in_proj_bias=torch.from_numpy(np.concatenate([p["bq"], p["bk"], p["bv"]])),
+                              out_proj_weight=torch.from_numpy(p["Wo"]), out_proj_bias=torch.from_numpy(p["bo"]))
+    return m, OM.MhaStep(p, window, B), p
+
+
+@pytest.mark.parametrize("E,heads,window,B", [(64, 2, 1, 3), (128, 4, 3, 5), (256, 4, 8, 130), (512, 4, 16, 7),
+                                              (256, 2, 64, 3), (1024, 16, 24, 2)])
+def test_mha_steps_vs_oracle(E, heads, window, B):
+    rng = np.random.default_rng(E + window)
+    m, sm, _ = _make(E, heads, window, B, rng)
+    assert m.delay == window - 1
+    for t in range(window + 5):
+        x = _bf16(rng.standard_normal((B, E)))
+        y = m.forward_step(torch.from_numpy(x).to(torch.bfloat16).cuda())
+        r = sm.forward_step(x)
+        assert (y is None) == (r is None), t
+        if y is not None:
+            assert rel_err(np_of(y), r) <= 2e-2, t
+
+
+def test_mha_batch_update_state_and_state_round_trip():
+    rng = np.random.default_rng(5)
+    E, heads, window, B = 128, 2, 6, 4
+    m, sm, p = _make(E, heads, window, B, rng)
+    xs = [_bf16(rng.standard_normal((B, E))) for _ in range(14)]
+    for t, x in enumerate(xs):
+        if t == 9:
+            probe = _bf16(rng.standard_normal((B, E)))
+            yp = m.forward_step(torch.from_numpy(probe).to(torch.bfloat16).cuda(), update_state=False)
+            assert rel_err(np_of(yp), sm.forward_step(probe, update_state=False)) <= 2e-2
+            st, n = m.state_dict_stream()
+            assert n == 9 and tuple(st.shape) == (window - 1, 2, B, E)
+            m2, _, _ = _make(E, heads, window, B, np.random.default_rng(5))
+            m2.load_state_stream(st, n)
+        y = m.forward_step(torch.from_numpy(x).to(torch.bfloat16).cuda())
+        r = sm.forward_step(x)
+        if t >= 9:
+            y2 = m2.forward_step(torch.from_numpy(x).to(torch.bfloat16).cuda())
+            assert torch.equal(y, y2)
+        if y is not None:
+            assert rel_err(np_of(y), r) <= 2e-2
+    # batch mode over one window (T = n)
+    clip = np.stack(xs[:window], axis=2)
+    yb = m.forward(torch.from_numpy(clip).cuda())
+    assert rel_err(np_of(yb), OM.mha_forward(p, clip)) <= 2e-2
+    m.clean_state()
+    for t in range(window):
+        y = m.forward_step(torch.from_numpy(xs[t]).to(torch.bfloat16).cuda())
+        assert (y is None) == (t < window - 1)
+    assert rel_err(np_of(y), OM.mha_forward(p, clip)[:, :, -1]) <= 2e-2
