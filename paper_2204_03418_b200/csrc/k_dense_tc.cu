@@ -647,6 +647,7 @@ const Variant kVariants[] = {
     CO_TC_VARIANT(2, 32, 4, 32), CO_TC_VARIANT(2, 64, 2, 32), CO_TC_VARIANT(3, 16, 4, 16),
     CO_TC_VARIANT(3, 32, 2, 32), CO_TC_VARIANT(3, 32, 3, 32), CO_TC_VARIANT(3, 32, 4, 32),
     CO_TC_VARIANT(3, 64, 2, 32), CO_TC_VARIANT(5, 16, 4, 16), CO_TC_VARIANT(5, 32, 2, 16),
+    CO_TC_VARIANT(5, 32, 3, 16),
     CO_TC_VARIANT(9, 16, 2, 16),
 };
 
