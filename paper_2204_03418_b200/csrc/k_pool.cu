@@ -98,6 +98,34 @@ __device__ __forceinline__ void spatial_reduce(const Geom& g, const Tin* __restr
   }
 }
 
+// Compile-time KH x KW window (dilation 1): every tap's load is issued before
+// any is combined (predicated, no per-tap branch), so a thread has KH*KW
+// 16-byte loads in flight -- the runtime-bounds loop above issues them one at a
+// time.  Same tap order, so the same results bit for bit.
+template <typename Tin, int V, bool MAX, int KH, int KW>
+__device__ __forceinline__ void spatial_reduce_fixed(const Geom& g, const Tin* __restrict__ fb, int ho, int wo,
+                                                     int c0, float (&s)[V]) {
+  const int h0 = ho * g.sh - g.ph, w0 = wo * g.sw - g.pw;
+  Vec<Tin, V> x[KH * KW];
+  bool ok[KH * KW];
+#pragma unroll
+  for (int u = 0; u < KH; ++u)
+#pragma unroll
+    for (int v = 0; v < KW; ++v) {
+      const int hi = h0 + u, wi = w0 + v;
+      ok[u * KW + v] = hi >= 0 && hi < g.H && wi >= 0 && wi < g.W;
+      if (ok[u * KW + v]) x[u * KW + v] = *reinterpret_cast<const Vec<Tin, V>*>(fb + (int64_t(hi) * g.W + wi) * g.Cin + c0);
+    }
+#pragma unroll
+  for (int j = 0; j < V; ++j) s[j] = MAX ? -INFINITY : 0.f;
+#pragma unroll
+  for (int t = 0; t < KH * KW; ++t) {
+    if (!ok[t]) continue;
+#pragma unroll
+    for (int j = 0; j < V; ++j) s[j] = MAX ? fmaxf(s[j], to_f(x[t].v[j])) : s[j] + to_f(x[t].v[j]);
+  }
+}
+
 template <int V, bool MAX>
 __device__ __forceinline__ void combine(float (&acc)[V], const float (&s)[V]) {
 #pragma unroll
@@ -299,8 +327,8 @@ __global__ void k_pool_rebuild(Geom g, Tr* __restrict__ st, int64_t m_next) {
 // Step: reduce the new frame spatially (x == NULL: a padding frame), then the
 // temporal part (temporal_step).  Ring layout [slot][B][Ho][Wo][C] in Tr (input
 // dtype for MAX, fp32 for AVG).
-template <typename Tin, typename Tout, typename Tr, int V, bool MAX, int CH, bool VH>
-__global__ void __launch_bounds__(256, CH == 1 ? 4 : 2) k_step_pool(Geom g, StepArgs a) {
+template <typename Tin, typename Tout, typename Tr, int V, bool MAX, int CH, bool VH, int KHW = 0>
+__global__ void __launch_bounds__(256, (CH == 1 && KHW == 0) ? 4 : 2) k_step_pool(Geom g, StepArgs a) {
   const int CV = g.Cin / V;
   const int64_t total = g.B * g.HWo * CV;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -315,7 +343,10 @@ __global__ void __launch_bounds__(256, CH == 1 ? 4 : 2) k_step_pool(Geom g, Step
     const int ho = p / g.Wo, wo = p - (p / g.Wo) * g.Wo;
     float s[V], win[V];
     if (x) {
-      spatial_reduce<Tin, V, MAX, CH>(g, x + b * a.x_bstride, ho, wo, c0, s);
+      if constexpr (KHW > 0)
+        spatial_reduce_fixed<Tin, V, MAX, KHW / 10, KHW % 10>(g, x + b * a.x_bstride, ho, wo, c0, s);
+      else
+        spatial_reduce<Tin, V, MAX, CH>(g, x + b * a.x_bstride, ho, wo, c0, s);
     } else {
 #pragma unroll
       for (int j = 0; j < V; ++j) s[j] = MAX ? -INFINITY : 0.f;
@@ -498,7 +529,11 @@ cudaError_t step_v(const Geom& g, const StepArgs& a, cudaStream_t s) {
                      : step_split<Tin, Tout, Tr, V, MAX, false>(g, a, g.pool_G, s);
   const int64_t total = g.B * g.HWo * (g.Cin / V);
   const int grid = grid_for(total);
+  const int khw = (g.dh == 1 && g.dw == 1 && g.kh <= 3 && g.kw <= 3 && g.kh == g.kw) ? g.kh * 10 + g.kw : 0;
   if (g.pool_vh) k_step_pool<Tin, Tout, Tr, V, MAX, kChunk, true><<<grid, 256, 0, s>>>(g, a);
+  else if (khw == 33) k_step_pool<Tin, Tout, Tr, V, MAX, 1, false, 33><<<grid, 256, 0, s>>>(g, a);
+  else if (khw == 22) k_step_pool<Tin, Tout, Tr, V, MAX, 1, false, 22><<<grid, 256, 0, s>>>(g, a);
+  else if (khw == 11) k_step_pool<Tin, Tout, Tr, V, MAX, 1, false, 11><<<grid, 256, 0, s>>>(g, a);
   else if (deep_chunks(g, total)) k_step_pool<Tin, Tout, Tr, V, MAX, kChunk, false><<<grid, 256, 0, s>>>(g, a);
   else k_step_pool<Tin, Tout, Tr, V, MAX, 1, false><<<grid, 256, 0, s>>>(g, a);
   return cudaGetLastError();
