@@ -132,3 +132,57 @@ def residual_forward(descs: Sequence[O.Desc], Ws, biases, relu: Sequence[int], x
     T_out = cur.shape[2]
     y = cur + x[:, :, c:c + T_out].reshape(cur.shape)
     return np.maximum(y, 0.0) if relu_out else y
+
+
+class BroadcastReduceStep:
+    """BroadcastReduce(branches, reduce) in step mode (PAPER.md P:462-509,
+    Listing 3 "co.BroadcastReduce(conv, co.Delay(1))", Listing 4 reduce="concat";
+    Principle 7 P:280-288).  A branch is an ``oracle.Stack``
+    or None (identity).  Each branch with delay d_i < d_max is suffixed with
+    Delay(d_max - d_i) on its Ready outputs; the merge is Ready when every
+    aligned branch is (tick n >= d_max); reduce "sum" adds, "concat" stacks
+    channels in branch order.  Branches must keep the frame rate (stride 1)."""
+
+    def __init__(self, branches, delays, reduce: str = "sum"):
+        assert reduce in ("sum", "concat")
+        self.branches, self.reduce = list(branches), reduce
+        self.delays = [int(d) for d in delays]
+        self.delay = max(self.delays)
+        self.clean_state()
+
+    def clean_state(self):
+        for br in self.branches:
+            if br is not None:
+                br.clean_state()
+        self.n = 0
+        self.outs = [[] for _ in self.branches]       # each branch's Ready outputs, oldest first
+
+    def forward_step(self, x, update_state: bool = True):
+        x = np.asarray(x, np.float64)
+        aligned = []
+        for i, br in enumerate(self.branches):
+            y = x if br is None else br.forward_step(x, update_state)
+            hist = self.outs[i] + ([y] if y is not None else [])
+            k = self.delay - self.delays[i]              # the Delay(d_max - d_i) suffix
+            aligned.append(hist[-1 - k] if len(hist) > k and self.n >= self.delay else None)
+            if update_state:
+                self.outs[i] = hist[-(k + 1):] if y is not None else self.outs[i]
+        if update_state:
+            self.n += 1
+        if any(a is None for a in aligned):
+            return None
+        if self.reduce == "sum":
+            return sum(aligned[1:], aligned[0].copy())
+        return np.concatenate(aligned, axis=1)
+
+
+def broadcast_reduce_forward(branch_fns, x: np.ndarray, reduce: str = "sum") -> np.ndarray:
+    """Batch mode: every branch's batch output (a callable on the clip, or None =
+    identity), each truncated to the shortest branch length T_min keeping the
+    first T_min columns -- the columns the step mode's delay alignment pairs
+    (A24) -- then summed or concatenated over channels."""
+    x = np.asarray(x, np.float64)
+    ys = [x.copy() if f is None else f(x) for f in branch_fns]
+    T_min = min(y.shape[2] for y in ys)
+    ys = [y[:, :, :T_min] for y in ys]
+    return sum(ys[1:], ys[0].copy()) if reduce == "sum" else np.concatenate(ys, axis=1)

@@ -140,3 +140,61 @@ def test_construction_errors():
         OC.skip_delay([_conv_desc(2, 2, 0)], shrink=True)
     with pytest.raises(ValueError):      # no equal padding without shrink
         OC.skip_delay([_conv_desc(2, 3, 0)], shrink=False)
+
+
+def test_broadcast_reduce_conv_delay_equals_residual():
+    """Listing 3: BroadcastReduce(conv, Delay(1)) == Residual(conv)
+    for an equal-padding conv -- in step mode and batch mode."""
+    rng = np.random.default_rng(6)
+    d = _conv_desc(3, 3, 1)
+    W = rng.standard_normal(d.w_shape) / 5
+    b = rng.standard_normal(3) * 0.1
+    B, T = 2, 8
+    frames = [rng.standard_normal((B, 3, 5, 4)) for _ in range(T)]
+    conv = O.Stack([d], [W], [b], [0], [0], B)
+    br = OC.BroadcastReduceStep([conv, None], [1, 0], "sum")
+    res = OC.ResidualStep([d], [W], [b], [0], [0], B)
+    assert br.delay == res.delay == 1
+    for x in frames:
+        a, r = br.forward_step(x), res.forward_step(x)
+        assert (a is None) == (r is None)
+        if a is not None:
+            np.testing.assert_allclose(a, r, rtol=1e-13, atol=1e-13)
+    clip = np.stack(frames, axis=2)
+    yb = OC.broadcast_reduce_forward([lambda c: O.forward(d, W, b, c), None], clip)
+    np.testing.assert_allclose(yb, OC.residual_forward([d], [W], [b], [0], clip), rtol=1e-13, atol=1e-13)
+
+
+def test_broadcast_reduce_identities_scale_and_concat():
+    """All-identity branches with sum scale by the branch count; concat stacks
+    channels (SPEC.md:443, S:430)."""
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((2, 3, 4, 5))
+    s3 = OC.BroadcastReduceStep([None, None, None], [0, 0, 0], "sum")
+    np.testing.assert_array_equal(s3.forward_step(x), 3 * x)
+    cat = OC.BroadcastReduceStep([None, None], [0, 0], "concat")
+    np.testing.assert_array_equal(cat.forward_step(x), np.concatenate([x, x], axis=1))
+
+
+def test_broadcast_reduce_step_equals_batch_unpadded_branches():
+    """Branches of different receptive fields without padding: each Ready step
+    output equals the batch merge column with the same index (delay alignment,
+    A24); the composite delay is the maximum (Principle 7)."""
+    rng = np.random.default_rng(8)
+    d3, d5 = _conv_desc(2, 3, 0), _conv_desc(2, 5, 0)
+    W3, W5 = rng.standard_normal(d3.w_shape) / 4, rng.standard_normal(d5.w_shape) / 5
+    b3, b5 = rng.standard_normal(2) * 0.1, rng.standard_normal(2) * 0.1
+    B, T = 2, 11
+    frames = [rng.standard_normal((B, 2, 5, 4)) for _ in range(T)]
+    for reduce in ("sum", "concat"):
+        br = OC.BroadcastReduceStep([O.Stack([d3], [W3], [b3], [0], [0], B), O.Stack([d5], [W5], [b5], [0], [0], B),
+                                     None], [2, 4, 0], reduce)
+        assert br.delay == 4
+        outs = [br.forward_step(x) for x in frames]
+        assert all((o is None) == (t < 4) for t, o in enumerate(outs))
+        clip = np.stack(frames, axis=2)
+        yb = OC.broadcast_reduce_forward([lambda c: O.forward(d3, W3, b3, c), lambda c: O.forward(d5, W5, b5, c),
+                                          None], clip, reduce)
+        got = np.stack([o for o in outs if o is not None], axis=2)
+        assert got.shape == yb.shape
+        np.testing.assert_allclose(got, yb, rtol=1e-12, atol=1e-12)
