@@ -242,6 +242,33 @@ int co_stack_steps_host(co_stack* st, const void* x_host, int64_t T, void* y_hos
 int co_stack_delay(const co_stack* st, int64_t* d_nn);
 int co_stack_clean(co_stack* st, co_stream stream);
 
+/* ---- composition: BroadcastReduce ------------------------ */
+
+/* BroadcastReduce(branches, reduce) (Listing 3
+ * "co.BroadcastReduce(conv, co.Delay(1))", Listing 4 reduce="concat";
+ * Principle 7 P:280-288): the input step is broadcast to
+ * every branch -- a co_stack (owned by the caller, used by this composite only)
+ * or NULL for the identity -- and the branch outputs are merged.  Branches keep
+ * the frame rate (accumulated temporal stride 1) and share the output spatial
+ * shape; stack branches share the output dtype (the composite's); for SUM the
+ * channel count is common and an identity branch in another dtype is added
+ * with conversion; CONCAT needs one dtype.  A branch with delay d_i < d_max is suffixed with Delay(d_max - d_i)
+ * on its Ready outputs (a ring of d_max - d_i + 1 output frames), so the
+ * composite's delay is d_max and it is Ready when every aligned branch is.
+ * CONCAT stacks the channels in branch order.  Batch mode merges the first
+ * T_min output columns of every branch (the columns the delay alignment pairs;
+ * DESIGN.md A24). */
+typedef enum { CO_REDUCE_SUM = 0, CO_REDUCE_CONCAT = 1 } co_reduce;
+typedef struct co_parallel co_parallel;
+int co_parallel_create(co_stack* const* branches, int n_branches, int reduce, co_parallel** out);
+int co_parallel_destroy(co_parallel* p);               /* frees the composite, not the branch stacks */
+int co_parallel_step(co_parallel* p, const void* x, void* y, int update_state, int* ready, co_stream stream);
+int co_parallel_forward(co_parallel* p, const void* x, int64_t T, void* y, int64_t* T_out, co_stream stream);
+int co_parallel_clean(co_parallel* p, co_stream stream);
+int co_parallel_delay(const co_parallel* p, int64_t* delay);
+/* Output geometry: channels (sum: the common count; concat: the total). */
+int co_parallel_out_channels(const co_parallel* p, int32_t* channels);
+
 /* ---- continual single-output multi-head attention -------- */
 
 /* co.MultiheadAttention in "single-output" mode (SPEC.md:

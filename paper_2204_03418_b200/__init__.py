@@ -23,7 +23,7 @@ import torch
 from . import _abi
 from ._abi import CoConvDesc, CoInfo, CoMhaDesc, check, lib
 
-__all__ = ["Conv", "Delay", "MultiheadAttention", "Pool", "Residual", "Stack", "channels_last", "is_channels_last", "load"]
+__all__ = ["BroadcastReduce", "Conv", "Delay", "MultiheadAttention", "Pool", "Residual", "Stack", "channels_last", "is_channels_last", "load"]
 
 _DT = {torch.float32: _abi.CO_F32, torch.bfloat16: _abi.CO_BF16}
 
@@ -409,6 +409,73 @@ class Residual:
 
     def clean_state(self, stream=None):
         check(lib().co_residual_clean(self._h, _stream(stream)))
+
+
+class BroadcastReduce:
+    """``co.BroadcastReduce(*branches, reduce=...)`` (PAPER.md P:462-509,
+    Listing 3 / Listing 4): the step is broadcast to every
+    branch (a :class:`Stack`, or None for the identity), shorter-delay branches
+    are delayed to the longest (Principle 7), and the outputs are summed or
+    concatenated over channels.  The branch stacks are driven by the composite."""
+
+    def __init__(self, branches: Sequence[Optional["Stack"]], reduce: str = "sum"):
+        self.branches = list(branches)
+        arr = (C.c_void_p * len(self.branches))(*[(b._h.value if b is not None else None) for b in self.branches])
+        h = C.c_void_p()
+        check(lib().co_parallel_create(arr, len(self.branches), {"sum": 0, "concat": 1}[reduce], C.byref(h)))
+        self._h = h
+        first = next(b for b in self.branches if b is not None)
+        l0, ll = first.layers[0], first.layers[-1]
+        self.n_streams, self.in_channels, self.in_spatial, self.dtype = l0.n_streams, l0.in_channels, l0.in_spatial, l0.dtype
+        self.out_spatial, self.out_dtype, self.device = ll.out_spatial, ll.out_dtype, l0.device
+        c = C.c_int32()
+        check(lib().co_parallel_out_channels(self._h, C.byref(c)))
+        self.out_channels = c.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().co_parallel_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def delay(self) -> int:
+        d = C.c_int64()
+        check(lib().co_parallel_delay(self._h, C.byref(d)))
+        return d.value
+
+    def forward_step(self, x: torch.Tensor, update_state: bool = True, out: Optional[torch.Tensor] = None,
+                     stream=None) -> Optional[torch.Tensor]:
+        y = out if out is not None else _empty_cl((self.n_streams, self.out_channels) + self.out_spatial,
+                                                  self.out_dtype, self.device)
+        r = C.c_int()
+        check(lib().co_parallel_step(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), int(update_state),
+                                     C.byref(r), _stream(stream)))
+        return y if r.value else None
+
+    def forward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        T = x.shape[2]
+        T_min = T
+        for b in self.branches:
+            if b is None:
+                continue
+            t = T
+            for c in b.layers:
+                v = C.c_int64()
+                check(lib().co_forward_out_len(c._h, t, C.byref(v)))
+                t = v.value
+            T_min = min(T_min, t)
+        y = _empty_cl((self.n_streams, self.out_channels, T_min) + self.out_spatial, self.out_dtype, self.device)
+        To = C.c_int64()
+        check(lib().co_parallel_forward(self._h, C.c_void_p(x.data_ptr()), T, C.c_void_p(y.data_ptr()), C.byref(To),
+                                        _stream(stream)))
+        return y
+
+    def clean_state(self, stream=None):
+        check(lib().co_parallel_clean(self._h, _stream(stream)))
 
 
 class MultiheadAttention:

@@ -32,7 +32,8 @@ EXPORTS = ["co_conv_create", "co_conv_destroy", "co_conv_info", "co_delay", "co_
            "co_forward", "co_forward_out_len", "co_state_bytes", "co_state_get", "co_state_set",
            "co_state_clean", "co_stack_create", "co_stack_destroy", "co_stack_step", "co_stack_step_host", "co_stack_steps_host", "co_stack_delay",
            "co_stack_clean", "co_state_clean_streams", "co_stream_ready", "co_stack_clean_streams",
-           "co_stack_stream_ready", "co_mha_create", "co_mha_destroy", "co_mha_step", "co_mha_forward", "co_mha_clean",
+           "co_stack_stream_ready", "co_parallel_create", "co_parallel_destroy", "co_parallel_step",
+           "co_parallel_forward", "co_parallel_clean", "co_parallel_delay", "co_parallel_out_channels", "co_mha_create", "co_mha_destroy", "co_mha_step", "co_mha_forward", "co_mha_clean",
            "co_mha_delay", "co_mha_state_bytes", "co_mha_state_get", "co_mha_state_set", "co_residual_create", "co_residual_destroy", "co_residual_step", "co_residual_forward",
            "co_residual_clean", "co_residual_delay", "co_last_error", "co_abi_version"]
 
@@ -104,6 +105,13 @@ def lib():
             L.co_stream_ready.argtypes = [vp, C.POINTER(C.c_uint8)]
             L.co_stack_clean_streams.argtypes = [vp, C.POINTER(C.c_uint8), vp]
             L.co_stack_stream_ready.argtypes = [vp, C.POINTER(C.c_uint8)]
+            L.co_parallel_create.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.POINTER(vp)]
+            L.co_parallel_destroy.argtypes = [vp]
+            L.co_parallel_step.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_int), vp]
+            L.co_parallel_forward.argtypes = [vp, vp, C.c_int64, vp, i64p, vp]
+            L.co_parallel_clean.argtypes = [vp, vp]
+            L.co_parallel_delay.argtypes = [vp, i64p]
+            L.co_parallel_out_channels.argtypes = [vp, C.POINTER(C.c_int32)]
             L.co_mha_create.argtypes = [C.POINTER(CoMhaDesc), vp, vp, vp, vp, C.c_int, C.POINTER(vp)]
             L.co_mha_destroy.argtypes = [vp]
             L.co_mha_step.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_int), vp]

@@ -1015,16 +1015,16 @@ extern "C" int co_residual_step(co_residual* r, const void* x, void* y, int upda
   return CO_OK;
 }
 
-extern "C" int co_residual_forward(co_residual* r, const void* x, int64_t T, void* y, int64_t* T_out,
-                                   co_stream stream) {
-  if (!r || !x || !y) return fail(CO_ERR_ARG, "null argument");
+// Batch forward of a layer sequence (stream-ordered temporaries between layers).
+static int layers_forward(const std::vector<co_conv*>& layers, const void* x, int64_t T, void* y, int64_t* T_out,
+                          co_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const void* cur = x;
   int64_t Tc = T;
   void* tmp_prev = nullptr;
-  const int L = int(r->body.size());
+  const int L = int(layers.size());
   for (int l = 0; l < L; ++l) {
-    co_conv* h = r->body[l];
+    co_conv* h = layers[l];
     int64_t Tn = 0;
     co_forward_out_len(h, Tc, &Tn);
     if (Tn < 1) { if (tmp_prev) cudaFreeAsync(tmp_prev, s); return fail(CO_ERR_LENGTH, "residual: T' < 1 at layer %d", l); }
@@ -1042,6 +1042,26 @@ extern "C" int co_residual_forward(co_residual* r, const void* x, int64_t T, voi
     cur = dst;
     Tc = Tgot;
   }
+  if (T_out) *T_out = Tc;
+  return CO_OK;
+}
+
+// Output length of a layer sequence's batch forward.
+static int64_t layers_out_len(const std::vector<co_conv*>& layers, int64_t T) {
+  for (co_conv* h : layers) {
+    int64_t t = 0;
+    co_forward_out_len(h, T, &t);
+    T = t;
+  }
+  return T;
+}
+
+extern "C" int co_residual_forward(co_residual* r, const void* x, int64_t T, void* y, int64_t* T_out,
+                                   co_stream stream) {
+  if (!r || !x || !y) return fail(CO_ERR_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t Tc = 0;
+  if (int rc = layers_forward(r->body, x, T, y, &Tc, stream)) return rc;
   // identity branch: the input clip, cropped by (f_acc-1)/2 at each end when shrink
   const int64_t c = r->shrink ? r->d_skip : 0;
   const int64_t fe = r->frame_elems;
@@ -1339,5 +1359,224 @@ extern "C" int co_mha_state_set(co_mha* m, const void* src, size_t bytes, int64_
                               cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   }
   m->n = n;
+  return CO_OK;
+}
+
+// ----------------------------------------------------------------- broadcast-reduce
+// BroadcastReduce (include/co.h): branches are stacks (or the
+// identity); a branch with delay d_i < d_max keeps a ring of its last
+// k_i + 1 = d_max - d_i + 1 Ready outputs (+ a scratch slot) and contributes the
+// one of k_i Ready outputs ago; the merge adds (k_compose.cu) or copies channel
+// slices.
+
+struct co_parallel {
+  std::vector<co_stack*> br;         // nullptr = identity
+  int reduce = CO_REDUCE_SUM;
+  std::vector<int64_t> d, k, count, C;
+  std::vector<int> dt;               // per-branch output dtype (SUM may mix: the identity's is the input's)
+  int64_t d_max = 0, n = 0;
+  std::vector<void*> out, ring;      // per branch: step output buffer, alignment ring
+  int64_t B = 0, HWo = 0, Ctot = 0, in_frame = 0;
+  int dtype = 0;
+};
+
+extern "C" int co_parallel_create(co_stack* const* branches, int n_branches, int reduce, co_parallel** out) {
+  if (!branches || n_branches < 1 || !out) return fail(CO_ERR_ARG, "bad argument");
+  if (reduce != CO_REDUCE_SUM && reduce != CO_REDUCE_CONCAT) return fail(CO_ERR_ARG, "bad reduce");
+  *out = nullptr;
+  // the common input: any stack branch's first layer (an all-identity composite has no geometry source)
+  const Geom* in = nullptr;
+  for (int i = 0; i < n_branches; ++i)
+    if (branches[i]) { in = &branches[i]->layers.front()->g; break; }
+  if (!in) return fail(CO_ERR_ARG, "at least one branch must be a stack");
+  co_parallel* p = new (std::nothrow) co_parallel();
+  if (!p) return fail(CO_ERR_OOM, "host allocation");
+  auto bail = [&](int code) { co_parallel_destroy(p); return code; };
+  p->reduce = reduce;
+  p->B = in->B;
+  p->in_frame = in->frame_elems;
+  int64_t Ho = -1, Wo = -1;
+  int odt = -1;
+  for (int i = 0; i < n_branches; ++i) {
+    co_stack* st = branches[i];
+    int64_t di = 0, ci, ho, wo;
+    int dt;
+    if (st) {
+      const Geom& a = st->layers.front()->g;
+      const Geom& z = st->layers.back()->g;
+      if (a.B != in->B || a.H != in->H || a.W != in->W || a.Cin != in->Cin || a.in_dtype != in->in_dtype)
+        return bail(fail(CO_ERR_SHAPE, "branch %d: input differs from branch inputs", i));
+      int64_t s_acc = 1;
+      for (co_conv* h : st->layers) s_acc *= h->g.st;
+      if (s_acc != 1) return bail(fail(CO_ERR_SHAPE, "branch %d: accumulated temporal stride %lld != 1", i, (long long)s_acc));
+      co_stack_delay(st, &di);
+      ci = z.Cout; ho = z.Ho; wo = z.Wo; dt = z.out_dtype;
+    } else {
+      ci = in->Cin; ho = in->H; wo = in->W; dt = in->in_dtype;
+    }
+    if (Ho < 0) { Ho = ho; Wo = wo; }
+    if (st && odt < 0) odt = dt;       // the composite's output dtype: the (first) stack branch's
+    if (ho != Ho || wo != Wo) return bail(fail(CO_ERR_SHAPE, "branch %d: output shape differs", i));
+    if (st && dt != odt) return bail(fail(CO_ERR_SHAPE, "branch %d: output dtype differs", i));
+    if (!st && reduce == CO_REDUCE_CONCAT && dt != in->in_dtype)
+      return bail(fail(CO_ERR_SHAPE, "branch %d: dtype differs", i));
+    p->dt.push_back(dt);
+    if (reduce == CO_REDUCE_SUM && !p->C.empty() && ci != p->C[0])
+      return bail(fail(CO_ERR_SHAPE, "branch %d: sum needs equal channel counts", i));
+    p->br.push_back(st); p->d.push_back(di); p->C.push_back(ci);
+    p->d_max = std::max(p->d_max, di);
+  }
+  p->HWo = Ho * Wo;
+  p->dtype = odt;
+  p->Ctot = reduce == CO_REDUCE_SUM ? p->C[0] : 0;
+  if (reduce == CO_REDUCE_CONCAT)
+    for (int64_t c : p->C) p->Ctot += c;
+  if (reduce == CO_REDUCE_CONCAT)
+    for (int i = 0; i < n_branches; ++i)
+      if (p->dt[i] != odt) return bail(fail(CO_ERR_SHAPE, "concat: branch %d dtype differs", i));
+  for (int i = 0; i < n_branches; ++i) {
+    p->k.push_back(p->d_max - p->d[i]);
+    p->count.push_back(0);
+    const size_t fb = size_t(p->B) * p->HWo * p->C[i] * dsize(p->dt[i]);
+    void* o = nullptr;
+    void* r = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (p->br[i]) e = cudaMalloc(&o, fb);
+    if (e == cudaSuccess && p->k[i] > 0) e = cudaMalloc(&r, fb * size_t(p->k[i] + 2));
+    p->out.push_back(o); p->ring.push_back(r);
+    if (e != cudaSuccess) return bail(fail(CO_ERR_OOM, "branch buffers: %s", cudaGetErrorString(e)));
+  }
+  *out = p;
+  return CO_OK;
+}
+
+extern "C" int co_parallel_destroy(co_parallel* p) {
+  if (!p) return CO_OK;
+  for (void* o : p->out) cudaFree(o);
+  for (void* r : p->ring) cudaFree(r);
+  delete p;
+  return CO_OK;
+}
+
+// Merge branch frames src[i] (each B * HWo * C_i, stream stride sstride[i]) into y.
+static int merge_into(co_parallel* p, const std::vector<const void*>& src, const std::vector<int64_t>& sstride,
+                      void* y, int64_t ystride, int64_t cols, cudaStream_t s) {
+  const size_t esz = dsize(p->dtype);
+  const int nb = int(src.size());
+  if (p->reduce == CO_REDUCE_SUM) {
+    // start from the first branch in the output dtype, add the others (converted)
+    int first = 0;
+    while (p->dt[first] != p->dtype) ++first;
+    const size_t row = size_t(cols) * p->HWo * p->Ctot * esz;
+    CO_CUDA(cudaMemcpy2DAsync(y, size_t(ystride) * esz, src[first], size_t(sstride[first]) * esz, row, p->B,
+                              cudaMemcpyDeviceToDevice, s));
+    for (int i = 0; i < nb; ++i)
+      if (i != first)
+        CO_CUDA(co::launch_residual_add(p->dtype, y, ystride, p->dt[i], src[i], sstride[i], p->B,
+                                        cols * p->HWo * p->Ctot, CO_ACT_NONE, s));
+    return CO_OK;
+  }
+  int64_t off = 0;   // concat: channel slice per branch, pixel rows of every stream
+  for (int i = 0; i < nb; ++i) {
+    for (int64_t b = 0; b < p->B; ++b)
+      CO_CUDA(cudaMemcpy2DAsync(static_cast<char*>(y) + (size_t(b) * ystride + off) * esz, size_t(p->Ctot) * esz,
+                                static_cast<const char*>(src[i]) + size_t(b) * sstride[i] * esz, size_t(p->C[i]) * esz,
+                                size_t(p->C[i]) * esz, size_t(cols) * p->HWo, cudaMemcpyDeviceToDevice, s));
+    off += p->C[i];
+  }
+  return CO_OK;
+}
+
+extern "C" int co_parallel_step(co_parallel* p, const void* x, void* y, int update_state, int* ready,
+                                co_stream stream) {
+  if (!p || !x || !y) return fail(CO_ERR_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = int(p->br.size());
+  std::vector<const void*> aligned(nb, nullptr);
+  std::vector<int64_t> stride(nb);
+  bool all = p->n >= p->d_max;
+  for (int i = 0; i < nb; ++i) {
+    const size_t fb = size_t(p->B) * p->HWo * p->C[i] * dsize(p->dt[i]);
+    int r = 1;
+    const void* fresh = x;
+    if (p->br[i]) {
+      if (int rc = co_stack_step(p->br[i], x, p->out[i], update_state, &r, stream)) return rc;
+      fresh = p->out[i];
+    }
+    stride[i] = p->HWo * p->C[i];
+    const int64_t k = p->k[i];
+    if (k == 0) {
+      aligned[i] = r ? fresh : nullptr;
+    } else {
+      char* ring = static_cast<char*>(p->ring[i]);
+      const int64_t R = k + 1;
+      if (r) {
+        char* slot = ring + size_t(update_state ? floor_mod(p->count[i], R) : R) * fb;   // scratch when probing
+        CO_CUDA(cudaMemcpyAsync(slot, fresh, fb, cudaMemcpyDeviceToDevice, s));
+      }
+      const int64_t idx = p->count[i] + (r ? 1 : 0) - 1 - k;     // the output k Ready outputs ago
+      aligned[i] = (r && idx >= 0) ? ring + size_t(floor_mod(idx, R)) * fb : nullptr;
+      if (r && update_state) ++p->count[i];
+    }
+    all = all && aligned[i];
+  }
+  if (all)
+    if (int rc = merge_into(p, aligned, stride, y, p->HWo * p->Ctot, 1, s)) return rc;
+  if (update_state) ++p->n;
+  if (ready) *ready = all ? 1 : 0;
+  return CO_OK;
+}
+
+extern "C" int co_parallel_forward(co_parallel* p, const void* x, int64_t T, void* y, int64_t* T_out,
+                                   co_stream stream) {
+  if (!p || !x || !y || T < 1) return fail(CO_ERR_ARG, "bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = int(p->br.size());
+  std::vector<int64_t> Ti(nb);
+  int64_t T_min = T;
+  for (int i = 0; i < nb; ++i) {
+    Ti[i] = p->br[i] ? layers_out_len(p->br[i]->layers, T) : T;
+    T_min = std::min(T_min, Ti[i]);
+  }
+  if (T_min < 1) return fail(CO_ERR_LENGTH, "broadcast-reduce: T' < 1");
+  std::vector<void*> tmp(nb, nullptr);
+  std::vector<const void*> src(nb);
+  std::vector<int64_t> sstride(nb);
+  int rc = CO_OK;
+  for (int i = 0; i < nb && !rc; ++i) {
+    sstride[i] = Ti[i] * p->HWo * p->C[i];
+    if (!p->br[i]) { src[i] = x; continue; }
+    cudaError_t e = cudaMallocAsync(&tmp[i], size_t(p->B) * sstride[i] * dsize(p->dt[i]), s);
+    if (e != cudaSuccess) { rc = fail(CO_ERR_OOM, "%s", cudaGetErrorString(e)); break; }
+    int64_t t = 0;
+    rc = layers_forward(p->br[i]->layers, x, T, tmp[i], &t, stream);
+    src[i] = tmp[i];
+  }
+  if (!rc) rc = merge_into(p, src, sstride, y, T_min * p->HWo * p->Ctot, T_min, s);
+  for (void* t : tmp)
+    if (t) cudaFreeAsync(t, s);
+  if (!rc && T_out) *T_out = T_min;
+  return rc;
+}
+
+extern "C" int co_parallel_clean(co_parallel* p, co_stream stream) {
+  if (!p) return fail(CO_ERR_ARG, "null composite");
+  for (co_stack* st : p->br)
+    if (st)
+      if (int rc = co_stack_clean(st, stream)) return rc;
+  for (size_t i = 0; i < p->count.size(); ++i) p->count[i] = 0;
+  p->n = 0;
+  return CO_OK;
+}
+
+extern "C" int co_parallel_delay(const co_parallel* p, int64_t* delay) {
+  if (!p || !delay) return fail(CO_ERR_ARG, "null argument");
+  *delay = p->d_max;
+  return CO_OK;
+}
+
+extern "C" int co_parallel_out_channels(const co_parallel* p, int32_t* channels) {
+  if (!p || !channels) return fail(CO_ERR_ARG, "null argument");
+  *channels = int32_t(p->Ctot);
   return CO_OK;
 }

@@ -183,3 +183,81 @@ def test_residual_construction_errors():
     convs, _ = _layers([(16, 32, (3, 3, 3), (1, 1, 1), 1, False)], 2, 4, 4, rng)
     with pytest.raises(CoError):          # channel count changes
         co.Residual(convs)
+
+
+def _branch(specs, B, H, W, rng, last_fp32=True):
+    import paper_2204_03418_b200 as co
+    convs, (descs, Ws, bs, relu, rnd) = _layers(specs, B, H, W, rng, last_fp32=last_fp32)
+    return co.Stack(convs), O.Stack(descs, Ws, bs, relu, rnd, B), (descs, Ws, bs, relu, rnd)
+
+
+def test_broadcast_reduce_conv_delay_is_the_residual():
+    """Listing 3: BroadcastReduce(conv, Delay(1)) == Residual(conv) (equal padding)."""
+    import paper_2204_03418_b200 as co
+    rng = np.random.default_rng(21)
+    B, H, W = 2, 5, 6
+    st, om, _ = _branch([(32, 32, (3, 3, 3), (1, 1, 1), 1, False)], B, H, W, rng)
+    br = co.BroadcastReduce([st, None], "sum")
+    ref = OC.BroadcastReduceStep([om, None], [1, 0], "sum")
+    assert br.delay == 1
+    for t in range(7):
+        x = _bf16(rng.standard_normal((B, 32, H, W)))
+        y = br.forward_step(to_cl(x, torch.bfloat16))
+        r = ref.forward_step(x)
+        assert (y is None) == (r is None), t
+        if y is not None:
+            assert rel_err(np_of(y), r) <= 1e-4, t
+
+
+@pytest.mark.parametrize("reduce", ["concat", "sum"])
+def test_broadcast_reduce_inception_style(reduce):
+    """Listing 4-style block: 1x1, 3x3x3 (no temporal padding), temporal 5x1x1
+    depthwise and the identity, concatenated (or summed): branch delays 0 / 2 /
+    4 / 0 aligned to 4; step outputs and the batch form vs the oracle."""
+    import paper_2204_03418_b200 as co
+    rng = np.random.default_rng(22)
+    B, H, W, C = 2, 5, 6, 32
+    specs = [[(C, C, (1, 1, 1), (0, 0, 0), 1, True)], [(C, C, (3, 3, 3), (0, 1, 1), 1, False)],
+             [(C, C, (5, 1, 1), (0, 0, 0), C, False)]]
+    fp32 = reduce == "sum"          # concat needs one dtype: bf16 branches (the identity's), bf16 bar
+    made = [_branch(sp, B, H, W, rng, last_fp32=fp32) for sp in specs]
+    tol = 1e-4 if fp32 else 2e-2
+    br = co.BroadcastReduce([m[0] for m in made] + [None], reduce)
+    ref = OC.BroadcastReduceStep([m[1] for m in made] + [None], [0, 2, 4, 0], reduce)
+    assert br.delay == 4 and br.out_channels == (4 * C if reduce == "concat" else C)
+    frames = [_bf16(rng.standard_normal((B, C, H, W))) for _ in range(10)]
+    for t, x in enumerate(frames):
+        if t == 6:
+            probe = _bf16(rng.standard_normal((B, C, H, W)))
+            yp = br.forward_step(to_cl(probe, torch.bfloat16), update_state=False)
+            assert rel_err(np_of(yp), ref.forward_step(probe, update_state=False)) <= tol
+        y = br.forward_step(to_cl(x, torch.bfloat16))
+        r = ref.forward_step(x)
+        assert (y is None) == (r is None), t
+        if y is not None:
+            assert rel_err(np_of(y), r) <= tol, t
+    clip = np.stack(frames, axis=2)
+    yb = br.forward(to_cl(clip, torch.bfloat16))
+    ref_b = OC.broadcast_reduce_forward(
+        [lambda c, m=m: _batch_layers(m[2], c) for m in made] + [None], clip, reduce)
+    assert yb.shape[2] == ref_b.shape[2] == 6
+    assert rel_err(np_of(yb), ref_b) <= tol
+    br.clean_state(); ref.clean_state()
+    for t, x in enumerate(frames[:6]):
+        y = br.forward_step(to_cl(x, torch.bfloat16))
+        r = ref.forward_step(x)
+        assert (y is None) == (r is None)
+        if y is not None:
+            assert rel_err(np_of(y), r) <= tol
+
+
+def _batch_layers(parts, c):
+    descs, Ws, bs, relu, rnd = parts
+    cur = c
+    for d, Wt, b, r, q in zip(descs, Ws, bs, relu, rnd):
+        cur = O.forward(d, Wt, b, cur)
+        if r:
+            cur = np.maximum(cur, 0.0)
+        if q:
+            cur = O.bf16_round(cur)
+    return cur
