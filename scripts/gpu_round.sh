@@ -4,9 +4,10 @@
 # 1. build + the GPU test suite; 2. bench.py on every config (JSON lines under
 # gpurun_out/bench_<tag>_c<N>.json) and the reference arm; 3. the companion
 # benches (pooling, chunked steps, MHA); 4. the ncu launch list of the default
-# bench command and one `--set full` capture of its dominant kernel (each only
-# after the same command exited 0 without ncu).  Summarise afterwards with
-# scripts/ncu_summary.py and copy what is judged into profiles/.
+# bench command (after the same command exited 0 without ncu).  One ncu run per
+# gpurun call: the `--set full` captures go through scripts/gpu_ncu_full.sh in
+# calls of their own.  Summarise with scripts/ncu_summary.py and copy what is
+# judged into profiles/.
 set -u
 TAG=${1:-rX}
 OUT=gpurun_out
@@ -26,7 +27,4 @@ B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e"
 $B > $OUT/plain_${TAG}.log 2>&1 && \
   timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches_${TAG}_c2.csv $B > $OUT/ncu_launches_${TAG}.log 2>&1
-$B > $OUT/plain2_${TAG}.log 2>&1 && \
-  timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_step_dense_tc -s 5 -c 1 \
-    -o $OUT/prof_${TAG}_c2 $B > $OUT/ncu_full_${TAG}.log 2>&1
 ls $OUT | tail -30
