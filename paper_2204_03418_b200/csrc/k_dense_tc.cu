@@ -520,9 +520,12 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
         }
       }
     }
+    // accumulator consumed: every tcgen05.ld above was waited on (wait::ld), so a
+    // relaxed arrive suffices -- the state / y stores need no ordering with the
+    // MMA warp, and a release arrive would stall on them (ptx::mbar_arrive_relaxed)
     ptx::tc_fence_before();
-    if constexpr (PAIR == 2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&acc_empty[buf]), 0));
-    else ptx::mbar_arrive(&acc_empty[buf]);
+    if constexpr (PAIR == 2) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&acc_empty[buf]), 0));
+    else ptx::mbar_arrive_relaxed(&acc_empty[buf]);
   }
   }
   // ===================== teardown (all threads) =====================

@@ -41,6 +41,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Relaxed arrive: no release fence.  For the epilogue's "accumulator consumed"
+// signal, whose only hazard (TMEM reads vs the next MMA writes) is already
+// closed by tcgen05.wait::ld + tcgen05.fence::before_thread_sync; a release
+// arrive would also wait for every global store the thread has in flight
+// (MEMBAR.ALL.CTA, and MEMBAR.ALL.GPU at cluster scope -- measured as the top
+// stall of the CTA-pair kernels).
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -187,6 +196,9 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // peer bit of a CTA-pair shared address: clearing it names the leader CTA's copy
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
