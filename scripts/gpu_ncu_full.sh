@@ -6,6 +6,6 @@ set -u
 TAG=$1; KREGEX=$2; SKIP=$3; shift 3
 mkdir -p gpurun_out
 "$@" > gpurun_out/plain_${TAG}.log 2>&1 || { echo "command failed without ncu"; exit 1; }
-timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:$KREGEX -s $SKIP -c 1 \
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on --kernel-name-base ${NCU_NAME_BASE:-function} -k "regex:$KREGEX" -s $SKIP -c 1 \
   -o gpurun_out/prof_${TAG} "$@" > gpurun_out/ncu_full_${TAG}.log 2>&1
 tail -2 gpurun_out/ncu_full_${TAG}.log
