@@ -653,6 +653,46 @@ extern "C" int co_forward_steps(co_conv* h, const void* x, int64_t T, void* y, u
   const int64_t total = T + (pad_end ? g.pt : 0);
   int64_t r_count = 0;
   int rc = CO_OK;
+  if (total == T && T > 1 && h->kernel_used == CO_KERNEL_DENSE_TC && co::dense_tc_chunkable(h->tc, g)) {
+    // chunked tensor-core steps: chunks of Tc frames, one launch each, item-batch-
+    // major so each tile's state stays L2-resident across its frames (§8f f2);
+    // FLAT stages a chunk time-major, so Tc bounds that copy to ~1 GB
+    const int64_t frame_bytes = g.B * g.frame_elems * int64_t(dsize(g.in_dtype));
+    int64_t Tc = std::max<int64_t>(1, std::min<int64_t>({T, 256, (int64_t(1) << 30) / std::max<int64_t>(frame_bytes, 1)}));
+    if (const char* e = getenv("CO_CHUNK_T")) Tc = std::max<int64_t>(1, std::min<int64_t>(Tc, atoi(e)));   // tests
+    constexpr int kTick = 2 + co::kMaxKt;
+    std::vector<int> ticks(size_t(Tc) * kTick);
+    int* dticks = nullptr;
+    CO_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dticks), ticks.size() * sizeof(int), s));
+    int last = 0;
+    for (int64_t t0 = 0; t0 < T && rc == CO_OK; t0 += Tc) {
+      const int64_t tn = std::min(Tc, T - t0);
+      const int64_t oi0 = r_count;
+      for (int64_t t = 0; t < tn; ++t) {
+        StepArgs a;
+        const int r = clock_args(g, clock + t, a);
+        int* tk = ticks.data() + t * kTick;
+        tk[0] = r;
+        tk[1] = int(r_count - oi0);
+        for (int k = 0; k < co::kMaxKt; ++k) tk[2 + k] = a.slot[k];
+        if (ready_mask) ready_mask[t0 + t] = uint8_t(r);
+        r_count += r;
+        last = r;
+      }
+      cudaError_t e = cudaMemcpyAsync(dticks, ticks.data(), size_t(tn) * kTick * sizeof(int), cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess)
+        e = co::dense_tc_steps(h->tc, g, static_cast<const char*>(x) + size_t(t0) * frame * isz, tn, T, dticks,
+                               static_cast<char*>(y) + size_t(oi0) * oframe * osz, cap * oframe, state, h->bias, s);
+      if (e != cudaSuccess) rc = fail(CO_ERR_CUDA, "chunked dense steps: %s", cudaGetErrorString(e));
+      clock += tn;
+    }
+    cudaFreeAsync(dticks, s);
+    if (scratch) cudaFreeAsync(scratch, s);
+    if (rc) return rc;
+    if (update_state) { h->last_n = clock - 1; h->last_ready = last; }
+    if (n_ready) *n_ready = r_count;
+    return CO_OK;
+  }
   if (total > 0 && h->kernel_used == CO_KERNEL_DEPTHWISE && co::depthwise_chunkable(h->dw, g)) {
     // chunked: the whole fold in one launch, state in registers
     cudaError_t e = co::depthwise_steps(h->dw, g, x, T, total, clock, y, cap * oframe, state, h->bias, s);

@@ -65,6 +65,7 @@ constexpr int kMaxStages = 6;   // operand pipeline depth: as many as fit in sha
 // its columns), then the producer and MMA warps
 __host__ __device__ constexpr int tc_threads(int eg, int cs = 1) { return 32 * (4 * eg * cs + 2); }
 constexpr int kApad = 512;        // slack after each A stage (junk rows may read past the box)
+constexpr int kTickInts = 2 + kMaxKt;   // chunked steps: [emit, output index, slot[kMaxKt]] per tick
 enum { MODE_HALO = 0, MODE_FLAT = 1, MODE_KLOOP = 2 };
 
 struct TcParams {
@@ -95,6 +96,14 @@ struct TcParams {
   int dbg;                        // CO_TC_DEBUG bits (experiments only): 1 no state/y traffic, 2 no MMA,
                                   // 4 no A loads, 8 no TMEM reads, 16 (with 2) no accumulator handshakes
   int Cq;
+  // chunked co_forward_steps (HALO / FLAT): T frames per item,
+  // processed item-batch-major so a tile's state stays L2-resident between its
+  // frames; ticks = T rows of kTickInts: [emit, output index, ring slot of tap k...]
+  int T;
+  int x_tmul;                     // HALO chunks: frame (b, t) is clip "stream" b x_tmul + t (x_tmul = clip length)
+  const int* ticks;
+  int64_t y_tstride;              // elements between a stream's consecutive Ready outputs in y
+  int64_t a_trows;                // FLAT: rows between frames of the time-major staged clip
   float* state;
   void* y;
   int64_t y_bstride;
@@ -202,27 +211,35 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
             ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(w_peer), 0));
           }
         }
-        for (int64_t item = unit; item < p.n_items; item += n_units) {
-          ptx::mbar_wait(&empty[s], ph ^ 1);
-          if (p.dbg & 4) {
-            if (leader) ptx::mbar_arrive(&full[s]);
-            if (++s == p.stages) { s = 0; ph ^= 1; }
-            continue;
-          }
-          // the leader's barrier counts both CTAs' A bytes (pair-TMA completes on it)
-          if (leader) ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes * PAIR);
-          const int64_t tile = tile_of(item);
-          uint8_t* dst = a_s + s * p.a_stride;
-          if (p.mode == MODE_FLAT) {
-            if constexpr (PAIR == 2) ptx::tma_load_3d_pair(dst, &tmap, &full[s], 0, int(tile * 128), 0);
-            else ptx::tma_load_3d(dst, &tmap, &full[s], 0, int(tile * 128), 0);
-          } else {
-            const int b = int(tile / p.tiles_per_stream);
-            const int ho0 = int(tile % p.tiles_per_stream) * p.MT;
-            if constexpr (PAIR == 2) ptx::tma_load_5d_pair(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
-            else ptx::tma_load_5d(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
-          }
-          if (++s == p.stages) { s = 0; ph ^= 1; }
+        // works in item-batch-major order (T == 1: one work per item, as before)
+        for (int64_t bi = unit; bi < p.n_items; bi += int64_t(EG) * n_units) {
+          const int64_t left = (p.n_items - bi + n_units - 1) / n_units;
+          const int nb = left < EG ? int(left) : EG;
+          for (int t = 0; t < p.T; ++t)
+            for (int e = 0; e < nb; ++e) {
+              const int64_t item = bi + int64_t(e) * n_units;
+              ptx::mbar_wait(&empty[s], ph ^ 1);
+              if (p.dbg & 4) {
+                if (leader) ptx::mbar_arrive(&full[s]);
+                if (++s == p.stages) { s = 0; ph ^= 1; }
+                continue;
+              }
+              // the leader's barrier counts both CTAs' A bytes (pair-TMA completes on it)
+              if (leader) ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes * PAIR);
+              const int64_t tile = tile_of(item);
+              uint8_t* dst = a_s + s * p.a_stride;
+              if (p.mode == MODE_FLAT) {
+                const int row = int(tile * 128 + t * p.a_trows);     // staged clip: frame t's rows
+                if constexpr (PAIR == 2) ptx::tma_load_3d_pair(dst, &tmap, &full[s], 0, row, 0);
+                else ptx::tma_load_3d(dst, &tmap, &full[s], 0, row, 0);
+              } else {
+                const int b = int(tile / p.tiles_per_stream) * p.x_tmul + t;   // clip: (stream, frame) -> b T + t
+                const int ho0 = int(tile % p.tiles_per_stream) * p.MT;
+                if constexpr (PAIR == 2) ptx::tma_load_5d_pair(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
+                else ptx::tma_load_5d(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
+              }
+              if (++s == p.stages) { s = 0; ph ^= 1; }
+            }
         }
       } else {
         const int per_stream = p.tiles_h * p.tiles_w;
@@ -293,7 +310,9 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       if constexpr (PAIR == 2) ptx::mbar_wait(w_peer, 0);
       const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_u32(w_s), NB * 16, 128);
       const int kc2 = p.Cin / 16;                       // MMAs (K = 16) per spatial tap
-      for (int64_t item = unit; item < p.n_items; item += n_units) {
+      int64_t n_works = 0;                              // this unit's works: items x T frames
+      for (int64_t item = unit; item < p.n_items; item += n_units) n_works += p.T;
+      for (int64_t w = 0; w < n_works; ++w) {
         if (!(p.dbg & 16)) ptx::mbar_wait(&acc_empty[e], eph ^ 1);
         ptx::tc_fence_after();
         ptx::mbar_wait(&full[s], ph);
@@ -389,10 +408,15 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   const int64_t stiles = p.splane >> 7;                // state tiles per slot (S[slot][tile][Cq][128][4])
   constexpr int NQ = CE / 4;                           // channel quads per thread and pass
   constexpr int NS = (KT > 1) ? KT - 1 : 1;
-  int li = e;
-  for (int64_t item = unit + int64_t(e) * n_units; item < p.n_items; item += EG * int64_t(n_units), li += EG) {
-    const int buf = li % NBUF;                         // accumulator buffer of this item
+  // One work (an item at one tick) of this group: buf / bph pick the accumulator,
+  // tk the chunk's tick row (nullptr: the launch's single tick from p).  Called
+  // from two loops so the one-step path keeps its own (lower) register use.
+  auto work = [&](const int64_t item, const int64_t li, const int* tk) {
+    const int buf = int(li % NBUF);                    // accumulator buffer of this work
     const uint32_t bph = uint32_t(li / NBUF) & 1u;
+    const int emit = tk ? tk[0] : p.emit;
+    const int64_t yt = tk ? int64_t(tk[1]) * p.y_tstride : 0;
+    auto slot = [&](int k) -> int { return tk ? tk[2 + k] : p.slot[k]; };
     const int64_t tile = tile_of(item);
     // ---- this row's output pixel
     bool valid;
@@ -424,18 +448,18 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       // ---- prefetch the state this pass needs (pass 0: before the accumulator is ready)
       float4 sv[NS][NQ];
       if (KT > 1 && valid && !(p.dbg & 1)) {
-        if (p.emit) {
+        if (emit) {
           const float4* src = reinterpret_cast<const float4*>(p.state) +
-                              ((int64_t(p.slot[KT - 1]) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
+                              ((int64_t(slot(KT - 1)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
           for (int i = 0; i < NQ; ++i) sv[0][i] = __ldcs(src + i * 128);
         }
         if (p.update) {
 #pragma unroll
           for (int k = 1; k < KT - 1; ++k) {
-            if (p.slot[k] < 0) continue;
+            if (slot(k) < 0) continue;
             const float4* src = reinterpret_cast<const float4*>(p.state) +
-                                ((int64_t(p.slot[k]) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
+                                ((int64_t(slot(k)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
             for (int i = 0; i < NQ; ++i) sv[k][i] = __ldcs(src + i * 128);
           }
@@ -447,7 +471,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       }
       float v[16];
       // ---- (1) complete + emit
-      if (p.emit) {
+      if (emit) {
 #pragma unroll
         for (int c = 0; c < CE; c += 16) {
           if (!(p.dbg & 8)) ptx::tmem_ld16(t_row + uint32_t((KT - 1) * CC + cb + c), v);
@@ -467,7 +491,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
 #pragma unroll
               for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
             }
-            const int64_t yoff = b * p.y_bstride + (pix - b * p.HWo) * p.Cout + c0 + cb + c;
+            const int64_t yoff = b * p.y_bstride + yt + (pix - b * p.HWo) * p.Cout + c0 + cb + c;
             if (p.out_f32) {
               float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + yoff);
 #pragma unroll
@@ -486,9 +510,9 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
         // ---- (2) accumulate into pending outputs
 #pragma unroll
         for (int k = KT - 2; k >= 1; --k) {
-          if (p.slot[k] < 0) continue;
+          if (slot(k) < 0) continue;
           float4* dst = reinterpret_cast<float4*>(p.state) +
-                        ((int64_t(p.slot[k]) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
+                        ((int64_t(slot(k)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
           for (int c = 0; c < CE; c += 16) {
             if (!(p.dbg & 8)) ptx::tmem_ld16(t_row + uint32_t(k * CC + cb + c), v);
@@ -504,9 +528,9 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
           }
         }
         // ---- (3) start the newest output (overwrites the emitted slot)
-        if (p.slot[0] >= 0) {
+        if (slot(0) >= 0) {
           float4* dst = reinterpret_cast<float4*>(p.state) +
-                        ((int64_t(p.slot[0]) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
+                        ((int64_t(slot(0)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
           for (int c = 0; c < CE; c += 16) {
             if (!(p.dbg & 8)) ptx::tmem_ld16(t_row + uint32_t(cb + c), v);
@@ -526,6 +550,22 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     ptx::tc_fence_before();
     if constexpr (PAIR == 2) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&acc_empty[buf]), 0));
     else ptx::mbar_arrive_relaxed(&acc_empty[buf]);
+  };
+  if (!p.ticks) {
+    int64_t li = e;
+    for (int64_t item = unit + int64_t(e) * n_units; item < p.n_items; item += EG * int64_t(n_units), li += EG)
+      work(item, li, nullptr);
+  } else {
+    // chunked: item bi + e n_units of every batch, all T frames in order; the work
+    // index over the unit's sequence (batch-major, then frame, then item) picks the buffer
+    int64_t wbase = 0;
+    for (int64_t bi = unit; bi < p.n_items; bi += int64_t(EG) * n_units) {
+      const int64_t left = (p.n_items - bi + n_units - 1) / n_units;
+      const int nb = left < EG ? int(left) : EG;
+      for (int t = 0; e < nb && t < p.T; ++t)
+        work(bi + int64_t(e) * n_units, wbase + int64_t(t) * nb + e, p.ticks + t * kTickInts);
+      wbase += int64_t(nb) * p.T;
+    }
   }
   }
   // ===================== teardown (all threads) =====================
@@ -734,6 +774,13 @@ bool plan_resident(const Geom& g, Plan& pl) {
   }
   const int a_bytes = (g.Cin / 8) * a_rows * 16;
   const int a_stride = ((a_bytes + kApad + 1023) / 1024) * 1024;
+  // The MMA of tap (u, v) reads 128 rows from row u Wp + v of every channel
+  // block: up to (kh-1) Wp + kw - 1 + 128 rows, past the box into the next
+  // stage (junk rows, discarded) -- and past the LAST stage into whatever
+  // follows, so the allocation keeps that over-read inside shared memory.
+  const int max_row = flat ? 128 : (g.kh - 1) * Wp + (g.kw - 1) + 128;
+  const int over = std::max(0, (max_row - a_rows) * (g.Cin % 64 == 0 && swa_enabled() ? 128 : 16));
+  const size_t tail = size_t(std::max(0, over - (a_stride - a_bytes)));
   const int64_t K = int64_t(g.Cin) * g.kh * g.kw;
   const int eg_pin = pinned_eg();
   const char* pair_env = getenv("CO_TC_PAIR");    // A/B runs: pin 1 or 2
@@ -745,7 +792,7 @@ bool plan_resident(const Geom& g, Plan& pl) {
     if (eg_pin && v.EG != eg_pin) continue;
     if (v.CS != pinned_cs() || (pair_env && v.PAIR != atoi(pair_env))) continue;
     const int64_t w_bytes = int64_t(v.KT * v.CC) * K * 2 / v.PAIR;   // per CTA
-    const size_t fixed = 1024 + size_t((w_bytes + 1023) / 1024 * 1024) + 512 + v.CC * 4;
+    const size_t fixed = 1024 + size_t((w_bytes + 1023) / 1024 * 1024) + 512 + v.CC * 4 + tail;
     if (fixed + 2 * size_t(a_stride) > kSmemLimit) continue;
     const bool fits = fixed + 2 * size_t(a_stride) <= kSmemBudget;
     // prefer: staying under the L1 cliff (a CTA pair halves the resident
@@ -970,14 +1017,35 @@ static cudaError_t ensure_stage(DenseTC* t, size_t need) {
   return e;
 }
 
-cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const float* bias, cudaStream_t s) {
+// One launch: a step (T == 1), or a chunk of T frames of a clip x (B, T, H, W,
+// Cin) with the tick table `ticks` on the device (HALO / FLAT only).
+static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const float* bias, cudaStream_t s,
+                             int T, const int* ticks, int64_t y_tstride) {
   const Plan& pl = t->pl;
   const Geom& k = pl.gk;
   const void* x = a.x;
   int64_t x_bstride = a.x_bstride;
   const int64_t frame = int64_t(g.H) * g.W * g.Cin;
   int64_t n_batch = k.B;                        // the tensor map's outermost extent
-  if (g.raw) {                                  // the frame ring: (f + 1) slots of B streams
+  int64_t flat_rows = k.B * k.HWo;              // FLAT: rows of the tensor map
+  const int64_t clip_T = T > 1 ? a.x_bstride / frame : 1;   // frames per stream of the clip x points into
+  if (T > 1) {
+    if (pl.mode == MODE_FLAT) {
+      // FLAT tiles are 128 consecutive (stream, pixel) rows of one frame: stage the
+      // chunk time-major, (T, B*HW, Cin), so frame t's rows are contiguous
+      if (cudaError_t e = ensure_stage(t, size_t(T) * g.B * frame * 2)) return e;
+      for (int tt = 0; tt < T; ++tt)
+        if (cudaError_t e = cudaMemcpy2DAsync(t->xstage + size_t(tt) * g.B * frame, frame * 2,
+                                              static_cast<const __nv_bfloat16*>(x) + size_t(tt) * frame,
+                                              size_t(a.x_bstride) * 2, frame * 2, g.B, cudaMemcpyDeviceToDevice, s))
+          return e;
+      x = t->xstage;
+      flat_rows = int64_t(T) * k.B * k.HWo;
+    } else {
+      n_batch = k.B * clip_T;                   // HALO: frame (b, t) is "stream" b T + t of the clip
+      x_bstride = frame;
+    }
+  } else if (g.raw) {                           // the frame ring: (f + 1) slots of B streams
     x = a.state;
     x_bstride = frame;
     n_batch = k.B * (g.f + 1);
@@ -997,7 +1065,7 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
     if (cudaError_t e = cudaGetLastError()) return e;
     x = t->xstage;
     x_bstride = kframe;
-  } else if (!x || (pl.mode == MODE_FLAT && x_bstride != frame)) {
+  } else if (T == 1 && (!x || (pl.mode == MODE_FLAT && x_bstride != frame))) {
     // zero frame (pad_end) or a strided clip column in flat mode: stage it densely
     if (cudaError_t e = ensure_stage(t, size_t(g.B) * frame * 2)) return e;
     cudaError_t e = x ? cudaMemcpy2DAsync(t->xstage, frame * 2, x, x_bstride * 2, frame * 2, g.B,
@@ -1012,7 +1080,7 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   auto encode = get_encode();
   if (pl.mode == MODE_FLAT) {
     const cuuint32_t cw = pl.swa ? 64 : 8;    // channels per row of the box (128-B swizzled or 16-B)
-    cuuint64_t dims[3] = {cw, cuuint64_t(k.B * k.HWo), cuuint64_t(k.Cin / cw)};
+    cuuint64_t dims[3] = {cw, cuuint64_t(flat_rows), cuuint64_t(k.Cin / cw)};
     cuuint64_t strides[2] = {cuuint64_t(k.Cin) * 2, cw * 2};
     cuuint32_t box[3] = {cw, 128, cuuint32_t(k.Cin / cw)};
     cuuint32_t es[3] = {1, 1, 1};
@@ -1086,6 +1154,11 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
   p.swa = pl.swa;
   p.a_rows = pl.chunk_stride / 16;
   p.Cq = g.Cq;
+  p.T = T;
+  p.x_tmul = int(clip_T);
+  p.ticks = ticks;
+  p.y_tstride = y_tstride;
+  p.a_trows = k.B * k.HWo;
   p.state = a.state;
   p.y = a.y;
   p.y_bstride = a.y_bstride;
@@ -1124,6 +1197,33 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
     cfg.numAttrs = 1;
   }
   return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(pl.var->fn), args);
+}
+
+cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const float* bias, cudaStream_t s) {
+  return tc_launch(t, g, a, bias, s, 1, nullptr, 0);
+}
+
+bool dense_tc_chunkable(const DenseTC* t, const Geom& g) {
+  if (const char* e = getenv("CO_CHUNK"))       // experiment / test knob: 0 = always fold per step
+    if (!atoi(e)) return false;
+  // HALO only: FLAT chunks must first be staged time-major (a 128-row tile spans
+  // streams), which costs more than the L2 reuse saves (measured on C5: 9.5 M
+  // chunked vs 9.7 M per-step stream-steps/s); CO_CHUNK_FLAT=1 enables it for A/B runs
+  const bool flat_ok = getenv("CO_CHUNK_FLAT") && atoi(getenv("CO_CHUNK_FLAT"));
+  return t && !g.raw && !t->pl.wcols && (t->pl.mode == MODE_HALO || (flat_ok && t->pl.mode == MODE_FLAT)) &&
+         g.st == 1;
+}
+
+cudaError_t dense_tc_steps(DenseTC* t, const Geom& g, const void* x, int64_t T, int64_t clip_T, const int* ticks_dev,
+                           void* y, int64_t y_bstride, float* state, const float* bias, cudaStream_t s) {
+  StepArgs a{};
+  a.x = x;
+  a.x_bstride = clip_T * int64_t(g.H) * g.W * g.Cin;
+  a.y = y;
+  a.y_bstride = y_bstride;
+  a.state = state;
+  a.update = 1;
+  return tc_launch(t, g, a, bias, s, int(T), ticks_dev, g.HWo * g.Cout);
 }
 
 }  // namespace co
