@@ -121,3 +121,36 @@ def test_fullsize_step_equals_batch_all_streams(cid):
             assert excess <= 0, (l, excess)
         del chk, clip, yb, ys
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cid,layer", [(2, 0), (3, 1)])
+def test_fullsize_chunked_steps_equal_per_step_fold(cid, layer, monkeypatch):
+    """At the full stream count and frame size: co_forward_steps through the
+    chunked kernels (tcgen05 HALO for C2, k_steps_dw_t for C3-b) equals the
+    per-step fold (CO_CHUNK=0) bit for bit -- outputs, ready mask and the
+    canonical state after the clip."""
+    import paper_2204_03418_b200 as co
+    from paper_2204_03418_b200 import synth
+    cfg = synth.config(cid)
+    L = cfg.layers[layer]
+    Wt, bt = synth.params(cfg)[layer]
+    T = 7
+    g = torch.Generator(device="cuda").manual_seed(11)
+    clip = co.channels_last(torch.randn((cfg.n_streams, L.cin, T) + tuple(cfg.in_spatial), generator=g,
+                                        device="cuda").to(torch.bfloat16))
+    res = {}
+    for chunk in ("1", "0"):
+        monkeypatch.setenv("CO_CHUNK", chunk)
+        conv = co.Conv(L.cin, L.cout, L.kernel, weight=Wt.cuda(), bias=bt.cuda(), stride=L.stride,
+                       padding=L.padding, dilation=L.dilation, groups=L.groups, spatial_rank=cfg.spatial_rank,
+                       in_spatial=tuple(cfg.in_spatial), n_streams=cfg.n_streams, dtype=cfg.dtype,
+                       out_dtype=torch.float32)
+        ys, mask = conv.forward_steps(clip)
+        st, _ = conv.state_dict_stream()
+        torch.cuda.synchronize()
+        res[chunk] = (ys, mask, st)
+        del conv
+    (ya, ma, sa), (yb, mb, sb) = res["1"], res["0"]
+    assert torch.equal(ma, mb) and int(ma.sum()) == T - (L.kernel[0] - 1)
+    assert torch.equal(ya, yb)
+    assert torch.equal(sa, sb)
