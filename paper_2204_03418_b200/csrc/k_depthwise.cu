@@ -350,6 +350,133 @@ __global__ void __launch_bounds__(kDwThreads, 2) k_steps_dw_t(const DwParams p, 
   }
 }
 
+// ------------------------------------------------------------------ K2c: chunked spatial steps
+// The K2 stencil folded over a clip: a CTA owns one tile
+// (stream b, TH output rows) for all T frames; thread = (channel quad q, strip
+// of PX output pixels), fixed for the clip, with its strip's kt-1 pending
+// outputs in registers (Q[j][px], the K3c shift register).  Per frame the
+// tile's input halo is staged by cp.async into one of two buffers (frame t+1
+// lands while frame t is folded); the taps are folded in K2's order (u, v, k),
+// so the result equals the per-step kernel bit for bit.  The fp32 ring is read
+// before and written after the clip only.
+template <int KT, int KH, int KW, int PX>
+__global__ void __launch_bounds__(1024, 1) k_steps_dw_st(const DwParams p, const ChunkArgs c) {
+  constexpr int NQ = KT > 1 ? KT - 1 : 1;
+  extern __shared__ __align__(16) uint8_t smem[];
+  float* ws = reinterpret_cast<float*>(smem);                       // [KT][KH][KW][C]
+  float* bs = ws + KT * KH * KW * p.C;                              // [C]
+  __nv_bfloat16* xs0 = reinterpret_cast<__nv_bfloat16*>(bs + p.C);  // 2 x [HR][WC][C]
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int i = tid; i < KT * KH * KW * p.C; i += nthr) ws[i] = p.w[i];
+  for (int i = tid; i < p.C; i += nthr) bs[i] = p.bias[i];
+  const int q = tid % p.Cq;
+  const int sidx = tid / p.Cq;                                      // this thread's strip in the tile
+  const int spr = (p.Wo + PX - 1) / PX;
+  const int c8 = p.C / 8;
+  const int row_chunks = p.WC * c8;
+  const size_t buf_elems = size_t(p.HR) * p.WC * p.C;
+  const float4* ws4 = reinterpret_cast<const float4*>(ws) + q;
+  const int R = KT - 1;
+  for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    const int64_t b = tile / p.bands;
+    const int ho0 = int(tile % p.bands) * p.TH;
+    const int th = min(p.TH, p.Ho - ho0);
+    const int r = sidx / spr;
+    const int wo0 = (sidx - r * spr) * PX;
+    const bool active = sidx < th * spr;
+    const int64_t pin0 = int64_t(ho0 + r) * p.Wo + wo0;
+    const int64_t pix0 = b * p.HWo + pin0;
+    __syncthreads();   // the previous tile finished reading both halo buffers (and ws / bs are visible)
+    auto stage = [&](int t, int buf) {   // frame t's halo -> buffer buf (zero fill outside the frame / clip)
+      const __nv_bfloat16* xb = (t < c.T) ? c.x + b * c.x_bstride + int64_t(t) * p.H * p.W * p.C : nullptr;
+      const uint32_t dst0 = static_cast<uint32_t>(__cvta_generic_to_shared(xs0 + buf * buf_elems));
+      for (int rr = 0; rr < p.HR; ++rr) {
+        const int hi = ho0 - p.ph + rr;
+        const bool row_in = xb && hi >= 0 && hi < p.H;
+        for (int i = tid; i < row_chunks; i += nthr) {
+          const int cc = i / c8, ch = i - (i / c8) * c8;
+          const int wi = cc - p.pw;
+          const bool in = row_in && wi >= 0 && wi < p.W;
+          const void* src = in ? static_cast<const void*>(xb + (int64_t(hi) * p.W + wi) * p.C + ch * 8)
+                               : static_cast<const void*>(p.w);
+          const uint32_t dst = dst0 + uint32_t(rr * row_chunks + i) * 16u;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(in ? 16 : 0)
+                       : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // the strip's pending outputs: Q[j] = output i0 + j (i0 completes at the first tick)
+    float4 Q[NQ][PX];
+    const int64_t i0 = c.m0 - (KT - 1);
+#pragma unroll
+    for (int j = 0; j < NQ; ++j)
+#pragma unroll
+      for (int x = 0; x < PX; ++x) {
+        Q[j][x] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (KT > 1 && active && wo0 + x < p.Wo && i0 + j >= 0)
+          Q[j][x] = __ldcs(reinterpret_cast<const float4*>(p.state + ((int64_t((i0 + j) % R) * p.plane) + pix0 + x) * p.C) + q);
+      }
+    const float4 bias4 = reinterpret_cast<const float4*>(bs)[q];
+    stage(0, 0);
+    for (int64_t t = 0; t < c.total; ++t) {
+      const int buf = int(t & 1);
+      if (t + 1 < c.total) {
+        __syncthreads();                                  // buffer buf ^ 1 is no longer read (frame t-1)
+        stage(int(t + 1), buf ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();                                    // frame t's halo visible to every thread
+      if (!active) continue;
+      const __nv_bfloat16* xs = xs0 + buf * buf_elems;
+      float4 acc[KT][PX];
+#pragma unroll
+      for (int k = 0; k < KT; ++k)
+#pragma unroll
+        for (int x = 0; x < PX; ++x) acc[k][x] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < KH; ++u) {
+        float4 xv[PX + KW - 1];
+        const __nv_bfloat16* xr = xs + (int64_t(r + u) * p.WC + wo0) * p.C + 4 * q;
+#pragma unroll
+        for (int tt = 0; tt < PX + KW - 1; ++tt) xv[tt] = ld_bf16x4(xr + int64_t(tt) * p.C);
+#pragma unroll
+        for (int v = 0; v < KW; ++v)
+#pragma unroll
+          for (int k = 0; k < KT; ++k) {
+            const float4 w = ws4[((k * KH + u) * KW + v) * p.Cq];
+#pragma unroll
+            for (int x = 0; x < PX; ++x) acc[k][x] = f4_fma(w, xv[x + v], acc[k][x]);
+          }
+      }
+      const bool emit = c.n0 + t >= c.d;
+#pragma unroll
+      for (int x = 0; x < PX; ++x) {
+        if (wo0 + x >= p.Wo) continue;
+        if (emit) {
+          float4 v = f4_add(acc[KT - 1][x], bias4);
+          if (KT > 1) v = f4_add(Q[0][x], v);
+          st_out4(p, b, (c.n0 + t - c.oi0) * p.HWo + pin0 + x, q, f4_act(v, p.act));
+        }
+        if (KT > 1) {
+#pragma unroll
+          for (int j = 1; j < KT - 1; ++j) Q[j - 1][x] = f4_add(Q[j][x], acc[KT - 1 - j][x]);
+          Q[NQ - 1][x] = acc[0][x];
+        }
+      }
+    }
+    const int64_t i1 = c.m0 + c.total - (KT - 1);
+#pragma unroll
+    for (int j = 0; j < NQ; ++j)
+#pragma unroll
+      for (int x = 0; x < PX; ++x)
+        if (KT > 1 && active && wo0 + x < p.Wo && i1 + j >= 0)
+          __stcs(reinterpret_cast<float4*>(p.state + ((int64_t((i1 + j) % R) * p.plane) + pix0 + x) * p.C) + q, Q[j][x]);
+  }
+}
+
 // ------------------------------------------------------------------ RAW layout
 // (SURVEY §8f f1): a Ready step reads the window's kt frames from the frame
 // ring (slot[k]) and writes y; no state traffic beyond those reads.  Thread =
@@ -471,7 +598,8 @@ struct DwVariant {
 #define CO_DW_PX 2                      // output pixels per thread strip (experiments: -DCO_DW_PX=n)
 #endif
 #define CO_DW_ST(kt, kh, kw) {kt, kh, kw, (DwFn)k_step_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>, \
-                              (kt <= 3 ? CO_DW_PX : 2), (DwFn)k_step_dw_raw<kt, kh, kw>}
+                              (kt <= 3 ? CO_DW_PX : 2), (DwFn)k_step_dw_raw<kt, kh, kw>, \
+                              (DwChunkFn)k_steps_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>}
 #define CO_DW_T(kt) {kt, 1, 1, (DwFn)k_step_dw_t<kt>, 1, (DwFn)k_step_dw_raw<kt, 1, 1>, (DwChunkFn)k_steps_dw_t<kt>}
 const DwVariant kDwVariants[] = {
     CO_DW_ST(1, 3, 3), CO_DW_ST(2, 3, 3), CO_DW_ST(3, 3, 3), CO_DW_ST(5, 3, 3), CO_DW_ST(3, 5, 5),
@@ -585,10 +713,34 @@ Depthwise* depthwise_create(const Geom& g, const void* w_dev, std::string& err) 
   return t;
 }
 
+// Chunked K2 tile plan: TH output rows per CTA with one thread per (quad, strip),
+// two halo buffers; 0 rows = not chunkable.
+static int st_chunk_rows(const Depthwise* t, const Geom& g, int& WC, size_t& smem) {
+  const int px = t->pl.var->PX;
+  const int spr = (g.Wo + px - 1) / px;
+  const int Cq = g.Cout / 4;
+  if (Cq * spr > 1024) return 0;
+  WC = std::max(g.W + 2 * g.pw, spr * px + g.kw - 1);
+  int TH = std::min(g.Ho, 1024 / (Cq * spr));
+  for (; TH >= 1; --TH) {
+    smem = size_t(g.kt * g.kh * g.kw + 1) * g.Cin * 4 + 2 * size_t(TH + g.kh - 1) * WC * g.Cin * 2;
+    if (smem <= 200 * 1024) return TH;
+  }
+  return 0;
+}
+
 bool depthwise_chunkable(const Depthwise* t, const Geom& g) {
   if (const char* e = getenv("CO_CHUNK"))       // experiment / test knob: 0 = always fold per step
     if (!atoi(e)) return false;
-  return t && t->pl.temporal && t->pl.var->chunk && !g.raw && g.st == 1 && g.dt == 1 && g.kt >= 2;
+  if (!t || !t->pl.var->chunk || g.raw || g.st != 1 || g.dt != 1 || g.kt < 2) return false;
+  if (t->pl.temporal) return true;
+  // chunked K2 (k_steps_dw_st) is correct but slower than the per-step K2 on C3-a
+  // (1.12 M vs 1.48 M stream-steps/s: shared-memory / latency bound at one
+  // 672-thread CTA per SM), so the stencil folds per step unless CO_CHUNK_ST=1
+  if (!(getenv("CO_CHUNK_ST") && atoi(getenv("CO_CHUNK_ST")))) return false;
+  int WC;
+  size_t smem;
+  return st_chunk_rows(t, g, WC, smem) > 0;
 }
 
 cudaError_t depthwise_steps(Depthwise* t, const Geom& g, const void* x, int64_t T, int64_t total, int64_t n0, void* y,
@@ -612,11 +764,28 @@ cudaError_t depthwise_steps(Depthwise* t, const Geom& g, const void* x, int64_t 
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  void* args[] = {&p, &c};
+  if (!t->pl.temporal) {   // K2c: one CTA per (stream, TH-row band), Cq x strips threads
+    int WC;
+    size_t smem;
+    const int TH = st_chunk_rows(t, g, WC, smem);
+    if (TH < 1) return cudaErrorInvalidValue;
+    p.H = g.H; p.W = g.W; p.ph = g.ph; p.pw = g.pw;
+    p.TH = TH; p.HR = TH + g.kh - 1; p.WC = WC;
+    p.bands = (g.Ho + TH - 1) / TH;
+    p.n_tiles = g.B * p.bands;
+    const int spr = (g.Wo + t->pl.var->PX - 1) / t->pl.var->PX;
+    const int threads = p.Cq * TH * spr;
+    cudaFuncSetAttribute(t->pl.var->chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, t->pl.var->chunk, threads, smem);
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(p.n_tiles, int64_t(sms) * std::max(per_sm, 1))));
+    return cudaLaunchKernel(reinterpret_cast<const void*>(t->pl.var->chunk), dim3(unsigned(grid)), dim3(threads),
+                            args, smem, s);
+  }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, t->pl.var->chunk, kDwThreads, 0);
   const int64_t items = p.plane * p.Cq;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>((items + kDwThreads - 1) / kDwThreads,
                                                               int64_t(sms) * std::max(per_sm, 1))));
-  void* args[] = {&p, &c};
   return cudaLaunchKernel(reinterpret_cast<const void*>(t->pl.var->chunk), dim3(unsigned(grid)), dim3(kDwThreads),
                           args, 0, s);
 }

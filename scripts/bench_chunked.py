@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Chunked vs per-step co_forward_steps (SURVEY §8f f2 -- "report them
-separately from online per-step numbers").  Workloads: C3's temporal depthwise
-layer (k_steps_dw_t: state in registers across the clip), C2's dense layer and
+separately from online per-step numbers").  Workloads: C3's depthwise layers
+(k_steps_dw_st / k_steps_dw_t: state in registers across the clip), C2's dense layer and
 C5's Conv1d (tcgen05: one launch per chunk, item-batch-major, so a tile's state
 stays L2-resident across its frames), each at its BASELINE.json stream count,
 driven through co_forward_steps over device clips of T frames (seeded N(0,1));
@@ -26,6 +26,7 @@ sys.path.insert(0, ROOT)
 
 
 WORKLOADS = {   # name: (BASELINE config id, layer index, description)
+    "c3a": (3, 0, "BASELINE.json configs[2] layer 1 (depthwise 3x3x3, C=192, 28x28; chunked K2 stencil)"),
     "c3b": (3, 1, "BASELINE.json configs[2] layer 2 (depthwise kt=5, C=192, 28x28)"),
     "c2": (2, 0, "BASELINE.json configs[1] (dense 3x3x3, 64->64, 56x56; tcgen05 HALO)"),
     "c5": (5, 0, "BASELINE.json configs[4] (Conv1d kt=9 dil 2, 256->256, 25 joints; tcgen05 FLAT pair)"),

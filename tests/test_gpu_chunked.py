@@ -159,3 +159,33 @@ def test_dense_chunked_matches_oracle():
     assert len(got) == len(ref) == 36 - (d.receptive_field - 1)
     g = np.stack(got)
     assert rel_err(g, np.stack(ref).reshape(g.shape)) <= 1e-4
+
+
+@pytest.mark.parametrize("kt,k,pad", [(3, 3, (0, 1, 1)), (2, 3, (1, 1, 1)), (5, 3, (2, 1, 1)), (3, 5, (0, 2, 2)),
+                                      (1, 3, (0, 1, 1))])
+def test_depthwise_stencil_chunked_equals_per_step(kt, k, pad, monkeypatch):
+    """Chunked K2 (k_steps_dw_st: halo staged per frame, state in registers)
+    equals the per-step K2 fold bit for bit, across consecutive calls."""
+    rng = np.random.default_rng(kt * 7 + k)
+    B, C, H, W = 2, 32, 6, 9
+    d = O.Desc(2, C, C, (kt, k, k), padding=pad, groups=C, in_spatial=(H, W))
+    Wt = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
+    bt = rng.standard_normal(C) * 0.1
+    monkeypatch.setenv("CO_CHUNK_ST", "1")        # off by default (slower); keep it covered
+    runs = {}
+    for chunk in ("1", "0"):
+        monkeypatch.setenv("CO_CHUNK", chunk)
+        conv, _, _, _ = make_pair(d, Wt, bt, B, dtype=torch.bfloat16, out_dtype=torch.float32, kernel="depthwise",
+                                  activation="relu")
+        rng2 = np.random.default_rng(3)
+        outs = []
+        for T in (2, kt + 5, 4):
+            ys, mask = conv.forward_steps(_clip(rng2, B, C, T, H, W))
+            outs.append((ys.clone(), mask.clone()))
+        st, _ = conv.state_dict_stream()
+        runs[chunk] = (outs, st.clone(), conv.kernel_name)
+    (oa, sa, ka), (ob, sb, kb) = runs["1"], runs["0"]
+    assert "k_step_dw_st" in ka
+    for (ya, ma), (yb, mb) in zip(oa, ob):
+        assert torch.equal(ma, mb) and torch.equal(ya, yb)
+    assert torch.equal(sa, sb)

@@ -123,11 +123,11 @@ def test_fullsize_step_equals_batch_all_streams(cid):
         torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("cid,layer", [(2, 0), (3, 1)])
+@pytest.mark.parametrize("cid,layer", [(2, 0), (3, 0), (3, 1)])
 def test_fullsize_chunked_steps_equal_per_step_fold(cid, layer, monkeypatch):
     """At the full stream count and frame size: co_forward_steps through the
     chunked kernels (tcgen05 HALO for C2, k_steps_dw_t for C3-b) equals the
-    per-step fold (CO_CHUNK=0) bit for bit -- outputs, ready mask and the
+    per-step fold (CO_CHUNK=0) bit for bit (C3-a: the chunked K2 stencil) -- outputs, ready mask and the
     canonical state after the clip."""
     import paper_2204_03418_b200 as co
     from paper_2204_03418_b200 import synth
@@ -135,6 +135,7 @@ def test_fullsize_chunked_steps_equal_per_step_fold(cid, layer, monkeypatch):
     L = cfg.layers[layer]
     Wt, bt = synth.params(cfg)[layer]
     T = 7
+    monkeypatch.setenv("CO_CHUNK_ST", "1")        # C3-a's chunked stencil is off by default; keep it covered
     g = torch.Generator(device="cuda").manual_seed(11)
     clip = co.channels_last(torch.randn((cfg.n_streams, L.cin, T) + tuple(cfg.in_spatial), generator=g,
                                         device="cuda").to(torch.bfloat16))
