@@ -44,7 +44,10 @@ constexpr int kDwThreads = 256;
 #define CO_DW_NB 2
 #endif
 constexpr int kNB = CO_DW_NB;           // K3 items per thread per batch (state loads in flight)
-constexpr size_t kHaloBudget = 72 * 1024;
+#ifndef CO_DW_HALO_KB
+#define CO_DW_HALO_KB 72                // K2 staged-halo bytes per CTA (experiments: -DCO_DW_HALO_KB=n)
+#endif
+constexpr size_t kHaloBudget = size_t(CO_DW_HALO_KB) * 1024;
 
 struct DwParams {
   const __nv_bfloat16* x;               // frame of stream 0 (nullptr = zero frame)
