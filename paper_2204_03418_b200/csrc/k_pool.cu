@@ -21,6 +21,7 @@
 // pixel, vector of V channels); consecutive threads take consecutive channel
 // vectors, so frame reads, ring accesses and output writes are coalesced
 // 16-byte accesses.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -35,6 +36,9 @@ namespace {
 // Temporal windows of at least this many taps use the block decomposition
 // (temporal_step VH) instead of the direct fold of kt-1 ring slots.
 constexpr int kVhMinKt = 6;
+}  // namespace
+bool pool_band_enabled();
+namespace {
 
 // Loads in flight per thread in the window loops (4 x 16 B: enough with >= 32
 // resident warps per SM; deeper chunks cost registers and occupancy).
@@ -357,6 +361,94 @@ __global__ void __launch_bounds__(256, (CH == 1 && KHW == 0) ? 4 : 2) k_step_poo
   }
 }
 
+// Row-band kernel for spatial windows (e.g. the I3D-style 3x3 s2 max pool): a
+// CTA takes a band of TH output rows of one stream, stages the input rows the
+// band's windows touch into shared memory with 16-byte cp.async (each input
+// row read from HBM once, however many windows overlap it -- the plain kernel
+// relies on L1 for that and measured 23% L1 hits on the stride-2 windows), then
+// thread = (output pixel of the band, channel vector) reduces its window from
+// shared memory in spatial_reduce's tap order (so the two kernels agree bit
+// for bit) and runs the temporal part.  Out-of-frame taps are skipped, so
+// MAX's -inf padding needs no fill.
+template <typename Tin, typename Tout, typename Tr, int V, bool MAX, bool VH>
+__global__ void __launch_bounds__(1024) k_step_pool_band(Geom g, StepArgs a, int TH, int rows) {
+  extern __shared__ __align__(16) uint8_t pool_smem[];
+  Tin* xs = reinterpret_cast<Tin*>(pool_smem);                  // [rows][W][C]
+  const int CV = g.Cin / V;
+  const int bands = (g.Ho + TH - 1) / TH;
+  const int64_t SE = g.B * g.HWo * g.Cin;
+  Tr* st = reinterpret_cast<Tr*>(a.state);
+  const Tin* x = static_cast<const Tin*>(a.x);
+  const int row_chunks = int(int64_t(g.W) * g.Cin * sizeof(Tin) / 16);
+  for (int64_t band = blockIdx.x; band < g.B * bands; band += gridDim.x) {
+    const int64_t b = band / bands;
+    const int ho0 = int(band % bands) * TH;
+    const int hi0 = ho0 * g.sh - g.ph;                             // first input row the band touches
+    __syncthreads();                                                // previous band finished reading xs
+    if (x) {
+      const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
+      for (int rr = 0; rr < rows; ++rr) {
+        const int hi = hi0 + rr;
+        if (hi < 0 || hi >= g.H) continue;
+        const char* src = reinterpret_cast<const char*>(x + b * a.x_bstride + int64_t(hi) * g.W * g.Cin);
+        for (int i = threadIdx.x; i < row_chunks; i += blockDim.x)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(base + uint32_t((rr * row_chunks + i) * 16)),
+                       "l"(src + int64_t(i) * 16)
+                       : "memory");
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+    __syncthreads();
+    const int th = min(TH, g.Ho - ho0);
+    for (int idx = threadIdx.x; idx < th * g.Wo * CV; idx += blockDim.x) {
+      const int c0 = (idx % CV) * V;
+      const int pl = idx / CV;                                      // pixel within the band
+      const int ho = ho0 + pl / g.Wo, wo = pl % g.Wo;
+      float s[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) s[j] = MAX ? -INFINITY : 0.f;
+      if (x) {
+        for (int u = 0; u < g.kh; ++u) {
+          const int hi = ho * g.sh - g.ph + u * g.dh;
+          if (hi < 0 || hi >= g.H) continue;
+          for (int v = 0; v < g.kw; ++v) {
+            const int wi = wo * g.sw - g.pw + v * g.dw;
+            if (wi < 0 || wi >= g.W) continue;
+            const Vec<Tin, V> xv = *reinterpret_cast<const Vec<Tin, V>*>(xs + ((hi - hi0) * g.W + wi) * g.Cin + c0);
+#pragma unroll
+            for (int j = 0; j < V; ++j) s[j] = MAX ? fmaxf(s[j], to_f(xv.v[j])) : s[j] + to_f(xv.v[j]);
+          }
+        }
+      }
+      const int64_t r = b * g.HWo + int64_t(ho) * g.Wo + wo;
+      float win[V];
+      temporal_step<Tr, V, MAX, VH, 1>(g, a, st, SE, r * g.Cin + c0, s, win);
+      if (a.emit)
+        store_out<Tout, V, MAX>(g, reinterpret_cast<Tout*>(a.y) + b * a.y_bstride + (r - b * g.HWo) * g.Cout + c0, win);
+    }
+  }
+}
+
+// Band plan: TH output rows whose input rows fit in ~96 KB of shared memory and
+// whose (pixel, vector) threads fit a 1024-thread CTA; 0 = no band kernel.
+int band_rows(const Geom& g, int V, int& rows, size_t& smem) {
+  if (g.kh * g.kw < 2 || (int64_t(g.W) * g.Cin * (g.in_dtype == BF16 ? 2 : 4)) % 16) return 0;
+  const size_t row_bytes = size_t(g.W) * g.Cin * (g.in_dtype == BF16 ? 2 : 4);
+  const int CV = g.Cin / V;
+  // one output row per CTA (measured best on max3: 74.7 us vs 84.6 us at 2 rows and
+  // 98.7 us at 4 -- small CTAs, many per SM, overlap one another's staging), or
+  // just enough rows for 128 threads
+  int th_max = std::min(g.Ho, std::min(1024 / std::max(1, g.Wo * CV), (128 + g.Wo * CV - 1) / std::max(1, g.Wo * CV)));
+  th_max = std::max(th_max, 1);
+  if (const char* e = getenv("CO_POOL_BAND_TH")) th_max = std::min(th_max, std::max(1, atoi(e)));   // A/B runs
+  for (int TH = th_max; TH >= 1; --TH) {
+    rows = (TH - 1) * g.sh + (g.kh - 1) * g.dh + 1;
+    smem = size_t(rows) * row_bytes;
+    if (smem <= 96 * 1024) return TH;
+  }
+  return 0;
+}
+
 // Few output rows (e.g. the expanded global pool: one 1x1 row per stream) give
 // the one-thread-per-vector kernel too few threads to cover HBM latency, so
 // this variant gives each output row (b, pixel) a block of G x CV threads:
@@ -530,6 +622,22 @@ cudaError_t step_v(const Geom& g, const StepArgs& a, cudaStream_t s) {
   const int64_t total = g.B * g.HWo * (g.Cin / V);
   const int grid = grid_for(total);
   const int khw = (g.dh == 1 && g.dw == 1 && g.kh <= 3 && g.kw <= 3 && g.kh == g.kw) ? g.kh * 10 + g.kw : 0;
+  int rows = 0;
+  size_t smem = 0;
+  const int TH = pool_band_enabled() ? band_rows(g, V, rows, smem) : 0;
+  if (TH > 0) {   // spatial window: stage the band's input rows once (k_step_pool_band)
+    const int threads = std::min(1024, (TH * g.Wo * (g.Cin / V) + 31) / 32 * 32);
+    const int64_t nb = g.B * ((g.Ho + TH - 1) / TH);
+    const void* fn = g.pool_vh ? (const void*)k_step_pool_band<Tin, Tout, Tr, V, MAX, true>
+                               : (const void*)k_step_pool_band<Tin, Tout, Tr, V, MAX, false>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+    const int bgrid = int(std::min<int64_t>(nb, int64_t(num_sms()) * std::max(per_sm, 1)));
+    if (g.pool_vh) k_step_pool_band<Tin, Tout, Tr, V, MAX, true><<<bgrid, threads, smem, s>>>(g, a, TH, rows);
+    else k_step_pool_band<Tin, Tout, Tr, V, MAX, false><<<bgrid, threads, smem, s>>>(g, a, TH, rows);
+    return cudaGetLastError();
+  }
   if (g.pool_vh) k_step_pool<Tin, Tout, Tr, V, MAX, kChunk, true><<<grid, 256, 0, s>>>(g, a);
   else if (khw == 33) k_step_pool<Tin, Tout, Tr, V, MAX, 1, false, 33><<<grid, 256, 0, s>>>(g, a);
   else if (khw == 22) k_step_pool<Tin, Tout, Tr, V, MAX, 1, false, 22><<<grid, 256, 0, s>>>(g, a);
@@ -624,6 +732,11 @@ cudaError_t launch_pool_rebuild(const Geom& g, void* state, int64_t m_next, cuda
                             : rebuild_t<float, true>(g, state, m_next, s);
 }
 
+bool pool_band_enabled() {
+  const char* e = getenv("CO_POOL_BAND");                       // A/B and test knob (default on)
+  return !e || atoi(e) != 0;
+}
+
 int pool_block_decomposition(const Geom& g) {
   if (const char* e = getenv("CO_POOL_VH")) return atoi(e) ? 1 : 0;   // experiment / test knob
   return g.kt >= kVhMinKt ? 1 : 0;
@@ -654,7 +767,11 @@ std::string pool_kernel_name(const Geom& g) {
   const int G = g.pool_G;
   const char* kind = g.op == OP_MAX_POOL ? "max" : "avg";
   const char* vh = g.pool_vh ? ",vh" : "";
+  int rows;
+  size_t smem;
   if (G > 1) snprintf(out, 64, "k_step_pool_split<%s,V%d,G%d%s>", kind, vec_width(g), G, vh);
+  else if (pool_band_enabled() && band_rows(g, vec_width(g), rows, smem) > 0)
+    snprintf(out, 64, "k_step_pool_band<%s,V%d%s>", kind, vec_width(g), vh);
   else snprintf(out, 64, "k_step_pool<%s,V%d%s>", kind, vec_width(g), vh);
   return out;
 }

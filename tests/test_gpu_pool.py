@@ -67,14 +67,17 @@ def _compare(kind, y, ref, out_dtype):
         assert rel_err(y, ref) <= 1e-4
 
 
-@pytest.fixture(params=[("auto", None), ("1", "0"), ("3", "0"), ("1", "1"), ("3", "1")],
-                ids=["auto", "G1_fold", "G3_fold", "G1_vh", "G3_vh"])
+@pytest.fixture(params=[("auto", None), ("1", "0"), ("3", "0"), ("1", "1"), ("3", "1"), ("1b", "0")],
+                ids=["auto", "G1_fold", "G3_fold", "G1_vh", "G3_vh", "G1_fold_noband"])
 def pool_lanes(request, monkeypatch):
     """Step-kernel variant (k_pool.cu): AUTO, or forced lanes (CO_POOL_G: 1 =
     plain kernel, 3 = split kernel) x temporal scheme (CO_POOL_VH: 0 = direct
     fold of the ring, 1 = block decomposition).  Returns "exact" when the
     variant reduces in the batch kernel's order (AVG bitwise step == batch)."""
     G, vh = request.param
+    if G == "1b":                                  # the plain kernel without the row-band staging
+        G = "1"
+        monkeypatch.setenv("CO_POOL_BAND", "0")
     if G != "auto":
         monkeypatch.setenv("CO_POOL_G", G)
         monkeypatch.setenv("CO_POOL_VH", vh)
