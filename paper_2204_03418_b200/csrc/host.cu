@@ -663,7 +663,10 @@ extern "C" int co_forward_steps(co_conv* h, const void* x, int64_t T, void* y, u
     constexpr int kTick = 2 + co::kMaxKt;
     std::vector<int> ticks(size_t(Tc) * kTick);
     int* dticks = nullptr;
-    CO_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dticks), ticks.size() * sizeof(int), s));
+    if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&dticks), ticks.size() * sizeof(int), s)) {
+      if (scratch) cudaFreeAsync(scratch, s);
+      return fail(CO_ERR_OOM, "tick table: %s", cudaGetErrorString(e));
+    }
     int last = 0;
     for (int64_t t0 = 0; t0 < T && rc == CO_OK; t0 += Tc) {
       const int64_t tn = std::min(Tc, T - t0);
@@ -1149,8 +1152,11 @@ extern "C" int co_state_clean_streams(co_conv* h, const uint8_t* mask, co_stream
   cudaStream_t s = (cudaStream_t)stream;
   int64_t* dids = nullptr;
   CO_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dids), ids.size() * sizeof(int64_t), s));
-  CO_CUDA(cudaMemcpyAsync(dids, ids.data(), ids.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-  cudaError_t e = cudaSuccess;
+  cudaError_t e = cudaMemcpyAsync(dids, ids.data(), ids.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(dids, s);
+    return fail(CO_ERR_CUDA, "clean streams: %s", cudaGetErrorString(e));
+  }
   const int nm = int(ids.size());
   if (!g.raw && g.op == CO_OP_CONV) {
     if (g.R > 0) e = co::launch_clean_streams_psum(g, h->state, dids, nm, s);
