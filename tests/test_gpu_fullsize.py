@@ -155,3 +155,70 @@ def test_fullsize_chunked_steps_equal_per_step_fold(cid, layer, monkeypatch):
     assert torch.equal(ma, mb) and int(ma.sum()) == T - (L.kernel[0] - 1)
     assert torch.equal(ya, yb)
     assert torch.equal(sa, sb)
+
+
+def _sampled(B):
+    return sorted({0, B // 2, B - 1})
+
+
+@pytest.mark.parametrize("name", ["x3d64", "max3"])
+def test_fullsize_pooling_sampled_streams_vs_oracle(name):
+    """scripts/bench_pool.py's workloads at their full stream counts, in the
+    bench's launch configuration: sampled streams against the fp64 pooling
+    oracle (MAX exact; AVG within 1e-4 of the RMS on fp32 outputs)."""
+    import paper_2204_03418_b200 as co
+    from oracle import pool as OP
+    import scripts.bench_pool as bp
+    w = bp.WORKLOADS[name]
+    B, C, H, W = w["B"], w["C"], w["H"], w["W"]
+    p = co.Pool(w["kind"], C, w["kernel"], stride=w["stride"], padding=w["padding"], in_spatial=(H, W), n_streams=B,
+                out_dtype=torch.float32)
+    assert p.kernel_name == co.Pool(w["kind"], C, w["kernel"], stride=w["stride"], padding=w["padding"],
+                                    in_spatial=(H, W), n_streams=B).kernel_name
+    sb = _sampled(B)
+    sms = {b: OP.PoolStep(w["kind"], C, (H, W), w["kernel"], w["stride"], w["padding"], (1, 1, 1), B=1) for b in sb}
+    g = torch.Generator(device="cuda").manual_seed(3)
+    n_ready = 0
+    for t in range(p.delay + 3):
+        x = co.channels_last(torch.randn((B, C, H, W), generator=g, device="cuda").to(torch.bfloat16))
+        y = p.forward_step(x)
+        for b in sb:
+            r = sms[b].forward_step(np_of(x[b:b + 1]))
+            assert (y is None) == (r is None)
+            if y is not None:
+                got = np_of(y[b:b + 1])
+                if w["kind"] == "max":
+                    np.testing.assert_array_equal(got, r.reshape(got.shape))
+                else:
+                    assert rel_err(got, r.reshape(got.shape)) <= 1e-4
+        n_ready += y is not None
+    assert n_ready == 3
+
+
+def test_fullsize_mha_sampled_streams_vs_oracle():
+    """scripts/bench_mha.py's workload (E=1024, 16 heads, window 64, 1024
+    streams): sampled streams against the fp64 MHA oracle at the bf16 bar."""
+    import paper_2204_03418_b200 as co
+    from oracle import mha as OM
+    B, E, H, n = 1024, 1024, 16, 64
+    rng = np.random.default_rng(4)
+    p = {"heads": H}
+    for k in ("Wq", "Wk", "Wv", "Wo"):
+        p[k] = torch.from_numpy(rng.standard_normal((E, E)) / np.sqrt(E)).to(torch.bfloat16).double().numpy()
+    for k in ("bq", "bk", "bv", "bo"):
+        p[k] = torch.from_numpy(rng.standard_normal(E) * 0.1).float().double().numpy()
+    m = co.MultiheadAttention(E, H, n, n_streams=B, out_dtype=torch.float32,
+                              in_proj_weight=torch.from_numpy(np.concatenate([p["Wq"], p["Wk"], p["Wv"]])),
+                              in_proj_bias=torch.from_numpy(np.concatenate([p["bq"], p["bk"], p["bv"]])),
+                              out_proj_weight=torch.from_numpy(p["Wo"]), out_proj_bias=torch.from_numpy(p["bo"]))
+    sb = _sampled(B)
+    sms = {b: OM.MhaStep(p, n, 1) for b in sb}
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for t in range(n + 2):
+        x = torch.randn((B, E), generator=g, device="cuda").to(torch.bfloat16)
+        y = m.forward_step(x)
+        for b in sb:
+            r = sms[b].forward_step(np_of(x[b:b + 1]))
+            assert (y is None) == (r is None)
+            if y is not None:
+                assert rel_err(np_of(y[b:b + 1]), r) <= 2e-2
