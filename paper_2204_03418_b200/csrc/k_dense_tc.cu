@@ -727,6 +727,12 @@ constexpr size_t kSmemLimit = 227 * 1024;
 // state loads and HBM throughput drops ~20% (measured: scripts/bw_probe.cu,
 // full bandwidth at 190 KB of shared memory, -18% at 200 KB).
 constexpr size_t kSmemBudget = 190 * 1024;
+// HALO (weights resident): a lower budget.  Its epilogue warps carry the whole
+// state RMW, so L1 room for in-flight loads beats deeper A pipelines:
+// C2 measured 1.19 M (one CTA, 173 KB) / 1.19 M (pair, 4 stages, 177 KB) /
+// 1.24 M (pair, 3 stages, 147 KB) / 1.20 M (pair, 2 stages, 117 KB); C4 layer 2
+// (pair) 0.438 ms at 164 KB, 0.391 ms at 134 KB.
+constexpr size_t kHaloBudget = 150 * 1024;
 
 // 128-B swizzled A operand (TMA boxes with 128-B rows instead of 16-B ones):
 // default on, CO_TC_SWA=0 restores the interleaved layout (A/B runs).
@@ -759,6 +765,21 @@ int pinned_eg() {
   return eg_env ? atoi(eg_env) : 0;
 }
 
+int pinned_cc() {
+  const char* v = getenv("CO_TC_CC");           // A/B runs only
+  return v ? atoi(v) : 0;
+}
+
+int pinned_ce() {
+  const char* v = getenv("CO_TC_CE");           // A/B runs only
+  return v ? atoi(v) : 0;
+}
+
+int pinned_stages() {
+  const char* v = getenv("CO_TC_STAGES");       // A/B runs only: cap the A pipeline depth
+  return v ? std::max(2, atoi(v)) : kMaxStages;
+}
+
 // HALO / FLAT: weights resident.  Largest CC whose weights + 2 A stages fit.
 bool plan_resident(const Geom& g, Plan& pl) {
   if (g.sh != 1 || g.sw != 1 || g.dh != 1 || g.dw != 1 || g.Cin % 16 != 0 || g.Cin / 8 > 256) return false;
@@ -782,6 +803,8 @@ bool plan_resident(const Geom& g, Plan& pl) {
   const int over = std::max(0, (max_row - a_rows) * (g.Cin % 64 == 0 && swa_enabled() ? 128 : 16));
   const size_t tail = size_t(std::max(0, over - (a_stride - a_bytes)));
   const int64_t K = int64_t(g.Cin) * g.kh * g.kw;
+  // FLAT (C5's 64 KB A stages) keeps the general budget: its pair fits only there
+  const size_t budget = flat ? kSmemBudget : kHaloBudget;
   const int eg_pin = pinned_eg();
   const char* pair_env = getenv("CO_TC_PAIR");    // A/B runs: pin 1 or 2
   const Variant* best = nullptr;
@@ -789,23 +812,24 @@ bool plan_resident(const Geom& g, Plan& pl) {
   for (const Variant& v : kVariants) {
     if (v.KT != g.kt || g.Cout % v.CC != 0) continue;
     if (v.KH && (v.KH != g.kh || v.KW != g.kw || v.KC * 16 != g.Cin)) continue;
-    if (eg_pin && v.EG != eg_pin) continue;
+    if ((eg_pin && v.EG != eg_pin) || (pinned_cc() && v.CC != pinned_cc()) || (pinned_ce() && v.CE != pinned_ce()))
+      continue;
     if (v.CS != pinned_cs() || (pair_env && v.PAIR != atoi(pair_env))) continue;
     const int64_t w_bytes = int64_t(v.KT * v.CC) * K * 2 / v.PAIR;   // per CTA
     const size_t fixed = 1024 + size_t((w_bytes + 1023) / 1024 * 1024) + 512 + v.CC * 4 + tail;
     if (fixed + 2 * size_t(a_stride) > kSmemLimit) continue;
-    const bool fits = fixed + 2 * size_t(a_stride) <= kSmemBudget;
-    // prefer: staying under the L1 cliff (a CTA pair halves the resident
-    // weights), a specialised (unrolled) variant, one CTA over a pair (measured
-    // faster on C2 when both fit: the pair's 64-channel epilogue costs more than
-    // its MMA saves), more channels per part, more epilogue groups
+    const bool fits = fixed + 2 * size_t(a_stride) <= budget;
+    // prefer: staying under the L1 budget (a CTA pair halves the resident
+    // weights), a specialised (unrolled) variant, one CTA over a pair when both
+    // fit (the pair's 64-channel epilogue costs more than its MMA saves), more
+    // channels per part, more epilogue groups
     const int64_t rank = (fits ? 100000000 : 0) + (v.KH ? 10000000 : 0) + (v.PAIR == 1 ? 1000000 : 0) + v.CC * 1000 + v.EG;
     if (rank > best_rank) {
       best = &v;
       best_rank = rank;
       pl.w_bytes = int(w_bytes);
-      const size_t cap = fits ? kSmemBudget : kSmemLimit;
-      pl.stages = int(std::min<size_t>(kMaxStages, (cap - fixed) / size_t(a_stride)));
+      const size_t cap = fits ? budget : kSmemLimit;
+      pl.stages = int(std::min<size_t>(pinned_stages(), (cap - fixed) / size_t(a_stride)));
       pl.smem = fixed + size_t(pl.stages) * a_stride;
     }
   }
@@ -864,7 +888,8 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
   const int stage = (b_off + b_bytes + 1023) / 1024 * 1024;
   const size_t fixed = 1024 + 512 + best->CC * 4;
   const size_t cap = (fixed + 2 * size_t(stage) <= kSmemBudget) ? kSmemBudget : kSmemLimit;
-  const int stages = int(std::min<size_t>(kMaxStages, (cap - fixed) / size_t(stage)));
+  const char* ks = getenv("CO_TC_KSTAGES");     // A/B runs only: cap the K pipeline depth
+  const int stages = int(std::min<size_t>(ks ? std::max(2, atoi(ks)) : kMaxStages, (cap - fixed) / size_t(stage)));
   if (stages < 2) return false;
   pl.var = best;
   pl.mode = MODE_KLOOP;

@@ -157,7 +157,7 @@ def test_fullsize_chunked_steps_equal_per_step_fold(cid, layer, monkeypatch):
     assert torch.equal(sa, sb)
 
 
-def _sampled(B):
+def _sample_streams(B):
     return sorted({0, B // 2, B - 1})
 
 
@@ -175,7 +175,7 @@ def test_fullsize_pooling_sampled_streams_vs_oracle(name):
                 out_dtype=torch.float32)
     assert p.kernel_name == co.Pool(w["kind"], C, w["kernel"], stride=w["stride"], padding=w["padding"],
                                     in_spatial=(H, W), n_streams=B).kernel_name
-    sb = _sampled(B)
+    sb = _sample_streams(B)
     sms = {b: OP.PoolStep(w["kind"], C, (H, W), w["kernel"], w["stride"], w["padding"], (1, 1, 1), B=1) for b in sb}
     g = torch.Generator(device="cuda").manual_seed(3)
     n_ready = 0
@@ -211,7 +211,7 @@ def test_fullsize_mha_sampled_streams_vs_oracle():
                               in_proj_weight=torch.from_numpy(np.concatenate([p["Wq"], p["Wk"], p["Wv"]])),
                               in_proj_bias=torch.from_numpy(np.concatenate([p["bq"], p["bk"], p["bv"]])),
                               out_proj_weight=torch.from_numpy(p["Wo"]), out_proj_bias=torch.from_numpy(p["bo"]))
-    sb = _sampled(B)
+    sb = _sample_streams(B)
     sms = {b: OM.MhaStep(p, n, 1) for b in sb}
     g = torch.Generator(device="cuda").manual_seed(5)
     for t in range(n + 2):
