@@ -93,6 +93,7 @@ struct TcParams {
   int ring_slot[kMaxKt];          // RAW layout: ring slot of temporal tap k
   int swa, a_rows;                // A staged swizzled: 0 none, 1 128-B rows ([Cin/64][rows][128 B]),
                                   // 2 64-B rows (KLOOP with kb = 32); rows per 64-channel block
+  int ystage, y_off;              // HALO bf16: y transposed through a per-warp shared-memory buffer at y_off
   int dbg;                        // CO_TC_DEBUG bits (experiments only): 1 no state/y traffic, 2 no MMA,
                                   // 4 no A loads, 8 no TMEM reads, 16 (with 2) no accumulator handshakes
   int Cq;
@@ -113,6 +114,14 @@ struct TcParams {
 
 __device__ __forceinline__ void bar_sync_named(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// state load without an L1 allocation (CO_TC_DEBUG bit 32: experiment)
+__device__ __forceinline__ float4 ld_state_na(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
@@ -159,6 +168,8 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   // 16-byte aligned: the epilogue reads the bias as float4
   float* bias_s = reinterpret_cast<float*>(bars + ((2 * kMaxStages + 2 * NBUF + 3 + 1) & ~1));
 
+  constexpr int NS = (KT > 1) ? KT - 1 : 1;            // state slots an item reads
+  constexpr int NQ = CE / 4;                           // channel quads per thread and pass
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int grid = gridDim.x;
@@ -406,8 +417,12 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   const int m = q * 32 + lane;                         // accumulator row = tile pixel
   const int64_t plane = p.plane;
   const int64_t stiles = p.splane >> 7;                // state tiles per slot (S[slot][tile][Cq][128][4])
-  constexpr int NQ = CE / 4;                           // channel quads per thread and pass
-  constexpr int NS = (KT > 1) ? KT - 1 : 1;
+  // y staging (p.ystage): this warp's 32 rows x CE bf16 channels, 16-B units
+  // swizzled so both the row-wise writes and the column-wise reads are
+  // conflict-free per quarter warp
+  constexpr int YU = CE / 8;                           // 16-B units per row
+  uint4* ybuf = reinterpret_cast<uint4*>(smem + p.y_off) + warp * 32 * YU;
+  auto yswz = [](int row) { return (row / (8 / YU)) & (YU - 1); };
   // One work (an item at one tick) of this group: buf / bph pick the accumulator,
   // tk the chunk's tick row (nullptr: the launch's single tick from p).  Called
   // from two loops so the one-step path keeps its own (lower) register use.
@@ -447,12 +462,18 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     for (int cb = cs * CPW; cb < (cs + 1) * CPW; cb += CE) {
       // ---- prefetch the state this pass needs (pass 0: before the accumulator is ready)
       float4 sv[NS][NQ];
-      if (KT > 1 && valid && !(p.dbg & 1)) {
+      if (p.dbg & 64) {
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) sv[k][i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (KT > 1 && valid && !(p.dbg & 65)) {
         if (emit) {
           const float4* src = reinterpret_cast<const float4*>(p.state) +
                               ((int64_t(slot(KT - 1)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
-          for (int i = 0; i < NQ; ++i) sv[0][i] = __ldcs(src + i * 128);
+          for (int i = 0; i < NQ; ++i) sv[0][i] = (p.dbg & 32) ? ld_state_na(src + i * 128) : __ldcs(src + i * 128);
         }
         if (p.update) {
 #pragma unroll
@@ -461,7 +482,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
             const float4* src = reinterpret_cast<const float4*>(p.state) +
                                 ((int64_t(slot(k)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
-            for (int i = 0; i < NQ; ++i) sv[k][i] = __ldcs(src + i * 128);
+            for (int i = 0; i < NQ; ++i) sv[k][i] = (p.dbg & 32) ? ld_state_na(src + i * 128) : __ldcs(src + i * 128);
           }
         }
       }
@@ -476,8 +497,9 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
         for (int c = 0; c < CE; c += 16) {
           if (!(p.dbg & 8)) ptx::tmem_ld16(t_row + uint32_t((KT - 1) * CC + cb + c), v);
           ptx::tc_wait_ld();
-          if (valid && !(p.dbg & 1)) {
+          if (!(p.dbg & 257)) {
             // y = (P + S) + b, the activation only behind a uniform branch
+            // (computed on every lane: the bf16 stores below pair lanes up)
 #pragma unroll
             for (int i = 0; i < 16; i += 4) {
               const float4 bb = *reinterpret_cast<const float4*>(bias_s + cb + c + i);
@@ -494,16 +516,65 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
             const int64_t yoff = b * p.y_bstride + yt + (pix - b * p.HWo) * p.Cout + c0 + cb + c;
             if (p.out_f32) {
               float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + yoff);
+              if (valid) {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) yp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                for (int i = 0; i < 4; ++i) yp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+              }
             } else {
-              uint4* yp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + yoff);
+              uint4 h[2];
 #pragma unroll
               for (int i = 0; i < 2; ++i)
-                yp[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
-                                   pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+                h[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                                  pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+              __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(p.y);
+              if (p.ystage) {                   // row = lane, written out after the pass
+                ybuf[lane * YU + (((c >> 3) + 0) ^ yswz(lane))] = h[0];
+                ybuf[lane * YU + (((c >> 3) + 1) ^ yswz(lane))] = h[1];
+              } else if (p.dbg & 512) {
+                if (valid) {
+                  reinterpret_cast<uint4*>(yb + yoff)[0] = h[0];
+                  reinterpret_cast<uint4*>(yb + yoff)[1] = h[1];
+                }
+              } else {
+                // A thread's 16 channels are one 32-B sector, written as two 16-B
+                // halves.  Lanes 2k / 2k+1 swap halves so that each store
+                // instruction writes whole sectors (even: its own first half and the
+                // partner's first half; odd: the partner's second half and its own),
+                // not 32 half sectors the L2 has to merge.
+                const bool odd = lane & 1;
+                const uint4 give = odd ? h[0] : h[1];
+                uint4 got;
+                got.x = __shfl_xor_sync(0xffffffffu, give.x, 1);
+                got.y = __shfl_xor_sync(0xffffffffu, give.y, 1);
+                got.z = __shfl_xor_sync(0xffffffffu, give.z, 1);
+                got.w = __shfl_xor_sync(0xffffffffu, give.w, 1);
+                const int64_t poff = __shfl_xor_sync(0xffffffffu, (long long)yoff, 1);
+                const bool pvalid = __shfl_xor_sync(0xffffffffu, int(valid), 1) != 0;
+                // store 1: the even lane's pixel (first half by even, second by odd)
+                if (odd ? pvalid : valid)
+                  *reinterpret_cast<uint4*>(yb + (odd ? poff + 8 : yoff)) = odd ? got : h[0];
+                // store 2: the odd lane's pixel
+                if (odd ? valid : pvalid)
+                  *reinterpret_cast<uint4*>(yb + (odd ? yoff + 8 : poff)) = odd ? h[1] : got;
+              }
             }
           }
+        }
+        if (p.ystage && !(p.dbg & 257)) {
+          // the warp's 32 rows go out row-contiguously: 32 / YU rows of CE
+          // channels per store instruction (whole 2 CE-byte runs, not 16-B pieces)
+          __syncwarp();
+          const int64_t ybase = b * p.y_bstride + yt + (pix - b * p.HWo) * p.Cout + c0 + cb;
+          __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(p.y);
+#pragma unroll
+          for (int j = 0; j < YU; ++j) {
+            const int q = j * (32 / YU) + lane / YU, k = lane % YU;
+            const uint4 val = ybuf[q * YU + (k ^ yswz(q))];
+            const int64_t qoff = __shfl_sync(0xffffffffu, (long long)ybase, q);
+            const bool qv = __shfl_sync(0xffffffffu, int(valid), q) != 0;
+            if (qv) *reinterpret_cast<uint4*>(yb + qoff + 8 * k) = val;
+          }
+          __syncwarp();
         }
       }
       if (p.update && KT > 1) {
@@ -522,7 +593,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
               for (int i = 0; i < 4; ++i) {
                 float4 t4 = sv[k][c / 4 + i];
                 t4.x += v[4 * i]; t4.y += v[4 * i + 1]; t4.z += v[4 * i + 2]; t4.w += v[4 * i + 3];
-                __stcs(dst + (c / 4 + i) * 128, t4);
+                if (!(p.dbg & 128)) __stcs(dst + (c / 4 + i) * 128, t4);
               }
             }
           }
@@ -538,7 +609,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
             if (valid && !(p.dbg & 1)) {
 #pragma unroll
               for (int i = 0; i < 4; ++i)
-                __stcs(dst + (c / 4 + i) * 128, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+                if (!(p.dbg & 128)) __stcs(dst + (c / 4 + i) * 128, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
             }
           }
         }
@@ -717,6 +788,7 @@ struct Plan {
   int n_split = 0, MT = 0, Wp = 0, tiles_per_stream = 0;
   int TH = 0, TW = 0, tiles_h = 0, tiles_w = 0, kb = 0, n_cb = 0, b_bytes = 0, b_off = 0;
   int a_bytes = 0, a_stride = 0, chunk_stride = 0, w_bytes = 0, w_off = 0, stages = 2;
+  int ystage = 0, y_off = 0;      // HALO bf16: y stores transposed through shared memory
   int64_t n_tiles = 0;
   size_t smem = 0;
 };
@@ -773,6 +845,13 @@ int pinned_cc() {
 int pinned_ce() {
   const char* v = getenv("CO_TC_CE");           // A/B runs only
   return v ? atoi(v) : 0;
+}
+
+// y stores transposed through shared memory (HALO, bf16 y): CO_TC_YSTAGE=0|1
+// overrides (A/B runs)
+int ystage_mode() {
+  const char* v = getenv("CO_TC_YSTAGE");
+  return v ? atoi(v) : 1;
 }
 
 int pinned_stages() {
@@ -834,6 +913,23 @@ bool plan_resident(const Geom& g, Plan& pl) {
     }
   }
   if (!best) return false;
+  if (!flat && ystage_mode() && best->CS == 1) {
+    // per epilogue warp 32 rows x CE bf16 channels, after the stages, the
+    // barriers / bias and the over-read tail
+    const size_t ybytes = size_t(best->EG) * 4 * 32 * best->CE * 2;
+    const size_t w_al = (size_t(pl.w_bytes) + 1023) / 1024 * 1024;
+    const size_t rest = 512 + best->CC * 4 + tail;
+    for (int st = pl.stages; st >= 2; --st) {
+      const size_t y_off = (w_al + size_t(st) * a_stride + rest + 1023) / 1024 * 1024;
+      if (1024 + y_off + ybytes <= kSmemLimit) {
+        pl.ystage = 1;
+        pl.y_off = int(y_off);
+        pl.stages = st;
+        pl.smem = 1024 + y_off + ybytes;
+        break;
+      }
+    }
+  }
   pl.var = best;
   pl.mode = flat ? MODE_FLAT : MODE_HALO;
   pl.MT = MT;
@@ -1017,8 +1113,8 @@ DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
     snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d%s%s>", pl.var->KT, pl.var->CC, pl.var->EG,
              pl.var->PAIR > 1 ? ",pair" : "", mname);
   if (getenv("CO_LOG"))
-    fprintf(stderr, "[co] %s: %d parts, %lld tiles, %d stages x %d B, smem %zu B\n", buf, pl.n_split,
-            (long long)pl.n_tiles, pl.stages, pl.a_stride, pl.smem);
+    fprintf(stderr, "[co] %s: %d parts, %lld tiles, %d stages x %d B, smem %zu B%s\n", buf, pl.n_split,
+            (long long)pl.n_tiles, pl.stages, pl.a_stride, pl.smem, pl.ystage ? ", y staged" : "");
   t->name = buf;
   return t;
 }
@@ -1172,6 +1268,8 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   p.emit = a.emit; p.update = a.update; p.act = g.act; p.out_f32 = (g.out_dtype == F32);
   static const int dbg = getenv("CO_TC_DEBUG") ? atoi(getenv("CO_TC_DEBUG")) : 0;
   p.dbg = dbg;
+  p.ystage = (pl.ystage && g.out_dtype == BF16) ? 1 : 0;
+  p.y_off = pl.y_off;
   p.raw_kh = g.raw ? g.kh : 0;
   p.kflat = pl.kflat;
   p.raw_B = int(g.B);

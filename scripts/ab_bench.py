@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--timeout", type=float, default=240, help="seconds per variant run")
     ap.add_argument("variants", nargs="*")
     a = ap.parse_args()
     for var in a.variants or [""]:
@@ -25,9 +26,13 @@ def main():
         for kv in var.split():
             k, v = kv.split("=", 1)
             env[k] = v
-        out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", str(a.config), "--steps",
-                              str(a.steps), "--warmup", str(a.warmup), "--no-e2e", "--no-cpu-baseline"],
-                             env=env, capture_output=True, text=True)
+        try:
+            out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", str(a.config),
+                                  "--steps", str(a.steps), "--warmup", str(a.warmup), "--no-e2e", "--no-cpu-baseline"],
+                                 env=env, capture_output=True, text=True, timeout=a.timeout)
+        except subprocess.TimeoutExpired:
+            print(f"[{var or 'default'}] timed out after {a.timeout:.0f} s", flush=True)
+            continue
         lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
         if not lines:
             print(f"[{var or 'default'}] failed: {out.stderr[-300:]}")
