@@ -91,8 +91,21 @@ __device__ __forceinline__ void st_out4(const DwParams& p, int64_t b, int64_t pi
 __device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
+// Packed fp32 FMA (sm_100 FFMA2): two IEEE fmas (round to nearest) per
+// instruction, so results equal fmaf lane by lane -- half the FMA issue slots
+// of the stencil, which is issue-bound at ~60% busy with scalar FFMA.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&c)));
+  return *reinterpret_cast<const float2*>(&d);
+}
 __device__ __forceinline__ float4 f4_fma(float4 w, float4 x, float4 acc) {
-  return make_float4(fmaf(w.x, x.x, acc.x), fmaf(w.y, x.y, acc.y), fmaf(w.z, x.z, acc.z), fmaf(w.w, x.w, acc.w));
+  const float2 lo = ffma2(make_float2(w.x, w.y), make_float2(x.x, x.y), make_float2(acc.x, acc.y));
+  const float2 hi = ffma2(make_float2(w.z, w.w), make_float2(x.z, x.w), make_float2(acc.z, acc.w));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 __device__ __forceinline__ float4 f4_act(float4 v, int act) {
   if (act == 1) {
