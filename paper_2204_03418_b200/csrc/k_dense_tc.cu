@@ -66,7 +66,12 @@ constexpr int kMaxStages = 6;   // operand pipeline depth: as many as fit in sha
 __host__ __device__ constexpr int tc_threads(int eg, int cs = 1) { return 32 * (4 * eg * cs + 2); }
 constexpr int kApad = 512;        // slack after each A stage (junk rows may read past the box)
 constexpr int kTickInts = 2 + kMaxKt;   // chunked steps: [emit, output index, slot[kMaxKt]] per tick
-enum { MODE_HALO = 0, MODE_FLAT = 1, MODE_KLOOP = 2 };
+constexpr int kMaxAStages = 4;  // KHALO: input-halo ring depth
+// KHALO: HALO's implicit im2col (one input-halo box per 64-channel block, the
+// spatial taps as shifted descriptors) with the weights streamed per (tap,
+// channel block) through the stage ring like KLOOP -- for stride-1 layers
+// whose weights do not fit in shared memory (C4 layer 4)
+enum { MODE_HALO = 0, MODE_FLAT = 1, MODE_KLOOP = 2, MODE_KHALO = 3 };
 
 struct TcParams {
   int B, H, W, Cin, Cout, Ho, Wo;
@@ -78,6 +83,7 @@ struct TcParams {
   int MT, Wp, tiles_per_stream;   // halo mode geometry
   int TH, TW, tiles_h, tiles_w;   // kloop output tile (TH x TW <= 128 pixels)
   int kb, n_cb;                   // kloop: input channels per K chunk, chunks per tap
+  int ka_stages, ka_stride;       // KHALO: input-halo ring (at the start of shared memory)
   int b_bytes, b_off;             // kloop: B chunk bytes, B offset inside a stage
   int64_t n_tiles, n_items;
   int n_split;
@@ -163,10 +169,12 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   uint64_t* acc_full = bars + 2 * kMaxStages;           // [NBUF]
   uint64_t* acc_empty = bars + 2 * kMaxStages + NBUF;   // [NBUF]
   uint64_t* w_full = bars + 2 * kMaxStages + 2 * NBUF;
-  uint64_t* w_peer = bars + 2 * kMaxStages + 2 * NBUF + 1;   // PAIR: the peer's weight half landed
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 2 * NBUF + 2);
+  uint64_t* w_peer = w_full + 1;                        // PAIR: the peer's weight half landed
+  uint64_t* a_full = w_full + 2;                        // [kMaxAStages] KHALO halo ring
+  uint64_t* a_empty = a_full + kMaxAStages;             // [kMaxAStages]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(a_empty + kMaxAStages);
   // 16-byte aligned: the epilogue reads the bias as float4
-  float* bias_s = reinterpret_cast<float*>(bars + ((2 * kMaxStages + 2 * NBUF + 3 + 1) & ~1));
+  float* bias_s = reinterpret_cast<float*>(bars + ((2 * kMaxStages + 2 * NBUF + 2 + 2 * kMaxAStages + 1 + 1) & ~1));
 
   constexpr int NS = (KT > 1) ? KT - 1 : 1;            // state slots an item reads
   constexpr int NQ = CE / 4;                           // channel quads per thread and pass
@@ -183,6 +191,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   const int part = unit % p.n_split;
   const int c0 = part * CC;                             // first output channel of this part
   const bool kloop = (p.mode == MODE_KLOOP);
+  const bool khalo = (p.mode == MODE_KHALO);
   constexpr int NB = N / PAIR;                          // weight rows held by this CTA
   auto tile_of = [&](int64_t item) -> int64_t { return (item / p.n_split) * PAIR + rank; };
 
@@ -191,6 +200,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     for (int e = 0; e < NBUF; ++e) { ptx::mbar_init(&acc_full[e], 1); ptx::mbar_init(&acc_empty[e], 128 * CS * PAIR); }
     ptx::mbar_init(w_full, 1);
     ptx::mbar_init(w_peer, 1);
+    for (int s = 0; s < kMaxAStages; ++s) { ptx::mbar_init(&a_full[s], 1); ptx::mbar_init(&a_empty[s], 1); }
     ptx::fence_mbar_init();
   }
   if (warp == kMma) {
@@ -210,7 +220,41 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wpack) + size_t(part * PAIR + rank) * p.w_bytes;
       int s = 0;
       uint32_t ph = 0;
-      if (!kloop) {
+      if (khalo) {
+        int as = 0;
+        uint32_t aph = 0;
+        for (int64_t item = unit; item < p.n_items; item += n_units) {
+          const int64_t tile = tile_of(item);
+          const int b = int(tile / p.tiles_per_stream);
+          const int ho0 = int(tile % p.tiles_per_stream) * p.MT;
+          for (int cb = 0; cb < p.n_cb; ++cb) {
+            // the 64-channel block's input halo, then its (tap) weight chunks
+            ptx::mbar_wait(&a_empty[as], aph ^ 1);
+            uint8_t* adst = smem + as * p.ka_stride;
+            if constexpr (PAIR == 2) {
+              if (leader) ptx::mbar_arrive_expect_tx(&a_full[as], p.a_bytes * PAIR);
+              ptx::tma_load_5d_pair(adst, &tmap, &a_full[as], 0, -p.pw, ho0 - p.ph, cb, b);
+            } else {
+              ptx::mbar_arrive_expect_tx(&a_full[as], p.a_bytes);
+              ptx::tma_load_5d(adst, &tmap, &a_full[as], 0, -p.pw, ho0 - p.ph, cb, b);
+            }
+            if (++as == p.ka_stages) { as = 0; aph ^= 1; }
+            for (int tap = 0; tap < p.kh * p.kw; ++tap) {
+              const int kblk = tap * p.n_cb + cb;       // packed K index (u kw + v) Cin + ci, in 64-blocks
+              ptx::mbar_wait(&empty[s], ph ^ 1);
+              uint8_t* dst = a_s + s * p.a_stride;
+              if constexpr (PAIR == 2) {
+                if (leader) ptx::mbar_arrive_expect_tx(&full[s], p.b_bytes * PAIR);
+                ptx::tma_load_4d_pair(dst, &wmap, &full[s], 0, 0, kblk, part * PAIR + int(rank));
+              } else {
+                ptx::mbar_arrive_expect_tx(&full[s], p.b_bytes);
+                ptx::bulk_g2s(dst, wsrc + size_t(kblk) * p.b_bytes, p.b_bytes, &full[s]);
+              }
+              if (++s == p.stages) { s = 0; ph ^= 1; }
+            }
+          }
+        }
+      } else if (!kloop) {
         ptx::mbar_arrive_expect_tx(w_full, p.w_bytes);
         for (int off = 0; off < p.w_bytes; off += 32768) {
           const int n = min(32768, p.w_bytes - off);
@@ -316,6 +360,44 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     };
     if (PAIR == 2 && !leader) {
       // the peer's tensor-core work is issued by the leader
+    } else if (khalo) {
+      const int taps = p.kh * p.kw;
+      const uint32_t ka_base = ptx::smem_u32(smem);
+      int as = 0;
+      uint32_t aph = 0;
+      for (int64_t item = unit; item < p.n_items; item += n_units) {
+        ptx::mbar_wait(&acc_empty[e], eph ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem + uint32_t(e * BUF);
+        for (int cb = 0; cb < p.n_cb; ++cb) {
+          ptx::mbar_wait(&a_full[as], aph);
+          ptx::tc_fence_after();
+          const uint64_t a0 = ptx::smem_desc_sw128(ka_base + uint32_t(as * p.ka_stride));
+          for (int tap = 0; tap < taps; ++tap) {
+            const int u = tap / p.kw, v = tap - (tap / p.kw) * p.kw;
+            ptx::mbar_wait(&full[s], ph);
+            ptx::tc_fence_after();
+            const uint32_t st = a_base + uint32_t(s * p.a_stride);
+            const uint64_t bd = (PAIR == 1) ? ptx::smem_desc(st, NB * 16, 128) : ptx::smem_desc_sw128(st);
+            const uint64_t bstep = (PAIR == 1) ? uint64_t(2 * NB) : 2u;
+            const uint64_t ad = a0 + uint64_t(u * p.Wp + v) * 8u;   // tap (u, v): shift by u Wp + v 128-B rows
+            if (ptx::elect_one()) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                mma(d_tmem, ad + uint64_t(j) * 2u, bd + uint64_t(j) * bstep, (cb | tap | j) ? 1u : 0u);
+              commit(&empty[s]);      // weight stage free once these MMAs retire
+            }
+            __syncwarp();
+            if (++s == p.stages) { s = 0; ph ^= 1; }
+          }
+          if (ptx::elect_one()) commit(&a_empty[as]);   // halo free after its last tap
+          __syncwarp();
+          if (++as == p.ka_stages) { as = 0; aph ^= 1; }
+        }
+        if (ptx::elect_one()) commit(&acc_full[e]);
+        __syncwarp();
+        if (++e == NBUF) { e = 0; eph ^= 1; }
+      }
     } else if (!kloop) {
       ptx::mbar_wait(w_full, 0);
       if constexpr (PAIR == 2) ptx::mbar_wait(w_peer, 0);
@@ -440,7 +522,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       pix = tile * 128 + m;
       valid = pix < plane;
       b = valid ? pix / p.HWo : 0;
-    } else if (p.mode == MODE_HALO) {
+    } else if (p.mode == MODE_HALO || p.mode == MODE_KHALO) {
       b = tile / p.tiles_per_stream;
       const int ho = int(tile % p.tiles_per_stream) * p.MT + m / p.Wp;
       const int wo = m % p.Wp;
@@ -789,6 +871,7 @@ struct Plan {
   int TH = 0, TW = 0, tiles_h = 0, tiles_w = 0, kb = 0, n_cb = 0, b_bytes = 0, b_off = 0;
   int a_bytes = 0, a_stride = 0, chunk_stride = 0, w_bytes = 0, w_off = 0, stages = 2;
   int ystage = 0, y_off = 0;      // HALO bf16: y stores transposed through shared memory
+  int ka_stages = 0, ka_stride = 0;   // KHALO input-halo ring
   int64_t n_tiles = 0;
   size_t smem = 0;
 };
@@ -852,6 +935,12 @@ int pinned_ce() {
 int ystage_mode() {
   const char* v = getenv("CO_TC_YSTAGE");
   return v ? atoi(v) : 1;
+}
+
+// KHALO for stride-1 K-pipeline layers (CO_TC_KHALO=0 keeps KLOOP: A/B runs)
+bool khalo_enabled() {
+  const char* v = getenv("CO_TC_KHALO");
+  return !v || atoi(v) != 0;
 }
 
 int pinned_stages() {
@@ -1004,6 +1093,36 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
   pl.n_tiles = g.B * pl.tiles_h * pl.tiles_w;
   pl.kflat = flat;
   if (flat) { pl.tiles_h = 1; pl.tiles_w = 1; pl.n_tiles = (g.B * g.HWo + 127) / 128; }
+  // KHALO: stride 1, 64-channel blocks, a halo TMA box (<= 256 rows of Wp <= 128)
+  const int Wp = g.Wo + g.kw - 1;
+  const int MT = Wp <= 128 ? std::min(128 / Wp, g.Ho) : 0;
+  if (khalo_enabled() && !flat && !g.raw && swa == 1 && g.sh == 1 && g.sw == 1 && g.dh == 1 && g.dw == 1 &&
+      MT > 0 && MT + g.kh - 1 <= 256) {
+    const int a_rows = Wp * (MT + g.kh - 1);
+    const int ka_bytes = a_rows * 128;
+    const int ka_stride = (ka_bytes + 1023) / 1024 * 1024;
+    const int b_stride = (b_bytes + 1023) / 1024 * 1024;
+    const int ka_stages = 2;
+    // the last halo stage's taps read up to (kh-1) Wp + kw - 1 rows past its
+    // start + 128: inside the weight ring that follows (junk rows, discarded)
+    const size_t fixed2 = fixed + size_t(ka_stages) * ka_stride;
+    const size_t cap2 = (fixed2 + 2 * size_t(b_stride) <= kSmemBudget) ? kSmemBudget : kSmemLimit;
+    const int bst = int(std::min<size_t>(ks ? std::max(2, atoi(ks)) : kMaxStages, (cap2 - fixed2) / size_t(b_stride)));
+    if (bst >= 2 && size_t((g.kh - 1) * Wp + g.kw - 1 + 128) * 128 <= size_t(ka_stride) + size_t(bst) * b_stride) {
+      pl.mode = MODE_KHALO;
+      pl.MT = MT; pl.Wp = Wp;
+      pl.tiles_per_stream = (g.Ho + MT - 1) / MT;
+      pl.n_tiles = g.B * pl.tiles_per_stream;
+      pl.TH = pl.TW = pl.tiles_h = pl.tiles_w = 0;
+      pl.a_bytes = ka_bytes;
+      pl.ka_stages = ka_stages; pl.ka_stride = ka_stride;
+      pl.a_stride = b_stride; pl.b_off = 0;
+      pl.stages = bst;
+      pl.w_off = ka_stages * ka_stride;
+      pl.chunk_stride = a_rows * 16;
+      pl.smem = fixed2 + size_t(bst) * b_stride;
+    }
+  }
   return true;
 }
 
@@ -1066,7 +1185,7 @@ void dense_tc_state_layout(Geom& g) {
     g.splane = (g.B * g.HWo + 127) / 128 * 128;
     return;
   }
-  if (pl.mode == MODE_HALO) {
+  if (pl.mode == MODE_HALO || pl.mode == MODE_KHALO) {
     g.sTH = pl.MT; g.sTW = g.Wo; g.sRS = pl.Wp; g.stiles_h = pl.tiles_per_stream; g.stiles_w = 1;
   } else {
     g.sTH = pl.TH; g.sTW = pl.TW; g.sRS = pl.TW; g.stiles_h = pl.tiles_h; g.stiles_w = pl.tiles_w;
@@ -1093,7 +1212,7 @@ DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
   }
   k_pack_tc_weights<<<unsigned((total + 255) / 256), 256>>>(wsrc, t->wpack, k.Cout, k.Cin, k.kt, k.kh, k.kw,
                                                            pl.var->CC, pl.n_split, pl.var->PAIR,
-                                                           (pl.mode == MODE_KLOOP && pl.var->PAIR == 2) ? pl.kb : 0);
+                                                           ((pl.mode == MODE_KLOOP || pl.mode == MODE_KHALO) && pl.var->PAIR == 2) ? pl.kb : 0);
   e = cudaGetLastError();
   if (wtmp) { cudaDeviceSynchronize(); cudaFree(wtmp); }
   if (e != cudaSuccess) { err = cudaGetErrorString(e); dense_tc_destroy(t); return nullptr; }
@@ -1104,7 +1223,7 @@ DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, dev);
   char buf[128];
-  const char* mname = pl.mode == MODE_KLOOP ? (pl.wcols ? ",kloop+wcols" : ",kloop") : "";
+  const char* mname = pl.mode == MODE_KLOOP ? (pl.wcols ? ",kloop+wcols" : ",kloop") : pl.mode == MODE_KHALO ? ",khalo" : "";
   if (pl.var->KH)
     snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d,%dx%dx%d%s%s%s>", pl.var->KT, pl.var->CC, pl.var->EG,
              pl.var->KH, pl.var->KW, pl.var->KC * 16, pl.var->CS > 1 ? ",split" : "",
@@ -1224,10 +1343,11 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
     cuuint64_t strides[4] = {cuuint64_t(k.Cin) * 2, cuuint64_t(k.W) * k.Cin * 2, 16, cuuint64_t(x_bstride) * 2};
     cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
     CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE;
-    if (pl.mode == MODE_HALO && pl.swa) {
-      // 64-channel (128-B) rows, swizzled: smem [Cin/64][halo rows][128 B]
+    if ((pl.mode == MODE_HALO && pl.swa) || pl.mode == MODE_KHALO) {
+      // 64-channel (128-B) rows, swizzled: smem [Cin/64][halo rows][128 B] (KHALO: one block per box)
       dims[0] = 64; dims[3] = cuuint64_t(k.Cin / 64); strides[2] = 128;
-      box[0] = 64; box[1] = cuuint32_t(pl.Wp); box[2] = cuuint32_t(pl.MT + k.kh - 1); box[3] = cuuint32_t(k.Cin / 64);
+      box[0] = 64; box[1] = cuuint32_t(pl.Wp); box[2] = cuuint32_t(pl.MT + k.kh - 1);
+      box[3] = pl.mode == MODE_KHALO ? 1u : cuuint32_t(k.Cin / 64);
       box[4] = 1;
       sw = CU_TENSOR_MAP_SWIZZLE_128B;
     } else if (pl.mode == MODE_HALO) {
@@ -1259,6 +1379,7 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   p.MT = pl.MT; p.Wp = pl.Wp; p.tiles_per_stream = pl.tiles_per_stream;
   p.TH = pl.TH; p.TW = pl.TW; p.tiles_h = pl.tiles_h; p.tiles_w = pl.tiles_w;
   p.kb = pl.kb; p.n_cb = pl.n_cb; p.b_bytes = pl.b_bytes; p.b_off = pl.b_off;
+  p.ka_stages = pl.ka_stages; p.ka_stride = pl.ka_stride;
   const int pair = pl.var->PAIR;
   const int64_t units_tiles = (pl.n_tiles + pair - 1) / pair;     // tiles per unit position (pairs take 2)
   p.n_tiles = pl.n_tiles; p.n_split = pl.n_split; p.n_items = units_tiles * pl.n_split;
@@ -1292,7 +1413,7 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   // KLOOP pairs stream their weight halves through a tensor map over the packed
   // weights [part*2 + half][K/8][N/2][8]: box = one chunk (kb/8 K-groups)
   CUtensorMap wmap = map;
-  if (pl.mode == MODE_KLOOP && pl.var->PAIR == 2) {
+  if ((pl.mode == MODE_KLOOP || pl.mode == MODE_KHALO) && pl.var->PAIR == 2) {
     const int NBh = pl.var->KT * pl.var->CC / 2;
     const int64_t nblk = int64_t(k.Cin) * k.kh * k.kw / pl.kb;        // kb-element K blocks
     cuuint64_t dims[4] = {cuuint64_t(pl.kb), cuuint64_t(NBh), cuuint64_t(nblk), cuuint64_t(pl.n_split * 2)};

@@ -18,8 +18,8 @@
 //  * K2 (spatial kh x kw stencil): persistent CTAs keep the packed fp32 weights
 //    [kt][kh][kw][C] in shared memory; per tile (stream, band of TH output
 //    rows) the input halo (TH+kh-1) x (W+2pw) x C is staged in shared memory by
-//    cp.async (16 B, zero-fill = spatial padding) while the first batch's state
-//    loads are already in flight; the 3x3 taps are then read from shared memory
+//    cp.async (16 B, zero-fill = spatial padding), then each strip issues its
+//    state loads before its taps; the 3x3 taps are read from shared memory
 //    (8 B per tap per thread, conflict-free: consecutive threads, consecutive
 //    8-byte words);
 //  * K3 (temporal-only, 1x1 spatial): a pure streaming kernel, no halo.

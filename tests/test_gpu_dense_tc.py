@@ -34,6 +34,12 @@ CASES = {
     "kloop_dil": dict(desc=O.Desc(2, 16, 32, (2, 3, 3), padding=(0, 2, 2), dilation=(1, 2, 2), in_spatial=(9, 9)), B=2),
     "kloop_wide": dict(desc=O.Desc(2, 16, 32, (3, 1, 3), stride=(1, 1, 2), padding=(0, 0, 1), in_spatial=(3, 300)), B=2),
     "kloop_kt1_s2": dict(desc=O.Desc(2, 64, 128, (1, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1), in_spatial=(10, 14)), B=3),
+    # KHALO: stride 1 with weights too large to stay resident -- one input-halo box
+    # per 64-channel block, taps as shifted descriptors, weights streamed (C4 layer 4)
+    "khalo_c4l4like": dict(desc=O.Desc(2, 256, 128, (3, 3, 3), padding=(0, 1, 1), in_spatial=(12, 20)), B=2),
+    "khalo_bigK": dict(desc=O.Desc(2, 256, 64, (3, 3, 3), padding=(0, 1, 1), in_spatial=(7, 9)), B=3),
+    "khalo_pt1": dict(desc=O.Desc(2, 192, 64, (3, 3, 3), padding=(1, 1, 1), in_spatial=(6, 30)), B=2),
+    "khalo_kt1_single": dict(desc=O.Desc(2, 256, 256, (1, 3, 3), padding=(0, 1, 1), in_spatial=(9, 11)), B=3),
     # small-Cin stems: W-im2col'd frame (C4 layer 1 shaped), KLOOP (stride 2) and HALO (stride 1)
     "stem_c4like": dict(desc=O.Desc(2, 3, 32, (5, 7, 7), stride=(1, 2, 2), padding=(0, 3, 3), in_spatial=(20, 22)), B=2),
     "stem_halo": dict(desc=O.Desc(2, 3, 16, (3, 3, 3), padding=(1, 1, 1), in_spatial=(9, 10)), B=2),
@@ -45,7 +51,8 @@ CASES = {
 }
 FORCE_KLOOP = {"halo_c2like", "halo_kt5", "flat_c5like"}   # also run these through the K pipeline
 PAIR_CASES = ["halo_c2like", "halo_c2like_oddtiles", "flat_c5full"]   # CTA-pair (cta_group::2) variants
-KPAIR_CASES = ["kloop_c4l3like", "kloop_bigK", "kloop_st3", "stem_c4like", "kloop_s2"]   # KLOOP CTA pairs
+KPAIR_CASES = ["kloop_c4l3like", "kloop_bigK", "kloop_st3", "stem_c4like", "kloop_s2",
+               "khalo_c4l4like"]   # KLOOP / KHALO CTA pairs
 
 
 def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force_kloop=False, pair=False):
@@ -60,6 +67,8 @@ def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force
         b = rng.standard_normal(d.cout) * 0.1
     if force_kloop:
         os.environ["CO_TC_MODE"] = "kloop"
+    if force_kloop or case.startswith("kloop"):
+        os.environ["CO_TC_KHALO"] = "0"              # keep the strided-gather K pipeline covered
     if pair:
         os.environ["CO_TC_PAIR"] = "2"
         os.environ["CO_TC_KPAIR"] = "2"
@@ -69,12 +78,16 @@ def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force
         os.environ.pop("CO_TC_MODE", None)
         os.environ.pop("CO_TC_PAIR", None)
         os.environ.pop("CO_TC_KPAIR", None)
+        os.environ.pop("CO_TC_KHALO", None)
     if pair:
         assert "pair" in conv.kernel_name, conv.kernel_name
     ref_conv, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="direct")
     assert conv.kernel_used == "dense_tc", conv.kernel_name
     if force_kloop or case.startswith("kloop") or case == "stem_c4like":  # (kloop_st3: spatial stride 2)
         assert "kloop" in conv.kernel_name, conv.kernel_name
+    if case.startswith("khalo"):
+        assert "khalo" in conv.kernel_name, conv.kernel_name
+        assert ("pair" in conv.kernel_name) == (not case.endswith("single")), conv.kernel_name
     H, Wd = d.in_hw
     shp = (B, d.cin) + ((H,) if d.spatial_rank >= 1 else ()) + ((Wd,) if d.spatial_rank >= 2 else ())
     steps = steps or (d.receptive_field + 4 + 3 * (d.stride[0] - 1))
@@ -135,7 +148,8 @@ def test_dense_tc_bf16_output(case):
     assert_bf16_rounding_bound(y, ref)
 
 
-@pytest.mark.parametrize("case", ["halo_c2like", "flat_c5like", "kloop_s2", "stem_c4like", "halo_st2", "kloop_st3"])
+@pytest.mark.parametrize("case", ["halo_c2like", "flat_c5like", "kloop_s2", "stem_c4like", "halo_st2", "kloop_st3",
+                                  "khalo_c4l4like", "khalo_pt1"])
 def test_dense_tc_state_and_steps(case):
     """State get vs oracle O5, update_state=False purity, forward_steps fold."""
     d, B = CASES[case]["desc"], CASES[case]["B"]
