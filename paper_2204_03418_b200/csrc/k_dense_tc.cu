@@ -60,7 +60,8 @@ namespace co {
 
 namespace {
 
-constexpr int kMaxStages = 6;   // operand pipeline depth: as many as fit in shared memory
+constexpr int kMaxStages = 8;   // operand pipeline depth (barrier slots): as many as fit in shared memory
+constexpr int kMaxStagesStd = 6;   // HALO / FLAT / KLOOP: 7-8 measured no better (C4 K-loop layers)
 // EG epilogue groups of 4*CS warps (CS warps share a TMEM lane quadrant and split
 // its columns), then the producer and MMA warps
 __host__ __device__ constexpr int tc_threads(int eg, int cs = 1) { return 32 * (4 * eg * cs + 2); }
@@ -69,8 +70,12 @@ constexpr int kTickInts = 2 + kMaxKt;   // chunked steps: [emit, output index, s
 constexpr int kMaxAStages = 4;  // KHALO: input-halo ring depth
 // KHALO: HALO's implicit im2col (one input-halo box per 64-channel block, the
 // spatial taps as shifted descriptors) with the weights streamed per (tap,
-// channel block) through the stage ring like KLOOP -- for stride-1 layers
-// whose weights do not fit in shared memory (C4 layer 4)
+// channel block) through the stage ring like KLOOP -- for layers whose weights
+// do not fit in shared memory (C4 layers 3-5).  Spatial stride s splits the
+// input into s x s phase sub-images (residues of the row / column mod s): tap
+// (u, v) reads phase ((u-ph) mod s, (v-pw) mod s) at a whole-row shift, and
+// each phase halo is one TMA box with elementStrides = s, so a stride-2 layer
+// stages ~4 (MT+1) x (Wo+1) rows per channel block instead of 9 x 128.
 enum { MODE_HALO = 0, MODE_FLAT = 1, MODE_KLOOP = 2, MODE_KHALO = 3 };
 
 struct TcParams {
@@ -84,6 +89,7 @@ struct TcParams {
   int TH, TW, tiles_h, tiles_w;   // kloop output tile (TH x TW <= 128 pixels)
   int kb, n_cb;                   // kloop: input channels per K chunk, chunks per tap
   int ka_stages, ka_stride;       // KHALO: input-halo ring (at the start of shared memory)
+  int ka_phase, dmin_h, dmin_w;   // KHALO: bytes per phase halo; first sub-row / column offset floor(-p / s)
   int b_bytes, b_off;             // kloop: B chunk bytes, B offset inside a stage
   int64_t n_tiles, n_items;
   int n_split;
@@ -231,13 +237,16 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
             // the 64-channel block's input halo, then its (tap) weight chunks
             ptx::mbar_wait(&a_empty[as], aph ^ 1);
             uint8_t* adst = smem + as * p.ka_stride;
-            if constexpr (PAIR == 2) {
-              if (leader) ptx::mbar_arrive_expect_tx(&a_full[as], p.a_bytes * PAIR);
-              ptx::tma_load_5d_pair(adst, &tmap, &a_full[as], 0, -p.pw, ho0 - p.ph, cb, b);
-            } else {
-              ptx::mbar_arrive_expect_tx(&a_full[as], p.a_bytes);
-              ptx::tma_load_5d(adst, &tmap, &a_full[as], 0, -p.pw, ho0 - p.ph, cb, b);
-            }
+            const int n_ph = p.sh * p.sw;
+            if (!(PAIR == 2 && !leader)) ptx::mbar_arrive_expect_tx(&a_full[as], p.a_bytes * n_ph * PAIR);
+            for (int rr = 0; rr < p.sh; ++rr)
+              for (int rc = 0; rc < p.sw; ++rc) {
+                // phase (rr, rc): original rows s (ho0 + dmin_h + i) + rr, columns s (dmin_w + j) + rc
+                uint8_t* pd = adst + (rr * p.sw + rc) * p.ka_phase;
+                const int r0 = p.sh * (ho0 + p.dmin_h) + rr, c0w = p.sw * p.dmin_w + rc;
+                if constexpr (PAIR == 2) ptx::tma_load_5d_pair(pd, &tmap, &a_full[as], 0, c0w, r0, cb, b);
+                else ptx::tma_load_5d(pd, &tmap, &a_full[as], 0, c0w, r0, cb, b);
+              }
             if (++as == p.ka_stages) { as = 0; aph ^= 1; }
             for (int tap = 0; tap < p.kh * p.kw; ++tap) {
               const int kblk = tap * p.n_cb + cb;       // packed K index (u kw + v) Cin + ci, in 64-blocks
@@ -363,6 +372,18 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     } else if (khalo) {
       const int taps = p.kh * p.kw;
       const uint32_t ka_base = ptx::smem_u32(smem);
+      // per-tap descriptor offset (16-B units): phase block + row shift, computed
+      // once (runtime-divisor divisions would otherwise sit in the issue loop)
+      uint32_t* tap_tab = reinterpret_cast<uint32_t*>(bias_s + CC);
+      for (int tap = lane; tap < taps; tap += 32) {
+        const int u = tap / p.kw, v = tap - (tap / p.kw) * p.kw;
+        // input row s ho + u - ph = s (ho + floor((u-ph)/s)) + (u-ph) mod s
+        const int eu = u - p.ph + p.sh * 8, ev = v - p.pw + p.sw * 8;   // shifted nonnegative
+        const int rr = eu % p.sh, rc = ev % p.sw;
+        const int du = eu / p.sh - 8 - p.dmin_h, dv = ev / p.sw - 8 - p.dmin_w;
+        tap_tab[tap] = uint32_t((rr * p.sw + rc) * p.ka_phase) / 16u + uint32_t(du * p.Wp + dv) * 8u;
+      }
+      __syncwarp();
       int as = 0;
       uint32_t aph = 0;
       for (int64_t item = unit; item < p.n_items; item += n_units) {
@@ -374,13 +395,12 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
           ptx::tc_fence_after();
           const uint64_t a0 = ptx::smem_desc_sw128(ka_base + uint32_t(as * p.ka_stride));
           for (int tap = 0; tap < taps; ++tap) {
-            const int u = tap / p.kw, v = tap - (tap / p.kw) * p.kw;
             ptx::mbar_wait(&full[s], ph);
             ptx::tc_fence_after();
             const uint32_t st = a_base + uint32_t(s * p.a_stride);
             const uint64_t bd = (PAIR == 1) ? ptx::smem_desc(st, NB * 16, 128) : ptx::smem_desc_sw128(st);
             const uint64_t bstep = (PAIR == 1) ? uint64_t(2 * NB) : 2u;
-            const uint64_t ad = a0 + uint64_t(u * p.Wp + v) * 8u;   // tap (u, v): shift by u Wp + v 128-B rows
+            const uint64_t ad = a0 + tap_tab[tap];     // phase block, then a du Wp + dv row shift
             if (ptx::elect_one()) {
 #pragma unroll
               for (int j = 0; j < 4; ++j)
@@ -871,7 +891,7 @@ struct Plan {
   int TH = 0, TW = 0, tiles_h = 0, tiles_w = 0, kb = 0, n_cb = 0, b_bytes = 0, b_off = 0;
   int a_bytes = 0, a_stride = 0, chunk_stride = 0, w_bytes = 0, w_off = 0, stages = 2;
   int ystage = 0, y_off = 0;      // HALO bf16: y stores transposed through shared memory
-  int ka_stages = 0, ka_stride = 0;   // KHALO input-halo ring
+  int ka_stages = 0, ka_stride = 0, ka_phase = 0, dmin_h = 0, dmin_w = 0;   // KHALO input-halo ring
   int64_t n_tiles = 0;
   size_t smem = 0;
 };
@@ -945,7 +965,7 @@ bool khalo_enabled() {
 
 int pinned_stages() {
   const char* v = getenv("CO_TC_STAGES");       // A/B runs only: cap the A pipeline depth
-  return v ? std::max(2, atoi(v)) : kMaxStages;
+  return v ? std::max(2, atoi(v)) : kMaxStagesStd;
 }
 
 // HALO / FLAT: weights resident.  Largest CC whose weights + 2 A stages fit.
@@ -1071,10 +1091,10 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
   int b_off = swa ? std::max(a_bytes, 128 * kb * 2) : (a_bytes + (128 - rows) * 16 + 127) / 128 * 128;
   if (best->PAIR == 2) b_off = (b_off + 1023) / 1024 * 1024;   // swizzled B rows: 1 KB-aligned atoms
   const int stage = (b_off + b_bytes + 1023) / 1024 * 1024;
-  const size_t fixed = 1024 + 512 + best->CC * 4;
+  const size_t fixed = 1024 + 512 + best->CC * 4 + 64 * 4;   // + the KHALO tap table
   const size_t cap = (fixed + 2 * size_t(stage) <= kSmemBudget) ? kSmemBudget : kSmemLimit;
   const char* ks = getenv("CO_TC_KSTAGES");     // A/B runs only: cap the K pipeline depth
-  const int stages = int(std::min<size_t>(ks ? std::max(2, atoi(ks)) : kMaxStages, (cap - fixed) / size_t(stage)));
+  const int stages = int(std::min<size_t>(ks ? std::max(2, atoi(ks)) : kMaxStagesStd, (cap - fixed) / size_t(stage)));
   if (stages < 2) return false;
   pl.var = best;
   pl.mode = MODE_KLOOP;
@@ -1093,29 +1113,43 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
   pl.n_tiles = g.B * pl.tiles_h * pl.tiles_w;
   pl.kflat = flat;
   if (flat) { pl.tiles_h = 1; pl.tiles_w = 1; pl.n_tiles = (g.B * g.HWo + 127) / 128; }
-  // KHALO: stride 1, 64-channel blocks, a halo TMA box (<= 256 rows of Wp <= 128)
-  const int Wp = g.Wo + g.kw - 1;
-  const int MT = Wp <= 128 ? std::min(128 / Wp, g.Ho) : 0;
-  if (khalo_enabled() && !flat && !g.raw && swa == 1 && g.sh == 1 && g.sw == 1 && g.dh == 1 && g.dw == 1 &&
-      MT > 0 && MT + g.kh - 1 <= 256) {
-    const int a_rows = Wp * (MT + g.kh - 1);
-    const int ka_bytes = a_rows * 128;
-    const int ka_stride = (ka_bytes + 1023) / 1024 * 1024;
+  // KHALO: stride s <= 2 (s x s phase halos), dilation 1, 64-channel blocks,
+  // phase boxes of <= 256 elements per dimension
+  auto fdiv = [](int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+  const int sh = g.sh, sw = g.sw;
+  const int dmin_h = fdiv(-g.ph, sh), dmin_w = fdiv(-g.pw, sw);
+  const int Wq = g.Wo + fdiv(g.kw - 1 - g.pw, sw) - dmin_w;     // phase-halo row width
+  const int MT = Wq <= 128 ? std::min(128 / Wq, g.Ho) : 0;
+  const int prow = MT + fdiv(g.kh - 1 - g.ph, sh) - dmin_h;      // phase-halo rows
+  if (khalo_enabled() && !flat && !g.raw && swa == 1 && sh == sw && sh <= 2 && g.dh == 1 && g.dw == 1 && MT > 0 &&
+      g.kh * g.kw <= 64 &&
+      prow * sh <= 256 && Wq * sw <= 256) {
+    const int a_rows = Wq * prow;
+    const int ka_phase = (a_rows * 128 + 1023) / 1024 * 1024;
+    const int ka_stride = ka_phase * sh * sw;
     const int b_stride = (b_bytes + 1023) / 1024 * 1024;
     const int ka_stages = 2;
-    // the last halo stage's taps read up to (kh-1) Wp + kw - 1 rows past its
-    // start + 128: inside the weight ring that follows (junk rows, discarded)
+    // the last phase's taps read up to (prow - MT) Wq + (Wq - Wo) rows past its
+    // start + 128: inside the next phase / stage / the weight ring (junk rows)
     const size_t fixed2 = fixed + size_t(ka_stages) * ka_stride;
-    const size_t cap2 = (fixed2 + 2 * size_t(b_stride) <= kSmemBudget) ? kSmemBudget : kSmemLimit;
-    const int bst = int(std::min<size_t>(ks ? std::max(2, atoi(ks)) : kMaxStages, (cap2 - fixed2) / size_t(b_stride)));
-    if (bst >= 2 && size_t((g.kh - 1) * Wp + g.kw - 1 + 128) * 128 <= size_t(ka_stride) + size_t(bst) * b_stride) {
+    // the K-pipelined layers are tensor-bound and their epilogues wait on the
+    // MMA, so the weight ring takes all of shared memory (C4: L3 1.73 -> 1.42 ms,
+    // L5 1.53 -> 1.39 ms against the 190 KB budget); CO_TC_KHALO_SMEM (KB) caps it
+    const char* kf = getenv("CO_TC_KHALO_SMEM");
+    const size_t cap2 = kf ? std::min(kSmemLimit, size_t(atoi(kf)) * 1024) : kSmemLimit;
+    const int bst = fixed2 + 2 * size_t(b_stride) <= cap2
+                        ? int(std::min<size_t>(ks ? std::max(2, atoi(ks)) : kMaxStages, (cap2 - fixed2) / size_t(b_stride)))
+                        : 0;
+    const size_t over = size_t((prow - MT) * Wq + (Wq - g.Wo) + 128) * 128;
+    if (bst >= 2 && over <= size_t(ka_phase) + size_t(bst) * b_stride) {
       pl.mode = MODE_KHALO;
-      pl.MT = MT; pl.Wp = Wp;
+      pl.MT = MT; pl.Wp = Wq;
       pl.tiles_per_stream = (g.Ho + MT - 1) / MT;
       pl.n_tiles = g.B * pl.tiles_per_stream;
       pl.TH = pl.TW = pl.tiles_h = pl.tiles_w = 0;
-      pl.a_bytes = ka_bytes;
-      pl.ka_stages = ka_stages; pl.ka_stride = ka_stride;
+      pl.a_bytes = a_rows * 128;                 // per phase box
+      pl.ka_stages = ka_stages; pl.ka_stride = ka_stride; pl.ka_phase = ka_phase;
+      pl.dmin_h = dmin_h; pl.dmin_w = dmin_w;
       pl.a_stride = b_stride; pl.b_off = 0;
       pl.stages = bst;
       pl.w_off = ka_stages * ka_stride;
@@ -1348,6 +1382,10 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
       dims[0] = 64; dims[3] = cuuint64_t(k.Cin / 64); strides[2] = 128;
       box[0] = 64; box[1] = cuuint32_t(pl.Wp); box[2] = cuuint32_t(pl.MT + k.kh - 1);
       box[3] = pl.mode == MODE_KHALO ? 1u : cuuint32_t(k.Cin / 64);
+      if (pl.mode == MODE_KHALO) {     // one phase sub-image: every s-th column / row
+        box[1] = cuuint32_t(pl.Wp * k.sw); box[2] = cuuint32_t((pl.a_bytes / 128 / pl.Wp) * k.sh);
+        es[1] = cuuint32_t(k.sw); es[2] = cuuint32_t(k.sh);
+      }
       box[4] = 1;
       sw = CU_TENSOR_MAP_SWIZZLE_128B;
     } else if (pl.mode == MODE_HALO) {
@@ -1379,7 +1417,8 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   p.MT = pl.MT; p.Wp = pl.Wp; p.tiles_per_stream = pl.tiles_per_stream;
   p.TH = pl.TH; p.TW = pl.TW; p.tiles_h = pl.tiles_h; p.tiles_w = pl.tiles_w;
   p.kb = pl.kb; p.n_cb = pl.n_cb; p.b_bytes = pl.b_bytes; p.b_off = pl.b_off;
-  p.ka_stages = pl.ka_stages; p.ka_stride = pl.ka_stride;
+  p.ka_stages = pl.ka_stages; p.ka_stride = pl.ka_stride; p.ka_phase = pl.ka_phase;
+  p.dmin_h = pl.dmin_h; p.dmin_w = pl.dmin_w;
   const int pair = pl.var->PAIR;
   const int64_t units_tiles = (pl.n_tiles + pair - 1) / pair;     // tiles per unit position (pairs take 2)
   p.n_tiles = pl.n_tiles; p.n_split = pl.n_split; p.n_items = units_tiles * pl.n_split;

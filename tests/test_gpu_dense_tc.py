@@ -40,6 +40,15 @@ CASES = {
     "khalo_bigK": dict(desc=O.Desc(2, 256, 64, (3, 3, 3), padding=(0, 1, 1), in_spatial=(7, 9)), B=3),
     "khalo_pt1": dict(desc=O.Desc(2, 192, 64, (3, 3, 3), padding=(1, 1, 1), in_spatial=(6, 30)), B=2),
     "khalo_kt1_single": dict(desc=O.Desc(2, 256, 256, (1, 3, 3), padding=(0, 1, 1), in_spatial=(9, 11)), B=3),
+    # strided KHALO: 2 x 2 phase sub-images, each one elementStrides = 2 TMA box (C4 layers 3 / 5)
+    "khalo_s2_c4l3like": dict(desc=O.Desc(2, 128, 128, (3, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1),
+                                          in_spatial=(12, 20)), B=2),
+    "khalo_s2_odd": dict(desc=O.Desc(2, 64, 64, (3, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1), in_spatial=(13, 17)),
+                         B=3),
+    "khalo_s2_nopad_single": dict(desc=O.Desc(2, 64, 32, (3, 3, 3), stride=(1, 2, 2), in_spatial=(11, 12)), B=2),
+    "khalo_s2_1x1": dict(desc=O.Desc(2, 64, 64, (3, 1, 1), stride=(1, 2, 2), in_spatial=(8, 10)), B=2),
+    "khalo_s2_kt1_single": dict(desc=O.Desc(2, 64, 128, (1, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1),
+                                            in_spatial=(10, 14)), B=3),
     # small-Cin stems: W-im2col'd frame (C4 layer 1 shaped), KLOOP (stride 2) and HALO (stride 1)
     "stem_c4like": dict(desc=O.Desc(2, 3, 32, (5, 7, 7), stride=(1, 2, 2), padding=(0, 3, 3), in_spatial=(20, 22)), B=2),
     "stem_halo": dict(desc=O.Desc(2, 3, 16, (3, 3, 3), padding=(1, 1, 1), in_spatial=(9, 10)), B=2),
@@ -52,7 +61,7 @@ CASES = {
 FORCE_KLOOP = {"halo_c2like", "halo_kt5", "flat_c5like"}   # also run these through the K pipeline
 PAIR_CASES = ["halo_c2like", "halo_c2like_oddtiles", "flat_c5full"]   # CTA-pair (cta_group::2) variants
 KPAIR_CASES = ["kloop_c4l3like", "kloop_bigK", "kloop_st3", "stem_c4like", "kloop_s2",
-               "khalo_c4l4like"]   # KLOOP / KHALO CTA pairs
+               "khalo_c4l4like", "khalo_s2_c4l3like"]   # KLOOP / KHALO CTA pairs
 
 
 def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force_kloop=False, pair=False):
@@ -149,7 +158,7 @@ def test_dense_tc_bf16_output(case):
 
 
 @pytest.mark.parametrize("case", ["halo_c2like", "flat_c5like", "kloop_s2", "stem_c4like", "halo_st2", "kloop_st3",
-                                  "khalo_c4l4like", "khalo_pt1"])
+                                  "khalo_c4l4like", "khalo_pt1", "khalo_s2_odd"])
 def test_dense_tc_state_and_steps(case):
     """State get vs oracle O5, update_state=False purity, forward_steps fold."""
     d, B = CASES[case]["desc"], CASES[case]["B"]
