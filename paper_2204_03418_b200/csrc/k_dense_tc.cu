@@ -1073,7 +1073,7 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
     if (getenv("CO_TC_KPAIR") && pair != want) break;
     for (const Variant& v : kVariants) {
       if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.CS != 1 || v.PAIR != pair) continue;
-      if (eg_pin && v.EG != eg_pin) continue;
+      if ((eg_pin && v.EG != eg_pin) || (pinned_cc() && v.CC != pinned_cc())) continue;
       // prefer the widest N (fewest A re-reads), then more groups; narrower
       // parts do not help few-row GEMMs (measured on the MHA projections: the
       // K pipeline's latency per item, not the SM count, bounds them)
