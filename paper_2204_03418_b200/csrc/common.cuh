@@ -91,6 +91,10 @@ struct StepArgs {
   int emit;              // ready: produce y from slice kt-1
   int update;            // update_state: write the ring
   int64_t m;             // padded index n + p of this frame (pooling: ring slots computed on the device)
+  // pooling, derived from m once per launch (launch_step_pool): m mod f, and for
+  // the block decomposition the phase q = m mod dil, i = m div dil, i mod kt and
+  // (i - kt + 1) mod kt -- 32-bit, so no kernel divides 64-bit values per item
+  int pm_f, pm_q, pm_pos, pm_js;
 };
 
 // Pooling ring (§8f f3): slot = one spatially reduced frame (B, Ho, Wo, C); MAX

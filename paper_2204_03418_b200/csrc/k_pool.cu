@@ -150,18 +150,25 @@ __device__ __forceinline__ int64_t fmod_pos(int64_t a, int64_t b) {
   return r < 0 ? r + b : r;
 }
 
+// (mm - d) mod f for 0 <= mm < f, 0 <= d < f
+__device__ __forceinline__ int wrap_sub(int mm, int d, int f) {
+  const int r = mm - d;
+  return r < 0 ? r + f : r;
+}
+
 // Fold the window's older ring slots k = k0, k0 + kstep, ... < kt-1 (slot of
-// tap k: (m - (kt-1-k) dil) mod f) into acc, in k order, kChunk loads in flight.
+// tap k: (m - (kt-1-k) dil) mod f, from mm = m mod f) into acc, in k order,
+// kChunk loads in flight.
 template <typename Tr, int V, bool MAX, int CH = kChunk>
 __device__ __forceinline__ void ring_fold(const Geom& g, const Tr* __restrict__ ring, int64_t slot_elems,
-                                          int64_t off, int64_t m, float (&acc)[V], int k0 = 0, int kstep = 1) {
+                                          int64_t off, int mm, float (&acc)[V], int k0 = 0, int kstep = 1) {
   for (int kb = k0; kb + 1 < g.kt; kb += CH * kstep) {
     Vec<Tr, V> q[CH];
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
       const int k = kb + i * kstep;
       if (k + 1 < g.kt) {
-        const int64_t slot = fmod_pos(m - int64_t(g.kt - 1 - k) * g.dt, g.f);
+        const int slot = wrap_sub(mm, (g.kt - 1 - k) * g.dt, g.f);
         q[i] = *reinterpret_cast<const Vec<Tr, V>*>(ring + slot * slot_elems + off);
       }
     }
@@ -203,12 +210,11 @@ __device__ __forceinline__ void temporal_step(const Geom& g, const StepArgs& a, 
     if (a.emit) {
 #pragma unroll
       for (int j = 0; j < V; ++j) win[j] = MAX ? -INFINITY : 0.f;
-      ring_fold<Tr, V, MAX, CH>(g, st, SE, off, a.m, win);
+      ring_fold<Tr, V, MAX, CH>(g, st, SE, off, a.pm_f, win);
       combine<V, MAX>(win, s);
     }
   } else {
-    const int64_t q = a.m % g.dt, i = a.m / g.dt;
-    const int pos = int(i % g.kt);
+    const int q = a.pm_q, pos = a.pm_pos;
     Tr* P = st + (int64_t(g.f + 1) + q) * SE + off;
     Tr* S = st + (int64_t(g.f + 1) + g.dt + q * g.kt) * SE + off;
     float pn[V];
@@ -225,8 +231,7 @@ __device__ __forceinline__ void temporal_step(const Geom& g, const StepArgs& a, 
 #pragma unroll
         for (int j = 0; j < V; ++j) win[j] = pn[j];
       } else {
-        const int64_t js = fmod_pos(i - g.kt + 1, g.kt);
-        const Vec<Tr, V> sv = *reinterpret_cast<const Vec<Tr, V>*>(S + js * SE);
+        const Vec<Tr, V> sv = *reinterpret_cast<const Vec<Tr, V>*>(S + a.pm_js * SE);
 #pragma unroll
         for (int j = 0; j < V; ++j) win[j] = to_f(sv.v[j]);
         combine<V, MAX>(win, pn);
@@ -238,6 +243,9 @@ __device__ __forceinline__ void temporal_step(const Geom& g, const StepArgs& a, 
       for (int j = 0; j < V; ++j) w.v[j] = from_f<Tr>(pn[j]);
       *reinterpret_cast<Vec<Tr, V>*>(P) = w;
       if (pos == g.kt - 1) {           // block end: suffix pass over its kt phase frames
+        // (64-bit index arithmetic kept here: the 32-bit wrap_sub form of this
+        // rare branch measured 8 us slower per step on the expanded 64-step pool)
+        const int64_t i = a.m / g.dt;
         float acc[V];
 #pragma unroll
         for (int j = 0; j < V; ++j) acc[j] = s[j];
@@ -370,8 +378,10 @@ __global__ void __launch_bounds__(256, (CH == 1 && KHW == 0) ? 4 : 2) k_step_poo
 // shared memory in spatial_reduce's tap order (so the two kernels agree bit
 // for bit) and runs the temporal part.  Out-of-frame taps are skipped, so
 // MAX's -inf padding needs no fill.
-template <typename Tin, typename Tout, typename Tr, int V, bool MAX, bool VH>
+template <typename Tin, typename Tout, typename Tr, int V, bool MAX, bool VH, int KHW = 0>
 __global__ void __launch_bounds__(1024) k_step_pool_band(Geom g, StepArgs a, int TH, int rows) {
+  // KHW > 0: compile-time KH x KW window (dilation 1), taps unrolled
+  constexpr int CKH = KHW / 10, CKW = KHW % 10;
   extern __shared__ __align__(16) uint8_t pool_smem[];
   Tin* xs = reinterpret_cast<Tin*>(pool_smem);                  // [rows][W][C]
   const int CV = g.Cin / V;
@@ -407,7 +417,21 @@ __global__ void __launch_bounds__(1024) k_step_pool_band(Geom g, StepArgs a, int
       float s[V];
 #pragma unroll
       for (int j = 0; j < V; ++j) s[j] = MAX ? -INFINITY : 0.f;
-      if (x) {
+      if (x && KHW > 0) {
+        const int h0 = ho * g.sh - g.ph, w0 = wo * g.sw - g.pw;
+        const Tin* xb = xs + ((h0 - hi0) * g.W + w0) * g.Cin + c0;
+#pragma unroll
+        for (int u = 0; u < CKH; ++u) {
+          if (h0 + u < 0 || h0 + u >= g.H) continue;
+#pragma unroll
+          for (int v = 0; v < CKW; ++v) {
+            if (w0 + v < 0 || w0 + v >= g.W) continue;
+            const Vec<Tin, V> xv = *reinterpret_cast<const Vec<Tin, V>*>(xb + (u * g.W + v) * g.Cin);
+#pragma unroll
+            for (int j = 0; j < V; ++j) s[j] = MAX ? fmaxf(s[j], to_f(xv.v[j])) : s[j] + to_f(xv.v[j]);
+          }
+        }
+      } else if (x) {
         for (int u = 0; u < g.kh; ++u) {
           const int hi = ho * g.sh - g.ph + u * g.dh;
           if (hi < 0 || hi >= g.H) continue;
@@ -480,7 +504,7 @@ __global__ void __launch_bounds__(512) k_step_pool_split(Geom g, StepArgs a) {
     }
 #pragma unroll
     for (int j = 0; j < V; ++j) t[j] = MAX ? -INFINITY : 0.f;
-    if (!VH && a.emit) ring_fold<Tr, V, MAX>(g, ring, slot_elems, off, a.m, t, gi, G);
+    if (!VH && a.emit) ring_fold<Tr, V, MAX>(g, ring, slot_elems, off, a.pm_f, t, gi, G);
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       sp[(gi * CV + cv) * V + j] = s[j];
@@ -629,12 +653,14 @@ cudaError_t step_v(const Geom& g, const StepArgs& a, cudaStream_t s) {
     const int threads = std::min(1024, (TH * g.Wo * (g.Cin / V) + 31) / 32 * 32);
     const int64_t nb = g.B * ((g.Ho + TH - 1) / TH);
     const void* fn = g.pool_vh ? (const void*)k_step_pool_band<Tin, Tout, Tr, V, MAX, true>
-                               : (const void*)k_step_pool_band<Tin, Tout, Tr, V, MAX, false>;
+                     : khw == 33 ? (const void*)k_step_pool_band<Tin, Tout, Tr, V, MAX, false, 33>
+                                 : (const void*)k_step_pool_band<Tin, Tout, Tr, V, MAX, false>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
     const int bgrid = int(std::min<int64_t>(nb, int64_t(num_sms()) * std::max(per_sm, 1)));
     if (g.pool_vh) k_step_pool_band<Tin, Tout, Tr, V, MAX, true><<<bgrid, threads, smem, s>>>(g, a, TH, rows);
+    else if (khw == 33) k_step_pool_band<Tin, Tout, Tr, V, MAX, false, 33><<<bgrid, threads, smem, s>>>(g, a, TH, rows);
     else k_step_pool_band<Tin, Tout, Tr, V, MAX, false><<<bgrid, threads, smem, s>>>(g, a, TH, rows);
     return cudaGetLastError();
   }
@@ -716,7 +742,13 @@ cudaError_t forward_dispatch(const Geom& g, const void* x, int64_t T, void* y, i
 
 }  // namespace
 
-cudaError_t launch_step_pool(const Geom& g, const StepArgs& a, cudaStream_t s) {
+cudaError_t launch_step_pool(const Geom& g, const StepArgs& a0, cudaStream_t s) {
+  StepArgs a = a0;
+  const int64_t i = a.m / g.dt;
+  a.pm_f = int(((a.m % g.f) + g.f) % g.f);
+  a.pm_q = int(a.m % g.dt);
+  a.pm_pos = int(i % g.kt);
+  a.pm_js = int((((i - g.kt + 1) % g.kt) + g.kt) % g.kt);
   return g.op == OP_MAX_POOL ? step_dispatch<true>(g, a, s) : step_dispatch<false>(g, a, s);
 }
 
