@@ -806,15 +806,22 @@ __global__ void k_wcols_weights(const __nv_bfloat16* __restrict__ w, __nv_bfloat
 // output pixel builds its KP channels in registers (unrolled, compile-time j)
 // and writes them as KP/8 16-byte stores (consecutive threads, consecutive
 // 2*KP-byte rows); the inputs it reads overlap its neighbours' (L1 hits).
-template <int KP>
+template <int KP, int CIN = 0>
 __global__ void __launch_bounds__(256) k_wcols_frame(const __nv_bfloat16* __restrict__ x, int64_t x_bstride,
                                                      __nv_bfloat16* __restrict__ xp, int64_t B, int H, int W,
-                                                     int Cin, int Wo, int kw, int sw, int dw, int pw) {
+                                                     int Cin_rt, int Wo, int kw, int sw, int dw, int pw) {
+  // CIN > 0: the channel count at compile time (RGB stems), so the unrolled
+  // j -> (v, c) split is free instead of a runtime division per channel
+  const int Cin = CIN > 0 ? CIN : Cin_rt;
   const int64_t total = B * H * Wo;
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  const int wo = int(i % Wo);
-  const int64_t r = i / Wo;
+  // the warp's 32 pixels are one contiguous run of xp: staged in shared memory
+  // and stored linearly, 512 contiguous bytes per store instruction
+  __shared__ __align__(16) uint4 stage[256 * (KP / 8)];
+  const bool live = i < total;                                  // (all lanes stay for the warp's stores)
+  const int64_t ic = live ? i : total - 1;
+  const int wo = int(ic % Wo);
+  const int64_t r = ic / Wo;
   const int h = int(r % H);
   const int64_t b = r / H;
   const __nv_bfloat16* xr = x ? x + b * x_bstride + int64_t(h) * W * Cin : nullptr;
@@ -828,9 +835,20 @@ __global__ void __launch_bounds__(256) k_wcols_frame(const __nv_bfloat16* __rest
     if (xr && v < kw && wi >= 0 && wi < W) val = xr[int64_t(wi) * Cin + c];
     vals[j] = val;
   }
-  uint4* dst = reinterpret_cast<uint4*>(xp + i * KP);
+  constexpr int U = KP / 8;                                     // 16-B units per pixel
+  const int lane = threadIdx.x & 31;
+  uint4* ws = stage + (threadIdx.x & ~31) * U;
+  const int64_t wbase = i - lane;
+  const int nw = (total - wbase) < 32 ? int(total - wbase) : 32;
 #pragma unroll
-  for (int t = 0; t < KP / 8; ++t) dst[t] = reinterpret_cast<const uint4*>(vals)[t];
+  for (int t = 0; t < U; ++t) ws[lane * U + ((t + lane) % U)] = reinterpret_cast<const uint4*>(vals)[t];
+  __syncwarp();
+  uint4* dst = reinterpret_cast<uint4*>(xp + wbase * KP);
+#pragma unroll
+  for (int t = 0; t < U; ++t) {
+    const int k = t * 32 + lane, px = k / U, u = k % U;
+    if (px < nw) dst[k] = ws[px * U + ((u + px) % U)];
+  }
 }
 
 typedef void (*KernFn)(const CUtensorMap, const CUtensorMap, const TcParams);
@@ -1332,7 +1350,10 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
     const __nv_bfloat16* xs = static_cast<const __nv_bfloat16*>(x);
     switch (pl.Kp) {
       case 16: k_wcols_frame<16><<<nb, 256, 0, s>>>(xs, x_bstride, t->xstage, g.B, g.H, g.W, g.Cin, g.Wo, g.kw, g.sw, g.dw, g.pw); break;
-      case 32: k_wcols_frame<32><<<nb, 256, 0, s>>>(xs, x_bstride, t->xstage, g.B, g.H, g.W, g.Cin, g.Wo, g.kw, g.sw, g.dw, g.pw); break;
+      case 32:
+        if (g.Cin == 3) k_wcols_frame<32, 3><<<nb, 256, 0, s>>>(xs, x_bstride, t->xstage, g.B, g.H, g.W, g.Cin, g.Wo, g.kw, g.sw, g.dw, g.pw);
+        else k_wcols_frame<32><<<nb, 256, 0, s>>>(xs, x_bstride, t->xstage, g.B, g.H, g.W, g.Cin, g.Wo, g.kw, g.sw, g.dw, g.pw);
+        break;
       case 48: k_wcols_frame<48><<<nb, 256, 0, s>>>(xs, x_bstride, t->xstage, g.B, g.H, g.W, g.Cin, g.Wo, g.kw, g.sw, g.dw, g.pw); break;
       default: k_wcols_frame<64><<<nb, 256, 0, s>>>(xs, x_bstride, t->xstage, g.B, g.H, g.W, g.Cin, g.Wo, g.kw, g.sw, g.dw, g.pw); break;
     }
