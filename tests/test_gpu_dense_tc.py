@@ -47,6 +47,9 @@ CASES = {
                          B=3),
     "khalo_s2_nopad_single": dict(desc=O.Desc(2, 64, 32, (3, 3, 3), stride=(1, 2, 2), in_spatial=(11, 12)), B=2),
     "khalo_s2_1x1": dict(desc=O.Desc(2, 64, 64, (3, 1, 1), stride=(1, 2, 2), in_spatial=(8, 10)), B=2),
+    "khalo_st2": dict(desc=O.Desc(2, 256, 64, (3, 3, 3), stride=(2, 1, 1), padding=(1, 1, 1), in_spatial=(6, 9)), B=2),
+    "khalo_tdil2_s2": dict(desc=O.Desc(2, 128, 64, (3, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1), dilation=(2, 1, 1),
+                                       in_spatial=(9, 13)), B=2),
     "khalo_s2_kt1_single": dict(desc=O.Desc(2, 64, 128, (1, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1),
                                             in_spatial=(10, 14)), B=3),
     # small-Cin stems: W-im2col'd frame (C4 layer 1 shaped), KLOOP (stride 2) and HALO (stride 1)
@@ -158,7 +161,7 @@ def test_dense_tc_bf16_output(case):
 
 
 @pytest.mark.parametrize("case", ["halo_c2like", "flat_c5like", "kloop_s2", "stem_c4like", "halo_st2", "kloop_st3",
-                                  "khalo_c4l4like", "khalo_pt1", "khalo_s2_odd"])
+                                  "khalo_c4l4like", "khalo_pt1", "khalo_s2_odd", "khalo_st2", "khalo_tdil2_s2"])
 def test_dense_tc_state_and_steps(case):
     """State get vs oracle O5, update_state=False purity, forward_steps fold."""
     d, B = CASES[case]["desc"], CASES[case]["B"]
