@@ -50,6 +50,9 @@ CASES = {
                                                      in_spatial=(6, 6)), B, torch.bfloat16, "depthwise", "psum", rng),
     "depthwise_t": lambda rng, B: _conv_case(O.Desc(2, 32, 32, (5, 1, 1), groups=32, in_spatial=(4, 5)), B,
                                              torch.bfloat16, "depthwise", "psum", rng),
+    # KHALO (weights streamed, stride-2 phase halos): the tile-padded state under per-stream clean masks
+    "dense_khalo_s2": lambda rng, B: _conv_case(O.Desc(2, 128, 64, (3, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1),
+                                                       in_spatial=(8, 10)), B, torch.bfloat16, "dense_tc", "psum", rng),
     "raw_dense": lambda rng, B: _conv_case(O.Desc(2, 32, 32, (3, 3, 3), padding=(1, 1, 1), in_spatial=(5, 6)), B,
                                            torch.bfloat16, "auto", "raw", rng),
 }
