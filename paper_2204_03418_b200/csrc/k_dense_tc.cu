@@ -1075,6 +1075,16 @@ bool plan_resident(const Geom& g, Plan& pl) {
 }
 
 // KLOOP: K streamed through a stage ring; any spatial stride/dilation <= 8.
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
 bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
   if (g.Cin % 16 != 0 || g.Cin / 8 > 256 || g.sh > 8 || g.sw > 8) return false;
   // flat: rows are 128 consecutive (stream, pixel) pairs (RAW 1x1 layers)
@@ -1092,10 +1102,15 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
     for (const Variant& v : kVariants) {
       if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.CS != 1 || v.PAIR != pair) continue;
       if ((eg_pin && v.EG != eg_pin) || (pinned_cc() && v.CC != pinned_cc())) continue;
-      // prefer the widest N (fewest A re-reads), then more groups; narrower
-      // parts do not help few-row GEMMs (measured on the MHA projections: the
-      // K pipeline's latency per item, not the SM count, bounds them)
-      auto rank = [](const Variant* x) { return x->CC * 1000 + x->EG; };
+      // prefer a width whose items fill at least half the SMs, then the widest
+      // N (fewest A re-reads), then more groups (MHA: the 1024 x 1024 output
+      // projection is 32 items at N = 256, 128 at N = 64)
+      const int64_t tiles = flat ? (g.B * g.HWo + 127) / 128 : g.B * ((g.Ho + TH - 1) / TH) * ((g.Wo + TW - 1) / TW);
+      auto rank = [&](const Variant* x) {
+        const int64_t items = (tiles + x->PAIR - 1) / x->PAIR * (g.Cout / x->CC) * x->PAIR;
+        const bool fills = getenv("CO_TC_FILL") && !atoi(getenv("CO_TC_FILL")) ? true : items * 2 >= sm_count();
+        return (fills ? 1000000 : 0) + x->CC * 1000 + x->EG;
+      };
       if (!best || rank(&v) > rank(best)) best = &v;
     }
     if (best) break;
