@@ -89,6 +89,8 @@ struct TcParams {
   int TH, TW, tiles_h, tiles_w;   // kloop output tile (TH x TW <= 128 pixels)
   int kb, n_cb;                   // kloop: input channels per K chunk, chunks per tap
   int ka_stages, ka_stride;       // KHALO: input-halo ring (at the start of shared memory)
+  int mc;                         // KLOOP, PAIR == 1: cluster of mc CTAs on consecutive row tiles of one
+                                  // part; each loads 1/mc of every weight chunk, multicast to all
   int ka_phase, dmin_h, dmin_w;   // KHALO: bytes per phase halo; first sub-row / column offset floor(-p / s)
   int b_bytes, b_off;             // kloop: B chunk bytes, B offset inside a stage
   int64_t n_tiles, n_items;
@@ -106,6 +108,7 @@ struct TcParams {
   int swa, a_rows;                // A staged swizzled: 0 none, 1 128-B rows ([Cin/64][rows][128 B]),
                                   // 2 64-B rows (KLOOP with kb = 32); rows per 64-channel block
   int ystage, y_off;              // HALO bf16: y transposed through a per-warp shared-memory buffer at y_off
+  int l2last;                     // HALO / FLAT: frame tiles loaded with an L2 evict_last policy
   int dbg;                        // CO_TC_DEBUG bits (experiments only): 1 no state/y traffic, 2 no MMA,
                                   // 4 no A loads, 8 no TMEM reads, 16 (with 2) no accumulator handshakes
   int Cq;
@@ -190,19 +193,22 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   // CTA pairs (cta_group::2, PAIR == 2): the cluster's two CTAs share one M = 256
   // MMA issued by the leader; each holds the A rows of its own 128-row tile and
   // half (N/2 rows) of the part's weights, so per-CTA weight shared memory halves.
-  const uint32_t rank = (PAIR == 2) ? ptx::cluster_ctarank() : 0u;
-  const bool leader = (rank == 0);
-  const int unit = blockIdx.x / PAIR;                   // work unit: a CTA or a CTA pair
-  const int n_units = grid / PAIR;
+  const int CLU = (PAIR == 2) ? 2 : p.mc;              // CTAs per cluster (pair / weight multicast group)
+  const uint32_t rank = (CLU > 1) ? ptx::cluster_ctarank() : 0u;
+  const bool leader = (PAIR == 1) || (rank == 0);
+  const uint16_t mc_mask = uint16_t((1u << CLU) - 1u);
+  const int unit = blockIdx.x / CLU;                    // work unit: a CTA, a CTA pair or a multicast cluster
+  const int n_units = grid / CLU;
   const int part = unit % p.n_split;
   const int c0 = part * CC;                             // first output channel of this part
   const bool kloop = (p.mode == MODE_KLOOP);
   const bool khalo = (p.mode == MODE_KHALO);
   constexpr int NB = N / PAIR;                          // weight rows held by this CTA
-  auto tile_of = [&](int64_t item) -> int64_t { return (item / p.n_split) * PAIR + rank; };
+  auto tile_of = [&](int64_t item) -> int64_t { return (item / p.n_split) * CLU + rank; };
 
   if (warp == kProducer && lane == 0) {
-    for (int s = 0; s < p.stages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    // multicast clusters: a stage is free once every CTA of the cluster consumed it
+    for (int s = 0; s < p.stages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], PAIR == 1 ? CLU : 1); }
     for (int e = 0; e < NBUF; ++e) { ptx::mbar_init(&acc_full[e], 1); ptx::mbar_init(&acc_empty[e], 128 * CS * PAIR); }
     ptx::mbar_init(w_full, 1);
     ptx::mbar_init(w_peer, 1);
@@ -215,7 +221,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   }
   for (int i = threadIdx.x; i < CC; i += blockDim.x) bias_s[i] = p.bias[c0 + i];
   ptx::tc_fence_before();
-  if constexpr (PAIR == 2) ptx::cluster_sync(); else __syncthreads();
+  if (CLU > 1) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
@@ -223,7 +229,9 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     // ===================== TMA producer =====================
     if (lane == 0) {
       ptx::prefetch_tmap(&tmap);
-      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wpack) + size_t(part * PAIR + rank) * p.w_bytes;
+      const uint64_t l2pol = p.l2last ? ptx::l2_policy_evict_last() : 0;
+      const uint8_t* wsrc =
+          reinterpret_cast<const uint8_t*>(p.wpack) + size_t(part * PAIR + (PAIR == 2 ? rank : 0u)) * p.w_bytes;
       int s = 0;
       uint32_t ph = 0;
       if (khalo) {
@@ -292,15 +300,27 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
               if (leader) ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes * PAIR);
               const int64_t tile = tile_of(item);
               uint8_t* dst = a_s + s * p.a_stride;
+              // p.l2last: the frame tile every channel part re-reads is kept in L2
+              // (evict_last) while the state streams through (evict_first)
               if (p.mode == MODE_FLAT) {
                 const int row = int(tile * 128 + t * p.a_trows);     // staged clip: frame t's rows
-                if constexpr (PAIR == 2) ptx::tma_load_3d_pair(dst, &tmap, &full[s], 0, row, 0);
-                else ptx::tma_load_3d(dst, &tmap, &full[s], 0, row, 0);
+                if (p.l2last) {
+                  if constexpr (PAIR == 2) ptx::tma_load_3d_pair_hint(dst, &tmap, &full[s], 0, row, 0, l2pol);
+                  else ptx::tma_load_3d_hint(dst, &tmap, &full[s], 0, row, 0, l2pol);
+                } else {
+                  if constexpr (PAIR == 2) ptx::tma_load_3d_pair(dst, &tmap, &full[s], 0, row, 0);
+                  else ptx::tma_load_3d(dst, &tmap, &full[s], 0, row, 0);
+                }
               } else {
                 const int b = int(tile / p.tiles_per_stream) * p.x_tmul + t;   // clip: (stream, frame) -> b T + t
                 const int ho0 = int(tile % p.tiles_per_stream) * p.MT;
-                if constexpr (PAIR == 2) ptx::tma_load_5d_pair(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
-                else ptx::tma_load_5d(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
+                if (p.l2last) {
+                  if constexpr (PAIR == 2) ptx::tma_load_5d_pair_hint(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b, l2pol);
+                  else ptx::tma_load_5d_hint(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b, l2pol);
+                } else {
+                  if constexpr (PAIR == 2) ptx::tma_load_5d_pair(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
+                  else ptx::tma_load_5d(dst, &tmap, &full[s], 0, -p.pw, ho0 - p.ph, 0, b);
+                }
               }
               if (++s == p.stages) { s = 0; ph ^= 1; }
             }
@@ -325,10 +345,19 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
                 uint8_t* dst = a_s + s * p.a_stride;
                 const int cw = wo0 * p.sw + v * p.dw - p.pw, ch = ho0 * p.sh + u * p.dh - p.ph;
                 const int cc = p.swa ? cb : cb * (p.kb / 8);   // swizzled: kb-channel blocks
+                // weight chunk: whole (one CTA), or this CTA's 1/mc byte range multicast to the cluster
+                auto load_b = [&]() {
+                  if (CLU > 1) {
+                    const uint32_t piece = uint32_t(p.b_bytes / CLU);
+                    ptx::bulk_g2s_mc(dst + p.b_off + rank * piece, bsrc + rank * piece, piece, &full[s], mc_mask);
+                  } else {
+                    ptx::bulk_g2s(dst + p.b_off, bsrc, p.b_bytes, &full[s]);
+                  }
+                };
                 if (p.kflat) {    // rows tile*128 .. of ring slot k, viewed as a (B*HW, Cin) matrix
                   ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes + p.b_bytes);
                   ptx::tma_load_4d(dst, &tmap, &full[s], 0, int(tile * 128), cc, p.ring_slot[kk]);
-                  ptx::bulk_g2s(dst + p.b_off, bsrc, p.b_bytes, &full[s]);
+                  load_b();
                 } else if constexpr (PAIR == 2) {
                   if (leader) ptx::mbar_arrive_expect_tx(&full[s], (p.a_bytes + p.b_bytes) * PAIR);
                   ptx::tma_load_5d_pair(dst, &tmap, &full[s], 0, cw, ch, cc, bb);
@@ -336,7 +365,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
                 } else {
                   ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes + p.b_bytes);
                   ptx::tma_load_5d(dst, &tmap, &full[s], 0, cw, ch, cc, bb);
-                  ptx::bulk_g2s(dst + p.b_off, bsrc, p.b_bytes, &full[s]);
+                  load_b();
                 }
                 bsrc += p.b_bytes;
                 kg += p.kb / 8;
@@ -499,7 +528,9 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               if (j < nk) mma(d_tmem, ad + uint64_t(j) * astep, bd + uint64_t(j) * bstep, (ch | j) ? 1u : 0u);
-            commit(&empty[s]);    // stage free once these MMAs retire
+            // stage free once these MMAs retire (multicast: in every CTA of the cluster)
+            if (PAIR == 1 && CLU > 1) ptx::tc_commit_mc(&empty[s], mc_mask);
+            else commit(&empty[s]);
           }
           __syncwarp();
           if (++s == p.stages) { s = 0; ph ^= 1; }
@@ -743,7 +774,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   }
   // ===================== teardown (all threads) =====================
   ptx::tc_fence_before();
-  if constexpr (PAIR == 2) ptx::cluster_sync(); else __syncthreads();
+  if (CLU > 1) ptx::cluster_sync(); else __syncthreads();   // no CTA leaves while peers may still signal it
   if (warp == kMma) {
     ptx::tc_fence_after();
     if constexpr (PAIR == 2) ptx::tmem_dealloc_pair(tmem, TMEM_COLS);
@@ -1456,7 +1487,15 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   p.ka_stages = pl.ka_stages; p.ka_stride = pl.ka_stride; p.ka_phase = pl.ka_phase;
   p.dmin_h = pl.dmin_h; p.dmin_w = pl.dmin_w;
   const int pair = pl.var->PAIR;
-  const int64_t units_tiles = (pl.n_tiles + pair - 1) / pair;     // tiles per unit position (pairs take 2)
+  // weight-multicast clusters for one-CTA K-pipeline layers (CO_TC_MC = cluster size, A/B runs)
+  int mc = 1;
+  if (pl.mode == MODE_KLOOP && pair == 1 && T == 1) {
+    const char* e = getenv("CO_TC_MC");
+    mc = e ? std::max(1, std::min(8, atoi(e))) : 1;
+    while (mc > 1 && ((pl.b_bytes / 16) % mc != 0 || pl.n_tiles < mc)) mc /= 2;
+  }
+  const int clu = pair > 1 ? pair : mc;                  // CTAs per cluster
+  const int64_t units_tiles = (pl.n_tiles + clu - 1) / clu;       // tiles per unit position (clusters take clu)
   p.n_tiles = pl.n_tiles; p.n_split = pl.n_split; p.n_items = units_tiles * pl.n_split;
   p.a_bytes = pl.a_bytes; p.a_stride = pl.a_stride; p.stages = pl.stages; p.chunk_stride = pl.chunk_stride;
   p.w_bytes = pl.w_bytes; p.w_off = pl.w_off;
@@ -1465,6 +1504,10 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   static const int dbg = getenv("CO_TC_DEBUG") ? atoi(getenv("CO_TC_DEBUG")) : 0;
   p.dbg = dbg;
   p.ystage = (pl.ystage && g.out_dtype == BF16) ? 1 : 0;
+  {
+    const char* e = getenv("CO_TC_L2LAST");     // A/B runs
+    p.l2last = (pl.mode == MODE_HALO || pl.mode == MODE_FLAT) && (e ? atoi(e) != 0 : false);
+  }
   p.y_off = pl.y_off;
   p.raw_kh = g.raw ? g.kh : 0;
   p.kflat = pl.kflat;
@@ -1483,8 +1526,9 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   p.y_bstride = a.y_bstride;
   p.wpack = t->wpack;
   p.bias = bias;
-  const int per = std::max(1, t->num_sms / pair / pl.n_split);
-  const int64_t grid = std::min<int64_t>(per, units_tiles) * pl.n_split * pair;
+  p.mc = mc;
+  const int per = std::max(1, t->num_sms / clu / pl.n_split);
+  const int64_t grid = std::min<int64_t>(per, units_tiles) * pl.n_split * clu;
   // KLOOP pairs stream their weight halves through a tensor map over the packed
   // weights [part*2 + half][K/8][N/2][8]: box = one chunk (kb/8 K-groups)
   CUtensorMap wmap = map;
@@ -1507,9 +1551,9 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  if (pair > 1) {
+  if (clu > 1) {
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = unsigned(pair);
+    attr[0].val.clusterDim.x = unsigned(clu);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;

@@ -143,6 +143,20 @@ def test_dense_tc_cta_pair(case):
     assert np.array_equal(y, ref)
 
 
+@pytest.mark.parametrize("case", ["kloop_s2", "kloop_dil", "stem_c4like", "kloop_kt1_s2"])
+@pytest.mark.parametrize("mc", ["2", "4"])
+def test_dense_tc_weight_multicast(case, mc, monkeypatch):
+    """One-CTA K-pipeline layers in weight-multicast clusters (CO_TC_MC): each
+    CTA loads 1/mc of every weight chunk and multicasts it, stages are released
+    by every CTA's commit -- same results as the oracle, bit for bit in the
+    integer regime."""
+    monkeypatch.setenv("CO_TC_MC", mc)
+    _, y, ref, yd = _run(case)
+    assert rel_err(y, ref) <= 1e-4 and rel_err(y, yd) <= 1e-4
+    _, y, ref, _ = _run(case, integer=True)
+    assert np.array_equal(y, ref)
+
+
 @pytest.mark.parametrize("case", sorted(FORCE_KLOOP))
 def test_dense_tc_forced_kloop(case):
     """The same layers through the K pipeline (CO_TC_MODE=kloop) agree with the oracle."""
