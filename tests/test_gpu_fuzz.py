@@ -1,0 +1,71 @@
+"""Seeded random-shape sweep of the dispatched bf16 kernels (tcgen05 HALO / FLAT /
+KLOOP / KHALO, pairs, depthwise) against the generic CUDA-core kernel
+(k_step_direct, itself pinned to the fp64 oracle in test_gpu_direct.py) on the
+same inputs, over enough ticks to pass the delay: the planner's corner cases
+(ragged tiles, odd stream counts, phase halos of odd sizes, temporal stride and
+dilation) at sizes the oracle would take minutes for.  fp32 outputs, bar 1e-4
+of the RMS (A16: both sides accumulate exact bf16 products in fp32).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from tests.helpers import np_of, rel_err, to_cl
+
+pytestmark = pytest.mark.gpu
+
+
+def _shape(rng):
+    dense = rng.random() < 0.75
+    kt = int(rng.choice([1, 2, 3, 5]))
+    kh = int(rng.choice([1, 3, 3, 5]))
+    s = int(rng.choice([1, 1, 2]))
+    ph = kh // 2 if rng.random() < 0.8 else 0
+    pt = int(rng.integers(0, kt)) if rng.random() < 0.3 else 0
+    st = 2 if (kt > 1 and rng.random() < 0.2) else 1
+    dt = 2 if (kt > 1 and st == 1 and rng.random() < 0.2) else 1
+    H = int(rng.integers(kh + 2, 30))
+    W = int(rng.integers(kh + 2, 40))
+    if dense:
+        cin = int(rng.choice([16, 32, 64, 128, 192, 256]))
+        cout = int(rng.choice([16, 32, 64, 96, 128, 160, 256]))
+        groups = 1
+    else:
+        cin = cout = groups = int(rng.choice([32, 64, 96]))
+        s = 1
+    if pt > dt * (kt - 1):
+        pt = 0
+    d = O.Desc(2, cin, cout, (kt, kh, kh), stride=(st, s, s), padding=(pt, ph, ph), dilation=(dt, 1, 1),
+               groups=groups, in_spatial=(H, W))
+    B = int(rng.integers(1, 6))
+    return d, B
+
+
+CASES = list(range(120))   # ~40% KHALO, ~35% HALO / FLAT, ~25% depthwise / K-loop / direct
+
+
+@pytest.mark.parametrize("seed", CASES)
+def test_fuzz_dispatched_vs_direct(seed):
+    import paper_2204_03418_b200 as co
+    rng = np.random.default_rng(9000 + seed)
+    d, B = _shape(rng)
+    W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
+    b = rng.standard_normal(d.cout) * 0.1
+    Wt = torch.from_numpy(W).to(torch.bfloat16).cuda()
+    bt = torch.from_numpy(b).float().cuda()
+    mk = lambda kernel: co.Conv(d.cin, d.cout, d.kernel, weight=Wt, bias=bt, stride=d.stride, padding=d.padding,
+                                dilation=d.dilation, groups=d.groups, spatial_rank=2, in_spatial=d.in_spatial,
+                                n_streams=B, dtype=torch.bfloat16, out_dtype=torch.float32, kernel=kernel)
+    fast, ref = mk("auto"), mk("direct")
+    H, Wd = d.in_hw
+    ys, rs = [], []
+    for t in range(d.receptive_field + 3 * d.stride[0] + 2):
+        x = to_cl(rng.standard_normal((B, d.cin, H, Wd)), torch.bfloat16)
+        y, r = fast.forward_step(x), ref.forward_step(x)
+        assert (y is None) == (r is None), (t, fast.kernel_name)
+        if y is not None:
+            ys.append(np_of(y)); rs.append(np_of(r))
+    assert ys, d
+    err = rel_err(np.stack(ys), np.stack(rs))
+    assert err <= 1e-4, (fast.kernel_name, d, B, err)
