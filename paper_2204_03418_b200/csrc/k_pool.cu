@@ -390,6 +390,8 @@ __global__ void __launch_bounds__(1024) k_step_pool_band(Geom g, StepArgs a, int
   Tr* st = reinterpret_cast<Tr*>(a.state);
   const Tin* x = static_cast<const Tin*>(a.x);
   const int row_chunks = int(int64_t(g.W) * g.Cin * sizeof(Tin) / 16);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // see k_step_pool_split
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int64_t band = blockIdx.x; band < g.B * bands; band += gridDim.x) {
     const int64_t b = band / bands;
     const int ho0 = int(band % bands) * TH;
@@ -490,6 +492,10 @@ __global__ void __launch_bounds__(512) k_step_pool_split(Geom g, StepArgs a) {
   const int64_t slot_elems = g.B * g.HWo * g.Cin;
   const Tin* x = static_cast<const Tin*>(a.x);
   const int c0 = cv * V;
+  // programmatic dependent launch (launch_step_pool): let the next step's
+  // blocks be scheduled, and wait for the previous grid's frame / ring writes
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int64_t r = blockIdx.x; r < g.B * g.HWo; r += gridDim.x) {
     const int p = int(r % g.HWo);
     const int64_t b = r / g.HWo;
@@ -614,6 +620,11 @@ bool deep_chunks(const Geom& g, int64_t threads) {
   return threads < int64_t(num_sms()) * 2048 * 4 || g.kh * g.kw > 16;
 }
 
+bool pool_pdl() {
+  const char* e = getenv("CO_PDL");            // CO_PDL=0: plain stream serialization (A/B)
+  return !e || atoi(e) != 0;
+}
+
 int grid_for(int64_t total) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -634,8 +645,19 @@ cudaError_t step_split(const Geom& g, const StepArgs& a, int G, cudaStream_t s) 
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_step_pool_split<Tin, Tout, Tr, V, MAX, VH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem));
-  k_step_pool_split<Tin, Tout, Tr, V, MAX, VH><<<grid, dim3(CV, G), smem, s>>>(g, a);
-  return cudaGetLastError();
+  // launched with programmatic stream serialization: consecutive steps (a few
+  // microseconds each for the expanded global pool) overlap launch and drain
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(CV), unsigned(G));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pool_pdl() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_step_pool_split<Tin, Tout, Tr, V, MAX, VH>, g, a);
 }
 
 template <typename Tin, typename Tout, typename Tr, int V, bool MAX>
@@ -659,10 +681,19 @@ cudaError_t step_v(const Geom& g, const StepArgs& a, cudaStream_t s) {
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
     const int bgrid = int(std::min<int64_t>(nb, int64_t(num_sms()) * std::max(per_sm, 1)));
-    if (g.pool_vh) k_step_pool_band<Tin, Tout, Tr, V, MAX, true><<<bgrid, threads, smem, s>>>(g, a, TH, rows);
-    else if (khw == 33) k_step_pool_band<Tin, Tout, Tr, V, MAX, false, 33><<<bgrid, threads, smem, s>>>(g, a, TH, rows);
-    else k_step_pool_band<Tin, Tout, Tr, V, MAX, false><<<bgrid, threads, smem, s>>>(g, a, TH, rows);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(bgrid));
+    cfg.blockDim = dim3(unsigned(threads));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pool_pdl() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (g.pool_vh) return cudaLaunchKernelEx(&cfg, k_step_pool_band<Tin, Tout, Tr, V, MAX, true>, g, a, TH, rows);
+    if (khw == 33) return cudaLaunchKernelEx(&cfg, k_step_pool_band<Tin, Tout, Tr, V, MAX, false, 33>, g, a, TH, rows);
+    return cudaLaunchKernelEx(&cfg, k_step_pool_band<Tin, Tout, Tr, V, MAX, false>, g, a, TH, rows);
   }
   if (g.pool_vh) k_step_pool<Tin, Tout, Tr, V, MAX, kChunk, true><<<grid, 256, 0, s>>>(g, a);
   else if (khw == 33) k_step_pool<Tin, Tout, Tr, V, MAX, 1, false, 33><<<grid, 256, 0, s>>>(g, a);
