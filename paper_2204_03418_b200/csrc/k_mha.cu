@@ -19,6 +19,7 @@
 // regions 2 MB apart and ran at a third of HBM bandwidth).  Batch mode (co_mha_forward) runs the same
 // kernel with keys / values read from the projected clip (all T columns).
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -48,6 +49,10 @@ __global__ void __launch_bounds__(256, 4) k_mha_attend(const MhaArgs a) {
   const int ks = lane / LPK;          // key subgroup
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   const int64_t rows = a.B * a.T;
+  // programmatic dependent launch: scheduled while the QKV projection drains,
+  // reads its output only after griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int64_t w = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); w < rows * a.heads; w += warps) {
     const int h = int(w % a.heads);
     const int64_t r = w / a.heads;                 // row = (b, t)
@@ -176,13 +181,25 @@ cudaError_t launch_mha_attend(const MhaArgs& a, cudaStream_t s) {
     const int64_t cap = int64_t(sms) * (per_sm > 0 ? per_sm : 1);
     return int(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
   };
+  const char* pe = getenv("CO_PDL");
+  auto launch = [&](auto fn) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid_of((const void*)fn)));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (!pe || atoi(pe) != 0) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, a);
+  };
   switch (a.E / a.heads) {
-    case 32: k_mha_attend<32><<<grid_of((const void*)k_mha_attend<32>), 256, 0, s>>>(a); break;
-    case 64: k_mha_attend<64><<<grid_of((const void*)k_mha_attend<64>), 256, 0, s>>>(a); break;
-    case 128: k_mha_attend<128><<<grid_of((const void*)k_mha_attend<128>), 256, 0, s>>>(a); break;
+    case 32: return launch(k_mha_attend<32>);
+    case 64: return launch(k_mha_attend<64>);
+    case 128: return launch(k_mha_attend<128>);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace co
