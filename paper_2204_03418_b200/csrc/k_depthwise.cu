@@ -184,6 +184,10 @@ __global__ void __launch_bounds__(256, CO_DW_ST_MINB) k_step_dw_st(const DwParam
   const float4* ws4 = reinterpret_cast<const float4*>(ws) + q;     // + ((k*KH + u)*KW + v) * Cq
   const float4 bias4 = reinterpret_cast<const float4*>(bs)[q];
   (void)bias4;
+  // programmatic dependent launch: weights staged above overlap the previous
+  // kernel's drain; frames / state only after it completed
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
     const int64_t b = tile / p.bands;
@@ -258,6 +262,8 @@ __global__ void __launch_bounds__(256, CO_DW_ST_MINB) k_step_dw_st(const DwParam
 #endif
 template <int KT>
 __global__ void __launch_bounds__(kDwThreads, CO_DW_T_MINB) k_step_dw_t(const DwParams p) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // see k_step_dw_st
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t n_items = p.plane * p.Cq;
   const int64_t stride = int64_t(gridDim.x) * kDwThreads;
   for (int64_t base = int64_t(blockIdx.x) * kDwThreads + threadIdx.x; base < n_items; base += kNB * stride) {
@@ -834,8 +840,18 @@ cudaError_t depthwise_step(Depthwise* t, const Geom& g, const StepArgs& a, const
   if (g.raw)
     return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->raw), dim3(unsigned(t->grid)), dim3(kDwThreads),
                             args, 0, s);
-  return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->fn), dim3(unsigned(t->grid)),
-                          dim3(pl.temporal ? kDwThreads : pl.threads), args, pl.temporal ? 0 : pl.smem, s);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(t->grid));
+  cfg.blockDim = dim3(pl.temporal ? kDwThreads : pl.threads);
+  cfg.dynamicSmemBytes = pl.temporal ? 0 : pl.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  const char* pe = getenv("CO_PDL");            // programmatic dependent launch (CO_PDL=0: off)
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (!pe || atoi(pe) != 0) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(pl.var->fn), args);
 }
 
 }  // namespace co
