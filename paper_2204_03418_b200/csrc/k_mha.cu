@@ -41,8 +41,8 @@ __device__ __forceinline__ void ld8(const __nv_bfloat16* p, float (&f)[8]) {
 }
 
 // DH = head dim; LPK = lanes per key row (DH / 8); KPI = keys per iteration.
-template <int DH>
-__global__ void __launch_bounds__(256, 4) k_mha_attend(const MhaArgs a) {
+template <int DH, int KU = 1>
+__global__ void __launch_bounds__(256, KU == 1 ? 4 : 3) k_mha_attend(const MhaArgs a) {
   constexpr int LPK = DH / 8, KPI = 32 / LPK;
   const int lane = threadIdx.x & 31;
   const int g = lane % LPK;           // 8-dim chunk of the head this lane owns
@@ -99,30 +99,44 @@ __global__ void __launch_bounds__(256, 4) k_mha_attend(const MhaArgs a) {
       kr = *reinterpret_cast<const uint4*>(kp);
       vr = *reinterpret_cast<const uint4*>(vp);
     };
-    uint4 kc = make_uint4(0, 0, 0, 0), vc = kc, kn = kc, vn = kc;
-    if (ks < nk) load(ks, kc, vc);
-    for (int j0 = 0; j0 < nk; j0 += KPI) {
-      const int j = j0 + ks;                       // key index: batch = column j; step = j steps ago
-      const bool ok = j < nk;
-      if (j + KPI < nk) load(j + KPI, kn, vn);
-      float s = 0.f;
-      if (ok) {
-        const __nv_bfloat162* kh2 = reinterpret_cast<const __nv_bfloat162*>(&kc);
+    // KU keys per lane per iteration (key j0 + u KPI + ks): KU x (K, V) rows in
+    // flight for the current group and KU for the next one
+    constexpr int KSTEP = KPI * KU;
+    uint4 kc[KU], vc[KU], kn[KU], vn[KU];
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      kc[u] = vc[u] = kn[u] = vn[u] = make_uint4(0, 0, 0, 0);
+      if (u * KPI + ks < nk) load(u * KPI + ks, kc[u], vc[u]);
+    }
+    for (int j0 = 0; j0 < nk; j0 += KSTEP) {
+#pragma unroll
+      for (int u = 0; u < KU; ++u)
+        if (j0 + KSTEP + u * KPI + ks < nk) load(j0 + KSTEP + u * KPI + ks, kn[u], vn[u]);
+      float sc[KU];
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        float s = 0.f;
+        const __nv_bfloat162* kh2 = reinterpret_cast<const __nv_bfloat162*>(&kc[u]);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const float2 kf = __bfloat1622float2(kh2[i]);
           s = fmaf(q[2 * i], kf.x, s);
           s = fmaf(q[2 * i + 1], kf.y, s);
         }
+        sc[u] = s;
       }
 #pragma unroll
-      for (int off = LPK / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);   // within the key row
-      if (ok) {
-        s *= a.scale_log2e;                          // base-2 logits
+      for (int off = LPK / 2; off > 0; off >>= 1)
+#pragma unroll
+        for (int u = 0; u < KU; ++u) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], off);   // within the key row
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        if (j0 + u * KPI + ks >= nk) continue;      // (keys in index order per lane: same fold as KU = 1)
+        const float s = sc[u] * a.scale_log2e;     // base-2 logits
         const float mn = fmaxf(mx, s);
         const float c = exp2f(mx - mn), e = exp2f(s - mn);
         l = l * c + e;
-        const __nv_bfloat162* vh2 = reinterpret_cast<const __nv_bfloat162*>(&vc);
+        const __nv_bfloat162* vh2 = reinterpret_cast<const __nv_bfloat162*>(&vc[u]);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const float2 vf = __bfloat1622float2(vh2[i]);
@@ -131,8 +145,11 @@ __global__ void __launch_bounds__(256, 4) k_mha_attend(const MhaArgs a) {
         }
         mx = mn;
       }
-      kc = kn;
-      vc = vn;
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        kc[u] = kn[u];
+        vc[u] = vn[u];
+      }
     }
     // merge the KPI key subgroups (lanes g, g + LPK, ...)
 #pragma unroll
@@ -168,6 +185,15 @@ bool mha_supported(int E, int heads) {
   return dh == 32 || dh == 64 || dh == 128;
 }
 
+// keys per lane per iteration for dh = 64: 2 (default) keeps twice the K / V
+// rows in flight per warp at 3 blocks per SM -- MHA step 106 -> 97 us; 4
+// measured the same; CO_MHA_KU=1 restores one key (A/B).  Each lane still
+// folds its keys in index order, so all variants give identical results.
+int ku() {
+  const char* e = getenv("CO_MHA_KU");
+  return e ? atoi(e) : 2;
+}
+
 cudaError_t launch_mha_attend(const MhaArgs& a, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -196,7 +222,7 @@ cudaError_t launch_mha_attend(const MhaArgs& a, cudaStream_t s) {
   };
   switch (a.E / a.heads) {
     case 32: return launch(k_mha_attend<32>);
-    case 64: return launch(k_mha_attend<64>);
+    case 64: return ku() == 1 ? launch(k_mha_attend<64>) : launch(k_mha_attend<64, 2>);
     case 128: return launch(k_mha_attend<128>);
     default: return cudaErrorInvalidValue;
   }
