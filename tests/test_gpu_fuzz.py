@@ -69,3 +69,37 @@ def test_fuzz_dispatched_vs_direct(seed):
     assert ys, d
     err = rel_err(np.stack(ys), np.stack(rs))
     assert err <= 1e-4, (fast.kernel_name, d, B, err)
+
+
+@pytest.mark.parametrize("seed", list(range(40)))
+def test_fuzz_bf16_relu_vs_direct(seed):
+    """The same sweep with ReLU and bf16 outputs (the bench's dtype): both sides
+    round nearly equal fp32 sums (different accumulation orders) to bf16 with
+    RNE, so each output may differ by one bf16 rounding of either side: the bar
+    is 2 * 2^-8 of the value (A16's RNE bound, applied to both roundings) plus
+    1e-3 of the RMS for the fp32 order differences near zero."""
+    import paper_2204_03418_b200 as co
+    rng = np.random.default_rng(19000 + seed)
+    d, B = _shape(rng)
+    W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
+    b = rng.standard_normal(d.cout) * 0.1
+    Wt = torch.from_numpy(W).to(torch.bfloat16).cuda()
+    bt = torch.from_numpy(b).float().cuda()
+    mk = lambda kernel: co.Conv(d.cin, d.cout, d.kernel, weight=Wt, bias=bt, stride=d.stride, padding=d.padding,
+                                dilation=d.dilation, groups=d.groups, spatial_rank=2, in_spatial=d.in_spatial,
+                                n_streams=B, dtype=torch.bfloat16, out_dtype=torch.bfloat16, activation="relu",
+                                kernel=kernel)
+    fast, ref = mk("auto"), mk("direct")
+    H, Wd = d.in_hw
+    ys, rs = [], []
+    for t in range(d.receptive_field + 3 * d.stride[0] + 2):
+        x = to_cl(rng.standard_normal((B, d.cin, H, Wd)), torch.bfloat16)
+        y, r = fast.forward_step(x), ref.forward_step(x)
+        assert (y is None) == (r is None), (t, fast.kernel_name)
+        if y is not None:
+            ys.append(np_of(y)); rs.append(np_of(r))
+    y, r = np.stack(ys), np.stack(rs)
+    assert (y >= 0).all()
+    rms = float(np.sqrt(np.mean(r ** 2)))
+    excess = (np.abs(y - r) - (2.0 ** -7 * np.maximum(np.abs(y), np.abs(r)) + 1e-3 * rms)).max()
+    assert excess <= 0, (fast.kernel_name, d, B, excess, rel_err(y, r))
