@@ -13,9 +13,15 @@ order (Assumption 1): step ``(B, C, S1, S2)``, clip
 axes have size 1 (Conv1d inputs are passed as ``(B, C, S1)`` or ``(B, C)`` and
 reshaped here).
 
-"parity unpinned" items: none at function level; the state layout/head
-convention (O5, ``head``) is an ABI decision pinned only by its definition
-(DESIGN.md, "Unpinned").
+"parity unpinned" items: none at function level.  ``head`` (the ring
+position of the next output to complete) is pinned by observation in
+tests/test_oracle_pins.py (``test_head_is_next_output_index``): from the delay
+on it equals the number of Ready outputs emitted so far mod R, and canonical
+slot 0 equals PyTorch's partial batch column of that index.
+
+``CO_ORACLE_LIB`` (test infrastructure only, scripts/oracle_mutants.py): load
+this prebuilt oracle library instead of building ``liboracle.so`` -- the
+mutation check runs the pins against deliberately broken oracles.
 """
 from __future__ import annotations
 
@@ -62,7 +68,7 @@ def lib():
     global _lib
     with _lock:
         if _lib is None:
-            L = C.CDLL(build())
+            L = C.CDLL(os.environ.get("CO_ORACLE_LIB") or build())
             dp = C.POINTER(C.c_double)
             L.or_validate.argtypes = [C.POINTER(_Desc)]
             for fn in ("or_receptive_field", "or_delay", "or_ring_slots"):

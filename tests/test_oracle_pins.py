@@ -192,6 +192,72 @@ def test_cin_identity_random(seed):
     assert mask.tolist() == expect
 
 
+@pytest.mark.parametrize("cin,groups,cout", [(4, 2, 6), (6, 3, 3), (8, 4, 8), (6, 2, 4)])
+def test_grouped_conv_between_dense_and_depthwise(cin, groups, cout):
+    """Groups strictly between 1 and Cin (the channel offset g(o) Cin/g + c' of
+    O1 is only exercised there): batch and step outputs == torch f64 conv3d."""
+    rng = np.random.default_rng(77 + cin * 10 + groups)
+    d = O.Desc(2, cin, cout, (3, 2, 3), stride=(1, 1, 2), padding=(1, 1, 0), groups=groups, in_spatial=(4, 5))
+    W = rng.standard_normal(d.w_shape)
+    b = rng.standard_normal(cout)
+    x = rng.standard_normal((2, cin, 7, 4, 5))
+    ref = torch_conv(d, W, b, x, d.padding[0])
+    np.testing.assert_allclose(O.forward(d, W, b, x), ref, rtol=0, atol=1e-12 * max(1.0, np.abs(ref).max()))
+    ys, _ = O.StepMachine(d, W, b, 2).forward_steps(x, pad_end=True)
+    np.testing.assert_allclose(ys, ref, rtol=0, atol=1e-12 * max(1.0, np.abs(ref).max()))
+
+
+@pytest.mark.parametrize("kt,dil,p,s", [(3, 1, 0, 2), (3, 2, 1, 3), (5, 1, 2, 2), (2, 3, 0, 2), (4, 1, 0, 3)])
+def test_out_len_matches_library_including_too_short(kt, dil, p, s):
+    """S:63-65: T' = floor((T + 2p - f)/s) + 1, an error when T' < 1.  Pinned
+    against torch's own output length for every short T (torch raises where the
+    clip is too short, which must be exactly where T' < 1)."""
+    d = O.Desc(0, 1, 1, (kt,), stride=(s,), padding=(p,), dilation=(dil,))
+    for T in range(0, 12):
+        try:
+            t_lib = F.conv1d(torch.zeros(1, 1, T, dtype=torch.float64), torch.zeros(1, 1, kt, dtype=torch.float64),
+                             stride=s, padding=p, dilation=dil).shape[-1]
+        except RuntimeError:
+            t_lib = 0
+        assert max(d.out_len(T), 0) == t_lib, (T, d.out_len(T), t_lib)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_ring_slots_is_max_pending_outputs(seed):
+    """R, the canonical state's slot count, pinned by observation: the largest
+    number of outputs that have received a contribution from a consumed frame
+    but are not complete yet, counted on PyTorch's partial batch columns over
+    a long run (outputs under stride that are never emitted are not pending)."""
+    rng = np.random.default_rng(8800 + seed)
+    d = rand_desc(rng)
+    B = 1
+    H, Wd = d.in_hw
+    W = rng.standard_normal(d.w_shape) + 3.0           # no zero weights: a consumed tap always contributes
+    sm = O.StepMachine(d, W, None, B)
+    f, p, s, R = d.receptive_field, d.padding[0], d.stride[0], d.ring_slots
+    T = d.delay + 3 * f + 2 * s
+    frames = [rng.standard_normal((B, d.cin, H, Wd)) + 5.0 for _ in range(T)]
+    d0 = O.Desc(**{**d.__dict__, "padding": (0,) + tuple(d.padding[1:])})
+    emitted, most = 0, 0
+    for n, xt in enumerate(frames, start=1):
+        if sm.forward_step(xt) is not None:
+            emitted += 1
+        L = p + n + 2 * f + 2 * s
+        clip = np.zeros((B, d.cin, L, H, Wd))
+        for t in range(n):
+            clip[:, :, p + t] = frames[t]
+        ref = torch_conv(d0, W, None, clip, 0)
+        # output column i is pending iff it is not emitted yet and a consumed real frame feeds it
+        pending = 0
+        for i in range(emitted, ref.shape[2]):
+            taps = [i * s + k * d.dilation[0] for k in range(d.kernel[0])]
+            if any(p <= q < p + n for q in taps):
+                pending += 1
+        most = max(most, pending)
+        assert sm.state().shape[0] == R
+    assert most == R, (most, R)
+
+
 @pytest.mark.parametrize("seed", range(40))
 def test_step_equals_sliding_window_bruteforce(seed):
     """O3 (ring of raw frames) vs O7 (re-run the batch conv over the whole
@@ -361,6 +427,48 @@ def test_head_convention_definition():
         heads.append(sm.head)
         sm.forward_step(np.ones((1, 1)))
     assert heads == [0, 1, 0, 1, 0, 1]
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_head_is_next_output_index(seed):
+    """head pinned by observation, not by its formula: from the delay on, the
+    ring position of the next output to complete equals the number of Ready
+    outputs emitted so far (the n-th Ready tick is d + n s) mod R, and
+    that output is the one canonical slot 0 holds -- PyTorch's batch column of
+    the same index over the consumed frames (Definition 1).  The
+    emitted outputs are themselves PyTorch's full batch columns 0, 1, 2, ...
+    in order, so the count is the batch column index."""
+    rng = np.random.default_rng(4400 + seed)
+    d = rand_desc(rng)
+    B = 2
+    H, Wd = d.in_hw
+    W = rng.standard_normal(d.w_shape)
+    sm = O.StepMachine(d, W, None, B)
+    R, f, p, s = d.ring_slots, d.receptive_field, d.padding[0], d.stride[0]
+    T = d.delay + 2 * max(R, 1) * s + 3
+    frames = [rng.standard_normal((B, d.cin, H, Wd)) for _ in range(T)]
+    d0 = O.Desc(**{**d.__dict__, "padding": (0,) + tuple(d.padding[1:])})
+    emitted = 0
+    for n, xt in enumerate(frames, start=1):
+        y = sm.forward_step(xt)
+        # the padded clip [p zeros | frames consumed so far | zeros for the future]
+        L = p + n + (R + 1) * s + f
+        clip = np.zeros((B, d.cin, L, H, Wd))
+        for t in range(n):
+            clip[:, :, p + t] = frames[t]
+        ref = torch_conv(d0, W, None, clip, 0)
+        if y is not None:
+            tol = 1e-12 * max(1.0, np.abs(ref).max())
+            np.testing.assert_allclose(y, ref[:, :, emitted], rtol=0, atol=tol)
+            emitted += 1
+        assert sm.n == n
+        if R == 0 or n < d.delay:
+            continue
+        # observed: `emitted` outputs so far, so the next one to complete is column `emitted`
+        assert sm.head == emitted % R, (n, sm.head, emitted, R)
+        st = sm.state()
+        np.testing.assert_allclose(st[0], ref[:, :, emitted], rtol=0, atol=1e-12 * max(1.0, np.abs(ref).max()))
+    assert emitted == len([t for t in range(T) if t >= d.delay and (t - d.delay) % s == 0])
 
 
 # --------------------------------------------------------------- stack + bf16
