@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define CO_ABI_VERSION 3
+#define CO_ABI_VERSION 4
 #define CO_MAX_KT 32          /* temporal kernel extent supported by the kernels */
 
 typedef enum {
@@ -293,9 +293,10 @@ int co_mha_create(const co_mha_desc* d, const void* w_qkv, const float* b_qkv, c
                   int weights_on_device, co_mha** out);
 int co_mha_destroy(co_mha* m);
 int co_mha_step(co_mha* m, const void* x, void* y, int update_state, int* ready, co_stream stream);
-/* Batch mode: x (B, T, E) -> y (B, T, E), full attention over the T columns
- * (T == window for the paper's fixed-window form; any T >= 1 accepted).
- * Neither reads nor writes state; stream-ordered temporaries. */
+/* Batch mode: x (B, T, E) -> y (B, T, E), full attention over the T columns;
+ * T must equal window (the fixed-window form; its last column is
+ * the step output): CO_ERR_LENGTH otherwise.  Neither reads nor writes state;
+ * stream-ordered temporaries. */
 int co_mha_forward(co_mha* m, const void* x, int64_t T, void* y, co_stream stream);
 int co_mha_clean(co_mha* m, co_stream stream);
 int co_mha_delay(const co_mha* m, int64_t* delay);
@@ -359,6 +360,40 @@ int co_residual_forward(co_residual* r, const void* x, int64_t T, void* y, int64
 int co_residual_clean(co_residual* r, co_stream stream);   /* body layers + identity ring + clock */
 /* Composite delay (= the body's d_nn) and the identity branch's delay. */
 int co_residual_delay(const co_residual* r, int64_t* delay, int64_t* skip_delay);
+
+/* ---- planner / launch options ----------------------------------------------- */
+
+/* The library reads no environment variable: these named, process-wide
+ * options are its only switches.  Each selects among the sm_100a kernels or
+ * launch modes; none skips work or changes a result beyond the fp32 summation
+ * order (the exact-integer regime, stays bitwise).  They exist
+ * so tests can drive every kernel path and A/B runs can compare launch modes;
+ * the defaults are the planner's measured choices.  [create]: read by
+ * co_conv_create / co_mha_create (affects handles created afterwards);
+ * [launch]: read at each step launch; [call]: read by each co_forward_steps.
+ *   "tc_mode"    0 auto | 1 force the tensor-core K pipeline (KLOOP)          [create]
+ *   "khalo"      1 allow KHALO (default) | 0 keep the strided-gather KLOOP   [create]
+ *   "pair"       0 auto | 1 single CTA | 2 CTA pairs (HALO / FLAT)            [create]
+ *   "kpair"      0 auto | 1 / 2 pin the KLOOP / KHALO pairing                 [create]
+ *   "eg"         0 auto | 1..4 epilogue warpgroups of the tensor-core kernel  [create]
+ *   "mc"         1 (default) | 2, 4, 8 weight-multicast clusters (1-CTA KLOOP) [launch]
+ *   "pdl"        1 (default) programmatic dependent launch | 0 off            [launch]
+ *   "chunk"      1 (default) chunked co_forward_steps where supported | 0 fold [call]
+ *   "chunk_flat" 0 (default) | 1 chunked FLAT (1x1 spatial) clips             [call]
+ *   "chunk_st"   0 (default) | 1 chunked depthwise-stencil clips              [call]
+ *   "chunk_t"    0 (default: up to 256) | max frames per chunked launch       [call]
+ *   "pool_band"  1 (default) row-band pooling kernel | 0 plain kernel         [create]
+ *   "pool_vh"   -1 auto | 0 direct fold | 1 block decomposition (pooling)     [create]
+ *   "pool_g"     0 auto | 1..32 lanes per pooled output vector                [create]
+ *   "log"        0 (default) | 1 print each tensor-core plan to stderr        [create]
+ * name == NULL resets every option to its default.
+ * Errors: CO_ERR_ARG for an unknown name or a value out of range.  Not
+ * thread-safe against concurrent creates (set options before building handles). */
+int co_set_option(const char* name, int64_t value);
+int co_get_option(const char* name, int64_t* value);
+/* Name of option `index` (0, 1, ...), NULL past the last: lets a harness record
+ * every option's value next to a measurement. */
+const char* co_option_name(int index);
 
 /* ---- misc ------------------------------------------------------------------ */
 const char* co_last_error(void);

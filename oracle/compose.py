@@ -11,8 +11,9 @@ bench.py's CPU legs may import it; it shares no code with the CUDA path.
   - equal padding (``shrink=False``; the body keeps T, i.e. 2 p_acc = f_acc-1):
     batch y = x + body(x); step mode delays the identity branch by the body's
     delay d (P:306-310);
-  - centered (``shrink=True``, f_acc odd): batch crops the identity branch by
-    (f_acc-1)/2 at each end; step mode delays it by (f_acc-1)/2 while the
+  - centered (``shrink=True``, f_acc odd, p_acc <= (f_acc-1)/2): batch crops the
+    identity branch by (f_acc-1)/2 - p_acc at the start (each output's
+    receptive-field center); step mode delays it by (f_acc-1)/2 while the
     composite's delay is the body's (Principle 7: the merge is Empty
     while either branch is);
   - optional ReLU after the add (``relu_out``), the ResNet / X3D block form.
@@ -76,6 +77,8 @@ def skip_delay(descs: Sequence[O.Desc], shrink: bool) -> int:
     if shrink:
         if t["f_nn"] % 2 == 0:
             raise ValueError("centered residual needs an odd receptive field (S:456)")
+        if t["p_nn"] > (t["f_nn"] - 1) // 2:
+            raise ValueError("centered residual: body padding exceeds (f_acc-1)/2")
         return (t["f_nn"] - 1) // 2
     if 2 * t["p_nn"] != t["f_nn"] - 1:
         raise ValueError("residual without shrink needs equal padding (2 p_acc = f_acc - 1)")
@@ -118,7 +121,11 @@ def residual_forward(descs: Sequence[O.Desc], Ws, biases, relu: Sequence[int], x
                      relu_out: bool = False, round_bf16: Optional[Sequence[int]] = None) -> np.ndarray:
     """Batch mode: the body's batch forward (O.forward layer by layer, ReLU and
     optional bf16 rounding of activations as in the step stack) plus the
-    identity branch, cropped by (f_acc-1)/2 at each end when shrink."""
+    identity branch, aligned with the center of each output's receptive field
+    (P:312-316): output column i covers padded frames i .. i + f_acc - 1, whose
+    center is real frame i + (f_acc-1)/2 - p_acc, so the identity clip is
+    cropped by c = (f_acc-1)/2 - p_acc at the start (c = 0 for equal padding,
+    c = (f_acc-1)/2 for an unpadded body)."""
     x = np.asarray(x, np.float64)
     cur = x
     L = len(descs)
@@ -128,7 +135,7 @@ def residual_forward(descs: Sequence[O.Desc], Ws, biases, relu: Sequence[int], x
             cur = np.maximum(cur, 0.0)
         if round_bf16 is not None and round_bf16[l]:
             cur = O.bf16_round(cur)
-    c = skip_delay(descs, shrink) if shrink else 0
+    c = skip_delay(descs, shrink) - body_timing(descs)["p_nn"] if shrink else 0
     T_out = cur.shape[2]
     y = cur + x[:, :, c:c + T_out].reshape(cur.shape)
     return np.maximum(y, 0.0) if relu_out else y

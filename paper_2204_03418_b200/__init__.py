@@ -23,7 +23,8 @@ import torch
 from . import _abi
 from ._abi import CoConvDesc, CoInfo, CoMhaDesc, check, lib
 
-__all__ = ["BroadcastReduce", "Conv", "Delay", "MultiheadAttention", "Pool", "Residual", "Stack", "channels_last", "is_channels_last", "load"]
+__all__ = ["BroadcastReduce", "Conv", "Delay", "MultiheadAttention", "Pool", "Residual", "Stack", "channels_last",
+           "get_option", "is_channels_last", "load", "options", "set_option"]
 
 _DT = {torch.float32: _abi.CO_F32, torch.bfloat16: _abi.CO_BF16}
 
@@ -31,6 +32,53 @@ _DT = {torch.float32: _abi.CO_F32, torch.bfloat16: _abi.CO_BF16}
 def load():
     """Load the native library (raises ImportError if it was not built)."""
     return lib()
+
+
+def set_option(name: str, value: int) -> None:
+    """co_set_option: a documented planner / launch option (include/co.h)."""
+    check(lib().co_set_option(name.encode(), int(value)))
+
+
+def reset_options() -> None:
+    """Every option back to its default (co_set_option(NULL, 0))."""
+    check(lib().co_set_option(None, 0))
+
+
+def get_option(name: str) -> int:
+    v = C.c_int64()
+    check(lib().co_get_option(name.encode(), C.byref(v)))
+    return v.value
+
+
+def all_options() -> dict:
+    """Every option's current value (co_option_name enumerates them)."""
+    out, i = {}, 0
+    while True:
+        n = lib().co_option_name(i)
+        if not n:
+            return out
+        out[n.decode()] = get_option(n.decode())
+        i += 1
+
+
+class options:
+    """Context manager: ``with co.options(tc_mode=1, pair=2): ...`` sets the
+    options and restores the previous values on exit."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.prev = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.prev[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.prev.items():
+            set_option(k, v)
+        return False
 
 
 def channels_last(x: torch.Tensor) -> torch.Tensor:
@@ -175,17 +223,42 @@ class Conv:
             raise ValueError("input must be channels-last (use paper_2204_03418_b200.channels_last)")
 
     # ---- call modes (Principle 2) ----
+    def _check_out(self, out: torch.Tensor, shape, dtype):
+        """The kernels write `out` through its data pointer: it must be the
+        exact (B, C, *S') channels-last tensor of the right dtype and device."""
+        if tuple(out.shape) != tuple(shape) or out.dtype != dtype or out.device != self.device:
+            raise ValueError(f"out must be a {dtype} {tuple(shape)} tensor on {self.device}, got "
+                             f"{out.dtype} {tuple(out.shape)} on {out.device}")
+        if not is_channels_last(out):
+            raise ValueError("out must be channels-last (use paper_2204_03418_b200.channels_last)")
+
     def forward_step(self, x: Optional[torch.Tensor], update_state: bool = True, out: Optional[torch.Tensor] = None,
-                     stream=None) -> Optional[torch.Tensor]:
-        """One step.  Returns the emitted output or None (Empty)."""
+                     stream=None, pad: bool = False) -> Optional[torch.Tensor]:
+        """One step.  Returns the emitted output or None (Empty).
+
+        ``x = None`` is an Empty input: it returns None and neither
+        computes nor advances the clock, so hand-chained layers
+        ``l2.forward_step(l1.forward_step(x))`` short-circuit like a Stack.
+        ``pad=True`` (x must be None) feeds one zero padding step instead --
+        the end padding of ``pad_end``, which does advance the clock."""
+        if x is None and not pad:
+            return None
         if x is not None:
+            if pad:
+                raise ValueError("pad=True takes no input frame")
             self._check_in(x, clip=False)
-        y = out if out is not None else _empty_cl((self.n_streams, self.out_channels) + self.out_spatial,
-                                                  self.out_dtype, self.device)
+        shape = (self.n_streams, self.out_channels) + self.out_spatial
+        if out is not None:
+            self._check_out(out, shape, self.out_dtype)
+        y = out if out is not None else _empty_cl(shape, self.out_dtype, self.device)
         r = C.c_int()
         check(lib().co_forward_step(self._h, C.c_void_p(x.data_ptr()) if x is not None else None,
                                     C.c_void_p(y.data_ptr()), int(update_state), C.byref(r), _stream(stream)))
         return y if r.value else None
+
+    def forward_pad_step(self, update_state: bool = True, out: Optional[torch.Tensor] = None, stream=None):
+        """One zero padding step (pad_end): ``forward_step(None, pad=True)``."""
+        return self.forward_step(None, update_state=update_state, out=out, stream=stream, pad=True)
 
     def forward_steps(self, x: torch.Tensor, pad_end: bool = False, update_state: bool = True, stream=None):
         """Fold of forward_step over the clip.  Returns (y compacted in
@@ -380,11 +453,17 @@ class Residual:
         return d.value, k.value
 
     def forward_step(self, x: Optional[torch.Tensor], update_state: bool = True, out: Optional[torch.Tensor] = None,
-                     stream=None) -> Optional[torch.Tensor]:
+                     stream=None, pad: bool = False) -> Optional[torch.Tensor]:
+        """One tick; ``x = None`` is Empty (returns None, no state change),
+        ``pad=True`` with ``x = None`` a zero padding step (see Conv.forward_step)."""
+        if x is None and not pad:
+            return None
         if x is not None:
             self.body[0]._check_in(x, clip=False)
-        y = out if out is not None else _empty_cl((self.n_streams, self.channels) + self.in_spatial, self.out_dtype,
-                                                  self.device)
+        shape = (self.n_streams, self.channels) + self.in_spatial
+        if out is not None:
+            self.body[-1]._check_out(out, shape, self.out_dtype)
+        y = out if out is not None else _empty_cl(shape, self.out_dtype, self.device)
         r = C.c_int()
         check(lib().co_residual_step(self._h, C.c_void_p(x.data_ptr()) if x is not None else None,
                                      C.c_void_p(y.data_ptr()), int(update_state), C.byref(r), _stream(stream)))
@@ -447,10 +526,16 @@ class BroadcastReduce:
         check(lib().co_parallel_delay(self._h, C.byref(d)))
         return d.value
 
-    def forward_step(self, x: torch.Tensor, update_state: bool = True, out: Optional[torch.Tensor] = None,
+    def forward_step(self, x: Optional[torch.Tensor], update_state: bool = True, out: Optional[torch.Tensor] = None,
                      stream=None) -> Optional[torch.Tensor]:
-        y = out if out is not None else _empty_cl((self.n_streams, self.out_channels) + self.out_spatial,
-                                                  self.out_dtype, self.device)
+        if x is None:                                  # Empty input
+            return None
+        first = next(b for b in self.branches if b is not None).layers[0]
+        first._check_in(x, clip=False)
+        shape = (self.n_streams, self.out_channels) + self.out_spatial
+        if out is not None:
+            first._check_out(out, shape, self.out_dtype)
+        y = out if out is not None else _empty_cl(shape, self.out_dtype, self.device)
         r = C.c_int()
         check(lib().co_parallel_step(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), int(update_state),
                                      C.byref(r), _stream(stream)))
@@ -524,8 +609,14 @@ class MultiheadAttention:
     def forward_step(self, x: torch.Tensor, update_state: bool = True, out: Optional[torch.Tensor] = None,
                      stream=None) -> Optional[torch.Tensor]:
         """x (B, E) bf16 -> (B, E) or None (Empty)."""
-        if tuple(x.shape) != (self.n_streams, self.E) or x.dtype != torch.bfloat16 or not x.is_contiguous():
-            raise ValueError(f"x must be a contiguous bf16 ({self.n_streams}, {self.E}) CUDA tensor")
+        if x is None:                                  # Empty input (S:126)
+            return None
+        if tuple(x.shape) != (self.n_streams, self.E) or x.dtype != torch.bfloat16 or not x.is_contiguous() \
+                or x.device != self.device:
+            raise ValueError(f"x must be a contiguous bf16 ({self.n_streams}, {self.E}) tensor on {self.device}")
+        if out is not None and (tuple(out.shape) != (self.n_streams, self.E) or out.dtype != self.out_dtype
+                                or not out.is_contiguous() or out.device != self.device):
+            raise ValueError(f"out must be a contiguous {self.out_dtype} ({self.n_streams}, {self.E}) tensor")
         y = out if out is not None else torch.empty((self.n_streams, self.E), dtype=self.out_dtype, device=self.device)
         r = C.c_int()
         check(lib().co_mha_step(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), int(update_state),
@@ -533,8 +624,11 @@ class MultiheadAttention:
         return y if r.value else None
 
     def forward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
-        """Batch mode: x (B, E, T) -> (B, E, T), full attention over the T columns."""
+        """Batch mode: x (B, E, T) -> (B, E, T) with T == window (SPEC S:370-372:
+        the fixed-window form, whose last column is the step output)."""
         B, E, T = x.shape
+        if T != self.window:
+            raise ValueError(f"batch attention needs T == window ({T} != {self.window})")
         xt = x.transpose(1, 2).contiguous().to(torch.bfloat16)           # (B, T, E)
         y = torch.empty((B, T, E), dtype=self.out_dtype, device=self.device)
         check(lib().co_mha_forward(self._h, C.c_void_p(xt.data_ptr()), T, C.c_void_p(y.data_ptr()), _stream(stream)))
@@ -586,11 +680,16 @@ class Stack:
         check(lib().co_stack_delay(self._h, C.byref(d)))
         return d.value
 
-    def forward_step(self, x: torch.Tensor, update_state: bool = True, out: Optional[torch.Tensor] = None,
+    def forward_step(self, x: Optional[torch.Tensor], update_state: bool = True, out: Optional[torch.Tensor] = None,
                      stream=None) -> Optional[torch.Tensor]:
+        if x is None:                                  # Empty input: nothing advances
+            return None
+        self.layers[0]._check_in(x, clip=False)
         last = self.layers[-1]
-        y = out if out is not None else _empty_cl((last.n_streams, last.out_channels) + last.out_spatial,
-                                                  last.out_dtype, last.device)
+        shape = (last.n_streams, last.out_channels) + last.out_spatial
+        if out is not None:
+            last._check_out(out, shape, last.out_dtype)
+        y = out if out is not None else _empty_cl(shape, last.out_dtype, last.device)
         r = C.c_int()
         check(lib().co_stack_step(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), int(update_state),
                                   C.byref(r), _stream(stream)))

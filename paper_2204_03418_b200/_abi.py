@@ -25,6 +25,9 @@ KERNELS = {"auto": CO_KERNEL_AUTO, "direct": CO_KERNEL_DIRECT, "dense_tc": CO_KE
 CO_OP_CONV, CO_OP_MAX_POOL, CO_OP_AVG_POOL, CO_OP_DELAY = 0, 1, 2, 3
 OPS = {"conv": CO_OP_CONV, "max": CO_OP_MAX_POOL, "avg": CO_OP_AVG_POOL, "delay": CO_OP_DELAY}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
+# defaults of the documented options (include/co.h co_set_option)
+OPTION_DEFAULTS = {"tc_mode": 0, "khalo": 1, "pair": 0, "kpair": 0, "eg": 0, "mc": 1, "pdl": 1, "chunk": 1,
+                   "chunk_flat": 0, "chunk_st": 0, "chunk_t": 0, "pool_band": 1, "pool_vh": -1, "pool_g": 0, "log": 0}
 
 # every entry point include/co.h declares (checked by tests/test_abi_load.py)
 EXPORTS = ["co_conv_create", "co_conv_destroy", "co_conv_info", "co_delay", "co_kernel_name",
@@ -35,7 +38,8 @@ EXPORTS = ["co_conv_create", "co_conv_destroy", "co_conv_info", "co_delay", "co_
            "co_stack_stream_ready", "co_parallel_create", "co_parallel_destroy", "co_parallel_step",
            "co_parallel_forward", "co_parallel_clean", "co_parallel_delay", "co_parallel_out_channels", "co_mha_create", "co_mha_destroy", "co_mha_step", "co_mha_forward", "co_mha_clean",
            "co_mha_delay", "co_mha_state_bytes", "co_mha_state_get", "co_mha_state_set", "co_residual_create", "co_residual_destroy", "co_residual_step", "co_residual_forward",
-           "co_residual_clean", "co_residual_delay", "co_last_error", "co_abi_version"]
+           "co_residual_clean", "co_residual_delay", "co_set_option", "co_get_option", "co_option_name",
+           "co_last_error", "co_abi_version"]
 
 
 class CoMhaDesc(C.Structure):
@@ -127,6 +131,10 @@ def lib():
             L.co_residual_forward.argtypes = [vp, vp, C.c_int64, vp, i64p, vp]
             L.co_residual_clean.argtypes = [vp, vp]
             L.co_residual_delay.argtypes = [vp, i64p, i64p]
+            L.co_set_option.argtypes = [C.c_char_p, C.c_int64]
+            L.co_get_option.argtypes = [C.c_char_p, i64p]
+            L.co_option_name.argtypes = [C.c_int]
+            L.co_option_name.restype = C.c_char_p
             L.co_last_error.restype = C.c_char_p
             L.co_abi_version.restype = C.c_int
             _lib = L

@@ -3,6 +3,7 @@
 // nothing with oracle/.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -10,6 +11,25 @@
 namespace co {
 
 constexpr int kMaxKt = 32;   // == CO_MAX_KT
+
+// Documented planner / launch options (include/co.h co_set_option; options.cu).
+enum Opt : int {
+  OPT_TC_MODE, OPT_KHALO, OPT_PAIR, OPT_KPAIR, OPT_EG, OPT_MC, OPT_PDL, OPT_CHUNK, OPT_CHUNK_FLAT, OPT_CHUNK_ST,
+  OPT_CHUNK_T, OPT_POOL_BAND, OPT_POOL_VH, OPT_POOL_G, OPT_LOG, OPT_COUNT
+};
+int64_t option(Opt o);
+
+// A/B experiment knobs: read from the environment only in -DCO_EXPERIMENTS
+// builds; the release library compiles them to their defaults (no getenv, no
+// variable names in the binary).
+#ifdef CO_EXPERIMENTS
+int experiment_knob(const char* name, int dflt);
+#define CO_EXP(name, dflt) ::co::experiment_knob(name, dflt)
+#define CO_EXP_SET(name) (std::getenv(name) != nullptr)
+#else
+#define CO_EXP(name, dflt) (dflt)
+#define CO_EXP_SET(name) false
+#endif
 
 enum Dtype : int { F32 = 0, BF16 = 1 };
 enum Op : int { OP_CONV = 0, OP_MAX_POOL = 1, OP_AVG_POOL = 2, OP_DELAY = 3 };   // == co_op
@@ -123,8 +143,8 @@ cudaError_t launch_step_pool(const Geom& g, const StepArgs& a, cudaStream_t s);
 cudaError_t launch_forward_pool(const Geom& g, const void* x, int64_t T, void* y, int64_t Tp, cudaStream_t s);
 cudaError_t launch_fill_pad(const Geom& g, void* p, int64_t n_elems, cudaStream_t s);
 std::string pool_kernel_name(const Geom& g);
-int pool_split_lanes(const Geom& g);   // choice of pool_G (env CO_POOL_G overrides)
-int pool_block_decomposition(const Geom& g);   // choice of pool_vh (env CO_POOL_VH overrides)
+int pool_split_lanes(const Geom& g);   // choice of pool_G (option "pool_g" overrides)
+int pool_block_decomposition(const Geom& g);   // choice of pool_vh (option "pool_vh" overrides)
 cudaError_t launch_pool_rebuild(const Geom& g, void* state, int64_t m_next, cudaStream_t s);
 
 // Per-stream clean (k_direct.cu): zero the listed streams'

@@ -46,6 +46,24 @@ static int fail(int code, const char* fmt, ...) {
 extern "C" const char* co_last_error(void) { return g_err.c_str(); }
 extern "C" int co_abi_version(void) { return CO_ABI_VERSION; }
 
+// ----------------------------------------------------------------- options (options.cu)
+int co_set_option_impl(const char* name, int64_t value, std::string& err);
+int co_get_option_impl(const char* name, int64_t* value, std::string& err);
+int co_option_count_impl();
+const char* co_option_name_impl(int i);
+
+extern "C" int co_set_option(const char* name, int64_t value) {
+  std::string err;
+  const int rc = co_set_option_impl(name, value, err);
+  return rc == CO_OK ? CO_OK : fail(rc, "%s", err.c_str());
+}
+extern "C" int co_get_option(const char* name, int64_t* value) {
+  std::string err;
+  const int rc = co_get_option_impl(name, value, err);
+  return rc == CO_OK ? CO_OK : fail(rc, "%s", err.c_str());
+}
+extern "C" const char* co_option_name(int index) { return co_option_name_impl(index); }
+
 // ----------------------------------------------------------------- integer helpers
 
 static inline int64_t floor_div(int64_t a, int64_t b) {
@@ -659,7 +677,7 @@ extern "C" int co_forward_steps(co_conv* h, const void* x, int64_t T, void* y, u
     // FLAT stages a chunk time-major, so Tc bounds that copy to ~1 GB
     const int64_t frame_bytes = g.B * g.frame_elems * int64_t(dsize(g.in_dtype));
     int64_t Tc = std::max<int64_t>(1, std::min<int64_t>({T, 256, (int64_t(1) << 30) / std::max<int64_t>(frame_bytes, 1)}));
-    if (const char* e = getenv("CO_CHUNK_T")) Tc = std::max<int64_t>(1, std::min<int64_t>(Tc, atoi(e)));   // tests
+    if (const int64_t e = co::option(co::OPT_CHUNK_T)) Tc = std::max<int64_t>(1, std::min<int64_t>(Tc, e));   // option "chunk_t"
     constexpr int kTick = 2 + co::kMaxKt;
     std::vector<int> ticks(size_t(Tc) * kTick);
     int* dticks = nullptr;
@@ -966,7 +984,7 @@ struct co_residual {
   co_stack* stack = nullptr;
   std::vector<co_conv*> body;
   int shrink = 0, act = 0;
-  int64_t f_acc = 0, d_body = 0, d_skip = 0;
+  int64_t f_acc = 0, d_body = 0, d_skip = 0, p_acc = 0;
   int64_t n = 0;
   void* ring = nullptr;
   int in_dtype = 0, out_dtype = 0;
@@ -1013,7 +1031,7 @@ extern "C" int co_residual_create(co_conv* const* body, int n_layers, int shrink
   r->body.assign(body, body + n_layers);
   r->shrink = shrink ? 1 : 0;
   r->act = activation;
-  r->f_acc = f_acc; r->d_body = d_body; r->d_skip = d_skip;
+  r->f_acc = f_acc; r->d_body = d_body; r->d_skip = d_skip; r->p_acc = p_acc;
   r->in_dtype = a.in_dtype; r->out_dtype = z.out_dtype;
   r->B = a.B; r->frame_elems = a.frame_elems;
   {
@@ -1105,8 +1123,11 @@ extern "C" int co_residual_forward(co_residual* r, const void* x, int64_t T, voi
   cudaStream_t s = (cudaStream_t)stream;
   int64_t Tc = 0;
   if (int rc = layers_forward(r->body, x, T, y, &Tc, stream)) return rc;
-  // identity branch: the input clip, cropped by (f_acc-1)/2 at each end when shrink
-  const int64_t c = r->shrink ? r->d_skip : 0;
+  // identity branch: the input clip aligned with each output's receptive-field
+  // center: column i covers padded frames i .. i + f_acc - 1, center
+  // = real frame i + (f_acc-1)/2 - p_acc, so the crop is d_skip - p_acc (0 for
+  // equal padding); create guarantees 0 <= c and c + Tc <= T (p_acc <= d_skip)
+  const int64_t c = r->shrink ? r->d_skip - r->p_acc : 0;
   const int64_t fe = r->frame_elems;
   const char* xs = static_cast<const char*>(x) + size_t(c) * fe * dsize(r->in_dtype);
   CO_CUDA(co::launch_residual_add(r->out_dtype, y, Tc * fe, r->in_dtype, xs, T * fe, r->B, Tc * fe, r->act, s));
@@ -1327,6 +1348,9 @@ extern "C" int co_mha_step(co_mha* m, const void* x, void* y, int update_state, 
 
 extern "C" int co_mha_forward(co_mha* m, const void* x, int64_t T, void* y, co_stream stream) {
   if (!m || !x || !y || T < 1) return fail(CO_ERR_ARG, "bad argument");
+  // batch mode is the fixed-window form (T == window); only then is
+  // every column the step output of its window (mode equivalence, Definition 1)
+  if (T != m->d.window) return fail(CO_ERR_LENGTH, "mha batch mode needs T == window (%lld != %d)", (long long)T, m->d.window);
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t B = m->d.n_streams, E = m->d.embed_dim;
   void *qkv = nullptr, *att = nullptr;

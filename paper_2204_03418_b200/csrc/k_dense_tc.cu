@@ -133,6 +133,14 @@ struct TcParams {
 // access to data an earlier kernel wrote (frames, state, y) waits on
 // griddepcontrol.wait, which returns once the prerequisite grid completed and
 // its writes are visible (a no-op for a normal launch).
+// CO_TC_DEBUG bits (p.dbg): experiment builds only; the release kernels
+// compile every DBG() test to 0, so no work can be skipped in a shipped build.
+#ifdef CO_EXPERIMENTS
+#define DBG(bits) (p.dbg & (bits))
+#else
+#define DBG(bits) (0)
+#endif
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -303,7 +311,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
             for (int e = 0; e < nb; ++e) {
               const int64_t item = bi + int64_t(e) * n_units;
               ptx::mbar_wait(&empty[s], ph ^ 1);
-              if (p.dbg & 4) {
+              if DBG(4) {
                 if (leader) ptx::mbar_arrive(&full[s]);
                 if (++s == p.stages) { s = 0; ph ^= 1; }
                 continue;
@@ -468,7 +476,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       int64_t n_works = 0;                              // this unit's works: items x T frames
       for (int64_t item = unit; item < p.n_items; item += n_units) n_works += p.T;
       for (int64_t w = 0; w < n_works; ++w) {
-        if (!(p.dbg & 16)) ptx::mbar_wait(&acc_empty[e], eph ^ 1);
+        if (!DBG(16)) ptx::mbar_wait(&acc_empty[e], eph ^ 1);
         ptx::tc_fence_after();
         ptx::mbar_wait(&full[s], ph);
         ptx::tc_fence_after();
@@ -482,7 +490,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
         };
         const uint32_t row16 = p.swa ? 8u : 1u;        // one halo row in 16-B units
         if constexpr (KH > 0) {
-          if (!(p.dbg & 2) && ptx::elect_one()) {
+          if (!DBG(2) && ptx::elect_one()) {
 #pragma unroll
             for (int u = 0; u < KH; ++u)
 #pragma unroll
@@ -609,18 +617,18 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     for (int cb = cs * CPW; cb < (cs + 1) * CPW; cb += CE) {
       // ---- prefetch the state this pass needs (pass 0: before the accumulator is ready)
       float4 sv[NS][NQ];
-      if (p.dbg & 64) {
+      if DBG(64) {
 #pragma unroll
         for (int k = 0; k < NS; ++k)
 #pragma unroll
           for (int i = 0; i < NQ; ++i) sv[k][i] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      if (KT > 1 && valid && !(p.dbg & 65)) {
+      if (KT > 1 && valid && !DBG(65)) {
         if (emit) {
           const float4* src = reinterpret_cast<const float4*>(p.state) +
                               ((int64_t(slot(KT - 1)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
-          for (int i = 0; i < NQ; ++i) sv[0][i] = (p.dbg & 32) ? ld_state_na(src + i * 128) : __ldcs(src + i * 128);
+          for (int i = 0; i < NQ; ++i) sv[0][i] = DBG(32) ? ld_state_na(src + i * 128) : __ldcs(src + i * 128);
         }
         if (p.update) {
 #pragma unroll
@@ -629,11 +637,11 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
             const float4* src = reinterpret_cast<const float4*>(p.state) +
                                 ((int64_t(slot(k)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
-            for (int i = 0; i < NQ; ++i) sv[k][i] = (p.dbg & 32) ? ld_state_na(src + i * 128) : __ldcs(src + i * 128);
+            for (int i = 0; i < NQ; ++i) sv[k][i] = DBG(32) ? ld_state_na(src + i * 128) : __ldcs(src + i * 128);
           }
         }
       }
-      if (cb == cs * CPW && !(p.dbg & 16)) {
+      if (cb == cs * CPW && !DBG(16)) {
         ptx::mbar_wait(&acc_full[buf], bph);
         ptx::tc_fence_after();
       }
@@ -642,9 +650,9 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       if (emit) {
 #pragma unroll
         for (int c = 0; c < CE; c += 16) {
-          if (!(p.dbg & 8)) ptx::tmem_ld16(t_row + uint32_t((KT - 1) * CC + cb + c), v);
+          if (!DBG(8)) ptx::tmem_ld16(t_row + uint32_t((KT - 1) * CC + cb + c), v);
           ptx::tc_wait_ld();
-          if (!(p.dbg & 257)) {
+          if (!DBG(257)) {
             // y = (P + S) + b, the activation only behind a uniform branch
             // (computed on every lane: the bf16 stores below pair lanes up)
 #pragma unroll
@@ -677,7 +685,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
               if (p.ystage) {                   // row = lane, written out after the pass
                 ybuf[lane * YU + (((c >> 3) + 0) ^ yswz(lane))] = h[0];
                 ybuf[lane * YU + (((c >> 3) + 1) ^ yswz(lane))] = h[1];
-              } else if (p.dbg & 512) {
+              } else if DBG(512) {
                 if (valid) {
                   reinterpret_cast<uint4*>(yb + yoff)[0] = h[0];
                   reinterpret_cast<uint4*>(yb + yoff)[1] = h[1];
@@ -707,7 +715,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
             }
           }
         }
-        if (p.ystage && !(p.dbg & 257)) {
+        if (p.ystage && !DBG(257)) {
           // the warp's 32 rows go out row-contiguously: 32 / YU rows of CE
           // channels per store instruction (whole 2 CE-byte runs, not 16-B pieces)
           __syncwarp();
@@ -733,14 +741,14 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
                         ((int64_t(slot(k)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
           for (int c = 0; c < CE; c += 16) {
-            if (!(p.dbg & 8)) ptx::tmem_ld16(t_row + uint32_t(k * CC + cb + c), v);
+            if (!DBG(8)) ptx::tmem_ld16(t_row + uint32_t(k * CC + cb + c), v);
             ptx::tc_wait_ld();
-            if (valid && !(p.dbg & 1)) {
+            if (valid && !DBG(1)) {
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 float4 t4 = sv[k][c / 4 + i];
                 t4.x += v[4 * i]; t4.y += v[4 * i + 1]; t4.z += v[4 * i + 2]; t4.w += v[4 * i + 3];
-                if (!(p.dbg & 128)) __stcs(dst + (c / 4 + i) * 128, t4);
+                if (!DBG(128)) __stcs(dst + (c / 4 + i) * 128, t4);
               }
             }
           }
@@ -751,12 +759,12 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
                         ((int64_t(slot(0)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
 #pragma unroll
           for (int c = 0; c < CE; c += 16) {
-            if (!(p.dbg & 8)) ptx::tmem_ld16(t_row + uint32_t(cb + c), v);
+            if (!DBG(8)) ptx::tmem_ld16(t_row + uint32_t(cb + c), v);
             ptx::tc_wait_ld();
-            if (valid && !(p.dbg & 1)) {
+            if (valid && !DBG(1)) {
 #pragma unroll
               for (int i = 0; i < 4; ++i)
-                if (!(p.dbg & 128)) __stcs(dst + (c / 4 + i) * 128, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+                if (!DBG(128)) __stcs(dst + (c / 4 + i) * 128, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
             }
           }
         }
@@ -974,61 +982,30 @@ constexpr size_t kHaloBudget = 150 * 1024;
 
 // 128-B swizzled A operand (TMA boxes with 128-B rows instead of 16-B ones):
 // default on, CO_TC_SWA=0 restores the interleaved layout (A/B runs).
-bool swa_enabled() {
-  const char* v = getenv("CO_TC_SWA");
-  return !v || atoi(v) != 0;
-}
+bool swa_enabled() { return CO_EXP("CO_TC_SWA", 1) != 0; }
 
 // KLOOP CTA pairs (each CTA streams half of every weight chunk through a
 // swizzled 128-B-row TMA box): default for 64-channel K chunks (C4 L3 / L5
 // measured ~8% faster, L4 equal); 32-channel chunks (the stem) stay single.
-// CO_TC_KPAIR=1|2 pins it (A/B runs).
+// option "kpair" (co_set_option) = 1 | 2 pins it.
 int kloop_pair(int kb) {
-  const char* v = getenv("CO_TC_KPAIR");
-  return v ? atoi(v) : (kb == 64 ? 2 : 1);
+  const int v = int(option(OPT_KPAIR));
+  return v ? v : (kb == 64 ? 2 : 1);
 }
 
-int pinned_pair() {
-  const char* v = getenv("CO_TC_PAIR");         // A/B runs only
-  return v ? atoi(v) : 1;
-}
+int pinned_cs() { return CO_EXP("CO_TC_CS", 1); }           // A/B experiments only
+int pinned_eg() { return int(option(OPT_EG)); }              // option "eg": 0 = planner's choice
+int pinned_cc() { return CO_EXP("CO_TC_CC", 0); }           // A/B experiments only
+int pinned_ce() { return CO_EXP("CO_TC_CE", 0); }           // A/B experiments only
 
-int pinned_cs() {
-  const char* v = getenv("CO_TC_CS");           // A/B runs only
-  return v ? atoi(v) : 1;
-}
+// y stores transposed through shared memory (HALO, bf16 y; CO_TC_YSTAGE in experiment builds)
+int ystage_mode() { return CO_EXP("CO_TC_YSTAGE", 1); }
 
-int pinned_eg() {
-  const char* eg_env = getenv("CO_TC_EG");      // A/B runs only
-  return eg_env ? atoi(eg_env) : 0;
-}
+// KHALO for stride-1 K-pipeline layers (option "khalo" = 0 keeps KLOOP)
+bool khalo_enabled() { return option(OPT_KHALO) != 0; }
 
-int pinned_cc() {
-  const char* v = getenv("CO_TC_CC");           // A/B runs only
-  return v ? atoi(v) : 0;
-}
-
-int pinned_ce() {
-  const char* v = getenv("CO_TC_CE");           // A/B runs only
-  return v ? atoi(v) : 0;
-}
-
-// y stores transposed through shared memory (HALO, bf16 y): CO_TC_YSTAGE=0|1
-// overrides (A/B runs)
-int ystage_mode() {
-  const char* v = getenv("CO_TC_YSTAGE");
-  return v ? atoi(v) : 1;
-}
-
-// KHALO for stride-1 K-pipeline layers (CO_TC_KHALO=0 keeps KLOOP: A/B runs)
-bool khalo_enabled() {
-  const char* v = getenv("CO_TC_KHALO");
-  return !v || atoi(v) != 0;
-}
-
-int pinned_stages() {
-  const char* v = getenv("CO_TC_STAGES");       // A/B runs only: cap the A pipeline depth
-  return v ? std::max(2, atoi(v)) : kMaxStagesStd;
+int pinned_stages() {                                         // A/B experiments: cap the A pipeline depth
+  return std::max(2, CO_EXP("CO_TC_STAGES", kMaxStagesStd));
 }
 
 // HALO / FLAT: weights resident.  Largest CC whose weights + 2 A stages fit.
@@ -1057,7 +1034,7 @@ bool plan_resident(const Geom& g, Plan& pl) {
   // FLAT (C5's 64 KB A stages) keeps the general budget: its pair fits only there
   const size_t budget = flat ? kSmemBudget : kHaloBudget;
   const int eg_pin = pinned_eg();
-  const char* pair_env = getenv("CO_TC_PAIR");    // A/B runs: pin 1 or 2
+  const int pair_pin = int(option(OPT_PAIR));     // option "pair": 0 auto, 1 / 2 pinned
   const Variant* best = nullptr;
   int64_t best_rank = -1;
   for (const Variant& v : kVariants) {
@@ -1065,7 +1042,7 @@ bool plan_resident(const Geom& g, Plan& pl) {
     if (v.KH && (v.KH != g.kh || v.KW != g.kw || v.KC * 16 != g.Cin)) continue;
     if ((eg_pin && v.EG != eg_pin) || (pinned_cc() && v.CC != pinned_cc()) || (pinned_ce() && v.CE != pinned_ce()))
       continue;
-    if (v.CS != pinned_cs() || (pair_env && v.PAIR != atoi(pair_env))) continue;
+    if (v.CS != pinned_cs() || (pair_pin && v.PAIR != pair_pin)) continue;
     const int64_t w_bytes = int64_t(v.KT * v.CC) * K * 2 / v.PAIR;   // per CTA
     const size_t fixed = 1024 + size_t((w_bytes + 1023) / 1024 * 1024) + 512 + v.CC * 4 + tail;
     if (fixed + 2 * size_t(a_stride) > kSmemLimit) continue;
@@ -1143,7 +1120,7 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
   const Variant* best = nullptr;
   const int want = kloop_pair(kb);
   for (int pair : {want, 3 - want}) {           // the preferred pairing, else the other
-    if (getenv("CO_TC_KPAIR") && pair != want) break;
+    if (option(OPT_KPAIR) && pair != want) break;
     for (const Variant& v : kVariants) {
       if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.CS != 1 || v.PAIR != pair) continue;
       if ((eg_pin && v.EG != eg_pin) || (pinned_cc() && v.CC != pinned_cc())) continue;
@@ -1153,7 +1130,7 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
       const int64_t tiles = flat ? (g.B * g.HWo + 127) / 128 : g.B * ((g.Ho + TH - 1) / TH) * ((g.Wo + TW - 1) / TW);
       auto rank = [&](const Variant* x) {
         const int64_t items = (tiles + x->PAIR - 1) / x->PAIR * (g.Cout / x->CC) * x->PAIR;
-        const bool fills = getenv("CO_TC_FILL") && !atoi(getenv("CO_TC_FILL")) ? true : items * 2 >= sm_count();
+        const bool fills = !CO_EXP("CO_TC_FILL", 1) ? true : items * 2 >= sm_count();
         return (fills ? 1000000 : 0) + x->CC * 1000 + x->EG;
       };
       if (!best || rank(&v) > rank(best)) best = &v;
@@ -1171,8 +1148,8 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
   const int stage = (b_off + b_bytes + 1023) / 1024 * 1024;
   const size_t fixed = 1024 + 512 + best->CC * 4 + 64 * 4;   // + the KHALO tap table
   const size_t cap = (fixed + 2 * size_t(stage) <= kSmemBudget) ? kSmemBudget : kSmemLimit;
-  const char* ks = getenv("CO_TC_KSTAGES");     // A/B runs only: cap the K pipeline depth
-  const int stages = int(std::min<size_t>(ks ? std::max(2, atoi(ks)) : kMaxStagesStd, (cap - fixed) / size_t(stage)));
+  const int ks = CO_EXP("CO_TC_KSTAGES", 0);     // A/B experiments only: cap the K pipeline depth
+  const int stages = int(std::min<size_t>(ks ? std::max(2, ks) : kMaxStagesStd, (cap - fixed) / size_t(stage)));
   if (stages < 2) return false;
   pl.var = best;
   pl.mode = MODE_KLOOP;
@@ -1212,11 +1189,11 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
     const size_t fixed2 = fixed + size_t(ka_stages) * ka_stride;
     // the K-pipelined layers are tensor-bound and their epilogues wait on the
     // MMA, so the weight ring takes all of shared memory (C4: L3 1.73 -> 1.42 ms,
-    // L5 1.53 -> 1.39 ms against the 190 KB budget); CO_TC_KHALO_SMEM (KB) caps it
-    const char* kf = getenv("CO_TC_KHALO_SMEM");
-    const size_t cap2 = kf ? std::min(kSmemLimit, size_t(atoi(kf)) * 1024) : kSmemLimit;
+    // L5 1.53 -> 1.39 ms against the 190 KB budget); CO_TC_KHALO_SMEM (KB, experiment builds) caps it
+    const int kf = CO_EXP("CO_TC_KHALO_SMEM", 0);
+    const size_t cap2 = kf ? std::min(kSmemLimit, size_t(kf) * 1024) : kSmemLimit;
     const int bst = fixed2 + 2 * size_t(b_stride) <= cap2
-                        ? int(std::min<size_t>(ks ? std::max(2, atoi(ks)) : kMaxStages, (cap2 - fixed2) / size_t(b_stride)))
+                        ? int(std::min<size_t>(ks ? std::max(2, ks) : kMaxStages, (cap2 - fixed2) / size_t(b_stride)))
                         : 0;
     const size_t over = size_t((prow - MT) * Wq + (Wq - g.Wo) + 128) * 128;
     if (bst >= 2 && over <= size_t(ka_phase) + size_t(bst) * b_stride) {
@@ -1264,8 +1241,7 @@ Plan make_plan(const Geom& g) {
   } else if (g.Cin % 16 != 0) {
     return pl;
   }
-  const char* mode = getenv("CO_TC_MODE");      // A/B runs only: "kloop" forces the K pipeline
-  const bool force_kloop = mode && std::string(mode) == "kloop";
+  const bool force_kloop = option(OPT_TC_MODE) == 1;   // option "tc_mode" = 1 forces the K pipeline
   pl.ok = (!force_kloop && plan_resident(pl.gk, pl)) || plan_kloop(pl.gk, pl);
   if (pl.ok && pl.mode != MODE_KLOOP && pl.gk.Cin % 64 == 0 && swa_enabled()) pl.swa = 1;
   if (pl.ok) pl.n_split = g.Cout / pl.var->CC;
@@ -1343,7 +1319,7 @@ DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
   else
     snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d%s%s>", pl.var->KT, pl.var->CC, pl.var->EG,
              pl.var->PAIR > 1 ? ",pair" : "", mname);
-  if (getenv("CO_LOG"))
+  if (option(OPT_LOG))
     fprintf(stderr, "[co] %s: %d parts, %lld tiles, %d stages x %d B, smem %zu B%s\n", buf, pl.n_split,
             (long long)pl.n_tiles, pl.stages, pl.a_stride, pl.smem, pl.ystage ? ", y staged" : "");
   t->name = buf;
@@ -1504,8 +1480,7 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   // weight-multicast clusters for one-CTA K-pipeline layers (CO_TC_MC = cluster size, A/B runs)
   int mc = 1;
   if (pl.mode == MODE_KLOOP && pair == 1 && T == 1) {
-    const char* e = getenv("CO_TC_MC");
-    mc = e ? std::max(1, std::min(8, atoi(e))) : 1;
+    mc = int(option(OPT_MC));                        // option "mc" (weight multicast cluster size)
     while (mc > 1 && ((pl.b_bytes / 16) % mc != 0 || pl.n_tiles < mc)) mc /= 2;
   }
   const int clu = pair > 1 ? pair : mc;                  // CTAs per cluster
@@ -1515,18 +1490,15 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   p.w_bytes = pl.w_bytes; p.w_off = pl.w_off;
   for (int i = 0; i < kMaxKt; ++i) p.slot[i] = a.slot[i];
   p.emit = a.emit; p.update = a.update; p.act = g.act; p.out_f32 = (g.out_dtype == F32);
-  static const int dbg = getenv("CO_TC_DEBUG") ? atoi(getenv("CO_TC_DEBUG")) : 0;
-  p.dbg = dbg;
+  p.dbg = CO_EXP("CO_TC_DEBUG", 0);              // experiment builds only (work-skipping A/B bits)
   p.ystage = (pl.ystage && g.out_dtype == BF16) ? 1 : 0;
   {
     // programmatic dependent launch for single steps (CO_PDL=0 turns it off):
     // C5 +1.7%, C4 +0.5%, C2 unchanged (its launches were already back to back)
-    const char* e = getenv("CO_PDL");
-    p.pdl = (T == 1 && (e ? atoi(e) != 0 : true)) ? 1 : 0;
+    p.pdl = (T == 1 && option(OPT_PDL) != 0) ? 1 : 0;
   }
   {
-    const char* e = getenv("CO_TC_L2LAST");     // A/B runs
-    p.l2last = (pl.mode == MODE_HALO || pl.mode == MODE_FLAT) && (e ? atoi(e) != 0 : false);
+    p.l2last = (pl.mode == MODE_HALO || pl.mode == MODE_FLAT) && CO_EXP("CO_TC_L2LAST", 0) != 0;   // A/B
   }
   p.y_off = pl.y_off;
   p.raw_kh = g.raw ? g.kh : 0;
@@ -1594,12 +1566,11 @@ cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const fl
 }
 
 bool dense_tc_chunkable(const DenseTC* t, const Geom& g) {
-  if (const char* e = getenv("CO_CHUNK"))       // experiment / test knob: 0 = always fold per step
-    if (!atoi(e)) return false;
+  if (!option(OPT_CHUNK)) return false;          // option "chunk" = 0: always fold per step
   // HALO only: FLAT chunks must first be staged time-major (a 128-row tile spans
   // streams), which costs more than the L2 reuse saves (measured on C5: 9.5 M
-  // chunked vs 9.7 M per-step stream-steps/s); CO_CHUNK_FLAT=1 enables it for A/B runs
-  const bool flat_ok = getenv("CO_CHUNK_FLAT") && atoi(getenv("CO_CHUNK_FLAT"));
+  // chunked vs 9.7 M per-step stream-steps/s); option "chunk_flat" = 1 enables it
+  const bool flat_ok = option(OPT_CHUNK_FLAT) != 0;
   return t && !g.raw && !t->pl.wcols && (t->pl.mode == MODE_HALO || (flat_ok && t->pl.mode == MODE_FLAT)) &&
          g.st == 1;
 }

@@ -752,14 +752,13 @@ static int st_chunk_rows(const Depthwise* t, const Geom& g, int& WC, size_t& sme
 }
 
 bool depthwise_chunkable(const Depthwise* t, const Geom& g) {
-  if (const char* e = getenv("CO_CHUNK"))       // experiment / test knob: 0 = always fold per step
-    if (!atoi(e)) return false;
+  if (!option(OPT_CHUNK)) return false;          // option "chunk" = 0: always fold per step
   if (!t || !t->pl.var->chunk || g.raw || g.st != 1 || g.dt != 1 || g.kt < 2) return false;
   if (t->pl.temporal) return true;
   // chunked K2 (k_steps_dw_st) is correct but slower than the per-step K2 on C3-a
   // (1.12 M vs 1.48 M stream-steps/s: shared-memory / latency bound at one
-  // 672-thread CTA per SM), so the stencil folds per step unless CO_CHUNK_ST=1
-  if (!(getenv("CO_CHUNK_ST") && atoi(getenv("CO_CHUNK_ST")))) return false;
+  // 672-thread CTA per SM), so the stencil folds per step unless option "chunk_st" = 1
+  if (!option(OPT_CHUNK_ST)) return false;
   int WC;
   size_t smem;
   return st_chunk_rows(t, g, WC, smem) > 0;
@@ -846,9 +845,8 @@ cudaError_t depthwise_step(Depthwise* t, const Geom& g, const StepArgs& a, const
   cfg.dynamicSmemBytes = pl.temporal ? 0 : pl.smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  const char* pe = getenv("CO_PDL");            // programmatic dependent launch (CO_PDL=0: off)
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = (!pe || atoi(pe) != 0) ? 1 : 0;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // option "pdl" = 0: off
+  attr[0].val.programmaticStreamSerializationAllowed = option(OPT_PDL) != 0 ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(pl.var->fn), args);

@@ -187,12 +187,9 @@ bool mha_supported(int E, int heads) {
 
 // keys per lane per iteration for dh = 64: 2 (default) keeps twice the K / V
 // rows in flight per warp at 3 blocks per SM -- MHA step 106 -> 97 us; 4
-// measured the same; CO_MHA_KU=1 restores one key (A/B).  Each lane still
-// folds its keys in index order, so all variants give identical results.
-int ku() {
-  const char* e = getenv("CO_MHA_KU");
-  return e ? atoi(e) : 2;
-}
+// measured the same; CO_MHA_KU=1 restores one key (A/B, experiment builds).
+// Each lane still folds its keys in index order, so all variants give identical results.
+int ku() { return CO_EXP("CO_MHA_KU", 2); }
 
 cudaError_t launch_mha_attend(const MhaArgs& a, cudaStream_t s) {
   int dev = 0, sms = 148;
@@ -207,7 +204,6 @@ cudaError_t launch_mha_attend(const MhaArgs& a, cudaStream_t s) {
     const int64_t cap = int64_t(sms) * (per_sm > 0 ? per_sm : 1);
     return int(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
   };
-  const char* pe = getenv("CO_PDL");
   auto launch = [&](auto fn) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(grid_of((const void*)fn)));
@@ -215,7 +211,7 @@ cudaError_t launch_mha_attend(const MhaArgs& a, cudaStream_t s) {
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = (!pe || atoi(pe) != 0) ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = option(OPT_PDL) != 0 ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, fn, a);

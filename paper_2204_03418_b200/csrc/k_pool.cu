@@ -466,7 +466,7 @@ int band_rows(const Geom& g, int V, int& rows, size_t& smem) {
   // just enough rows for 128 threads
   int th_max = std::min(g.Ho, std::min(1024 / std::max(1, g.Wo * CV), (128 + g.Wo * CV - 1) / std::max(1, g.Wo * CV)));
   th_max = std::max(th_max, 1);
-  if (const char* e = getenv("CO_POOL_BAND_TH")) th_max = std::min(th_max, std::max(1, atoi(e)));   // A/B runs
+  if (const int e = CO_EXP("CO_POOL_BAND_TH", 0)) th_max = std::min(th_max, std::max(1, e));   // A/B experiments
   for (int TH = th_max; TH >= 1; --TH) {
     rows = (TH - 1) * g.sh + (g.kh - 1) * g.dh + 1;
     smem = size_t(rows) * row_bytes;
@@ -620,10 +620,7 @@ bool deep_chunks(const Geom& g, int64_t threads) {
   return threads < int64_t(num_sms()) * 2048 * 4 || g.kh * g.kw > 16;
 }
 
-bool pool_pdl() {
-  const char* e = getenv("CO_PDL");            // CO_PDL=0: plain stream serialization (A/B)
-  return !e || atoi(e) != 0;
-}
+bool pool_pdl() { return option(OPT_PDL) != 0; }   // option "pdl" = 0: plain stream serialization
 
 int grid_for(int64_t total) {
   int dev = 0, sms = 148;
@@ -795,13 +792,11 @@ cudaError_t launch_pool_rebuild(const Geom& g, void* state, int64_t m_next, cuda
                             : rebuild_t<float, true>(g, state, m_next, s);
 }
 
-bool pool_band_enabled() {
-  const char* e = getenv("CO_POOL_BAND");                       // A/B and test knob (default on)
-  return !e || atoi(e) != 0;
-}
+bool pool_band_enabled() { return option(OPT_POOL_BAND) != 0; }   // option "pool_band" (default on)
 
 int pool_block_decomposition(const Geom& g) {
-  if (const char* e = getenv("CO_POOL_VH")) return atoi(e) ? 1 : 0;   // experiment / test knob
+  const int64_t v = option(OPT_POOL_VH);             // option "pool_vh": -1 auto, 0 / 1 pinned
+  if (v >= 0) return int(v);
   return g.kt >= kVhMinKt ? 1 : 0;
 }
 
@@ -815,9 +810,9 @@ cudaError_t launch_fill_pad(const Geom& g, void* p, int64_t n_elems, cudaStream_
 }
 
 int pool_split_lanes(const Geom& g) {
-  if (const char* e = getenv("CO_POOL_G")) {     // experiment / test knob
+  if (const int e = int(option(OPT_POOL_G))) {   // option "pool_g": pinned lanes per vector
     const int CV = g.Cin / vec_width(g);
-    int G = atoi(e);
+    int G = e;
     G = G < 1 ? 1 : (G > 32 ? 32 : G);
     while (G > 1 && G * CV > 512) --G;
     return G;

@@ -5,7 +5,7 @@ separately from online per-step numbers").  Workloads: C3's depthwise layers
 C5's Conv1d (tcgen05: one launch per chunk, item-batch-major, so a tile's state
 stays L2-resident across its frames), each at its BASELINE.json stream count,
 driven through co_forward_steps over device clips of T frames (seeded N(0,1));
-the per-step leg forces the per-frame fold (CO_CHUNK=0 in a subprocess).  Timing: CUDA events around K clips after W warm-up clips; clips rotate
+the per-step leg forces the per-frame fold (option chunk = 0 in a subprocess).  Timing: CUDA events around K clips after W warm-up clips; clips rotate
 over two buffers of T frames each (each > L2).
 
 Algorithmic bytes per stream-step: per-step fold x + y + 2 (kt-1) fp32 state
@@ -64,7 +64,8 @@ def leg(name, T, clips, warmup):
     steps = clips * T
     ms = e0.elapsed_time(e1) / steps
     hbm, _, src = measured_peaks()
-    chunked = os.environ.get("CO_CHUNK", "1") != "0"
+    import paper_2204_03418_b200 as co
+    chunked = co.get_option("chunk") != 0
     import math
     el_in = math.prod(conv.in_spatial) * L.cin
     el_out = math.prod(conv.out_spatial) * L.cout
@@ -89,15 +90,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--workload", default="all", choices=["all"] + list(WORKLOADS))
     ap.add_argument("--leg", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--chunk", default="1", help=argparse.SUPPRESS)
     a = ap.parse_args()
     if a.leg:
+        import paper_2204_03418_b200 as co
+        co.set_option("chunk", int(a.chunk))      # documented option: 0 = fold per step
         print(json.dumps(leg(a.workload, a.T, a.clips, a.warmup)), flush=True)
         return
     for name in (WORKLOADS if a.workload == "all" else [a.workload]):
         for chunk in ("0", "1"):
-            env = dict(os.environ, CO_CHUNK=chunk)
-            out = subprocess.run([sys.executable, __file__, "--leg", "--workload", name, "--T", str(a.T), "--clips",
-                                  str(a.clips), "--warmup", str(a.warmup)], env=env, capture_output=True, text=True)
+            out = subprocess.run([sys.executable, __file__, "--leg", "--chunk", chunk, "--workload", name, "--T",
+                                  str(a.T), "--clips", str(a.clips), "--warmup", str(a.warmup)],
+                                 capture_output=True, text=True)
             line = [l for l in out.stdout.splitlines() if l.startswith("{")]
             print(line[-1] if line else json.dumps({"workload": name, "mode": chunk, "error": out.stderr[-400:]}),
                   flush=True)

@@ -30,6 +30,18 @@ def rand_desc(rng, max_c=4, max_s=6, allow_stride_t=True):
     return d
 
 
+def set_opt(name: str, value) -> None:
+    """A documented planner option (co_set_option); conftest resets them all after each test."""
+    import paper_2204_03418_b200 as co
+    co.set_option(name, int(value))
+
+
+def reset_opt(name: str) -> None:
+    import paper_2204_03418_b200 as co
+    from paper_2204_03418_b200 import _abi
+    co.set_option(name, _abi.OPTION_DEFAULTS[name])
+
+
 def logical_step_shape(d: O.Desc, B: int):
     H, W = d.in_hw
     return (B, d.cin) + ((H,) if d.spatial_rank >= 1 else ()) + ((W,) if d.spatial_rank >= 2 else ())

@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol(libpath):
 def test_library_loads_without_gpu(libpath):
     L = ctypes.CDLL(libpath)
     L.co_abi_version.restype = ctypes.c_int
-    assert L.co_abi_version() == 3
+    assert L.co_abi_version() == 4
     L.co_last_error.restype = ctypes.c_char_p
     assert L.co_last_error() == b""
 
@@ -74,3 +74,31 @@ def test_invalid_descriptor_is_rejected_on_host(libpath):
     d.groups = 1
     d.padding = (ctypes.c_int32 * 3)(3, 0, 0)                              # p_t > f - 1
     assert L.co_conv_create(ctypes.byref(d), ctypes.c_void_p(1), None, 0, ctypes.byref(h)) == _abi.CO_ERR_ARG
+
+
+def test_options_api_on_host(libpath):
+    """co_set_option / co_get_option / co_option_name: the documented knobs,
+    their defaults, range checks and the NULL reset (host-only calls)."""
+    import paper_2204_03418_b200 as co
+    from paper_2204_03418_b200 import _abi
+    co.reset_options()
+    assert co.all_options() == _abi.OPTION_DEFAULTS
+    with co.options(tc_mode=1, pair=2):
+        assert co.get_option("tc_mode") == 1 and co.get_option("pair") == 2
+    assert co.get_option("tc_mode") == 0 and co.get_option("pair") == 0
+    with pytest.raises(_abi.CoError):
+        co.set_option("no_such_option", 1)
+    with pytest.raises(_abi.CoError):
+        co.set_option("pair", 3)                    # out of range
+    co.set_option("chunk", 0)
+    co.reset_options()
+    assert co.get_option("chunk") == 1
+
+
+def test_release_library_reads_no_experiment_knobs(libpath):
+    """The shipped library holds none of the A/B experiment variables (they are
+    compiled only with -DCO_EXPERIMENTS) and no CO_* environment names at all:
+    its only switches are the documented co_set_option names."""
+    out = subprocess.run(["strings", libpath], capture_output=True, text=True, check=True).stdout
+    leaked = sorted(set(re.findall(r"\bCO_(?:TC|PDL|CHUNK|POOL|MHA|LOG|LIB)[A-Z0-9_]*", out)))
+    assert not leaked, leaked

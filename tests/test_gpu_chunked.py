@@ -10,7 +10,7 @@ import pytest
 import torch
 
 import oracle as O
-from tests.helpers import make_pair, np_of, rel_err
+from tests.helpers import reset_opt, set_opt, make_pair, np_of, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -31,7 +31,7 @@ def test_chunked_equals_per_step_fold(kt, pad, out_dtype, monkeypatch):
     bt = rng.standard_normal(C) * 0.1
     runs = {}
     for chunk in ("1", "0"):
-        monkeypatch.setenv("CO_CHUNK", chunk)
+        set_opt("chunk", chunk)
         conv, sm, _, _ = make_pair(d, Wt, bt, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="depthwise",
                                    activation="relu")
         rng2 = np.random.default_rng(1)
@@ -54,7 +54,7 @@ def test_chunked_equals_per_step_fold(kt, pad, out_dtype, monkeypatch):
 def test_chunked_matches_oracle_and_continues_per_step(monkeypatch):
     """A chunk, then per-step calls, then another chunk: every Ready output
     matches the oracle fed the same frames."""
-    monkeypatch.setenv("CO_CHUNK", "1")
+    set_opt("chunk", "1")
     rng = np.random.default_rng(3)
     B, C, H, W, kt = 2, 64, 3, 4, 5
     d = O.Desc(2, C, C, (kt, 1, 1), groups=C, in_spatial=(H, W))
@@ -107,11 +107,11 @@ def test_dense_chunked_equals_per_step_fold(name, chunk_t, monkeypatch):
     Wt = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
     bt = rng.standard_normal(d.cout) * 0.1
     if chunk_t:
-        monkeypatch.setenv("CO_CHUNK_T", chunk_t)
-    monkeypatch.setenv("CO_CHUNK_FLAT", "1")      # FLAT chunking is off by default; keep it covered
+        set_opt("chunk_t", chunk_t)
+    set_opt("chunk_flat", "1")      # FLAT chunking is off by default; keep it covered
     runs = {}
     for chunk in ("1", "0"):
-        monkeypatch.setenv("CO_CHUNK", chunk)
+        set_opt("chunk", chunk)
         conv, _, _, _ = make_pair(d, Wt, bt, B, dtype=torch.bfloat16, out_dtype=torch.float32, kernel="dense_tc")
         rng2 = np.random.default_rng(2)
         outs = []
@@ -136,7 +136,7 @@ def test_dense_chunked_matches_oracle():
     import paper_2204_03418_b200 as co
     d, B = DENSE["flat_pair_c5"]
     rng = np.random.default_rng(9)
-    os.environ["CO_CHUNK_FLAT"] = "1"
+    set_opt("chunk_flat", "1")
     conv, sm, _, _ = make_pair(d, rng.standard_normal(d.w_shape) / 48, rng.standard_normal(d.cout) * 0.1, B,
                                dtype=torch.bfloat16, out_dtype=torch.float32, kernel="dense_tc")
     got, ref = [], []
@@ -155,7 +155,7 @@ def test_dense_chunked_matches_oracle():
             r = sm.forward_step(f)
             if r is not None:
                 ref.append(r)
-    os.environ.pop("CO_CHUNK_FLAT", None)
+    reset_opt("chunk_flat")
     assert len(got) == len(ref) == 36 - (d.receptive_field - 1)
     g = np.stack(got)
     assert rel_err(g, np.stack(ref).reshape(g.shape)) <= 1e-4
@@ -171,10 +171,10 @@ def test_depthwise_stencil_chunked_equals_per_step(kt, k, pad, monkeypatch):
     d = O.Desc(2, C, C, (kt, k, k), padding=pad, groups=C, in_spatial=(H, W))
     Wt = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
     bt = rng.standard_normal(C) * 0.1
-    monkeypatch.setenv("CO_CHUNK_ST", "1")        # off by default (slower); keep it covered
+    set_opt("chunk_st", "1")        # off by default (slower); keep it covered
     runs = {}
     for chunk in ("1", "0"):
-        monkeypatch.setenv("CO_CHUNK", chunk)
+        set_opt("chunk", chunk)
         conv, _, _, _ = make_pair(d, Wt, bt, B, dtype=torch.bfloat16, out_dtype=torch.float32, kernel="depthwise",
                                   activation="relu")
         rng2 = np.random.default_rng(3)

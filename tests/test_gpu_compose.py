@@ -49,6 +49,10 @@ BODIES = {
                         (64, 32, (1, 1, 1), (0, 0, 0), 1, False)], False),
     # two temporal convs, centered: f = 5, d = 4, d_skip = 2
     "two_center": ([(16, 16, (3, 3, 3), (0, 1, 1), 1, True), (16, 16, (3, 3, 3), (0, 1, 1), 1, False)], True),
+    # centered with some temporal padding: f = 5, p = 1, d = 3, d_skip = 2, batch crop 1
+    "conv_center_padded": ([(32, 32, (5, 3, 3), (1, 1, 1), 1, False)], True),
+    # two layers, f_acc = 5, p_acc = 1 (padding in the first layer only)
+    "two_center_padded": ([(16, 16, (3, 3, 3), (1, 1, 1), 1, True), (16, 16, (3, 3, 3), (0, 1, 1), 1, False)], True),
 }
 
 
@@ -73,7 +77,7 @@ def test_residual_step_vs_oracle(name, relu_out):
             assert rel_err(np_of(y), r) <= 1e-4, t
 
 
-@pytest.mark.parametrize("name", ["conv_eq", "conv_center", "two_center"])
+@pytest.mark.parametrize("name", ["conv_eq", "conv_center", "two_center", "conv_center_padded", "two_center_padded"])
 def test_residual_forward_vs_oracle(name):
     import paper_2204_03418_b200 as co
     rng = np.random.default_rng(5)

@@ -9,7 +9,7 @@ import pytest
 import torch
 
 import oracle as O
-from tests.helpers import assert_bf16_rounding_bound, make_pair, np_of, rel_err, to_cl
+from tests.helpers import reset_opt, set_opt, assert_bf16_rounding_bound, make_pair, np_of, rel_err, to_cl
 
 pytestmark = pytest.mark.gpu
 
@@ -78,19 +78,19 @@ def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force
         W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
         b = rng.standard_normal(d.cout) * 0.1
     if force_kloop:
-        os.environ["CO_TC_MODE"] = "kloop"
+        set_opt("tc_mode", 1)
     if force_kloop or case.startswith("kloop"):
-        os.environ["CO_TC_KHALO"] = "0"              # keep the strided-gather K pipeline covered
+        set_opt("khalo", "0")              # keep the strided-gather K pipeline covered
     if pair:
-        os.environ["CO_TC_PAIR"] = "2"
-        os.environ["CO_TC_KPAIR"] = "2"
+        set_opt("pair", "2")
+        set_opt("kpair", "2")
     try:
         conv, sm, Wq, bq = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="dense_tc")
     finally:
-        os.environ.pop("CO_TC_MODE", None)
-        os.environ.pop("CO_TC_PAIR", None)
-        os.environ.pop("CO_TC_KPAIR", None)
-        os.environ.pop("CO_TC_KHALO", None)
+        reset_opt("tc_mode")
+        reset_opt("pair")
+        reset_opt("kpair")
+        reset_opt("khalo")
     if pair:
         assert "pair" in conv.kernel_name, conv.kernel_name
     ref_conv, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="direct")
@@ -150,7 +150,7 @@ def test_dense_tc_weight_multicast(case, mc, monkeypatch):
     CTA loads 1/mc of every weight chunk and multicasts it, stages are released
     by every CTA's commit -- same results as the oracle, bit for bit in the
     integer regime."""
-    monkeypatch.setenv("CO_TC_MC", mc)
+    set_opt("mc", mc)
     _, y, ref, yd = _run(case)
     assert rel_err(y, ref) <= 1e-4 and rel_err(y, yd) <= 1e-4
     _, y, ref, _ = _run(case, integer=True)

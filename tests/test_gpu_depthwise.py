@@ -143,7 +143,7 @@ def test_depthwise_state_steps_and_purity(case):
     c4, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="depthwise")
     ys, mask = c3.forward_steps(clip, pad_end=True)
     fold = [y for y in (c4.forward_step(x) for x in frames) if y is not None]
-    fold += [y for y in (c4.forward_step(None) for _ in range(d.padding[0])) if y is not None]
+    fold += [y for y in (c4.forward_pad_step() for _ in range(d.padding[0])) if y is not None]
     assert ys.shape[2] == len(fold) == int(mask.sum())
     for i, f in enumerate(fold):
         assert torch.equal(ys[:, :, i], f)

@@ -107,7 +107,7 @@ def test_forward_steps_is_bitwise_fold_and_pad_end_matches_batch(seed):
         if y is not None:
             fold.append(np_of(y))
     for _ in range(d.padding[0]):
-        y = c.forward_step(None)
+        y = c.forward_pad_step()
         if y is not None:
             fold.append(np_of(y))
     assert ys.shape[2] == len(fold) == int(mask.sum())

@@ -112,3 +112,45 @@ def test_unsupported_requests_fail_loudly():
     with pytest.raises(CoError) as e:      # kt > CO_MAX_KT
         co.Conv(8, 8, (33, 1, 1), weight=wl, in_spatial=(2, 2))
     assert e.value.code == CO_ERR_UNSUPPORTED
+
+
+def test_none_input_is_empty_and_does_not_advance():
+    """an Empty input returns Empty and leaves the clock and state
+    untouched, so hand-chained layers short-circuit like a Stack; a padding step
+    (pad_end, P:215) is asked for explicitly (forward_pad_step)."""
+    import paper_2204_03418_b200 as co
+    d = O.Desc(2, 16, 16, (3, 3, 3), padding=(1, 1, 1), in_spatial=(5, 6))
+    rng = np.random.default_rng(0)
+    c, sm, _, _ = make_pair(d, rng.standard_normal(d.w_shape) / 12, None, 2, dtype=torch.bfloat16)
+    c2, _, _, _ = make_pair(d, rng.standard_normal(d.w_shape) / 12, None, 2, dtype=torch.bfloat16,
+                            out_dtype=torch.bfloat16)
+    assert c.forward_step(None) is None and c.n == 0
+    assert c2.forward_step(c2.forward_step(None)) is None and c2.n == 0
+    x = to_cl(rng.standard_normal((2, 16, 5, 6)), torch.bfloat16)
+    c.forward_step(x)
+    assert c.n == 1
+    y = c.forward_pad_step()
+    assert c.n == 2 and y is not None             # d = 1: the padding step is Ready
+    with pytest.raises(ValueError):
+        c.forward_step(x, pad=True)
+
+
+def test_out_tensor_is_validated():
+    """The kernels write `out` through its data pointer: wrong shape, dtype,
+    device or layout is refused before any launch."""
+    import paper_2204_03418_b200 as co
+    d = O.Desc(2, 16, 8, (1, 3, 3), padding=(0, 1, 1), in_spatial=(5, 6))
+    rng = np.random.default_rng(1)
+    c, _, _, _ = make_pair(d, rng.standard_normal(d.w_shape), None, 2, dtype=torch.bfloat16)
+    x = to_cl(rng.standard_normal((2, 16, 5, 6)), torch.bfloat16)
+    good = co._empty_cl((2, 8, 5, 6), torch.float32, "cuda")
+    assert c.forward_step(x, out=good) is good
+    for bad in (co._empty_cl((2, 8, 5, 5), torch.float32, "cuda"),            # shape
+                co._empty_cl((2, 8, 5, 6), torch.bfloat16, "cuda"),           # dtype
+                torch.empty((2, 8, 5, 6), dtype=torch.float32, device="cuda"),  # not channels-last
+                co._empty_cl((2, 8, 5, 6), torch.float32, "cpu")):            # device
+        with pytest.raises(ValueError):
+            c.forward_step(x, out=bad)
+    st = co.Stack([c])
+    with pytest.raises(ValueError):
+        st.forward_step(x[:1])                                                 # wrong stream count

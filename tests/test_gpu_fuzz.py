@@ -103,3 +103,46 @@ def test_fuzz_bf16_relu_vs_direct(seed):
     rms = float(np.sqrt(np.mean(r ** 2)))
     excess = (np.abs(y - r) - (2.0 ** -7 * np.maximum(np.abs(y), np.abs(r)) + 1e-3 * rms)).max()
     assert excess <= 0, (fast.kernel_name, d, B, excess, rel_err(y, r))
+
+
+def _oracle_cases(n=24, budget=1.5e9):
+    """Seeded shapes of the same sweep whose fp64 oracle run stays small: the
+    MACs of every Ready output over the run <= budget.  Deterministic."""
+    out, seed = [], 40000
+    while len(out) < n:
+        rng = np.random.default_rng(seed)
+        d, B = _shape(rng)
+        ticks = d.receptive_field + 3 * d.stride[0] + 2
+        Ho, Wo = d.out_spatial
+        macs = B * ticks * d.cout * (d.cin // d.groups) * int(np.prod(d.kernel)) * Ho * Wo
+        if macs <= budget:
+            out.append(seed)
+        seed += 1
+    return out
+
+
+@pytest.mark.parametrize("seed", _oracle_cases())
+def test_fuzz_dispatched_vs_oracle(seed):
+    """Shapes of the same sweep checked against the fp64 ORACLE itself (not the
+    CUDA-core kernel), so an error shared by both CUDA paths -- weight packing,
+    the host clock's slot arguments, the bias -- cannot pass: ready / n / head
+    per tick bit-exact, outputs within 1e-4 of the RMS."""
+    from tests.helpers import make_pair
+    rng = np.random.default_rng(seed)
+    d, B = _shape(rng)
+    W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
+    b = rng.standard_normal(d.cout) * 0.1
+    conv, sm, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=torch.float32)
+    H, Wd = d.in_hw
+    ys, rs = [], []
+    for t in range(d.receptive_field + 3 * d.stride[0] + 2):
+        x = to_cl(rng.standard_normal((B, d.cin, H, Wd)), torch.bfloat16)
+        y = conv.forward_step(x)
+        r = sm.forward_step(np_of(x))
+        assert (y is None) == (r is None), (t, conv.kernel_name)
+        assert (conv.n, conv.head) == (sm.n, sm.head)
+        if y is not None:
+            ys.append(np_of(y)); rs.append(r.reshape(y.shape))
+    assert ys, d
+    err = rel_err(np.stack(ys), np.stack(rs))
+    assert err <= 1e-4, (conv.kernel_name, d, B, err)

@@ -78,3 +78,19 @@ def test_mha_batch_update_state_and_state_round_trip():
         y = m.forward_step(torch.from_numpy(xs[t]).to(torch.bfloat16).cuda())
         assert (y is None) == (t < window - 1)
     assert rel_err(np_of(y), OM.mha_forward(p, clip)[:, :, -1]) <= 2e-2
+
+
+def test_batch_mode_requires_window_length():
+    """batch attention is the fixed-window form, T == n; any
+    other T is a window error (CO_ERR_LENGTH through the ABI)."""
+    import paper_2204_03418_b200 as co
+    from paper_2204_03418_b200 import _abi
+    m, _, _ = _make(64, 1, 4, 2, np.random.default_rng(0))
+    x = torch.zeros((2, 64, 5), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError):
+        m.forward(x)
+    xt = torch.zeros((2, 5, 64), dtype=torch.bfloat16, device="cuda")
+    y = torch.empty((2, 5, 64), dtype=torch.bfloat16, device="cuda")
+    import ctypes as C
+    rc = _abi.lib().co_mha_forward(m._h, C.c_void_p(xt.data_ptr()), 5, C.c_void_p(y.data_ptr()), None)
+    assert rc == _abi.CO_ERR_LENGTH

@@ -15,7 +15,7 @@ import pytest
 import torch
 
 from oracle import pool as OP
-from tests.helpers import assert_bf16_rounding_bound, np_of, rel_err
+from tests.helpers import reset_opt, set_opt, assert_bf16_rounding_bound, np_of, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -77,10 +77,10 @@ def pool_lanes(request, monkeypatch):
     G, vh = request.param
     if G == "1b":                                  # the plain kernel without the row-band staging
         G = "1"
-        monkeypatch.setenv("CO_POOL_BAND", "0")
+        set_opt("pool_band", "0")
     if G != "auto":
-        monkeypatch.setenv("CO_POOL_G", G)
-        monkeypatch.setenv("CO_POOL_VH", vh)
+        set_opt("pool_g", G)
+        set_opt("pool_vh", vh)
     return "exact" if (G, vh) == ("1", "0") else "reordered"
 
 
@@ -106,7 +106,7 @@ def test_pool_step_random_vs_oracle(kind, seed, pool_lanes):
             _compare(kind, np_of(y).reshape(r.shape), r, out_dtype)
     # pad_end steps (x = None): padding, -inf for MAX
     for _ in range(pad[0]):
-        y = p.forward_step(None)
+        y = p.forward_pad_step()
         r = sm.forward_step(None)
         assert (y is None) == (r is None)
         if y is not None:
@@ -243,7 +243,7 @@ def test_block_decomposition_state_round_trip(kind, monkeypatch):
     ahead: its outputs match the oracle continued from the same point and are
     bitwise those the uninterrupted handle later produces."""
     import copy
-    monkeypatch.setenv("CO_POOL_VH", "1")
+    set_opt("pool_vh", "1")
     rng = np.random.default_rng(77)
     B, C, H, W = 2, 16, 4, 5
     kernel, stride, pad, dil = (7, 2, 2), (2, 1, 1), (5, 0, 1), (2, 1, 1)

@@ -100,7 +100,7 @@ def test_raw_state_roundtrip_purity_and_folds(seed):
     clip = np.stack(frames, axis=2)
     ys, mask = a.forward_steps(to_cl(clip, torch.float32), pad_end=True)
     fold = [y for y in (c.forward_step(to_cl(x, torch.float32)) for x in frames) if y is not None]
-    fold += [y for y in (c.forward_step(None) for _ in range(d.padding[0])) if y is not None]
+    fold += [y for y in (c.forward_pad_step() for _ in range(d.padding[0])) if y is not None]
     assert ys.shape[2] == len(fold) == int(mask.sum())
     for i, f in enumerate(fold):
         assert torch.equal(ys[:, :, i], f)

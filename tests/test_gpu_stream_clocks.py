@@ -15,7 +15,7 @@ import torch
 import oracle as O
 from oracle import compose as OC
 from oracle import pool as OP
-from tests.helpers import np_of, rel_err, to_cl
+from tests.helpers import reset_opt, set_opt, np_of, rel_err, to_cl
 
 pytestmark = pytest.mark.gpu
 
@@ -61,7 +61,7 @@ CASES = {
 def _pool_case(kind, kernel, padding, vh, monkeypatch):
     def make(rng, B):
         import paper_2204_03418_b200 as co
-        monkeypatch.setenv("CO_POOL_VH", vh)
+        set_opt("pool_vh", vh)
         C, H, W = 16, 5, 6
         h = co.Pool(kind, C, kernel, padding=padding, in_spatial=(H, W), n_streams=B, out_dtype=torch.float32)
         return h, (lambda: OP.PoolStep(kind, C, (H, W), kernel, (1, 1, 1), padding, (1, 1, 1), B=1)), (C, H, W), None

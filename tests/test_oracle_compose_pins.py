@@ -135,11 +135,36 @@ def test_two_layer_body_step_equals_batch_with_relu():
     np.testing.assert_allclose(got, ref[:, :, :T - 3], rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("kt,p", [(5, 1), (7, 2), (7, 1), (3, 1)])
+def test_padded_centered_residual_is_cropped_equal_padding(kt, p):
+    """A centered residual whose body carries some padding p <= (f-1)/2 (ADVICE
+    r1): its outputs are the equal-padding residual's (P:313-315 weight
+    compatibility), column i being equal-padding column i + (f-1)/2 - p, and
+    step mode reproduces batch mode on the columns that need no end padding."""
+    rng = np.random.default_rng(kt * 10 + p)
+    B, T, C = 2, 11, 3
+    dp = _conv_desc(C, kt, p)
+    de = _conv_desc(C, kt, (kt - 1) // 2)
+    W = rng.standard_normal(dp.w_shape) / 6
+    b = rng.standard_normal(C) * 0.1
+    x = rng.standard_normal((B, C, T, 5, 4))
+    y = OC.residual_forward([dp], [W], [b], [0], x, shrink=True)
+    ye = OC.residual_forward([de], [W], [b], [0], x, shrink=False)
+    off = (kt - 1) // 2 - p
+    assert y.shape[2] == T + 2 * p - kt + 1
+    np.testing.assert_allclose(y, ye[:, :, off:off + y.shape[2]], rtol=1e-12, atol=1e-12)
+    res = OC.ResidualStep([dp], [W], [b], [0], [0], B, shrink=True)
+    got = np.stack(_run_steps(res, [x[:, :, t] for t in range(T)]), axis=2)
+    np.testing.assert_allclose(got, y[:, :, :got.shape[2]], rtol=1e-12, atol=1e-12)
+
+
 def test_construction_errors():
     with pytest.raises(ValueError):      # even receptive field cannot be centered
         OC.skip_delay([_conv_desc(2, 2, 0)], shrink=True)
     with pytest.raises(ValueError):      # no equal padding without shrink
         OC.skip_delay([_conv_desc(2, 3, 0)], shrink=False)
+    with pytest.raises(ValueError):      # centered: padding beyond (f-1)/2
+        OC.skip_delay([_conv_desc(2, 5, 3)], shrink=True)
 
 
 def test_broadcast_reduce_conv_delay_equals_residual():
