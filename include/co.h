@@ -78,7 +78,12 @@ typedef enum {
  * RAW: a ring of the last f input frames in the input dtype (SPEC's layout,
  * S:227); a Ready step contracts the whole window (K = kt kh kw Cin/g),
  * a non-Ready step only stores its frame.  Same outputs (Definition 1). */
-typedef enum { CO_STATE_PSUM = 0, CO_STATE_RAW = 1 } co_state_layout;
+typedef enum { CO_STATE_PSUM = 0, CO_STATE_RAW = 1, CO_STATE_AUTO = 2 } co_state_layout;
+/* AUTO: the planner picks per layer -- RAW for bf16 dense layers with a 1x1
+ * spatial kernel (the flat tensor-core RAW kernel) when the RAW ring moves at
+ * most half the bytes of the fp32 partial sums per step (kt+1 frames vs
+ * 2 (kt-1) fp32 output slots), PSUM otherwise; co_conv_info reports the
+ * choice.  Use PSUM where a workload mandates fp32 state. */
 
 /* Operation of a handle ("Pooling:
  * co.AvgPool1d, co.MaxPool1d, etc.").  A pooling handle has
@@ -241,6 +246,40 @@ int co_stack_steps_host(co_stack* st, const void* x_host, int64_t T, void* y_hos
 /* Accumulated delay d_NN (Principle 6 in the worked-example reading, A3). */
 int co_stack_delay(const co_stack* st, int64_t* d_nn);
 int co_stack_clean(co_stack* st, co_stream stream);
+
+/* ---- CUDA-graph step loops ---------------------------------------------------- */
+
+/* A stack's tick schedule is a function of the host clocks alone (readiness
+ * n >= d and (n-d) mod s == 0; ring slots from n, the a1/a5
+ * rows), so a run of ticks can be captured once into a CUDA graph and
+ * replayed with one launch -- no per-tick host work or launch latency, which
+ * is what small stream shards are bound by.
+ * co_stack_graph_create records the next n_ticks ticks of `st` (update_state =
+ * 1) from the current clocks, tick t reading the device frame x[t] (host array
+ * of n_ticks device pointers, layer 0's input layout) and writing the last
+ * layer's Ready output to y[t] (device pointers, may repeat); nothing executes
+ * and no clock moves.  co_graph_launch enqueues the recorded ticks on `stream`
+ * and advances every layer's clock by n_ticks (*n_ready, host, = the ticks on
+ * which the stack was Ready).  It refuses with CO_ERR_ARG unless every layer's
+ * clock is where the recorded schedule starts: the same n, or, once all
+ * transients are past (n >= f + p + d + 2s), the same phase modulo a period of
+ * every clock-derived kernel argument -- so in steady state a graph of any
+ * multiple of that period replays indefinitely, and outputs equal the eager
+ * fold of co_stack_step bit for bit.  Also CO_ERR_ARG if a layer's internal
+ * staging moved since capture, CO_ERR_UNSUPPORTED while a per-stream clean
+ * (co_stack_clean_streams) is still pending.  The graph keeps pointers to the
+ * stack, its layers and x / y: they must outlive it.  Programmatic dependent
+ * launch edges are captured when the driver instantiates them (co_graph_info
+ * reports pdl = 1), else the graph uses plain launches. */
+typedef struct co_graph co_graph;
+int co_stack_graph_create(co_stack* st, int64_t n_ticks, const void* const* x, void* const* y, co_graph** out);
+int co_graph_upload(co_graph* g, co_stream stream);      /* optional: pre-upload before the first launch */
+/* The stack's schedule period in ticks: in steady state a graph of any
+ * multiple of it returns every layer to its captured phase (replays forever). */
+int co_stack_graph_period(const co_stack* st, int64_t* period);
+int co_graph_launch(co_graph* g, int64_t* n_ready, co_stream stream);
+int co_graph_info(const co_graph* g, int64_t* n_ticks, int* pdl);
+int co_graph_destroy(co_graph* g);
 
 /* ---- composition: BroadcastReduce ------------------------ */
 

@@ -23,7 +23,7 @@ import torch
 from . import _abi
 from ._abi import CoConvDesc, CoInfo, CoMhaDesc, check, lib
 
-__all__ = ["BroadcastReduce", "Conv", "Delay", "MultiheadAttention", "Pool", "Residual", "Stack", "channels_last",
+__all__ = ["BroadcastReduce", "Conv", "Delay", "Graph", "MultiheadAttention", "Pool", "Residual", "Stack", "channels_last",
            "get_option", "is_channels_last", "load", "options", "set_option"]
 
 _DT = {torch.float32: _abi.CO_F32, torch.bfloat16: _abi.CO_BF16}
@@ -95,6 +95,14 @@ def _empty_cl(shape: Sequence[int], dtype, device) -> torch.Tensor:
     return torch.empty(phys, dtype=dtype, device=device).movedim(-1, 1)
 
 
+def _device(device) -> torch.device:
+    """torch.device with an explicit CUDA index (the current device for "cuda")."""
+    d = torch.device(device)
+    if d.type == "cuda" and d.index is None:
+        d = torch.device("cuda", torch.cuda.current_device())
+    return d
+
+
 def _stream(stream) -> C.c_void_p:
     s = torch.cuda.current_stream() if stream is None else stream
     return C.c_void_p(s.cuda_stream)
@@ -142,7 +150,7 @@ class Conv:
                  dtype: torch.dtype = torch.bfloat16, out_dtype: Optional[torch.dtype] = None,
                  activation: Optional[str] = None, kernel: str = "auto", state_layout: str = "psum",
                  device="cuda", op: str = "conv"):
-        self.device = torch.device(device)
+        self.device = _device(device)
         self.dtype, self.out_dtype = dtype, (out_dtype or dtype)
         self.spatial_rank, self.n_streams = spatial_rank, n_streams
         self.in_channels, self.out_channels = in_channels, out_channels
@@ -162,7 +170,6 @@ class Conv:
         d.state_layout = _abi.STATE_LAYOUTS[state_layout]
         d.op = _abi.OPS[op]
         self.op = op
-        self.state_layout = state_layout if op == "conv" else "raw"
         self._desc = d
         h = C.c_void_p()
         with torch.cuda.device(self.device):
@@ -179,6 +186,8 @@ class Conv:
                 check(lib().co_conv_create(C.byref(d), None, None, 0, C.byref(h)))
         self._h = h
         info = self.info()
+        # the layout the handle keeps ("auto" resolved by the planner; pooling / delay keep frame rings)
+        self.state_layout = "raw" if info.state_layout == _abi.CO_STATE_RAW else "psum"
         self.out_spatial: Tuple[int, ...] = tuple(info.out_spatial[:spatial_rank])
         self.in_spatial: Tuple[int, ...] = tuple(ins[:spatial_rank])
 
@@ -208,6 +217,10 @@ class Conv:
     @property
     def kernel_name(self) -> str:
         return lib().co_kernel_name(self._h).decode()
+
+    @property
+    def state_layout_used(self) -> str:
+        return self.state_layout
 
     @property
     def kernel_used(self) -> str:
@@ -576,7 +589,7 @@ class MultiheadAttention:
                  out_proj_bias: Optional[torch.Tensor] = None, n_streams: int = 1,
                  out_dtype: torch.dtype = torch.bfloat16, device="cuda"):
         self.E, self.heads, self.window, self.n_streams = embed_dim, num_heads, window, n_streams
-        self.out_dtype, self.device = out_dtype, torch.device(device)
+        self.out_dtype, self.device = out_dtype, _device(device)
         d = CoMhaDesc()
         d.embed_dim, d.num_heads, d.window, d.n_streams = embed_dim, num_heads, window, n_streams
         d.out_dtype = _DT[out_dtype]
@@ -711,6 +724,33 @@ class Stack:
     def clean_state(self, stream=None):
         check(lib().co_stack_clean(self._h, _stream(stream)))
 
+    @property
+    def graph_period(self) -> int:
+        """co_stack_graph_period: a steady-state graph of a multiple of this many
+        ticks replays indefinitely."""
+        p = C.c_int64()
+        check(lib().co_stack_graph_period(self._h, C.byref(p)))
+        return p.value
+
+    def capture(self, xs: Sequence[torch.Tensor], ys: Sequence[torch.Tensor]) -> "Graph":
+        """co_stack_graph_create: record the next len(xs) ticks (frame xs[t] in,
+        the Ready output to ys[t]) as one CUDA graph; clocks do not move until
+        Graph.launch() replays them."""
+        if len(xs) != len(ys) or not xs:
+            raise ValueError("need one output buffer per frame")
+        last = self.layers[-1]
+        shape = (last.n_streams, last.out_channels) + last.out_spatial
+        for x in xs:
+            self.layers[0]._check_in(x, clip=False)
+        for y in ys:
+            last._check_out(y, shape, last.out_dtype)
+        n = len(xs)
+        xa = (C.c_void_p * n)(*[x.data_ptr() for x in xs])
+        ya = (C.c_void_p * n)(*[y.data_ptr() for y in ys])
+        h = C.c_void_p()
+        check(lib().co_stack_graph_create(self._h, n, xa, ya, C.byref(h)))
+        return Graph(h, self, list(xs), list(ys))
+
     def clean_streams(self, streams, stream=None):
         """Restart the given streams (indices or bool mask): layer 0 now, each
         later layer when the stream's first valid input reaches it."""
@@ -723,3 +763,40 @@ class Stack:
         m = (C.c_uint8 * B)()
         check(lib().co_stack_stream_ready(self._h, m))
         return torch.tensor(list(m), dtype=torch.bool)
+
+
+class Graph:
+    """A captured run of stack ticks (co_graph): ``launch()`` replays them as
+    the stack's next ticks and returns how many were Ready."""
+
+    def __init__(self, h, stack: "Stack", xs, ys):
+        self._h, self.stack, self._keep = h, stack, (xs, ys)   # the graph holds these pointers
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().co_graph_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def n_ticks(self) -> int:
+        n, p = C.c_int64(), C.c_int()
+        check(lib().co_graph_info(self._h, C.byref(n), C.byref(p)))
+        return n.value
+
+    @property
+    def pdl(self) -> bool:
+        n, p = C.c_int64(), C.c_int()
+        check(lib().co_graph_info(self._h, C.byref(n), C.byref(p)))
+        return bool(p.value)
+
+    def upload(self, stream=None):
+        check(lib().co_graph_upload(self._h, _stream(stream)))
+
+    def launch(self, stream=None) -> int:
+        nr = C.c_int64()
+        check(lib().co_graph_launch(self._h, C.byref(nr), _stream(stream)))
+        return nr.value

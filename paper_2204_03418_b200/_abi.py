@@ -17,8 +17,8 @@ if os.environ.get("CO_LIB_VARIANT"):            # experiment builds only (build.
 CO_OK, CO_ERR_ARG, CO_ERR_SHAPE, CO_ERR_LENGTH, CO_ERR_UNSUPPORTED, CO_ERR_CUDA, CO_ERR_OOM = 0, -1, -2, -3, -4, -5, -6
 CO_F32, CO_BF16 = 0, 1
 CO_ACT_NONE, CO_ACT_RELU = 0, 1
-CO_STATE_PSUM, CO_STATE_RAW = 0, 1
-STATE_LAYOUTS = {"psum": CO_STATE_PSUM, "raw": CO_STATE_RAW}
+CO_STATE_PSUM, CO_STATE_RAW, CO_STATE_AUTO = 0, 1, 2
+STATE_LAYOUTS = {"psum": CO_STATE_PSUM, "raw": CO_STATE_RAW, "auto": CO_STATE_AUTO}
 CO_KERNEL_AUTO, CO_KERNEL_DIRECT, CO_KERNEL_DENSE_TC, CO_KERNEL_DEPTHWISE, CO_KERNEL_POOL, CO_KERNEL_COPY = range(6)
 KERNELS = {"auto": CO_KERNEL_AUTO, "direct": CO_KERNEL_DIRECT, "dense_tc": CO_KERNEL_DENSE_TC,
            "depthwise": CO_KERNEL_DEPTHWISE, "pool": CO_KERNEL_POOL, "copy": CO_KERNEL_COPY}
@@ -38,7 +38,8 @@ EXPORTS = ["co_conv_create", "co_conv_destroy", "co_conv_info", "co_delay", "co_
            "co_stack_stream_ready", "co_parallel_create", "co_parallel_destroy", "co_parallel_step",
            "co_parallel_forward", "co_parallel_clean", "co_parallel_delay", "co_parallel_out_channels", "co_mha_create", "co_mha_destroy", "co_mha_step", "co_mha_forward", "co_mha_clean",
            "co_mha_delay", "co_mha_state_bytes", "co_mha_state_get", "co_mha_state_set", "co_residual_create", "co_residual_destroy", "co_residual_step", "co_residual_forward",
-           "co_residual_clean", "co_residual_delay", "co_set_option", "co_get_option", "co_option_name",
+           "co_residual_clean", "co_residual_delay", "co_stack_graph_create", "co_stack_graph_period", "co_graph_upload", "co_graph_launch",
+           "co_graph_info", "co_graph_destroy", "co_set_option", "co_get_option", "co_option_name",
            "co_last_error", "co_abi_version"]
 
 
@@ -131,6 +132,12 @@ def lib():
             L.co_residual_forward.argtypes = [vp, vp, C.c_int64, vp, i64p, vp]
             L.co_residual_clean.argtypes = [vp, vp]
             L.co_residual_delay.argtypes = [vp, i64p, i64p]
+            L.co_stack_graph_create.argtypes = [vp, C.c_int64, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]
+            L.co_graph_upload.argtypes = [vp, vp]
+            L.co_stack_graph_period.argtypes = [vp, i64p]
+            L.co_graph_launch.argtypes = [vp, i64p, vp]
+            L.co_graph_info.argtypes = [vp, i64p, C.POINTER(C.c_int)]
+            L.co_graph_destroy.argtypes = [vp]
             L.co_set_option.argtypes = [C.c_char_p, C.c_int64]
             L.co_get_option.argtypes = [C.c_char_p, i64p]
             L.co_option_name.argtypes = [C.c_int]

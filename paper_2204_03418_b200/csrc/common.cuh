@@ -18,6 +18,7 @@ enum Opt : int {
   OPT_CHUNK_T, OPT_POOL_BAND, OPT_POOL_VH, OPT_POOL_G, OPT_LOG, OPT_COUNT
 };
 int64_t option(Opt o);
+void set_thread_no_pdl(int v);   // graph capture fallback: plain launches on this thread
 
 // A/B experiment knobs: read from the environment only in -DCO_EXPERIMENTS
 // builds; the release library compiles them to their defaults (no getenv, no

@@ -177,7 +177,8 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
     if (t != CO_F32 && t != CO_BF16) return fail(CO_ERR_ARG, "dtype must be CO_F32 or CO_BF16");
   if (d->w_dtype != d->in_dtype) return fail(CO_ERR_ARG, "w_dtype must equal in_dtype");
   if (d->activation != CO_ACT_NONE && d->activation != CO_ACT_RELU) return fail(CO_ERR_ARG, "bad activation");
-  if (d->state_layout != CO_STATE_PSUM && d->state_layout != CO_STATE_RAW) return fail(CO_ERR_ARG, "bad state_layout");
+  if (d->state_layout != CO_STATE_PSUM && d->state_layout != CO_STATE_RAW && d->state_layout != CO_STATE_AUTO)
+    return fail(CO_ERR_ARG, "bad state_layout");
   if (d->op != CO_OP_CONV && d->op != CO_OP_MAX_POOL && d->op != CO_OP_AVG_POOL && d->op != CO_OP_DELAY)
     return fail(CO_ERR_ARG, "bad op");
   const bool pool = d->op != CO_OP_CONV;
@@ -208,6 +209,19 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
   g.slot_elems = int64_t(g.Cq) * 4 * g.splane;
   g.op = d->op;
   g.raw = pool || d->state_layout == CO_STATE_RAW;   // pooling / delay always keep a frame ring
+  if (!pool && d->state_layout == CO_STATE_AUTO) {
+    // The planner's choice, by the bytes each layout moves per
+    // stream-step -- RAW: the frame store + the window's kt frames; PSUM: the
+    // 2 (kt-1) fp32 partial-sum accesses -- where the RAW tensor-core kernel is
+    // the 1x1 (FLAT) one, which reaches its roofline (C5: 2.2x the PSUM
+    // layout's throughput measured); spatial RAW windows stay PSUM (their K
+    // pipeline is shared-memory bound at small N).
+    const double raw_b = double(g.kt + 1) * double(g.H) * g.W * g.Cin * 2;
+    const double psum_b = 2.0 * (g.kt - 1) * double(g.HWo) * g.Cout * 4;
+    const bool flat = g.kh == 1 && g.kw == 1 && g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0;
+    g.raw = d->in_dtype == CO_BF16 && d->groups == 1 && flat && g.kt > 1 && 2.0 * raw_b <= psum_b &&
+            g.Cin % 16 == 0 && g.Cout % 16 == 0;
+  }
   if (g.op == CO_OP_DELAY) {
     if (g.kh != 1 || g.kw != 1 || g.sh != 1 || g.sw != 1 || g.ph || g.pw || g.dh != 1 || g.dw != 1 || g.pt ||
         g.st != 1 || g.dt != 1)
@@ -1648,5 +1662,179 @@ extern "C" int co_parallel_delay(const co_parallel* p, int64_t* delay) {
 extern "C" int co_parallel_out_channels(const co_parallel* p, int32_t* channels) {
   if (!p || !channels) return fail(CO_ERR_ARG, "null argument");
   *channels = int32_t(p->Ctot);
+  return CO_OK;
+}
+
+// ----------------------------------------------------------------- CUDA-graph step loops
+
+// A stack's tick sequence depends only on the host clocks (a1: readiness, ring
+// slots and the clock-derived kernel arguments are integer functions of each
+// layer's n), so n_ticks consecutive ticks can be captured
+// once and replayed: the replay is valid whenever every layer's clock is where
+// the captured schedule starts -- the same n, or, once past the transients,
+// the same phase modulo a period of all those functions.
+struct co_graph {
+  co_stack* st = nullptr;
+  int64_t n_ticks = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<int64_t> n_cap, gen_cap, period, steady;
+  int pdl = 1;
+};
+
+static int64_t gcd64(int64_t a, int64_t b) { while (b) { const int64_t t = a % b; a = b; b = t; } return a; }
+static int64_t lcm64(int64_t a, int64_t b) { return a / gcd64(a, b) * b; }
+
+// A period (in the layer's own steps) of every clock-derived argument of its
+// step launches: partial-sum ring slots floor((m - k dil)/s) mod R and the
+// stride phase (n - d) mod s repeat every s R steps; the RAW / Delay frame
+// rings every f (slot m mod f); pooling adds the block decomposition's
+// (m div dil) mod kt.
+static int64_t clock_period(const Geom& g) {
+  const int64_t s = std::max(1, g.st), f = std::max(1, g.f);
+  if (g.op == CO_OP_DELAY) return f;
+  if (g.op != CO_OP_CONV) return lcm64(lcm64(f, s), int64_t(std::max(1, g.dt)) * std::max(1, g.kt));
+  if (g.raw) return lcm64(f, s);
+  return s * std::max(1, g.R);
+}
+// From this clock on the schedule is periodic (no output index < 0, past the delay).
+static int64_t clock_steady(const Geom& g) { return int64_t(g.f) + g.pt + g.delay + 2 * g.st; }
+
+static int64_t layer_gen(const co_conv* h) { return h->tc ? co::dense_tc_buffer_gen(h->tc) : 0; }
+
+// Advance the host side of one stack tick without launching anything: the
+// clocks and last-step readiness exactly as co_stack_step leaves them.
+static int dry_tick(co_stack* st) {
+  st->last_ready = 0;
+  for (co_conv* h : st->layers) {
+    const Geom& g = h->g;
+    const int r = (g.op == CO_OP_DELAY) ? (h->n >= g.delay)
+                                         : ((h->n >= g.delay) && floor_mod(h->n - g.delay, g.st) == 0);
+    h->last_n = h->n;
+    h->last_ready = r;
+    ++h->n;
+    if (!r) return 0;
+  }
+  st->last_ready = 1;
+  return 1;
+}
+
+extern "C" int co_stack_graph_create(co_stack* st, int64_t n_ticks, const void* const* x, void* const* y,
+                                     co_graph** out) {
+  if (!st || n_ticks < 1 || !x || !y || !out) return fail(CO_ERR_ARG, "bad argument");
+  *out = nullptr;
+  for (int64_t t = 0; t < n_ticks; ++t)
+    if (!x[t] || !y[t]) return fail(CO_ERR_ARG, "null frame / output pointer at tick %lld", (long long)t);
+  for (const auto& p : st->pending)
+    if (!p.empty()) return fail(CO_ERR_UNSUPPORTED, "a per-stream clean is pending: step eagerly until it lands");
+  const size_t L = st->layers.size();
+  std::vector<int64_t> n0(L), ln(L);
+  std::vector<int> lr(L);
+  for (size_t l = 0; l < L; ++l) { n0[l] = st->layers[l]->n; ln[l] = st->layers[l]->last_n; lr[l] = st->layers[l]->last_ready; }
+  const int sr = st->last_ready;
+  auto restore = [&]() {
+    for (size_t l = 0; l < L; ++l) { st->layers[l]->n = n0[l]; st->layers[l]->last_n = ln[l]; st->layers[l]->last_ready = lr[l]; }
+    st->last_ready = sr;
+  };
+  cudaStream_t cs = nullptr;
+  CO_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  co_graph* G = new (std::nothrow) co_graph();
+  if (!G) { cudaStreamDestroy(cs); return fail(CO_ERR_OOM, "host allocation"); }
+  int rc = CO_OK;
+  // first with programmatic dependent launch (captured as programmatic edges),
+  // then, if this driver cannot instantiate those, with plain launches
+  for (int pdl = 1; pdl >= 0; --pdl) {
+    co::set_thread_no_pdl(pdl ? 0 : 1);
+    rc = CO_OK;
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) { rc = fail(CO_ERR_CUDA, "begin capture: %s", cudaGetErrorString(e)); break; }
+    for (int64_t t = 0; t < n_ticks && !rc; ++t) {
+      int r = 0;
+      rc = co_stack_step(st, x[t], y[t], 1, &r, cs);
+    }
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(cs, &graph);
+    restore();
+    if (rc) { if (graph) cudaGraphDestroy(graph); break; }
+    if (e != cudaSuccess) { cudaGetLastError(); rc = fail(CO_ERR_CUDA, "end capture: %s", cudaGetErrorString(e)); continue; }
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      cudaGraphDestroy(graph);
+      rc = fail(CO_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+      continue;
+    }
+    G->graph = graph; G->exec = exec; G->pdl = pdl;
+    break;
+  }
+  co::set_thread_no_pdl(0);
+  cudaStreamDestroy(cs);
+  if (rc || !G->exec) { delete G; return rc ? rc : fail(CO_ERR_CUDA, "graph capture failed"); }
+  G->st = st;
+  G->n_ticks = n_ticks;
+  for (co_conv* h : st->layers) {
+    G->n_cap.push_back(h->n);
+    G->gen_cap.push_back(layer_gen(h));
+    G->period.push_back(clock_period(h->g));
+    G->steady.push_back(clock_steady(h->g));
+  }
+  *out = G;
+  return CO_OK;
+}
+
+extern "C" int co_stack_graph_period(const co_stack* st, int64_t* period) {
+  if (!st || !period) return fail(CO_ERR_ARG, "null argument");
+  // layer l steps once per s_acc(l) ticks (the product of the strides below it)
+  int64_t P = 1, s_acc = 1;
+  for (const co_conv* h : st->layers) {
+    P = lcm64(P, clock_period(h->g) * s_acc);
+    s_acc *= std::max(1, h->g.st);
+  }
+  *period = P;
+  return CO_OK;
+}
+
+extern "C" int co_graph_upload(co_graph* G, co_stream stream) {
+  if (!G) return fail(CO_ERR_ARG, "null graph");
+  CO_CUDA(cudaGraphUpload(G->exec, (cudaStream_t)stream));
+  return CO_OK;
+}
+
+extern "C" int co_graph_launch(co_graph* G, int64_t* n_ready, co_stream stream) {
+  if (!G) return fail(CO_ERR_ARG, "null graph");
+  co_stack* st = G->st;
+  for (const auto& p : st->pending)
+    if (!p.empty()) return fail(CO_ERR_UNSUPPORTED, "a per-stream clean is pending");
+  for (size_t l = 0; l < st->layers.size(); ++l) {
+    const co_conv* h = st->layers[l];
+    if (layer_gen(h) != G->gen_cap[l])
+      return fail(CO_ERR_ARG, "layer %zu's staging buffers moved since capture: capture again", l);
+    const int64_t n = h->n, c = G->n_cap[l];
+    const bool same = n == c ||
+                      (n >= G->steady[l] && c >= G->steady[l] && floor_mod(n - c, G->period[l]) == 0);
+    if (!same)
+      return fail(CO_ERR_ARG, "layer %zu clock %lld is not at the captured phase (%lld mod %lld)", l, (long long)n,
+                  (long long)c, (long long)G->period[l]);
+  }
+  CO_CUDA(cudaGraphLaunch(G->exec, (cudaStream_t)stream));
+  int64_t nr = 0;
+  for (int64_t t = 0; t < G->n_ticks; ++t) nr += dry_tick(st);
+  if (n_ready) *n_ready = nr;
+  return CO_OK;
+}
+
+extern "C" int co_graph_destroy(co_graph* G) {
+  if (!G) return CO_OK;
+  if (G->exec) cudaGraphExecDestroy(G->exec);
+  if (G->graph) cudaGraphDestroy(G->graph);
+  delete G;
+  return CO_OK;
+}
+
+extern "C" int co_graph_info(const co_graph* G, int64_t* n_ticks, int* pdl) {
+  if (!G) return fail(CO_ERR_ARG, "null graph");
+  if (n_ticks) *n_ticks = G->n_ticks;
+  if (pdl) *pdl = G->pdl;
   return CO_OK;
 }

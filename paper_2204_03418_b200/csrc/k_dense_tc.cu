@@ -1255,6 +1255,7 @@ struct DenseTC {
   __nv_bfloat16* wpack = nullptr;
   __nv_bfloat16* xstage = nullptr;   // dense staging (strided clips in flat mode, zero frames, W-im2col)
   size_t xstage_bytes = 0;
+  int64_t gen = 0;                   // bumped whenever xstage moves (captured graphs hold its address)
   int num_sms = 148;
   std::string name;
 };
@@ -1334,12 +1335,14 @@ void dense_tc_destroy(DenseTC* t) {
 }
 
 const char* dense_tc_name(const DenseTC* t) { return t->name.c_str(); }
+int64_t dense_tc_buffer_gen(const DenseTC* t) { return t ? t->gen : 0; }
 
 static cudaError_t ensure_stage(DenseTC* t, size_t need) {
   if (t->xstage_bytes >= need) return cudaSuccess;
   cudaFree(t->xstage);
   t->xstage = nullptr;
   t->xstage_bytes = 0;
+  ++t->gen;
   cudaError_t e = cudaMalloc(&t->xstage, need);
   if (e == cudaSuccess) t->xstage_bytes = need;
   return e;

@@ -49,8 +49,14 @@ int find(const char* name) {
 
 }  // namespace
 
+// graph capture on this thread without programmatic dependent launch (the
+// fallback when a driver cannot instantiate captured PDL edges)
+thread_local int t_no_pdl = 0;
+void set_thread_no_pdl(int v) { t_no_pdl = v; }
+
 int64_t option(Opt o) {
   init_once();
+  if (o == OPT_PDL && t_no_pdl) return 0;
   return g_val[o].load(std::memory_order_relaxed);
 }
 

@@ -1,11 +1,19 @@
 """Multi-GPU plumbing for the continual-conv step.
 
 Streams are independent (one handle's streams share only the clock and the
-read-only weights), so the path partitions without any data exchange:
-rank r of a world of g processes owns the contiguous global streams
-[r*B, (r+1)*B) and runs its own handles on its own GPU.  There is no collective
-on the hot path; torch.distributed (NCCL on GPUs, gloo in the CPU tests) only
-carries the barrier before timing and the end-of-run counters:
+read-only weights, "the same global clock"), so the path partitions
+without any data exchange.  Strong scaling (the default, BASELINE.json configs
+"1024 streams sharded over 1/2/4/8 GPUs"): the config's global
+stream count B is fixed and rank r of g owns the contiguous global streams
+[floor(r B / g), floor((r+1) B / g)) -- shards differ by at most one stream
+when g does not divide B.  Weak scaling (an option): every rank runs B streams,
+rank r owning [r B, (r+1) B).  A config with fewer streams than ranks (C1's
+single stream) runs as independent replicas.  Each rank builds its own handles
+on its own GPU; weights are regenerated bitwise identically from the seed.
+
+There is no collective on the hot path; torch.distributed (NCCL on GPUs, gloo
+in the CPU tests) only carries the barrier before timing and the end-of-run
+counters:
 
 * SUM over ranks of [stream_steps, parity_fails]
 * MAX over ranks of [elapsed_ms, max_rel_err]
@@ -23,19 +31,14 @@ from typing import Tuple
 class Shard:
     rank: int
     world: int
-    per_rank: int          # streams per rank (weak scaling: fixed per GPU)
+    lo: int                # first global stream of this rank
+    hi: int                # one past the last
+    n_global: int          # streams of the whole job
+    scaling: str = "strong"
 
     @property
-    def lo(self) -> int:
-        return self.rank * self.per_rank
-
-    @property
-    def hi(self) -> int:
-        return (self.rank + 1) * self.per_rank
-
-    @property
-    def n_global(self) -> int:
-        return self.world * self.per_rank
+    def per_rank(self) -> int:
+        return self.hi - self.lo
 
 
 def env_rank_world() -> Tuple[int, int, int]:
@@ -44,10 +47,18 @@ def env_rank_world() -> Tuple[int, int, int]:
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def shard(rank: int, world: int, per_rank: int) -> Shard:
-    if world < 1 or not (0 <= rank < world) or per_rank < 1:
-        raise ValueError(f"bad shard rank={rank} world={world} per_rank={per_rank}")
-    return Shard(rank, world, per_rank)
+def shard(rank: int, world: int, n: int, scaling: str = "strong") -> Shard:
+    """This rank's streams.  strong: n global streams split into contiguous,
+    near-equal blocks (replicas of all n when n < world); weak: n per rank."""
+    if world < 1 or not (0 <= rank < world) or n < 1:
+        raise ValueError(f"bad shard rank={rank} world={world} n={n}")
+    if scaling == "weak":
+        return Shard(rank, world, rank * n, (rank + 1) * n, world * n, "weak")
+    if scaling != "strong":
+        raise ValueError(f"scaling must be 'strong' or 'weak', not {scaling!r}")
+    if n < world:                                  # e.g. C1's one stream: independent replicas
+        return Shard(rank, world, 0, n, n, "replicas")
+    return Shard(rank, world, rank * n // world, (rank + 1) * n // world, n, "strong")
 
 
 def _dist():
