@@ -425,6 +425,8 @@ int co_residual_delay(const co_residual* r, int64_t* delay, int64_t* skip_delay)
  *   "pool_vh"   -1 auto | 0 direct fold | 1 block decomposition (pooling)     [create]
  *   "pool_g"     0 auto | 1..32 lanes per pooled output vector                [create]
  *   "log"        0 (default) | 1 print each tensor-core plan to stderr        [create]
+ *   "stem"       1 (default) small-Cin stems build their W-im2col in shared
+ *                memory | 0 a separate HBM W-im2col pass per step            [create]
  * name == NULL resets every option to its default.
  * Errors: CO_ERR_ARG for an unknown name or a value out of range.  Not
  * thread-safe against concurrent creates (set options before building handles). */

@@ -76,7 +76,16 @@ constexpr int kMaxAStages = 4;  // KHALO: input-halo ring depth
 // (u, v) reads phase ((u-ph) mod s, (v-pw) mod s) at a whole-row shift, and
 // each phase halo is one TMA box with elementStrides = s, so a stride-2 layer
 // stages ~4 (MT+1) x (Wo+1) rows per channel block instead of 9 x 128.
-enum { MODE_HALO = 0, MODE_FLAT = 1, MODE_KLOOP = 2, MODE_KHALO = 3 };
+// STEM (small-Cin stems such as C4's RGB 5x7x7 s(1,2,2) layer): the W-im2col
+// is built in shared memory, not in HBM.  Per tile the producer bulk-copies the
+// few raw input rows it needs (Cin = 3 channels: 672-B rows), and one epilogue
+// warpgroup expands them -- overlapped with its own state loads -- into an
+// im2col image [K group][row][16 B] whose row (pixel wo of raw row q) holds the
+// window x[q, wo sw + v - pw, c] at K index v Cin + c.  Rows are stored by row
+// phase (q mod sh), so spatial tap u of a tile's TH output rows is ONE shifted
+// descriptor (phase u mod sh, first row u div sh), and both channel parts of the
+// tile run consecutively on the same image (weights streamed per tap).
+enum { MODE_HALO = 0, MODE_FLAT = 1, MODE_KLOOP = 2, MODE_KHALO = 3, MODE_STEM = 4 };
 
 struct TcParams {
   int B, H, W, Cin, Cout, Ho, Wo;
@@ -113,6 +122,17 @@ struct TcParams {
   int dbg;                        // CO_TC_DEBUG bits (experiments only): 1 no state/y traffic, 2 no MMA,
                                   // 4 no A loads, 8 no TMEM reads, 16 (with 2) no accumulator handshakes
   int Cq;
+  // MODE_STEM: raw rows -> shared-memory W-im2col image (see above)
+  const __nv_bfloat16* x;         // the step's frame (stream 0); nullptr = zero frame
+  int64_t x_bstride;              // elements between streams
+  int st_Hin, st_Win, st_cin;     // raw frame geometry
+  int st_sw, st_pw, st_kwc;       // horizontal stride / padding, real K of a tap (kw Cin)
+  int st_nraw;                    // raw rows per tile: (TH-1) sh + kh
+  int st_rpitch, st_pad;          // bytes per padded raw row in shared memory, zero elements before the data
+  int st_raw_off;                 // shared offset of the 2 raw-row buffers
+  int st_img_rows, st_img_bytes;  // rows / bytes of one image buffer (2 buffers at offset 0)
+  int st_groups, st_data_groups;  // 8-element K groups of the image, groups holding data
+  int st_phase_base[2];           // first image row of each row phase (sh <= 2)
   // chunked co_forward_steps (HALO / FLAT): T frames per item,
   // processed item-batch-major so a tile's state stays L2-resident between its
   // frames; ticks = T rows of kTickInts: [emit, output index, ring slot of tap k...]
@@ -165,7 +185,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 // at (kt-1) * CE / 4 float4 per thread); KH, KW, KC (= Cin / 16) > 0: compile-
 // time tap / K loops of the HALO / FLAT modes, fully unrolled, so the issuing
 // warp spends ~3 uniform instructions per tcgen05.mma.
-template <int KT, int CC, int EG, int CE, int KH = 0, int KW = 0, int KC = 0, int CS = 1, int PAIR = 1>
+template <int KT, int CC, int EG, int CE, int KH = 0, int KW = 0, int KC = 0, int CS = 1, int PAIR = 1,
+          bool STM = false>
 __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     k_step_dense_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap wmap,
                     const TcParams p) {
@@ -230,13 +251,37 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     ptx::mbar_init(w_full, 1);
     ptx::mbar_init(w_peer, 1);
     for (int s = 0; s < kMaxAStages; ++s) { ptx::mbar_init(&a_full[s], 1); ptx::mbar_init(&a_empty[s], 1); }
+    if (p.mode == MODE_STEM) {
+      // images: full when the converting group's 128 CS threads arrived, empty on the
+      // MMA's commit; raw rows: full on the bulk copies' bytes, empty when converted
+      for (int b = 0; b < 2; ++b) { ptx::mbar_init(&a_full[b], 128 * CS); ptx::mbar_init(&a_empty[2 + b], 128 * CS); }
+    }
     ptx::fence_mbar_init();
   }
   if (warp == kMma) {
     if constexpr (PAIR == 2) ptx::tmem_alloc_pair(tmem_holder, TMEM_COLS);
     else ptx::tmem_alloc(tmem_holder, TMEM_COLS);
   }
-  for (int i = threadIdx.x; i < CC; i += blockDim.x) bias_s[i] = p.bias[c0 + i];
+  // MODE_STEM only in the STM instantiations (the shared-memory W-im2col code
+  // stays out of every other variant's registers)
+  constexpr bool kStem = STM && PAIR == 1 && CS == 1;
+  const bool stem = kStem && (p.mode == MODE_STEM);
+  // STEM CTAs serve every channel part (all Cout biases); other modes one part
+  if (stem) {
+    for (int i = threadIdx.x; i < p.Cout; i += blockDim.x) bias_s[i] = p.bias[i];
+    // zero the image K groups that never hold data and the raw rows' padding, once
+    // (the converter writes only data groups, the bulk copies only row interiors)
+    for (int b = 0; b < 2; ++b)
+      for (int gq = p.st_data_groups; gq < p.st_groups; ++gq) {
+        uint4* z = reinterpret_cast<uint4*>(smem + b * p.st_img_bytes + gq * p.st_img_rows * 16);
+        for (int i = threadIdx.x; i < p.st_img_rows; i += blockDim.x) z[i] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    uint4* zr = reinterpret_cast<uint4*>(smem + p.st_raw_off);
+    for (int i = threadIdx.x; i < 2 * p.st_nraw * p.st_rpitch / 16; i += blockDim.x) zr[i] = make_uint4(0u, 0u, 0u, 0u);
+    ptx::fence_proxy_async();                           // generic zeros, read by the tensor cores
+  } else {
+    for (int i = threadIdx.x; i < CC; i += blockDim.x) bias_s[i] = p.bias[c0 + i];
+  }
   ptx::tc_fence_before();
   if (CLU > 1) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
@@ -252,7 +297,41 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
           reinterpret_cast<const uint8_t*>(p.wpack) + size_t(part * PAIR + (PAIR == 2 ? rank : 0u)) * p.w_bytes;
       int s = 0;
       uint32_t ph = 0;
-      if (khalo) {
+      if (stem) {
+        if (p.pdl) pdl_wait();
+        const int rowbytes = p.st_Win * p.st_cin * 2;
+        // raw rows of CTA-local tile T into raw buffer T & 1 (one tile ahead of the weights)
+        auto load_raw = [&](int64_t T) {
+          const int64_t tile = int64_t(blockIdx.x) + T * grid;
+          if (tile >= p.n_tiles) return;
+          const int rb = int(T & 1);
+          ptx::mbar_wait(&a_empty[2 + rb], (uint32_t(T >> 1) & 1u) ^ 1u);
+          const int bs = int(tile / p.tiles_h);
+          const int r0 = int(tile % p.tiles_h) * p.TH * p.sh - p.ph;
+          int nv = 0;
+          for (int q = 0; q < p.st_nraw; ++q) nv += (p.x && r0 + q >= 0 && r0 + q < p.st_Hin) ? 1 : 0;
+          if (!nv) { ptx::mbar_arrive(&a_full[2 + rb]); return; }
+          ptx::mbar_arrive_expect_tx(&a_full[2 + rb], uint32_t(nv * rowbytes));
+          uint8_t* dst = smem + p.st_raw_off + rb * p.st_nraw * p.st_rpitch + p.st_pad * 2;
+          const __nv_bfloat16* src = p.x + int64_t(bs) * p.x_bstride;
+          for (int q = 0; q < p.st_nraw; ++q)
+            if (r0 + q >= 0 && r0 + q < p.st_Hin)
+              ptx::bulk_g2s(dst + q * p.st_rpitch, src + int64_t(r0 + q) * p.st_Win * p.st_cin, rowbytes, &a_full[2 + rb]);
+        };
+        load_raw(0);
+        for (int64_t T = 0; int64_t(blockIdx.x) + T * grid < p.n_tiles; ++T) {
+          load_raw(T + 1);
+          for (int pt = 0; pt < p.n_split; ++pt) {
+            const uint8_t* bsrc = reinterpret_cast<const uint8_t*>(p.wpack) + size_t(pt) * p.w_bytes;
+            for (int u = 0; u < p.kh; ++u) {
+              ptx::mbar_wait(&empty[s], ph ^ 1);
+              ptx::mbar_arrive_expect_tx(&full[s], p.b_bytes);
+              ptx::bulk_g2s(a_s + s * p.a_stride, bsrc + size_t(u) * p.b_bytes, p.b_bytes, &full[s]);
+              if (++s == p.stages) { s = 0; ph ^= 1; }
+            }
+          }
+        }
+      } else if (khalo) {
         if (p.pdl) pdl_wait();
         int as = 0;
         uint32_t aph = 0;
@@ -419,6 +498,44 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     };
     if (PAIR == 2 && !leader) {
       // the peer's tensor-core work is issued by the leader
+    } else if (stem) {
+      const uint32_t lbo = uint32_t(p.st_img_rows) * 16u;       // bytes between the image's K groups
+      const int nk = p.kb / 16;                                  // MMAs (K = 16) per tap
+      int64_t li = 0;
+      for (int64_t T = 0; int64_t(blockIdx.x) + T * grid < p.n_tiles; ++T) {
+        const int b = int(T & 1);
+        ptx::mbar_wait(&a_full[b], uint32_t(T >> 1) & 1u);      // the tile's image was built
+        ptx::tc_fence_after();
+        const uint64_t a0 = ptx::smem_desc(ptx::smem_u32(smem + b * p.st_img_bytes), lbo, 128);
+        for (int pt = 0; pt < p.n_split; ++pt, ++li) {
+          ptx::mbar_wait(&acc_empty[e], eph ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t d_tmem = tmem + uint32_t(e * BUF);
+          for (int u = 0; u < p.kh; ++u) {
+            ptx::mbar_wait(&full[s], ph);
+            ptx::tc_fence_after();
+            const uint64_t bd = ptx::smem_desc(a_base + uint32_t(s * p.a_stride), NB * 16, 128);
+            // tap u: phase u mod sh, first row u div sh (16-B units per row)
+            const uint64_t ad = a0 + uint64_t(p.st_phase_base[u % p.sh] + (u / p.sh) * p.Wo);
+            if (ptx::elect_one()) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                if (j < nk) mma(d_tmem, ad + uint64_t(j) * (2u * lbo >> 4), bd + uint64_t(j) * uint64_t(2 * NB),
+                                (u | j) ? 1u : 0u);
+              commit(&empty[s]);
+            }
+            __syncwarp();
+            if (++s == p.stages) { s = 0; ph ^= 1; }
+          }
+          if (ptx::elect_one()) {
+            commit(&acc_full[e]);
+            if (pt == p.n_split - 1) commit(&a_empty[b]);          // image free after the tile's last part
+          }
+          __syncwarp();
+          if (++e == NBUF) { e = 0; eph ^= 1; }
+        }
+      }
+      (void)li;
     } else if (khalo) {
       const int taps = p.kh * p.kw;
       const uint32_t ka_base = ptx::smem_u32(smem);
@@ -581,13 +698,66 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   // One work (an item at one tick) of this group: buf / bph pick the accumulator,
   // tk the chunk's tick row (nullptr: the launch's single tick from p).  Called
   // from two loops so the one-step path keeps its own (lower) register use.
-  auto work = [&](const int64_t item, const int64_t li, const int* tk) {
+  // STEM: build CTA-local tile T's W-im2col image from its raw rows (this
+  // group's 128 CS threads), then release the raw buffer and publish the image
+  const int gtid = threadIdx.x - e * 128 * CS;          // thread index inside the group
+  auto convert = [&](int64_t T) {
+    if constexpr (!kStem) return;
+    const int64_t tile = int64_t(blockIdx.x) + T * grid;
+    if (tile >= p.n_tiles) return;
+    const int b = int(T & 1);
+    const uint32_t tph = uint32_t(T >> 1) & 1u;
+    ptx::mbar_wait(&a_empty[b], tph ^ 1u);               // the MMA is done with tile T-2's image
+    ptx::mbar_wait(&a_full[2 + b], tph);                 // tile T's raw rows landed
+    const int r0 = int(tile % p.tiles_h) * p.TH * p.sh - p.ph;
+    uint8_t* img = smem + b * p.st_img_bytes;
+    const uint8_t* raw = smem + p.st_raw_off + b * p.st_nraw * p.st_rpitch;
+    const int Wo = p.Wo, nt = p.st_nraw * Wo, gstride = p.st_img_rows * 16;
+    for (int task = gtid; task < nt; task += 128 * CS) {
+      const int q = task / Wo, wo = task - q * Wo;
+      const int row = p.st_phase_base[q % p.sh] + (q / p.sh) * Wo + wo;
+      uint32_t w[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) w[k] = 0u;
+      if (p.x && r0 + q >= 0 && r0 + q < p.st_Hin) {
+        // the window x[q, wo sw - pw + v, c] = padded-row elements e0 .. e0 + kwc - 1
+        const int e0 = p.st_pad + (wo * p.st_sw - p.st_pw) * p.st_cin;
+        const uint32_t* rw = reinterpret_cast<const uint32_t*>(raw + q * p.st_rpitch) + (e0 >> 1);
+        const int nw = p.st_data_groups * 4;             // 32-bit words of the data groups
+        if (e0 & 1) {                                    // window starts mid-word: funnel pairs
+          uint32_t prev = rw[0];
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (k < nw) { const uint32_t nx = rw[k + 1]; w[k] = __byte_perm(prev, nx, 0x5432); prev = nx; }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (k < nw) w[k] = rw[k];
+        }
+        // K index >= kw Cin: zero (the packed weights are zero there too)
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          if (2 * k >= p.st_kwc) w[k] = 0u;
+          else if (2 * k + 1 >= p.st_kwc) w[k] &= 0xFFFFu;
+        }
+      }
+#pragma unroll
+      for (int gq = 0; gq < 4; ++gq)
+        if (gq < p.st_data_groups)
+          *reinterpret_cast<uint4*>(img + gq * gstride + row * 16) =
+              make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
+    }
+    ptx::fence_proxy_async();                             // generic image writes -> tensor-core reads
+    ptx::mbar_arrive(&a_empty[2 + b]);                    // raw rows consumed
+    ptx::mbar_arrive(&a_full[b]);                         // image ready
+  };
+  auto work = [&](const int64_t tile, const int c0v, const int64_t li, const int* tk) {
     const int buf = int(li % NBUF);                    // accumulator buffer of this work
     const uint32_t bph = uint32_t(li / NBUF) & 1u;
     const int emit = tk ? tk[0] : p.emit;
     const int64_t yt = tk ? int64_t(tk[1]) * p.y_tstride : 0;
     auto slot = [&](int k) -> int { return tk ? tk[2 + k] : p.slot[k]; };
-    const int64_t tile = tile_of(item);
+    const int bias0 = stem ? c0v : 0;                  // bias_s holds all Cout (STEM) or this part's CC
     // ---- this row's output pixel
     bool valid;
     int64_t pix, b;
@@ -626,7 +796,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       if (KT > 1 && valid && !DBG(65)) {
         if (emit) {
           const float4* src = reinterpret_cast<const float4*>(p.state) +
-                              ((int64_t(slot(KT - 1)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
+                              ((int64_t(slot(KT - 1)) * stiles + stile) * p.Cq + (c0v + cb) / 4) * 128 + m;
 #pragma unroll
           for (int i = 0; i < NQ; ++i) sv[0][i] = DBG(32) ? ld_state_na(src + i * 128) : __ldcs(src + i * 128);
         }
@@ -635,12 +805,14 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
           for (int k = 1; k < KT - 1; ++k) {
             if (slot(k) < 0) continue;
             const float4* src = reinterpret_cast<const float4*>(p.state) +
-                                ((int64_t(slot(k)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
+                                ((int64_t(slot(k)) * stiles + stile) * p.Cq + (c0v + cb) / 4) * 128 + m;
 #pragma unroll
             for (int i = 0; i < NQ; ++i) sv[k][i] = DBG(32) ? ld_state_na(src + i * 128) : __ldcs(src + i * 128);
           }
         }
       }
+      // STEM: the first part of tile T converts tile T+1 while this item's state loads fly
+      if (stem && cb == cs * CPW && li % p.n_split == 0) convert(li / p.n_split + 1);
       if (cb == cs * CPW && !DBG(16)) {
         ptx::mbar_wait(&acc_full[buf], bph);
         ptx::tc_fence_after();
@@ -657,7 +829,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
             // (computed on every lane: the bf16 stores below pair lanes up)
 #pragma unroll
             for (int i = 0; i < 16; i += 4) {
-              const float4 bb = *reinterpret_cast<const float4*>(bias_s + cb + c + i);
+              const float4 bb = *reinterpret_cast<const float4*>(bias_s + bias0 + cb + c + i);
               if (KT > 1) {
                 const float4 t4 = sv[0][(c + i) >> 2];
                 v[i] += t4.x; v[i + 1] += t4.y; v[i + 2] += t4.z; v[i + 3] += t4.w;
@@ -668,7 +840,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
 #pragma unroll
               for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
             }
-            const int64_t yoff = b * p.y_bstride + yt + (pix - b * p.HWo) * p.Cout + c0 + cb + c;
+            const int64_t yoff = b * p.y_bstride + yt + (pix - b * p.HWo) * p.Cout + c0v + cb + c;
             if (p.out_f32) {
               float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + yoff);
               if (valid) {
@@ -719,7 +891,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
           // the warp's 32 rows go out row-contiguously: 32 / YU rows of CE
           // channels per store instruction (whole 2 CE-byte runs, not 16-B pieces)
           __syncwarp();
-          const int64_t ybase = b * p.y_bstride + yt + (pix - b * p.HWo) * p.Cout + c0 + cb;
+          const int64_t ybase = b * p.y_bstride + yt + (pix - b * p.HWo) * p.Cout + c0v + cb;
           __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(p.y);
 #pragma unroll
           for (int j = 0; j < YU; ++j) {
@@ -738,7 +910,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
         for (int k = KT - 2; k >= 1; --k) {
           if (slot(k) < 0) continue;
           float4* dst = reinterpret_cast<float4*>(p.state) +
-                        ((int64_t(slot(k)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
+                        ((int64_t(slot(k)) * stiles + stile) * p.Cq + (c0v + cb) / 4) * 128 + m;
 #pragma unroll
           for (int c = 0; c < CE; c += 16) {
             if (!DBG(8)) ptx::tmem_ld16(t_row + uint32_t(k * CC + cb + c), v);
@@ -756,7 +928,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
         // ---- (3) start the newest output (overwrites the emitted slot)
         if (slot(0) >= 0) {
           float4* dst = reinterpret_cast<float4*>(p.state) +
-                        ((int64_t(slot(0)) * stiles + stile) * p.Cq + (c0 + cb) / 4) * 128 + m;
+                        ((int64_t(slot(0)) * stiles + stile) * p.Cq + (c0v + cb) / 4) * 128 + m;
 #pragma unroll
           for (int c = 0; c < CE; c += 16) {
             if (!DBG(8)) ptx::tmem_ld16(t_row + uint32_t(cb + c), v);
@@ -777,10 +949,16 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     if constexpr (PAIR == 2) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&acc_empty[buf]), 0));
     else ptx::mbar_arrive_relaxed(&acc_empty[buf]);
   };
-  if (!p.ticks) {
+  if (stem) {
+    // CTA-local works li = (tile T, part li mod n_split); group e takes every EG-th
+    const int64_t n_t = p.n_tiles > blockIdx.x ? (p.n_tiles - blockIdx.x + grid - 1) / grid : 0;
+    if (e == 0) convert(0);
+    for (int64_t li = e; li < n_t * p.n_split; li += EG)
+      work(int64_t(blockIdx.x) + (li / p.n_split) * grid, int(li % p.n_split) * CC, li, nullptr);
+  } else if (!p.ticks) {
     int64_t li = e;
     for (int64_t item = unit + int64_t(e) * n_units; item < p.n_items; item += EG * int64_t(n_units), li += EG)
-      work(item, li, nullptr);
+      work(tile_of(item), c0, li, nullptr);
   } else {
     // chunked: item bi + e n_units of every batch, all T frames in order; the work
     // index over the unit's sequence (batch-major, then frame, then item) picks the buffer
@@ -789,7 +967,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       const int64_t left = (p.n_items - bi + n_units - 1) / n_units;
       const int nb = left < EG ? int(left) : EG;
       for (int t = 0; e < nb && t < p.T; ++t)
-        work(bi + int64_t(e) * n_units, wbase + int64_t(t) * nb + e, p.ticks + t * kTickInts);
+        work(tile_of(bi + int64_t(e) * n_units), c0, wbase + int64_t(t) * nb + e, p.ticks + t * kTickInts);
       wbase += int64_t(nb) * p.T;
     }
   }
@@ -912,6 +1090,7 @@ struct Variant {
   int KH = 0, KW = 0, KC = 0;     // > 0: specialised (unrolled) HALO/FLAT variant for this kernel / Cin
   int CS = 1;                     // epilogue warps per TMEM lane quadrant (column split)
   int PAIR = 1;                   // 2: CTA pairs (cta_group::2, M = 256), HALO / FLAT only
+  int STEM = 0;                   // 1: the MODE_STEM instantiation (shared-memory W-im2col)
 };
 
 #define CO_TC_VARIANT(kt, cc, eg, ce) {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce>}
@@ -923,6 +1102,8 @@ struct Variant {
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, 0, 0, 0, 1, 2>, 0, 0, 0, 1, 2}
 #define CO_TC_PAIR(kt, cc, eg, ce, kh, kw, kc) \
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, kh, kw, kc, 1, 2>, kh, kw, kc, 1, 2}
+#define CO_TC_STEMV(kt, cc, eg, ce) \
+  {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, 0, 0, 0, 1, 1, true>, 0, 0, 0, 1, 1, 1}
 const Variant kVariants[] = {
     CO_TC_PAIR(3, 32, 2, 32, 3, 3, 4), CO_TC_PAIR(3, 32, 3, 32, 3, 3, 4), CO_TC_PAIR(9, 16, 2, 16, 1, 1, 16),
     CO_TC_PAIR(1, 128, 2, 32, 3, 3, 4), CO_TC_SPEC(1, 128, 2, 32, 3, 3, 4), CO_TC_PAIR(3, 64, 2, 32, 3, 3, 4),
@@ -936,6 +1117,9 @@ const Variant kVariants[] = {
     CO_TC_VARIANT(3, 64, 2, 32), CO_TC_VARIANT(5, 16, 4, 16), CO_TC_VARIANT(5, 32, 2, 16),
     CO_TC_VARIANT(5, 32, 3, 16),
     CO_TC_VARIANT(9, 16, 2, 16),
+    // STEM twins of the K-pipeline variants small-Cin stems plan to (plan_stem)
+    CO_TC_STEMV(1, 64, 4, 32), CO_TC_STEMV(2, 32, 4, 32), CO_TC_STEMV(3, 32, 3, 32), CO_TC_STEMV(5, 32, 3, 16),
+    CO_TC_STEMV(9, 16, 2, 16),
 };
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -963,6 +1147,9 @@ struct Plan {
   int a_bytes = 0, a_stride = 0, chunk_stride = 0, w_bytes = 0, w_off = 0, stages = 2;
   int ystage = 0, y_off = 0;      // HALO bf16: y stores transposed through shared memory
   int ka_stages = 0, ka_stride = 0, ka_phase = 0, dmin_h = 0, dmin_w = 0;   // KHALO input-halo ring
+  // STEM (fused W-im2col): raw rows per tile, padded raw-row pitch / left pad, image rows / bytes
+  int st_nraw = 0, st_rpitch = 0, st_pad = 0, st_img_rows = 0, st_img_bytes = 0, st_raw_off = 0;
+  int st_groups = 0, st_data_groups = 0, st_phase_base[2] = {0, 0};
   int64_t n_tiles = 0;
   size_t smem = 0;
 };
@@ -1038,7 +1225,7 @@ bool plan_resident(const Geom& g, Plan& pl) {
   const Variant* best = nullptr;
   int64_t best_rank = -1;
   for (const Variant& v : kVariants) {
-    if (v.KT != g.kt || g.Cout % v.CC != 0) continue;
+    if (v.KT != g.kt || g.Cout % v.CC != 0 || v.STEM) continue;
     if (v.KH && (v.KH != g.kh || v.KW != g.kw || v.KC * 16 != g.Cin)) continue;
     if ((eg_pin && v.EG != eg_pin) || (pinned_cc() && v.CC != pinned_cc()) || (pinned_ce() && v.CE != pinned_ce()))
       continue;
@@ -1122,7 +1309,7 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
   for (int pair : {want, 3 - want}) {           // the preferred pairing, else the other
     if (option(OPT_KPAIR) && pair != want) break;
     for (const Variant& v : kVariants) {
-      if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.CS != 1 || v.PAIR != pair) continue;
+      if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.CS != 1 || v.PAIR != pair || v.STEM) continue;
       if ((eg_pin && v.EG != eg_pin) || (pinned_cc() && v.CC != pinned_cc())) continue;
       // prefer a width whose items fill at least half the SMs, then the widest
       // N (fewest A re-reads), then more groups (MHA: the 1024 x 1024 output
@@ -1215,6 +1402,58 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
   return true;
 }
 
+// STEM: the W-im2col of a small-Cin stem built in shared memory from raw rows
+// (MODE_STEM above) instead of an HBM pass.  Takes the K-pipeline plan of the
+// W-im2col'd layer (variant, weight chunks) and replaces its A operand.
+bool plan_stem(const Geom& g, Plan& pl) {
+  const Geom& k = pl.gk;
+  if (!option(OPT_STEM) || pl.mode != MODE_KLOOP || pl.var->PAIR != 1 || pl.var->CS != 1) return false;
+  // an STM instantiation for this kt: the widest channel part, then more epilogue groups
+  const Variant* twin = nullptr;
+  for (const Variant& v : kVariants)
+    if (v.STEM && v.KT == g.kt && g.Cout % v.CC == 0 &&
+        (!twin || v.CC * 100 + v.EG > twin->CC * 100 + twin->EG))
+      twin = &v;
+  if (!twin) return false;
+  if (pl.tiles_w != 1 || pl.TW != g.Wo || k.sh > 2 || g.dh != 1 || g.dw != 1 || (k.Cin != 16 && k.Cin != 32)) return false;
+  if ((int64_t(g.W) * g.Cin * 2) % 16 != 0 || pl.kb != k.Cin) return false;
+  const int sh = k.sh, TH = pl.TH, Wo = g.Wo;
+  const int nraw = (TH - 1) * sh + k.kh;
+  int base[2] = {0, 0}, rows = 0;
+  for (int ph = 0; ph < sh; ++ph) {
+    base[ph] = rows;
+    rows += ((nraw - ph + sh - 1) / sh) * Wo;
+  }
+  const int img_rows = rows + 128;                        // + the 128-row MMA's over-read past the last phase
+  const int groups = k.Cin / 8, data_groups = (g.kw * g.Cin + 7) / 8;
+  const int img_bytes = (groups * img_rows * 16 + 1023) / 1024 * 1024;
+  // padded raw row: zeros before (>= pw Cin + 1 for the mid-word funnel) and after the data
+  const int pad = ((g.pw * g.Cin + 1 + 7) / 8) * 8;
+  const int max_e = pad + ((Wo - 1) * g.sw - g.pw) * g.Cin + data_groups * 8 + 1;
+  const int rpitch = ((std::max(pad + g.W * g.Cin, max_e + 1) * 2 + 15) / 16) * 16;
+  const int raw_off = 2 * img_bytes;
+  const int w_off = ((raw_off + 2 * nraw * rpitch) + 1023) / 1024 * 1024;
+  const int N = twin->KT * twin->CC;
+  const int b_bytes = (pl.kb / 8) * N * 16;               // one tap's weight chunk of one part
+  const int b_stride = (b_bytes + 1023) / 1024 * 1024;
+  const size_t fixed = 1024 + 512 + size_t(g.Cout) * 4 + 64 * 4 + size_t(w_off);
+  const int stages = int(std::min<size_t>(kMaxStagesStd, (kSmemBudget > fixed ? kSmemBudget - fixed : 0) / b_stride));
+  if (stages < 2 || fixed + size_t(stages) * b_stride > kSmemLimit) return false;
+  pl.mode = MODE_STEM;
+  pl.var = twin;
+  pl.st_nraw = nraw; pl.st_rpitch = rpitch; pl.st_pad = pad; pl.st_img_rows = img_rows; pl.st_img_bytes = img_bytes;
+  pl.st_raw_off = raw_off; pl.st_groups = groups; pl.st_data_groups = data_groups;
+  pl.st_phase_base[0] = base[0]; pl.st_phase_base[1] = base[1];
+  pl.w_off = w_off;
+  pl.b_bytes = b_bytes;
+  pl.w_bytes = N * k.Cin * k.kh * k.kw * 2;
+  pl.a_stride = b_stride; pl.b_off = 0; pl.a_bytes = 0;
+  pl.stages = stages;
+  pl.swa = 0;
+  pl.smem = fixed + size_t(stages) * b_stride;
+  return true;
+}
+
 Plan make_plan(const Geom& g) {
   Plan pl;
   if (g.in_dtype != BF16 || g.groups != 1 || g.Cout % 4 != 0) return pl;
@@ -1243,7 +1482,8 @@ Plan make_plan(const Geom& g) {
   }
   const bool force_kloop = option(OPT_TC_MODE) == 1;   // option "tc_mode" = 1 forces the K pipeline
   pl.ok = (!force_kloop && plan_resident(pl.gk, pl)) || plan_kloop(pl.gk, pl);
-  if (pl.ok && pl.mode != MODE_KLOOP && pl.gk.Cin % 64 == 0 && swa_enabled()) pl.swa = 1;
+  if (pl.ok && pl.wcols) plan_stem(g, pl);
+  if (pl.ok && pl.mode != MODE_KLOOP && pl.mode != MODE_STEM && pl.gk.Cin % 64 == 0 && swa_enabled()) pl.swa = 1;
   if (pl.ok) pl.n_split = g.Cout / pl.var->CC;
   return pl;
 }
@@ -1312,7 +1552,8 @@ DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, dev);
   char buf[128];
-  const char* mname = pl.mode == MODE_KLOOP ? (pl.wcols ? ",kloop+wcols" : ",kloop") : pl.mode == MODE_KHALO ? ",khalo" : "";
+  const char* mname = pl.mode == MODE_KLOOP ? (pl.wcols ? ",kloop+wcols" : ",kloop")
+                      : pl.mode == MODE_KHALO ? ",khalo" : pl.mode == MODE_STEM ? ",stem" : "";
   if (pl.var->KH)
     snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d,%dx%dx%d%s%s%s>", pl.var->KT, pl.var->CC, pl.var->EG,
              pl.var->KH, pl.var->KW, pl.var->KC * 16, pl.var->CS > 1 ? ",split" : "",
@@ -1380,6 +1621,16 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
     x = a.state;
     x_bstride = frame;
     n_batch = k.B * (g.f + 1);
+  } else if (pl.mode == MODE_STEM) {
+    // the kernel bulk-copies raw rows itself: they must be 16-B aligned
+    if (x && ((reinterpret_cast<uintptr_t>(x) & 15) || (x_bstride * 2) % 16)) {
+      if (cudaError_t e = ensure_stage(t, size_t(g.B) * frame * 2)) return e;
+      if (cudaError_t e = cudaMemcpy2DAsync(t->xstage, frame * 2, x, x_bstride * 2, frame * 2, g.B,
+                                            cudaMemcpyDeviceToDevice, s))
+        return e;
+      x = t->xstage;
+      x_bstride = frame;
+    }
   } else if (pl.wcols) {
     // small-Cin stem: W-im2col the frame (a zero frame stays zero)
     const int64_t kframe = int64_t(k.H) * k.W * k.Cin;
@@ -1410,9 +1661,11 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
     x_bstride = frame;
   }
   CUtensorMap map;
-  CUresult r;
+  CUresult r = CUDA_SUCCESS;
   auto encode = get_encode();
-  if (pl.mode == MODE_FLAT) {
+  if (pl.mode == MODE_STEM) {
+    memset(&map, 0, sizeof(map));                     // STEM reads raw rows by bulk copy: no A tensor map
+  } else if (pl.mode == MODE_FLAT) {
     const cuuint32_t cw = pl.swa ? 64 : 8;    // channels per row of the box (128-B swizzled or 16-B)
     cuuint64_t dims[3] = {cw, cuuint64_t(flat_rows), cuuint64_t(k.Cin / cw)};
     cuuint64_t strides[2] = {cuuint64_t(k.Cin) * 2, cw * 2};
@@ -1511,6 +1764,16 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   p.swa = pl.swa;
   p.a_rows = pl.chunk_stride / 16;
   p.Cq = g.Cq;
+  if (pl.mode == MODE_STEM) {
+    p.x = static_cast<const __nv_bfloat16*>(x);
+    p.x_bstride = x_bstride;
+    p.st_Hin = g.H; p.st_Win = g.W; p.st_cin = g.Cin;
+    p.st_sw = g.sw; p.st_pw = g.pw; p.st_kwc = g.kw * g.Cin;
+    p.st_nraw = pl.st_nraw; p.st_rpitch = pl.st_rpitch; p.st_pad = pl.st_pad; p.st_raw_off = pl.st_raw_off;
+    p.st_img_rows = pl.st_img_rows; p.st_img_bytes = pl.st_img_bytes;
+    p.st_groups = pl.st_groups; p.st_data_groups = pl.st_data_groups;
+    p.st_phase_base[0] = pl.st_phase_base[0]; p.st_phase_base[1] = pl.st_phase_base[1];
+  }
   p.T = T;
   p.x_tmul = int(clip_T);
   p.ticks = ticks;
@@ -1523,7 +1786,9 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   p.bias = bias;
   p.mc = mc;
   const int per = std::max(1, t->num_sms / clu / pl.n_split);
-  const int64_t grid = std::min<int64_t>(per, units_tiles) * pl.n_split * clu;
+  // STEM: a CTA serves every part of its tiles (one image per tile), one CTA per SM
+  const int64_t grid = pl.mode == MODE_STEM ? std::min<int64_t>(t->num_sms, pl.n_tiles)
+                                            : std::min<int64_t>(per, units_tiles) * pl.n_split * clu;
   // KLOOP pairs stream their weight halves through a tensor map over the packed
   // weights [part*2 + half][K/8][N/2][8]: box = one chunk (kb/8 K-groups)
   CUtensorMap wmap = map;

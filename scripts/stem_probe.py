@@ -10,6 +10,7 @@ import json
 import os
 import statistics
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -43,6 +44,9 @@ def main():
             cur = y
     torch.cuda.synchronize()
     for spec in a.layers.split(";"):
+        if spec == "sleep":
+            time.sleep(5)
+            continue
         ls = [int(v) for v in spec.split(",")]
         K = a.steps
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(ls) + 1)] for _ in range(K)]

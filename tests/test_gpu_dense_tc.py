@@ -53,8 +53,21 @@ CASES = {
     "khalo_s2_kt1_single": dict(desc=O.Desc(2, 64, 128, (1, 3, 3), stride=(1, 2, 2), padding=(0, 1, 1),
                                             in_spatial=(10, 14)), B=3),
     # small-Cin stems: W-im2col'd frame (C4 layer 1 shaped), KLOOP (stride 2) and HALO (stride 1)
-    "stem_c4like": dict(desc=O.Desc(2, 3, 32, (5, 7, 7), stride=(1, 2, 2), padding=(0, 3, 3), in_spatial=(20, 22)), B=2),
+    "stem_c4like": dict(desc=O.Desc(2, 3, 32, (5, 7, 7), stride=(1, 2, 2), padding=(0, 3, 3), in_spatial=(20, 24)), B=2),
     "stem_halo": dict(desc=O.Desc(2, 3, 16, (3, 3, 3), padding=(1, 1, 1), in_spatial=(9, 10)), B=2),
+    # STEM (shared-memory W-im2col): two channel parts on one image, 7 output rows per tile
+    # (19 raw rows in 2 row phases), a 2-channel stem (Kp 16, even window starts), a
+    # 1-row tile of a wide frame, odd channel count with a 3-wide kernel
+    "stem_2parts": dict(desc=O.Desc(2, 3, 64, (5, 7, 7), stride=(1, 2, 2), padding=(0, 3, 3), in_spatial=(30, 32)),
+                        B=3),
+    "stem_c2": dict(desc=O.Desc(2, 2, 32, (3, 5, 5), stride=(1, 2, 2), padding=(0, 2, 2), in_spatial=(17, 24)), B=2),
+    "stem_wide": dict(desc=O.Desc(2, 3, 32, (2, 7, 7), stride=(1, 2, 2), padding=(0, 3, 3), in_spatial=(9, 248)),
+                      B=2),
+    "stem_k3c5": dict(desc=O.Desc(2, 5, 32, (3, 3, 3), stride=(1, 2, 2), padding=(1, 1, 1), in_spatial=(15, 16)),
+                      B=3),
+    # raw rows not a multiple of 16 B (22 x 3 bf16): no bulk copy -- the HBM W-im2col pass
+    "stem_unaligned": dict(desc=O.Desc(2, 3, 32, (5, 7, 7), stride=(1, 2, 2), padding=(0, 3, 3), in_spatial=(20, 22)),
+                           B=2),
     # temporal stride > 1 (Principle 5): skipped ticks are Empty, only
     # the slices feeding an emitted output touch the ring (A20)
     "halo_st2": dict(desc=O.Desc(2, 32, 32, (3, 3, 3), stride=(2, 1, 1), padding=(1, 1, 1), in_spatial=(6, 7)), B=2),
@@ -67,7 +80,7 @@ KPAIR_CASES = ["kloop_c4l3like", "kloop_bigK", "kloop_st3", "stem_c4like", "kloo
                "khalo_c4l4like", "khalo_s2_c4l3like"]   # KLOOP / KHALO CTA pairs
 
 
-def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force_kloop=False, pair=False):
+def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force_kloop=False, pair=False, stem=True):
     import os
     d, B = CASES[case]["desc"], CASES[case]["B"]
     rng = np.random.default_rng(seed)
@@ -84,6 +97,8 @@ def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force
     if pair:
         set_opt("pair", "2")
         set_opt("kpair", "2")
+    if not stem:
+        set_opt("stem", 0)                        # the HBM W-im2col pass + strided-gather K pipeline
     try:
         conv, sm, Wq, bq = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="dense_tc")
     finally:
@@ -91,12 +106,16 @@ def _run(case, integer=False, steps=None, out_dtype=torch.float32, seed=0, force
         reset_opt("pair")
         reset_opt("kpair")
         reset_opt("khalo")
+        reset_opt("stem")
     if pair:
         assert "pair" in conv.kernel_name, conv.kernel_name
     ref_conv, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="direct")
     assert conv.kernel_used == "dense_tc", conv.kernel_name
-    if force_kloop or case.startswith("kloop") or case == "stem_c4like":  # (kloop_st3: spatial stride 2)
+    if force_kloop or case.startswith("kloop"):  # (kloop_st3: spatial stride 2)
         assert "kloop" in conv.kernel_name, conv.kernel_name
+    if case.startswith("stem_") and case != "stem_halo":
+        fused = stem and not pair and case != "stem_unaligned"
+        assert (",stem" if fused else "kloop+wcols") in conv.kernel_name, conv.kernel_name
     if case.startswith("khalo"):
         assert "khalo" in conv.kernel_name, conv.kernel_name
         assert ("pair" in conv.kernel_name) == (not case.endswith("single")), conv.kernel_name
@@ -245,3 +264,48 @@ def test_c4_stack_reduced_spatial_vs_oracle():
             ys.append(np_of(y)); refs.append(r)
     y, ref = np.stack(ys), np.stack(refs).reshape(np.stack(ys).shape)
     assert rel_err(y, ref) <= 2e-2
+
+
+STEM_CASES = ["stem_c4like", "stem_2parts", "stem_c2", "stem_wide", "stem_k3c5"]
+
+
+@pytest.mark.parametrize("case", STEM_CASES)
+def test_stem_equals_hbm_wcols_path(case):
+    """The shared-memory W-im2col (MODE_STEM) feeds the tensor cores the same
+    operands in the same K order as the HBM W-im2col pass, so both paths are
+    bitwise equal -- and equal to the oracle in the integer regime."""
+    _, ya, ref, _ = _run(case, seed=3)
+    _, yb, _, _ = _run(case, seed=3, stem=False)
+    assert np.array_equal(ya, yb)
+    _, yi, ri, _ = _run(case, integer=True, seed=4)
+    assert np.array_equal(yi, ri)
+
+
+@pytest.mark.parametrize("B,H,W", [(48, 56, 56), (7, 112, 112)])
+def test_stem_many_tiles_per_cta(B, H, W):
+    """C4-stem shapes with several tiles per CTA (image / raw-row double
+    buffers wrapping, the conversion one tile ahead): stem == HBM W-im2col
+    path bit for bit over the delay and a few Ready ticks, and the pad step."""
+    import paper_2204_03418_b200 as co
+    d = O.Desc(2, 3, 64, (5, 7, 7), stride=(1, 2, 2), padding=(0, 3, 3), in_spatial=(H, W))
+    rng = np.random.default_rng(B)
+    Wt = torch.from_numpy(rng.standard_normal(d.w_shape) / 12).to(torch.bfloat16).cuda()
+    bt = torch.from_numpy(rng.standard_normal(64) * 0.1).float().cuda()
+    mk = lambda: co.Conv(3, 64, d.kernel, weight=Wt, bias=bt, stride=d.stride, padding=d.padding, in_spatial=(H, W),
+                         n_streams=B, out_dtype=torch.float32, activation="relu")
+    a = mk()
+    with co.options(stem=0):
+        b = mk()
+    assert ",stem" in a.kernel_name and "wcols" in b.kernel_name
+    g = torch.Generator(device="cuda").manual_seed(1)
+    for t in range(7):
+        x = co.channels_last(torch.randn((B, 3, H, W), generator=g, device="cuda").to(torch.bfloat16))
+        ya, yb = a.forward_step(x), b.forward_step(x)
+        assert (ya is None) == (yb is None)
+        if ya is not None:
+            assert torch.equal(ya, yb)
+    ya, yb = a.forward_pad_step(), b.forward_pad_step()
+    assert torch.equal(ya, yb)
+    sa, _ = a.state_dict_stream()
+    sb, _ = b.state_dict_stream()
+    assert torch.equal(sa, sb)
