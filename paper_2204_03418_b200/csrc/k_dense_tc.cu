@@ -119,6 +119,7 @@ struct TcParams {
   int ystage, y_off;              // HALO bf16: y transposed through a per-warp shared-memory buffer at y_off
   int l2last;                     // HALO / FLAT: frame tiles loaded with an L2 evict_last policy
   int pdl;                        // launched with programmatic stream serialization (see pdl_wait)
+  int l2pf;                       // L2 bulk prefetch of the state one item ahead (epilogue)
   int dbg;                        // CO_TC_DEBUG bits (experiments only): 1 no state/y traffic, 2 no MMA,
                                   // 4 no A loads, 8 no TMEM reads, 16 (with 2) no accumulator handshakes
   int Cq;
@@ -751,6 +752,23 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     ptx::mbar_arrive(&a_empty[2 + b]);                    // raw rows consumed
     ptx::mbar_arrive(&a_full[b]);                         // image ready
   };
+  // L2 prefetch of an item's state rows (every slot the step reads: the emit
+  // slot and the accumulated ones), issued by one thread of the group one item
+  // ahead: a (slot, tile, part) block is CC/4 channel quads x 128 rows x 16 B,
+  // contiguous, so it is one bulk prefetch -- DRAM -> L2 runs ahead of the
+  // epilogue's register loads, which then see L2 latency.
+  auto prefetch_state = [&](const int64_t tile, const int c0v) {
+    if (KT < 2 || gtid != 0 || !p.l2pf) return;
+    const int64_t stiles = p.splane >> 7;
+    auto one = [&](int sl) {
+      const float4* src = reinterpret_cast<const float4*>(p.state) + ((int64_t(sl) * stiles + tile) * p.Cq + c0v / 4) * 128;
+      ptx::bulk_prefetch_l2(src, uint32_t(CC) * 512u);
+    };
+    if (p.emit) one(p.slot[KT - 1]);
+    if (p.update)
+      for (int k = 1; k < KT - 1; ++k)
+        if (p.slot[k] >= 0) one(p.slot[k]);
+  };
   auto work = [&](const int64_t tile, const int c0v, const int64_t li, const int* tk) {
     const int buf = int(li % NBUF);                    // accumulator buffer of this work
     const uint32_t bph = uint32_t(li / NBUF) & 1u;
@@ -952,13 +970,21 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   if (stem) {
     // CTA-local works li = (tile T, part li mod n_split); group e takes every EG-th
     const int64_t n_t = p.n_tiles > blockIdx.x ? (p.n_tiles - blockIdx.x + grid - 1) / grid : 0;
+    auto tile_li = [&](int64_t li) { return int64_t(blockIdx.x) + (li / p.n_split) * grid; };
     if (e == 0) convert(0);
-    for (int64_t li = e; li < n_t * p.n_split; li += EG)
-      work(int64_t(blockIdx.x) + (li / p.n_split) * grid, int(li % p.n_split) * CC, li, nullptr);
+    if (e < n_t * p.n_split) prefetch_state(tile_li(e), int(e % p.n_split) * CC);
+    for (int64_t li = e; li < n_t * p.n_split; li += EG) {
+      if (li + EG < n_t * p.n_split) prefetch_state(tile_li(li + EG), int((li + EG) % p.n_split) * CC);
+      work(tile_li(li), int(li % p.n_split) * CC, li, nullptr);
+    }
   } else if (!p.ticks) {
     int64_t li = e;
-    for (int64_t item = unit + int64_t(e) * n_units; item < p.n_items; item += EG * int64_t(n_units), li += EG)
+    const int64_t step = EG * int64_t(n_units);
+    if (unit + int64_t(e) * n_units < p.n_items) prefetch_state(tile_of(unit + int64_t(e) * n_units), c0);
+    for (int64_t item = unit + int64_t(e) * n_units; item < p.n_items; item += step, li += EG) {
+      if (item + step < p.n_items) prefetch_state(tile_of(item + step), c0);
       work(tile_of(item), c0, li, nullptr);
+    }
   } else {
     // chunked: item bi + e n_units of every batch, all T frames in order; the work
     // index over the unit's sequence (batch-major, then frame, then item) picks the buffer
@@ -1102,12 +1128,19 @@ struct Variant {
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, 0, 0, 0, 1, 2>, 0, 0, 0, 1, 2}
 #define CO_TC_PAIR(kt, cc, eg, ce, kh, kw, kc) \
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, kh, kw, kc, 1, 2>, kh, kw, kc, 1, 2}
+// CTA pairs whose one epilogue group splits every item's channels over 2 x 4 warps
+// (CS = 2): an item's state traffic is drained by 8 warps at once instead of 4
+#define CO_TC_PAIRGS(kt, cc, eg, ce, cs) \
+  {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, 0, 0, 0, cs, 2>, 0, 0, 0, cs, 2}
 #define CO_TC_STEMV(kt, cc, eg, ce) \
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, 0, 0, 0, 1, 1, true>, 0, 0, 0, 1, 1, 1}
 const Variant kVariants[] = {
     CO_TC_PAIR(3, 32, 2, 32, 3, 3, 4), CO_TC_PAIR(3, 32, 3, 32, 3, 3, 4), CO_TC_PAIR(9, 16, 2, 16, 1, 1, 16),
     CO_TC_PAIR(1, 128, 2, 32, 3, 3, 4), CO_TC_SPEC(1, 128, 2, 32, 3, 3, 4), CO_TC_PAIR(3, 64, 2, 32, 3, 3, 4),
     CO_TC_PAIRG(3, 64, 2, 32), CO_TC_PAIRG(5, 32, 2, 16),
+#ifdef CO_EXPERIMENTS
+    CO_TC_PAIRGS(3, 64, 1, 32, 2), CO_TC_PAIRG(3, 32, 3, 32),   // measured slower on C4 L3 / L4 / L5
+#endif
     CO_TC_SPLIT(3, 32, 2, 16, 3, 3, 4, 2), CO_TC_SPLIT(3, 32, 3, 16, 3, 3, 4, 2),
     CO_TC_SPEC(3, 32, 2, 32, 3, 3, 4), CO_TC_SPEC(3, 32, 3, 32, 3, 3, 4), CO_TC_SPEC(9, 16, 2, 16, 1, 1, 16),
     CO_TC_VARIANT(1, 32, 4, 32), CO_TC_VARIANT(1, 64, 4, 32), CO_TC_VARIANT(1, 128, 2, 32),
@@ -1309,7 +1342,9 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
   for (int pair : {want, 3 - want}) {           // the preferred pairing, else the other
     if (option(OPT_KPAIR) && pair != want) break;
     for (const Variant& v : kVariants) {
-      if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.CS != 1 || v.PAIR != pair || v.STEM) continue;
+      // K-pipeline pairs may split an item's channels over 2 x 4 epilogue warps (CS = 2)
+      if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.PAIR != pair || v.STEM) continue;
+      if (v.CS != 1 && !(pair == 2 && v.CS == 2 && CO_EXP("CO_TC_KCS", 0))) continue;
       if ((eg_pin && v.EG != eg_pin) || (pinned_cc() && v.CC != pinned_cc())) continue;
       // prefer a width whose items fill at least half the SMs, then the widest
       // N (fewest A re-reads), then more groups (MHA: the 1024 x 1024 output
@@ -1318,7 +1353,7 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
       auto rank = [&](const Variant* x) {
         const int64_t items = (tiles + x->PAIR - 1) / x->PAIR * (g.Cout / x->CC) * x->PAIR;
         const bool fills = !CO_EXP("CO_TC_FILL", 1) ? true : items * 2 >= sm_count();
-        return (fills ? 1000000 : 0) + x->CC * 1000 + x->EG;
+        return (fills ? 1000000 : 0) + x->CC * 1000 + (x->CS == 2 ? 500 : 0) + x->EG;
       };
       if (!best || rank(&v) > rank(best)) best = &v;
     }
@@ -1747,6 +1782,9 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   for (int i = 0; i < kMaxKt; ++i) p.slot[i] = a.slot[i];
   p.emit = a.emit; p.update = a.update; p.act = g.act; p.out_f32 = (g.out_dtype == F32);
   p.dbg = CO_EXP("CO_TC_DEBUG", 0);              // experiment builds only (work-skipping A/B bits)
+  // measured (same box, interleaved A/B): C2 (HALO) 0.205 -> 0.200 ms, C5 (FLAT) 1.53 -> 1.40 ms;
+  // the C4 KHALO layers unchanged, the stem (4 slots read per item) 1.49 -> 1.62 ms
+  p.l2pf = CO_EXP("CO_TC_L2PF", (pl.mode == MODE_HALO || pl.mode == MODE_FLAT) ? 1 : 0);
   p.ystage = (pl.ystage && g.out_dtype == BF16) ? 1 : 0;
   {
     // programmatic dependent launch for single steps (CO_PDL=0 turns it off):
