@@ -456,9 +456,17 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
                   }
                 };
                 if (p.kflat) {    // rows tile*128 .. of ring slot k, viewed as a (B*HW, Cin) matrix
-                  ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes + p.b_bytes);
-                  ptx::tma_load_4d(dst, &tmap, &full[s], 0, int(tile * 128), cc, p.ring_slot[kk]);
-                  load_b();
+                  if constexpr (PAIR == 2) {
+                    // CTA pair: each CTA its own 128 rows and its N/2 half of the weight
+                    // chunk, both completing on the leader's barrier
+                    if (leader) ptx::mbar_arrive_expect_tx(&full[s], (p.a_bytes + p.b_bytes) * PAIR);
+                    ptx::tma_load_4d_pair(dst, &tmap, &full[s], 0, int(tile * 128), cc, p.ring_slot[kk]);
+                    ptx::tma_load_4d_pair(dst + p.b_off, &wmap, &full[s], 0, 0, kg / (p.kb / 8), part * PAIR + int(rank));
+                  } else {
+                    ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes + p.b_bytes);
+                    ptx::tma_load_4d(dst, &tmap, &full[s], 0, int(tile * 128), cc, p.ring_slot[kk]);
+                    load_b();
+                  }
                 } else if constexpr (PAIR == 2) {
                   if (leader) ptx::mbar_arrive_expect_tx(&full[s], (p.a_bytes + p.b_bytes) * PAIR);
                   ptx::tma_load_5d_pair(dst, &tmap, &full[s], 0, cw, ch, cc, bb);
@@ -1137,7 +1145,7 @@ struct Variant {
 const Variant kVariants[] = {
     CO_TC_PAIR(3, 32, 2, 32, 3, 3, 4), CO_TC_PAIR(3, 32, 3, 32, 3, 3, 4), CO_TC_PAIR(9, 16, 2, 16, 1, 1, 16),
     CO_TC_PAIR(1, 128, 2, 32, 3, 3, 4), CO_TC_SPEC(1, 128, 2, 32, 3, 3, 4), CO_TC_PAIR(3, 64, 2, 32, 3, 3, 4),
-    CO_TC_PAIRG(3, 64, 2, 32), CO_TC_PAIRG(5, 32, 2, 16),
+    CO_TC_PAIRG(3, 64, 2, 32), CO_TC_PAIRG(5, 32, 2, 16), CO_TC_PAIRG(1, 256, 2, 32),
 #ifdef CO_EXPERIMENTS
     CO_TC_PAIRGS(3, 64, 1, 32, 2), CO_TC_PAIRG(3, 32, 3, 32),   // measured slower on C4 L3 / L4 / L5
 #endif

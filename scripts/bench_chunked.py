@@ -63,7 +63,7 @@ def leg(name, T, clips, warmup):
         e1.synchronize()
     steps = clips * T
     ms = e0.elapsed_time(e1) / steps
-    hbm, _, src = measured_peaks()
+    hbm, _, _, src = measured_peaks()
     import paper_2204_03418_b200 as co
     chunked = co.get_option("chunk") != 0
     import math

@@ -61,7 +61,7 @@ def main():
             time.sleep(0.002)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
-    hbm, bf16, src = measured_peaks()
+    hbm, bf16, _, src = measured_peaks()
     att_bytes = B * (2 * n * E * 2 + 3 * E * 2 + E * 2)
     proj_flops = 8.0 * B * E * E
     proj_bytes = B * E * 2 * (1 + 3 + 1 + 1) + 4 * E * E * 2

@@ -90,7 +90,7 @@ def run(name, steps, warmup):
             time.sleep(0.002)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    hbm, _, src = measured_peaks()
+    hbm, _, _, src = measured_peaks()
     vh = ",vh" in p.kernel_name
     ab = alg_bytes(w, Ho, Wo, vh) * B
     ach = ab / (ms / 1e3) / 1e9
