@@ -1352,6 +1352,7 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
     for (const Variant& v : kVariants) {
       // K-pipeline pairs may split an item's channels over 2 x 4 epilogue warps (CS = 2)
       if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.PAIR != pair || v.STEM) continue;
+      if (v.PAIR == 2 && v.KT == 1 && !flat) continue;        // kt = 1 pairs: the RAW flat window contractions
       if (v.CS != 1 && !(pair == 2 && v.CS == 2 && CO_EXP("CO_TC_KCS", 0))) continue;
       if ((eg_pin && v.EG != eg_pin) || (pinned_cc() && v.CC != pinned_cc())) continue;
       // prefer a width whose items fill at least half the SMs, then the widest

@@ -1,0 +1,28 @@
+#!/bin/bash
+# ncu --set full capture of every bench layer at a Ready step (GPU box; one
+# layer per process via scripts/layer_probe.py, each run first without ncu).
+# Usage: bash scripts/ncu_all_layers.sh <tag>   -> gpurun_out/<tag>_c<C>l<L>[_raw].ncu-rep
+# Summarise here with scripts/ncu_summary.py (profiles/<tag>_*.txt, ncu_traffic.json).
+set -u
+TAG=${1:-r2}
+mkdir -p gpurun_out
+# config layer state kernel-regex launches-before-the-2nd-Ready-step
+CASES="1 0 psum k_step_direct 3
+2 0 psum k_step_dense_tc 3
+3 0 psum k_step_dw 3
+3 1 psum k_step_dw 5
+4 0 psum k_step_dense_tc 5
+4 1 psum k_step_dense_tc 1
+4 2 psum k_step_dense_tc 3
+4 3 psum k_step_dense_tc 3
+4 4 psum k_step_dense_tc 3
+5 0 psum k_step_dense_tc 17
+5 0 raw k_step_dense_tc 1"
+echo "$CASES" | while read C L S K N; do
+  suf=""; [ "$S" = raw ] && suf="_raw"
+  out=gpurun_out/${TAG}_c${C}l${L}${suf}
+  python scripts/layer_probe.py --config $C --layer $L --state $S --steps 3 > $out.plain.log 2>&1 || { echo "plain run failed: $C $L $S"; continue; }
+  ncu --set full --clock-control none --import-source on -k regex:$K -s $N -c 1 -o $out \
+      python scripts/layer_probe.py --config $C --layer $L --state $S --steps 3 > $out.ncu.log 2>&1
+  echo "$C $L $S rc=$? $(tail -1 $out.plain.log)"
+done

@@ -27,7 +27,7 @@ def test_c5_auto_layout_is_raw():
     W, b = synth.params(cfg)[0]
     c = co.Conv(L.cin, L.cout, L.kernel, weight=W.cuda(), bias=b.cuda(), dilation=L.dilation, spatial_rank=1,
                 in_spatial=cfg.in_spatial, n_streams=64, state_layout="auto")
-    assert c.state_layout == "raw", c.kernel_name
+    assert c.state_layout == "raw" and c.kernel_name == "k_step_dense_tc<1,256,2,pair,kloop>", c.kernel_name
     cfg2 = synth.config(2, n_streams=2)
     W2, b2 = synth.params(cfg2)[0]
     L2 = cfg2.layers[0]
