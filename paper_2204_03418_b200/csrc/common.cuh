@@ -116,6 +116,9 @@ struct StepArgs {
   // the block decomposition the phase q = m mod dil, i = m div dil, i mod kt and
   // (i - kt + 1) mod kt -- 32-bit, so no kernel divides 64-bit values per item
   int pm_f, pm_q, pm_pos, pm_js;
+  // RAW layout, dense 1x1 kernel: the Ready step reads the new frame straight
+  // from x and stores it into ring slot raw_store itself (-1: the host copied it)
+  int raw_store = -1;
 };
 
 // Pooling ring (§8f f3): slot = one spatially reduced frame (B, Ho, Wo, C); MAX

@@ -13,7 +13,9 @@ void dense_tc_state_layout(Geom& g);
 DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err);
 void dense_tc_destroy(DenseTC* t);
 const char* dense_tc_name(const DenseTC* t);
-int64_t dense_tc_buffer_gen(const DenseTC* t);   // changes whenever a step's staging buffer moves
+int64_t dense_tc_buffer_gen(const DenseTC* t);
+// RAW layout: can the Ready-step kernel read frame x directly and store it into its ring slot?
+bool dense_tc_fuses_raw_store(const DenseTC* t, const Geom& g, int64_t x_bstride);   // changes whenever a step's staging buffer moves
 cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const float* bias, cudaStream_t s);
 // Chunked steps: T consecutive ticks of a clip in one launch --
 // x points at the chunk's first frame of a clip (B, clip_T, H, W, Cin) -- item-batch-major so each tile's state stays L2-resident

@@ -466,15 +466,23 @@ static int step_raw(co_conv* h, int64_t& n, float* state, const void* x, int64_t
   const int cur = update_state ? int(floor_mod(m, g.f)) : g.f;
   const size_t fb = size_t(g.frame_elems) * dsize(g.in_dtype);
   char* slot = reinterpret_cast<char*>(state) + size_t(cur) * g.B * fb;
-  if (x) CO_CUDA(cudaMemcpy2DAsync(slot, fb, x, size_t(x_bstride) * dsize(g.in_dtype), fb, g.B,
-                                   cudaMemcpyDeviceToDevice, s));
-  else CO_CUDA(cudaMemsetAsync(slot, 0, g.B * fb, s));
+  // a Ready step of the flat tensor-core kernel reads x itself and stores it into the
+  // ring from shared memory (no separate copy of the frame); otherwise copy it here
+  const bool fused = r && x && h->kernel_used == CO_KERNEL_DENSE_TC &&
+                     (reinterpret_cast<uintptr_t>(x) & 15) == 0 && co::dense_tc_fuses_raw_store(h->tc, g, x_bstride);
+  if (fused) {
+  } else if (x) {
+    CO_CUDA(cudaMemcpy2DAsync(slot, fb, x, size_t(x_bstride) * dsize(g.in_dtype), fb, g.B, cudaMemcpyDeviceToDevice, s));
+  } else {
+    CO_CUDA(cudaMemsetAsync(slot, 0, g.B * fb, s));
+  }
   if (r) {
     StepArgs a;
     for (int k = 0; k < co::kMaxKt; ++k) a.slot[k] = -1;
     for (int k = 0; k + 1 < g.kt; ++k) a.slot[k] = int(floor_mod(m - int64_t(g.kt - 1 - k) * g.dt, g.f));
     a.slot[g.kt - 1] = cur;
-    a.x = nullptr; a.x_bstride = g.frame_elems;
+    a.x = fused ? x : nullptr; a.x_bstride = g.frame_elems;
+    a.raw_store = fused ? cur : -1;
     a.y = y; a.y_bstride = y_bstride;
     a.state = state;
     a.emit = 1;

@@ -112,6 +112,7 @@ struct TcParams {
   int slot[kMaxKt];
   int emit, update, act, out_f32;
   int raw_kh, raw_B;
+  int raw_xslot, raw_xk;          // RAW flat: tap raw_xk reads the frame from xmap, stored into ring slot raw_xslot (-1: no)
   int kflat;                      // KLOOP over 128 flattened (stream, pixel) rows (RAW, 1x1 spatial)              // RAW layout: real spatial kh (the K loop walks kt*kh rows), streams per ring slot
   int ring_slot[kMaxKt];          // RAW layout: ring slot of temporal tap k
   int swa, a_rows;                // A staged swizzled: 0 none, 1 128-B rows ([Cin/64][rows][128 B]),
@@ -190,7 +191,7 @@ template <int KT, int CC, int EG, int CE, int KH = 0, int KW = 0, int KC = 0, in
           bool STM = false>
 __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     k_step_dense_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap wmap,
-                    const TcParams p) {
+                    const __grid_constant__ CUtensorMap xmap, const TcParams p) {
   // wmap: the packed weights as a tensor, used by KLOOP CTA pairs (each CTA
   // streams its N/2 half of every B chunk with a pair TMA load)
   constexpr int N = KT * CC;
@@ -428,6 +429,18 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       } else {
         if (p.pdl) pdl_wait();
         const int per_stream = p.tiles_h * p.tiles_w;
+        // RAW flat fused ring store: stages holding chunks of the new frame, stored into
+        // the ring from shared memory once the MMA released them (tile * 16 + cc, -1 none)
+        int pend[kMaxStages];
+        for (int i = 0; i < kMaxStages; ++i) pend[i] = -1;
+        const bool xstore = p.kflat && p.raw_xslot >= 0 && part == 0;
+        auto flush = [&](int st) {
+          if (pend[st] < 0) return;
+          ptx::tma_store_4d(&tmap, a_s + st * p.a_stride, 0, (pend[st] >> 5) * 128, pend[st] & 31, p.raw_xslot);
+          ptx::bulk_commit();
+          ptx::bulk_wait_read0();                         // the stage may be refilled now
+          pend[st] = -1;
+        };
         for (int64_t item = unit; item < p.n_items; item += n_units) {
           const int64_t tile = tile_of(item);
           const int b = p.kflat ? 0 : int(tile / per_stream);
@@ -443,6 +456,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
             for (int v = 0; v < p.kw; ++v)
               for (int cb = 0; cb < p.n_cb; ++cb) {
                 ptx::mbar_wait(&empty[s], ph ^ 1);
+                if (xstore) flush(s);
                 uint8_t* dst = a_s + s * p.a_stride;
                 const int cw = wo0 * p.sw + v * p.dw - p.pw, ch = ho0 * p.sh + u * p.dh - p.ph;
                 const int cc = p.swa ? cb : cb * (p.kb / 8);   // swizzled: kb-channel blocks
@@ -456,17 +470,22 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
                   }
                 };
                 if (p.kflat) {    // rows tile*128 .. of ring slot k, viewed as a (B*HW, Cin) matrix
+                  // the new frame (tap raw_xk) straight from x when the kernel stores it into the ring
+                  const bool fromx = p.raw_xslot >= 0 && kk == p.raw_xk;
+                  const CUtensorMap* am = fromx ? &xmap : &tmap;
+                  const int aslot = fromx ? 0 : p.ring_slot[kk];
                   if constexpr (PAIR == 2) {
                     // CTA pair: each CTA its own 128 rows and its N/2 half of the weight
                     // chunk, both completing on the leader's barrier
                     if (leader) ptx::mbar_arrive_expect_tx(&full[s], (p.a_bytes + p.b_bytes) * PAIR);
-                    ptx::tma_load_4d_pair(dst, &tmap, &full[s], 0, int(tile * 128), cc, p.ring_slot[kk]);
+                    ptx::tma_load_4d_pair(dst, am, &full[s], 0, int(tile * 128), cc, aslot);
                     ptx::tma_load_4d_pair(dst + p.b_off, &wmap, &full[s], 0, 0, kg / (p.kb / 8), part * PAIR + int(rank));
                   } else {
                     ptx::mbar_arrive_expect_tx(&full[s], p.a_bytes + p.b_bytes);
-                    ptx::tma_load_4d(dst, &tmap, &full[s], 0, int(tile * 128), cc, p.ring_slot[kk]);
+                    ptx::tma_load_4d(dst, am, &full[s], 0, int(tile * 128), cc, aslot);
                     load_b();
                   }
+                  if (xstore && fromx) pend[s] = int(tile) * 32 + cc;
                 } else if constexpr (PAIR == 2) {
                   if (leader) ptx::mbar_arrive_expect_tx(&full[s], (p.a_bytes + p.b_bytes) * PAIR);
                   ptx::tma_load_5d_pair(dst, &tmap, &full[s], 0, cw, ch, cc, bb);
@@ -481,6 +500,15 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
                 if (++s == p.stages) { s = 0; ph ^= 1; }
               }
           }
+        }
+        if (xstore) {
+          // the last stages' new-frame chunks: store each once the MMA released it
+          for (int i = 0; i < p.stages; ++i) {
+            ptx::mbar_wait(&empty[s], ph ^ 1);
+            flush(s);
+            if (++s == p.stages) { s = 0; ph ^= 1; }
+          }
+          ptx::bulk_wait0();
         }
       }
     }
@@ -1116,7 +1144,7 @@ __global__ void __launch_bounds__(256) k_wcols_frame(const __nv_bfloat16* __rest
   }
 }
 
-typedef void (*KernFn)(const CUtensorMap, const CUtensorMap, const TcParams);
+typedef void (*KernFn)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
 
 struct Variant {
   int KT, CC, EG, CE;
@@ -1621,6 +1649,9 @@ void dense_tc_destroy(DenseTC* t) {
 
 const char* dense_tc_name(const DenseTC* t) { return t->name.c_str(); }
 int64_t dense_tc_buffer_gen(const DenseTC* t) { return t ? t->gen : 0; }
+bool dense_tc_fuses_raw_store(const DenseTC* t, const Geom& g, int64_t x_bstride) {
+  return t && g.raw && t->pl.kflat && g.kt > 1 && x_bstride == g.frame_elems && CO_EXP("CO_TC_RAWSTORE", 1);
+}
 
 static cudaError_t ensure_stage(DenseTC* t, size_t need) {
   if (t->xstage_bytes >= need) return cudaSuccess;
@@ -1851,7 +1882,26 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  void* args[] = {&map, &wmap, &p};
+  // RAW flat: the Ready step reads the new frame from x (a map like the ring's,
+  // one slot) and stores it into its ring slot from shared memory
+  CUtensorMap xmap = map;
+  p.raw_xslot = -1;
+  p.raw_xk = -1;
+  if (pl.kflat && a.raw_store >= 0 && a.x) {
+    const cuuint32_t cw = pl.swa ? cuuint32_t(pl.kb) : 8;
+    cuuint64_t dims[4] = {cw, cuuint64_t(g.B * g.HWo), cuuint64_t(k.Cin / cw), 1};
+    cuuint64_t strides[3] = {cuuint64_t(k.Cin) * 2, cuuint64_t(cw) * 2, cuuint64_t(g.B) * frame * 2};
+    cuuint32_t box[4] = {cw, 128, pl.swa ? 1u : cuuint32_t(pl.kb / 8), 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (encode(&xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(a.x), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE,
+               pl.swa == 1 ? CU_TENSOR_MAP_SWIZZLE_128B : pl.swa == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    p.raw_xslot = a.raw_store;
+    p.raw_xk = g.kt - 1;
+  }
+  void* args[] = {&map, &wmap, &xmap, &p};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(grid));
   cfg.blockDim = dim3(tc_threads(pl.var->EG, pl.var->CS));

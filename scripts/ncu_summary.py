@@ -4,7 +4,7 @@ DRAM traffic table profiles/ncu_traffic.json that bench.py reports as
 roofline.traffic (dram__bytes_read.sum + dram__bytes_write.sum per launch,
 divided by the streams one launch processes).
 
-usage: scripts/ncu_summary.py <tag> <rep> <streams> <kernel name as bench.py reports it> [...]
+usage: scripts/ncu_summary.py <tag> <rep or raw csv> <streams> <layer key ("<config>/L<i>[/raw]")> [...]
        (one name per captured launch, in launch order)
 """
 import csv
@@ -31,7 +31,11 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """The raw metrics page: from a report, or from its saved CSV (ncu -i rep --page raw --csv)."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return rows[0], rows[1], rows[2:]
 
