@@ -346,8 +346,10 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
             ptx::mbar_wait(&a_empty[as], aph ^ 1);
             uint8_t* adst = smem + as * p.ka_stride;
             const int n_ph = p.sh * p.sw;
-            if (!(PAIR == 2 && !leader)) ptx::mbar_arrive_expect_tx(&a_full[as], p.a_bytes * n_ph * PAIR);
-            for (int rr = 0; rr < p.sh; ++rr)
+            if (DBG(4)) {                               // experiment: no halo loads
+              if (!(PAIR == 2 && !leader)) ptx::mbar_arrive(&a_full[as]);
+            } else if (!(PAIR == 2 && !leader)) ptx::mbar_arrive_expect_tx(&a_full[as], p.a_bytes * n_ph * PAIR);
+            for (int rr = 0; rr < p.sh && !DBG(4); ++rr)
               for (int rc = 0; rc < p.sw; ++rc) {
                 // phase (rr, rc): original rows s (ho0 + dmin_h + i) + rr, columns s (dmin_w + j) + rc
                 uint8_t* pd = adst + (rr * p.sw + rc) * p.ka_phase;
@@ -360,7 +362,9 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
               const int kblk = tap * p.n_cb + cb;       // packed K index (u kw + v) Cin + ci, in 64-blocks
               ptx::mbar_wait(&empty[s], ph ^ 1);
               uint8_t* dst = a_s + s * p.a_stride;
-              if constexpr (PAIR == 2) {
+              if (DBG(1024)) {                          // experiment: no weight loads
+                if (leader) ptx::mbar_arrive(&full[s]);
+              } else if constexpr (PAIR == 2) {
                 if (leader) ptx::mbar_arrive_expect_tx(&full[s], p.b_bytes * PAIR);
                 ptx::tma_load_4d_pair(dst, &wmap, &full[s], 0, 0, kblk, part * PAIR + int(rank));
               } else {
@@ -590,6 +594,37 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       __syncwarp();
       int as = 0;
       uint32_t aph = 0;
+      if constexpr (KH > 0 && KC == 0 && PAIR == 2) {
+        // compile-time taps (the C4 layers' 3 x 3): tap offsets in registers, each
+        // chunk's 4 MMAs + commit in one branch-free elected issue
+        uint32_t toff[KH * KW];
+#pragma unroll
+        for (int t = 0; t < KH * KW; ++t) toff[t] = tap_tab[t];
+        for (int64_t item = unit; item < p.n_items; item += n_units) {
+          ptx::mbar_wait(&acc_empty[e], eph ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t d_tmem = tmem + uint32_t(e * BUF);
+          for (int cb = 0; cb < p.n_cb; ++cb) {
+            ptx::mbar_wait(&a_full[as], aph);
+            ptx::tc_fence_after();
+            const uint64_t a0 = ptx::smem_desc_sw128(ka_base + uint32_t(as * p.ka_stride));
+#pragma unroll
+            for (int tap = 0; tap < KH * KW; ++tap) {
+              ptx::mbar_wait(&full[s], ph);
+              ptx::tc_fence_after();
+              const uint64_t bd = ptx::smem_desc_sw128(a_base + uint32_t(s * p.a_stride));
+              ptx::mma4_commit_pair(d_tmem, a0 + toff[tap], 2u, bd, 2u, idesc, (cb | tap) ? 1u : 0u, &empty[s], 0x3);
+              if (++s == p.stages) { s = 0; ph ^= 1; }
+            }
+            if (ptx::elect_one()) commit(&a_empty[as]);   // halo free after its last tap
+            __syncwarp();
+            if (++as == p.ka_stages) { as = 0; aph ^= 1; }
+          }
+          if (ptx::elect_one()) commit(&acc_full[e]);
+          __syncwarp();
+          if (++e == NBUF) { e = 0; eph ^= 1; }
+        }
+      } else
       for (int64_t item = unit; item < p.n_items; item += n_units) {
         ptx::mbar_wait(&acc_empty[e], eph ^ 1);
         ptx::tc_fence_after();
@@ -1168,12 +1203,15 @@ struct Variant {
 // (CS = 2): an item's state traffic is drained by 8 warps at once instead of 4
 #define CO_TC_PAIRGS(kt, cc, eg, ce, cs) \
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, 0, 0, 0, cs, 2>, 0, 0, 0, cs, 2}
+// KHALO pairs with compile-time 3 x 3 taps (the C4 layers): KH = KW = 3, KC = 0
+#define CO_TC_KH3(kt, cc, eg, ce) \
+  {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, 3, 3, 0, 1, 2>, 3, 3, 0, 1, 2}
 #define CO_TC_STEMV(kt, cc, eg, ce) \
   {kt, cc, eg, ce, (KernFn)k_step_dense_tc<kt, cc, eg, ce, 0, 0, 0, 1, 1, true>, 0, 0, 0, 1, 1, 1}
 const Variant kVariants[] = {
     CO_TC_PAIR(3, 32, 2, 32, 3, 3, 4), CO_TC_PAIR(3, 32, 3, 32, 3, 3, 4), CO_TC_PAIR(9, 16, 2, 16, 1, 1, 16),
     CO_TC_PAIR(1, 128, 2, 32, 3, 3, 4), CO_TC_SPEC(1, 128, 2, 32, 3, 3, 4), CO_TC_PAIR(3, 64, 2, 32, 3, 3, 4),
-    CO_TC_PAIRG(3, 64, 2, 32), CO_TC_PAIRG(5, 32, 2, 16), CO_TC_PAIRG(1, 256, 2, 32),
+    CO_TC_PAIRG(3, 64, 2, 32), CO_TC_PAIRG(5, 32, 2, 16), CO_TC_PAIRG(1, 256, 2, 32), CO_TC_KH3(3, 64, 2, 32),
 #ifdef CO_EXPERIMENTS
     CO_TC_PAIRGS(3, 64, 1, 32, 2), CO_TC_PAIRG(3, 32, 3, 32),   // measured slower on C4 L3 / L4 / L5
 #endif
@@ -1379,7 +1417,9 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
     if (option(OPT_KPAIR) && pair != want) break;
     for (const Variant& v : kVariants) {
       // K-pipeline pairs may split an item's channels over 2 x 4 epilogue warps (CS = 2)
-      if (v.KT != g.kt || g.Cout % v.CC != 0 || v.KH || v.PAIR != pair || v.STEM) continue;
+      // KC == 0 KH / KW variants: compile-time taps of the K pipeline (KHALO), this kernel size only
+      if (v.KT != g.kt || g.Cout % v.CC != 0 || v.PAIR != pair || v.STEM) continue;
+      if (v.KH && (v.KC != 0 || v.KH != g.kh || v.KW != g.kw || !CO_EXP("CO_TC_KH3", 1))) continue;
       if (v.PAIR == 2 && v.KT == 1 && !flat) continue;        // kt = 1 pairs: the RAW flat window contractions
       if (v.CS != 1 && !(pair == 2 && v.CS == 2 && CO_EXP("CO_TC_KCS", 0))) continue;
       if ((eg_pin && v.EG != eg_pin) || (pinned_cc() && v.CC != pinned_cc())) continue;
@@ -1390,7 +1430,7 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
       auto rank = [&](const Variant* x) {
         const int64_t items = (tiles + x->PAIR - 1) / x->PAIR * (g.Cout / x->CC) * x->PAIR;
         const bool fills = !CO_EXP("CO_TC_FILL", 1) ? true : items * 2 >= sm_count();
-        return (fills ? 1000000 : 0) + x->CC * 1000 + (x->CS == 2 ? 500 : 0) + x->EG;
+        return (fills ? 1000000 : 0) + x->CC * 1000 + (x->CS == 2 ? 500 : 0) + (x->KH ? 100 : 0) + x->EG;
       };
       if (!best || rank(&v) > rank(best)) best = &v;
     }

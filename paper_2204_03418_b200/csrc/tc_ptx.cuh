@@ -322,6 +322,30 @@ __device__ __forceinline__ void mma_bf16_ss_pair(uint32_t d_tmem, uint64_t a_des
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Four K16 MMAs of one chunk on the pair (A / B descriptors advanced by astep /
+// bstep 16-B units each) and the commit of their completion to `bar` in the CTAs
+// of `mask`, issued by one elected lane of the converged warp with no branch:
+// the per-chunk issue cost of the K-pipelined layers (ncu: the MMA warp's loop,
+// not the operands, set their pace).
+__device__ __forceinline__ void mma4_commit_pair(uint32_t d_tmem, uint64_t a, uint64_t astep, uint64_t b,
+                                                 uint64_t bstep, uint32_t idesc, uint32_t accumulate, uint64_t* bar,
+                                                 uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.u32 t, 0, 0;\n\t"
+      "add.u64 a1, %1, %2;\n\tadd.u64 a2, a1, %2;\n\tadd.u64 a3, a2, %2;\n\t"
+      "add.u64 b1, %3, %4;\n\tadd.u64 b2, b1, %4;\n\tadd.u64 b3, b2, %4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %5, t;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%7], %8;\n\t}"
+      ::"r"(d_tmem), "l"(a), "l"(astep), "l"(b), "l"(bstep), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 // arrive on the mbarrier at this offset in every CTA of `mask` once the pair's prior MMAs complete
 __device__ __forceinline__ void tc_commit_pair(uint64_t* bar, uint16_t mask) {
   asm volatile(
