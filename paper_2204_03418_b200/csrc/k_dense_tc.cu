@@ -1666,7 +1666,10 @@ DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
   char buf[128];
   const char* mname = pl.mode == MODE_KLOOP ? (pl.wcols ? ",kloop+wcols" : ",kloop")
                       : pl.mode == MODE_KHALO ? ",khalo" : pl.mode == MODE_STEM ? ",stem" : "";
-  if (pl.var->KH)
+  if (pl.var->KH && pl.var->KC == 0)          // compile-time taps of the K pipeline
+    snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d,%dx%d%s%s>", pl.var->KT, pl.var->CC, pl.var->EG,
+             pl.var->KH, pl.var->KW, pl.var->PAIR > 1 ? ",pair" : "", mname);
+  else if (pl.var->KH)
     snprintf(buf, sizeof(buf), "k_step_dense_tc<%d,%d,%d,%dx%dx%d%s%s%s>", pl.var->KT, pl.var->CC, pl.var->EG,
              pl.var->KH, pl.var->KW, pl.var->KC * 16, pl.var->CS > 1 ? ",split" : "",
              pl.var->PAIR > 1 ? ",pair" : "", mname);

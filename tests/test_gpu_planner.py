@@ -10,8 +10,8 @@ EXPECTED = {
     2: ["k_step_dense_tc<3,32,3,3x3x64,pair>"],                      # HALO, CTA pair, 150 KB budget
     3: ["k_step_dw_st<3,3,3>", "k_step_dw_t<5>"],
     4: ["k_step_dense_tc<5,32,3,stem>", "k_step_dense_tc<1,128,2,3x3x64,pair>",
-        "k_step_dense_tc<3,64,2,pair,khalo>", "k_step_dense_tc<3,64,2,pair,khalo>",
-        "k_step_dense_tc<3,64,2,pair,khalo>"],                       # stem, HALO pair, 3 x KHALO (stride 2 / 1 / 2)
+        "k_step_dense_tc<3,64,2,3x3,pair,khalo>", "k_step_dense_tc<3,64,2,3x3,pair,khalo>",
+        "k_step_dense_tc<3,64,2,3x3,pair,khalo>"],                   # STEM, HALO pair, 3 x KHALO (stride 2 / 1 / 2)
     5: ["k_step_dense_tc<9,16,2,1x1x256,pair>"],                     # FLAT pair (fp32 partial-sum layout)
 }
 
