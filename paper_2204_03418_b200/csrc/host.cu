@@ -16,6 +16,7 @@
 #include "../../include/co.h"
 #include "common.cuh"
 #include "dense_tc.cuh"
+#include "stem_raw.cuh"
 #include "depthwise.cuh"
 
 using co::Geom;
@@ -221,6 +222,12 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
     const bool flat = g.kh == 1 && g.kw == 1 && g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0;
     g.raw = d->in_dtype == CO_BF16 && d->groups == 1 && flat && g.kt > 1 && 2.0 * raw_b <= psum_b &&
             g.Cin % 16 == 0 && g.Cout % 16 == 0;
+    // small-Cin stems (RGB input, e.g. C4 layer 1): the RAW ring of raw frames is
+    // an order of magnitude smaller than the partial sums (C4: 0.45 MB against
+    // 6.4 MB per stream-step) and k_stem_raw.cu contracts the window on the
+    // tensor cores with its weights resident
+    co::StemRawPlan sp;
+    if (!g.raw && g.kt > 1 && 2.0 * raw_b <= psum_b && co::stem_raw_plan(g, sp)) g.raw = 1;
   }
   if (g.op == CO_OP_DELAY) {
     if (g.kh != 1 || g.kw != 1 || g.sh != 1 || g.sw != 1 || g.ph || g.pw || g.dh != 1 || g.dw != 1 || g.pt ||

@@ -54,6 +54,7 @@
 #include <string>
 
 #include "dense_tc.cuh"
+#include "stem_raw.cuh"
 #include "tc_ptx.cuh"
 
 namespace co {
@@ -1610,9 +1611,16 @@ struct DenseTC {
   int64_t gen = 0;                   // bumped whenever xstage moves (captured graphs hold its address)
   int num_sms = 148;
   std::string name;
+  // RAW-ring small-Cin stem (k_stem_raw.cu): its own plan and kernel
+  bool stemraw = false;
+  StemRawPlan sp;
 };
 
-bool dense_tc_supported(const Geom& g) { return make_plan(g).ok && get_encode() != nullptr; }
+bool dense_tc_supported(const Geom& g) {
+  StemRawPlan sp;
+  if (g.raw && !make_plan(g).ok) return stem_raw_plan(g, sp);
+  return make_plan(g).ok && get_encode() != nullptr;
+}
 
 void dense_tc_state_layout(Geom& g) {
   const Plan pl = make_plan(g);
@@ -1636,6 +1644,21 @@ void dense_tc_state_layout(Geom& g) {
 
 DenseTC* dense_tc_create(const Geom& g, const void* w_dev, std::string& err) {
   Plan pl = make_plan(g);
+  if (g.raw && !pl.ok) {
+    // a small-Cin stem over the RAW ring: the resident-weight W-im2col kernel
+    DenseTC* t = new DenseTC();
+    if (!stem_raw_plan(g, t->sp)) { err = "unsupported shape"; delete t; return nullptr; }
+    t->stemraw = true;
+    cudaError_t e = cudaMalloc(&t->wpack, stem_raw_wpack_elems(t->sp, g) * 2);
+    if (e == cudaSuccess) e = stem_raw_pack(g, t->sp, w_dev, t->wpack);
+    if (e == cudaSuccess) e = stem_raw_prepare();
+    if (e != cudaSuccess) { err = cudaGetErrorString(e); dense_tc_destroy(t); return nullptr; }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    t->name = stem_raw_name(t->sp);
+    return t;
+  }
   if (!pl.ok) { err = "unsupported shape"; return nullptr; }
   if (!get_encode()) { err = "cuTensorMapEncodeTiled unavailable"; return nullptr; }
   DenseTC* t = new DenseTC();
@@ -1693,7 +1716,7 @@ void dense_tc_destroy(DenseTC* t) {
 const char* dense_tc_name(const DenseTC* t) { return t->name.c_str(); }
 int64_t dense_tc_buffer_gen(const DenseTC* t) { return t ? t->gen : 0; }
 bool dense_tc_fuses_raw_store(const DenseTC* t, const Geom& g, int64_t x_bstride) {
-  return t && g.raw && t->pl.kflat && g.kt > 1 && x_bstride == g.frame_elems && CO_EXP("CO_TC_RAWSTORE", 1);
+  return t && g.raw && !t->stemraw && t->pl.kflat && g.kt > 1 && x_bstride == g.frame_elems && CO_EXP("CO_TC_RAWSTORE", 1);
 }
 
 static cudaError_t ensure_stage(DenseTC* t, size_t need) {
@@ -1970,6 +1993,7 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
 }
 
 cudaError_t dense_tc_step(DenseTC* t, const Geom& g, const StepArgs& a, const float* bias, cudaStream_t s) {
+  if (t->stemraw) return stem_raw_step(g, t->sp, a, t->wpack, bias, t->num_sms, s);
   return tc_launch(t, g, a, bias, s, 1, nullptr, 0);
 }
 

@@ -180,3 +180,98 @@ def test_raw_depthwise_vs_oracle(case):
     assert rel_err(np.stack(ys), np.stack(refs)) <= 1e-4
     st, _ = conv.state_dict_stream()
     assert np.array_equal(_canon_to_oracle(st, d, B), sm.history())
+
+
+# Small-Cin stems over the RAW ring (k_stem_raw.cu): the W-im2col image built in
+# shared memory per (tile, temporal tap), weights resident, one window
+# contraction per Ready step.  Shapes span several 128-row tiles with ragged
+# last tiles, stride 1 / 2, odd padding (mid-word windows), a zero K group
+# (kw Cin = 21 -> Kp 32) and none (kw Cin = 9, 16), temporal stride and
+# dilation, temporal padding.
+RAW_STEM = {
+    "c4stem": dict(desc=O.Desc(2, 3, 64, (5, 7, 7), stride=(1, 2, 2), padding=(0, 3, 3), in_spatial=(36, 40)), B=3),
+    "c4stem_wide": dict(desc=O.Desc(2, 3, 64, (5, 7, 7), stride=(1, 2, 2), padding=(0, 3, 3), in_spatial=(30, 112)),
+                        B=2),
+    "s1_k3": dict(desc=O.Desc(2, 3, 32, (3, 3, 3), padding=(1, 1, 1), in_spatial=(9, 16)), B=2),
+    "cin4_st2_dil2": dict(desc=O.Desc(2, 4, 32, (3, 5, 5), stride=(2, 1, 2), padding=(1, 2, 2),
+                                      dilation=(2, 1, 1), in_spatial=(11, 14)), B=2),
+    "cin1_k2": dict(desc=O.Desc(2, 1, 64, (2, 3, 3), padding=(0, 1, 1), in_spatial=(10, 24)), B=4),
+    "cin2_ph0": dict(desc=O.Desc(2, 2, 32, (4, 3, 8), stride=(1, 2, 1), padding=(0, 0, 0), in_spatial=(13, 24)), B=2),
+}
+
+
+@pytest.mark.parametrize("case", list(RAW_STEM))
+@pytest.mark.parametrize("integer", [False, True])
+def test_raw_stem_tc_vs_oracle(case, integer):
+    d, B = RAW_STEM[case]["desc"], RAW_STEM[case]["B"]
+    rng = np.random.default_rng(3100)
+    if integer:
+        W = rng.integers(-2, 3, d.w_shape).astype(np.float64)
+        b = rng.integers(-2, 3, d.cout).astype(np.float64)
+    else:
+        W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
+        b = rng.standard_normal(d.cout) * 0.1
+    for out_dtype in (torch.float32, torch.bfloat16):
+        conv, sm, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, out_dtype=out_dtype, kernel="dense_tc",
+                                   state_layout="raw", activation="relu" if out_dtype == torch.bfloat16 else None)
+        assert conv.kernel_used == "dense_tc" and "stem_raw" in conv.kernel_name, conv.kernel_name
+        ys, refs = [], []
+        for t in range(d.receptive_field + 2 * d.stride[0] + 3):
+            x = rng.integers(-2, 3, _shape(d, B)).astype(np.float64) if integer else rng.standard_normal(_shape(d, B))
+            xt = to_cl(x, torch.bfloat16)
+            y = conv.forward_step(xt)
+            r = sm.forward_step(np_of(xt))
+            assert (y is None) == (r is None)
+            assert (conv.n, conv.head) == (sm.n, sm.head)
+            if y is not None:
+                ys.append(np_of(y)); refs.append(r.reshape(y.shape))
+        assert ys
+        y, ref = np.stack(ys), np.stack(refs)
+        if out_dtype == torch.bfloat16:
+            ref = np.maximum(ref, 0.0)
+            if integer:
+                # integer sums are exact in fp32: the bf16 output is RNE of the exact value
+                assert np.array_equal(y, torch.from_numpy(ref).to(torch.bfloat16).double().numpy())
+            else:
+                from tests.helpers import assert_bf16_rounding_bound
+                assert_bf16_rounding_bound(y, ref)
+        elif integer:
+            assert np.array_equal(y, ref)
+        else:
+            assert rel_err(y, ref) <= 1e-4
+        st, _ = conv.state_dict_stream()
+        assert np.array_equal(_canon_to_oracle(st, d, B), sm.history())
+
+
+def test_raw_stem_auto_layout_and_zero_frames():
+    """CO_STATE_AUTO picks the RAW ring for the C4 stem shape (0.45 MB against
+    6.4 MB of partial sums per stream-step); pad steps (zero frames) and
+    update_state = 0 probes behave as on the oracle."""
+    d = O.Desc(2, 3, 64, (5, 7, 7), stride=(1, 2, 2), padding=(2, 3, 3), in_spatial=(24, 32))
+    B = 2
+    rng = np.random.default_rng(3200)
+    W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
+    b = rng.standard_normal(d.cout) * 0.1
+    conv, sm, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="auto", state_layout="auto")
+    assert "stem_raw" in conv.kernel_name, conv.kernel_name
+    ys, refs = [], []
+    for t in range(9):
+        xt = to_cl(rng.standard_normal(_shape(d, B)), torch.bfloat16)
+        if t == 6:   # a probe: the output of this frame without advancing the state
+            yp = conv.forward_step(xt, update_state=False)
+            rp = sm.forward_step(np_of(xt), update_state=False)
+            assert (yp is None) == (rp is None)
+            if yp is not None:
+                assert rel_err(np_of(yp), rp.reshape(yp.shape)) <= 1e-4
+        y = conv.forward_step(xt)
+        r = sm.forward_step(np_of(xt))
+        assert (y is None) == (r is None)
+        if y is not None:
+            ys.append(np_of(y)); refs.append(r.reshape(y.shape))
+    for _ in range(d.padding[0]):
+        y = conv.forward_pad_step()
+        r = sm.forward_step(None)
+        assert (y is None) == (r is None)
+        if y is not None:
+            ys.append(np_of(y)); refs.append(r.reshape(y.shape))
+    assert rel_err(np.stack(ys), np.stack(refs)) <= 1e-4
