@@ -47,9 +47,10 @@ namespace {
 
 constexpr int kNI = 4;           // image ring
 constexpr int kNR = 4;           // raw-row ring
-constexpr int kConvWarps = 8;    // expander warps
-constexpr int kThreads = 32 * (4 + kConvWarps + 2);
-constexpr int kProducer = 4 + kConvWarps, kMma = 5 + kConvWarps;
+constexpr int kEpiWarps = 8;     // two epilogue groups of 4 warps (alternate tiles)
+constexpr int kExpWarps = 8;     // two expander groups of 4 warps (alternate images)
+constexpr int kThreads = 32 * (kEpiWarps + kExpWarps + 2);
+constexpr int kProducer = kEpiWarps + kExpWarps, kMma = kProducer + 1;
 constexpr size_t kSmemLimit = 227 * 1024;
 
 struct SrParams {
@@ -85,6 +86,15 @@ struct SrParams {
 #define TWAIT(bar, par, acc) ptx::mbar_wait(bar, par)
 #endif
 
+// position in a ring of n buffers: index and phase parity, advanced without division
+struct Ring {
+  int i = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++i == n) { i = 0; ph ^= 1u; }
+  }
+};
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -94,7 +104,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 // image's A descriptors held in registers and the issue loop unrolled
 template <int N, int SW, int PER>
 __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_constant__ SrParams p) {
-  constexpr int NBUF = (512 / N) < 4 ? (512 / N) : 4;   // TMEM accumulator ring
+  constexpr int NBUF = 4;                              // TMEM accumulators: 2 per epilogue group
   constexpr int CP = 8 / SW;                            // padded channels per pixel (16 / SW bytes)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -115,8 +125,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kProducer && lane == 0) {
     ptx::mbar_init(w_full, 1);
-    for (int r = 0; r < kNR; ++r) { ptx::mbar_init(&raw_full[r], 1); ptx::mbar_init(&raw_empty[r], kConvWarps); }
-    for (int i = 0; i < kNI; ++i) { ptx::mbar_init(&img_full[i], kConvWarps); ptx::mbar_init(&img_empty[i], 1); }
+    for (int r = 0; r < kNR; ++r) { ptx::mbar_init(&raw_full[r], 1); ptx::mbar_init(&raw_empty[r], 4); }
+    for (int i = 0; i < kNI; ++i) { ptx::mbar_init(&img_full[i], 4); ptx::mbar_init(&img_empty[i], 1); }
     for (int e = 0; e < NBUF; ++e) { ptx::mbar_init(&acc_full[e], 1); ptx::mbar_init(&acc_empty[e], 4); }
     ptx::fence_mbar_init();
   }
@@ -136,10 +146,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
   const int grid = gridDim.x;
-  const int64_t n_tiles = SDBG(8) ? 0 : p.n_tiles;
+  const int n_tiles = SDBG(8) ? 0 : int(p.n_tiles);     // < 2^31 (stem_raw_plan)
   long long tw0 = 0, tw1 = 0;                             // experiment builds: cycles spent waiting
   const long long tstart = clock64();
-  (void)tstart;
+  (void)tstart; (void)tw0; (void)tw1;
 
   if (warp == kProducer) {
     // ===================== producer: resident weights, then raw rows per (tile, k) =====================
@@ -149,15 +159,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
       for (int off = 0; off < p.w_bytes; off += 32768)
         ptx::bulk_g2s(w_s + off, wsrc + off, uint32_t(std::min(32768, p.w_bytes - off)), w_full);
       const int rowbytes = p.W * p.Cin * 2;
-      int64_t j = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += grid) {
-        const int64_t b = tile / p.tiles_h;
-        const int r0 = int(tile % p.tiles_h) * p.TH * p.sh - p.ph;
+      Ring rr;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += grid) {
+        const int b = tile / p.tiles_h;
+        const int r0 = (tile - b * p.tiles_h) * p.TH * p.sh - p.ph;
         const int lo = max(0, -r0), hi = min(p.nraw, p.H - r0);
-        const __nv_bfloat16* fb = p.ring + b * p.frame_elems + int64_t(r0) * p.W * p.Cin;
-        for (int k = 0; k < p.kt; ++k, ++j) {
-          const int rb = int(j % kNR);
-          TWAIT(&raw_empty[rb], (uint32_t(j / kNR) & 1u) ^ 1u, tw0);
+        const __nv_bfloat16* fb = p.ring + int64_t(b) * p.frame_elems + int64_t(r0) * p.W * p.Cin;
+        for (int k = 0; k < p.kt; ++k, rr.next(kNR)) {
+          const int rb = rr.i;
+          TWAIT(&raw_empty[rb], rr.ph ^ 1u, tw0);
           if (hi <= lo || SDBG(4)) { ptx::mbar_arrive(&raw_full[rb]); continue; }
           // the tile's in-frame rows are contiguous in the frame: one bulk copy
           ptx::mbar_arrive_expect_tx(&raw_full[rb], uint32_t((hi - lo) * rowbytes));
@@ -167,16 +177,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
         }
       }
     }
-  } else if (warp >= 4 && warp < 4 + kConvWarps) {
+  } else if (warp >= kEpiWarps && warp < kEpiWarps + kExpWarps) {
     // ===================== expanders: raw rows -> channel-padded phase rows =====================
     // 16-B chunk t of image row q holds the SW pixels x = t SW + i - pw, CP channels
     // each.  Raw rows sit back to back in shared memory (one bulk copy) after pad
     // zero elements; a pixel outside the frame row is zeroed by a per-thread mask
     // (a thread keeps its column slot t).  Thread = (column slot t, row group):
-    // the rows of a thread's column are independent (unrolled).
-    constexpr int kConvThreads = 32 * kConvWarps;
-    const int ct = threadIdx.x - 128;
-    const int cols = p.Wp <= 64 ? 64 : 128, ngroups = kConvThreads / cols;
+    // the rows of a thread's column are independent (unrolled).  Group g (4 warps)
+    // builds images j = g, g + 2, ...
+    const int g = (warp - kEpiWarps) >> 2;
+    const int ct = threadIdx.x - 32 * kEpiWarps - 128 * g;
+    const int cols = p.Wp <= 64 ? 64 : 128, ngroups = 128 / cols;
     const int t = ct % cols, qg = ct / cols;
     const bool fast3 = SW == 2 && p.Cin == 3;              // RGB at stride 2: word loads + byte permutes
     // element of the first pixel of chunk t in a padded raw row, and its word / parity
@@ -185,13 +196,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
     bool pin[SW];                                           // pixel i of this column inside the frame row
 #pragma unroll
     for (int i = 0; i < SW; ++i) pin[i] = t * SW + i - p.pw >= 0 && t * SW + i - p.pw < p.W;
-    int64_t j = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += grid) {
-      const int r0 = int(tile % p.tiles_h) * p.TH * p.sh - p.ph;
-      for (int k = 0; k < p.kt; ++k, ++j) {
-        const int ib = int(j % kNI), rb = int(j % kNR);
-        TWAIT(&img_empty[ib], (uint32_t(j / kNI) & 1u) ^ 1u, tw0);   // the MMAs of image j - kNI are done
-        TWAIT(&raw_full[rb], uint32_t(j / kNR) & 1u, tw1);           // image j's raw rows landed
+    Ring ri, rr;                                         // image / raw-buffer position of image j
+    int j = 0;                                           // image index of (tile, k) in this CTA
+    for (int tile = blockIdx.x; tile < n_tiles; tile += grid) {
+      const int r0 = (tile % p.tiles_h) * p.TH * p.sh - p.ph;
+      for (int k = 0; k < p.kt; ++k, ++j, ri.next(kNI), rr.next(kNR)) {
+        if ((j & 1) != g) continue;
+        const int ib = ri.i, rb = rr.i;
+        TWAIT(&img_empty[ib], ri.ph ^ 1u, tw0);          // the MMAs of image j - kNI are done
+        TWAIT(&raw_full[rb], rr.ph, tw1);                // image j's raw rows landed
         uint4* im = reinterpret_cast<uint4*>(img + ib * p.img_bytes);
         const uint8_t* rw0 = raw + rb * p.raw_bytes;
         if (t < p.Wp && !SDBG(1)) {
@@ -268,17 +281,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
     ptx::tc_fence_after();
     const uint64_t bd0 = ptx::smem_desc(ptx::smem_u32(w_s), uint32_t(N * 16), 128);
     const uint64_t bstep = uint64_t(2 * N);               // one K16 step, 16-B units
-    int e = 0;
-    uint32_t eph = 0;
-    int64_t j = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += grid) {
-      TWAIT(&acc_empty[e], eph ^ 1u, tw0);
+    Ring re, ri;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += grid) {
+      const int e = re.i;
+      TWAIT(&acc_empty[e], re.ph ^ 1u, tw0);
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem + uint32_t(e * N);
       uint64_t bd = bd0;
-      for (int k = 0; k < p.kt; ++k, ++j) {
-        const int ib = int(j % kNI);
-        TWAIT(&img_full[ib], uint32_t(j / kNI) & 1u, tw1);
+      for (int k = 0; k < p.kt; ++k, ri.next(kNI)) {
+        const int ib = ri.i;
+        TWAIT(&img_full[ib], ri.ph, tw1);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           if constexpr (PER > 0) {
@@ -304,22 +316,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
         else ptx::tc_commit(&acc_full[e]);
       }
       __syncwarp();
-      if (++e == NBUF) { e = 0; eph ^= 1u; }
+      re.next(NBUF);
     }
-  } else if (warp < 4) {
+  } else if (warp < kEpiWarps) {
     // ===================== epilogue: y = acc + bias (ReLU), bf16 / fp32 =====================
-    const int m = warp * 32 + lane;                       // accumulator row = tile row slot
+    // group eg (4 warps) takes the CTA's tiles eg, eg + 2, ...: accumulators eg, eg + 2
+    const int eg = warp >> 2;
+    const int m = (warp & 3) * 32 + lane;                 // accumulator row = tile row slot
     const int r = m / p.Wp, wo = m - (m / p.Wp) * p.Wp;
-    int e = 0;
-    uint32_t eph = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += grid) {
-      const int64_t b = tile / p.tiles_h;
-      const int ho = int(tile % p.tiles_h) * p.TH + r;
+    Ring re;                                             // over this group's 2 accumulators
+    for (int tile = blockIdx.x + eg * grid; tile < n_tiles; tile += 2 * grid) {
+      const int b = tile / p.tiles_h;
+      const int ho = (tile - b * p.tiles_h) * p.TH + r;
       const bool valid = r < p.TH && wo < p.Wo && ho < p.Ho;
-      TWAIT(&acc_full[e], eph, tw0);
+      const int e = eg + 2 * re.i;
+      TWAIT(&acc_full[e], re.ph, tw0);
       ptx::tc_fence_after();
-      const uint32_t t_row = tmem + (uint32_t(warp * 32) << 16) + uint32_t(e * N);
-      const int64_t yoff = b * p.y_bstride + (int64_t(ho) * p.Wo + wo) * p.Cout;
+      const uint32_t t_row = tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(e * N);
+      const int64_t yoff = int64_t(b) * p.y_bstride + (int64_t(ho) * p.Wo + wo) * p.Cout;
 #pragma unroll 1
       for (int c = 0; c < N; c += 16) {
         float v[16] = {};
@@ -361,11 +375,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_relaxed(&acc_empty[e]);
-      if (++e == NBUF) { e = 0; eph ^= 1u; }
+      re.next(2);
     }
   }
 #ifdef CO_EXPERIMENTS
-  if (SDBG(512) && blockIdx.x < 2 && lane == 0 && (warp == 0 || warp == 4 || warp == kProducer || warp == kMma))
+  if (SDBG(512) && blockIdx.x < 2 && lane == 0 && (warp == 0 || warp == kEpiWarps || warp == kProducer || warp == kMma))
     printf("cta %d warp %2d total %lld wait0 %lld wait1 %lld\n", blockIdx.x, warp, clock64() - tstart, tw0, tw1);
 #endif
   ptx::tc_fence_before();
@@ -426,6 +440,7 @@ bool stem_raw_plan(const Geom& g, StemRawPlan& sp) {
   sp.TH = 128 / sp.Wp;
   sp.tiles_h = (g.Ho + sp.TH - 1) / sp.TH;
   sp.n_tiles = g.B * sp.tiles_h;
+  if (sp.n_tiles >= (int64_t(1) << 31)) return false;
   const int sh = g.sh;
   sp.nraw = (sp.TH - 1) * sh + g.kh;
   int rows = 0;

@@ -196,7 +196,7 @@ RAW_STEM = {
     "cin4_st2_dil2": dict(desc=O.Desc(2, 4, 32, (3, 5, 5), stride=(2, 1, 2), padding=(1, 2, 2),
                                       dilation=(2, 1, 1), in_spatial=(11, 14)), B=2),
     "cin1_k2": dict(desc=O.Desc(2, 1, 64, (2, 3, 3), padding=(0, 1, 1), in_spatial=(10, 24)), B=4),
-    "cin2_ph0": dict(desc=O.Desc(2, 2, 32, (4, 3, 8), stride=(1, 2, 1), padding=(0, 0, 0), in_spatial=(13, 24)), B=2),
+    "cin2_ph0": dict(desc=O.Desc(2, 2, 32, (4, 3, 4), stride=(1, 2, 1), padding=(0, 0, 0), in_spatial=(13, 24)), B=2),
 }
 
 
