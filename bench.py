@@ -645,6 +645,12 @@ def run_all(args, world, rank):
                 head["e2e"] = run_e2e(args, *ctx[:5], world)
             if rank == 0 and world == 1 and not args.no_cpu_baseline:
                 head["cpu_baseline"] = cpu_baseline(cfg)
+        if cid == 4 and args.config == "all" and args.state == "config":
+            # C4's companion: the planner's layout per layer (CO_STATE_AUTO), i.e. the RGB stem
+            # over the RAW frame ring (k_step_stem_raw), the rest on fp32 partial sums
+            e2, _ = run_config(cfg, args, world, rank, label=cfg.workload + " [planner layouts: RAW-ring stem]",
+                               state="auto")
+            configs["C4/auto"] = e2
         if cid == 5 and args.config == "all" and args.state == "config" and entry["state"] != ["psum"]:
             # C5's companion: the fp32 partial-sum layout against its own roofline
             e2, _ = run_config(cfg, args, world, rank, label=cfg.workload + " [fp32 partial-sum state]",
