@@ -148,7 +148,11 @@ typedef struct {
 
 /* ---- lifetime ------------------------------------------------------------ */
 
-/* Create a layer.  `weights` (Cout, Cin/g, kt, kh, kw) in w_dtype and `bias`
+/* Create a layer: the co.Conv constructor of Listing 1 with the
+ * nn.Conv arguments it extends (Principle 1: identical / extended
+ * constructors, identical weights -- the (Cout, Cin/g, kt, kh, kw) tensor of
+ * nn.Conv3d, so a regular layer's state_dict loads unchanged).
+ * `weights` (Cout, Cin/g, kt, kh, kw) in w_dtype and `bias`
  * (Cout, fp32, may be NULL) are host pointers if weights_on_device == 0, else
  * device pointers; both are copied and repacked, so the caller may free them on
  * return.  The fp32 state (R slots x B x S1' x S2' x Cout) is allocated and
@@ -156,7 +160,8 @@ typedef struct {
  * CO_ERR_CUDA.  Synchronises the current device once (setup, not the hot path). */
 int co_conv_create(const co_conv_desc* desc, const void* weights, const float* bias,
                    int weights_on_device, co_conv** out);
-int co_conv_destroy(co_conv* h);                      /* frees weights, state, clock; NULL ok */
+int co_conv_destroy(co_conv* h);                      /* frees weights, state, clock; NULL ok (no paper
+                                                         passage: the C ABI's ownership rule) */
 int co_conv_info(const co_conv* h, co_info* info);    /* host, final on return */
 int co_delay(const co_conv* h, int64_t* delay);       /* d = f - p - 1 */
 const char* co_kernel_name(const co_conv* h);         /* name of the dispatched step kernel */
@@ -218,6 +223,9 @@ int co_forward_out_len(const co_conv* h, int64_t T, int64_t* T_out);
  * padding is zero).  `bytes` must equal co_state_bytes().  get fills *meta with the clock; set restores the
  * clock from *meta (its geometry fields must match: CO_ERR_SHAPE).  A get ->
  * set round trip is bitwise (checkpoint / resume). */
+/* co_state_bytes: the size of the module's internal state (the buffers P:110-116
+ * step, clean with clean_state() and skip with update_state=False) in the
+ * canonical layout above. */
 int co_state_bytes(const co_conv* h, size_t* bytes);
 int co_state_get(co_conv* h, void* dst, size_t bytes, co_info* meta, co_stream stream);
 int co_state_set(co_conv* h, const void* src, size_t bytes, const co_info* meta, co_stream stream);
@@ -437,7 +445,7 @@ int co_get_option(const char* name, int64_t* value);
 const char* co_option_name(int index);
 
 /* ---- misc ------------------------------------------------------------------ */
-const char* co_last_error(void);
+const char* co_last_error(void);   /* no paper passage: the ABI's error channel (conventions above) */
 int co_abi_version(void);
 
 #ifdef __cplusplus

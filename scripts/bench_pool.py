@@ -125,7 +125,14 @@ def main():
     ap.add_argument("--workload", default="all", choices=["all"] + list(WORKLOADS))
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
+                    help="documented planner option (co.set_option), e.g. pool_g=4")
     a = ap.parse_args()
+    if a.option:
+        import paper_2204_03418_b200 as co
+        for kv in a.option:
+            k, v = kv.split("=", 1)
+            co.set_option(k, int(v))
     for name in (WORKLOADS if a.workload == "all" else [a.workload]):
         run(name, a.steps, a.warmup)
 
