@@ -18,13 +18,15 @@ CASES="1 0 psum k_step_direct 3
 4 3 psum k_step_dense_tc 3
 4 4 psum k_step_dense_tc 3
 5 0 psum k_step_dense_tc 17
-5 0 raw k_step_dense_tc 1"
+5 0 raw k_step_dense_tc 1
+4 0 raw k_step_stem_raw 1"
 echo "$CASES" | while read C L S K N; do
   suf=""; [ "$S" = raw ] && suf="_raw"
   out=gpurun_out/${TAG}_c${C}l${L}${suf}
-  python scripts/layer_probe.py --config $C --layer $L --state $S --steps 3 > $out.plain.log 2>&1 || { echo "plain run failed: $C $L $S"; continue; }
+  st=$S; [ "$K" = k_step_stem_raw ] && st=auto           # the planner's RAW stem (other layers PSUM)
+  python scripts/layer_probe.py --config $C --layer $L --state $st --steps 3 > $out.plain.log 2>&1 || { echo "plain run failed: $C $L $S"; continue; }
   ncu --set full --clock-control none --import-source on -k regex:$K -s $N -c 1 -o $out \
-      python scripts/layer_probe.py --config $C --layer $L --state $S --steps 3 > $out.ncu.log 2>&1
+      python scripts/layer_probe.py --config $C --layer $L --state $st --steps 3 > $out.ncu.log 2>&1
   rc=$?
   # the raw metrics page travels back (the full reports would pass gpurun's 64 MiB limit);
   # reports named in KEEP stay whole for source-level reading
