@@ -179,6 +179,23 @@ __device__ __forceinline__ float4 ld_state_na(const float4* p) {
   return v;
 }
 
+// state store: st.global.cs (streaming); experiment builds can A/B other flavours
+// (CO_TC_DEBUG 2048: plain st.global, 4096: L1::no_allocate, 8192: .wt)
+template <typename P>
+__device__ __forceinline__ void st_state(const P& p, float4* dst, float4 v) {
+#ifdef CO_EXPERIMENTS
+  if (p.dbg & 2048) { *dst = v; return; }
+  if (p.dbg & 4096) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w) : "memory");
+    return;
+  }
+  if (p.dbg & 8192) { __stwt(dst, v); return; }
+#endif
+  (void)p;
+  __stcs(dst, v);
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -1010,7 +1027,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
               for (int i = 0; i < 4; ++i) {
                 float4 t4 = sv[k][c / 4 + i];
                 t4.x += v[4 * i]; t4.y += v[4 * i + 1]; t4.z += v[4 * i + 2]; t4.w += v[4 * i + 3];
-                if (!DBG(128)) __stcs(dst + (c / 4 + i) * 128, t4);
+                if (!DBG(128)) st_state(p, dst + (c / 4 + i) * 128, t4);
               }
             }
           }
@@ -1026,7 +1043,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
             if (valid && !DBG(1)) {
 #pragma unroll
               for (int i = 0; i < 4; ++i)
-                if (!DBG(128)) __stcs(dst + (c / 4 + i) * 128, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+                if (!DBG(128)) st_state(p, dst + (c / 4 + i) * 128, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
             }
           }
         }

@@ -13,7 +13,7 @@ import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def _layers(specs, B, seed, out_last=torch.float32):
+def _layers(specs, B, seed, out_last=torch.float32, layouts=None):
     import paper_2204_03418_b200 as co
     rng = np.random.default_rng(seed)
     convs, spat = [], None
@@ -25,9 +25,12 @@ def _layers(specs, B, seed, out_last=torch.float32):
         convs.append(co.Conv(cin, cout, k, weight=Wt.cuda(), bias=bt.cuda(), stride=s, padding=p, dilation=dil,
                              groups=g, spatial_rank=2, in_spatial=(H, W),
                              n_streams=B, dtype=torch.bfloat16, out_dtype=out_last if last else torch.bfloat16,
-                             activation=None if last else "relu"))
+                             activation=None if last else "relu",
+                             state_layout=layouts[l] if layouts else "psum"))
     return convs
 
+
+LAYOUTS = {"rawstem_khalo": ["auto", "psum"]}
 
 STACKS = {
     # C2-shaped dense HALO pair -> depthwise temporal (the C3-b kernel): rings 2 and 4
@@ -36,6 +39,9 @@ STACKS = {
     # C4 stem (W-im2col KLOOP) -> a strided KHALO layer
     "stem_khalo": ([(3, 64, (5, 7, 7), (1, 2, 2), (0, 3, 3), 1, (1, 1, 1), 20, 22),
                     (64, 128, (3, 3, 3), (1, 2, 2), (0, 1, 1), 1, (1, 1, 1), 10, 11)], 2),
+    # the C4 stem over the planner's RAW frame ring (k_step_stem_raw) -> a strided KHALO layer
+    "rawstem_khalo": ([(3, 64, (5, 7, 7), (1, 2, 2), (0, 3, 3), 1, (1, 1, 1), 20, 24),
+                       (64, 128, (3, 3, 3), (1, 2, 2), (0, 1, 1), 1, (1, 1, 1), 10, 12)], 2),
     # C5-shaped FLAT pair, kt 9, dilation 2 (16 ring slots in two phase rings)
     "flat_c5": ([(256, 256, (9, 1, 1), (1, 1, 1), (0, 0, 0), 1, (2, 1, 1), 25, 1)], 8),
     # temporal stride 2 then a dense layer (Empty ticks inside the graph)
@@ -59,8 +65,10 @@ def test_graph_replay_equals_eager_fold(name):
     bitwise equal."""
     import paper_2204_03418_b200 as co
     specs, B = STACKS[name]
-    A = co.Stack(_layers(specs, B, 7))
-    Bs = co.Stack(_layers(specs, B, 7))
+    A = co.Stack(_layers(specs, B, 7, layouts=LAYOUTS.get(name)))
+    Bs = co.Stack(_layers(specs, B, 7, layouts=LAYOUTS.get(name)))
+    if name == "rawstem_khalo":
+        assert "stem_raw" in A.layers[0].kernel_name, A.layers[0].kernel_name
     cin, H, W = specs[0][0], specs[0][7], specs[0][8]
     warm = max(c.receptive_field + c.info().padding_t for c in A.layers) * 3 + 8
     P = A.graph_period

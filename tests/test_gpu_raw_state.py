@@ -275,3 +275,106 @@ def test_raw_stem_auto_layout_and_zero_frames():
         if y is not None:
             ys.append(np_of(y)); refs.append(r.reshape(y.shape))
     assert rel_err(np.stack(ys), np.stack(refs)) <= 1e-4
+
+
+def _stem_desc(rng):
+    """A random shape k_step_stem_raw covers: Cin <= 8 / sw, kw (8 / sw) <= 32,
+    spatial strides <= 2, 16-B raw rows, Cout 32 or 64."""
+    sw = int(rng.integers(1, 3))
+    cp = 8 // sw
+    cin = int(rng.integers(1, cp + 1))
+    kw = int(rng.integers(1, 32 // cp + 1))
+    kh = int(rng.integers(1, 8))
+    sh = int(rng.integers(1, 3))
+    kt = int(rng.integers(1, 6))
+    dil = int(rng.integers(1, 3))
+    f = dil * (kt - 1) + 1
+    pt = int(rng.integers(0, f))
+    st = int(rng.integers(1, 3))
+    ph, pw = int(rng.integers(0, kh // 2 + 1)), int(rng.integers(0, kw // 2 + 1))
+    unit = 8 // np.gcd(8, cin)                       # W Cin * 2 bytes a multiple of 16
+    W = unit * int(rng.integers(max(1, -(-kw // unit)), 48 // unit + 2))
+    H = int(rng.integers(max(kh - 2 * ph, 1), 20))
+    cout = int(rng.choice([32, 64]))
+    return O.Desc(2, cin, cout, (kt, kh, kw), stride=(st, sh, sw), padding=(pt, ph, pw), dilation=(dil, 1, 1),
+                  in_spatial=(H, W))
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_raw_stem_random_shapes_vs_oracle(seed):
+    """Random small-Cin shapes on the RAW-ring stem kernel (strides, paddings,
+    odd kernels, temporal stride / dilation / padding, ragged tiles) against the
+    fp64 oracle over the delay and several Ready ticks; the ring is the oracle's
+    history bit for bit."""
+    rng = np.random.default_rng(5000 + seed)
+    d = _stem_desc(rng)
+    while not d.valid():
+        d = _stem_desc(rng)
+    B = int(rng.integers(1, 4))
+    W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
+    b = rng.standard_normal(d.cout) * 0.1
+    conv, sm, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="dense_tc", state_layout="raw")
+    assert "stem_raw" in conv.kernel_name, (conv.kernel_name, d)
+    ys, refs = [], []
+    for t in range(d.receptive_field + 3 * d.stride[0] + 2):
+        xt = to_cl(rng.standard_normal(_shape(d, B)), torch.bfloat16)
+        y = conv.forward_step(xt)
+        r = sm.forward_step(np_of(xt))
+        assert (y is None) == (r is None)
+        assert (conv.n, conv.head) == (sm.n, sm.head)
+        if y is not None:
+            ys.append(np_of(y)); refs.append(r.reshape(y.shape))
+    if ys:
+        assert rel_err(np.stack(ys), np.stack(refs)) <= 1e-4, d
+    st, _ = conv.state_dict_stream()
+    if d.receptive_field > 1:
+        assert np.array_equal(_canon_to_oracle(st, d, B), sm.history())
+
+
+def test_raw_stem_state_probe_fold_and_batch():
+    """The RAW stem handle's contract beyond single steps: a get -> set round
+    trip continues bitwise, an update_state = False probe leaves the ring
+    untouched, forward_steps equals the per-step fold bit for bit, and the
+    batch forward matches the step outputs."""
+    import paper_2204_03418_b200 as co
+    d = O.Desc(2, 3, 64, (5, 7, 7), stride=(1, 2, 2), padding=(2, 3, 3), in_spatial=(26, 40))
+    B = 2
+    rng = np.random.default_rng(5100)
+    W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
+    b = rng.standard_normal(d.cout) * 0.1
+    a, sm, Wq, bq = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="dense_tc", state_layout="raw")
+    c, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="dense_tc", state_layout="raw")
+    assert "stem_raw" in a.kernel_name
+    frames = [to_cl(rng.standard_normal(_shape(d, B)), torch.bfloat16) for _ in range(12)]
+    for x in frames[:6]:
+        a.forward_step(x); c.forward_step(x)
+    st, meta = a.state_dict_stream()
+    # probe: same output as a real step, state unchanged
+    yp = a.forward_step(frames[6], update_state=False)
+    st2, _ = a.state_dict_stream()
+    assert torch.equal(st, st2)
+    # round trip into a fresh handle continues bit for bit
+    e, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="dense_tc", state_layout="raw")
+    e.load_state_stream(st, meta)
+    for x in frames[6:]:
+        ya, ye = a.forward_step(x), e.forward_step(x)
+        assert (ya is None) == (ye is None)
+        if ya is not None:
+            assert torch.equal(ya, ye)
+    if yp is not None:
+        ya6 = c.forward_step(frames[6])
+        assert torch.equal(yp, ya6)
+    # forward_steps over a clip == the per-step fold (same kernel, same order)
+    f1, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="dense_tc", state_layout="raw")
+    f2, _, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="dense_tc", state_layout="raw")
+    clip = torch.stack(frames, dim=2)
+    ys, mask = f1.forward_steps(co.channels_last(clip), pad_end=True)
+    fold = [y for y in (f2.forward_step(x) for x in frames) if y is not None]
+    fold += [y for y in (f2.forward_pad_step() for _ in range(d.padding[0])) if y is not None]
+    assert ys.shape[2] == len(fold) == int(mask.sum())
+    for i, y in enumerate(fold):
+        assert torch.equal(ys[:, :, i], y)
+    # batch mode (the generic kernel) against the oracle's batch forward
+    clip_np = np.stack([np_of(x) for x in frames], axis=2)
+    yb = f1.forward(co.channels_last(clip))
+    assert rel_err(np_of(yb), O.forward(d, Wq, bq, clip_np)) <= 1e-4
