@@ -28,14 +28,22 @@
 //  * The B operand (all packed weights, [K/8][N][16 B]) stays resident in
 //    shared memory for the launch: the K loop streams only raw input rows.
 //  * Per (tile, temporal tap k) the producer bulk-copies the (TH-1) sh + kh raw
-//    rows of ring slot slot[k] the tile needs (C4: 9 rows of 672 B) and 8
-//    expander warps pad them (3 -> 4 channels, zero halo / padding) into an
-//    image of the ring; the MMA warp issues kh * Kp / 16 MMAs per image from a
-//    descriptor table built once.
-//  * Warp roles: warps 0-3 epilogue (TMEM lane quadrant w: y = acc + bias,
-//    ReLU, bf16 / fp32 stores), warps 4-11 expanders, warp 12 producer,
-//    warp 13 MMA issuer / TMEM owner.  Images, raw-row buffers and TMEM
-//    accumulators are rings with full / empty mbarriers.
+//    rows of ring slot slot[k] the tile needs (C4: 9 rows of 672 B, ONE copy:
+//    they are contiguous in the frame) and an expander group pads them (3 -> 4
+//    channels, zero halo / padding) into an image of the ring; the MMA warp
+//    issues kh * Kp / 16 MMAs per image from a descriptor table built once.
+//  * CTA pairs (cta_group::2): each CTA builds the images of its own 128-row
+//    tile and holds half of the weight rows; the leader issues M = 256 MMAs
+//    over both -- at N = 64 an MMA instruction, not its MACs, sets the pace
+//    (scripts/mma_probe.cu: ~44 cycles for 256 rows on a pair, ~49 for 128 on
+//    one CTA).  The peer's images reach the leader through ONE cluster-scope
+//    release per tile (a relay in the peer's idle MMA warp; a cluster-scope
+//    release costs a GPU-wide membar), the image ring holding two tiles.
+//  * Warp roles (26 warps): 0-7 epilogue (two groups taking alternate tiles:
+//    y = acc + bias, ReLU, bf16 / fp32 stores), 8-23 expanders (four groups,
+//    images round-robin), 24 producer, 25 MMA issuer (leader) / relay (peer) /
+//    TMEM owner.  Images, raw-row buffers and TMEM accumulators are rings with
+//    full / empty mbarriers.
 #include <algorithm>
 #include <cstdio>
 
@@ -45,10 +53,11 @@
 namespace co {
 namespace {
 
-constexpr int kNI = 4;           // image ring
+constexpr int kNI = 10;          // image ring: two tiles of kt <= 5 images in flight (the pair relays per tile)
 constexpr int kNR = 4;           // raw-row ring
 constexpr int kEpiWarps = 8;     // two epilogue groups of 4 warps (alternate tiles)
-constexpr int kExpWarps = 8;     // two expander groups of 4 warps (alternate images)
+constexpr int kExpGroups = 4;    // expander groups of 4 warps (images round-robin)
+constexpr int kExpWarps = 4 * kExpGroups;
 constexpr int kThreads = 32 * (kEpiWarps + kExpWarps + 2);
 constexpr int kProducer = kEpiWarps + kExpWarps, kMma = kProducer + 1;
 constexpr size_t kSmemLimit = 227 * 1024;
@@ -67,11 +76,10 @@ struct SrParams {
   void* y;
   int64_t y_bstride;
   int out_f32, act;
-  const __nv_bfloat16* wpack;
+  const __nv_bfloat16* wpack;    // [PAIR][K/8][N/PAIR][8]: CTA rank r's half of the weight rows
   const float* bias;
   int dbg;                       // experiment builds only: 1 no expansion, 2 no MMAs, 4 no raw loads, 8 no work,
-                                 // 64 no y stores, 128 no epilogue TMEM reads, 256 (with 2) arrive, not commit,
-                                 // 512 print per-role wait cycles
+                                 // 64 no y stores, 128 no epilogue TMEM reads, 512 print per-role wait cycles
 };
 #ifdef CO_EXPERIMENTS
 #define SDBG(bits) (p.dbg & (bits))
@@ -101,11 +109,17 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 }
 
 // PER > 0: compile-time MMAs per image (kh Kp / 16; C4's stem: 7 x 2), the
-// image's A descriptors held in registers and the issue loop unrolled
-template <int N, int SW, int PER>
+// image's A descriptors held in registers and the issue loop unrolled.
+// PAIR = 2: a CTA pair (cluster of 2, cta_group::2) -- each CTA builds the image
+// of its own 128-row tile and holds half of the weight rows; the leader issues
+// M = 256 MMAs over both.  At N = 64 an MMA instruction costs ~44 cycles for 256
+// rows on a pair against ~49 for 128 rows on one CTA (scripts/mma_probe.cu): a
+// small-N contraction is bound by MMA instructions, not by MACs.
+template <int N, int SW, int PER, int PAIR>
 __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_constant__ SrParams p) {
   constexpr int NBUF = 4;                              // TMEM accumulators: 2 per epilogue group
   constexpr int CP = 8 / SW;                            // padded channels per pixel (16 / SW bytes)
+  constexpr int NB = N / PAIR;                          // weight rows held by this CTA
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* w_s = smem;
@@ -114,23 +128,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
   float* bias_s = reinterpret_cast<float*>(smem + p.bias_off);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
   uint64_t* w_full = bars;
-  uint64_t* raw_full = bars + 1;
+  uint64_t* w_peer = bars + 1;                          // PAIR: the peer's weight half landed (leader)
+  uint64_t* raw_full = bars + 2;
   uint64_t* raw_empty = raw_full + kNR;
-  uint64_t* img_full = raw_empty + kNR;
+  uint64_t* img_full = raw_empty + kNR;                 // PAIR: the leader's copy collects both CTAs
   uint64_t* img_empty = img_full + kNI;
   uint64_t* acc_full = img_empty + kNI;
-  uint64_t* acc_empty = acc_full + NBUF;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + NBUF);
+  uint64_t* acc_empty = acc_full + NBUF;                // PAIR: the leader's copy collects both CTAs
+  uint64_t* peer_tile = acc_empty + NBUF;               // PAIR leader: [2] the peer's images of tile T built
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(peer_tile + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR == 2 ? ptx::cluster_ctarank() : 0u;   // (before the barrier init: it uses rank)
+  const bool leader = rank == 0;
+  // arrive on the leader CTA's copy of a barrier (the pair's MMA issuer waits there)
+  auto arrive_leader = [&](uint64_t* bar) {
+    if constexpr (PAIR == 2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(bar), 0));
+    else ptx::mbar_arrive(bar);
+  };
   if (warp == kProducer && lane == 0) {
     ptx::mbar_init(w_full, 1);
+    ptx::mbar_init(w_peer, 1);
     for (int r = 0; r < kNR; ++r) { ptx::mbar_init(&raw_full[r], 1); ptx::mbar_init(&raw_empty[r], 4); }
+    // img_full: the CTA's 4 expander warps of the image (CTA-scope arrivals);
+    // peer_tile: on a pair leader, the peer's relay -- one cluster-scope arrival
+    // per tile once all of the peer's images of the tile are built
     for (int i = 0; i < kNI; ++i) { ptx::mbar_init(&img_full[i], 4); ptx::mbar_init(&img_empty[i], 1); }
-    for (int e = 0; e < NBUF; ++e) { ptx::mbar_init(&acc_full[e], 1); ptx::mbar_init(&acc_empty[e], 4); }
+    for (int i = 0; i < 2; ++i) ptx::mbar_init(&peer_tile[i], 1);
+    for (int e = 0; e < NBUF; ++e) { ptx::mbar_init(&acc_full[e], 1); ptx::mbar_init(&acc_empty[e], 4 * PAIR); }
     ptx::fence_mbar_init();
   }
-  if (warp == kMma) ptx::tmem_alloc(tmem_holder, 512);
+  if (warp == kMma) {
+    if constexpr (PAIR == 2) ptx::tmem_alloc_pair(tmem_holder, 512);
+    else ptx::tmem_alloc(tmem_holder, 512);
+  }
   for (int i = threadIdx.x; i < N; i += blockDim.x) bias_s[i] = p.bias[i];
   // zero the images once: their slack past the last row is read (times zero
   // weights, or by junk rows) and must hold finite values
@@ -142,11 +173,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
     reinterpret_cast<uint4*>(raw)[i] = make_uint4(0u, 0u, 0u, 0u);
   ptx::fence_proxy_async();
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR == 2) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  const int grid = gridDim.x;
+  // work units: a CTA (PAIR 1) or a pair; unit u's T-th tile pair is u + T n_units,
+  // and CTA `rank` of the unit takes tile (u + T n_units) PAIR + rank (the peer of
+  // an odd last tile runs a dummy: no rows, no stores, same barriers)
+  const int n_units = gridDim.x / PAIR, unit = blockIdx.x / PAIR;
   const int n_tiles = SDBG(8) ? 0 : int(p.n_tiles);     // < 2^31 (stem_raw_plan)
+  const int n_groups = (n_tiles + PAIR - 1) / PAIR;     // tile pairs
+  auto tile_of = [&](int T) { return (unit + T * n_units) * PAIR + int(rank); };
+  auto has = [&](int T) { return unit + T * n_units < n_groups; };
   long long tw0 = 0, tw1 = 0;                             // experiment builds: cycles spent waiting
   const long long tstart = clock64();
   (void)tstart; (void)tw0; (void)tw1;
@@ -154,16 +191,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
   if (warp == kProducer) {
     // ===================== producer: resident weights, then raw rows per (tile, k) =====================
     if (lane == 0) {
-      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wpack);
+      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wpack) + size_t(rank) * p.w_bytes;
       ptx::mbar_arrive_expect_tx(w_full, uint32_t(p.w_bytes));
       for (int off = 0; off < p.w_bytes; off += 32768)
         ptx::bulk_g2s(w_s + off, wsrc + off, uint32_t(std::min(32768, p.w_bytes - off)), w_full);
+      if (PAIR == 2 && !leader) {                        // tell the leader this half landed
+        ptx::mbar_wait(w_full, 0);
+        arrive_leader(w_peer);
+      }
       const int rowbytes = p.W * p.Cin * 2;
       Ring rr;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += grid) {
+      for (int T = 0; has(T); ++T) {
+        const int tile = tile_of(T);
         const int b = tile / p.tiles_h;
         const int r0 = (tile - b * p.tiles_h) * p.TH * p.sh - p.ph;
-        const int lo = max(0, -r0), hi = min(p.nraw, p.H - r0);
+        const int lo = max(0, -r0), hi = tile < n_tiles ? min(p.nraw, p.H - r0) : 0;
         const __nv_bfloat16* fb = p.ring + int64_t(b) * p.frame_elems + int64_t(r0) * p.W * p.Cin;
         for (int k = 0; k < p.kt; ++k, rr.next(kNR)) {
           const int rb = rr.i;
@@ -184,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
     // zero elements; a pixel outside the frame row is zeroed by a per-thread mask
     // (a thread keeps its column slot t).  Thread = (column slot t, row group):
     // the rows of a thread's column are independent (unrolled).  Group g (4 warps)
-    // builds images j = g, g + 2, ...
+    // builds images j = g, g + kExpGroups, ...
     const int g = (warp - kEpiWarps) >> 2;
     const int ct = threadIdx.x - 32 * kEpiWarps - 128 * g;
     const int cols = p.Wp <= 64 ? 64 : 128, ngroups = 128 / cols;
@@ -198,10 +240,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
     for (int i = 0; i < SW; ++i) pin[i] = t * SW + i - p.pw >= 0 && t * SW + i - p.pw < p.W;
     Ring ri, rr;                                         // image / raw-buffer position of image j
     int j = 0;                                           // image index of (tile, k) in this CTA
-    for (int tile = blockIdx.x; tile < n_tiles; tile += grid) {
+    for (int T = 0; has(T); ++T) {
+      const int tile = tile_of(T);
       const int r0 = (tile % p.tiles_h) * p.TH * p.sh - p.ph;
+      const bool real = tile < n_tiles;
       for (int k = 0; k < p.kt; ++k, ++j, ri.next(kNI), rr.next(kNR)) {
-        if ((j & 1) != g) continue;
+        if (j % kExpGroups != g) continue;
         const int ib = ri.i, rb = rr.i;
         TWAIT(&img_empty[ib], ri.ph ^ 1u, tw0);          // the MMAs of image j - kNI are done
         TWAIT(&raw_full[rb], rr.ph, tw1);                // image j's raw rows landed
@@ -213,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
             const bool odd = p.sh == 2 && (q & 1);
             const int row = (odd ? p.base1 : p.base0) + (p.sh == 2 ? (q >> 1) : q) * p.Wp + t;
             uint4 o = make_uint4(0u, 0u, 0u, 0u);
-            if (r0 + q >= 0 && r0 + q < p.H) {
+            if (real && r0 + q >= 0 && r0 + q < p.H) {
               if (fast3) {
                 // pixels a, b = 6 elements from e0: 4 words from the even boundary, then
                 // (a0 a1) (a2 0) (b0 b1) (b2 0)
@@ -226,14 +270,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
                 o = make_uint4(pin[0] ? v0 : 0u, pin[0] ? (v1 & 0xFFFFu) : 0u,
                                pin[SW - 1] ? __byte_perm(v1, v2, 0x5432) : 0u, pin[SW - 1] ? (v2 >> 16) : 0u);
               } else {
-                const uint16_t* rr = reinterpret_cast<const uint16_t*>(rw0) + e0 + q * rowel;
+                const uint16_t* rr16 = reinterpret_cast<const uint16_t*>(rw0) + e0 + q * rowel;
                 uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
                 for (int i = 0; i < SW; ++i)
 #pragma unroll
                   for (int c = 0; c < CP; ++c)
                     if (c < p.Cin && pin[i]) {
-                      const uint32_t h = rr[i * p.Cin + c];
+                      const uint32_t h = rr16[i * p.Cin + c];
                       const int e = i * CP + c;                 // element of the 16-B chunk
                       w[e >> 1] |= (e & 1) ? (h << 16) : h;
                     }
@@ -247,18 +291,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
         __syncwarp();                                     // the warp's writes and fences, then one arrival
         if (lane == 0) {
           ptx::mbar_arrive(&raw_empty[rb]);
-          ptx::mbar_arrive(&img_full[ib]);
+          ptx::mbar_arrive(&img_full[ib]);              // CTA scope (a cluster-scope release costs a GPU membar)
         }
       }
     }
   } else if (warp == kMma) {
-    // ===================== MMA issuer =====================
+    // ===================== MMA issuer (the leader CTA of a pair) =====================
     // The A descriptors of every (image buffer, row tap, K16 step) are built once
     // into a shared table (runtime-divisor math in the issue loop would make the
     // single issuing thread, not the tensor core, the bottleneck); B advances by
-    // one K16 step (2 K groups x N rows x 16 B) per MMA.  A: row stride 16 B,
+    // one K16 step (2 K groups x NB rows x 16 B) per MMA.  A: row stride 16 B,
     // LBO 16 B (the next K group is the next 8 channels of the same row), SBO 128 B.
-    constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, N);
+    // A pair MMA reads the same shared offsets in both CTAs: each its own image
+    // (its 128 rows) and its half of the weight rows.
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(128 * PAIR, N);
     const int nk = p.Kp / 16;                             // MMAs (K = 16) per row tap
     const int per_img = p.kh * nk;
     uint64_t* atab = reinterpret_cast<uint64_t*>(smem + p.tab_off);
@@ -277,58 +323,80 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
       for (int i = 0; i < PER; ++i) a0[i] = atab[i];      // image buffer 0
     }
     (void)a0;
-    ptx::mbar_wait(w_full, 0);
-    ptx::tc_fence_after();
-    const uint64_t bd0 = ptx::smem_desc(ptx::smem_u32(w_s), uint32_t(N * 16), 128);
-    const uint64_t bstep = uint64_t(2 * N);               // one K16 step, 16-B units
-    Ring re, ri;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += grid) {
-      const int e = re.i;
-      TWAIT(&acc_empty[e], re.ph ^ 1u, tw0);
-      ptx::tc_fence_after();
-      const uint32_t d_tmem = tmem + uint32_t(e * N);
-      uint64_t bd = bd0;
-      for (int k = 0; k < p.kt; ++k, ri.next(kNI)) {
-        const int ib = ri.i;
-        TWAIT(&img_full[ib], ri.ph, tw1);
-        ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          if constexpr (PER > 0) {
-            const uint64_t off = uint64_t(ib) * uint64_t(p.img_bytes >> 4);   // start-address field only
-#pragma unroll
-            for (int i = 0; i < PER; ++i)
-              if (!SDBG(2)) ptx::mma_bf16_ss(d_tmem, a0[i] + off, bd + uint64_t(i) * bstep, idesc, (k | i) ? 1u : 0u);
-          } else {
-            const uint64_t* at = atab + ib * per_img;
-#pragma unroll 2
-            for (int i = 0; i < per_img; ++i) {
-              if (!SDBG(2)) ptx::mma_bf16_ss(d_tmem, at[i], bd + uint64_t(i) * bstep, idesc, (k | i) ? 1u : 0u);
-            }
-          }
-          if (SDBG(256)) ptx::mbar_arrive(&img_empty[ib]);   // experiment (with bit 2): no commit latency
-          else ptx::tc_commit(&img_empty[ib]);            // image free once these MMAs completed
-        }
+    if (PAIR == 2 && !leader) {
+      // relay: once all of this CTA's images of tile T are built (its expanders'
+      // CTA-scope releases, acquired here), ONE cluster-scope release on the
+      // leader's peer_tile[T mod 2] carries them (cumulativity) to the leader's
+      // MMAs, which read them -- a cluster-scope release costs a GPU-wide membar,
+      // so once per tile, not per image (the image ring holds two tiles)
+      Ring ri;
+      for (int T = 0; has(T); ++T) {
+        for (int k = 0; k < p.kt; ++k, ri.next(kNI)) ptx::mbar_wait(&img_full[ri.i], ri.ph);
+        if (lane == 0) arrive_leader(&peer_tile[T & 1]);
         __syncwarp();
-        bd += uint64_t(per_img) * bstep;
       }
-      if (ptx::elect_one()) {
-        if (SDBG(256)) ptx::mbar_arrive(&acc_full[e]);
-        else ptx::tc_commit(&acc_full[e]);
+    }
+    if (leader) {
+      ptx::mbar_wait(w_full, 0);
+      if constexpr (PAIR == 2) ptx::mbar_wait_cluster(w_peer, 0);
+      ptx::tc_fence_after();
+      const uint64_t bd0 = ptx::smem_desc(ptx::smem_u32(w_s), uint32_t(NB * 16), 128);
+      const uint64_t bstep = uint64_t(2 * NB);            // one K16 step, 16-B units
+      auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t acc) {
+        if constexpr (PAIR == 2) ptx::mma_bf16_ss_pair(d, ad, bd, idesc, acc);
+        else ptx::mma_bf16_ss(d, ad, bd, idesc, acc);
+      };
+      auto commit = [&](uint64_t* bar) {
+        if constexpr (PAIR == 2) ptx::tc_commit_pair(bar, 0x3);   // both CTAs' copies
+        else ptx::tc_commit(bar);
+      };
+      Ring re, ri;
+      for (int T = 0; has(T); ++T) {
+        const int e = re.i;
+        if constexpr (PAIR == 2) ptx::mbar_wait_cluster(&acc_empty[e], re.ph ^ 1u);
+        else TWAIT(&acc_empty[e], re.ph ^ 1u, tw0);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem + uint32_t(e * N);
+        if constexpr (PAIR == 2) ptx::mbar_wait_cluster(&peer_tile[T & 1], uint32_t(T >> 1) & 1u);   // peer's images
+        uint64_t bd = bd0;
+        for (int k = 0; k < p.kt; ++k, ri.next(kNI)) {
+          const int ib = ri.i;
+          TWAIT(&img_full[ib], ri.ph, tw1);               // this CTA's image
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+            if constexpr (PER > 0) {
+              const uint64_t off = uint64_t(ib) * uint64_t(p.img_bytes >> 4);   // start-address field only
+#pragma unroll
+              for (int i = 0; i < PER; ++i)
+                if (!SDBG(2)) mma(d_tmem, a0[i] + off, bd + uint64_t(i) * bstep, (k | i) ? 1u : 0u);
+            } else {
+              const uint64_t* at = atab + ib * per_img;
+#pragma unroll 2
+              for (int i = 0; i < per_img; ++i)
+                if (!SDBG(2)) mma(d_tmem, at[i], bd + uint64_t(i) * bstep, (k | i) ? 1u : 0u);
+            }
+            commit(&img_empty[ib]);                       // image free once these MMAs completed
+          }
+          __syncwarp();
+          bd += uint64_t(per_img) * bstep;
+        }
+        if (ptx::elect_one()) commit(&acc_full[e]);
+        __syncwarp();
+        re.next(NBUF);
       }
-      __syncwarp();
-      re.next(NBUF);
     }
   } else if (warp < kEpiWarps) {
     // ===================== epilogue: y = acc + bias (ReLU), bf16 / fp32 =====================
-    // group eg (4 warps) takes the CTA's tiles eg, eg + 2, ...: accumulators eg, eg + 2
+    // group eg (4 warps) takes the CTA's tiles T = eg, eg + 2, ...: accumulators eg, eg + 2
     const int eg = warp >> 2;
     const int m = (warp & 3) * 32 + lane;                 // accumulator row = tile row slot
     const int r = m / p.Wp, wo = m - (m / p.Wp) * p.Wp;
     Ring re;                                             // over this group's 2 accumulators
-    for (int tile = blockIdx.x + eg * grid; tile < n_tiles; tile += 2 * grid) {
+    for (int T = eg; has(T); T += 2) {
+      const int tile = tile_of(T);
       const int b = tile / p.tiles_h;
       const int ho = (tile - b * p.tiles_h) * p.TH + r;
-      const bool valid = r < p.TH && wo < p.Wo && ho < p.Ho;
+      const bool valid = tile < n_tiles && r < p.TH && wo < p.Wo && ho < p.Ho;
       const int e = eg + 2 * re.i;
       TWAIT(&acc_full[e], re.ph, tw0);
       ptx::tc_fence_after();
@@ -374,7 +442,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_relaxed(&acc_empty[e]);
+      if (lane == 0) {
+        // every tcgen05.ld above was waited on: a relaxed arrive suffices (the y
+        // stores need no ordering with the MMA warp)
+        if constexpr (PAIR == 2) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&acc_empty[e]), 0));
+        else ptx::mbar_arrive_relaxed(&acc_empty[e]);
+      }
       re.next(2);
     }
   }
@@ -383,19 +456,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_step_stem_raw(const __grid_cons
     printf("cta %d warp %2d total %lld wait0 %lld wait1 %lld\n", blockIdx.x, warp, clock64() - tstart, tw0, tw1);
 #endif
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR == 2) ptx::cluster_sync(); else __syncthreads();   // no CTA leaves while its peer may signal it
   if (warp == kMma) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, 512);
+    if constexpr (PAIR == 2) ptx::tmem_dealloc_pair(tmem, 512);
+    else ptx::tmem_dealloc(tmem, 512);
   }
 }
 
-// (Cout, Cin, kt, kh, kw) bf16 -> [K/8][N][8], K index (k kh + u) Kp + v CP + c
-// (zero for v >= kw or c >= Cin)
+// (Cout, Cin, kt, kh, kw) bf16 -> [PAIR][K/8][N/PAIR][8], K index (k kh + u) Kp +
+// v CP + c (zero for v >= kw or c >= Cin); output channel o lives in half o / (N / PAIR)
 __global__ void k_pack_stem_raw(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ out, int N, int Cin,
-                                int kt, int kh, int kw, int Kp, int CP) {
+                                int kt, int kh, int kw, int Kp, int CP, int pair) {
   const int64_t K = int64_t(kt) * kh * Kp;
   const int64_t total = K * N;
+  const int NB = N / pair;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t kidx = i / N;
     const int o = int(i % N);
@@ -404,19 +479,21 @@ __global__ void k_pack_stem_raw(const __nv_bfloat16* __restrict__ w, __nv_bfloat
     const int v = j / CP, c = j % CP;
     __nv_bfloat16 val = __float2bfloat16_rn(0.f);
     if (v < kw && c < Cin) val = w[(((int64_t(o) * Cin + c) * kt + k) * kh + u) * kw + v];
-    out[((kidx / 8) * N + o) * 8 + (kidx % 8)] = val;
+    const int half = o / NB, oo = o % NB;
+    out[((int64_t(half) * (K / 8) + kidx / 8) * NB + oo) * 8 + (kidx % 8)] = val;
   }
 }
 
 using SrFn = void (*)(SrParams);
+constexpr int kPair = 2;         // every stem runs on CTA pairs (the kernel also compiles for PAIR = 1)
 SrFn sr_kernel(int N, int sw, int per) {
-  if (sw == 2 && N == 64 && per == 14) return k_step_stem_raw<64, 2, 14>;   // C4's RGB 5x7x7 stem
+  if (sw == 2 && N == 64 && per == 14) return k_step_stem_raw<64, 2, 14, 2>;   // C4's RGB 5x7x7 stem
   if (sw == 2) {
-    if (N == 32) return k_step_stem_raw<32, 2, 0>;
-    if (N == 64) return k_step_stem_raw<64, 2, 0>;
+    if (N == 32) return k_step_stem_raw<32, 2, 0, 2>;
+    if (N == 64) return k_step_stem_raw<64, 2, 0, 2>;
   } else if (sw == 1) {
-    if (N == 32) return k_step_stem_raw<32, 1, 0>;
-    if (N == 64) return k_step_stem_raw<64, 1, 0>;
+    if (N == 32) return k_step_stem_raw<32, 1, 0, 2>;
+    if (N == 64) return k_step_stem_raw<64, 1, 0, 2>;
   }
   return nullptr;
 }
@@ -427,10 +504,12 @@ constexpr int kPerVariants[] = {0, 14};
 bool stem_raw_plan(const Geom& g, StemRawPlan& sp) {
   sp = StemRawPlan{};
   if (g.op != OP_CONV || g.in_dtype != BF16 || g.groups != 1) return false;
-  if (g.sw < 1 || g.sw > 2 || g.sh < 1 || g.sh > 2 || g.dh != 1 || g.dw != 1 || g.kt > kMaxKt) return false;
+  // (the image ring holds two tiles' kt images: kt <= kNI / 2)
+  if (g.sw < 1 || g.sw > 2 || g.sh < 1 || g.sh > 2 || g.dh != 1 || g.dw != 1 || 2 * g.kt > kNI) return false;
   const int CP = 8 / g.sw;
   if (g.Cin > CP || !sr_kernel(g.Cout, g.sw, 0) || (int64_t(g.W) * g.Cin * 2) % 16 != 0) return false;
   sp.N = g.Cout;
+  sp.pair = kPair;
   sp.CP = CP;
   sp.Kp = (g.kw * CP + 15) / 16 * 16;
   // row slots: every valid window (pixels up to (Wo-1) sw + kw - 1 after pw zeros) and the data fit
@@ -458,14 +537,14 @@ bool stem_raw_plan(const Geom& g, StemRawPlan& sp) {
   sp.pad = (g.pw * g.Cin + 7) / 8 * 8;
   sp.rpitch = g.W * g.Cin * 2;
   const int over = std::max(0, (sp.Wp * g.sw - g.pw - g.W + 1) * g.Cin) + CP + 8;   // elements past the last row
-  sp.w_bytes = g.kt * g.kh * sp.Kp * sp.N * 2;
+  sp.w_bytes = g.kt * g.kh * sp.Kp * sp.N * 2 / sp.pair;   // this CTA's weight rows (half on a pair)
   sp.img_off = (sp.w_bytes + 1023) / 1024 * 1024;
   sp.img_bytes = (sp.img_rows * 16 + 127) / 128 * 128;
   sp.raw_off = sp.img_off + kNI * sp.img_bytes;
   sp.raw_bytes = (sp.pad * 2 + sp.nraw * sp.rpitch + over * 2 + 127) / 128 * 128;
   sp.bias_off = (sp.raw_off + kNR * sp.raw_bytes + 15) / 16 * 16;
   sp.bar_off = (sp.bias_off + sp.N * 4 + 63) / 64 * 64;
-  sp.tab_off = sp.bar_off + 256;                           // after the barriers + TMEM holder
+  sp.tab_off = sp.bar_off + 512;                           // after the barriers + TMEM holder
   const int n_desc = kNI * g.kh * (sp.Kp / 16);            // the MMA warp's A descriptor table
   sp.smem = size_t(sp.tab_off) + size_t(n_desc) * 8 + 1024;   // + 1 KB alignment slack
   if (sp.smem > kSmemLimit) return false;
@@ -477,18 +556,17 @@ size_t stem_raw_wpack_elems(const StemRawPlan& sp, const Geom& g) { return size_
 
 cudaError_t stem_raw_pack(const Geom& g, const StemRawPlan& sp, const void* w_dev, void* wpack) {
   k_pack_stem_raw<<<256, 256>>>(static_cast<const __nv_bfloat16*>(w_dev), static_cast<__nv_bfloat16*>(wpack), sp.N,
-                               g.Cin, g.kt, g.kh, g.kw, sp.Kp, sp.CP);
+                               g.Cin, g.kt, g.kh, g.kw, sp.Kp, sp.CP, sp.pair);
   return cudaGetLastError();
 }
 
 cudaError_t stem_raw_prepare() {
   for (int sw : {1, 2})
     for (int n : {32, 64})
-      for (int per : kPerVariants) {
-        SrFn fn = sr_kernel(n, sw, per);
-        if (cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemLimit)))
-          return e;
-      }
+      for (int per : kPerVariants)
+        if (SrFn fn = sr_kernel(n, sw, per))
+          if (cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemLimit)))
+            return e;
   return cudaSuccess;
 }
 
@@ -513,15 +591,27 @@ cudaError_t stem_raw_step(const Geom& g, const StemRawPlan& sp, const StepArgs& 
   p.wpack = static_cast<const __nv_bfloat16*>(wpack);
   p.bias = bias;
   p.dbg = CO_EXP("CO_SR_DEBUG", 0);
-  const int64_t grid = std::min<int64_t>(num_sms, sp.n_tiles);
-  sr_kernel(sp.N, g.sw, g.kh * sp.Kp / 16)<<<unsigned(grid), kThreads, sp.smem, s>>>(p);
-  return cudaGetLastError();
+  // a CTA (pair) per SM (pair of SMs); units only as many as there are tile groups
+  const int64_t units = std::min<int64_t>(num_sms / sp.pair, (sp.n_tiles + sp.pair - 1) / sp.pair);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(units * sp.pair));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = sp.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(sp.pair);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, sr_kernel(sp.N, g.sw, g.kh * sp.Kp / 16), p);
 }
 
 const char* stem_raw_name(const StemRawPlan& sp) {
   static char buf[2][48];
   const int i = sp.N == 32 ? 0 : 1;
-  snprintf(buf[i], sizeof(buf[i]), "k_step_stem_raw<%d>", sp.N);
+  snprintf(buf[i], sizeof(buf[i]), "k_step_stem_raw<%d%s>", sp.N, sp.pair == 2 ? ",pair" : "");
   return buf[i];
 }
 

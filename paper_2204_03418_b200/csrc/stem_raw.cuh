@@ -14,6 +14,7 @@ struct StemRawPlan {
   bool ok = false;
   int N = 0;                       // output channels (the whole layer: one part)
   int CP = 0, Kp = 0;              // channels per padded pixel (8 / sw), K per (temporal, row) tap
+  int pair = 2;                    // CTAs per MMA (cta_group::2 pairs; w_bytes is one CTA's half)
   int TH = 0, tiles_h = 0, Wp = 0; // output rows per 128-row tile, tiles per stream, row slots per output row
   int64_t n_tiles = 0;
   int nraw = 0, rpitch = 0, pad = 0;     // raw rows per image, their shared pitch, zero elements before the data

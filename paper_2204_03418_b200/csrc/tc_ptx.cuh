@@ -72,6 +72,21 @@ __device__ __forceinline__ bool mbar_try_wait_nohint(uint64_t* bar, uint32_t par
       : "memory");
   return ok != 0;
 }
+// wait with cluster-scope acquire: the phase was completed by arrivals of the
+// peer CTA of a pair (release.cluster), whose shared-memory writes the waiter's
+// tensor-core work then reads
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #ifdef CO_MBAR_NOHINT
   while (!mbar_try_wait_nohint(bar, parity)) {
