@@ -121,6 +121,8 @@ struct TcParams {
   int ystage, y_off;              // HALO bf16: y transposed through a per-warp shared-memory buffer at y_off
   int l2last;                     // HALO / FLAT: frame tiles loaded with an L2 evict_last policy
   int pdl;                        // launched with programmatic stream serialization (see pdl_wait)
+  int fparts;                     // KHALO: channel parts float over items (item i -> part i mod n_split), so
+                                  // the grid need not be a multiple of the parts (weights stream per item)
   int l2pf;                       // L2 bulk prefetch of the state one item ahead (epilogue)
   int dbg;                        // CO_TC_DEBUG bits (experiments only): 1 no state/y traffic, 2 no MMA,
                                   // 4 no A loads, 8 no TMEM reads, 16 (with 2) no accumulator handshakes
@@ -300,7 +302,8 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     for (int i = threadIdx.x; i < 2 * p.st_nraw * p.st_rpitch / 16; i += blockDim.x) zr[i] = make_uint4(0u, 0u, 0u, 0u);
     ptx::fence_proxy_async();                           // generic zeros, read by the tensor cores
   } else {
-    for (int i = threadIdx.x; i < CC; i += blockDim.x) bias_s[i] = p.bias[c0 + i];
+    // floating parts (KHALO): every part's biases; otherwise this CTA's part
+    for (int i = threadIdx.x; i < (p.fparts ? p.Cout : CC); i += blockDim.x) bias_s[i] = p.bias[(p.fparts ? 0 : c0) + i];
   }
   ptx::tc_fence_before();
   if (CLU > 1) ptx::cluster_sync(); else __syncthreads();
@@ -359,6 +362,9 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
           const int64_t tile = tile_of(item);
           const int b = int(tile / p.tiles_per_stream);
           const int ho0 = int(tile % p.tiles_per_stream) * p.MT;
+          const int ipart = p.fparts ? int(item % p.n_split) : part;   // this item's channel part
+          const uint8_t* wsrc_i =
+              reinterpret_cast<const uint8_t*>(p.wpack) + size_t(ipart * PAIR + (PAIR == 2 ? rank : 0u)) * p.w_bytes;
           for (int cb = 0; cb < p.n_cb; ++cb) {
             // the 64-channel block's input halo, then its (tap) weight chunks
             ptx::mbar_wait(&a_empty[as], aph ^ 1);
@@ -384,10 +390,10 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
                 if (leader) ptx::mbar_arrive(&full[s]);
               } else if constexpr (PAIR == 2) {
                 if (leader) ptx::mbar_arrive_expect_tx(&full[s], p.b_bytes * PAIR);
-                ptx::tma_load_4d_pair(dst, &wmap, &full[s], 0, 0, kblk, part * PAIR + int(rank));
+                ptx::tma_load_4d_pair(dst, &wmap, &full[s], 0, 0, kblk, ipart * PAIR + int(rank));
               } else {
                 ptx::mbar_arrive_expect_tx(&full[s], p.b_bytes);
-                ptx::bulk_g2s(dst, wsrc + size_t(kblk) * p.b_bytes, p.b_bytes, &full[s]);
+                ptx::bulk_g2s(dst, wsrc_i + size_t(kblk) * p.b_bytes, p.b_bytes, &full[s]);
               }
               if (++s == p.stages) { s = 0; ph ^= 1; }
             }
@@ -600,7 +606,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
       const uint32_t ka_base = ptx::smem_u32(smem);
       // per-tap descriptor offset (16-B units): phase block + row shift, computed
       // once (runtime-divisor divisions would otherwise sit in the issue loop)
-      uint32_t* tap_tab = reinterpret_cast<uint32_t*>(bias_s + CC);
+      uint32_t* tap_tab = reinterpret_cast<uint32_t*>(bias_s + (p.fparts ? p.Cout : CC));
       for (int tap = lane; tap < taps; tap += 32) {
         const int u = tap / p.kw, v = tap - (tap / p.kw) * p.kw;
         // input row s ho + u - ph = s (ho + floor((u-ph)/s)) + (u-ph) mod s
@@ -864,7 +870,7 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
     const int emit = tk ? tk[0] : p.emit;
     const int64_t yt = tk ? int64_t(tk[1]) * p.y_tstride : 0;
     auto slot = [&](int k) -> int { return tk ? tk[2 + k] : p.slot[k]; };
-    const int bias0 = stem ? c0v : 0;                  // bias_s holds all Cout (STEM) or this part's CC
+    const int bias0 = (stem || p.fparts) ? c0v : 0;    // bias_s holds all Cout (STEM, floating parts) or this part's CC
     // ---- this row's output pixel
     bool valid;
     int64_t pix, b;
@@ -1069,10 +1075,12 @@ __global__ void __launch_bounds__(tc_threads(EG, CS), 1)
   } else if (!p.ticks) {
     int64_t li = e;
     const int64_t step = EG * int64_t(n_units);
-    if (unit + int64_t(e) * n_units < p.n_items) prefetch_state(tile_of(unit + int64_t(e) * n_units), c0);
+    auto c0_of = [&](int64_t item) { return p.fparts ? int(item % p.n_split) * CC : c0; };
+    if (unit + int64_t(e) * n_units < p.n_items)
+      prefetch_state(tile_of(unit + int64_t(e) * n_units), c0_of(unit + int64_t(e) * n_units));
     for (int64_t item = unit + int64_t(e) * n_units; item < p.n_items; item += step, li += EG) {
-      if (item + step < p.n_items) prefetch_state(tile_of(item + step), c0);
-      work(tile_of(item), c0, li, nullptr);
+      if (item + step < p.n_items) prefetch_state(tile_of(item + step), c0_of(item + step));
+      work(tile_of(item), c0_of(item), li, nullptr);
     }
   } else {
     // chunked: item bi + e n_units of every batch, all T frames in order; the work
@@ -1275,6 +1283,7 @@ struct Plan {
   // STEM (fused W-im2col): raw rows per tile, padded raw-row pitch / left pad, image rows / bytes
   int st_nraw = 0, st_rpitch = 0, st_pad = 0, st_img_rows = 0, st_img_bytes = 0, st_raw_off = 0;
   int st_groups = 0, st_data_groups = 0, st_phase_base[2] = {0, 0};
+  int fparts = 0;                 // KHALO: channel parts float over items (all SMs busy)
   int64_t n_tiles = 0;
   size_t smem = 0;
 };
@@ -1503,7 +1512,11 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
     const int ka_stages = 2;
     // the last phase's taps read up to (prow - MT) Wq + (Wq - Wo) rows past its
     // start + 128: inside the next phase / stage / the weight ring (junk rows)
-    const size_t fixed2 = fixed + size_t(ka_stages) * ka_stride;
+    // floating channel parts (weights stream per item anyway): a CTA may take any
+    // part's item, so the grid fills every SM (C4 L3-L5: 144 -> 148); its bias
+    // table then holds all Cout
+    const int fparts = (g.Cout / best->CC > 1 && CO_EXP("CO_TC_FPARTS", 1)) ? 1 : 0;
+    const size_t fixed2 = fixed + size_t(ka_stages) * ka_stride + (fparts ? size_t(g.Cout - best->CC) * 4 : 0);
     // the K-pipelined layers are tensor-bound and their epilogues wait on the
     // MMA, so the weight ring takes all of shared memory (C4: L3 1.73 -> 1.42 ms,
     // L5 1.53 -> 1.39 ms against the 190 KB budget); CO_TC_KHALO_SMEM (KB, experiment builds) caps it
@@ -1527,6 +1540,7 @@ bool plan_kloop(const Geom& g, Plan& pl, bool flat = false) {
       pl.w_off = ka_stages * ka_stride;
       pl.chunk_stride = a_rows * 16;
       pl.smem = fixed2 + size_t(bst) * b_stride;
+      pl.fparts = fparts;
     }
   }
   return true;
@@ -1947,8 +1961,11 @@ static cudaError_t tc_launch(DenseTC* t, const Geom& g, const StepArgs& a, const
   p.bias = bias;
   p.mc = mc;
   const int per = std::max(1, t->num_sms / clu / pl.n_split);
-  // STEM: a CTA serves every part of its tiles (one image per tile), one CTA per SM
+  // STEM: a CTA serves every part of its tiles (one image per tile), one CTA per SM;
+  // floating parts (KHALO, single steps): every SM, whatever the part count
+  p.fparts = (pl.fparts && T == 1) ? 1 : 0;
   const int64_t grid = pl.mode == MODE_STEM ? std::min<int64_t>(t->num_sms, pl.n_tiles)
+                       : p.fparts           ? std::min<int64_t>(t->num_sms / clu, units_tiles * pl.n_split) * clu
                                             : std::min<int64_t>(per, units_tiles) * pl.n_split * clu;
   // KLOOP pairs stream their weight halves through a tensor map over the packed
   // weights [part*2 + half][K/8][N/2][8]: box = one chunk (kb/8 K-groups)
