@@ -3,8 +3,14 @@
 // one TMEM accumulator, for M = 128 (cta_group::1) and M = 256 (cta_group::2,
 // a CTA pair), across N.  Operands are zero shared memory (no-swizzle K-major
 // descriptors); timing is clock64 around ITERS MMAs + commit + wait on the
-// issuing CTA.  Question it answers: is the ~70-cycle cost of an N = 64 MMA
-// (k_step_stem_raw) per instruction or per CTA?
+// issuing CTA; "walk" gives every MMA fresh operand addresses (A +4 KB, B the
+// next K16 step), as a real K loop does.  Questions it answers: is the ~70-cycle
+// cost of an N = 64 MMA (k_step_stem_raw) per instruction or per CTA, and does
+// the operand fetch alone keep up at larger N?  Measured (B200, 148 CTAs):
+// M = 128: 40.8 / 48.9 / 56.9 / 64.9 / 80.9 / 96.9 / 128.9 cycles at N = 32 / 64 /
+// 96 / 128 / 160 / 192 / 256; pairs (M = 256): 40.0 / 44.0 / 50.4 / 65.1 / 81.1 /
+// 97.1 / 129.1; identical with fresh operands -- an instruction floor of ~40
+// cycles below N = 128, the 128 N / 256 floor above.
 //
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2204_03418_b200/csrc \
 //        scripts/mma_probe.cu -o scripts/mma_probe
@@ -17,7 +23,7 @@ using namespace co;
 constexpr int ITERS = 256;
 
 template <int PAIR>
-__global__ void __launch_bounds__(128, 1) k_probe(int N, int lbo_bytes, long long* out) {
+__global__ void __launch_bounds__(128, 1) k_probe(int N, int lbo_bytes, long long* out, int walk) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 64 * 1024);
   uint32_t* holder = reinterpret_cast<uint32_t*>(bar + 2);
@@ -41,8 +47,12 @@ __global__ void __launch_bounds__(128, 1) k_probe(int N, int lbo_bytes, long lon
     long long t0 = clock64();
     if (ptx::elect_one()) {
       for (int i = 0; i < ITERS; ++i) {
-        if constexpr (PAIR == 2) ptx::mma_bf16_ss_pair(tmem, ad, bd, idesc, i ? 1u : 0u);
-        else ptx::mma_bf16_ss(tmem, ad, bd, idesc, i ? 1u : 0u);
+        // walk: each MMA reads fresh operands (A: the next 4 KB of a 32 KB region,
+        // B: the next K group pair of the weights), as a real K loop does
+        const uint64_t da = walk ? uint64_t((i & 7) * 256) : 0;            // 4 KB steps (16-B units)
+        const uint64_t db = walk ? uint64_t((i & 3) * 2 * (N / PAIR)) : 0;  // next K16 of B
+        if constexpr (PAIR == 2) ptx::mma_bf16_ss_pair(tmem, ad + da, bd + db, idesc, i ? 1u : 0u);
+        else ptx::mma_bf16_ss(tmem, ad + da, bd + db, idesc, i ? 1u : 0u);
       }
       if constexpr (PAIR == 2) ptx::tc_commit_pair(bar, 0x1);
       else ptx::tc_commit(bar);
@@ -62,7 +72,7 @@ __global__ void __launch_bounds__(128, 1) k_probe(int N, int lbo_bytes, long lon
 }
 
 template <int PAIR>
-long long run(int N, int lbo, int grid) {
+long long run(int N, int lbo, int grid, int walk = 0) {
   long long* d;
   cudaMalloc(&d, sizeof(long long));
   const size_t smem = 64 * 1024 + 64;
@@ -78,7 +88,7 @@ long long run(int N, int lbo, int grid) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  for (int rep = 0; rep < 2; ++rep) cudaLaunchKernelEx(&cfg, k_probe<PAIR>, N, lbo, d);
+  for (int rep = 0; rep < 2; ++rep) cudaLaunchKernelEx(&cfg, k_probe<PAIR>, N, lbo, d, walk);
   cudaError_t e = cudaDeviceSynchronize();
   long long h = -1;
   cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -89,10 +99,11 @@ long long run(int N, int lbo, int grid) {
 
 int main() {
   printf("cycles per MMA (K = 16, %d back-to-back, one accumulator)\n", ITERS);
-  for (int grid : {1, 148}) {
-    for (int N : {32, 64, 128, 256}) {
-      const long long a = run<1>(N, 16, grid), b = run<1>(N, 128 * 16, grid), c = run<2>(N, 16, grid);
-      printf("grid %3d N %3d: M=128 lbo16 %.1f  M=128 lbo2K %.1f  M=256 pair lbo16 %.1f  (floor %d / %d)\n", grid, N,
+  for (int walk : {0, 1}) {
+    printf(walk ? "fresh operands per MMA (A +4 KB, B +1 K16 step)\n" : "the same operands every MMA\n");
+    for (int N : {32, 64, 96, 128, 160, 192, 256}) {
+      const long long a = run<1>(N, 16, 148, walk), b = run<1>(N, 128 * 16, 148, walk), c = run<2>(N, 16, 148, walk);
+      printf("  N %3d: M=128 lbo16 %.1f  M=128 lbo2K %.1f  M=256 pair %.1f  (floor %d / %d)\n", N,
              double(a) / ITERS, double(b) / ITERS, double(c) / ITERS, 128 * N / 256, 256 * N / 512);
     }
   }
