@@ -435,6 +435,9 @@ int co_residual_delay(const co_residual* r, int64_t* delay, int64_t* skip_delay)
  *   "log"        0 (default) | 1 print each tensor-core plan to stderr        [create]
  *   "stem"       1 (default) small-Cin stems build their W-im2col in shared
  *                memory | 0 a separate HBM W-im2col pass per step            [create]
+ *   "dw_seg"     1 (default) depthwise stencils stream state + input rows
+ *                through a bulk-copy stage ring (k_step_dw_seg) | 0 the
+ *                per-thread-load K2 (k_step_dw_st)                           [create]
  * name == NULL resets every option to its default.
  * Errors: CO_ERR_ARG for an unknown name or a value out of range.  Not
  * thread-safe against concurrent creates (set options before building handles). */

@@ -34,6 +34,7 @@
 #include <string>
 
 #include "depthwise.cuh"
+#include "tc_ptx.cuh"
 
 namespace co {
 
@@ -65,6 +66,12 @@ struct DwParams {
   int64_t n_tiles;
   int WC, HR;                           // halo width (W + 2 pw) and rows (TH + kh - 1)
   int64_t frame;                        // RAW layout: elements of one stream's frame (H*W*C)
+  // K2s segment pipeline (k_step_dw_seg): units = (stream, output row, segment of WS pixels)
+  int64_t n_units;
+  int nseg, WS, WX, nst, spu, gthreads; // WX = WS + kw - 1 staged input columns; spu strips per unit
+  int ngroups;                          // consumer groups (alternate units)
+  const void* zeros;                    // >= WX * C * 2 zero bytes: the bulk-copy source of padding columns
+  int stage_bytes, x_off, stage_off, bar_off;   // shared-memory layout (bytes)
 };
 
 __device__ __forceinline__ float4 ld_bf16x4(const __nv_bfloat16* p) {
@@ -253,6 +260,197 @@ __global__ void __launch_bounds__(256, CO_DW_ST_MINB) k_step_dw_st(const DwParam
         apply<KT>(p, b, pin0 + j, pix0 + j, q, pre[j], reinterpret_cast<const float4*>(bs)[q], P);
       }
     }
+  }
+}
+
+// ------------------------------------------------------------------ K2s: segment pipeline
+// The stencil with its memory traffic decoupled from the arithmetic.  K2's
+// per-thread state loads are issued one strip ahead of their use and its halo
+// is loaded and waited for per tile, so its bytes in flight per SM (~30 KB)
+// sit below what HBM latency x bandwidth asks for (ncu: 0.69 of HBM, long-
+// scoreboard and barrier stalls).  Here one producer thread streams, per unit
+// (stream b, output row ho, segment of WS output pixels), the unit's state rows
+// (emit slot + accumulating slots: each one contiguous run of WS x C fp32 in
+// the channels-last layout) and its kh input-row pieces (WS + kw - 1 columns,
+// clipped to the frame) into a ring of `nst` shared-memory stages with bulk
+// copies (cp.async.bulk, mbarrier complete_tx), so nst - 2 units of loads are
+// in flight while the consumer groups compute alternate units: a thread =
+// (channel quad q, strip of PX pixels), taps read unpredicated from the stage
+// (padding columns / rows are bulk copies from a zero buffer), the thread's
+// weights at immediate offsets ([Cq][taps] layout), the per-slice FMA order
+// of K1 / K2 (bitwise equal), y and the written state slots stored straight
+// from registers.  A CTA walks a contiguous unit range, so the input
+// rows it re-reads for the next output row come from L2.
+#ifndef CO_DW_SEG_THREADS
+#define CO_DW_SEG_THREADS 384           // <= 12 warps (3 per SM sub-partition): up to 168 registers per thread
+#endif
+constexpr int kSegMaxThreads = CO_DW_SEG_THREADS;
+constexpr int kSegGroupMax = (kSegMaxThreads - 32) / 2;   // >= 2 consumer groups
+
+template <int KT, int KH, int KW, int PX>
+__global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_seg(const DwParams p) {
+  constexpr int NT = KT * KH * KW;                                  // taps per channel
+  extern __shared__ __align__(128) uint8_t smem[];
+  float4* wt = reinterpret_cast<float4*>(smem);                     // [Cq][NT] float4: a thread's taps at
+  float* bs = reinterpret_cast<float*>(wt + NT * p.Cq);             // immediate offsets (NT odd: conflict-free)
+  uint8_t* stages = smem + p.stage_off;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  uint64_t* empty = full + p.nst;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NT * p.Cq; i += blockDim.x) {
+    const int qq = i / NT, tap = i - qq * NT;
+    wt[i] = *reinterpret_cast<const float4*>(p.w + int64_t(tap) * p.C + 4 * qq);
+  }
+  for (int i = tid; i < p.C; i += blockDim.x) bs[i] = p.bias[i];
+  if (tid == 0) {
+    for (int s = 0; s < p.nst; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], p.gthreads / 32);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // see k_step_dw_st
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int64_t lo = p.n_units * blockIdx.x / gridDim.x;
+  const int64_t hi = p.n_units * (blockIdx.x + 1) / gridDim.x;
+  const int64_t rows_u = int64_t(p.Ho) * p.nseg;                   // units per stream
+  const int warp = tid / 32, lane = tid % 32;
+  const int64_t row_e = int64_t(p.WS) * p.C;                       // state elements per staged slot row
+  const int xrow_b = p.WX * p.C * 2;                                // bytes of one staged input row
+  if (warp == p.ngroups * p.gthreads / 32) {                        // ---- producer thread
+    if (lane != 0) return;
+    int64_t b = lo / rows_u;                                        // unit lo's (stream, row, segment),
+    int ho = int(lo - b * rows_u) / p.nseg;                         // then stepped incrementally
+    int sg = int(lo - b * rows_u) - ho * p.nseg;
+    const uint8_t* zsrc = static_cast<const uint8_t*>(p.zeros);
+    for (int64_t j = lo; j < hi; ++j) {
+      const int64_t i = j - lo;
+      const int s = int(i % p.nst);
+      if (i >= p.nst) ptx::mbar_wait(&empty[s], (uint32_t(i / p.nst) & 1u) ^ 1u);
+      const int wo0 = sg * p.WS;
+      const int wsz = min(p.WS, p.Wo - wo0);
+      uint8_t* st = stages + int64_t(s) * p.stage_bytes;
+      const int64_t pix0 = b * p.HWo + int64_t(ho) * p.Wo + wo0;
+      const uint32_t sbytes = uint32_t(wsz) * p.C * 4;
+      // staged column c holds input column wlo + c (c < ncol are read for real
+      // pixels); [a, e] is the part inside the frame, the rest is padding: zero
+      // bytes bulk-copied like the data, so the consumers read every tap
+      // unpredicated and no generic-proxy write ever touches a stage
+      const int wlo = wo0 - p.pw, ncol = wsz + KW - 1;
+      const int a = max(wlo, 0), e = min(wlo + ncol - 1, p.W - 1);
+      const uint32_t pxb = uint32_t(p.C) * 2;
+      uint32_t tx = 0;
+      if (KT > 1 && p.emit) tx += sbytes;
+      if (KT > 2 && p.update)
+        for (int k = 1; k < KT - 1; ++k) tx += (p.slot[k] >= 0) ? sbytes : 0u;
+      tx += uint32_t(KH * ncol) * pxb;                              // every staged column: data or zeros
+      ptx::mbar_arrive_expect_tx(&full[s], tx);
+      if (KT > 1 && p.emit)
+        ptx::bulk_g2s(st, p.state + (int64_t(p.slot[KT - 1]) * p.plane + pix0) * p.C, sbytes, &full[s]);
+      if (KT > 2 && p.update)
+        for (int k = 1; k < KT - 1; ++k)
+          if (p.slot[k] >= 0)
+            ptx::bulk_g2s(st + int64_t(k) * row_e * 4, p.state + (int64_t(p.slot[k]) * p.plane + pix0) * p.C,
+                          sbytes, &full[s]);
+      for (int u = 0; u < KH; ++u) {
+        const int hr = ho - p.ph + u;
+        uint8_t* row = st + p.x_off + u * xrow_b;
+        if (!p.x || hr < 0 || hr >= p.H || a > e) {
+          ptx::bulk_g2s(row, zsrc, uint32_t(ncol) * pxb, &full[s]);
+          continue;
+        }
+        if (a > wlo) ptx::bulk_g2s(row, zsrc, uint32_t(a - wlo) * pxb, &full[s]);
+        ptx::bulk_g2s(row + (a - wlo) * pxb, p.x + b * p.x_bstride + (int64_t(hr) * p.W + a) * p.C,
+                      uint32_t(e - a + 1) * pxb, &full[s]);
+        if (e - wlo + 1 < ncol)
+          ptx::bulk_g2s(row + (e - wlo + 1) * pxb, zsrc, uint32_t(ncol - (e - wlo + 1)) * pxb, &full[s]);
+      }
+      if (++sg == p.nseg) {
+        sg = 0;
+        if (++ho == p.Ho) { ho = 0; ++b; }
+      }
+    }
+    return;
+  }
+  // ---- consumers: group g takes units lo + g, lo + g + ngroups, ...
+  const int g = tid / p.gthreads, tg = tid - g * p.gthreads;
+  const bool active = tg < p.Cq * p.spu;
+  const int q = tg % p.Cq, sp = tg / p.Cq;                          // channel quad, strip of the unit
+  const float4* wq = wt + q * NT;
+  const float4 bias4 = reinterpret_cast<const float4*>(bs)[q];
+  const int cstep = p.C;                                            // elements between pixels (x, y, state)
+  for (int64_t j = lo + g; j < hi; j += p.ngroups) {
+    const int64_t i = j - lo;
+    const int s = int(i % p.nst);
+    ptx::mbar_wait(&full[s], uint32_t(i / p.nst) & 1u);
+    const uint32_t ju = uint32_t(j);                                // n_units < 2^31 (plan)
+    const int64_t b = ju / uint32_t(rows_u);
+    const int r = int(ju - uint32_t(b) * uint32_t(rows_u));
+    const int ho = r / p.nseg, wo0 = (r - ho * p.nseg) * p.WS;
+    const int wsz = min(p.WS, p.Wo - wo0);
+    if (active && sp * PX < wsz) {
+      const uint8_t* st = stages + int64_t(s) * p.stage_bytes;
+      const int c0 = sp * PX;                                       // first staged column / pixel of the strip
+      float4 acc[KT][PX];
+#pragma unroll
+      for (int k = 0; k < KT; ++k)
+#pragma unroll
+        for (int jj = 0; jj < PX; ++jj) acc[k][jj] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const __nv_bfloat16* xr = reinterpret_cast<const __nv_bfloat16*>(st + p.x_off) + int64_t(c0) * cstep + 4 * q;
+#pragma unroll
+      for (int u = 0; u < KH; ++u) {
+        float4 xv[PX + KW - 1];
+#pragma unroll
+        for (int t = 0; t < PX + KW - 1; ++t) xv[t] = ld_bf16x4(xr + t * cstep);
+        xr += p.WX * cstep;
+#pragma unroll
+        for (int v = 0; v < KW; ++v)
+#pragma unroll
+          for (int k = 0; k < KT; ++k) {
+            const float4 w = wq[(k * KH + u) * KW + v];
+#pragma unroll
+            for (int jj = 0; jj < PX; ++jj) acc[k][jj] = f4_fma(w, xv[jj + v], acc[k][jj]);
+          }
+      }
+      // emit / accumulate / start (apply()'s arithmetic); the read slots come
+      // from the stage only now, so no registers hold them across the taps
+      const float4* ss4 = reinterpret_cast<const float4*>(st) + int64_t(c0) * p.Cq + q;   // [KT-1][WS][Cq]
+      const int64_t pin0 = int64_t(ho) * p.Wo + wo0 + c0;
+      const int64_t yoff = b * p.y_bstride + pin0 * cstep + 4 * q;
+      float* sp_k[KT > 1 ? KT - 1 : 1];                             // written slot rows of pixel 0 of the strip
+#pragma unroll
+      for (int k = 0; k < KT - 1; ++k)
+        sp_k[k] = p.state + (int64_t(p.slot[k]) * p.plane + b * p.HWo + pin0) * cstep + 4 * q;
+#pragma unroll
+      for (int jj = 0; jj < PX; ++jj) {
+        if (c0 + jj >= wsz) continue;
+        if (p.emit) {
+          float4 v = f4_add(acc[KT - 1][jj], bias4);
+          if (KT > 1) v = f4_add(ss4[jj * p.Cq], v);
+          v = f4_act(v, p.act);
+          if (p.out_f32) {
+            *reinterpret_cast<float4*>(static_cast<float*>(p.y) + yoff + jj * cstep) = v;
+          } else {
+            __nv_bfloat162 lo2 = __floats2bfloat162_rn(v.x, v.y), hi2 = __floats2bfloat162_rn(v.z, v.w);
+            uint2 uu;
+            uu.x = *reinterpret_cast<uint32_t*>(&lo2);
+            uu.y = *reinterpret_cast<uint32_t*>(&hi2);
+            *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.y) + yoff + jj * cstep) = uu;
+          }
+        }
+        if (KT > 1 && p.update) {
+#pragma unroll
+          for (int k = KT - 2; k >= 1; --k)
+            if (p.slot[k] >= 0)
+              __stcs(reinterpret_cast<float4*>(sp_k[k] + jj * cstep),
+                     f4_add(ss4[(k * p.WS + jj) * p.Cq], acc[k][jj]));
+          if (p.slot[0] >= 0) __stcs(reinterpret_cast<float4*>(sp_k[0] + jj * cstep), acc[0][jj]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive_relaxed(&empty[s]);   // the stage's reads are consumed (see dense epilogue)
   }
 }
 
@@ -615,13 +813,20 @@ struct DwVariant {
   int PX = 1;                           // K2: output pixels per thread strip
   DwFn raw = nullptr;                   // RAW-layout kernel for this shape
   DwChunkFn chunk = nullptr;            // chunked-steps kernel (temporal only)
+  DwFn seg = nullptr;                   // K2s segment-pipeline kernel (spatial stencils)
+  int SPX = 4;                          // K2s: output pixels per thread strip
 };
 #ifndef CO_DW_PX
 #define CO_DW_PX 2                      // output pixels per thread strip (experiments: -DCO_DW_PX=n)
 #endif
+// K2s strip: 7 pixels (WS = 14: C3-a's 28-pixel rows in two units of 96
+// threads; weights read from shared memory once per 7 pixels), 4 for the
+// register-heavier 5x5 / kt = 5 stencils
+#define CO_DW_SEG_PX(kt, kh, kw) ((kt) <= 3 && (kh) * (kw) <= 9 ? 7 : 4)
 #define CO_DW_ST(kt, kh, kw) {kt, kh, kw, (DwFn)k_step_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>, \
                               (kt <= 3 ? CO_DW_PX : 2), (DwFn)k_step_dw_raw<kt, kh, kw>, \
-                              (DwChunkFn)k_steps_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>}
+                              (DwChunkFn)k_steps_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>, \
+                              (DwFn)k_step_dw_seg<kt, kh, kw, CO_DW_SEG_PX(kt, kh, kw)>, CO_DW_SEG_PX(kt, kh, kw)}
 #define CO_DW_T(kt) {kt, 1, 1, (DwFn)k_step_dw_t<kt>, 1, (DwFn)k_step_dw_raw<kt, 1, 1>, (DwChunkFn)k_steps_dw_t<kt>}
 const DwVariant kDwVariants[] = {
     CO_DW_ST(1, 3, 3), CO_DW_ST(2, 3, 3), CO_DW_ST(3, 3, 3), CO_DW_ST(5, 3, 3), CO_DW_ST(3, 5, 5),
@@ -635,7 +840,52 @@ struct DwPlan {
   int TH = 0, bands = 0, HR = 0, WC = 0;
   int64_t n_tiles = 0;
   size_t smem = 0;
+  // K2s segment pipeline (option "dw_seg")
+  bool seg = false;
+  int nseg = 0, WS = 0, WX = 0, nst = 0, spu = 0, gthreads = 0, ngroups = 0;
+  int stage_bytes = 0, x_off = 0, stage_off = 0, bar_off = 0;
+  int64_t n_units = 0;
+  size_t seg_smem = 0;
 };
+
+#ifndef CO_DW_SEG_SMEM_KB
+#define CO_DW_SEG_SMEM_KB 220           // K2s shared-memory budget per CTA (one CTA per SM)
+#endif
+
+// K2s plan: the fewest segments per output row whose strips fit one consumer
+// group (<= kSegGroupMax threads) and whose nst stages (ngroups + 2, else + 1)
+// fit the budget; up to three consumer groups (C3-a: 3 x 96 threads, 5 stages;
+// measured 0.37 ms with 2 groups / 4 stages, 0.30 with 3 / 5; experiments:
+// CO_DW_SEG_NG / _NST).
+bool make_seg_plan(const Geom& g, const DwVariant& v, DwPlan& pl) {
+  if (!v.seg || g.Cout / 4 > kSegGroupMax) return false;
+  const int PX = v.SPX, Cq = g.Cout / 4;
+  const size_t base = (size_t(g.kt * g.kh * g.kw + 1) * g.Cin * 4 + 127) / 128 * 128;
+  for (int nseg = 1; nseg <= g.Wo; ++nseg) {
+    const int WS = ((g.Wo + nseg - 1) / nseg + PX - 1) / PX * PX;
+    if (int64_t(nseg - 1) * WS >= g.Wo) continue;                  // would leave an empty segment
+    const int spu = WS / PX;
+    const int gth = (Cq * spu + 31) / 32 * 32;
+    if (gth > kSegGroupMax) continue;
+    const int ng = std::max(2, std::min(CO_EXP("CO_DW_SEG_NG", 3), (kSegMaxThreads - 32) / gth));
+    const int WX = WS + g.kw - 1;
+    const size_t x_off = size_t(std::max(g.kt - 1, 0)) * WS * g.Cout * 4;
+    const size_t sb = (x_off + size_t(g.kh) * WX * g.Cin * 2 + 127) / 128 * 128;
+    for (int nst = std::max(CO_EXP("CO_DW_SEG_NST", ng + 2), ng + 1); nst >= ng + 1; --nst) {
+      const size_t smem = base + nst * sb + 2 * size_t(nst) * 8;
+      if (smem > size_t(CO_DW_SEG_SMEM_KB) * 1024) continue;
+      pl.seg = true;
+      pl.nseg = nseg; pl.WS = WS; pl.WX = WX; pl.nst = nst; pl.spu = spu; pl.gthreads = gth; pl.ngroups = ng;
+      pl.stage_bytes = int(sb); pl.x_off = int(x_off); pl.stage_off = int(base);
+      pl.bar_off = int(base + nst * sb);
+      pl.n_units = g.B * g.Ho * nseg;
+      if (pl.n_units >= (int64_t(1) << 31)) return false;
+      pl.seg_smem = smem;
+      return true;
+    }
+  }
+  return false;
+}
 
 bool make_dw_plan(const Geom& g, DwPlan& pl) {
   if (g.in_dtype != BF16 || g.groups != g.Cin || g.Cin != g.Cout || g.Cin % 8 != 0) return false;
@@ -667,7 +917,8 @@ bool make_dw_plan(const Geom& g, DwPlan& pl) {
   const int Cq = g.Cin / 4;
   if (Cq > 256) return false;
   pl.threads = Cq * (256 / Cq);
-  return pl.smem <= 227 * 1024;
+  if (option(OPT_DW_SEG)) make_seg_plan(g, *pl.var, pl);
+  return pl.seg || pl.smem <= 227 * 1024;
 }
 
 }  // namespace
@@ -675,6 +926,7 @@ bool make_dw_plan(const Geom& g, DwPlan& pl) {
 struct Depthwise {
   DwPlan pl;
   float* w = nullptr;
+  void* zeros = nullptr;                // K2s: padding source (WX * C * 2 zero bytes)
   int grid = 0;
   std::string name;
 };
@@ -709,6 +961,21 @@ Depthwise* depthwise_create(const Geom& g, const void* w_dev, std::string& err) 
     }
     char buf[96];
     snprintf(buf, sizeof(buf), "k_step_dw_raw<%d,%d,%d>", pl.var->KT, pl.var->KH, pl.var->KW);
+    t->name = buf;
+    return t;
+  }
+  if (pl.seg) {
+    const size_t zb = size_t(pl.WX) * g.Cin * 2;
+    if ((e = cudaMalloc(&t->zeros, zb)) != cudaSuccess || (e = cudaMemset(t->zeros, 0, zb)) != cudaSuccess) {
+      err = cudaGetErrorString(e); depthwise_destroy(t); return nullptr;
+    }
+    e = cudaFuncSetAttribute(pl.var->seg, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.seg_smem));
+    if (e != cudaSuccess) { err = cudaGetErrorString(e); depthwise_destroy(t); return nullptr; }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.var->seg, pl.ngroups * pl.gthreads + 32, pl.seg_smem);
+    per_sm = std::max(per_sm, 1);
+    t->grid = int(std::max<int64_t>(1, std::min<int64_t>(pl.n_units, int64_t(sms) * per_sm)));
+    char buf[96];
+    snprintf(buf, sizeof(buf), "k_step_dw_seg<%d,%d,%d>", pl.var->KT, pl.var->KH, pl.var->KW);
     t->name = buf;
     return t;
   }
@@ -814,6 +1081,7 @@ cudaError_t depthwise_steps(Depthwise* t, const Geom& g, const void* x, int64_t 
 void depthwise_destroy(Depthwise* t) {
   if (!t) return;
   cudaFree(t->w);
+  cudaFree(t->zeros);
   delete t;
 }
 
@@ -839,17 +1107,22 @@ cudaError_t depthwise_step(Depthwise* t, const Geom& g, const StepArgs& a, const
   if (g.raw)
     return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->raw), dim3(unsigned(t->grid)), dim3(kDwThreads),
                             args, 0, s);
+  if (pl.seg) {
+    p.n_units = pl.n_units; p.nseg = pl.nseg; p.WS = pl.WS; p.WX = pl.WX; p.nst = pl.nst; p.spu = pl.spu;
+    p.gthreads = pl.gthreads; p.stage_bytes = pl.stage_bytes; p.x_off = pl.x_off; p.stage_off = pl.stage_off;
+    p.bar_off = pl.bar_off; p.ngroups = pl.ngroups; p.zeros = t->zeros;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(t->grid));
-  cfg.blockDim = dim3(pl.temporal ? kDwThreads : pl.threads);
-  cfg.dynamicSmemBytes = pl.temporal ? 0 : pl.smem;
+  cfg.blockDim = dim3(pl.seg ? pl.ngroups * pl.gthreads + 32 : pl.temporal ? kDwThreads : pl.threads);
+  cfg.dynamicSmemBytes = pl.seg ? pl.seg_smem : pl.temporal ? 0 : pl.smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // option "pdl" = 0: off
   attr[0].val.programmaticStreamSerializationAllowed = option(OPT_PDL) != 0 ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(pl.var->fn), args);
+  return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(pl.seg ? pl.var->seg : pl.var->fn), args);
 }
 
 }  // namespace co

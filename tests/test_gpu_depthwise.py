@@ -11,7 +11,7 @@ import pytest
 import torch
 
 import oracle as O
-from tests.helpers import assert_bf16_rounding_bound, make_pair, np_of, rel_err, to_cl
+from tests.helpers import assert_bf16_rounding_bound, make_pair, np_of, rel_err, set_opt, to_cl
 
 pytestmark = pytest.mark.gpu
 
@@ -29,6 +29,10 @@ CASES = {
     "st_kt5": dict(desc=dw(32, (5, 3, 3), (2, 1, 1), in_spatial=(7, 8)), B=2),
     "st_kt1": dict(desc=dw(16, (1, 3, 3), (0, 1, 1), in_spatial=(6, 5)), B=2),
     "st_5x5_nopad": dict(desc=dw(16, (3, 5, 5), (0, 0, 0), in_spatial=(9, 8)), B=2),
+    # enough (stream, row, segment) units that every K2s CTA wraps its stage ring
+    # several times; W = 56 splits each row into two segments, C3-a shape at 24 streams
+    "st_c3a_many": dict(desc=dw(192, (3, 3, 3), (0, 1, 1), in_spatial=(28, 28)), B=24),
+    "st_w56_seg": dict(desc=dw(64, (3, 3, 3), (0, 1, 1), in_spatial=(10, 56)), B=24),
     # C3-b shaped: temporal only 5x1x1
     "t_c3b": dict(desc=dw(192, (5, 1, 1), in_spatial=(28, 28)), B=2),
     "t_kt9_dil2": dict(desc=dw(64, (9, 1, 1), dilation=(2, 1, 1), in_spatial=(25, 1), rank=1), B=3),
@@ -83,6 +87,23 @@ def test_depthwise_vs_oracle_and_direct(case):
     conv, y, ref, yd = _run(case)
     assert rel_err(y, ref) <= 1e-4          # fp32 outputs of bf16 x bf16 products, fp32 sums
     assert np.array_equal(y, yd)            # same summation order as k_step_direct
+
+
+ST_CASES = [c for c in CASES if c.startswith("st_")]
+
+
+@pytest.mark.parametrize("case", ST_CASES)
+def test_depthwise_stencil_dispatch_and_per_thread_variant(case):
+    """Stencils dispatch to the segment-pipeline K2s (k_step_dw_seg: state rows
+    and input-row pieces through a bulk-copy stage ring) by default; option
+    dw_seg = 0 keeps the per-thread-load K2 (k_step_dw_st).  Both equal the
+    fp64 oracle and k_step_direct bit for bit (same per-slice FMA order)."""
+    conv, y, ref, yd = _run(case, steps=6)
+    assert conv.kernel_name.startswith("k_step_dw_seg"), conv.kernel_name
+    set_opt("dw_seg", 0)
+    conv0, y0, ref0, yd0 = _run(case, steps=6)
+    assert conv0.kernel_name.startswith("k_step_dw_st"), conv0.kernel_name
+    assert np.array_equal(y0, y) and np.array_equal(y0, yd0)
 
 
 @pytest.mark.parametrize("case", list(CASES))

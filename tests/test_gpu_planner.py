@@ -8,7 +8,7 @@ pytestmark = pytest.mark.gpu
 
 EXPECTED = {
     2: ["k_step_dense_tc<3,32,3,3x3x64,pair>"],                      # HALO, CTA pair, 150 KB budget
-    3: ["k_step_dw_st<3,3,3>", "k_step_dw_t<5>"],
+    3: ["k_step_dw_seg<3,3,3>", "k_step_dw_t<5>"],                  # K2s segment pipeline, K3
     4: ["k_step_dense_tc<5,32,3,stem>", "k_step_dense_tc<1,128,2,3x3x64,pair>",
         "k_step_dense_tc<3,64,2,3x3,pair,khalo>", "k_step_dense_tc<3,64,2,3x3,pair,khalo>",
         "k_step_dense_tc<3,64,2,3x3,pair,khalo>"],                   # STEM, HALO pair, 3 x KHALO (stride 2 / 1 / 2)
