@@ -377,8 +377,6 @@ __global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_seg(const DwParam
   const int g = tid / p.gthreads, tg = tid - g * p.gthreads;
   const bool active = tg < p.Cq * p.spu;
   const int q = tg % p.Cq, sp = tg / p.Cq;                          // channel quad, strip of the unit
-  const float4* wq = wt + q * NT;
-  const float4 bias4 = reinterpret_cast<const float4*>(bs)[q];
   const int cstep = p.C;                                            // elements between pixels (x, y, state)
   for (int64_t j = lo + g; j < hi; j += p.ngroups) {
     const int64_t i = j - lo;
@@ -389,17 +387,19 @@ __global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_seg(const DwParam
     const int r = int(ju - uint32_t(b) * uint32_t(rows_u));
     const int ho = r / p.nseg, wo0 = (r - ho * p.nseg) * p.WS;
     const int wsz = min(p.WS, p.Wo - wo0);
-    if (active && sp * PX < wsz) {
+    const int c0 = sp * PX;                                         // first staged column / pixel of the strip
+    const int nv = wsz - c0;                                        // real pixels of the strip (compared with
+    if (active && nv > 0) {                                         // the unrolled index: no per-pixel constants)
       const uint8_t* st = stages + int64_t(s) * p.stage_bytes;
-      const int c0 = sp * PX;                                       // first staged column / pixel of the strip
       float4 acc[KT][PX];
 #pragma unroll
       for (int k = 0; k < KT; ++k)
 #pragma unroll
         for (int jj = 0; jj < PX; ++jj) acc[k][jj] = make_float4(0.f, 0.f, 0.f, 0.f);
       const __nv_bfloat16* xr = reinterpret_cast<const __nv_bfloat16*>(st + p.x_off) + int64_t(c0) * cstep + 4 * q;
-#pragma unroll
-      for (int u = 0; u < KH; ++u) {
+      const float4* wq = wt + q * NT;
+#pragma unroll 1                                                    // rolled: fewer live registers (no spills)
+      for (int u = 0; u < KH; ++u, wq += KW) {
         float4 xv[PX + KW - 1];
 #pragma unroll
         for (int t = 0; t < PX + KW - 1; ++t) xv[t] = ld_bf16x4(xr + t * cstep);
@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_seg(const DwParam
         for (int v = 0; v < KW; ++v)
 #pragma unroll
           for (int k = 0; k < KT; ++k) {
-            const float4 w = wq[(k * KH + u) * KW + v];
+            const float4 w = wq[k * KH * KW + v];
 #pragma unroll
             for (int jj = 0; jj < PX; ++jj) acc[k][jj] = f4_fma(w, xv[jj + v], acc[k][jj]);
           }
@@ -416,6 +416,7 @@ __global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_seg(const DwParam
       // emit / accumulate / start (apply()'s arithmetic); the read slots come
       // from the stage only now, so no registers hold them across the taps
       const float4* ss4 = reinterpret_cast<const float4*>(st) + int64_t(c0) * p.Cq + q;   // [KT-1][WS][Cq]
+      const float4 bias4 = reinterpret_cast<const float4*>(bs)[q];  // re-read per unit: 4 registers fewer
       const int64_t pin0 = int64_t(ho) * p.Wo + wo0 + c0;
       const int64_t yoff = b * p.y_bstride + pin0 * cstep + 4 * q;
       float* sp_k[KT > 1 ? KT - 1 : 1];                             // written slot rows of pixel 0 of the strip
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_seg(const DwParam
         sp_k[k] = p.state + (int64_t(p.slot[k]) * p.plane + b * p.HWo + pin0) * cstep + 4 * q;
 #pragma unroll
       for (int jj = 0; jj < PX; ++jj) {
-        if (c0 + jj >= wsz) continue;
+        if (jj >= nv) continue;
         if (p.emit) {
           float4 v = f4_add(acc[KT - 1][jj], bias4);
           if (KT > 1) v = f4_add(ss4[jj * p.Cq], v);
