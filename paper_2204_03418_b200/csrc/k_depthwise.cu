@@ -310,7 +310,11 @@ __global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_seg(const DwParam
     ptx::fence_mbar_init();
   }
   __syncthreads();
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // see k_step_dw_st
+  // programmatic dependent launch: wait for the previous grid, but never trigger
+  // early -- dependents launch as these CTAs exit.  An early trigger lets a
+  // grid-stride successor (K3 in the C3 chain, several CTAs per SM) place its
+  // CTAs on whichever SMs this persistent grid frees first, unevenly: C3 tick
+  // 0.72 -> 0.62 M stream-steps/s measured with the trigger at entry.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t lo = p.n_units * blockIdx.x / gridDim.x;
   const int64_t hi = p.n_units * (blockIdx.x + 1) / gridDim.x;
