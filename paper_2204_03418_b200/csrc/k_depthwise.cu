@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_seg(const DwParam
   if (tid == 0) {
     for (int s = 0; s < p.nst; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], p.gthreads / 32);
+      ptx::mbar_init(&empty[s], p.ngroups * p.gthreads / 32);
     }
     ptx::fence_mbar_init();
   }
@@ -377,15 +377,29 @@ __global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_seg(const DwParam
     }
     return;
   }
-  // ---- consumers: group g takes units lo + g, lo + g + ngroups, ...
+  // ---- consumers: group g computes units lo + g, lo + g + ngroups, ...  Every
+  // consumer warp waits on every unit's full barrier in order and arrives on its
+  // empty barrier, its group's unit or not: a warp that skipped the other groups'
+  // stages could reach (stage s, fill k) while fill k - 1 -- issued earlier, but
+  // bulk copies complete in any order -- had not landed, and the parity wait
+  // would pass on the phase before (nst is not a multiple of ngroups); seen at
+  // the full C3-a size as one corrupted unit in ~10^5.
   const int g = tid / p.gthreads, tg = tid - g * p.gthreads;
   const bool active = tg < p.Cq * p.spu;
   const int q = tg % p.Cq, sp = tg / p.Cq;                          // channel quad, strip of the unit
   const int cstep = p.C;                                            // elements between pixels (x, y, state)
-  for (int64_t j = lo + g; j < hi; j += p.ngroups) {
-    const int64_t i = j - lo;
-    const int s = int(i % p.nst);
-    ptx::mbar_wait(&full[s], uint32_t(i / p.nst) & 1u);
+  int s = 0, gi = 0;                                                // unit i's stage and group (i mod nst, i mod ngroups)
+  uint32_t ph = 0;
+  for (int64_t j = lo; j < hi; ++j) {
+    ptx::mbar_wait(&full[s], ph);
+    const bool mine = gi == g;
+    const int s_cur = s;
+    if (++s == p.nst) { s = 0; ph ^= 1u; }
+    if (++gi == p.ngroups) gi = 0;
+    if (!mine) {
+      if (lane == 0) ptx::mbar_arrive_relaxed(&empty[s_cur]);
+      continue;
+    }
     const uint32_t ju = uint32_t(j);                                // n_units < 2^31 (plan)
     const int64_t b = ju / uint32_t(rows_u);
     const int r = int(ju - uint32_t(b) * uint32_t(rows_u));
@@ -394,7 +408,7 @@ __global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_seg(const DwParam
     const int c0 = sp * PX;                                         // first staged column / pixel of the strip
     const int nv = wsz - c0;                                        // real pixels of the strip (compared with
     if (active && nv > 0) {                                         // the unrolled index: no per-pixel constants)
-      const uint8_t* st = stages + int64_t(s) * p.stage_bytes;
+      const uint8_t* st = stages + int64_t(s_cur) * p.stage_bytes;
       float4 acc[KT][PX];
 #pragma unroll
       for (int k = 0; k < KT; ++k)
@@ -455,7 +469,7 @@ __global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_seg(const DwParam
       }
     }
     __syncwarp();
-    if (lane == 0) ptx::mbar_arrive_relaxed(&empty[s]);   // the stage's reads are consumed (see dense epilogue)
+    if (lane == 0) ptx::mbar_arrive_relaxed(&empty[s_cur]);   // the stage's reads are consumed (see dense epilogue)
   }
 }
 
