@@ -438,6 +438,10 @@ int co_residual_delay(const co_residual* r, int64_t* delay, int64_t* skip_delay)
  *   "dw_seg"     1 (default) depthwise stencils stream state + input rows
  *                through a bulk-copy stage ring (k_step_dw_seg) | 0 the
  *                per-thread-load K2 (k_step_dw_st)                           [create]
+ *   "mha_ring"   1 (default) step-mode MHA attention streams each stream's
+ *                K / V rings through a bulk-copy stage ring
+ *                (k_mha_attend_ring, <= 16 heads) | 0 the per-lane-load
+ *                kernel (k_mha_attend)                                        [launch]
  * name == NULL resets every option to its default.
  * Errors: CO_ERR_ARG for an unknown name or a value out of range.  Not
  * thread-safe against concurrent creates (set options before building handles). */

@@ -11,7 +11,7 @@ Roofline: the sum over the three launches of max(bytes / HBM, FLOPs / bf16
 peak): projections are GEMMs (8 B E^2 FLOPs per step), the attention reads the
 2 n E bf16 KV ring per stream (HBM-bound).
 
-usage: python scripts/bench_mha.py [--steps K] [--warmup W] [--streams B] [--window n]
+usage: python scripts/bench_mha.py [--steps K] [--warmup W] [--streams B] [--window n] [--option name=value]
 """
 from __future__ import annotations
 
@@ -33,11 +33,15 @@ def main():
     ap.add_argument("--embed", type=int, default=1024)
     ap.add_argument("--heads", type=int, default=16)
     ap.add_argument("--window", type=int, default=64)
+    ap.add_argument("--option", action="append", default=[], help="name=value library option (co_set_option)")
     a = ap.parse_args()
     import torch
     import paper_2204_03418_b200 as co
     from bench import ClockSampler, measured_peaks
     B, E, H, n = a.streams, a.embed, a.heads, a.window
+    for kv in a.option:
+        k, v = kv.split("=")
+        co.set_option(k, int(v))
     g = torch.Generator(device="cuda").manual_seed(7)
     w_in = torch.randn((3 * E, E), generator=g, device="cuda") / E ** 0.5
     w_out = torch.randn((E, E), generator=g, device="cuda") / E ** 0.5
@@ -52,8 +56,10 @@ def main():
     sampler = ClockSampler(torch.cuda.current_device())
     with sampler:
         e0.record()
+        h0 = time.perf_counter()
         for t in range(a.steps):
             assert m.forward_step(pool[t % 16], out=y) is not None
+        host_us = (time.perf_counter() - h0) / a.steps * 1e6      # host time per call (launch-bound check)
         e1.record()
         t_end = time.time() + 60
         while not e1.query() and time.time() < t_end:
@@ -71,7 +77,7 @@ def main():
            "higher_is_better": True, "dtype": "bf16", "data": "synthetic (seeded N(0,1) steps, N(0,1/E) weights)",
            "config": {"workload": f"CoOadTR-style attention E={E} heads={H} window={n}", "streams": B,
                       "kv_ring_MB": round(2 * n * B * E * 2 / 1e6, 1)},
-           "gpu_launches": 3 * a.steps,
+           "gpu_launches": 3 * a.steps, "host_us_per_step": round(host_us, 1), "options": a.option,
            "roofline": {"bound": "hbm+tensor", "t_roof_us": round(t_roof * 1e6, 2),
                         "frac": round(t_roof / (ms / 1e3), 4), "attention_bytes_per_step": att_bytes,
                         "projection_flops_per_step": proj_flops, "peak_hbm_gbs": hbm, "peak_bf16_tflops": bf16,
