@@ -163,6 +163,44 @@ def test_fullsize_chunked_steps_equal_per_step_fold(cid, layer, monkeypatch):
     assert torch.equal(sa, sb)
 
 
+def test_fullsize_k2s_pipeline_repeats_equal_k2():
+    """Race detector for the K2s stage pipeline at the full C3-a size (512
+    streams: ~29 K units per launch): three per-step folds through k_step_dw_seg
+    equal the per-thread-load K2 (dw_seg = 0) bit for bit -- outputs and final
+    state.  (Before every consumer warp waited on every stage's barrier in order,
+    a group could pass a parity wait one phase early: one corrupted unit in ~1e5,
+    in a different stream on every run.)"""
+    import paper_2204_03418_b200 as co
+    from paper_2204_03418_b200 import synth
+    cfg = synth.config(3)
+    L = cfg.layers[0]
+    Wt, bt = synth.params(cfg)[0]
+    T = 6
+    set_opt("chunk", 0)
+    g = torch.Generator(device="cuda").manual_seed(23)
+    clip = co.channels_last(torch.randn((cfg.n_streams, L.cin, T) + tuple(cfg.in_spatial), generator=g,
+                                        device="cuda").to(torch.bfloat16))
+
+    def run(seg):
+        set_opt("dw_seg", seg)
+        conv = co.Conv(L.cin, L.cout, L.kernel, weight=Wt.cuda(), bias=bt.cuda(), stride=L.stride,
+                       padding=L.padding, dilation=L.dilation, groups=L.groups, spatial_rank=cfg.spatial_rank,
+                       in_spatial=tuple(cfg.in_spatial), n_streams=cfg.n_streams, dtype=cfg.dtype,
+                       out_dtype=torch.float32)
+        assert conv.kernel_name.startswith("k_step_dw_seg" if seg else "k_step_dw_st"), conv.kernel_name
+        ys, _ = conv.forward_steps(clip)
+        st, _ = conv.state_dict_stream()
+        torch.cuda.synchronize()
+        return ys, st
+
+    y0, s0 = run(0)
+    for rep in range(3):
+        y1, s1 = run(1)
+        assert torch.equal(y1, y0), (rep, int((y1 != y0).sum()))
+        assert torch.equal(s1, s0), rep
+        del y1, s1
+
+
 def _sample_streams(B):
     return sorted({0, B // 2, B - 1})
 
