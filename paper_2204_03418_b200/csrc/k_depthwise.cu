@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_seg(const DwParam
   if (tid == 0) {
     for (int s = 0; s < p.nst; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], p.ngroups * p.gthreads / 32);
+      ptx::mbar_init(&empty[s], p.gthreads / 32);
     }
     ptx::fence_mbar_init();
   }
@@ -377,29 +377,29 @@ __global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_seg(const DwParam
     }
     return;
   }
-  // ---- consumers: group g computes units lo + g, lo + g + ngroups, ...  Every
-  // consumer warp waits on every unit's full barrier in order and arrives on its
-  // empty barrier, its group's unit or not: a warp that skipped the other groups'
-  // stages could reach (stage s, fill k) while fill k - 1 -- issued earlier, but
-  // bulk copies complete in any order -- had not landed, and the parity wait
-  // would pass on the phase before (nst is not a multiple of ngroups); seen at
-  // the full C3-a size as one corrupted unit in ~10^5.
+  // ---- consumers: group g takes units lo + g, lo + g + ngroups, ...  A parity
+  // wait must never run more than one phase ahead of its barrier: after unit i
+  // a group waits on unit i + ngroups, whose stage was last filled by unit
+  // i + ngroups - nst -- another group's (nst is not a multiple of ngroups),
+  // issued before unit i, but bulk copies complete in any order.  Had that fill
+  // not landed, the wait on full[] would pass on the phase before (seen at the
+  // full C3-a size as one corrupted unit in ~10^5).  So a consumer first waits
+  // for the stage's previous fill to have been *consumed* (the phase of empty[]
+  // the producer itself waits on before refilling: at most one behind, and its
+  // completion implies that fill landed), then for its own fill.  (Measured
+  // alternatives, both correct: every warp waiting on and releasing every stage
+  // in order, 0.272 ms on C3-a; the producer holding unit i back until unit
+  // i - 2 has landed, 0.284 ms.)
   const int g = tid / p.gthreads, tg = tid - g * p.gthreads;
   const bool active = tg < p.Cq * p.spu;
   const int q = tg % p.Cq, sp = tg / p.Cq;                          // channel quad, strip of the unit
   const int cstep = p.C;                                            // elements between pixels (x, y, state)
-  int s = 0, gi = 0;                                                // unit i's stage and group (i mod nst, i mod ngroups)
-  uint32_t ph = 0;
-  for (int64_t j = lo; j < hi; ++j) {
-    ptx::mbar_wait(&full[s], ph);
-    const bool mine = gi == g;
-    const int s_cur = s;
-    if (++s == p.nst) { s = 0; ph ^= 1u; }
-    if (++gi == p.ngroups) gi = 0;
-    if (!mine) {
-      if (lane == 0) ptx::mbar_arrive_relaxed(&empty[s_cur]);
-      continue;
-    }
+  for (int64_t j = lo + g; j < hi; j += p.ngroups) {
+    const int64_t i = j - lo;
+    const int s_cur = int(i % p.nst);
+    const uint32_t fill = uint32_t(i / p.nst);
+    if (fill > 0) ptx::mbar_wait(&empty[s_cur], (fill & 1u) ^ 1u);
+    ptx::mbar_wait(&full[s_cur], fill & 1u);
     const uint32_t ju = uint32_t(j);                                // n_units < 2^31 (plan)
     const int64_t b = ju / uint32_t(rows_u);
     const int r = int(ju - uint32_t(b) * uint32_t(rows_u));
