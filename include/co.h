@@ -442,6 +442,10 @@ int co_residual_delay(const co_residual* r, int64_t* delay, int64_t* skip_delay)
  *                K / V rings through a bulk-copy stage ring
  *                (k_mha_attend_ring, <= 16 heads) | 0 the per-lane-load
  *                kernel (k_mha_attend)                                        [launch]
+ *   "pool_seg"   1 (default) bf16 pooling layers with a spatial window and a
+ *                direct temporal fold stream input rows + ring rows through
+ *                a bulk-copy stage ring (k_step_pool_seg) | 0 the band /
+ *                plain kernels                                                [create / launch]
  * name == NULL resets every option to its default.
  * Errors: CO_ERR_ARG for an unknown name or a value out of range.  Not
  * thread-safe against concurrent creates (set options before building handles). */

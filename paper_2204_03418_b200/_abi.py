@@ -28,7 +28,7 @@ KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 # defaults of the documented options (include/co.h co_set_option)
 OPTION_DEFAULTS = {"tc_mode": 0, "khalo": 1, "pair": 0, "kpair": 0, "eg": 0, "mc": 1, "pdl": 1, "chunk": 1,
                    "chunk_flat": 0, "chunk_st": 0, "chunk_t": 0, "pool_band": 1, "pool_vh": -1, "pool_g": 0, "log": 0,
-                   "stem": 1, "dw_seg": 1, "mha_ring": 1}
+                   "stem": 1, "dw_seg": 1, "mha_ring": 1, "pool_seg": 1}
 
 # every entry point include/co.h declares (checked by tests/test_abi_load.py)
 EXPORTS = ["co_conv_create", "co_conv_destroy", "co_conv_info", "co_delay", "co_kernel_name",

@@ -15,7 +15,7 @@ constexpr int kMaxKt = 32;   // == CO_MAX_KT
 // Documented planner / launch options (include/co.h co_set_option; options.cu).
 enum Opt : int {
   OPT_TC_MODE, OPT_KHALO, OPT_PAIR, OPT_KPAIR, OPT_EG, OPT_MC, OPT_PDL, OPT_CHUNK, OPT_CHUNK_FLAT, OPT_CHUNK_ST,
-  OPT_CHUNK_T, OPT_POOL_BAND, OPT_POOL_VH, OPT_POOL_G, OPT_LOG, OPT_STEM, OPT_DW_SEG, OPT_MHA_RING, OPT_COUNT
+  OPT_CHUNK_T, OPT_POOL_BAND, OPT_POOL_VH, OPT_POOL_G, OPT_LOG, OPT_STEM, OPT_DW_SEG, OPT_MHA_RING, OPT_POOL_SEG, OPT_COUNT
 };
 int64_t option(Opt o);
 void set_thread_no_pdl(int v);   // graph capture fallback: plain launches on this thread

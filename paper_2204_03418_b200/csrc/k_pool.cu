@@ -28,6 +28,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 namespace co {
 
@@ -657,11 +658,216 @@ cudaError_t step_split(const Geom& g, const StepArgs& a, int G, cudaStream_t s) 
   return cudaLaunchKernelEx(&cfg, k_step_pool_split<Tin, Tout, Tr, V, MAX, VH>, g, a);
 }
 
+// ------------------------------------------------------------------ row pipeline (k_step_pool_seg)
+// The band kernel's work with its memory traffic decoupled from the arithmetic
+// (the K2s recipe, k_depthwise.cu): the band kernel stages a row's input rows
+// with cp.async, waits for them, reduces, then reads its ring slots -- one
+// dependent chain per block, ~0.5 of HBM on the I3D-style 3x3x3 max pool.  Here
+// a block walks a contiguous range of units (stream, output row); a producer
+// thread streams each unit's input rows (one contiguous run, clipped to the
+// frame) and, on Ready steps, the kt - 1 older ring-slot rows into a ring of
+// shared-memory stages by bulk copies; every consumer warp consumes every stage
+// (thread = (output pixel, V-channel vector)), reducing the window from shared
+// memory in the plain kernel's tap order and folding the ring rows in its slot
+// order -- the same operations in the same order, so results are bitwise those
+// of k_step_pool / k_step_pool_band.  Direct-fold windows only (kt < 6).
+struct PoolSegPlan {
+  int nst, stage_bytes;       // stage ring
+  int x_rows, xrow_b;         // staged input rows per unit, bytes per input row
+  int rrow_b, r_off;          // bytes per ring-slot row, offset of the ring rows in a stage
+  int cwarps;                 // consumer warps
+  int per_sm;
+};
+
+template <typename Tin, typename Tout, typename Tr, int V, bool MAX, int KHW = 0>
+__global__ void __launch_bounds__(1024) k_step_pool_seg(Geom g, StepArgs a, PoolSegPlan pl) {
+  // KHW > 0: compile-time KH x KW window (dilation 1), taps unrolled
+  constexpr int CKH = KHW / 10, CKW = KHW % 10;
+  extern __shared__ __align__(128) uint8_t seg_smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(seg_smem + size_t(pl.nst) * pl.stage_bytes);
+  uint64_t* empty = full + pl.nst;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < pl.nst; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], pl.cwarps);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // see k_step_pool_split
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int64_t units = g.B * g.Ho;
+  const int64_t lo = units * blockIdx.x / gridDim.x, hi = units * (blockIdx.x + 1) / gridDim.x;
+  const int64_t SE = g.B * g.HWo * g.Cin;
+  Tr* ring = reinterpret_cast<Tr*>(a.state);
+  const Tin* x = static_cast<const Tin*>(a.x);
+  const int nring = a.emit ? g.kt - 1 : 0;
+  if (warp == pl.cwarps) {                          // ---- producer thread
+    if (lane != 0) return;
+    int s = 0;
+    uint32_t ph = 0;                                // fill k of a stage waits for empty phase k - 1: parity ph ^ 1
+    bool refill = false;
+    int64_t b = lo / g.Ho;
+    int ho = int(lo - b * g.Ho);
+    for (int64_t u = lo; u < hi; ++u) {
+      if (refill) ptx::mbar_wait(&empty[s], ph ^ 1u);
+      uint8_t* st = seg_smem + size_t(s) * pl.stage_bytes;
+      const int hi0 = ho * g.sh - g.ph;
+      const int r_lo = max(hi0, 0), r_hi = min(hi0 + pl.x_rows - 1, g.H - 1);
+      const uint32_t xb = (x && r_hi >= r_lo) ? uint32_t(r_hi - r_lo + 1) * uint32_t(pl.xrow_b) : 0u;
+      const uint32_t tx = xb + uint32_t(nring) * uint32_t(pl.rrow_b);
+      if (tx == 0) {
+        ptx::mbar_arrive(&full[s]);
+      } else {
+        ptx::mbar_arrive_expect_tx(&full[s], tx);
+        if (xb) ptx::bulk_g2s(st + (r_lo - hi0) * pl.xrow_b, x + b * a.x_bstride + int64_t(r_lo) * g.W * g.Cin, xb, &full[s]);
+        for (int k = 0; k < nring; ++k) {
+          const int slot = wrap_sub(a.pm_f, (g.kt - 1 - k) * g.dt, g.f);
+          ptx::bulk_g2s(st + pl.r_off + k * pl.rrow_b,
+                        ring + int64_t(slot) * SE + (b * g.HWo + int64_t(ho) * g.Wo) * g.Cin, uint32_t(pl.rrow_b),
+                        &full[s]);
+        }
+      }
+      if (++s == pl.nst) { s = 0; ph ^= 1u; refill = true; }
+      if (++ho == g.Ho) { ho = 0; ++b; }
+    }
+    return;
+  }
+  // ---- consumers: thread = (output pixel wo, channel vector) of the unit's row
+  const int CV = g.Cin / V;
+  const bool active = tid < g.Wo * CV;
+  const int wo = tid / CV, c0 = (tid - wo * CV) * V;
+  const int w0 = wo * g.sw - g.pw;
+  int s = 0;
+  uint32_t ph = 0;
+  int64_t b = lo / g.Ho;
+  int ho = int(lo - b * g.Ho);
+  for (int64_t u = lo; u < hi; ++u) {
+    ptx::mbar_wait(&full[s], ph);
+    if (active) {
+      const uint8_t* st = seg_smem + size_t(s) * pl.stage_bytes;
+      const Tin* xs = reinterpret_cast<const Tin*>(st);
+      float sv[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) sv[j] = MAX ? -INFINITY : 0.f;
+      if (x && KHW > 0) {
+        const int hi0 = ho * g.sh - g.ph;
+        const Tin* xb = xs + w0 * g.Cin + c0;
+#pragma unroll
+        for (int uu = 0; uu < CKH; ++uu) {
+          if (hi0 + uu < 0 || hi0 + uu >= g.H) continue;
+#pragma unroll
+          for (int v = 0; v < CKW; ++v) {
+            if (w0 + v < 0 || w0 + v >= g.W) continue;
+            const Vec<Tin, V> xv = *reinterpret_cast<const Vec<Tin, V>*>(xb + (uu * g.W + v) * g.Cin);
+#pragma unroll
+            for (int j = 0; j < V; ++j) sv[j] = MAX ? fmaxf(sv[j], to_f(xv.v[j])) : sv[j] + to_f(xv.v[j]);
+          }
+        }
+      } else if (x) {
+        const int hi0 = ho * g.sh - g.ph;
+        for (int uu = 0; uu < g.kh; ++uu) {
+          const int hr = hi0 + uu * g.dh;
+          if (hr < 0 || hr >= g.H) continue;
+          for (int v = 0; v < g.kw; ++v) {
+            const int wi = w0 + v * g.dw;
+            if (wi < 0 || wi >= g.W) continue;
+            const Vec<Tin, V> xv = *reinterpret_cast<const Vec<Tin, V>*>(xs + ((uu * g.dh) * g.W + wi) * g.Cin + c0);
+#pragma unroll
+            for (int j = 0; j < V; ++j) sv[j] = MAX ? fmaxf(sv[j], to_f(xv.v[j])) : sv[j] + to_f(xv.v[j]);
+          }
+        }
+      }
+      const int64_t r = b * g.HWo + int64_t(ho) * g.Wo + wo;
+      if (a.slot[0] >= 0) {
+        Vec<Tr, V> w;
+#pragma unroll
+        for (int j = 0; j < V; ++j) w.v[j] = from_f<Tr>(sv[j]);
+        *reinterpret_cast<Vec<Tr, V>*>(ring + int64_t(a.slot[0]) * SE + r * g.Cin + c0) = w;
+      }
+      if (a.emit) {
+        float win[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) win[j] = MAX ? -INFINITY : 0.f;
+        const Tr* rs = reinterpret_cast<const Tr*>(st + pl.r_off) + wo * g.Cin + c0;
+        for (int k = 0; k + 1 < g.kt; ++k) {
+          const Vec<Tr, V> q = *reinterpret_cast<const Vec<Tr, V>*>(reinterpret_cast<const uint8_t*>(rs) + k * pl.rrow_b);
+#pragma unroll
+          for (int j = 0; j < V; ++j) win[j] = MAX ? fmaxf(win[j], to_f(q.v[j])) : win[j] + to_f(q.v[j]);
+        }
+        combine<V, MAX>(win, sv);
+        store_out<Tout, V, MAX>(g, reinterpret_cast<Tout*>(a.y) + b * a.y_bstride + (r - b * g.HWo) * g.Cout + c0, win);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive_relaxed(&empty[s]);   // the stage's reads are consumed
+    if (++s == pl.nst) { s = 0; ph ^= 1u; }
+    if (++ho == g.Ho) { ho = 0; ++b; }
+  }
+}
+
+// Plan of the row pipeline; false: the shape keeps the band / plain kernels.
+bool pool_seg_plan(const Geom& g, int V, PoolSegPlan& pl) {
+  if (option(OPT_POOL_SEG) == 0 || g.pool_vh || g.pool_G > 1 || g.kh * g.kw < 2 || g.in_dtype != BF16) return false;
+  const int esz = 2, resz = pool_ring_esz(g);
+  const int CV = g.Cin / V;
+  const int items = g.Wo * CV;
+  if (items > 992 || g.Cin % V) return false;
+  pl.cwarps = (items + 31) / 32;
+  pl.x_rows = (g.kh - 1) * g.dh + 1;
+  pl.xrow_b = g.W * g.Cin * esz;
+  pl.rrow_b = g.Wo * g.Cin * resz;
+  if (pl.xrow_b % 16 || pl.rrow_b % 16) return false;
+  pl.r_off = (pl.x_rows * pl.xrow_b + 127) / 128 * 128;
+  pl.stage_bytes = (pl.r_off + (g.kt - 1) * pl.rrow_b + 127) / 128 * 128;
+  // two blocks per SM with 3-4 stages each when they fit, else one block with up to 6
+  const int threads = pl.cwarps * 32 + 32;
+  if (4 * pl.stage_bytes <= 100 * 1024 && threads <= 512) { pl.nst = 4; pl.per_sm = 2; }
+  else if (3 * pl.stage_bytes <= 100 * 1024 && threads <= 512) { pl.nst = 3; pl.per_sm = 2; }
+  else {
+    pl.nst = std::min(6, int((200 * 1024) / pl.stage_bytes));
+    pl.per_sm = 1;
+    if (pl.nst < 3) return false;
+  }
+  return true;
+}
+
+template <typename Tin, typename Tout, typename Tr, int V, bool MAX, int KHW = 0>
+cudaError_t step_seg(const Geom& g, const StepArgs& a, const PoolSegPlan& pl, cudaStream_t s) {
+  const size_t smem = size_t(pl.nst) * pl.stage_bytes + 2 * size_t(pl.nst) * sizeof(uint64_t);
+  static size_t set_smem = 0;                      // (per instantiation)
+  if (smem > set_smem) {
+    cudaError_t e = cudaFuncSetAttribute(k_step_pool_seg<Tin, Tout, Tr, V, MAX, KHW>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    set_smem = smem;
+  }
+  const int64_t units = g.B * g.Ho;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(num_sms()) * pl.per_sm))));
+  cfg.blockDim = dim3(unsigned(pl.cwarps * 32 + 32));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pool_pdl() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_step_pool_seg<Tin, Tout, Tr, V, MAX, KHW>, g, a, pl);
+}
+
 template <typename Tin, typename Tout, typename Tr, int V, bool MAX>
 cudaError_t step_v(const Geom& g, const StepArgs& a, cudaStream_t s) {
   if (g.pool_G > 1)
     return g.pool_vh ? step_split<Tin, Tout, Tr, V, MAX, true>(g, a, g.pool_G, s)
                      : step_split<Tin, Tout, Tr, V, MAX, false>(g, a, g.pool_G, s);
+  if constexpr (std::is_same<Tin, __nv_bfloat16>::value) {
+    PoolSegPlan spl;
+    if (pool_seg_plan(g, V, spl) && (!a.x || (reinterpret_cast<uintptr_t>(a.x) % 16 == 0 && (a.x_bstride * 2) % 16 == 0)))
+      return (g.kh == 3 && g.kw == 3 && g.dh == 1 && g.dw == 1) ? step_seg<Tin, Tout, Tr, V, MAX, 33>(g, a, spl, s)
+                                                                 : step_seg<Tin, Tout, Tr, V, MAX>(g, a, spl, s);
+  }
   const int64_t total = g.B * g.HWo * (g.Cin / V);
   const int grid = grid_for(total);
   const int khw = (g.dh == 1 && g.dw == 1 && g.kh <= 3 && g.kw <= 3 && g.kh == g.kw) ? g.kh * 10 + g.kw : 0;
@@ -827,7 +1033,9 @@ std::string pool_kernel_name(const Geom& g) {
   const char* vh = g.pool_vh ? ",vh" : "";
   int rows;
   size_t smem;
+  PoolSegPlan spl;
   if (G > 1) snprintf(out, 64, "k_step_pool_split<%s,V%d,G%d%s>", kind, vec_width(g), G, vh);
+  else if (pool_seg_plan(g, vec_width(g), spl)) snprintf(out, 64, "k_step_pool_seg<%s,V%d>", kind, vec_width(g));
   else if (pool_band_enabled() && band_rows(g, vec_width(g), rows, smem) > 0)
     snprintf(out, 64, "k_step_pool_band<%s,V%d%s>", kind, vec_width(g), vh);
   else snprintf(out, 64, "k_step_pool<%s,V%d%s>", kind, vec_width(g), vh);

@@ -30,7 +30,7 @@ constexpr OptDef kOpts[OPT_COUNT] = {
     {"chunk_flat", 0, 0, 1},  {"chunk_st", 0, 0, 1},    {"chunk_t", 0, 0, 1 << 20},
     {"pool_band", 1, 0, 1},   {"pool_vh", -1, -1, 1},   {"pool_g", 0, 0, 32},    {"log", 0, 0, 1},
     {"stem", 1, 0, 1},        {"dw_seg", 1, 0, 1},
-    {"mha_ring", 1, 0, 1},
+    {"mha_ring", 1, 0, 1},    {"pool_seg", 1, 0, 1},
 };
 
 std::atomic<int64_t> g_val[OPT_COUNT] = {};

@@ -67,8 +67,8 @@ def _compare(kind, y, ref, out_dtype):
         assert rel_err(y, ref) <= 1e-4
 
 
-@pytest.fixture(params=[("auto", None), ("1", "0"), ("3", "0"), ("1", "1"), ("3", "1"), ("1b", "0")],
-                ids=["auto", "G1_fold", "G3_fold", "G1_vh", "G3_vh", "G1_fold_noband"])
+@pytest.fixture(params=[("auto", None), ("1", "0"), ("3", "0"), ("1", "1"), ("3", "1"), ("1b", "0"), ("1s", "0")],
+                ids=["auto", "G1_fold", "G3_fold", "G1_vh", "G3_vh", "G1_fold_noband", "G1_fold_noseg"])
 def pool_lanes(request, monkeypatch):
     """Step-kernel variant (k_pool.cu): AUTO, or forced lanes (CO_POOL_G: 1 =
     plain kernel, 3 = split kernel) x temporal scheme (CO_POOL_VH: 0 = direct
@@ -78,6 +78,10 @@ def pool_lanes(request, monkeypatch):
     if G == "1b":                                  # the plain kernel without the row-band staging
         G = "1"
         set_opt("pool_band", "0")
+        set_opt("pool_seg", "0")
+    if G == "1s":                                  # the band kernel instead of the bulk-copy row pipeline
+        G = "1"
+        set_opt("pool_seg", "0")
     if G != "auto":
         set_opt("pool_g", G)
         set_opt("pool_vh", vh)
@@ -272,3 +276,60 @@ def test_block_decomposition_state_round_trip(kind, monkeypatch):
             for b in ahead.pop(t, []):
                 assert torch.equal(b, y)
     assert not ahead or max(ahead) >= len(frames) - 1
+
+
+@pytest.mark.parametrize("kind", ["max", "avg"])
+@pytest.mark.parametrize("shape", [
+    # kernel,      stride,    pad,       dil,       H,  W,  C,  B
+    ((3, 3, 3), (1, 2, 2), (0, 1, 1), (1, 1, 1), 14, 14, 64, 5),     # the I3D-style bench shape, reduced
+    ((2, 3, 2), (1, 1, 2), (1, 2, 0), (2, 2, 1), 9, 12, 16, 3),      # temporal / row dilation, padded rows
+    ((4, 2, 3), (2, 2, 1), (2, 0, 2), (1, 1, 2), 7, 10, 8, 2),       # temporal stride, column dilation
+    ((1, 3, 3), (1, 1, 1), (0, 1, 1), (1, 1, 1), 8, 8, 24, 200),     # kt = 1 (no ring rows), more units than SMs
+])
+def test_pool_row_pipeline_vs_oracle_and_band(kind, shape):
+    """k_step_pool_seg (bulk-copy row pipeline, option pool_seg) against the fp64
+    pooling oracle over readiness, Ready ticks, an update_state = 0 probe and
+    pad_end steps, and bit for bit against the band / plain kernels (pool_seg =
+    0): same taps and ring slots in the same order."""
+    kernel, stride, pad, dil, H, W, C, B = shape
+    rng = np.random.default_rng(sum(kernel) * 7 + C)
+    outs = {}
+    for seg in (1, 0):
+        set_opt("pool_seg", seg)
+        set_opt("pool_g", 1)                       # (small shapes would otherwise take the split kernel)
+        rs = np.random.default_rng(1234)
+        p, sm = _make(kind, 2, kernel, stride, pad, dil, H, W, C, B, torch.bfloat16, torch.float32)
+        assert p.kernel_name.startswith("k_step_pool_seg" if seg else "k_step_pool"), p.kernel_name
+        assert seg or "seg" not in p.kernel_name
+        ys = []
+        T = sm.f + 2 * stride[0] + 4
+        for t in range(T):
+            xq = _quant(rs.standard_normal((B, C, H, W)), torch.bfloat16)
+            if t == sm.f + 1:
+                probe = _quant(rs.standard_normal((B, C, H, W)), torch.bfloat16)
+                yp = p.forward_step(_tcl(probe, torch.bfloat16), update_state=False)
+                rp = sm.forward_step(probe, update_state=False)
+                assert (yp is None) == (rp is None)
+                if yp is not None:
+                    ys.append(np_of(yp))
+                    if seg:
+                        _compare(kind, ys[-1].reshape(rp.shape), rp, torch.float32)
+            y = p.forward_step(_tcl(xq, torch.bfloat16))
+            r = sm.forward_step(xq)
+            assert (y is None) == (r is None), t
+            if y is not None:
+                ys.append(np_of(y))
+                if seg:
+                    _compare(kind, ys[-1].reshape(r.shape), r, torch.float32)
+        for _ in range(pad[0]):
+            y = p.forward_pad_step()
+            r = sm.forward_step(None)
+            assert (y is None) == (r is None)
+            if y is not None:
+                ys.append(np_of(y))
+                if seg:
+                    _compare(kind, ys[-1].reshape(r.shape), r, torch.float32)
+        outs[seg] = ys
+    assert len(outs[1]) == len(outs[0]) and len(outs[1]) > 0
+    for a, b in zip(outs[1], outs[0]):
+        np.testing.assert_array_equal(a, b)
