@@ -238,11 +238,12 @@ def ncu_traffic(key):
 
 def state_of(cfg, args):
     """State layout per config: BASELINE.json states 'fp32 state' for C2-C4 (the
-    partial-sum ring) and C1 is fp32 throughout; C5 states only
-    'bf16', so the planner's layout choice (CO_STATE_AUTO) applies there."""
+    partial-sum ring) and C1 is fp32 throughout; C3 and C5 state only
+    'bf16', so the planner's layout choice (CO_STATE_AUTO) applies there (C3: the
+    stencil keeps its partial sums, the temporal-only layer takes the RAW ring)."""
     if args.state != "config":
         return args.state
-    return "auto" if cfg.cid == 5 else "psum"
+    return "auto" if cfg.cid in (3, 5) else "psum"
 
 
 def build_layers(cfg, B, kernel="auto", state="psum"):
@@ -661,11 +662,11 @@ def run_all(args, world, rank):
             e2, _ = run_config(cfg, args, world, rank, label=cfg.workload + " [planner layouts: RAW-ring stem]",
                                state="auto")
             configs["C4/auto"] = e2
-        if cid == 5 and args.config == "all" and args.state == "config" and entry["state"] != ["psum"]:
-            # C5's companion: the fp32 partial-sum layout against its own roofline
+        if cid in (3, 5) and args.config == "all" and args.state == "config" and set(entry["state"]) != {"psum"}:
+            # C3's / C5's companion: the fp32 partial-sum layout against its own roofline
             e2, _ = run_config(cfg, args, world, rank, label=cfg.workload + " [fp32 partial-sum state]",
                                state="psum")
-            configs["C5/psum"] = e2
+            configs[f"C{cid}/psum"] = e2
         del ctx
         gc.collect()
         torch.cuda.empty_cache()

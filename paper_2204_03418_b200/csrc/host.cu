@@ -228,6 +228,12 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
     // tensor cores with its weights resident
     co::StemRawPlan sp;
     if (!g.raw && g.kt > 1 && 2.0 * raw_b <= psum_b && co::stem_raw_plan(g, sp)) g.raw = 1;
+    // temporal-only depthwise layers (C3-b): one streaming pass over the window's
+    // frames with the frame store fused (k_step_dw_traw), (kt + 2) bf16 frame
+    // accesses against 2 + 4 (kt - 1) for the partial sums
+    if (!g.raw && d->in_dtype == CO_BF16 && flat && g.kt > 1 && 2.0 * raw_b <= psum_b && d->groups == g.Cin &&
+        g.Cin == g.Cout && g.Cin % 8 == 0)
+      g.raw = 1;
   }
   if (g.op == CO_OP_DELAY) {
     if (g.kh != 1 || g.kw != 1 || g.sh != 1 || g.sw != 1 || g.ph || g.pw || g.dh != 1 || g.dw != 1 || g.pt ||
@@ -475,8 +481,10 @@ static int step_raw(co_conv* h, int64_t& n, float* state, const void* x, int64_t
   char* slot = reinterpret_cast<char*>(state) + size_t(cur) * g.B * fb;
   // a Ready step of the flat tensor-core kernel reads x itself and stores it into the
   // ring from shared memory (no separate copy of the frame); otherwise copy it here
-  const bool fused = r && x && h->kernel_used == CO_KERNEL_DENSE_TC &&
-                     (reinterpret_cast<uintptr_t>(x) & 15) == 0 && co::dense_tc_fuses_raw_store(h->tc, g, x_bstride);
+  const bool fused = r && x && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                     ((h->kernel_used == CO_KERNEL_DENSE_TC && co::dense_tc_fuses_raw_store(h->tc, g, x_bstride)) ||
+                      (h->kernel_used == CO_KERNEL_DEPTHWISE && co::depthwise_fuses_raw_store(h->dw, g, x_bstride) &&
+                       (reinterpret_cast<uintptr_t>(y) & 15) == 0 && (size_t(y_bstride) * dsize(g.out_dtype)) % 16 == 0));
   if (fused) {
   } else if (x) {
     CO_CUDA(cudaMemcpy2DAsync(slot, fb, x, size_t(x_bstride) * dsize(g.in_dtype), fb, g.B, cudaMemcpyDeviceToDevice, s));
@@ -488,7 +496,7 @@ static int step_raw(co_conv* h, int64_t& n, float* state, const void* x, int64_t
     for (int k = 0; k < co::kMaxKt; ++k) a.slot[k] = -1;
     for (int k = 0; k + 1 < g.kt; ++k) a.slot[k] = int(floor_mod(m - int64_t(g.kt - 1 - k) * g.dt, g.f));
     a.slot[g.kt - 1] = cur;
-    a.x = fused ? x : nullptr; a.x_bstride = g.frame_elems;
+    a.x = fused ? x : nullptr; a.x_bstride = fused ? x_bstride : g.frame_elems;
     a.raw_store = fused ? cur : -1;
     a.y = y; a.y_bstride = y_bstride;
     a.state = state;

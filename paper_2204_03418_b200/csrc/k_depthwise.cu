@@ -66,6 +66,7 @@ struct DwParams {
   int64_t n_tiles;
   int WC, HR;                           // halo width (W + 2 pw) and rows (TH + kh - 1)
   int64_t frame;                        // RAW layout: elements of one stream's frame (H*W*C)
+  int raw_store;                        // RAW temporal kernel: ring slot this step's frame (read from x) is stored into
   // K2s segment pipeline (k_step_dw_seg): units = (stream, output row, segment of WS pixels)
   int64_t n_units;
   int nseg, WS, WX, nst, spu, gthreads; // WX = WS + kw - 1 staged input columns; spu strips per unit
@@ -716,6 +717,79 @@ __global__ void __launch_bounds__(1024, 1) k_steps_dw_st(const DwParams p, const
   }
 }
 
+// ------------------------------------------------------------------ RAW layout, temporal only, fused store
+// A Ready step of a temporal-only depthwise layer over the RAW frame ring
+// as one streaming pass: thread item = (pixel, 8 channels), 16-byte
+// accesses; the new frame is read straight from x and stored into its ring slot
+// here (no separate frame copy), the window's kt - 1 older frames come from the
+// ring, y is written once: (kt + 2) frame-sized accesses per step against
+// 2 + 4 (kt - 1) for the fp32 partial sums (C3-b, kt = 5: 2.1 MB against 5.4 MB
+// per stream-step).  Two items per thread, all 2 kt loads issued before the
+// FMAs; per channel the same operations in the same order as k_step_dw_raw.
+template <int KT>
+__global__ void __launch_bounds__(kDwThreads, 3) k_step_dw_traw(const DwParams p) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(p.state);
+  const int64_t B = p.plane / p.HWo;
+  const int Co = p.C / 8;
+  const int64_t n_items = p.plane * Co;
+  const int64_t stride = int64_t(gridDim.x) * kDwThreads;
+  for (int64_t base = int64_t(blockIdx.x) * kDwThreads + threadIdx.x; base < n_items; base += 2 * stride) {
+    uint4 xv[2][KT];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int64_t it = base + j * stride;
+      if (it >= n_items) continue;
+      const int o = int(it % Co);
+      const int64_t pix = it / Co;
+      const int64_t b = pix / p.HWo;
+#pragma unroll
+      for (int k = 0; k < KT - 1; ++k)
+        xv[j][k] = *reinterpret_cast<const uint4*>(ring + (int64_t(p.slot[k]) * B) * p.frame + pix * p.C + 8 * o);
+      xv[j][KT - 1] = *reinterpret_cast<const uint4*>(p.x + b * p.x_bstride + (pix - b * p.HWo) * p.C + 8 * o);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int64_t it = base + j * stride;
+      if (it >= n_items) continue;
+      const int o = int(it % Co);
+      const int64_t pix = it / Co;
+      const int64_t b = pix / p.HWo;
+      if (p.raw_store >= 0)
+        __stcs(reinterpret_cast<uint4*>(ring + (int64_t(p.raw_store) * B) * p.frame + pix * p.C + 8 * o), xv[j][KT - 1]);
+      float4 acc[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        acc[h] = __ldg(reinterpret_cast<const float4*>(p.bias) + 2 * o + h);
+#pragma unroll
+        for (int k = 0; k < KT; ++k) {
+          const uint32_t w0 = h ? xv[j][k].z : xv[j][k].x, w1 = h ? xv[j][k].w : xv[j][k].y;
+          const float4 xf = make_float4(__uint_as_float(w0 << 16), __uint_as_float(w0 & 0xffff0000u),
+                                        __uint_as_float(w1 << 16), __uint_as_float(w1 & 0xffff0000u));
+          acc[h] = f4_add(acc[h], f4_fma(__ldg(reinterpret_cast<const float4*>(p.w + k * p.C) + 2 * o + h), xf,
+                                         make_float4(0.f, 0.f, 0.f, 0.f)));
+        }
+        acc[h] = f4_act(acc[h], p.act);
+      }
+      const int64_t off = b * p.y_bstride + (pix - b * p.HWo) * p.C + 8 * o;
+      if (p.out_f32) {
+        float4* yp = reinterpret_cast<float4*>(static_cast<float*>(p.y) + off);
+        __stcs(yp, acc[0]);
+        __stcs(yp + 1, acc[1]);
+      } else {
+        uint4 u;
+        __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&u);
+        hp[0] = __floats2bfloat162_rn(acc[0].x, acc[0].y);
+        hp[1] = __floats2bfloat162_rn(acc[0].z, acc[0].w);
+        hp[2] = __floats2bfloat162_rn(acc[1].x, acc[1].y);
+        hp[3] = __floats2bfloat162_rn(acc[1].z, acc[1].w);
+        *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + off) = u;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ RAW layout
 // (SURVEY §8f f1): a Ready step reads the window's kt frames from the frame
 // ring (slot[k]) and writes y; no state traffic beyond those reads.  Thread =
@@ -834,6 +908,7 @@ struct DwVariant {
   DwChunkFn chunk = nullptr;            // chunked-steps kernel (temporal only)
   DwFn seg = nullptr;                   // K2s segment-pipeline kernel (spatial stencils)
   int SPX = 4;                          // K2s: output pixels per thread strip
+  DwFn traw = nullptr;                  // RAW layout, temporal only: fused frame store (k_step_dw_traw)
 };
 #ifndef CO_DW_PX
 #define CO_DW_PX 2                      // output pixels per thread strip (experiments: -DCO_DW_PX=n)
@@ -846,7 +921,8 @@ struct DwVariant {
                               (kt <= 3 ? CO_DW_PX : 2), (DwFn)k_step_dw_raw<kt, kh, kw>, \
                               (DwChunkFn)k_steps_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>, \
                               (DwFn)k_step_dw_seg<kt, kh, kw, CO_DW_SEG_PX(kt, kh, kw)>, CO_DW_SEG_PX(kt, kh, kw)}
-#define CO_DW_T(kt) {kt, 1, 1, (DwFn)k_step_dw_t<kt>, 1, (DwFn)k_step_dw_raw<kt, 1, 1>, (DwChunkFn)k_steps_dw_t<kt>}
+#define CO_DW_T(kt) {kt, 1, 1, (DwFn)k_step_dw_t<kt>, 1, (DwFn)k_step_dw_raw<kt, 1, 1>, (DwChunkFn)k_steps_dw_t<kt>, \
+                     nullptr, 4, (DwFn)k_step_dw_traw<kt>}
 const DwVariant kDwVariants[] = {
     CO_DW_ST(1, 3, 3), CO_DW_ST(2, 3, 3), CO_DW_ST(3, 3, 3), CO_DW_ST(5, 3, 3), CO_DW_ST(3, 5, 5),
     CO_DW_T(2), CO_DW_T(3), CO_DW_T(4), CO_DW_T(5), CO_DW_T(7), CO_DW_T(9),
@@ -947,6 +1023,7 @@ struct Depthwise {
   float* w = nullptr;
   void* zeros = nullptr;                // K2s: padding source (WX * C * 2 zero bytes)
   int grid = 0;
+  int grid_traw = 0;                    // RAW temporal kernel with the fused frame store (16-byte items)
   std::string name;
 };
 
@@ -980,6 +1057,14 @@ Depthwise* depthwise_create(const Geom& g, const void* w_dev, std::string& err) 
     }
     char buf[96];
     snprintf(buf, sizeof(buf), "k_step_dw_raw<%d,%d,%d>", pl.var->KT, pl.var->KH, pl.var->KW);
+    if (pl.temporal && pl.var->traw) {
+      int per = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pl.var->traw, kDwThreads, 0);
+      const int64_t it8 = g.B * g.HWo * (g.Cout / 8);
+      t->grid_traw = int(std::max<int64_t>(1, std::min<int64_t>((it8 + 2 * kDwThreads - 1) / (2 * kDwThreads),
+                                                                int64_t(sms) * std::max(per, 1))));
+      snprintf(buf, sizeof(buf), "k_step_dw_traw<%d>", pl.var->KT);
+    }
     t->name = buf;
     return t;
   }
@@ -1106,6 +1191,10 @@ void depthwise_destroy(Depthwise* t) {
 
 const char* depthwise_name(const Depthwise* t) { return t->name.c_str(); }
 
+bool depthwise_fuses_raw_store(const Depthwise* t, const Geom& g, int64_t x_bstride) {
+  return t && g.raw && t->pl.temporal && t->grid_traw > 0 && g.Cout % 8 == 0 && (x_bstride * 2) % 16 == 0;
+}
+
 cudaError_t depthwise_step(Depthwise* t, const Geom& g, const StepArgs& a, const float* bias, cudaStream_t s) {
   const DwPlan& pl = t->pl;
   DwParams p{};
@@ -1123,6 +1212,20 @@ cudaError_t depthwise_step(Depthwise* t, const Geom& g, const StepArgs& a, const
   p.HWo = g.HWo; p.plane = g.B * g.HWo;
   p.TH = pl.TH; p.bands = pl.bands; p.n_tiles = pl.n_tiles; p.WC = pl.WC; p.HR = pl.HR;
   void* args[] = {&p};
+  if (g.raw && a.x && a.emit && depthwise_fuses_raw_store(t, g, a.x_bstride)) {
+    // Ready step reading the new frame from x (host.cu step_raw): one streaming pass, frame stored here
+    p.raw_store = a.raw_store;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(t->grid_traw));
+    cfg.blockDim = dim3(kDwThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = option(OPT_PDL) != 0 ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(pl.var->traw), args);
+  }
   if (g.raw)
     return cudaLaunchKernel(reinterpret_cast<const void*>(pl.var->raw), dim3(unsigned(t->grid)), dim3(kDwThreads),
                             args, 0, s);

@@ -36,6 +36,22 @@ def test_c5_auto_layout_is_raw():
     assert c2.state_layout == "psum"                  # spatial windows keep the partial sums
 
 
+def test_c3_auto_layout_temporal_depthwise_is_raw():
+    """C3 states only 'bf16' (BASELINE.json configs[2]): under CO_STATE_AUTO its
+    temporal-only layer (kt = 5) takes the RAW frame ring with the fused-store
+    streaming kernel (7 bf16 frame accesses per step against 18 for the fp32
+    partial sums); the 3x3x3 stencil keeps the partial sums (K2s)."""
+    import paper_2204_03418_b200 as co
+    from paper_2204_03418_b200 import synth
+    cfg = synth.config(3, n_streams=8)
+    names, layouts = [], []
+    for L, (W, b) in zip(cfg.layers, synth.params(cfg)):
+        c = co.Conv(L.cin, L.cout, L.kernel, weight=W.cuda(), bias=b.cuda(), padding=L.padding, groups=L.groups,
+                    in_spatial=cfg.in_spatial, n_streams=8, state_layout="auto")
+        names.append(c.kernel_name); layouts.append(c.state_layout)
+    assert layouts == ["psum", "raw"] and names == ["k_step_dw_seg<3,3,3>", "k_step_dw_traw<5>"], (layouts, names)
+
+
 @pytest.mark.parametrize("cid", sorted(EXPECTED))
 def test_bench_config_kernels(cid):
     from paper_2204_03418_b200 import synth

@@ -158,6 +158,9 @@ RAW_DW = {
     "ragged_st2": dict(desc=O.Desc(2, 24, 24, (3, 3, 3), stride=(2, 1, 1), padding=(1, 1, 1), groups=24,
                                    in_spatial=(9, 13)), B=3),
     "t_dil2": dict(desc=O.Desc(1, 64, 64, (9, 1), dilation=(2, 1), groups=64, in_spatial=(25, 1)), B=3),
+    "t_st2_pad": dict(desc=O.Desc(2, 24, 24, (4, 1, 1), stride=(2, 1, 1), padding=(2, 0, 0), groups=24,
+                                  in_spatial=(7, 5)), B=5),
+    "t_many": dict(desc=O.Desc(2, 40, 40, (3, 1, 1), groups=40, in_spatial=(30, 33)), B=37),   # several grid waves, ragged tail
 }
 
 
@@ -168,10 +171,19 @@ def test_raw_depthwise_vs_oracle(case):
     W = rng.standard_normal(d.w_shape) / np.sqrt(np.prod(d.w_shape[1:]))
     b = rng.standard_normal(d.cout) * 0.1
     conv, sm, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="depthwise", state_layout="raw")
-    assert "dw_raw" in conv.kernel_name, conv.kernel_name
+    temporal = d.kernel[1:] == (1,) * (len(d.kernel) - 1)
+    # temporal-only layers: the fused-store streaming kernel (the Ready step reads x itself)
+    assert ("dw_traw" if temporal else "dw_raw") in conv.kernel_name, conv.kernel_name
     ys, refs = [], []
-    for t in range(d.receptive_field + 5):
+    for t in range(d.receptive_field + 7):
         xt = to_cl(rng.standard_normal(_shape(d, B)), torch.bfloat16)
+        if t == d.receptive_field + 2:                     # a probe: Ready or not, the ring must not change
+            yp = conv.forward_step(xt, update_state=False)
+            rp = sm.forward_step(np_of(xt), update_state=False)
+            assert (yp is None) == (rp is None)
+            if yp is not None:
+                ys.append(np_of(yp)); refs.append(rp.reshape(yp.shape))
+            xt = to_cl(rng.standard_normal(_shape(d, B)), torch.bfloat16)
         y = conv.forward_step(xt)
         r = sm.forward_step(np_of(xt))
         assert (y is None) == (r is None)
