@@ -727,7 +727,7 @@ __global__ void __launch_bounds__(1024, 1) k_steps_dw_st(const DwParams p, const
 // per stream-step).  Two items per thread, all 2 kt loads issued before the
 // FMAs; per channel the same operations in the same order as k_step_dw_raw.
 template <int KT>
-__global__ void __launch_bounds__(kDwThreads, 3) k_step_dw_traw(const DwParams p) {
+__global__ void __launch_bounds__(kDwThreads, KT <= 3 ? 3 : 2) k_step_dw_traw(const DwParams p) {   // (no spills: 2 x KT x 4 load registers)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(p.state);
