@@ -95,7 +95,7 @@ def assert_bf16_rounding_bound(y, ref, fp32_tol=1e-4):
                           f"{float((np.abs(y - ref) - bound).max()):.3e}"
 
 
-def build_config_layers(cfg, B, last_fp32=True, kernel="auto", out_dtype=None):
+def build_config_layers(cfg, B, last_fp32=True, kernel="auto", out_dtype=None, state_layout="psum"):
     """The config's layers on B streams exactly as bench.py builds them (same
     dispatch, kernels and launch geometry); the final layer emits fp32 for
     parity (A16: same kernel, only the final conversion differs)."""
@@ -109,7 +109,7 @@ def build_config_layers(cfg, B, last_fp32=True, kernel="auto", out_dtype=None):
         c = co.Conv(L.cin, L.cout, L.kernel, weight=W.cuda(), bias=b.cuda(), stride=L.stride, padding=L.padding,
                     dilation=L.dilation, groups=L.groups, spatial_rank=cfg.spatial_rank, in_spatial=spat,
                     n_streams=B, dtype=cfg.dtype, out_dtype=od, activation="relu" if L.relu else None,
-                    kernel=kernel)
+                    kernel=kernel, state_layout=state_layout)
         d = O.Desc(cfg.spatial_rank, L.cin, L.cout, L.kernel, L.stride, L.padding, L.dilation, L.groups, spat)
         convs.append(c); descs.append(d); Ws.append(W.double().numpy()); bs.append(b.double().numpy())
         spat = tuple(c.out_spatial) + (1,) * (2 - len(c.out_spatial))

@@ -51,12 +51,15 @@ def _sampled(x, idx):
     return np_of(x[idx])
 
 
-@pytest.mark.parametrize("cid", [2, 3, 4, 5])
-def test_fullsize_sampled_streams_vs_oracle(cid):
+@pytest.mark.parametrize("cid,layout", [(2, "psum"), (3, "psum"), (4, "psum"), (5, "psum"),
+                                        (3, "auto"), (5, "auto")])   # auto: the planner layouts bench.py times for C3 / C5
+def test_fullsize_sampled_streams_vs_oracle(cid, layout):
     from paper_2204_03418_b200 import synth
     cfg = synth.config(cid)
     B = cfg.n_streams
-    convs, descs, Ws, bs = build_config_layers(cfg, B)
+    convs, descs, Ws, bs = build_config_layers(cfg, B, state_layout=layout)
+    if layout == "auto":
+        assert [c.state_layout for c in convs] == {3: ["psum", "raw"], 5: ["raw"]}[cid]
     d_nn = sum(d.delay for d in descs)
     # past the delay by two full turns of the largest ring (C5: its 16 slots,
     # both dilation phases), so every slot is written, completed and re-used
