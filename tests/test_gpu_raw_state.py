@@ -160,6 +160,9 @@ RAW_DW = {
     "t_dil2": dict(desc=O.Desc(1, 64, 64, (9, 1), dilation=(2, 1), groups=64, in_spatial=(25, 1)), B=3),
     "t_st2_pad": dict(desc=O.Desc(2, 24, 24, (4, 1, 1), stride=(2, 1, 1), padding=(2, 0, 0), groups=24,
                                   in_spatial=(7, 5)), B=5),
+    "s_valid": dict(desc=O.Desc(2, 16, 16, (2, 3, 3), groups=16, in_spatial=(9, 10)), B=3),      # unpadded stencil
+    "s_many": dict(desc=O.Desc(2, 48, 48, (3, 3, 3), padding=(0, 1, 1), groups=48, in_spatial=(11, 29)), B=41),
+    "s_5x5": dict(desc=O.Desc(2, 32, 32, (3, 5, 5), padding=(2, 2, 2), groups=32, in_spatial=(12, 17)), B=4),
     "t_many": dict(desc=O.Desc(2, 40, 40, (3, 1, 1), groups=40, in_spatial=(30, 33)), B=37),   # several grid waves, ragged tail
 }
 
