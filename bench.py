@@ -239,8 +239,8 @@ def ncu_traffic(key):
 def state_of(cfg, args):
     """State layout per config: BASELINE.json states 'fp32 state' for C2-C4 (the
     partial-sum ring) and C1 is fp32 throughout; C3 and C5 state only
-    'bf16', so the planner's layout choice (CO_STATE_AUTO) applies there (C3: the
-    stencil keeps its partial sums, the temporal-only layer takes the RAW ring)."""
+    'bf16', so the planner's layout choice (CO_STATE_AUTO) applies there (C3: both
+    depthwise layers take the RAW frame ring with the frame store fused)."""
     if args.state != "config":
         return args.state
     return "auto" if cfg.cid in (3, 5) else "psum"

@@ -15,6 +15,8 @@ cudaError_t depthwise_step(Depthwise* t, const Geom& g, const StepArgs& a, const
 // RAW layout, temporal-only layers: a Ready step can read the new frame from x and
 // store it into its ring slot itself (StepArgs.x / raw_store), no separate frame copy.
 bool depthwise_fuses_raw_store(const Depthwise* t, const Geom& g, int64_t x_bstride);
+// True when a RAW-layout stencil of this geometry has a rolling-row plan (the planner's test).
+bool depthwise_raw_pipeline(const Geom& g);
 // Chunked steps: the fold of `total` ticks starting at clock n0
 // over a clip x (B, T, H, W, C) (ticks >= T are padding frames) in one launch,
 // state kept in registers; y (B, n_ready, Ho, Wo, C) with stream stride y_bstride.

@@ -234,6 +234,15 @@ static int make_geom(const co_conv_desc* d, Geom& g) {
     if (!g.raw && d->in_dtype == CO_BF16 && flat && g.kt > 1 && 2.0 * raw_b <= psum_b && d->groups == g.Cin &&
         g.Cin == g.Cout && g.Cin % 8 == 0)
       g.raw = 1;
+    // "same"-padded stride-1 depthwise stencils (C3-a): rolling row sets over the
+    // window's frames (k_step_dw_rowraw), when the depthwise planner has a plan for it
+    if (!g.raw && d->in_dtype == CO_BF16 && g.kt > 1 && 2.0 * raw_b <= psum_b && d->groups == g.Cin &&
+        g.Cin == g.Cout && g.Cin % 8 == 0 && g.sh == 1 && g.sw == 1 && g.dh == 1 && g.dw == 1 && g.Ho == g.H &&
+        g.Wo == g.W && g.kh * g.kw > 1) {
+      Geom gr = g;
+      gr.raw = 1;
+      if (co::depthwise_raw_pipeline(gr)) g.raw = 1;
+    }
   }
   if (g.op == CO_OP_DELAY) {
     if (g.kh != 1 || g.kw != 1 || g.sh != 1 || g.sw != 1 || g.ph || g.pw || g.dh != 1 || g.dw != 1 || g.pt ||

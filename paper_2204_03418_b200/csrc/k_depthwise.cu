@@ -717,6 +717,171 @@ __global__ void __launch_bounds__(1024, 1) k_steps_dw_st(const DwParams p, const
   }
 }
 
+// ------------------------------------------------------------------ RAW layout, spatial stencil: rolling rows
+// A Ready step of a "same"-padded stride-1 stencil over the RAW frame ring
+// with every input row of every window frame copied exactly once:
+// a block owns a contiguous range of global output rows (stream b, row ho); a
+// producer thread streams the global input rows that range touches, in order,
+// as row sets -- row hr of each of the kt frames (the new frame from x, the older
+// ones from the ring), kt bulk copies of W C bf16 -- into a ring of nst row-set
+// stages whose kw - 1 side columns stay zero (the padding); all consumer warps
+// walk the output rows together: wait (once, in order) for the row sets up to the
+// window's last row, compute the kt kh kw taps of the row's pixels (thread =
+// (channel quad, strip of PX pixels); rows outside the frame read a zero stage),
+// write y, store the new frame's row into its ring slot, and release the row
+// sets the next output row no longer needs.  (The per-unit pipeline of K2s needs
+// kt kh row pieces per unit and is bound by the producer's issue rate: 0.73 ms.)
+template <int KT, int KH, int KW, int PX>
+__global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_rowraw(const DwParams p) {
+  constexpr int NT = KT * KH * KW;
+  extern __shared__ __align__(128) uint8_t smem[];
+  float4* wt = reinterpret_cast<float4*>(smem);                     // [Cq][NT] float4
+  float* bs = reinterpret_cast<float*>(wt + NT * p.Cq);
+  uint8_t* stages = smem + p.stage_off;                             // [nst + 1][KT][WX][C] bf16 (the last: zeros)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  uint64_t* empty = full + p.nst;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NT * p.Cq; i += blockDim.x) {
+    const int qq = i / NT, tap = i - qq * NT;
+    wt[i] = *reinterpret_cast<const float4*>(p.w + int64_t(tap) * p.C + 4 * qq);
+  }
+  for (int i = tid; i < p.C; i += blockDim.x) bs[i] = p.bias[i];
+  for (int i = tid; i < (p.nst + 1) * p.stage_bytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(stages)[i] = make_uint4(0u, 0u, 0u, 0u);
+  if (tid == 0) {
+    for (int s = 0; s < p.nst; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], p.gthreads / 32);
+    }
+    ptx::fence_mbar_init();
+  }
+  ptx::fence_proxy_async();                                          // the zeroed stages before any bulk copy into them
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");                // (no early trigger: see k_step_dw_seg)
+  const int64_t lo = p.n_units * blockIdx.x / gridDim.x;            // global output rows g = b H + ho
+  const int64_t hi = p.n_units * (blockIdx.x + 1) / gridDim.x;
+  if (lo >= hi) return;
+  const int warp = tid / 32, lane = tid % 32;
+  const int rowp_b = p.WX * p.C * 2;                                // bytes of one staged (padded) row
+  const int64_t B = p.plane / p.HWo;
+  const int64_t n_rows = B * p.H;
+  __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(p.state);
+  // global input rows this range touches (windows never cross a stream: rows outside it are zeros)
+  const int64_t g0 = max(lo - p.ph, (lo / p.H) * p.H);
+  const int64_t g1 = min(min(hi - 1 - p.ph + KH, ((hi - 1) / p.H + 1) * p.H), n_rows);   // exclusive
+  if (warp == p.gthreads / 32) {                                    // ---- producer thread
+    if (lane != 0) return;
+    const uint32_t rb = uint32_t(p.W) * p.C * 2;
+    for (int64_t gi = g0; gi < g1; ++gi) {
+      const int64_t i = gi - g0;
+      const int s = int(i % p.nst);
+      if (i >= p.nst) ptx::mbar_wait(&empty[s], (uint32_t(i / p.nst) & 1u) ^ 1u);
+      const int64_t b = gi / p.H;
+      const int hr = int(gi - b * p.H);
+      uint8_t* st = stages + int64_t(s) * p.stage_bytes + p.pw * p.C * 2;
+      ptx::mbar_arrive_expect_tx(&full[s], uint32_t(KT) * rb);
+#pragma unroll 1
+      for (int k = 0; k < KT; ++k) {
+        const __nv_bfloat16* fr = (k == KT - 1) ? p.x + b * p.x_bstride : ring + (int64_t(p.slot[k]) * B + b) * p.frame;
+        ptx::bulk_g2s(st + k * rowp_b, fr + int64_t(hr) * p.W * p.C, rb, &full[s]);
+      }
+    }
+    return;
+  }
+  // ---- consumers: every warp waits on every row set once, in order (no waiter runs ahead of a barrier)
+  const bool active = tid < p.Cq * p.spu;
+  const int q = tid % p.Cq, sp = tid / p.Cq;
+  const int cstep = p.C;
+  const int c0 = sp * PX;
+  const int nv = p.Wo - c0;                                         // real pixels of the strip (<= 0: none)
+  const uint32_t stages_a = ptx::smem_u32(stages), zst_a = stages_a + uint32_t(p.nst) * uint32_t(p.stage_bytes);
+  const uint32_t col_a = uint32_t(c0 * cstep + 4 * q) * 2u;         // this thread's first staged column / quad (bytes)
+  uint32_t coff[PX + KW - 1];
+#pragma unroll
+  for (int t = 0; t < PX + KW - 1; ++t) coff[t] = uint32_t(t * cstep) * 2u;
+  // 32-bit counters relative to g0, stages / parities stepped incrementally (64-bit
+  // divisions per row made the first version instruction-bound)
+  const int n_out = int(hi - lo), n_in = int(g1 - g0);
+  int waited = 0, ws = 0, released = 0, rs_i = 0;                   // row sets waited for / released, and their stages
+  uint32_t wph = 0;
+  int64_t b = lo / p.H;
+  int ho = int(lo - b * p.H);
+  int gi = int(lo - g0);                                            // this output row's own input row set, relative to g0
+  int cs = gi % p.nst;                                              // ... and its stage
+  for (int r = 0; r < n_out; ++r) {
+    const int last = min(gi - p.ph + KH - 1, gi + (p.H - 1 - ho));   // the window's last row inside the stream
+    for (; waited <= last; ++waited) {
+      ptx::mbar_wait(&full[ws], wph);
+      if (++ws == p.nst) { ws = 0; wph ^= 1u; }
+    }
+    if (active && nv > 0) {
+      float4 acc[PX];
+#pragma unroll
+      for (int jj = 0; jj < PX; ++jj) acc[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4* wq = wt + q * NT;
+#pragma unroll 1
+      for (int u = 0; u < KH; ++u) {
+        const int hr = ho - p.ph + u;
+        int su = cs - p.ph + u;                                     // stage of row set gi - ph + u
+        su += su < 0 ? p.nst : 0;
+        su -= su >= p.nst ? p.nst : 0;
+        // 32-bit shared addresses: row set + this thread's first column, then one add per load
+        uint32_t xa = ((hr < 0 || hr >= p.H) ? zst_a : stages_a + uint32_t(su) * uint32_t(p.stage_bytes)) + col_a;
+#pragma unroll
+        for (int k = 0; k < KT; ++k, xa += uint32_t(rowp_b)) {
+          float4 xv[PX + KW - 1];
+#pragma unroll
+          for (int t = 0; t < PX + KW - 1; ++t) {
+            const uint2 raw = ptx::lds64(xa + coff[t]);
+            xv[t] = make_float4(__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xffff0000u),
+                                __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xffff0000u));
+          }
+#pragma unroll
+          for (int v = 0; v < KW; ++v) {
+            const float4 w = wq[(k * KH + u) * KW + v];
+#pragma unroll
+            for (int jj = 0; jj < PX; ++jj) acc[jj] = f4_fma(w, xv[jj + v], acc[jj]);
+          }
+        }
+      }
+      const float4 bias4 = reinterpret_cast<const float4*>(bs)[q];
+      const int64_t pin0 = int64_t(ho) * p.Wo + c0;
+      const int64_t yoff = b * p.y_bstride + pin0 * cstep + 4 * q;
+      // the new frame's pixels of this strip: row set g, frame kt-1, columns c0 + pw ...
+      const uint8_t* crow = stages + cs * p.stage_bytes + (KT - 1) * rowp_b;
+      const uint2* xc = reinterpret_cast<const uint2*>(crow) + (int64_t(c0 + p.pw) * cstep + 4 * q) / 4;
+      __nv_bfloat16* rs = p.raw_store >= 0 ? ring + (int64_t(p.raw_store) * B + b) * p.frame + pin0 * cstep + 4 * q : nullptr;
+#pragma unroll
+      for (int jj = 0; jj < PX; ++jj) {
+        if (jj >= nv) continue;
+        const float4 v = f4_act(f4_add(acc[jj], bias4), p.act);
+        if (p.out_f32) {
+          *reinterpret_cast<float4*>(static_cast<float*>(p.y) + yoff + jj * cstep) = v;
+        } else {
+          __nv_bfloat162 lo2 = __floats2bfloat162_rn(v.x, v.y), hi2 = __floats2bfloat162_rn(v.z, v.w);
+          uint2 uu;
+          uu.x = *reinterpret_cast<uint32_t*>(&lo2);
+          uu.y = *reinterpret_cast<uint32_t*>(&hi2);
+          *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.y) + yoff + jj * cstep) = uu;
+        }
+        if (rs) __stcs(reinterpret_cast<uint2*>(rs + jj * cstep), xc[jj * cstep / 4]);
+      }
+    }
+    // release the row sets the next output row does not read (its window starts at its
+    // own stream's first row at the earliest)
+    const bool wrap = ho + 1 == p.H;
+    const int first_next = r + 1 < n_out ? (wrap ? gi + 1 : max(gi + 1 - p.ph, gi - ho)) : n_in;
+    __syncwarp();
+    for (; released < first_next; ++released) {
+      if (lane == 0) ptx::mbar_arrive_relaxed(&empty[rs_i]);
+      if (++rs_i == p.nst) rs_i = 0;
+    }
+    ++gi;
+    if (++cs == p.nst) cs = 0;
+    if (wrap) { ho = 0; ++b; } else ++ho;
+  }
+}
+
 // ------------------------------------------------------------------ RAW layout, temporal only, fused store
 // A Ready step of a temporal-only depthwise layer over the RAW frame ring
 // as one streaming pass: thread item = (pixel, 8 channels), 16-byte
@@ -909,6 +1074,7 @@ struct DwVariant {
   DwFn seg = nullptr;                   // K2s segment-pipeline kernel (spatial stencils)
   int SPX = 4;                          // K2s: output pixels per thread strip
   DwFn traw = nullptr;                  // RAW layout, temporal only: fused frame store (k_step_dw_traw)
+  DwFn rowraw = nullptr;                // RAW layout, "same"-padded stencils: rolling row sets, frame store fused
 };
 #ifndef CO_DW_PX
 #define CO_DW_PX 2                      // output pixels per thread strip (experiments: -DCO_DW_PX=n)
@@ -920,7 +1086,8 @@ struct DwVariant {
 #define CO_DW_ST(kt, kh, kw) {kt, kh, kw, (DwFn)k_step_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>, \
                               (kt <= 3 ? CO_DW_PX : 2), (DwFn)k_step_dw_raw<kt, kh, kw>, \
                               (DwChunkFn)k_steps_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>, \
-                              (DwFn)k_step_dw_seg<kt, kh, kw, CO_DW_SEG_PX(kt, kh, kw)>, CO_DW_SEG_PX(kt, kh, kw)}
+                              (DwFn)k_step_dw_seg<kt, kh, kw, CO_DW_SEG_PX(kt, kh, kw)>, CO_DW_SEG_PX(kt, kh, kw), nullptr, \
+                              (DwFn)k_step_dw_rowraw<kt, kh, kw, 4>}
 #define CO_DW_T(kt) {kt, 1, 1, (DwFn)k_step_dw_t<kt>, 1, (DwFn)k_step_dw_raw<kt, 1, 1>, (DwChunkFn)k_steps_dw_t<kt>, \
                      nullptr, 4, (DwFn)k_step_dw_traw<kt>}
 const DwVariant kDwVariants[] = {
@@ -982,6 +1149,32 @@ bool make_seg_plan(const Geom& g, const DwVariant& v, DwPlan& pl) {
   return false;
 }
 
+// Rolling-row plan of the RAW stencil (k_step_dw_rowraw): all consumer threads on one
+// output row (channel quads x strips of 4 pixels), kh + 2 row-set stages (kh + 1
+// if shared memory is short) + the zero stage.
+bool make_rowraw_plan(const Geom& g, const DwVariant& v, DwPlan& pl) {
+  if (!v.rowraw) return false;
+  const int PX = 4, Cq = g.Cout / 4;
+  const int spu = (g.Wo + PX - 1) / PX;
+  const int gth = (Cq * spu + 31) / 32 * 32;
+  if (gth + 32 > kSegMaxThreads) return false;
+  const int WX = std::max(g.W + g.kw - 1, spu * PX + g.kw - 1);
+  const size_t sb = (size_t(g.kt) * WX * g.Cin * 2 + 127) / 128 * 128;
+  const size_t base = (size_t(g.kt * g.kh * g.kw + 1) * g.Cin * 4 + 127) / 128 * 128;
+  for (int nst = g.kh + 2; nst >= g.kh + 1; --nst) {
+    const size_t smem = base + size_t(nst + 1) * sb + 2 * size_t(nst) * 8;
+    if (smem > size_t(227) * 1024) continue;
+    pl.seg = true;
+    pl.nseg = 1; pl.WS = g.Wo; pl.WX = WX; pl.nst = nst; pl.spu = spu; pl.gthreads = gth; pl.ngroups = 1;
+    pl.stage_bytes = int(sb); pl.x_off = 0; pl.stage_off = int(base);
+    pl.bar_off = int(base + size_t(nst + 1) * sb);
+    pl.n_units = g.B * g.Ho;
+    pl.seg_smem = smem;
+    return true;
+  }
+  return false;
+}
+
 bool make_dw_plan(const Geom& g, DwPlan& pl) {
   if (g.in_dtype != BF16 || g.groups != g.Cin || g.Cin != g.Cout || g.Cin % 8 != 0) return false;
   if (g.sh != 1 || g.sw != 1 || g.dh != 1 || g.dw != 1) return false;
@@ -993,6 +1186,8 @@ bool make_dw_plan(const Geom& g, DwPlan& pl) {
   }
   if (!pl.var) return false;
   pl.temporal = temporal;
+  if (g.raw && !temporal && option(OPT_DW_SEG) && g.Ho == g.H && g.Wo == g.W)
+    make_rowraw_plan(g, *pl.var, pl);   // RAW stencil, "same" padding: a row's threads store their own input pixels
   if (temporal || g.raw) return true;   // no staged halo (RAW reads the ring directly)
   // staged halo width: every strip reads PX + kw - 1 columns (zero beyond the frame)
   const int px = pl.var->PX;
@@ -1024,6 +1219,7 @@ struct Depthwise {
   void* zeros = nullptr;                // K2s: padding source (WX * C * 2 zero bytes)
   int grid = 0;
   int grid_traw = 0;                    // RAW temporal kernel with the fused frame store (16-byte items)
+  int grid_rowraw = 0;                  // RAW stencil over rolling row sets with the fused frame store
   std::string name;
 };
 
@@ -1064,6 +1260,13 @@ Depthwise* depthwise_create(const Geom& g, const void* w_dev, std::string& err) 
       t->grid_traw = int(std::max<int64_t>(1, std::min<int64_t>((it8 + 2 * kDwThreads - 1) / (2 * kDwThreads),
                                                                 int64_t(sms) * std::max(per, 1))));
       snprintf(buf, sizeof(buf), "k_step_dw_traw<%d>", pl.var->KT);
+    }
+    if (pl.seg) {   // RAW stencil over rolling row sets for Ready steps that read x (k_step_dw_rowraw)
+      if ((e = cudaFuncSetAttribute(pl.var->rowraw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.seg_smem))) != cudaSuccess) {
+        err = cudaGetErrorString(e); depthwise_destroy(t); return nullptr;
+      }
+      t->grid_rowraw = int(std::max<int64_t>(1, std::min<int64_t>(pl.n_units, int64_t(sms))));
+      snprintf(buf, sizeof(buf), "k_step_dw_rowraw<%d,%d,%d>", pl.var->KT, pl.var->KH, pl.var->KW);
     }
     t->name = buf;
     return t;
@@ -1192,7 +1395,13 @@ void depthwise_destroy(Depthwise* t) {
 const char* depthwise_name(const Depthwise* t) { return t->name.c_str(); }
 
 bool depthwise_fuses_raw_store(const Depthwise* t, const Geom& g, int64_t x_bstride) {
-  return t && g.raw && t->pl.temporal && t->grid_traw > 0 && g.Cout % 8 == 0 && (x_bstride * 2) % 16 == 0;
+  if (!t || !g.raw || g.Cout % 8 != 0 || (x_bstride * 2) % 16 != 0) return false;
+  return t->pl.temporal ? t->grid_traw > 0 : t->grid_rowraw > 0;
+}
+
+bool depthwise_raw_pipeline(const Geom& g) {
+  DwPlan pl;
+  return g.raw && make_dw_plan(g, pl) && !pl.temporal && pl.seg;
 }
 
 cudaError_t depthwise_step(Depthwise* t, const Geom& g, const StepArgs& a, const float* bias, cudaStream_t s) {
@@ -1224,6 +1433,15 @@ cudaError_t depthwise_step(Depthwise* t, const Geom& g, const StepArgs& a, const
     attr[0].val.programmaticStreamSerializationAllowed = option(OPT_PDL) != 0 ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (!pl.temporal) {   // the stencil over rolling row sets
+      p.n_units = pl.n_units; p.nseg = pl.nseg; p.WS = pl.WS; p.WX = pl.WX; p.nst = pl.nst; p.spu = pl.spu;
+      p.gthreads = pl.gthreads; p.stage_bytes = pl.stage_bytes; p.x_off = pl.x_off; p.stage_off = pl.stage_off;
+      p.bar_off = pl.bar_off; p.ngroups = pl.ngroups;
+      cfg.gridDim = dim3(unsigned(t->grid_rowraw));
+      cfg.blockDim = dim3(unsigned(pl.gthreads + 32));
+      cfg.dynamicSmemBytes = pl.seg_smem;
+      return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(pl.var->rowraw), args);
+    }
     return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(pl.var->traw), args);
   }
   if (g.raw)

@@ -59,7 +59,7 @@ def test_fullsize_sampled_streams_vs_oracle(cid, layout):
     B = cfg.n_streams
     convs, descs, Ws, bs = build_config_layers(cfg, B, state_layout=layout)
     if layout == "auto":
-        assert [c.state_layout for c in convs] == {3: ["psum", "raw"], 5: ["raw"]}[cid]
+        assert [c.state_layout for c in convs] == {3: ["raw", "raw"], 5: ["raw"]}[cid]
     d_nn = sum(d.delay for d in descs)
     # past the delay by two full turns of the largest ring (C5: its 16 slots,
     # both dilation phases), so every slot is written, completed and re-used

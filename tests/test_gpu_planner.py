@@ -36,11 +36,12 @@ def test_c5_auto_layout_is_raw():
     assert c2.state_layout == "psum"                  # spatial windows keep the partial sums
 
 
-def test_c3_auto_layout_temporal_depthwise_is_raw():
-    """C3 states only 'bf16' (BASELINE.json configs[2]): under CO_STATE_AUTO its
-    temporal-only layer (kt = 5) takes the RAW frame ring with the fused-store
-    streaming kernel (7 bf16 frame accesses per step against 18 for the fp32
-    partial sums); the 3x3x3 stencil keeps the partial sums (K2s)."""
+def test_c3_auto_layout_depthwise_is_raw():
+    """C3 states only 'bf16' (BASELINE.json configs[2]): under CO_STATE_AUTO both
+    layers take the RAW frame ring with the frame store fused -- the temporal-only
+    layer (kt = 5) as one streaming pass (7 bf16 frame accesses per step against 18
+    for the fp32 partial sums), the "same"-padded 3x3x3 stencil over rolling row
+    sets (5 against 10)."""
     import paper_2204_03418_b200 as co
     from paper_2204_03418_b200 import synth
     cfg = synth.config(3, n_streams=8)
@@ -49,7 +50,7 @@ def test_c3_auto_layout_temporal_depthwise_is_raw():
         c = co.Conv(L.cin, L.cout, L.kernel, weight=W.cuda(), bias=b.cuda(), padding=L.padding, groups=L.groups,
                     in_spatial=cfg.in_spatial, n_streams=8, state_layout="auto")
         names.append(c.kernel_name); layouts.append(c.state_layout)
-    assert layouts == ["psum", "raw"] and names == ["k_step_dw_seg<3,3,3>", "k_step_dw_traw<5>"], (layouts, names)
+    assert layouts == ["raw", "raw"] and names == ["k_step_dw_rowraw<3,3,3>", "k_step_dw_traw<5>"], (layouts, names)
 
 
 @pytest.mark.parametrize("cid", sorted(EXPECTED))

@@ -176,7 +176,9 @@ def test_raw_depthwise_vs_oracle(case):
     conv, sm, _, _ = make_pair(d, W, b, B, dtype=torch.bfloat16, kernel="depthwise", state_layout="raw")
     temporal = d.kernel[1:] == (1,) * (len(d.kernel) - 1)
     # temporal-only layers: the fused-store streaming kernel (the Ready step reads x itself)
-    assert ("dw_traw" if temporal else "dw_raw") in conv.kernel_name, conv.kernel_name
+    # "same"-padded stencils: rolling row sets over the window's frames (frame store fused too)
+    same = all(2 * pd == k - 1 for pd, k in zip(list(d.padding)[1:], list(d.kernel)[1:]))
+    assert ("dw_traw" if temporal else "dw_rowraw" if same else "dw_raw") in conv.kernel_name, conv.kernel_name
     ys, refs = [], []
     for t in range(d.receptive_field + 7):
         xt = to_cl(rng.standard_normal(_shape(d, B)), torch.bfloat16)
