@@ -1083,11 +1083,15 @@ struct DwVariant {
 // threads; weights read from shared memory once per 7 pixels), 4 for the
 // register-heavier 5x5 / kt = 5 stencils
 #define CO_DW_SEG_PX(kt, kh, kw) ((kt) <= 3 && (kh) * (kw) <= 9 ? 7 : 4)
+#ifndef CO_DW_ROWRAW_PX
+#define CO_DW_ROWRAW_PX 4                // rolling-row RAW stencil: output pixels per thread strip (C3-a: 4 -> 0.228 ms on
+                                        // 11 consumer warps, 7 -> 0.252 ms on 6)
+#endif
 #define CO_DW_ST(kt, kh, kw) {kt, kh, kw, (DwFn)k_step_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>, \
                               (kt <= 3 ? CO_DW_PX : 2), (DwFn)k_step_dw_raw<kt, kh, kw>, \
                               (DwChunkFn)k_steps_dw_st<kt, kh, kw, (kt <= 3 ? CO_DW_PX : 2)>, \
                               (DwFn)k_step_dw_seg<kt, kh, kw, CO_DW_SEG_PX(kt, kh, kw)>, CO_DW_SEG_PX(kt, kh, kw), nullptr, \
-                              (DwFn)k_step_dw_rowraw<kt, kh, kw, 4>}
+                              (DwFn)k_step_dw_rowraw<kt, kh, kw, CO_DW_ROWRAW_PX>}
 #define CO_DW_T(kt) {kt, 1, 1, (DwFn)k_step_dw_t<kt>, 1, (DwFn)k_step_dw_raw<kt, 1, 1>, (DwChunkFn)k_steps_dw_t<kt>, \
                      nullptr, 4, (DwFn)k_step_dw_traw<kt>}
 const DwVariant kDwVariants[] = {
@@ -1154,7 +1158,7 @@ bool make_seg_plan(const Geom& g, const DwVariant& v, DwPlan& pl) {
 // if shared memory is short) + the zero stage.
 bool make_rowraw_plan(const Geom& g, const DwVariant& v, DwPlan& pl) {
   if (!v.rowraw) return false;
-  const int PX = 4, Cq = g.Cout / 4;
+  const int PX = CO_DW_ROWRAW_PX, Cq = g.Cout / 4;
   const int spu = (g.Wo + PX - 1) / PX;
   const int gth = (Cq * spu + 31) / 32 * 32;
   if (gth + 32 > kSegMaxThreads) return false;
