@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(kSegMaxThreads, 1) k_step_dw_rowraw(const DwPa
 #pragma unroll
       for (int jj = 0; jj < PX; ++jj) acc[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
       const float4* wq = wt + q * NT;
-#pragma unroll 1
+#pragma unroll
       for (int u = 0; u < KH; ++u) {
         const int hr = ho - p.ph + u;
         int su = cs - p.ph + u;                                     // stage of row set gi - ph + u
