@@ -204,6 +204,44 @@ def test_fullsize_k2s_pipeline_repeats_equal_k2():
         del y1, s1
 
 
+def test_fullsize_raw_stencil_pipeline_all_streams_equal_plain_raw_kernel():
+    """All 512 streams of C3-a over the RAW frame ring: the rolling-row pipeline
+    (k_step_dw_rowraw, frame store fused) against the plain per-thread-load RAW
+    kernel (dw_seg = 0: k_step_dw_raw after a frame copy) -- outputs within fp32
+    summation-order noise (1e-5 of the RMS; a mis-synchronised stage would be off
+    by O(1)), the frame rings bit for bit; three repeats (race detector)."""
+    import paper_2204_03418_b200 as co
+    from paper_2204_03418_b200 import synth
+    cfg = synth.config(3)
+    L = cfg.layers[0]
+    Wt, bt = synth.params(cfg)[0]
+    T = 6
+    set_opt("chunk", 0)
+    g = torch.Generator(device="cuda").manual_seed(29)
+    clip = co.channels_last(torch.randn((cfg.n_streams, L.cin, T) + tuple(cfg.in_spatial), generator=g,
+                                        device="cuda").to(torch.bfloat16))
+
+    def run(seg):
+        set_opt("dw_seg", seg)
+        conv = co.Conv(L.cin, L.cout, L.kernel, weight=Wt.cuda(), bias=bt.cuda(), stride=L.stride,
+                       padding=L.padding, dilation=L.dilation, groups=L.groups, spatial_rank=cfg.spatial_rank,
+                       in_spatial=tuple(cfg.in_spatial), n_streams=cfg.n_streams, dtype=cfg.dtype,
+                       out_dtype=torch.float32, state_layout="raw")
+        assert conv.kernel_name.startswith("k_step_dw_rowraw" if seg else "k_step_dw_raw"), conv.kernel_name
+        ys, _ = conv.forward_steps(clip)
+        st, _ = conv.state_dict_stream()
+        torch.cuda.synchronize()
+        return ys, st
+
+    y0, s0 = run(0)
+    rms = y0.pow(2).mean().sqrt().item()
+    for rep in range(3):
+        y1, s1 = run(1)
+        assert (y1 - y0).abs().max().item() <= 1e-5 * rms, rep
+        assert torch.equal(s1, s0), rep
+        del y1, s1
+
+
 def _sample_streams(B):
     return sorted({0, B // 2, B - 1})
 
