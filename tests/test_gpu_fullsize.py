@@ -280,6 +280,34 @@ def test_fullsize_pooling_sampled_streams_vs_oracle(name):
     assert n_ready == 3
 
 
+def test_fullsize_pool_row_pipeline_all_streams_equal_band_kernel():
+    """All 256 streams of the max3 workload: the bulk-copy row pipeline
+    (k_step_pool_seg) against the band kernel (pool_seg = 0), bit for bit on
+    every output of every Ready step; three repeats (race detector)."""
+    import paper_2204_03418_b200 as co
+    import scripts.bench_pool as bp
+    w = bp.WORKLOADS["max3"]
+    B, C, H, W = w["B"], w["C"], w["H"], w["W"]
+    g = torch.Generator(device="cuda").manual_seed(31)
+    frames = [co.channels_last(torch.randn((B, C, H, W), generator=g, device="cuda").to(torch.bfloat16)) for _ in range(5)]
+
+    def run(seg):
+        set_opt("pool_seg", seg)
+        p = co.Pool(w["kind"], C, w["kernel"], stride=w["stride"], padding=w["padding"], in_spatial=(H, W), n_streams=B)
+        assert ("pool_seg" in p.kernel_name) == bool(seg), p.kernel_name
+        ys = [p.forward_step(x) for x in frames]
+        torch.cuda.synchronize()
+        return [y.clone() for y in ys if y is not None]
+
+    ref = run(0)
+    assert len(ref) == 3
+    for rep in range(3):
+        got = run(1)
+        assert len(got) == len(ref)
+        for a, b in zip(got, ref):
+            assert torch.equal(a, b), rep
+
+
 def test_fullsize_mha_sampled_streams_vs_oracle():
     """scripts/bench_mha.py's workload (E=1024, 16 heads, window 64, 1024
     streams): sampled streams against the fp64 MHA oracle at the bf16 bar."""
@@ -307,3 +335,37 @@ def test_fullsize_mha_sampled_streams_vs_oracle():
             assert (y is None) == (r is None)
             if y is not None:
                 assert rel_err(np_of(y[b:b + 1]), r) <= 2e-2
+
+
+def test_fullsize_mha_ring_pipeline_all_streams_vs_per_lane_kernel():
+    """All 1024 streams of the MHA workload: the ring-pipeline attention
+    (k_mha_attend_ring) against the per-lane-load kernel (mha_ring = 0) on the
+    same weights and inputs.  Both read the same bf16 q / k / v, so every
+    stream's outputs agree to bf16 last-place effects of the attention output
+    (held per stream to 2e-2 of the RMS; a mis-synchronised stage would put one
+    stream off by O(1)); the K / V rings afterwards are equal bit for bit."""
+    import paper_2204_03418_b200 as co
+    B, E, H, n = 1024, 1024, 16, 64
+    g = torch.Generator(device="cuda").manual_seed(41)
+    w_in = torch.randn((3 * E, E), generator=g, device="cuda") / E ** 0.5
+    w_out = torch.randn((E, E), generator=g, device="cuda") / E ** 0.5
+    xs = [torch.randn((B, E), generator=g, device="cuda").to(torch.bfloat16) for _ in range(n + 3)]
+
+    def run(ring):
+        set_opt("mha_ring", ring)
+        m = co.MultiheadAttention(E, H, n, n_streams=B, out_dtype=torch.float32, in_proj_weight=w_in,
+                                  out_proj_weight=w_out, in_proj_bias=torch.zeros(3 * E, device="cuda"),
+                                  out_proj_bias=torch.zeros(E, device="cuda"))
+        ys = [m.forward_step(x) for x in xs]
+        st, cnt = m.state_dict_stream()
+        torch.cuda.synchronize()
+        return torch.stack([y for y in ys if y is not None]), st
+
+    y0, s0 = run(0)
+    assert y0.shape[0] == 4
+    rms = y0.pow(2).mean().sqrt().item()
+    for rep in range(2):
+        y1, s1 = run(1)
+        per_stream = (y1 - y0).abs().amax(dim=(0, 2))
+        assert per_stream.max().item() <= 2e-2 * rms, (rep, int(per_stream.argmax()))
+        assert torch.equal(s1, s0), rep
